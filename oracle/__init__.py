@@ -1,0 +1,272 @@
+"""CPU oracle for SsNAL-EN — TEST INFRASTRUCTURE ONLY.
+
+Thin ctypes wrapper around libssnal_oracle.so (oracle/ssnal_oracle.c), the
+plain fp64 C implementation of the paper's method.  Only tests/,
+__graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference legs may
+import this module; the product package never does.  Shares no code with the
+CUDA path.
+
+Arrays: A is a C-contiguous float64 array of shape (n, m) (= column-major m x n,
+column i is A[i]).  Parity status of every function is listed in DESIGN.md
+("Oracle pins"); none is "parity unpinned".
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB = os.path.join(_HERE, "libssnal_oracle.so")
+_lib = None
+
+_d = ctypes.c_double
+_i64 = ctypes.c_int64
+_dp = ctypes.POINTER(ctypes.c_double)
+_lp = ctypes.POINTER(ctypes.c_int64)
+
+
+class Opts(ctypes.Structure):
+    _fields_ = [("sigma_factor", _d), ("sigma_max", _d), ("mu", _d), ("beta", _d), ("max_outer", ctypes.c_int32),
+                ("max_inner", ctypes.c_int32), ("max_bt", ctypes.c_int32), ("init_mode", ctypes.c_int32)]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [("status", ctypes.c_int32), ("outer_iters", ctypes.c_int32), ("newton_iters", ctypes.c_int32),
+                ("backtracks", ctypes.c_int32), ("aty_passes", ctypes.c_int32),
+                ("branch_steps", ctypes.c_int32 * 3), ("line_search_stalled", ctypes.c_int32),
+                ("active", ctypes.c_int64), ("res_kkt1", _d), ("res_kkt3", _d), ("primal_obj", _d),
+                ("dual_obj", _d), ("gap", _d), ("sigma_final", _d)]
+
+
+class Trace(ctypes.Structure):
+    _fields_ = [("outer", ctypes.c_int32), ("branch", ctypes.c_int32), ("r", ctypes.c_int64), ("s", _d),
+                ("psi", _d), ("res1", _d), ("gd", _d)]
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB):
+            raise RuntimeError(f"{LIB} missing: run tools/build.py")
+        L = ctypes.CDLL(LIB)
+        sig = {
+            "orc_penalty": (_d, [_dp, _i64, _d, _d]),
+            "orc_pstar": (_d, [_dp, _i64, _d, _d]),
+            "orc_prox": (_d, [_d, _d, _d, _d]),
+            "orc_prox_conj": (_d, [_d, _d, _d, _d]),
+            "orc_hstar": (_d, [_dp, _dp, _i64]),
+            "orc_aty": (None, [_dp, _i64, _i64, _dp, _dp]),
+            "orc_ax": (None, [_dp, _i64, _i64, _dp, _dp]),
+            "orc_psi": (_d, [_dp, _dp, _i64, _i64, _dp, _dp, _d, _d, _d]),
+            "orc_grad_psi": (None, [_dp, _dp, _i64, _i64, _dp, _dp, _d, _d, _d, _dp]),
+            "orc_zbar": (None, [_dp, _i64, _i64, _dp, _dp, _d, _d, _d, _dp]),
+            "orc_active_set": (_i64, [_dp, _i64, _d, _d, _lp]),
+            "orc_chol": (ctypes.c_int, [_dp, _i64]),
+            "orc_chol_solve": (None, [_dp, _i64, _dp]),
+            "orc_newton_direction": (ctypes.c_int, [_dp, _i64, _lp, _i64, _dp, _d, _dp]),
+            "orc_primal_obj": (_d, [_dp, _dp, _i64, _i64, _dp, _d, _d]),
+            "orc_dual_obj": (_d, [_dp, _i64, _dp, _dp, _i64, _d, _d]),
+            "orc_kkt_violation": (_d, [_dp, _dp, _i64, _i64, _dp, _d, _d]),
+            "orc_default_opts": (None, [ctypes.POINTER(Opts)]),
+            "orc_solve": (ctypes.c_int, [_dp, _dp, _i64, _i64, _d, _d, _d, _d, _dp, ctypes.POINTER(Opts), _dp, _dp,
+                                         ctypes.POINTER(Stats), ctypes.POINTER(Trace), _i64, _lp]),
+            "orc_aty_fused": (_i64, [_dp, _dp, _i64, _i64, _dp, _dp, _d, _d, _d, _dp, _lp, _dp, _dp, _dp]),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _f64(a):
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    return a, a.ctypes.data_as(_dp)
+
+
+def _A(A):
+    A = np.ascontiguousarray(A, dtype=np.float64)
+    assert A.ndim == 2, "A must be (n, m): column i of the m x n design is A[i]"
+    return A, A.shape[1], A.shape[0], A.ctypes.data_as(_dp)
+
+
+# --- Section 2: penalty, conjugate, prox -------------------------------------
+
+def prox(t, sigma, l1, l2):
+    """Eq. (6) left: prox_{σp}(t), elementwise."""
+    f = lib().orc_prox
+    return np.vectorize(lambda v: f(float(v), sigma, l1, l2), otypes=[np.float64])(t)
+
+
+def prox_conj(t, sigma, l1, l2):
+    """Eq. (6) right: prox_{p*/σ}(t/σ), elementwise, argument t."""
+    f = lib().orc_prox_conj
+    return np.vectorize(lambda v: f(float(v), sigma, l1, l2), otypes=[np.float64])(t)
+
+
+def pstar(z, l1, l2):
+    """Prop. 1: p*(z)."""
+    z, zp = _f64(np.atleast_1d(z))
+    return lib().orc_pstar(zp, len(z), l1, l2)
+
+
+def penalty(x, l1, l2):
+    x, xp = _f64(np.atleast_1d(x))
+    return lib().orc_penalty(xp, len(x), l1, l2)
+
+
+def hstar(y, b):
+    y, yp = _f64(y)
+    b, bp = _f64(b)
+    return lib().orc_hstar(yp, bp, len(y))
+
+
+# --- products and Section 3 ----------------------------------------------------
+
+def aty(A, y):
+    A, m, n, Ap = _A(A)
+    y, yp = _f64(y)
+    w = np.empty(n)
+    lib().orc_aty(Ap, m, n, yp, w.ctypes.data_as(_dp))
+    return w
+
+
+def ax(A, x):
+    A, m, n, Ap = _A(A)
+    x, xp = _f64(x)
+    out = np.empty(m)
+    lib().orc_ax(Ap, m, n, xp, out.ctypes.data_as(_dp))
+    return out
+
+
+def psi(A, b, x, y, sigma, l1, l2):
+    """Prop. 2(1): ψ(y) (including −‖x‖²/(2σ))."""
+    A, m, n, Ap = _A(A)
+    return lib().orc_psi(Ap, _f64(b)[1], m, n, _f64(x)[1], _f64(y)[1], sigma, l1, l2)
+
+
+def grad_psi(A, b, x, y, sigma, l1, l2):
+    """Eq. (15): ∇ψ(y)."""
+    A, m, n, Ap = _A(A)
+    g = np.empty(m)
+    b, bp = _f64(b)
+    x, xp = _f64(x)
+    y, yp = _f64(y)
+    lib().orc_grad_psi(Ap, bp, m, n, xp, yp, sigma, l1, l2, g.ctypes.data_as(_dp))
+    return g
+
+
+def zbar(A, x, y, sigma, l1, l2):
+    """Prop. 2(2): z̄ = prox_{p*/σ}(x/σ − Aᵀy)."""
+    A, m, n, Ap = _A(A)
+    z = np.empty(n)
+    x, xp = _f64(x)
+    y, yp = _f64(y)
+    lib().orc_zbar(Ap, m, n, xp, yp, sigma, l1, l2, z.ctypes.data_as(_dp))
+    return z
+
+
+def active_set(t, sigma, l1):
+    """Eq. (17): J = {i : |t_i| > σλ1} ascending."""
+    t, tp = _f64(t)
+    J = np.empty(max(len(t), 1), dtype=np.int64)
+    r = lib().orc_active_set(tp, len(t), sigma, l1, J.ctypes.data_as(_lp))
+    return J[:r].copy()
+
+
+def newton_direction(A, J, g, kappa):
+    """Eq. (18)/(19): d solving (I + κ A_J A_Jᵀ) d = −g.  Returns (d, branch)."""
+    A, m, n, Ap = _A(A)
+    J = np.ascontiguousarray(J, dtype=np.int64)
+    g, gp = _f64(g)
+    d = np.empty(m)
+    br = lib().orc_newton_direction(Ap, m, J.ctypes.data_as(_lp), len(J), gp, kappa, d.ctypes.data_as(_dp))
+    if br < 0:
+        raise FloatingPointError("oracle Cholesky failed")
+    return d, br
+
+
+def chol(M):
+    """Textbook Cholesky: returns lower L (column-major semantics on a symmetric M)."""
+    M = np.array(M, dtype=np.float64, order="F")
+    N = M.shape[0]
+    buf = np.ascontiguousarray(M.T.reshape(-1))  # column-major flat
+    rc = lib().orc_chol(buf.ctypes.data_as(_dp), N)
+    if rc != 0:
+        raise FloatingPointError("not SPD")
+    L = buf.reshape(N, N).T.copy()
+    return np.tril(L)
+
+
+def primal_obj(A, b, x, l1, l2):
+    """Eq. (1)."""
+    A, m, n, Ap = _A(A)
+    return lib().orc_primal_obj(Ap, _f64(b)[1], m, n, _f64(x)[1], l1, l2)
+
+
+def dual_obj(b, y, w, l1, l2):
+    """−h*(y) − p*(w) with w = Aᵀy (reading R2)."""
+    b, bp = _f64(b)
+    y, yp = _f64(y)
+    w, wp = _f64(w)
+    return lib().orc_dual_obj(bp, len(b), yp, wp, len(w), l1, l2)
+
+
+def kkt_violation(A, b, x, l1, l2):
+    """max_i v_i of the KKT inclusion Aᵀ(b−Ax) − λ2x ∈ λ1∂‖x‖₁."""
+    A, m, n, Ap = _A(A)
+    return lib().orc_kkt_violation(Ap, _f64(b)[1], m, n, _f64(x)[1], l1, l2)
+
+
+def default_opts(**kw) -> Opts:
+    o = Opts()
+    lib().orc_default_opts(ctypes.byref(o))
+    for k, v in kw.items():
+        setattr(o, k, v)
+    return o
+
+
+def solve(A, b, l1, l2, sigma0=5e-3, tol=1e-6, x0=None, trace_cap=0, **opts):
+    """Algorithm 1 (SsNAL-EN).  Returns (x, y, stats dict, trace list)."""
+    A, m, n, Ap = _A(A)
+    b, bp = _f64(b)
+    o = default_opts(**opts)
+    x = np.empty(n)
+    y = np.empty(m)
+    st = Stats()
+    x0p = None
+    if x0 is not None:
+        x0, x0p = _f64(x0)
+    tr = (Trace * max(trace_cap, 1))()
+    tl = ctypes.c_int64(0)
+    lib().orc_solve(Ap, bp, m, n, l1, l2, sigma0, tol, x0p, ctypes.byref(o), x.ctypes.data_as(_dp),
+                    y.ctypes.data_as(_dp), ctypes.byref(st), tr if trace_cap else None, trace_cap, ctypes.byref(tl))
+    stats = {f: getattr(st, f) for f, _ in Stats._fields_}
+    stats["branch_steps"] = list(st.branch_steps)
+    trace = [{f: getattr(tr[i], f) for f, _ in Trace._fields_} for i in range(min(tl.value, trace_cap))]
+    return x, y, stats, trace
+
+
+def aty_fused(A, b, y, x, sigma, l1, l2, with_grad=True):
+    """K1-equivalent: (w, J, P_J, partials[4], g)."""
+    A, m, n, Ap = _A(A)
+    b, bp = _f64(b)
+    y, yp = _f64(y)
+    x, xp = _f64(x)
+    w = np.empty(n)
+    J = np.empty(max(n, 1), dtype=np.int64)
+    PJ = np.empty(max(n, 1))
+    part = np.empty(4)
+    g = np.empty(m) if with_grad else None
+    r = lib().orc_aty_fused(Ap, bp, m, n, yp, xp, sigma, l1, l2, w.ctypes.data_as(_dp), J.ctypes.data_as(_lp),
+                            PJ.ctypes.data_as(_dp), part.ctypes.data_as(_dp),
+                            g.ctypes.data_as(_dp) if with_grad else None)
+    return w, J[:r].copy(), PJ[:r].copy(), part, g
+
+
+def lambda_max_l1(A, b):
+    """‖Aᵀb‖∞."""
+    return float(np.max(np.abs(aty(A, b))))
