@@ -1,0 +1,139 @@
+/*
+ * ssnal_en.h — C ABI of the B200 (sm_100a) SsNAL-EN hot path.
+ *
+ * Solves the Elastic Net  min_x ½‖Ax − b‖² + λ1‖x‖₁ + (λ2/2)‖x‖²   (Eq. (1))
+ * with the Semi-smooth Newton Augmented Lagrangian method of arXiv 2006.03970:
+ * Algorithm 1, ψ from Prop. 2, ∇ψ Eq. (15),
+ * the generalized Hessian V = I + κ A_J A_Jᵀ Eq. (16)-(18), the
+ * Sherman–Morrison–Woodbury form Eq. (19), Armijo line search Eq. (13)
+ * (μ = 0.2 at P:497), KKT residuals Eq. (20), σ ← 5σ.
+ * Readings of garbled / silent passages are listed in DESIGN.md ("Readings").
+ *
+ * Conventions (all entry points):
+ *   - fp64 throughout; A is column-major m × n with lda = m (column i = A + i*m).
+ *   - "host" pointers are ordinary CPU memory; "device" pointers are CUDA device memory
+ *     on the handle's device (e.g. torch.Tensor.data_ptr()).
+ *   - Functions return an SSNAL_* status; on failure a thread-local message is
+ *     available from ssnal_en_last_error().  No function falls back to the CPU.
+ *   - One solve in flight per handle; different handles are independent.
+ *   - Limits of this build: 2 ≤ m ≤ 1024, 1 ≤ n < 2^31.
+ */
+#ifndef SSNAL_EN_H
+#define SSNAL_EN_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  SSNAL_OK = 0,            /* converged (solve) / success                               */
+  SSNAL_NOT_CONVERGED = 1, /* iteration cap hit; x_out and stats are still written      */
+  SSNAL_EINVAL = 2,        /* bad argument (sizes, NaN/Inf, zero column, λ, σ0, tol …)   */
+  SSNAL_ECUDA = 3,         /* CUDA error or out of device memory                        */
+  SSNAL_ENUMERIC = 4       /* non-positive Cholesky pivot or NaN in an iterate          */
+};
+
+typedef struct ssnal_en_problem ssnal_en_problem; /* opaque handle */
+
+typedef struct {
+  int32_t status;          /* SSNAL_OK / SSNAL_NOT_CONVERGED / SSNAL_ENUMERIC            */
+  int32_t outer_iters;     /* augmented-Lagrangian iterations (the paper's "(k)", R23)   */
+  int32_t newton_iters;    /* semi-smooth Newton steps, summed over outer iterations      */
+  int32_t psi_evals;       /* ψ evaluations (Armijo trials incl. backtracks)              */
+  int32_t backtracks;      /* step halvings                                               */
+  int32_t aty_passes;      /* full passes over A (K1 launches)                            */
+  int32_t branch_steps[3]; /* Newton steps with r = 0, 0 < r < m (Eq. 19), r ≥ m (Eq. 18) */
+  int32_t line_search_stalled; /* max_backtracks reached at least once (R30)              */
+  int64_t active;          /* nnz(x) at return                                            */
+  double res_kkt1;         /* ‖y + b − Ax‖/(1 + ‖b‖) at the last evaluation, Eq. (20)    */
+  double res_kkt3;         /* ‖Aᵀy + z‖/(1 + ‖y‖ + ‖z‖) at the last outer step, Eq. (20) */
+  double primal_obj;       /* F(x), Eq. (1)                                               */
+  double dual_obj;         /* −h*(y) − p*(Aᵀy) at the final y (NaN if λ2 = 0)             */
+  double gap;              /* primal_obj − dual_obj ≥ 0                                   */
+  double sigma_final;      /* σ of the last inner solve                                   */
+  double time_device_s;    /* CUDA-event time of the solve on the handle's stream         */
+  double time_total_s;     /* host wall time of the call, copies included                 */
+  int64_t kernel_launches; /* kernels launched by this call                              */
+  double k1_time_s;        /* Σ device time of K1 launches (option time_k1 = 1), else 0   */
+  int32_t k1_launches;     /* K1 launches timed                                           */
+  int32_t reserved;
+} ssnal_en_stats;
+
+/* Copy A (host, column-major m × n) and b (host, m) to the current device; the handle owns
+ * the copies (caller may free its buffers).  Also computes λmax = ‖Aᵀb‖∞
+ * with one fused pass.  EINVAL: m < 2, m > 1024, n < 1, NaN/Inf or an all-zero column. */
+int ssnal_en_create(const double* A_colmajor, const double* b, int64_t m, int64_t n, ssnal_en_problem** out);
+
+/* Borrow device buffers dA (column-major, 16-byte aligned) and db; the caller keeps them
+ * alive until ssnal_en_destroy.  cuda_stream (cudaStream_t, may be NULL = legacy default)
+ * is used for every launch.  Inputs are validated on the device (NaN/Inf, zero columns). */
+int ssnal_en_create_device(const double* dA, const double* db, int64_t m, int64_t n, void* cuda_stream,
+                           ssnal_en_problem** out);
+
+/* ‖Aᵀb‖∞ computed at create (plain K1 pass).  λ1 ≥ this value gives x = 0. */
+double ssnal_en_lambda_max_l1(const ssnal_en_problem* p);
+
+/* Options (defaults from P:497 and DESIGN.md readings):
+ *   sigma_factor=5, sigma_max=1e8, mu=0.2, beta=0.5, max_outer=100, max_inner=100,
+ *   max_backtracks=50, init_mode=1 (y0 = A x0 − b when x0 ≠ 0, else y0 = 0; 0: always y0 = 0),
+ *   time_k1=0 (1: time every K1 launch with CUDA events → stats.k1_time_s),
+ *   cluster_size=0 (auto: 16 if the device allows, else 8).  EINVAL for unknown keys. */
+int ssnal_en_set_option(ssnal_en_problem* p, const char* key, double value);
+
+/* Read-only introspection: "m", "n", "k1_cols", "k1_stages", "k1_grid", "k1_smem",
+ * "cluster_size", "num_sms".  Returns NaN for unknown keys. */
+double ssnal_en_get_info(const ssnal_en_problem* p, const char* key);
+
+/* Solve Algorithm 1 for (λ1, λ2) in the paper's unnormalised units.
+ * σ0 > 0 is the initial augmented-Lagrangian parameter (5e-3 in P:497); tol > 0 the
+ * KKT tolerance: stop when res_kkt3 ≤ tol and res_kkt1 ≤ tol (Eq. (20), R7).
+ * x0 (host, n; NULL = cold start y0 = 0) warm-starts the multiplier.
+ * x_out (host, n, caller-owned) receives x, exactly zero off the active set.
+ * stats may be NULL.  Returns SSNAL_OK, SSNAL_NOT_CONVERGED, SSNAL_EINVAL (λ1 < 0, λ2 < 0,
+ * both zero, σ0 ≤ 0, tol ≤ 0), SSNAL_ENUMERIC or SSNAL_ECUDA. */
+int ssnal_en_solve(ssnal_en_problem* p, double lambda1, double lambda2, double sigma0, double tol,
+                   const double* x0, double* x_out, ssnal_en_stats* stats);
+
+/* As ssnal_en_solve with x0 / x_out as DEVICE pointers (x0 may be NULL; x0 == x_out allowed). */
+int ssnal_en_solve_device(ssnal_en_problem* p, double lambda1, double lambda2, double sigma0, double tol,
+                          const double* x0_dev, double* x_out_dev, ssnal_en_stats* stats);
+
+/* K1 hook (tests / bandwidth sweep).  All vector arguments are DEVICE pointers.
+ * One fused pass at y (m) with multiplier x (n) and (σ, λ1, λ2):
+ *   w_out (n) = Aᵀy; J_out (int32, capacity n) = {i : |x_i − σ w_i| > σλ1} ascending (Eq. (17));
+ *   PJ_out (capacity n) = prox_{σp}(x − σw)_J (Eq. (6)); *r_out (host) = |J|;
+ *   partials_out (host, 4) = [Σ P², Σ (x − P)², Σ z², Σ ((|w| − λ1)_+)²] with z = (x − P)/σ − w;
+ *   grad_out (device m, nullable) = y + b − A_J P_J (Eq. (15)).
+ * Synchronises the handle's stream before returning. */
+int ssnal_en_aty_fused(ssnal_en_problem* p, const double* y, const double* x, double sigma, double lambda1,
+                       double lambda2, double* w_out, int32_t* J_out, double* PJ_out, int64_t* r_out,
+                       double partials_out[4], double* grad_out);
+
+/* K1e hook: the K1 epilogue from a stored w0 (device, n) — or from w0 + s (w1 − w0) when
+ * w1 != NULL (Armijo backtrack by linearity) — without touching A.  Same outputs as
+ * ssnal_en_aty_fused except the gradient; w_out (nullable) receives the effective w. */
+int ssnal_en_epilogue(ssnal_en_problem* p, const double* w0, const double* w1, double s, const double* x,
+                      double sigma, double lambda1, double lambda2, double* w_out, int32_t* J_out,
+                      double* PJ_out, int64_t* r_out, double partials_out[4]);
+
+/* K2–K4 hook: the Newton direction d (device, m) solving (I_m + κ A_J A_Jᵀ) d = −g for the
+ * active set J (device int32, r entries, ascending) and g (device, m): r = 0 → d = −g;
+ * 0 < r < m → SMW Eq. (19); r ≥ m → m × m Cholesky Eq. (18).  *gd_out (host) = gᵀd,
+ * *branch_out (host) ∈ {0, 1, 2}.  SSNAL_ENUMERIC if a Cholesky pivot is not positive. */
+int ssnal_en_newton_direction(ssnal_en_problem* p, const int32_t* J, int64_t r, const double* g, double kappa,
+                              double* d_out, double* gd_out, int32_t* branch_out);
+
+void ssnal_en_destroy(ssnal_en_problem* p);
+
+/* Thread-local message of the last failure on this thread ("" if none). */
+const char* ssnal_en_last_error(void);
+
+/* Build identification string (arch, version). */
+const char* ssnal_en_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SSNAL_EN_H */

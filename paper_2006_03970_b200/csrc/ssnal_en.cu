@@ -1,0 +1,1074 @@
+// ssnal_en.cu — C ABI + solver driver for the B200 SsNAL-EN hot path.
+//
+// The driver enqueues the kernels of k_aty.cuh / k_newton.cuh on the handle's stream
+// and runs Algorithm 1 with the readings of DESIGN.md.  Control
+// decisions (inner stop, branch on r, Armijo) read one small EvalOut record back per
+// ψ evaluation; all vector arithmetic stays on the device.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <stdarg.h>
+
+#include <chrono>
+#include <string>
+#include <vector>
+
+#include "k_aty.cuh"
+#include "k_newton.cuh"
+#include "ssnal_en.h"
+
+using namespace ssn;
+
+namespace {
+
+thread_local std::string g_err;
+
+void set_err(const char* fmt, ...) __attribute__((format(printf, 1, 2)));
+void set_err(const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+}
+
+#define CK(call)                                                                         \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess) {                                                             \
+      set_err("%s:%d %s: %s", __FILE__, __LINE__, #call, cudaGetErrorString(e_));       \
+      return SSNAL_ECUDA;                                                                \
+    }                                                                                    \
+  } while (0)
+
+#define CKL()                                                                            \
+  do {                                                                                   \
+    cudaError_t e_ = cudaGetLastError();                                                 \
+    if (e_ != cudaSuccess) {                                                             \
+      set_err("%s:%d launch: %s", __FILE__, __LINE__, cudaGetErrorString(e_));           \
+      return SSNAL_ECUDA;                                                                \
+    }                                                                                    \
+  } while (0)
+
+constexpr double kEps = 2.220446049250313e-16;
+
+Scal make_scal(double sigma, double l1, double l2) {
+  // Same operation order as the oracle (plain IEEE double, no contraction on x86-64).
+  Scal s;
+  s.sigma = sigma;
+  s.l1 = l1;
+  s.l2 = l2;
+  s.thr = sigma * l1;
+  s.den = 1.0 + sigma * l2;
+  s.cpsi = (1.0 + sigma * l2) / (2.0 * sigma);
+  s.kappa = sigma / (1.0 + sigma * l2);
+  return s;
+}
+
+int mr_bucket(int64_t m) {
+  if (m <= 32) return 1;
+  if (m <= 64) return 2;
+  if (m <= 128) return 4;
+  if (m <= 256) return 8;
+  if (m <= 512) return 16;
+  return 32;
+}
+
+typedef void (*k1_fn)(const K1Params);
+typedef void (*gax_fn)(const double*, int64_t, const int32_t*, const double*, int64_t, double*);
+
+k1_fn k1_for(int mr) {
+  switch (mr) {
+    case 1: return k1_aty_fused<1>;
+    case 2: return k1_aty_fused<2>;
+    case 4: return k1_aty_fused<4>;
+    case 8: return k1_aty_fused<8>;
+    case 16: return k1_aty_fused<16>;
+    default: return k1_aty_fused<32>;
+  }
+}
+gax_fn gax_for(int mr) {
+  switch (mr) {
+    case 1: return k_gather_axpy<1>;
+    case 2: return k_gather_axpy<2>;
+    case 4: return k_gather_axpy<4>;
+    case 8: return k_gather_axpy<8>;
+    case 16: return k_gather_axpy<16>;
+    default: return k_gather_axpy<32>;
+  }
+}
+
+// Validation of A on the device: one warp per column; flag[0] = non-finite count,
+// flag[1] = zero-column count.
+__global__ void k_validate(const double* A, int64_t m, int64_t n, const double* b, int* flag) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = wid; i < n; i += nw) {
+    const double* col = A + i * m;
+    int bad = 0, nz = 0;
+    for (int64_t k = lane; k < m; k += 32) {
+      const double v = col[k];
+      if (!isfinite(v)) bad = 1;
+      if (v != 0.0) nz = 1;
+    }
+    bad = __any_sync(0xffffffffu, bad);
+    nz = __any_sync(0xffffffffu, nz);
+    if (lane == 0) {
+      if (bad) atomicAdd(&flag[0], 1);
+      if (!nz) atomicAdd(&flag[1], 1);
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x < 32) {
+    int bad = 0;
+    for (int64_t k = threadIdx.x; k < m; k += 32)
+      if (!isfinite(b[k])) bad = 1;
+    bad = __any_sync(0xffffffffu, bad);
+    if (threadIdx.x == 0 && bad) atomicAdd(&flag[0], 1);
+  }
+}
+
+// Primal objective pieces at x (support Jx, Px, rx) with resid = A x − b:
+// out[0] = ½‖resid‖², out[1] = Σ|x|, out[2] = Σ x², out[3] = nnz
+__global__ void k_objective(int64_t m, const double* resid, const double* Px, const int64_t* rx, double* out) {
+  __shared__ double red[3][32];
+  const int tid = threadIdx.x;
+  double a = 0, l1 = 0, q = 0;
+  for (int64_t k = tid; k < m; k += blockDim.x) a += resid[k] * resid[k];
+  const int64_t r = *rx;
+  for (int64_t i = tid; i < r; i += blockDim.x) {
+    l1 += fabs(Px[i]);
+    q += Px[i] * Px[i];
+  }
+  a = warp_allsum(a);
+  l1 = warp_allsum(l1);
+  q = warp_allsum(q);
+  if ((tid & 31) == 0) {
+    red[0][tid >> 5] = a;
+    red[1][tid >> 5] = l1;
+    red[2][tid >> 5] = q;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double s[3] = {0, 0, 0};
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w)
+      for (int j = 0; j < 3; ++j) s[j] += red[j][w];
+    out[0] = 0.5 * s[0];
+    out[1] = s[1];
+    out[2] = s[2];
+    out[3] = (double)r;
+  }
+}
+
+}  // namespace
+
+// ===========================================================================
+struct ssnal_en_problem {
+  int64_t m = 0, n = 0;
+  int dev = 0, nsm = 0;
+  const double* A = nullptr;
+  const double* b = nullptr;
+  double* A_own = nullptr;
+  double* b_own = nullptr;
+  cudaStream_t st = nullptr;
+  // K1 configuration
+  int MR = 0, C = 0, S = 0, G = 0;
+  int64_t T = 0;
+  size_t k1_smem = 0;
+  uint32_t stage_elems = 0, xstage_elems = 0;
+  int cluster = 16;
+  size_t chol_smem = 0;
+  int gax_grid = 0;
+  // device buffers
+  double* w[3] = {nullptr, nullptr, nullptr};  // current / trial / backtrack
+  double* x = nullptr;
+  int32_t* seg_idx = nullptr;
+  double* seg_P = nullptr;
+  int* cta_cnt = nullptr;
+  double* part_scal = nullptr;
+  double* part_vec = nullptr;
+  int32_t* J[2] = {nullptr, nullptr};
+  double* PJ[2] = {nullptr, nullptr};
+  int64_t* r_dev = nullptr;  // [0], [1]: J sets; [2]: support of x
+  int32_t* Jx = nullptr;
+  double* Px = nullptr;
+  double* y[2] = {nullptr, nullptr};
+  double* g[2] = {nullptr, nullptr};
+  double* d = nullptr;
+  double* u = nullptr;
+  double* tmpm = nullptr;
+  double* Mmat = nullptr;
+  double* W = nullptr;
+  int W_splits = 0;
+  int* info = nullptr;
+  EvalOut* ev_dev = nullptr;   // slots
+  EvalOut* ev_host = nullptr;  // pinned mirror
+  double* scratch = nullptr;   // small device scratch (objective, λmax)
+  double* scratch_host = nullptr;
+  int* flags = nullptr;
+  // state
+  double lambda_max = 0, nb = 0;
+  // options
+  double sigma_factor = 5.0, sigma_max = 1e8, mu = 0.2, beta = 0.5;
+  int max_outer = 100, max_inner = 100, max_bt = 50, init_mode = 1, time_k1 = 0;
+  // counters for the current call
+  int64_t launches = 0;
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> k1_pending;
+  double k1_time = 0;
+  int k1_count = 0;
+};
+
+namespace {
+
+int alloc(void** p, size_t bytes) {
+  cudaError_t e = cudaMalloc(p, bytes > 0 ? bytes : 16);
+  if (e != cudaSuccess) {
+    set_err("cudaMalloc(%zu): %s", bytes, cudaGetErrorString(e));
+    return SSNAL_ECUDA;
+  }
+  return SSNAL_OK;
+}
+
+#define AL(ptr, bytes)                                            \
+  do {                                                            \
+    int rc_ = alloc((void**)&(ptr), (bytes));                     \
+    if (rc_) return rc_;                                          \
+  } while (0)
+
+int configure(ssnal_en_problem* P) {
+  const int64_t m = P->m, n = P->n;
+  P->MR = mr_bucket(m);
+  const int64_t bytes_col = 8 * m;
+  int k = (int)(32768 / (K1_NWC * bytes_col));
+  if (k < 1) k = 1;
+  if (k > 32) k = 32;  // ≤ 256 columns per tile (per-tile epilogue buffers)
+  P->C = K1_NWC * k;
+  P->stage_elems = (uint32_t)(((int64_t)P->C * m + 15) / 16 * 16);
+  P->xstage_elems = (uint32_t)((P->C + 15) / 16 * 16);
+  const size_t per_stage = (size_t)(P->stage_elems + P->xstage_elems) * 8;
+  int S = (int)((200 * 1024) / per_stage);
+  if (S > 8) S = 8;
+  if (S < 2) S = 2;
+  while ((size_t)S * P->stage_elems < (size_t)K1_NWC * m + K1_NWC * 4 + K1_NWC) ++S;
+  P->S = S;
+  P->k1_smem = (size_t)S * per_stage + 2 * S * 8 + 2 * P->C * 8 + 2 * P->C * 8 + 2 * P->C * 4 + 16;
+  P->T = (n + P->C - 1) / P->C;
+  P->G = (int)(P->T < P->nsm ? P->T : P->nsm);
+  P->gax_grid = P->nsm;
+  if (P->k1_smem > 227 * 1024) {
+    set_err("K1 shared memory %zu exceeds 227 KB (m=%lld)", P->k1_smem, (long long)m);
+    return SSNAL_EINVAL;
+  }
+  CK(cudaFuncSetAttribute(k1_for(P->MR), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->k1_smem));
+  const size_t gsm = (size_t)8 * m * 8;
+  CK(cudaFuncSetAttribute(gax_for(P->MR), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsm));
+  P->chol_smem = (size_t)(32 * 33 + 32 + 8 * 32 * 32) * 8;
+  CK(cudaFuncSetAttribute(k_chol_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->chol_smem));
+  CK(cudaFuncSetAttribute(k_chol_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  CK(cudaFuncSetAttribute(k_chol_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(m * 8)));
+  // cluster size: 16 (non-portable) when schedulable, else 8
+  {
+    int want = P->cluster > 0 ? P->cluster : 16;
+    for (; want >= 1; want /= 2) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(want);
+      cfg.blockDim = dim3(256);
+      cfg.dynamicSmemBytes = P->chol_smem;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = want;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      int nclus = 0;
+      if (cudaOccupancyMaxActiveClusters(&nclus, k_chol_cluster, &cfg) == cudaSuccess && nclus >= 1) break;
+      cudaGetLastError();
+    }
+    P->cluster = want < 1 ? 1 : want;
+  }
+  return SSNAL_OK;
+}
+
+int allocate(ssnal_en_problem* P) {
+  const int64_t m = P->m, n = P->n;
+  for (int i = 0; i < 3; ++i) AL(P->w[i], n * 8);
+  AL(P->x, n * 8);
+  AL(P->seg_idx, n * 4);
+  AL(P->seg_P, n * 8);
+  AL(P->cta_cnt, (size_t)P->nsm * 4 + 64);
+  AL(P->part_scal, (size_t)P->nsm * 4 * 8 + 64);
+  AL(P->part_vec, (size_t)P->nsm * m * 8);
+  for (int i = 0; i < 2; ++i) {
+    AL(P->J[i], n * 4);
+    AL(P->PJ[i], n * 8);
+    AL(P->y[i], m * 8);
+    AL(P->g[i], m * 8);
+  }
+  AL(P->r_dev, 8 * 8);
+  AL(P->Jx, n * 4);
+  AL(P->Px, n * 8);
+  AL(P->d, m * 8);
+  AL(P->u, m * 8);
+  AL(P->tmpm, m * 8);
+  AL(P->Mmat, (size_t)m * m * 8);
+  P->W_splits = 16;
+  AL(P->W, (size_t)P->W_splits * m * m * 8);
+  AL(P->info, 64);
+  AL(P->ev_dev, sizeof(EvalOut) * 4);
+  AL(P->scratch, 64 * 8);
+  AL(P->flags, 64);
+  CK(cudaMallocHost((void**)&P->ev_host, sizeof(EvalOut) * 4));
+  CK(cudaMallocHost((void**)&P->scratch_host, 64 * 8));
+  return SSNAL_OK;
+}
+
+// ---------------- launch wrappers ----------------
+
+cudaEvent_t take_event(ssnal_en_problem* P) {
+  if (!P->ev_pool.empty()) {
+    cudaEvent_t e = P->ev_pool.back();
+    P->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+void harvest_k1(ssnal_en_problem* P) {  // call after a stream sync
+  for (auto& pr : P->k1_pending) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, pr.first, pr.second);
+    P->k1_time += ms * 1e-3;
+    P->k1_count++;
+    P->ev_pool.push_back(pr.first);
+    P->ev_pool.push_back(pr.second);
+  }
+  P->k1_pending.clear();
+}
+
+// K1 at y (device, m).  fused=0: plain w = Aᵀy into w_out (+ per-CTA max|w|).
+int launch_k1(ssnal_en_problem* P, const double* y, const double* x, const Scal& sc, int fused, double* w_out) {
+  K1Params k;
+  k.A = P->A;
+  k.m = P->m;
+  k.n = P->n;
+  k.y = y;
+  k.x = x;
+  k.w_out = w_out;
+  k.seg_idx = P->seg_idx;
+  k.seg_P = P->seg_P;
+  k.cta_cnt = P->cta_cnt;
+  k.part_scal = P->part_scal;
+  k.part_vec = fused ? P->part_vec : nullptr;
+  k.sc = sc;
+  k.C = P->C;
+  k.T = P->T;
+  k.stages = P->S;
+  k.fused = fused;
+  k.stage_elems = P->stage_elems;
+  k.xstage_elems = P->xstage_elems;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (P->time_k1) {
+    e0 = take_event(P);
+    e1 = take_event(P);
+    cudaEventRecord(e0, P->st);
+  }
+  k1_for(P->MR)<<<P->G, K1_THREADS, P->k1_smem, P->st>>>(k);
+  P->launches++;
+  if (P->time_k1) {
+    cudaEventRecord(e1, P->st);
+    P->k1_pending.push_back({e0, e1});
+  }
+  CKL();
+  return SSNAL_OK;
+}
+
+int launch_k1e(ssnal_en_problem* P, const double* w0, const double* w1, double s, const double* x, const Scal& sc,
+               double* w_out) {
+  K1eParams k;
+  k.n = P->n;
+  k.w0 = w0;
+  k.w1 = w1;
+  k.s = s;
+  k.x = x;
+  k.w_out = w_out;
+  k.seg_idx = P->seg_idx;
+  k.seg_P = P->seg_P;
+  k.cta_cnt = P->cta_cnt;
+  k.part_scal = P->part_scal;
+  k.sc = sc;
+  k.C = P->C;
+  k.T = P->T;
+  k1e_epilogue<<<P->G, K1E_THREADS, 0, P->st>>>(k);
+  P->launches++;
+  CKL();
+  return SSNAL_OK;
+}
+
+int launch_finalize(ssnal_en_problem* P, int32_t* J, double* PJ, int64_t* r_dev) {
+  k1_finalize<<<P->G, 256, 0, P->st>>>(P->seg_idx, P->seg_P, P->cta_cnt, P->G, P->T, P->C, P->n, J, PJ, r_dev);
+  P->launches++;
+  CKL();
+  return SSNAL_OK;
+}
+
+// parts (P->part_vec, `grid` rows) = Σ coef_a A[:, J_a] over r (host-known) columns
+int launch_gather(ssnal_en_problem* P, const int32_t* J, const double* coef, int64_t r, int* grid_out) {
+  int grid = (int)((r + 63) / 64);
+  if (grid > P->gax_grid) grid = P->gax_grid;
+  if (grid < 1) grid = 1;
+  gax_for(P->MR)<<<grid, 256, (size_t)8 * P->m * 8, P->st>>>(P->A, P->m, J, coef, r, P->part_vec);
+  P->launches++;
+  *grid_out = grid;
+  CKL();
+  return SSNAL_OK;
+}
+
+int launch_eval(ssnal_en_problem* P, const double* y, const Scal& sc, int with_grad, const int* valid, int nparts,
+                double* g_out, const int64_t* r_dev, int slot) {
+  k_eval_reduce<<<1, K5_THREADS, 0, P->st>>>(P->m, y, P->b, P->part_vec, valid, nparts, P->part_scal, P->G, sc,
+                                              P->nb, with_grad, g_out, r_dev, P->ev_dev + slot);
+  P->launches++;
+  CKL();
+  return SSNAL_OK;
+}
+
+int fetch_eval(ssnal_en_problem* P, int slot, EvalOut* out) {
+  CK(cudaMemcpyAsync(P->ev_host + slot, P->ev_dev + slot, sizeof(EvalOut), cudaMemcpyDeviceToHost, P->st));
+  CK(cudaStreamSynchronize(P->st));
+  harvest_k1(P);
+  *out = P->ev_host[slot];
+  return SSNAL_OK;
+}
+
+int launch_chol(ssnal_en_problem* P, double* M, int N) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(P->cluster);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = P->chol_smem;
+  cfg.stream = P->st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = P->cluster;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, k_chol_cluster, M, N, N, P->info));
+  P->launches++;
+  return SSNAL_OK;
+}
+
+// Newton direction for (J, r) at gradient g: d ← solution, *gd_dev ← gᵀd.  Eq. (18)/(19).
+int newton_direction(ssnal_en_problem* P, const int32_t* J, int64_t r, const double* g, double kappa, double* d,
+                     double* gd_dev, int* branch) {
+  const int64_t m = P->m;
+  if (r == 0) {
+    k_neg_copy<<<1, 1024, 0, P->st>>>(m, g, d, g, gd_dev);
+    P->launches++;
+    CKL();
+    *branch = 0;
+    return SSNAL_OK;
+  }
+  CK(cudaMemsetAsync(P->info, 0, sizeof(int), P->st));
+  if (r < m) {  // Sherman–Morrison–Woodbury, Eq. (19): factor κ⁻¹I_r + A_JᵀA_J (R13)
+    const int N = (int)r;
+    const int nt = (N + 31) / 32;
+    k_gram_smw<<<nt * (nt + 1) / 2, 256, 0, P->st>>>(P->A, m, J, N, 1.0 / kappa, P->Mmat);
+    P->launches++;
+    CKL();
+    int wg = (int)((r * 32 + 255) / 256);
+    if (wg > 4 * P->nsm) wg = 4 * P->nsm;
+    k_jt_gemv<<<wg, 256, 0, P->st>>>(P->A, m, J, r, g, P->u);
+    P->launches++;
+    CKL();
+    int rc = launch_chol(P, P->Mmat, N);
+    if (rc) return rc;
+    k_chol_solve<<<1, 1024, (size_t)N * 8, P->st>>>(P->Mmat, N, N, P->u, 1.0, P->u, nullptr, nullptr);
+    P->launches++;
+    CKL();
+    int grid = 0;
+    rc = launch_gather(P, J, P->u, r, &grid);
+    if (rc) return rc;
+    k_combine<<<1, 1024, 0, P->st>>>(m, g, -1.0, P->part_vec, grid, d, g, gd_dev);  // d = −g + A_J v
+    P->launches++;
+    CKL();
+    *branch = 1;
+    return SSNAL_OK;
+  }
+  // r ≥ m: Eq. (18), M = I_m + κ A_J A_Jᵀ
+  const int nt = (int)((m + 31) / 32);
+  const int tiles = nt * (nt + 1) / 2;
+  int ns = (int)((2 * P->nsm + tiles - 1) / tiles);
+  int64_t maxs = (r + 63) / 64;
+  if (ns > maxs) ns = (int)maxs;
+  if (ns > P->W_splits) ns = P->W_splits;
+  if (ns < 1) ns = 1;
+  k_gram_mm<<<dim3(tiles, ns), 256, 0, P->st>>>(P->A, m, J, r, P->W);
+  P->launches++;
+  CKL();
+  k_gram_mm_reduce<<<(unsigned)((m * m + 255) / 256), 256, 0, P->st>>>(P->W, ns, m, kappa, P->Mmat);
+  P->launches++;
+  CKL();
+  int rc = launch_chol(P, P->Mmat, (int)m);
+  if (rc) return rc;
+  k_chol_solve<<<1, 1024, (size_t)m * 8, P->st>>>(P->Mmat, (int)m, (int)m, g, -1.0, d, g, gd_dev);
+  P->launches++;
+  CKL();
+  *branch = 2;
+  return SSNAL_OK;
+}
+
+int check_args(ssnal_en_problem* P, double l1, double l2, double sigma0, double tol) {
+  if (!P) {
+    set_err("null handle");
+    return SSNAL_EINVAL;
+  }
+  if (!(l1 >= 0) || !(l2 >= 0) || (l1 == 0 && l2 == 0) || !isfinite(l1) || !isfinite(l2)) {
+    set_err("invalid lambda (l1=%g, l2=%g)", l1, l2);
+    return SSNAL_EINVAL;
+  }
+  if (!(sigma0 > 0) || !isfinite(sigma0)) {
+    set_err("invalid sigma0 %g", sigma0);
+    return SSNAL_EINVAL;
+  }
+  if (!(tol > 0)) {
+    set_err("invalid tol %g", tol);
+    return SSNAL_EINVAL;
+  }
+  return SSNAL_OK;
+}
+
+// ---------------- Algorithm 1 ----------------
+// x (P->x) holds x0 on entry (device); on exit P->x holds the solution.
+int solve_core(ssnal_en_problem* P, double l1, double l2, double sigma0, double tol, int have_x0,
+               ssnal_en_stats* S) {
+  const int64_t m = P->m, n = P->n;
+  memset(S, 0, sizeof(*S));
+  int rc;
+  int cur = 0;  // index of current J/PJ/y/g
+  int wcur = 0; // index of current w buffer (0..2)
+  EvalOut ev, evt;
+
+  // Support of x (Jx, Px, rx): K1e with w = 0, σ = 1, λ = 0 selects x ≠ 0 and P = x.
+  int64_t rx = 0;
+  if (have_x0) {
+    CK(cudaMemsetAsync(P->w[2], 0, n * 8, P->st));
+    const Scal s0 = make_scal(1.0, 0.0, 0.0);
+    if ((rc = launch_k1e(P, P->w[2], nullptr, 0.0, P->x, s0, nullptr))) return rc;
+    if ((rc = launch_finalize(P, P->Jx, P->Px, P->r_dev + 2))) return rc;
+    CK(cudaMemcpyAsync(P->scratch_host, P->r_dev + 2, 8, cudaMemcpyDeviceToHost, P->st));
+    CK(cudaStreamSynchronize(P->st));
+    memcpy(&rx, P->scratch_host, 8);
+  } else {
+    CK(cudaMemsetAsync(P->x, 0, n * 8, P->st));
+    CK(cudaMemsetAsync(P->r_dev + 2, 0, 8, P->st));
+  }
+  // Initial y, w (P:242 silent; reading R8)
+  if (rx > 0 && P->init_mode == 1) {
+    int grid = 0;
+    if ((rc = launch_gather(P, P->Jx, P->Px, rx, &grid))) return rc;
+    k_combine<<<1, 1024, 0, P->st>>>(m, P->b, -1.0, P->part_vec, grid, P->y[cur], nullptr, nullptr);  // A x0 − b
+    P->launches++;
+    CKL();
+    if ((rc = launch_k1(P, P->y[cur], nullptr, make_scal(1.0, 0.0, 0.0), 0, P->w[wcur]))) return rc;
+    S->aty_passes++;
+  } else {
+    CK(cudaMemsetAsync(P->y[cur], 0, m * 8, P->st));
+    CK(cudaMemsetAsync(P->w[wcur], 0, n * 8, P->st));
+  }
+
+  double sigma = sigma0;
+  int converged = 0, numeric = 0, k;
+  for (k = 0; k < P->max_outer && !numeric; ++k) {
+    const Scal sc = make_scal(sigma, l1, l2);
+    // EVAL(y, w) with the new (x, σ): K1e + finalize + gather (∇ψ) + reduce
+    if ((rc = launch_k1e(P, P->w[wcur], nullptr, 0.0, P->x, sc, nullptr))) return rc;
+    // partial scalars of K1e are in part_scal; they are reduced by the eval kernel
+    if ((rc = launch_finalize(P, P->J[cur], P->PJ[cur], P->r_dev + cur))) return rc;
+    // r needed on the host to size the gather: read it first
+    CK(cudaMemcpyAsync(P->scratch_host, P->r_dev + cur, 8, cudaMemcpyDeviceToHost, P->st));
+    CK(cudaStreamSynchronize(P->st));
+    int64_t r;
+    memcpy(&r, P->scratch_host, 8);
+    int grid = 0;
+    if (r > 0) {
+      if ((rc = launch_gather(P, P->J[cur], P->PJ[cur], r, &grid))) return rc;
+    }
+    // K1e wrote G scalar partials; the gather wrote `grid` vector partials
+    if ((rc = launch_eval(P, P->y[cur], sc, 1, nullptr, grid, P->g[cur], P->r_dev + cur, 0))) return rc;
+    if ((rc = fetch_eval(P, 0, &ev))) return rc;
+    S->psi_evals++;
+
+    for (int j = 0; j < P->max_inner; ++j) {
+      if (ev.res1 <= tol) break;  // inner stop, Eq. (20) res(kkt1) (R6)
+      int br = 0;
+      double* gd_dev = P->scratch;
+      if ((rc = newton_direction(P, P->J[cur], ev.r, P->g[cur], sc.kappa, P->d, gd_dev, &br))) return rc;
+      S->branch_steps[br]++;
+      // trial s = 1: y_t = y + d; K1 fused at y_t
+      const int tr = 1 - cur;
+      const int wtr = (wcur + 1) % 3, wbt = (wcur + 2) % 3;
+      k_axpy_m<<<(unsigned)((m + 255) / 256), 256, 0, P->st>>>(m, P->y[cur], 1.0, P->d, P->y[tr]);
+      P->launches++;
+      CKL();
+      if ((rc = launch_k1(P, P->y[tr], P->x, sc, 1, P->w[wtr]))) return rc;
+      S->aty_passes++;
+      if ((rc = launch_finalize(P, P->J[tr], P->PJ[tr], P->r_dev + tr))) return rc;
+      if ((rc = launch_eval(P, P->y[tr], sc, 1, P->cta_cnt, P->G, P->g[tr], P->r_dev + tr, 1))) return rc;
+      CK(cudaMemcpyAsync(&P->ev_dev[1].gd, gd_dev, 8, cudaMemcpyDeviceToDevice, P->st));
+      CK(cudaMemcpyAsync(P->scratch + 8, P->info, 4, cudaMemcpyDeviceToDevice, P->st));
+      CK(cudaMemcpyAsync(P->scratch_host + 8, P->scratch + 8, 8, cudaMemcpyDeviceToHost, P->st));
+      if ((rc = fetch_eval(P, 1, &evt))) return rc;
+      S->psi_evals++;
+      int info_h = 0;
+      memcpy(&info_h, P->scratch_host + 8, 4);
+      if (br > 0 && info_h != 0) {
+        numeric = 1;
+        set_err("Cholesky pivot not positive (branch %d, r=%lld)", br, (long long)ev.r);
+        break;
+      }
+      const double gd = evt.gd;
+      if (!isfinite(evt.psi) || !isfinite(gd)) {
+        numeric = 1;
+        set_err("non-finite psi/gd");
+        break;
+      }
+      // Armijo, Eq. (13) with μ, halving (R5), roundoff guard (R29)
+      double s = 1.0;
+      int nbt = 0;
+      bool ok = evt.psi - ev.psi <= P->mu * s * gd + 10.0 * kEps * ev.psimag;
+      while (!ok) {
+        if (nbt >= P->max_bt) {
+          S->line_search_stalled = 1;  // R30: accept the last s
+          break;
+        }
+        s *= P->beta;
+        nbt++;
+        // trial y + s d; w_s = w + s (w1 − w) (linearity of Aᵀ, R14)
+        k_axpy_m<<<(unsigned)((m + 255) / 256), 256, 0, P->st>>>(m, P->y[cur], s, P->d, P->y[tr]);
+        P->launches++;
+        CKL();
+        if ((rc = launch_k1e(P, P->w[wcur], P->w[wtr], s, P->x, sc, P->w[wbt]))) return rc;
+        if ((rc = launch_finalize(P, P->J[tr], P->PJ[tr], P->r_dev + tr))) return rc;
+        if ((rc = launch_eval(P, P->y[tr], sc, 0, nullptr, 0, nullptr, P->r_dev + tr, 2))) return rc;
+        EvalOut eb;
+        if ((rc = fetch_eval(P, 2, &eb))) return rc;
+        S->psi_evals++;
+        evt = eb;
+        ok = evt.psi - ev.psi <= P->mu * s * gd + 10.0 * kEps * ev.psimag;
+      }
+      S->backtracks += nbt;
+      // accept: y ← y + s d (Algorithm 1 step (3)); z implicit via P (step (4))
+      if (nbt == 0) {
+        cur = tr;
+        wcur = wtr;
+        ev = evt;
+      } else {
+        cur = tr;
+        wcur = wbt;  // materialised w + s (w1 − w)
+        // ∇ψ at the accepted point needs A_J P_J for the re-thresholded J (K2)
+        const int64_t r2 = evt.r;
+        int grid2 = 0;
+        if (r2 > 0) {
+          if ((rc = launch_gather(P, P->J[cur], P->PJ[cur], r2, &grid2))) return rc;
+        }
+        // scalar partials in part_scal still belong to the accepted K1e launch
+        if ((rc = launch_eval(P, P->y[cur], sc, 1, nullptr, grid2, P->g[cur], P->r_dev + cur, 0))) return rc;
+        if ((rc = fetch_eval(P, 0, &ev))) return rc;
+      }
+      S->newton_iters++;
+    }
+    if (numeric) break;
+    // Multiplier update Eq. (10): x ← x − σ(Aᵀy + z̄) = P (Moreau); res(kkt3) Eq. (20)
+    const double res3 = (sqrt(ev.s[1]) / sigma) / (1.0 + sqrt(ev.yy) + sqrt(ev.s[2]));
+    S->res_kkt3 = res3;
+    S->res_kkt1 = ev.res1;
+    if (rx > 0) {
+      k_zero_at<<<(unsigned)((rx + 255) / 256), 256, 0, P->st>>>(P->Jx, rx, P->x);
+      P->launches++;
+      CKL();
+    }
+    const int64_t rnew = ev.r;
+    if (rnew > 0) {
+      k_scatter<<<(unsigned)((rnew + 255) / 256), 256, 0, P->st>>>(P->J[cur], P->PJ[cur], rnew, P->x);
+      P->launches++;
+      CKL();
+      CK(cudaMemcpyAsync(P->Jx, P->J[cur], rnew * 4, cudaMemcpyDeviceToDevice, P->st));
+      CK(cudaMemcpyAsync(P->Px, P->PJ[cur], rnew * 8, cudaMemcpyDeviceToDevice, P->st));
+    }
+    CK(cudaMemcpyAsync(P->r_dev + 2, P->r_dev + cur, 8, cudaMemcpyDeviceToDevice, P->st));
+    rx = rnew;
+    if (res3 <= tol && ev.res1 <= tol) {  // R7
+      converged = 1;
+      k++;
+      break;
+    }
+    sigma = fmin(P->sigma_factor * sigma, P->sigma_max);  // P:497, R9
+  }
+  S->outer_iters = k;
+  S->sigma_final = sigma;
+  S->status = numeric ? SSNAL_ENUMERIC : (converged ? SSNAL_OK : SSNAL_NOT_CONVERGED);
+  // Stats: F(x) (Eq. (1)) via resid = A x − b; D(y) = −½yᵀy − bᵀy − Σ(|w|−λ1)²₊/(2λ2)
+  {
+    int grid = 0;
+    if (rx > 0) {
+      if ((rc = launch_gather(P, P->Jx, P->Px, rx, &grid))) return rc;
+    }
+    k_combine<<<1, 1024, 0, P->st>>>(m, P->b, -1.0, P->part_vec, grid, P->tmpm, nullptr, nullptr);
+    P->launches++;
+    CKL();
+    k_objective<<<1, 1024, 0, P->st>>>(m, P->tmpm, P->Px, P->r_dev + 2, P->scratch + 16);
+    P->launches++;
+    CKL();
+    CK(cudaMemcpyAsync(P->scratch_host + 16, P->scratch + 16, 4 * 8, cudaMemcpyDeviceToHost, P->st));
+    CK(cudaStreamSynchronize(P->st));
+    harvest_k1(P);
+    const double* o = P->scratch_host + 16;
+    S->primal_obj = o[0] + l1 * o[1] + 0.5 * l2 * o[2];
+    S->active = (int64_t)o[3];
+    S->dual_obj = (l2 > 0) ? (-(0.5 * ev.yy + ev.by) - ev.s[3] / (2.0 * l2)) : NAN;
+    S->gap = S->primal_obj - S->dual_obj;
+  }
+  return S->status;
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+const char* ssnal_en_last_error(void) { return g_err.c_str(); }
+
+const char* ssnal_en_version(void) { return "ssnal_en_b200 0.1 (sm_100a, fp64)"; }
+
+static int create_common(ssnal_en_problem* P) {
+  CK(cudaGetDevice(&P->dev));
+  CK(cudaDeviceGetAttribute(&P->nsm, cudaDevAttrMultiProcessorCount, P->dev));
+  int rc = configure(P);
+  if (rc) return rc;
+  rc = allocate(P);
+  if (rc) return rc;
+  // validate inputs on the device
+  CK(cudaMemsetAsync(P->flags, 0, 8, P->st));
+  k_validate<<<4 * P->nsm, 256, 0, P->st>>>(P->A, P->m, P->n, P->b, P->flags);
+  CKL();
+  int hf[2] = {0, 0};
+  CK(cudaMemcpyAsync(P->scratch_host, P->flags, 8, cudaMemcpyDeviceToHost, P->st));
+  CK(cudaStreamSynchronize(P->st));
+  memcpy(hf, P->scratch_host, 8);
+  if (hf[0]) {
+    set_err("A or b contains NaN/Inf (%d columns)", hf[0]);
+    return SSNAL_EINVAL;
+  }
+  if (hf[1]) {
+    set_err("A has %d all-zero columns", hf[1]);
+    return SSNAL_EINVAL;
+  }
+  // λmax = ‖Aᵀb‖∞ (plain K1 pass) and ‖b‖
+  rc = launch_k1(P, P->b, nullptr, make_scal(1.0, 0.0, 0.0), 0, P->w[0]);
+  if (rc) return rc;
+  k_max_partials<<<1, 32, 0, P->st>>>(P->part_scal, P->G, P->scratch);
+  CKL();
+  CK(cudaMemcpyAsync(P->scratch_host, P->scratch, 8, cudaMemcpyDeviceToHost, P->st));
+  std::vector<double> hb(P->m);
+  CK(cudaMemcpyAsync(hb.data(), P->b, P->m * 8, cudaMemcpyDeviceToHost, P->st));
+  CK(cudaStreamSynchronize(P->st));
+  P->lambda_max = P->scratch_host[0];
+  double nb = 0;
+  for (int64_t k = 0; k < P->m; ++k) nb += hb[k] * hb[k];
+  P->nb = sqrt(nb);
+  P->k1_pending.clear();
+  return SSNAL_OK;
+}
+
+static void destroy_bufs(ssnal_en_problem* P) {
+  if (!P) return;
+  for (int i = 0; i < 3; ++i) cudaFree(P->w[i]);
+  cudaFree(P->x);
+  cudaFree(P->seg_idx);
+  cudaFree(P->seg_P);
+  cudaFree(P->cta_cnt);
+  cudaFree(P->part_scal);
+  cudaFree(P->part_vec);
+  for (int i = 0; i < 2; ++i) {
+    cudaFree(P->J[i]);
+    cudaFree(P->PJ[i]);
+    cudaFree(P->y[i]);
+    cudaFree(P->g[i]);
+  }
+  cudaFree(P->r_dev);
+  cudaFree(P->Jx);
+  cudaFree(P->Px);
+  cudaFree(P->d);
+  cudaFree(P->u);
+  cudaFree(P->tmpm);
+  cudaFree(P->Mmat);
+  cudaFree(P->W);
+  cudaFree(P->info);
+  cudaFree(P->ev_dev);
+  cudaFree(P->scratch);
+  cudaFree(P->flags);
+  if (P->ev_host) cudaFreeHost(P->ev_host);
+  if (P->scratch_host) cudaFreeHost(P->scratch_host);
+  for (auto e : P->ev_pool) cudaEventDestroy(e);
+  for (auto& pr : P->k1_pending) {
+    cudaEventDestroy(pr.first);
+    cudaEventDestroy(pr.second);
+  }
+  cudaFree(P->A_own);
+  cudaFree(P->b_own);
+}
+
+static int check_dims(int64_t m, int64_t n) {
+  if (m < 2 || m > 1024 || n < 1 || n >= ((int64_t)1 << 31)) {
+    set_err("unsupported size m=%lld n=%lld (need 2<=m<=1024, 1<=n<2^31)", (long long)m, (long long)n);
+    return SSNAL_EINVAL;
+  }
+  return SSNAL_OK;
+}
+
+int ssnal_en_create(const double* A_colmajor, const double* b, int64_t m, int64_t n, ssnal_en_problem** out) {
+  if (!out || !A_colmajor || !b) {
+    set_err("null argument");
+    return SSNAL_EINVAL;
+  }
+  *out = nullptr;
+  int rc = check_dims(m, n);
+  if (rc) return rc;
+  ssnal_en_problem* P = new ssnal_en_problem();
+  P->m = m;
+  P->n = n;
+  if (cudaMalloc((void**)&P->A_own, (size_t)m * n * 8 + 64) != cudaSuccess ||
+      cudaMalloc((void**)&P->b_own, (size_t)m * 8 + 64) != cudaSuccess) {
+    set_err("cudaMalloc for A (%zu bytes) failed", (size_t)m * n * 8);
+    destroy_bufs(P);
+    delete P;
+    return SSNAL_ECUDA;
+  }
+  if (cudaMemcpy(P->A_own, A_colmajor, (size_t)m * n * 8, cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemcpy(P->b_own, b, (size_t)m * 8, cudaMemcpyHostToDevice) != cudaSuccess) {
+    set_err("H2D copy failed");
+    destroy_bufs(P);
+    delete P;
+    return SSNAL_ECUDA;
+  }
+  P->A = P->A_own;
+  P->b = P->b_own;
+  P->st = nullptr;
+  rc = create_common(P);
+  if (rc) {
+    destroy_bufs(P);
+    delete P;
+    return rc;
+  }
+  *out = P;
+  return SSNAL_OK;
+}
+
+int ssnal_en_create_device(const double* dA, const double* db, int64_t m, int64_t n, void* cuda_stream,
+                           ssnal_en_problem** out) {
+  if (!out || !dA || !db) {
+    set_err("null argument");
+    return SSNAL_EINVAL;
+  }
+  *out = nullptr;
+  int rc = check_dims(m, n);
+  if (rc) return rc;
+  if (((uintptr_t)dA & 15) != 0) {
+    set_err("dA must be 16-byte aligned");
+    return SSNAL_EINVAL;
+  }
+  ssnal_en_problem* P = new ssnal_en_problem();
+  P->m = m;
+  P->n = n;
+  P->A = dA;
+  P->b = db;
+  P->st = (cudaStream_t)cuda_stream;
+  rc = create_common(P);
+  if (rc) {
+    destroy_bufs(P);
+    delete P;
+    return rc;
+  }
+  *out = P;
+  return SSNAL_OK;
+}
+
+double ssnal_en_lambda_max_l1(const ssnal_en_problem* p) { return p ? p->lambda_max : NAN; }
+
+int ssnal_en_set_option(ssnal_en_problem* P, const char* key, double v) {
+  if (!P || !key) {
+    set_err("null argument");
+    return SSNAL_EINVAL;
+  }
+  std::string k(key);
+  if (k == "sigma_factor" && v > 1) P->sigma_factor = v;
+  else if (k == "sigma_max" && v > 0) P->sigma_max = v;
+  else if (k == "mu" && v > 0 && v < 0.5) P->mu = v;
+  else if (k == "beta" && v > 0 && v < 1) P->beta = v;
+  else if (k == "max_outer" && v >= 1) P->max_outer = (int)v;
+  else if (k == "max_inner" && v >= 1) P->max_inner = (int)v;
+  else if (k == "max_backtracks" && v >= 0) P->max_bt = (int)v;
+  else if (k == "init_mode" && (v == 0 || v == 1)) P->init_mode = (int)v;
+  else if (k == "time_k1") P->time_k1 = v != 0;
+  else if (k == "cluster_size" && (v == 1 || v == 2 || v == 4 || v == 8 || v == 16)) {
+    P->cluster = (int)v;
+  } else {
+    set_err("unknown option or bad value: %s=%g", key, v);
+    return SSNAL_EINVAL;
+  }
+  return SSNAL_OK;
+}
+
+double ssnal_en_get_info(const ssnal_en_problem* P, const char* key) {
+  if (!P || !key) return NAN;
+  std::string k(key);
+  if (k == "m") return (double)P->m;
+  if (k == "n") return (double)P->n;
+  if (k == "k1_cols") return P->C;
+  if (k == "k1_stages") return P->S;
+  if (k == "k1_grid") return P->G;
+  if (k == "k1_smem") return (double)P->k1_smem;
+  if (k == "cluster_size") return P->cluster;
+  if (k == "num_sms") return P->nsm;
+  return NAN;
+}
+
+static int solve_wrapped(ssnal_en_problem* P, double l1, double l2, double sigma0, double tol, const double* x0,
+                         int x0_dev, double* x_out, int xout_dev, ssnal_en_stats* stats) {
+  int rc = check_args(P, l1, l2, sigma0, tol);
+  if (rc) return rc;
+  auto t0 = std::chrono::steady_clock::now();
+  P->launches = 0;
+  P->k1_time = 0;
+  P->k1_count = 0;
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventRecord(e0, P->st));
+  if (x0) {
+    CK(cudaMemcpyAsync(P->x, x0, P->n * 8, x0_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, P->st));
+  }
+  ssnal_en_stats S;
+  rc = solve_core(P, l1, l2, sigma0, tol, x0 != nullptr, &S);
+  if (rc == SSNAL_ECUDA || rc == SSNAL_EINVAL) {
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return rc;
+  }
+  if (x_out) {
+    CK(cudaMemcpyAsync(x_out, P->x, P->n * 8, xout_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, P->st));
+  }
+  CK(cudaEventRecord(e1, P->st));
+  CK(cudaStreamSynchronize(P->st));
+  harvest_k1(P);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  S.time_device_s = ms * 1e-3;
+  S.time_total_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  S.kernel_launches = P->launches;
+  S.k1_time_s = P->k1_time;
+  S.k1_launches = P->k1_count;
+  if (stats) *stats = S;
+  return S.status;
+}
+
+int ssnal_en_solve(ssnal_en_problem* P, double l1, double l2, double sigma0, double tol, const double* x0,
+                   double* x_out, ssnal_en_stats* stats) {
+  return solve_wrapped(P, l1, l2, sigma0, tol, x0, 0, x_out, 0, stats);
+}
+
+int ssnal_en_solve_device(ssnal_en_problem* P, double l1, double l2, double sigma0, double tol, const double* x0,
+                          double* x_out, ssnal_en_stats* stats) {
+  return solve_wrapped(P, l1, l2, sigma0, tol, x0, 1, x_out, 1, stats);
+}
+
+int ssnal_en_aty_fused(ssnal_en_problem* P, const double* y, const double* x, double sigma, double l1, double l2,
+                       double* w_out, int32_t* J_out, double* PJ_out, int64_t* r_out, double partials_out[4],
+                       double* grad_out) {
+  if (!P || !y || !x || !w_out || !J_out || !PJ_out || !(sigma > 0)) {
+    set_err("invalid argument");
+    return SSNAL_EINVAL;
+  }
+  P->launches = 0;
+  const Scal sc = make_scal(sigma, l1, l2);
+  int rc = launch_k1(P, y, x, sc, 1, w_out);
+  if (rc) return rc;
+  rc = launch_finalize(P, J_out, PJ_out, P->r_dev + 3);
+  if (rc) return rc;
+  rc = launch_eval(P, y, sc, grad_out != nullptr, P->cta_cnt, P->G, grad_out ? grad_out : P->tmpm, P->r_dev + 3, 3);
+  if (rc) return rc;
+  EvalOut e;
+  rc = fetch_eval(P, 3, &e);
+  if (rc) return rc;
+  if (r_out) *r_out = e.r;
+  if (partials_out)
+    for (int j = 0; j < 4; ++j) partials_out[j] = e.s[j];
+  return SSNAL_OK;
+}
+
+int ssnal_en_epilogue(ssnal_en_problem* P, const double* w0, const double* w1, double s, const double* x,
+                      double sigma, double l1, double l2, double* w_out, int32_t* J_out, double* PJ_out,
+                      int64_t* r_out, double partials_out[4]) {
+  if (!P || !w0 || !x || !J_out || !PJ_out || !(sigma > 0)) {
+    set_err("invalid argument");
+    return SSNAL_EINVAL;
+  }
+  const Scal sc = make_scal(sigma, l1, l2);
+  int rc = launch_k1e(P, w0, w1, s, x, sc, w_out);
+  if (rc) return rc;
+  rc = launch_finalize(P, J_out, PJ_out, P->r_dev + 3);
+  if (rc) return rc;
+  rc = launch_eval(P, P->b, sc, 0, nullptr, 0, nullptr, P->r_dev + 3, 3);
+  if (rc) return rc;
+  EvalOut e;
+  rc = fetch_eval(P, 3, &e);
+  if (rc) return rc;
+  if (r_out) *r_out = e.r;
+  if (partials_out)
+    for (int j = 0; j < 4; ++j) partials_out[j] = e.s[j];
+  return SSNAL_OK;
+}
+
+int ssnal_en_newton_direction(ssnal_en_problem* P, const int32_t* J, int64_t r, const double* g, double kappa,
+                              double* d_out, double* gd_out, int32_t* branch_out) {
+  if (!P || (r > 0 && !J) || !g || !d_out || !(kappa > 0) || r < 0 || r > P->n) {
+    set_err("invalid argument");
+    return SSNAL_EINVAL;
+  }
+  int br = 0;
+  int rc = newton_direction(P, J, r, g, kappa, d_out, P->scratch, &br);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(P->scratch_host, P->scratch, 8, cudaMemcpyDeviceToHost, P->st));
+  CK(cudaMemcpyAsync(P->scratch_host + 1, P->info, 4, cudaMemcpyDeviceToHost, P->st));
+  CK(cudaStreamSynchronize(P->st));
+  if (gd_out) *gd_out = P->scratch_host[0];
+  if (branch_out) *branch_out = br;
+  int info = 0;
+  memcpy(&info, P->scratch_host + 1, 4);
+  if (br > 0 && info) {
+    set_err("Cholesky pivot not positive");
+    return SSNAL_ENUMERIC;
+  }
+  return SSNAL_OK;
+}
+
+void ssnal_en_destroy(ssnal_en_problem* P) {
+  if (!P) return;
+  if (P->st) cudaStreamSynchronize(P->st);
+  else cudaDeviceSynchronize();
+  destroy_bufs(P);
+  delete P;
+}
+
+}  // extern "C"

@@ -1,0 +1,192 @@
+"""ctypes binding of include/ssnal_en.h (argument marshalling only).
+
+Names follow the C ABI: ssnal_en_create / _create_device / _solve / _solve_device /
+_aty_fused / _epilogue / _newton_direction / _lambda_max_l1 / _set_option /
+_get_info / _destroy.  Device pointers are passed as integers (e.g.
+torch.Tensor.data_ptr()); host arrays as numpy float64 arrays.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libssnal_en.so")
+
+SSNAL_OK, SSNAL_NOT_CONVERGED, SSNAL_EINVAL, SSNAL_ECUDA, SSNAL_ENUMERIC = 0, 1, 2, 3, 4
+
+_d = ctypes.c_double
+_i64 = ctypes.c_int64
+_i32 = ctypes.c_int32
+_vp = ctypes.c_void_p
+_dp = ctypes.POINTER(ctypes.c_double)
+
+
+class Stats(ctypes.Structure):
+    """Mirror of ssnal_en_stats."""
+
+    _fields_ = [("status", _i32), ("outer_iters", _i32), ("newton_iters", _i32), ("psi_evals", _i32),
+                ("backtracks", _i32), ("aty_passes", _i32), ("branch_steps", _i32 * 3),
+                ("line_search_stalled", _i32), ("active", _i64), ("res_kkt1", _d), ("res_kkt3", _d),
+                ("primal_obj", _d), ("dual_obj", _d), ("gap", _d), ("sigma_final", _d),
+                ("time_device_s", _d), ("time_total_s", _d), ("kernel_launches", _i64), ("k1_time_s", _d),
+                ("k1_launches", _i32), ("reserved", _i32)]
+
+    def as_dict(self):
+        d = {f: getattr(self, f) for f, _ in self._fields_ if f != "reserved"}
+        d["branch_steps"] = list(self.branch_steps)
+        return d
+
+
+class SsnalError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"ssnal_en error {code}: {msg}")
+        self.code = code
+
+
+_lib = None
+
+
+def load_library():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: build it with `python tools/build.py` "
+                              "(there is no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        P = ctypes.POINTER
+        L.ssnal_en_create.argtypes = [_dp, _dp, _i64, _i64, P(_vp)]
+        L.ssnal_en_create_device.argtypes = [_vp, _vp, _i64, _i64, _vp, P(_vp)]
+        L.ssnal_en_lambda_max_l1.argtypes = [_vp]
+        L.ssnal_en_lambda_max_l1.restype = _d
+        L.ssnal_en_set_option.argtypes = [_vp, ctypes.c_char_p, _d]
+        L.ssnal_en_get_info.argtypes = [_vp, ctypes.c_char_p]
+        L.ssnal_en_get_info.restype = _d
+        L.ssnal_en_solve.argtypes = [_vp, _d, _d, _d, _d, _dp, _dp, P(Stats)]
+        L.ssnal_en_solve_device.argtypes = [_vp, _d, _d, _d, _d, _vp, _vp, P(Stats)]
+        L.ssnal_en_aty_fused.argtypes = [_vp, _vp, _vp, _d, _d, _d, _vp, _vp, _vp, P(_i64), _dp, _vp]
+        L.ssnal_en_epilogue.argtypes = [_vp, _vp, _vp, _d, _vp, _d, _d, _d, _vp, _vp, _vp, P(_i64), _dp]
+        L.ssnal_en_newton_direction.argtypes = [_vp, _vp, _i64, _vp, _d, _vp, _dp, P(_i32)]
+        L.ssnal_en_destroy.argtypes = [_vp]
+        L.ssnal_en_destroy.restype = None
+        L.ssnal_en_last_error.restype = ctypes.c_char_p
+        L.ssnal_en_version.restype = ctypes.c_char_p
+        for f in ("create", "create_device", "set_option", "solve", "solve_device", "aty_fused", "epilogue",
+                  "newton_direction"):
+            getattr(L, "ssnal_en_" + f).restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def _check(rc, allow=(SSNAL_OK,)):
+    if rc not in allow:
+        raise SsnalError(rc, load_library().ssnal_en_last_error().decode())
+    return rc
+
+
+def _f64(a):
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    return a, a.ctypes.data_as(_dp)
+
+
+class Problem:
+    """Handle around ssnal_en_problem.
+
+    Problem(A, b)                          host arrays; A is (n, m) C-contiguous = column-major m x n
+    Problem.from_device(dA, db, m, n, s)   device pointers (borrowed), s = cudaStream_t as int
+    """
+
+    def __init__(self, A=None, b=None, _handle=None, _keep=None):
+        self._lib = load_library()
+        self._keep = _keep
+        if _handle is not None:
+            self._h = _handle
+        else:
+            A, Ap = _f64(A)
+            b, bp = _f64(b)
+            n, m = A.shape
+            h = _vp()
+            _check(self._lib.ssnal_en_create(Ap, bp, m, n, ctypes.byref(h)))
+            self._h = h
+        self.m = int(self.info("m"))
+        self.n = int(self.info("n"))
+
+    @classmethod
+    def from_device(cls, dA: int, db: int, m: int, n: int, stream: int = 0, keep=None):
+        lib = load_library()
+        h = _vp()
+        _check(lib.ssnal_en_create_device(_vp(dA), _vp(db), m, n, _vp(stream), ctypes.byref(h)))
+        return cls(_handle=h, _keep=keep)
+
+    # -- introspection / options --
+    @property
+    def lambda_max_l1(self) -> float:
+        return self._lib.ssnal_en_lambda_max_l1(self._h)
+
+    def info(self, key: str) -> float:
+        return self._lib.ssnal_en_get_info(self._h, key.encode())
+
+    def set_option(self, key: str, value: float):
+        _check(self._lib.ssnal_en_set_option(self._h, key.encode(), float(value)))
+
+    # -- solves --
+    def solve(self, lambda1, lambda2, sigma0=5e-3, tol=1e-6, x0=None):
+        """Host-memory solve: returns (x, stats dict)."""
+        x = np.empty(self.n)
+        st = Stats()
+        x0p = None
+        if x0 is not None:
+            x0, x0p = _f64(x0)
+        rc = self._lib.ssnal_en_solve(self._h, lambda1, lambda2, sigma0, tol, x0p, x.ctypes.data_as(_dp),
+                                      ctypes.byref(st))
+        _check(rc, (SSNAL_OK, SSNAL_NOT_CONVERGED, SSNAL_ENUMERIC))
+        return x, st.as_dict()
+
+    def solve_device(self, lambda1, lambda2, sigma0, tol, x0_ptr, x_out_ptr):
+        st = Stats()
+        rc = self._lib.ssnal_en_solve_device(self._h, lambda1, lambda2, sigma0, tol,
+                                             _vp(x0_ptr) if x0_ptr else None, _vp(x_out_ptr), ctypes.byref(st))
+        _check(rc, (SSNAL_OK, SSNAL_NOT_CONVERGED, SSNAL_ENUMERIC))
+        return st.as_dict()
+
+    # -- kernel hooks (device pointers) --
+    def aty_fused(self, y, x, sigma, l1, l2, w_out, J_out, PJ_out, grad_out=0):
+        r = _i64(0)
+        part = (ctypes.c_double * 4)()
+        _check(self._lib.ssnal_en_aty_fused(self._h, _vp(y), _vp(x), sigma, l1, l2, _vp(w_out), _vp(J_out),
+                                            _vp(PJ_out), ctypes.byref(r), part, _vp(grad_out) if grad_out else None))
+        return r.value, list(part)
+
+    def epilogue(self, w0, w1, s, x, sigma, l1, l2, w_out, J_out, PJ_out):
+        r = _i64(0)
+        part = (ctypes.c_double * 4)()
+        _check(self._lib.ssnal_en_epilogue(self._h, _vp(w0), _vp(w1) if w1 else None, s, _vp(x), sigma, l1, l2,
+                                           _vp(w_out) if w_out else None, _vp(J_out), _vp(PJ_out),
+                                           ctypes.byref(r), part))
+        return r.value, list(part)
+
+    def newton_direction(self, J, r, g, kappa, d_out):
+        gd = _d(0)
+        br = _i32(0)
+        _check(self._lib.ssnal_en_newton_direction(self._h, _vp(J) if J else None, r, _vp(g), kappa, _vp(d_out),
+                                                   ctypes.byref(gd), ctypes.byref(br)))
+        return gd.value, br.value
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.ssnal_en_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
