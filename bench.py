@@ -1,0 +1,402 @@
+#!/usr/bin/env python3
+"""Benchmark of the SsNAL-EN hot path on B200 (BASELINE.json metric).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config cfg2|cfg3|cfg4|cfg5|cfg1] [--sweep]
+
+One "step" is one full time-to-solution of the workload: for cfg2 (BASELINE configs[1],
+the default) the warm-started 10-point λ path c = 0.9 … 0.1 at KKT tolerance 1e-6, i.e.
+every §8(a) row of SURVEY.md (K1 passes, re-thresholds, Newton systems, line searches,
+outer updates).  Inputs are synthetic (synth/), generated directly in HBM; A is 400 MB,
+larger than the 126 MB L2, so no flush is needed between steps.
+
+The JSON line carries: value (device-timed seconds per step, max over ranks), e2e (the same
+through the C-ABI with HOST buffers, create + H2D + solves + D2H inside the timed region),
+roofline of the dominant kernel (K1: algorithmic bytes per launch / mean launch time from CUDA
+events recorded on the launching stream during the timed steps), cpu_baseline (the oracle on
+this host, rank 0 only), clocks sampled during the timed region, gpu_launches.
+
+--impl reference: the base contract's reference arm is, for this paper-only tier, the CPU
+oracle (oracle/), timed on the host cores on the same workload (rank 0 only).
+Multi-GPU (torchrun): the path does not shard; each rank solves
+its own replica; value = max over ranks; scaling "weak".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "time-to-solution (s) at KKT 1e-6; fused A^T·y kernel GB/s vs B200 HBM peak"
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([s.strip() for s in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if "Active" in s[2 + i]
+                          and not s[2 + i].startswith("Not")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def lambdas(cfg, lmax_l1, c):
+    lmax = lmax_l1 / cfg.alpha
+    return c * cfg.alpha * lmax, c * (1 - cfg.alpha) * lmax
+
+
+def k1_bytes(m, n):
+    """Algorithmic bytes of one fused K1 launch: A once (8mn), x read + w write (16n), y (8m)."""
+    return 8 * m * n + 16 * n + 8 * m
+
+
+def run_path_device(P, cfg, lm, x_buf, x_prev_ptr=None):
+    """One step: the workload's solves on device buffers.  Returns (device_s, launches, stats list)."""
+    total_dev = 0.0
+    launches = 0
+    stats = []
+    prev = 0
+    for i, c in enumerate(cfg.cs):
+        l1, l2 = lambdas(cfg, lm, c)
+        x0 = x_buf.data_ptr() if (cfg.path and i > 0) else 0
+        st = P.solve_device(l1, l2, cfg.sigma0, cfg.tol, x0, x_buf.data_ptr())
+        total_dev += st["time_device_s"]
+        launches += st["kernel_launches"]
+        stats.append(st)
+    return total_dev, launches, stats
+
+
+def bench_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2006_03970_b200 import Problem
+
+    torch.cuda.set_device(local_rank)
+    cfg = synth.CONFIGS[args.config]
+    m, n = cfg.m, cfg.n
+    stream = torch.cuda.current_stream()
+    dA = torch.empty((n, m), dtype=torch.float64, device="cuda")
+    synth.fill_device(cfg, dA.data_ptr(), stream.cuda_stream)
+    b_host, _ = synth.response(cfg)
+    db = torch.from_numpy(b_host).cuda()
+    torch.cuda.synchronize()
+    P = Problem.from_device(dA.data_ptr(), db.data_ptr(), m, n, stream.cuda_stream, keep=(dA, db))
+    lm = P.lambda_max_l1
+    x_buf = torch.zeros(n, dtype=torch.float64, device="cuda")
+
+    for _ in range(args.warmup):
+        run_path_device(P, cfg, lm, x_buf)
+    torch.cuda.synchronize()
+
+    # ---- timed region: K steps, K1 launch events on the handle's stream ----
+    P.set_option("time_k1", 1)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    k1_time = 0.0
+    k1_launches = 0
+    launches = 0
+    dev_sum = 0.0
+    last_stats = None
+    with ClockSampler(local_rank) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            d, L, sts = run_path_device(P, cfg, lm, x_buf)
+            dev_sum += d
+            launches += L
+            k1_time += sum(s["k1_time_s"] for s in sts)
+            k1_launches += sum(s["k1_launches"] for s in sts)
+            last_stats = sts
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    P.set_option("time_k1", 0)
+    elapsed = ev0.elapsed_time(ev1) * 1e-3
+    t_step = elapsed / args.steps
+    if world > 1:
+        t = torch.tensor([t_step], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_step = float(t.item())
+
+    # ---- e2e: through the C-ABI with HOST buffers (create + H2D + solves + D2H) ----
+    A_host = None
+    e2e = None
+    if rank == 0 or world > 1:
+        A_host = torch.empty((n, m), dtype=torch.float64, pin_memory=True)
+        A_host.copy_(dA.cpu())
+        A_np = A_host.numpy()
+        e2e_times = []
+        h2d = d2h = 0
+        for it in range(max(1, min(args.steps, 3)) + 1):
+            t0 = time.perf_counter()
+            Q = Problem(A_np, b_host)
+            lmq = Q.lambda_max_l1
+            x_prev = None
+            hb = 8 * m * n + 8 * m
+            db_ = 0
+            for i, c in enumerate(cfg.cs):
+                l1, l2 = lambdas(cfg, lmq, c)
+                x_prev, st = Q.solve(l1, l2, cfg.sigma0, cfg.tol, x0=x_prev if cfg.path else None)
+                if cfg.path and i > 0:
+                    hb += 8 * n
+                db_ += 8 * n
+            Q.close()
+            dt = time.perf_counter() - t0
+            if it > 0:  # first iteration is the e2e warm-up
+                e2e_times.append(dt)
+            h2d, d2h = hb, db_
+        e2e_t = statistics.median(e2e_times)
+        if world > 1:
+            t = torch.tensor([e2e_t], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_t = float(t.item())
+        e2e = {"value": e2e_t, "unit": "s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
+
+    peak, peak_src = _peaks()
+    k1_avg = k1_time / max(k1_launches, 1)
+    k1_gbs = k1_bytes(m, n) / k1_avg / 1e9 if k1_launches else None
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "k1_traffic.json")
+    if os.path.exists(tp):
+        try:
+            tj = json.load(open(tp))
+            traffic = tj.get(args.config)
+        except Exception:
+            traffic = None
+    res = {
+        "metric": METRIC,
+        "value": t_step,
+        "unit": "s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": t_step * 1e3,
+        "higher_is_better": False,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (synth/, seeded; generated in HBM)",
+        "config": {"workload": f"{cfg.name}: m={m} n={n} " + ("warm-started path c=" + ",".join(f"{c:.3g}" for c in cfg.cs)
+                                                              if cfg.path else "c=" + ",".join(str(c) for c in cfg.cs)),
+                   "m": m, "n": n, "alpha": cfg.alpha, "tol": cfg.tol, "sigma0": cfg.sigma0,
+                   "l2_policy": f"A = {8 * m * n / 1e6:.0f} MB > 126 MB L2 (no flush needed)",
+                   "parallelism": f"replicas x{world}"},
+        "roofline": {"bound": "hbm", "achieved": k1_gbs, "peak": peak, "unit": "GB/s",
+                     "frac": (k1_gbs / peak) if k1_gbs else None, "traffic": traffic,
+                     "kernel": "k1_aty_fused", "bytes_per_launch": k1_bytes(m, n), "launches": k1_launches,
+                     "mean_launch_us": k1_avg * 1e6, "share_of_step": k1_time / max(elapsed, 1e-30),
+                     "peak_source": peak_src},
+        "e2e": e2e,
+        "gpu_launches": launches // max(args.steps, 1),
+        "clocks": clk.summary(),
+        "iterations": [{"c": round(c, 4), "outer": s["outer_iters"], "newton": s["newton_iters"],
+                        "passes": s["aty_passes"], "backtracks": s["backtracks"], "r": s["active"],
+                        "res1": s["res_kkt1"], "res3": s["res_kkt3"], "gap": s["gap"]}
+                       for c, s in zip(cfg.cs, last_stats)],
+    }
+    if rank == 0 and not args.no_cpu and world == 1:
+        res["cpu_baseline"] = cpu_baseline(cfg, b_host, A_host.numpy() if A_host is not None else dA.cpu().numpy())
+    P.close()
+    return res
+
+
+def cpu_baseline(cfg, b, A):
+    """The oracle (as it stands) on this host's cores, on the same workload (full path)."""
+    import oracle
+
+    cores = os.cpu_count()
+    lm = float(np.max(np.abs(oracle.aty(A, b))))
+    t0 = time.perf_counter()
+    x = None
+    for i, c in enumerate(cfg.cs):
+        l1, l2 = lambdas(cfg, lm, c)
+        x, _, st, _ = oracle.solve(A, b, l1, l2, sigma0=cfg.sigma0, tol=cfg.tol, x0=x if cfg.path and i > 0 else None)
+    dt = time.perf_counter() - t0
+    return {"value": dt, "unit": "s", "cores": int(os.environ.get("OMP_NUM_THREADS", cores)), "kind": "oracle",
+            "sample": f"full {cfg.name} workload ({len(cfg.cs)} solve(s)), OpenMP over columns"}
+
+
+def bench_reference(args, rank, world):
+    """Reference arm for this tier: the CPU oracle on the host cores (rank 0 only)."""
+    if rank != 0:
+        return None
+    import oracle
+
+    cfg = synth.CONFIGS[args.config]
+    A = synth.design(cfg)
+    b, _ = synth.response(cfg)
+    lm = float(np.max(np.abs(oracle.aty(A, b))))
+    steps = max(1, min(args.steps, 3))
+
+    def step():
+        x = None
+        for i, c in enumerate(cfg.cs):
+            l1, l2 = lambdas(cfg, lm, c)
+            x, _, _, _ = oracle.solve(A, b, l1, l2, sigma0=cfg.sigma0, tol=cfg.tol,
+                                      x0=x if cfg.path and i > 0 else None)
+
+    for _ in range(min(args.warmup, 1)):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        step()
+    t = (time.perf_counter() - t0) / steps
+    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count()))
+    return {"impl": "reference", "metric": METRIC, "value": t, "unit": "s", "n_gpus": world, "steps": steps,
+            "warmup": min(args.warmup, 1), "ms_per_step": t * 1e3, "higher_is_better": False, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (synth/, seeded)",
+            "config": {"workload": f"{cfg.name}: m={cfg.m} n={cfg.n}", "m": cfg.m, "n": cfg.n},
+            "cpu_baseline": {"value": t, "unit": "s", "cores": cores, "kind": "oracle",
+                             "sample": f"full {cfg.name} workload per step"},
+            "e2e": {"value": t, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def sweep(args):
+    """K1 bandwidth sweep: m = 500, n = 1e5 … 1e7, r ≈ 1e-4 n."""
+    import torch
+
+    from paper_2006_03970_b200 import Problem
+
+    peak, _ = _peaks()
+    base = synth.CONFIGS["cfg5"]
+    ns = [int(v) for v in args.sweep_n.split(",")]
+    stream = torch.cuda.current_stream()
+    nmax = max(ns)
+    dA = torch.empty((nmax, base.m), dtype=torch.float64, device="cuda")
+    synth.fill_device(base, dA.data_ptr(), stream.cuda_stream)
+    torch.cuda.synchronize()
+    for n in ns:
+        m = base.m
+        b = torch.from_numpy(synth.normals(5, 11, m)).cuda()
+        P = Problem.from_device(dA.data_ptr(), b.data_ptr(), m, n, stream.cuda_stream, keep=(dA, b))
+        y = torch.from_numpy(synth.normals(5, 12, m)).cuda()
+        x = torch.zeros(n, dtype=torch.float64, device="cuda")
+        w = torch.empty(n, dtype=torch.float64, device="cuda")
+        J = torch.empty(n, dtype=torch.int32, device="cuda")
+        PJ = torch.empty(n, dtype=torch.float64, device="cuda")
+        # λ1 at the (1 − 1e-4) quantile of |Aᵀy| (σ = 1, x = 0): r ≈ 1e-4 n
+        P.aty_fused(y.data_ptr(), x.data_ptr(), 1.0, 1e30, 0.1, w.data_ptr(), J.data_ptr(), PJ.data_ptr())
+        q = float(torch.quantile(w.abs()[: min(n, 16_000_000)].float(), 1 - 1e-4).item()) if n > 1 else 0.0
+        for lab, l1 in (("r~1e-4n", q), ("r~n/2", float(w.abs().median().item()))):
+            P.set_option("time_k1", 1)
+            ts = []
+            for it in range(args.sweep_reps + 3):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                r, _ = P.aty_fused(y.data_ptr(), x.data_ptr(), 1.0, l1, 0.1, w.data_ptr(), J.data_ptr(),
+                                   PJ.data_ptr())
+                e1.record(stream)
+                torch.cuda.synchronize()
+                if it >= 3:
+                    ts.append(e0.elapsed_time(e1) * 1e-3)
+            t = statistics.median(ts)
+            gbs = k1_bytes(m, n) / t / 1e9
+            print(json.dumps({"sweep": "k1", "m": m, "n": n, "case": lab, "r": r, "t_med_us": t * 1e6,
+                              "GBps": gbs, "frac_of_measured": gbs / peak, "pct_of_8TBps": gbs / 8000}), flush=True)
+        P.close()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg2", choices=list(synth.CONFIGS))
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--sweep", action="store_true", help="K1 bandwidth sweep instead of the TTS bench")
+    ap.add_argument("--sweep-n", default="100000,200000,500000,1000000,2000000,5000000,10000000")
+    ap.add_argument("--sweep-reps", type=int, default=20)
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours" and not args.sweep:
+        args.warmup = 3  # contract: W ≥ 3
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        res = bench_reference(args, rank, world)
+        if res is not None:
+            print(json.dumps(res), flush=True)
+        return
+
+    if args.sweep:
+        sweep(args)
+        return
+
+    import torch.distributed as dist
+
+    if world > 1:
+        import torch
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl")
+    res = bench_ours(args, rank, world, local_rank)
+    if rank == 0:
+        print(json.dumps(res), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
