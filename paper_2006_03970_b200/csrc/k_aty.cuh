@@ -6,9 +6,16 @@
 //                      ordered compaction of (J, P_J) into per-CTA segments, block
 //                      partial sums for ψ / res3 / the dual objective, and the per-CTA
 //                      m-vector Σ_{i∈J} P_i a_i used by ∇ψ (Eq. (15)).
-//                      A tiles stream HBM → smem through a multi-stage ring of 1D bulk
-//                      copies (cp.async.bulk, TMA) issued by one producer warp; 8 consumer
-//                      warps keep y in registers (lane ℓ owns rows ℓ + 32t).
+//                      Layout: one persistent CTA per SM owns a contiguous column range.
+//                      A (and x) tiles stream HBM → smem through a ring of 1D bulk copies
+//                      (cp.async.bulk = TMA, SASS UBLKCP) issued by one producer lane; each
+//                      of 7 consumer warps owns whole tiles (tile it → warp it mod 7), so
+//                      warps never wait on each other.  A warp computes 8 column dots at a
+//                      time with y in registers (lane ℓ owns rows ℓ + 32t), then a
+//                      transpose-reduce leaves column c's sum in lanes 4c..4c+3: the
+//                      epilogue runs lane-parallel, the active flags of 8 columns become one
+//                      byte of a bitmap.  Compaction happens once per CTA at the end from
+//                      that bitmap (P recomputed bit-identically from the stored w).
 // K1e k1e_epilogue   : the same epilogue from a stored w (or w0 + s(w1 − w0) for an
 //                      Armijo backtrack, by linearity of Aᵀ), no A traffic.
 // K1f k1_finalize    : concatenates the per-CTA segments in CTA order → ascending J.
@@ -18,8 +25,9 @@
 
 namespace ssn {
 
-constexpr int K1_NWC = 8;                    // consumer warps
+constexpr int K1_NWC = 7;                     // consumer warps (7 + producer = 256 threads → 255-register cap)
 constexpr int K1_THREADS = (K1_NWC + 1) * 32; // + 1 producer warp
+constexpr int K1_GRP = 8;                     // columns per transpose-reduce group
 
 struct K1Params {
   const double* A;
@@ -27,6 +35,7 @@ struct K1Params {
   const double* y;      // m, evaluation point
   const double* x;      // n, dense multiplier (fused mode)
   double* w_out;        // n
+  uint8_t* mask;        // n/8 (+pad): active bits, one byte per 8-column group
   int32_t* seg_idx;     // n-capacity segment storage (CTA b writes from c_lo(b))
   double* seg_P;        // n
   int* cta_cnt;         // G
@@ -41,6 +50,34 @@ struct K1Params {
   uint32_t xstage_elems;// doubles per x stage buffer (≥ C, multiple of 16)
 };
 
+// Reduce-scatter of 8 per-lane partial sums a[0..7] across the warp: afterwards every
+// lane holds the full sum of column (lane >> 2); lanes 4c..4c+3 are bitwise identical.
+SSN_DEV double reduce8(double (&a)[8], int lane) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const bool up = lane & 16;
+    const double send = up ? a[j] : a[j + 4];
+    const double keep = up ? a[j + 4] : a[j];
+    a[j] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const bool up = lane & 8;
+    const double send = up ? a[j] : a[j + 2];
+    const double keep = up ? a[j + 2] : a[j];
+    a[j] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+  {
+    const bool up = lane & 4;
+    const double send = up ? a[0] : a[1];
+    const double keep = up ? a[1] : a[0];
+    a[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+  }
+  a[0] += __shfl_xor_sync(0xffffffffu, a[0], 2);
+  a[0] += __shfl_xor_sync(0xffffffffu, a[0], 1);
+  return a[0];
+}
+
 template <int MR>
 __global__ void __launch_bounds__(K1_THREADS, 1) k1_aty_fused(const K1Params p) {
   extern __shared__ __align__(128) unsigned char smem[];
@@ -51,10 +88,8 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_aty_fused(const K1Params p) 
   double* xring = ring + (size_t)S * p.stage_elems;
   uint64_t* full = reinterpret_cast<uint64_t*>(xring + (size_t)S * p.xstage_elems);
   uint64_t* empty = full + S;
-  double* wtile = reinterpret_cast<double*>(empty + S);  // 2C
-  double* ptile = wtile + 2 * C;                         // 2C
-  int* ftile = reinterpret_cast<int*>(ptile + 2 * C);    // 2C
-  int* sh_cnt = ftile + 2 * C;
+  int* sh = reinterpret_cast<int*>(empty + S);  // small scratch (16 ints)
+  volatile int* slot_seq = sh + 16;              // S ints: tile last issued into each slot
 
   int64_t c_lo, c_hi;
   cta_cols(blockIdx.x, gridDim.x, p.T, C, p.n, &c_lo, &c_hi);
@@ -64,11 +99,15 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_aty_fused(const K1Params p) 
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
+      slot_seq[s] = -1;
     }
     fence_mbar_init();
   }
   __syncthreads();
 
+  // Slot s carries tiles s, s+S, s+2S, ... consumed by different warps.  A consumer must not
+  // try_wait on full[s] before its own tile was issued: the parity of a phase two steps ahead
+  // aliases the current one.  The producer publishes the issued tile number in slot_seq[s].
   if (warp == K1_NWC) {  // ---------------- producer warp ----------------
     if (lane == 0) {
       for (int64_t it = 0; it < ntiles; ++it) {
@@ -90,12 +129,13 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_aty_fused(const K1Params p) 
         mbar_arrive_expect_tx(&full[s], a16 + x16);
         bulk_g2s(dA, p.A + c0 * m, a16, &full[s]);
         if (x16) bulk_g2s(dX, p.x + c0, x16, &full[s]);
+        slot_seq[s] = (int)it;
       }
     }
     return;
   }
 
-  // ---------------- consumer warps ----------------
+  // ---------------- consumer warps: warp w owns tiles it ≡ w (mod K1_NWC) ----------------
   double yr[MR], gacc[MR];
 #pragma unroll
   for (int t = 0; t < MR; ++t) {
@@ -104,85 +144,112 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_aty_fused(const K1Params p) 
     gacc[t] = 0.0;
   }
   const Scal sc = p.sc;
-  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  const bool leader = (lane & 3) == 0;
+  const int gcol = lane >> 2;  // column of the 8-group this lane ends up holding
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;  // per leader lane, its columns in order
   bool any_active = false;
-  int cnt = 0;  // meaningful in warp 0
 
-  for (int64_t it = 0; it < ntiles; ++it) {
+  for (int64_t it = warp; it < ntiles; it += K1_NWC) {
     const int s = (int)(it % S);
+    if (lane == 0)
+      while (slot_seq[s] != (int)it) __nanosleep(32);
+    __syncwarp();
     mbar_wait(&full[s], (uint32_t)((it / S) & 1));
     const int64_t c0 = c_lo + it * C;
     const int nc = (int)((c_hi - c0) < C ? (c_hi - c0) : C);
     const double* Ts = ring + (size_t)s * p.stage_elems;
     const double* Xs = xring + (size_t)s * p.xstage_elems;
-    const int buf = (int)(it & 1);
-    for (int c = warp; c < nc; c += K1_NWC) {
-      const double* col = Ts + (size_t)c * m;
-      double a0 = 0.0, a1 = 0.0;
+    for (int g = 0; g * K1_GRP < nc; ++g) {
+      const double* base = Ts + (size_t)g * K1_GRP * m;
+      double a[K1_GRP];
+#pragma unroll
+      for (int c = 0; c < K1_GRP; ++c) a[c] = 0.0;
 #pragma unroll
       for (int t = 0; t < MR; ++t) {
         const int64_t row = lane + 32 * t;
-        const double v = row < m ? col[row] : 0.0;
-        if (t & 1) a1 = fma(yr[t], v, a1);
-        else a0 = fma(yr[t], v, a0);
-      }
-      const double w = warp_allsum(a0 + a1);
-      if (p.fused) {
-        const double xi = Xs[c];
-        const double tt = __dsub_rn(xi, __dmul_rn(sc.sigma, w));
-        const bool act = fabs(tt) > sc.thr;
-        const double P = prox_en(tt, sc.thr, sc.den);
-        const double dx = __dsub_rn(xi, P);
-        const double z = __dsub_rn(__ddiv_rn(dx, sc.sigma), w);
-        const double e = __dsub_rn(fabs(w), sc.l1);
-        s0 = __dadd_rn(s0, __dmul_rn(P, P));
-        s1 = __dadd_rn(s1, __dmul_rn(dx, dx));
-        s2 = __dadd_rn(s2, __dmul_rn(z, z));
-        if (e > 0.0) s3 = __dadd_rn(s3, __dmul_rn(e, e));
-        if (act) {
-          any_active = true;
+        if (row < m) {
+          const double yv = yr[t];
 #pragma unroll
-          for (int t = 0; t < MR; ++t) {
-            const int64_t row = lane + 32 * t;
-            if (row < m) gacc[t] = fma(P, col[row], gacc[t]);
-          }
+          for (int c = 0; c < K1_GRP; ++c) a[c] = fma(yv, base[(size_t)c * m + row], a[c]);
         }
-        if (lane == 0) {
-          wtile[buf * C + c] = w;
-          ptile[buf * C + c] = P;
-          ftile[buf * C + c] = act ? 1 : 0;
+      }
+      const double w = reduce8(a, lane);
+      const int c = g * K1_GRP + gcol;
+      const bool valid = c < nc;
+      if (p.fused) {
+        bool act = false;
+        double P = 0.0;
+        if (valid) {
+          const double xi = Xs[c];
+          const double tt = __dsub_rn(xi, __dmul_rn(sc.sigma, w));
+          act = fabs(tt) > sc.thr;
+          const double e = __dsub_rn(fabs(w), sc.l1);
+          if (xi == 0.0 && !act) {  // P = 0, x − P = 0, z = −w (exact shortcut of the line below)
+            if (leader) {
+              s2 = __dadd_rn(s2, __dmul_rn(w, w));
+              if (e > 0.0) s3 = __dadd_rn(s3, __dmul_rn(e, e));
+            }
+          } else {
+            P = prox_en(tt, sc.thr, sc.den);
+            const double dx = __dsub_rn(xi, P);
+            const double z = __dsub_rn(__ddiv_rn(dx, sc.sigma), w);
+            if (leader) {
+              s0 = __dadd_rn(s0, __dmul_rn(P, P));
+              s1 = __dadd_rn(s1, __dmul_rn(dx, dx));
+              s2 = __dadd_rn(s2, __dmul_rn(z, z));
+              if (e > 0.0) s3 = __dadd_rn(s3, __dmul_rn(e, e));
+            }
+          }
+          if (leader) p.w_out[c0 + c] = w;
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, act && leader);
+        unsigned m8 = 0;
+#pragma unroll
+        for (int q = 0; q < K1_GRP; ++q) m8 |= ((bal >> (4 * q)) & 1u) << q;
+        if (lane == 0) p.mask[(c0 >> 3) + g] = (uint8_t)m8;
+        if (m8) {
+          any_active = true;
+          unsigned mm = m8;
+          while (mm) {
+            const int q = __ffs(mm) - 1;
+            mm &= mm - 1;
+            const double Pq = __shfl_sync(0xffffffffu, P, 4 * q);
+            const double* colq = base + (size_t)q * m;
+#pragma unroll
+            for (int t = 0; t < MR; ++t) {
+              const int64_t row = lane + 32 * t;
+              if (row < m) gacc[t] = fma(Pq, colq[row], gacc[t]);
+            }
+          }
         }
       } else {
-        s0 = fmax(s0, fabs(w));
-        if (lane == 0) wtile[buf * C + c] = w;
-      }
-    }
-    named_bar_sync(1, K1_NWC * 32);
-    if (warp == 0) {
-      for (int base = 0; base < nc; base += 32) {
-        const int c = base + lane;
-        if (c < nc) p.w_out[c0 + c] = wtile[buf * C + c];
-        if (p.fused) {
-          const int f = (c < nc) ? ftile[buf * C + c] : 0;
-          const unsigned bal = __ballot_sync(0xffffffffu, f);
-          if (f) {
-            const int pos = cnt + __popc(bal & lanemask_lt());
-            p.seg_idx[c_lo + pos] = (int32_t)(c0 + c);
-            p.seg_P[c_lo + pos] = ptile[buf * C + c];
-          }
-          cnt += __popc(bal);
+        if (valid) {
+          s0 = fmax(s0, fabs(w));
+          if (leader) p.w_out[c0 + c] = w;
         }
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
     }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
   }
 
-  // ---------------- CTA reduction (fixed warp order) ----------------
-  named_bar_sync(1, K1_NWC * 32);  // ring is idle now: reuse it
-  double* rv = ring;                         // K1_NWC x m
-  double* rs = ring + (size_t)K1_NWC * m;    // K1_NWC x 4
+  // ---------------- CTA epilogue: fixed-order reductions, then ordered compaction ----------------
+  named_bar_sync(1, K1_NWC * 32);  // ring idle; this CTA's w / mask writes are visible CTA-wide
+  double* rv = ring;                       // K1_NWC x m
+  double* rs = ring + (size_t)K1_NWC * m;  // K1_NWC x 4
   int* ract = reinterpret_cast<int*>(rs + K1_NWC * 4);
+  // warp partial scalars: leader lanes 0,4,...,28 in lane order (plain mode: max over lanes)
+  double q4[4] = {s0, s1, s2, s3};
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    double acc = 0.0;
+    for (int l = 0; l < 32; l += 4) {
+      const double v = __shfl_sync(0xffffffffu, q4[j], l);
+      acc = p.fused ? __dadd_rn(acc, v) : fmax(acc, v);
+    }
+    if (!p.fused) acc = warp_allmax(q4[j]);
+    q4[j] = acc;
+  }
   if (p.fused && p.part_vec) {
 #pragma unroll
     for (int t = 0; t < MR; ++t) {
@@ -190,14 +257,11 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_aty_fused(const K1Params p) 
       if (row < m) rv[(size_t)warp * m + row] = gacc[t];
     }
   }
+  const bool wact = __any_sync(0xffffffffu, any_active);
   if (lane == 0) {
-    rs[warp * 4 + 0] = s0;
-    rs[warp * 4 + 1] = s1;
-    rs[warp * 4 + 2] = s2;
-    rs[warp * 4 + 3] = s3;
-    ract[warp] = any_active ? 1 : 0;
+    for (int j = 0; j < 4; ++j) rs[warp * 4 + j] = q4[j];
+    ract[warp] = wact ? 1 : 0;
   }
-  if (threadIdx.x == 0) *sh_cnt = cnt;
   named_bar_sync(1, K1_NWC * 32);
   const int tid = threadIdx.x;
   const int b = blockIdx.x;
@@ -206,15 +270,61 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_aty_fused(const K1Params p) 
     for (int wi = 1; wi < K1_NWC; ++wi)
       for (int j = 0; j < 4; ++j) q[j] = p.fused ? __dadd_rn(q[j], rs[wi * 4 + j]) : fmax(q[j], rs[wi * 4 + j]);
     for (int j = 0; j < 4; ++j) p.part_scal[b * 4 + j] = q[j];
-    p.cta_cnt[b] = p.fused ? *sh_cnt : 0;
   }
-  if (p.fused && p.part_vec && *sh_cnt > 0) {
+  if (!p.fused) {
+    if (tid == 0) p.cta_cnt[b] = 0;
+    return;
+  }
+  int anyv = 0;
+  for (int wi = 0; wi < K1_NWC; ++wi) anyv |= ract[wi];
+  if (p.part_vec && anyv) {
     for (int64_t k = tid; k < m; k += K1_NWC * 32) {
       double v = 0.0;
       for (int wi = 0; wi < K1_NWC; ++wi)
         if (ract[wi]) v += rv[(size_t)wi * m + k];
       p.part_vec[(size_t)b * m + k] = v;
     }
+  }
+  if (!anyv) {
+    if (tid == 0) p.cta_cnt[b] = 0;
+    return;
+  }
+  // ordered compaction: warp wi scans bytes [bw0, bw1) of this CTA's mask range
+  const int64_t byte_lo = c_lo >> 3, nbytes = (c_hi - c_lo + 7) >> 3;
+  const int64_t bw0 = byte_lo + nbytes * warp / K1_NWC, bw1 = byte_lo + nbytes * (warp + 1) / K1_NWC;
+  int cnt = 0;
+  for (int64_t q = bw0 + lane; q < bw1; q += 32) cnt += __popc((unsigned)p.mask[q]);
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  if (lane == 0) sh[warp] = cnt;
+  named_bar_sync(1, K1_NWC * 32);
+  int off = 0, tot = 0;
+  for (int wi = 0; wi < K1_NWC; ++wi) {
+    off += (wi < warp) ? sh[wi] : 0;
+    tot += sh[wi];
+  }
+  if (tid == 0) p.cta_cnt[b] = tot;
+  for (int64_t q0 = bw0; q0 < bw1; q0 += 32) {
+    const int64_t q = q0 + lane;
+    const unsigned byte = (q < bw1) ? (unsigned)p.mask[q] : 0u;
+    const int pc = __popc(byte);
+    int incl = pc;  // inclusive warp scan
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    int pos = off + incl - pc;
+    unsigned bb = byte;
+    while (bb) {
+      const int bit = __ffs(bb) - 1;
+      bb &= bb - 1;
+      const int64_t i = (q << 3) + bit;
+      const double w = p.w_out[i];
+      const double tt = __dsub_rn(p.x[i], __dmul_rn(sc.sigma, w));
+      p.seg_idx[c_lo + pos] = (int32_t)i;
+      p.seg_P[c_lo + pos] = prox_en(tt, sc.thr, sc.den);
+      ++pos;
+    }
+    off += __shfl_sync(0xffffffffu, incl, 31);
   }
 }
 
@@ -355,8 +465,11 @@ struct EvalOut {
   long long pad;
 };
 
-constexpr int K5_THREADS = 1024;
+constexpr int K5_THREADS = 256;  // 8 warps; CTA c owns rows [32c, 32c + 32)
 
+// Multi-CTA, deterministic: warp w of CTA c sums partial rows b ∈ [w·np/8, (w+1)·np/8)
+// in ascending b for its 32 rows; the 8 warp sums are added in warp order; the last CTA
+// (ticket counter) adds the per-CTA scalar partials in CTA order and writes EvalOut.
 __global__ void __launch_bounds__(K5_THREADS) k_eval_reduce(int64_t m, const double* __restrict__ y,
                                                             const double* __restrict__ bvec,
                                                             const double* __restrict__ part_vec,
@@ -364,67 +477,82 @@ __global__ void __launch_bounds__(K5_THREADS) k_eval_reduce(int64_t m, const dou
                                                             const double* __restrict__ part_scal, int nscal,
                                                             Scal sc, double nb, int with_grad,
                                                             double* __restrict__ g_out, const int64_t* r_in,
-                                                            EvalOut* out) {
-  __shared__ double red[3][K5_THREADS / 32];
+                                                            EvalOut* out, double* blk, unsigned* ticket) {
+  __shared__ double red[8][33];
+  __shared__ bool last;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  double yy = 0.0, by = 0.0, gg = 0.0;
-  for (int64_t k = tid; k < m; k += K5_THREADS) {
-    const double yk = y[k], bk = bvec[k];
-    yy += yk * yk;
-    by += bk * yk;
-    if (with_grad) {
-      double gp = 0.0;
-      int b = 0;
-      for (; b + 4 <= nparts; b += 4) {  // independent loads, ordered adds
-        const double v0 = (!part_valid || part_valid[b + 0]) ? part_vec[(size_t)(b + 0) * m + k] : 0.0;
-        const double v1 = (!part_valid || part_valid[b + 1]) ? part_vec[(size_t)(b + 1) * m + k] : 0.0;
-        const double v2 = (!part_valid || part_valid[b + 2]) ? part_vec[(size_t)(b + 2) * m + k] : 0.0;
-        const double v3 = (!part_valid || part_valid[b + 3]) ? part_vec[(size_t)(b + 3) * m + k] : 0.0;
-        gp += v0;
-        gp += v1;
-        gp += v2;
-        gp += v3;
+  const int64_t k = (int64_t)blockIdx.x * 32 + lane;
+  if (with_grad) {
+    const int b0 = (int)((int64_t)nparts * warp / 8), b1 = (int)((int64_t)nparts * (warp + 1) / 8);
+    double gp = 0.0;
+    if (k < m) {
+      int b = b0;
+      for (; b + 4 <= b1; b += 4) {
+        double v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          v[u] = (!part_valid || part_valid[b + u]) ? part_vec[(size_t)(b + u) * m + k] : 0.0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) gp += v[u];
       }
-      for (; b < nparts; ++b)
+      for (; b < b1; ++b)
         if (!part_valid || part_valid[b]) gp += part_vec[(size_t)b * m + k];
-      const double g = __dsub_rn(__dadd_rn(yk, bk), gp);
-      g_out[k] = g;
-      gg += g * g;
     }
-  }
-  yy = warp_allsum(yy);
-  by = warp_allsum(by);
-  gg = warp_allsum(gg);
-  if (lane == 0) {
-    red[0][warp] = yy;
-    red[1][warp] = by;
-    red[2][warp] = gg;
+    red[warp][lane] = gp;
   }
   __syncthreads();
-  if (tid == 0) {
-    double a = 0, bb = 0, c = 0;
-    for (int wi = 0; wi < K5_THREADS / 32; ++wi) {
-      a += red[0][wi];
-      bb += red[1][wi];
-      c += red[2][wi];
+  if (warp == 0) {
+    double yy = 0.0, by = 0.0, gg = 0.0;
+    if (k < m) {
+      const double yk = y[k], bk = bvec[k];
+      yy = yk * yk;
+      by = bk * yk;
+      if (with_grad) {
+        double gp = red[0][lane];
+        for (int wi = 1; wi < 8; ++wi) gp += red[wi][lane];
+        const double g = __dsub_rn(__dadd_rn(yk, bk), gp);
+        g_out[k] = g;
+        gg = g * g;
+      }
     }
-    double s[4] = {0, 0, 0, 0};
-    for (int q = 0; q < nscal; ++q)
-      for (int j = 0; j < 4; ++j) s[j] += part_scal[q * 4 + j];
-    EvalOut o;
-    o.yy = a;
-    o.by = bb;
-    o.gg = c;
-    for (int j = 0; j < 4; ++j) o.s[j] = s[j];
-    const double tprox = sc.cpsi * s[0];
-    o.psi = 0.5 * a + bb + tprox;
-    o.psimag = fabs(0.5 * a) + fabs(bb) + fabs(tprox);
-    o.res1 = with_grad ? sqrt(c) / (1.0 + nb) : -1.0;
-    o.gd = 0.0;
-    o.r = r_in ? (long long)*r_in : -1;
-    o.pad = 0;
-    *out = o;
+    yy = warp_allsum(yy);
+    by = warp_allsum(by);
+    gg = warp_allsum(gg);
+    if (lane == 0) {
+      blk[blockIdx.x * 3 + 0] = yy;
+      blk[blockIdx.x * 3 + 1] = by;
+      blk[blockIdx.x * 3 + 2] = gg;
+      __threadfence();
+      const unsigned t = atomicAdd(ticket, 1u);
+      last = (t == gridDim.x - 1);
+    }
   }
+  __syncthreads();
+  if (!last || tid != 0) return;
+  __threadfence();
+  double a = 0, bb = 0, c = 0;
+  for (unsigned q = 0; q < gridDim.x; ++q) {
+    a += __ldcg(blk + q * 3 + 0);
+    bb += __ldcg(blk + q * 3 + 1);
+    c += __ldcg(blk + q * 3 + 2);
+  }
+  double s[4] = {0, 0, 0, 0};
+  for (int q = 0; q < nscal; ++q)
+    for (int j = 0; j < 4; ++j) s[j] += part_scal[q * 4 + j];
+  EvalOut o;
+  o.yy = a;
+  o.by = bb;
+  o.gg = c;
+  for (int j = 0; j < 4; ++j) o.s[j] = s[j];
+  const double tprox = __dmul_rn(sc.cpsi, s[0]);
+  o.psi = __dadd_rn(__dadd_rn(__dmul_rn(0.5, a), bb), tprox);
+  o.psimag = fabs(0.5 * a) + fabs(bb) + fabs(tprox);
+  o.res1 = with_grad ? sqrt(c) / (1.0 + nb) : -1.0;
+  o.gd = 0.0;
+  o.r = r_in ? (long long)*r_in : -1;
+  o.pad = 0;
+  *out = o;
+  *ticket = 0u;  // ready for the next launch (stream-ordered)
 }
 
 // max over G plain-mode partials (λmax = ‖Aᵀb‖∞)

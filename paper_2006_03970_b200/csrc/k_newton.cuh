@@ -191,109 +191,109 @@ __global__ void k_gram_mm_reduce(const double* __restrict__ W, int ns, int64_t m
 
 // ---------------------------------------------------------------------------
 // K4: Cholesky by one cluster.  M is N × N column-major (ld), lower used/overwritten.
+// Right-looking, 32 × 32 tiles kept in L2 (__ldcg), per panel k:
+//   B: L_ik = A_ik L_kk^{-T} for i > k           (warp per tile, all CTAs)   | cluster barrier
+//   C: A_ij −= L_ik L_jkᵀ for k < j ≤ i           (warp per tile, all CTAs)   | cluster barrier
+//      look-ahead: the warp that updates tile (k+1, k+1) factors it right away,
+//      so panel k+1 needs no separate diagonal phase.
 // ---------------------------------------------------------------------------
 constexpr int CHT = 32;  // tile edge
+
+// Factor the 32×32 tile (k0, kn) of M in registers (lane = row), write L back.
+SSN_DEV void chol_diag_warp(double* M, int ld, int k0, int kn, int lane, int* info) {
+  double a[CHT];
+#pragma unroll
+  for (int c = 0; c < CHT; ++c)
+    a[c] = (lane < kn && c < kn) ? __ldcg(M + (int64_t)(k0 + lane) + (int64_t)(k0 + c) * ld)
+                                 : (lane == c ? 1.0 : 0.0);
+#pragma unroll
+  for (int j = 0; j < CHT; ++j) {
+    double ajj = __shfl_sync(0xffffffffu, a[j], j);
+    if (!(ajj > 0.0)) {
+      if (lane == 0) atomicExch(info, 1);
+      ajj = 1.0;
+    }
+    const double d = sqrt(ajj);
+    const double inv = 1.0 / d;
+    const double lij = (lane > j) ? a[j] * inv : (lane == j ? d : 0.0);
+    a[j] = lij;
+#pragma unroll
+    for (int c = j + 1; c < CHT; ++c) {
+      const double lcj = __shfl_sync(0xffffffffu, lij, c);
+      if (lane >= c) a[c] = fma(-lij, lcj, a[c]);
+    }
+  }
+  if (lane < kn) {
+#pragma unroll
+    for (int c = 0; c < CHT; ++c)
+      if (c <= lane && c < kn) M[(int64_t)(k0 + lane) + (int64_t)(k0 + c) * ld] = a[c];
+  }
+}
 
 __global__ void __launch_bounds__(256, 1) k_chol_cluster(double* M, int N, int ld, int* info) {
   namespace cg = cooperative_groups;
   cg::cluster_group cl = cg::this_cluster();
   const int rank = (int)cl.block_rank(), CS = (int)cl.num_blocks();
   extern __shared__ double dsm[];
-  double(*D)[33] = reinterpret_cast<double(*)[33]>(dsm);        // 32 x 33: diag tile
-  double* invd = dsm + 32 * 33;                                  // 32
-  double* wsm = invd + 32;                                       // 8 warps x 32 x 32
+  double(*D)[33] = reinterpret_cast<double(*)[33]>(dsm);  // L_kk
+  double* invd = dsm + 32 * 33;                            // 1 / L_kk[c][c]
+  double* wsm = invd + 32;                                 // 8 warps x 32 x 32
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nt = (N + CHT - 1) / CHT;
+  const int gw = rank + CS * warp;  // global warp id in the cluster
+  const int NWg = CS * 8;
 
-  for (int k = 0; k < nt; ++k) {
-    const int k0 = k * CHT, kn = min(CHT, N - k0);
-    // ---- Phase A: factor the diagonal tile (owner k % CS) ----
-    if (rank == k % CS) {
+  if (gw == 0) chol_diag_warp(M, ld, 0, min(CHT, N), lane, info);
+  cl.sync();
+  for (int k = 0; k + 1 < nt; ++k) {
+    const int k0 = k * CHT;  // kn = 32 for every panel but the last
+    // ---- B: L_ik = A_ik L_kk^{-T}, i > k ----
+    const int ntiles = nt - k - 1;
+    if (rank < ntiles) {  // CTAs with at least one tile load L_kk
       for (int e = tid; e < CHT * CHT; e += blockDim.x) {
         const int i = e & 31, j = e >> 5;
-        D[i][j] = (i < kn && j < kn) ? __ldcg(M + (int64_t)(k0 + i) + (int64_t)(k0 + j) * ld) : (i == j ? 1.0 : 0.0);
+        D[i][j] = (i >= j) ? __ldcg(M + (int64_t)(k0 + i) + (int64_t)(k0 + j) * ld) : 0.0;
       }
       __syncthreads();
-      if (warp == 0) {
-        for (int j = 0; j < CHT; ++j) {
-          if (lane == j) {
-            double v = D[j][j];
-            if (!(v > 0.0)) {
-              atomicExch(info, 1);
-              v = 1.0;
-            }
-            D[j][j] = sqrt(v);
-          }
-          __syncwarp();
-          if (lane > j) D[lane][j] = D[lane][j] / D[j][j];
-          __syncwarp();
-          if (lane > j) {
-            const double lij = D[lane][j];
-            for (int c = j + 1; c <= lane; ++c) D[lane][c] = fma(-lij, D[c][j], D[lane][c]);
-          }
-          __syncwarp();
-        }
-      }
+      if (tid < CHT) invd[tid] = 1.0 / D[tid][tid];
       __syncthreads();
-      for (int e = tid; e < CHT * CHT; e += blockDim.x) {
-        const int i = e & 31, j = e >> 5;
-        if (i < kn && j < kn && i >= j) M[(int64_t)(k0 + i) + (int64_t)(k0 + j) * ld] = D[i][j];
-      }
-    }
-    cl.sync();
-    if (k == nt - 1) break;
-    // ---- Phase B: L_ik = A_ik L_kk^{-T} for i > k (warp per tile) ----
-    {
-      const int ntiles = nt - k - 1;
-      bool mine = false;
-      for (int q = rank; q < ntiles; q += CS) mine = true;
-      if (mine) {
-        for (int e = tid; e < CHT * CHT; e += blockDim.x) {
-          const int i = e & 31, j = e >> 5;
-          D[i][j] = (i < kn && j < kn && i >= j) ? __ldcg(M + (int64_t)(k0 + i) + (int64_t)(k0 + j) * ld)
-                                                 : (i == j ? 1.0 : 0.0);
+      for (int q = gw; q < ntiles; q += NWg) {
+        const int row = (k + 1 + q) * CHT + lane;
+        double x[CHT];
+#pragma unroll
+        for (int c = 0; c < CHT; ++c) x[c] = (row < N) ? __ldcg(M + (int64_t)row + (int64_t)(k0 + c) * ld) : 0.0;
+#pragma unroll
+        for (int c = 0; c < CHT; ++c) {
+          double s0 = x[c], s1 = 0.0;
+#pragma unroll
+          for (int p = 0; p < c; ++p) {
+            if (p & 1) s1 = fma(-x[p], D[c][p], s1);
+            else s0 = fma(-x[p], D[c][p], s0);
+          }
+          x[c] = (s0 + s1) * invd[c];
         }
-        __syncthreads();
-        if (tid < CHT) invd[tid] = 1.0 / D[tid][tid];
-        __syncthreads();
-        for (int q = rank + CS * warp; q < ntiles; q += CS * 8) {
-          const int i0 = (k + 1 + q) * CHT;
-          const int row = i0 + lane;
-          double x[CHT];
+        if (row < N) {
 #pragma unroll
-          for (int c = 0; c < CHT; ++c)
-            x[c] = (row < N && c < kn) ? __ldcg(M + (int64_t)row + (int64_t)(k0 + c) * ld) : 0.0;
-#pragma unroll
-          for (int c = 0; c < CHT; ++c) {
-            double s = x[c];
-#pragma unroll
-            for (int p = 0; p < c; ++p) s = fma(-x[p], D[c][p], s);
-            x[c] = s * invd[c];
-          }
-          if (row < N) {
-#pragma unroll
-            for (int c = 0; c < CHT; ++c)
-              if (c < kn) M[(int64_t)row + (int64_t)(k0 + c) * ld] = x[c];
-          }
+          for (int c = 0; c < CHT; ++c) M[(int64_t)row + (int64_t)(k0 + c) * ld] = x[c];
         }
       }
     }
     cl.sync();
-    // ---- Phase C: C_ij −= L_ik L_jkᵀ for k < j ≤ i (warp per tile) ----
+    // ---- C: A_ij −= L_ik L_jkᵀ, k < j ≤ i; tile (k+1,k+1) first, then factored ----
     {
       const int rem = nt - k - 1;
       const int npairs = rem * (rem + 1) / 2;
       double* S = wsm + (size_t)warp * CHT * CHT;  // S[p*32 + l] = L_jk[l][p]
-      for (int q = rank + CS * warp; q < npairs; q += CS * 8) {
+      for (int q = gw; q < npairs; q += NWg) {
         int ii, jj;
-        tri_tile(q, &ii, &jj);
+        tri_tile(q, &ii, &jj);  // q = 0 → (0,0) = tile (k+1, k+1)
         const int i0 = (k + 1 + ii) * CHT, j0 = (k + 1 + jj) * CHT;
         const int row = i0 + lane;
         double a[CHT];
 #pragma unroll
         for (int p = 0; p < CHT; ++p) {
-          a[p] = (row < N && p < kn) ? __ldcg(M + (int64_t)row + (int64_t)(k0 + p) * ld) : 0.0;
-          S[p * CHT + lane] = (j0 + lane < N && p < kn) ? __ldcg(M + (int64_t)(j0 + lane) + (int64_t)(k0 + p) * ld) : 0.0;
+          a[p] = (row < N) ? __ldcg(M + (int64_t)row + (int64_t)(k0 + p) * ld) : 0.0;
+          S[p * CHT + lane] = (j0 + lane < N) ? __ldcg(M + (int64_t)(j0 + lane) + (int64_t)(k0 + p) * ld) : 0.0;
         }
         __syncwarp();
         double c[CHT];
@@ -317,6 +317,10 @@ __global__ void __launch_bounds__(256, 1) k_chol_cluster(double* M, int N, int l
             if (j0 + l < N && (i0 != j0 || l <= lane)) M[(int64_t)row + (int64_t)(j0 + l) * ld] = c[l];
         }
         __syncwarp();
+        if (q == 0) {  // look-ahead: factor the next diagonal tile now
+          __threadfence_block();
+          chol_diag_warp(M, ld, (k + 1) * CHT, min(CHT, N - (k + 1) * CHT), lane, info);
+        }
       }
     }
     cl.sync();

@@ -75,6 +75,7 @@ int mr_bucket(int64_t m) {
   if (m <= 128) return 4;
   if (m <= 256) return 8;
   if (m <= 512) return 16;
+  if (m <= 800) return 25;
   return 32;
 }
 
@@ -88,6 +89,7 @@ k1_fn k1_for(int mr) {
     case 4: return k1_aty_fused<4>;
     case 8: return k1_aty_fused<8>;
     case 16: return k1_aty_fused<16>;
+    case 25: return k1_aty_fused<25>;
     default: return k1_aty_fused<32>;
   }
 }
@@ -98,6 +100,7 @@ gax_fn gax_for(int mr) {
     case 4: return k_gather_axpy<4>;
     case 8: return k_gather_axpy<8>;
     case 16: return k_gather_axpy<16>;
+    case 25: return k_gather_axpy<25>;
     default: return k_gather_axpy<32>;
   }
 }
@@ -188,6 +191,7 @@ struct ssnal_en_problem {
   double* x = nullptr;
   int32_t* seg_idx = nullptr;
   double* seg_P = nullptr;
+  uint8_t* mask = nullptr;
   int* cta_cnt = nullptr;
   double* part_scal = nullptr;
   double* part_vec = nullptr;
@@ -210,6 +214,8 @@ struct ssnal_en_problem {
   double* scratch = nullptr;   // small device scratch (objective, λmax)
   double* scratch_host = nullptr;
   int* flags = nullptr;
+  double* blk = nullptr;       // eval-reduce per-CTA partials
+  unsigned* ticket = nullptr;  // eval-reduce last-block counter
   // state
   double lambda_max = 0, nb = 0;
   // options
@@ -244,10 +250,10 @@ int configure(ssnal_en_problem* P) {
   const int64_t m = P->m, n = P->n;
   P->MR = mr_bucket(m);
   const int64_t bytes_col = 8 * m;
-  int k = (int)(32768 / (K1_NWC * bytes_col));
+  int k = (int)(32768 / (K1_GRP * bytes_col));  // ~32 KB of A per tile
   if (k < 1) k = 1;
-  if (k > 32) k = 32;  // ≤ 256 columns per tile (per-tile epilogue buffers)
-  P->C = K1_NWC * k;
+  if (k > 32) k = 32;  // ≤ 256 columns per tile
+  P->C = K1_GRP * k;   // multiple of 8: one mask byte per 8 columns, 16-B aligned tiles
   P->stage_elems = (uint32_t)(((int64_t)P->C * m + 15) / 16 * 16);
   P->xstage_elems = (uint32_t)((P->C + 15) / 16 * 16);
   const size_t per_stage = (size_t)(P->stage_elems + P->xstage_elems) * 8;
@@ -256,7 +262,7 @@ int configure(ssnal_en_problem* P) {
   if (S < 2) S = 2;
   while ((size_t)S * P->stage_elems < (size_t)K1_NWC * m + K1_NWC * 4 + K1_NWC) ++S;
   P->S = S;
-  P->k1_smem = (size_t)S * per_stage + 2 * S * 8 + 2 * P->C * 8 + 2 * P->C * 8 + 2 * P->C * 4 + 16;
+  P->k1_smem = (size_t)S * per_stage + 2 * S * 8 + 64 + 4 * S + 16;
   P->T = (n + P->C - 1) / P->C;
   P->G = (int)(P->T < P->nsm ? P->T : P->nsm);
   P->gax_grid = P->nsm;
@@ -300,6 +306,7 @@ int allocate(ssnal_en_problem* P) {
   for (int i = 0; i < 3; ++i) AL(P->w[i], n * 8);
   AL(P->x, n * 8);
   AL(P->seg_idx, n * 4);
+  AL(P->mask, n / 8 + 64);
   AL(P->seg_P, n * 8);
   AL(P->cta_cnt, (size_t)P->nsm * 4 + 64);
   AL(P->part_scal, (size_t)P->nsm * 4 * 8 + 64);
@@ -323,6 +330,9 @@ int allocate(ssnal_en_problem* P) {
   AL(P->ev_dev, sizeof(EvalOut) * 4);
   AL(P->scratch, 64 * 8);
   AL(P->flags, 64);
+  AL(P->blk, (size_t)((m + 31) / 32) * 3 * 8 + 64);
+  AL(P->ticket, 64);
+  CK(cudaMemset(P->ticket, 0, 64));
   CK(cudaMallocHost((void**)&P->ev_host, sizeof(EvalOut) * 4));
   CK(cudaMallocHost((void**)&P->scratch_host, 64 * 8));
   return SSNAL_OK;
@@ -364,6 +374,7 @@ int launch_k1(ssnal_en_problem* P, const double* y, const double* x, const Scal&
   k.w_out = w_out;
   k.seg_idx = P->seg_idx;
   k.seg_P = P->seg_P;
+  k.mask = P->mask;
   k.cta_cnt = P->cta_cnt;
   k.part_scal = P->part_scal;
   k.part_vec = fused ? P->part_vec : nullptr;
@@ -433,8 +444,10 @@ int launch_gather(ssnal_en_problem* P, const int32_t* J, const double* coef, int
 
 int launch_eval(ssnal_en_problem* P, const double* y, const Scal& sc, int with_grad, const int* valid, int nparts,
                 double* g_out, const int64_t* r_dev, int slot) {
-  k_eval_reduce<<<1, K5_THREADS, 0, P->st>>>(P->m, y, P->b, P->part_vec, valid, nparts, P->part_scal, P->G, sc,
-                                              P->nb, with_grad, g_out, r_dev, P->ev_dev + slot);
+  const unsigned nblk = (unsigned)((P->m + 31) / 32);
+  k_eval_reduce<<<nblk, K5_THREADS, 0, P->st>>>(P->m, y, P->b, P->part_vec, valid, nparts, P->part_scal, P->G, sc,
+                                                 P->nb, with_grad, g_out, r_dev, P->ev_dev + slot, P->blk,
+                                                 P->ticket);
   P->launches++;
   CKL();
   return SSNAL_OK;
@@ -795,6 +808,7 @@ static void destroy_bufs(ssnal_en_problem* P) {
   cudaFree(P->x);
   cudaFree(P->seg_idx);
   cudaFree(P->seg_P);
+  cudaFree(P->mask);
   cudaFree(P->cta_cnt);
   cudaFree(P->part_scal);
   cudaFree(P->part_vec);
@@ -816,6 +830,8 @@ static void destroy_bufs(ssnal_en_problem* P) {
   cudaFree(P->ev_dev);
   cudaFree(P->scratch);
   cudaFree(P->flags);
+  cudaFree(P->blk);
+  cudaFree(P->ticket);
   if (P->ev_host) cudaFreeHost(P->ev_host);
   if (P->scratch_host) cudaFreeHost(P->scratch_host);
   for (auto e : P->ev_pool) cudaEventDestroy(e);

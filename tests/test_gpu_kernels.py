@@ -32,6 +32,10 @@ K1_CASES = [
     (synth.IID_STD, 1024, 300, 7, 30),
     (synth.IID_STD, 33, 4099, 8, 0),
     (synth.IID_STD, 129, 1500, 9, 1500),
+    # many tiles per CTA (ring slots reused by different warps): n ≫ 148 · C · stages
+    (synth.IID_STD, 500, 200_003, 10, 300),
+    (synth.IID_STD, 64, 300_001, 12, 3000),
+    (synth.GENO_STD, 800, 60_001, 13, 500),
 ]
 
 
