@@ -6,12 +6,11 @@
 // K2  k_gather_axpy    : per-CTA partials of Σ_a coef_a A[:, J_a]          (A_J v, A_J P_J)
 //     k_combine        : out = bs·base + Σ parts (fixed order), optional dot
 //     k_jt_gemv        : u = A_Jᵀ g                                          (SMW rhs)
-// K3  k_gram_smw       : κ⁻¹ I_r + A_JᵀA_J  (lower, r × r)                   Eq. (19)
-//     k_gram_mm        : split-K partials of A_J A_Jᵀ (lower tiles, m × m)    Eq. (18)
-//     k_gram_mm_reduce : I_m + κ Σ_splits
-// K4  k_chol_cluster   : blocked right-looking Cholesky by one thread-block cluster,
-//                        tiles in L2, cluster barriers between panel phases
-//     k_chol_solve     : L Lᵀ v = rhs (single CTA), optional scale and gᵀd
+// K3  k_gram<true>     : split-K partials of A_JᵀA_J (lower, r × r)            Eq. (19)
+//     k_gram<false>    : split-K partials of A_J A_Jᵀ (lower, m × m)            Eq. (18)
+//     k_gram_reduce    : κ⁻¹ I_r + Σ  /  I_m + κ Σ
+// K4  k_chol_cluster   : Cholesky by one thread-block cluster with the forward solve carried
+//                        as an extra matrix row and a block backward solve (one launch)
 #pragma once
 #include <cooperative_groups.h>
 #include "common.cuh"
@@ -83,7 +82,8 @@ __global__ void __launch_bounds__(1024) k_combine(int64_t m, const double* __res
 // u[a] = Σ_k A[k, J[a]] g[k]   (one warp per column)
 __global__ void __launch_bounds__(256) k_jt_gemv(const double* __restrict__ A, int64_t m,
                                                  const int32_t* __restrict__ J, int64_t r,
-                                                 const double* __restrict__ g, double* __restrict__ u) {
+                                                 const double* __restrict__ g, double* __restrict__ u,
+                                                 int64_t ustride) {
   const int lane = threadIdx.x & 31;
   const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -92,8 +92,14 @@ __global__ void __launch_bounds__(256) k_jt_gemv(const double* __restrict__ A, i
     double s = 0.0;
     for (int64_t k = lane; k < m; k += 32) s = fma(__ldg(col + k), g[k], s);
     s = warp_allsum(s);
-    if (lane == 0) u[a] = s;
+    if (lane == 0) u[a * ustride] = s;
   }
+}
+
+// dst[i * stride] = src[i]
+__global__ void k_copy_strided(int64_t n, const double* __restrict__ src, double* __restrict__ dst, int64_t stride) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[i * stride] = src[i];
 }
 
 // ---------------------------------------------------------------------------
@@ -107,24 +113,67 @@ SSN_DEV void tri_tile(int q, int* ti, int* tj) {  // q → (ti ≥ tj), row-majo
   *tj = q - i * (i + 1) / 2;
 }
 
-// M[a + b*r] = Σ_k A[k,J_a] A[k,J_b] (+ kinv if a == b), a ≥ b
-__global__ void __launch_bounds__(256) k_gram_smw(const double* __restrict__ A, int64_t m,
-                                                  const int32_t* __restrict__ J, int r, double kinv,
-                                                  double* __restrict__ M) {
+// Split-K Gram tiles.  A 32 × 32 operand block element (row ρ, col γ) is A[rowbase+ρ, J[colbase+γ]]:
+//   SMW   (Eq. (19)): out(a, b) = Σ_k A[k,J_a] A[k,J_b]   — blocks over rows k, columns a / b tiles
+//   m × m (Eq. (18)): out(k, l) = Σ_a A[k,J_a] A[l,J_a]   — blocks over row tiles k / l, columns a
+// Each CTA owns one lower tile and one contiguous slice of the reduction index, double-buffers
+// the next 32-slice in registers while computing the current one from smem, and writes its
+// partial tile to W[split]; a reduce kernel sums the splits in order.
+template <bool SMW>
+__global__ void __launch_bounds__(256) k_gram(const double* __restrict__ A, int64_t m,
+                                              const int32_t* __restrict__ J, int64_t r, double* __restrict__ W,
+                                              int64_t wld) {
   __shared__ double sA[32][33], sB[32][33];
   int ti, tj;
   tri_tile(blockIdx.x, &ti, &tj);
-  const int a0 = ti * 32, b0 = tj * 32;
+  const int64_t o0 = (int64_t)ti * 32, o1 = (int64_t)tj * 32;   // output tile origin
+  const int s = blockIdx.y, ns = gridDim.y;
+  const int64_t K = SMW ? m : r;                                 // reduction length
+  const int64_t nch = (K + 31) / 32;
+  const int64_t c_lo = nch * s / ns, c_hi = nch * (s + 1) / ns;  // chunk slice
   const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
+  // element q of this thread in a 32 × 32 block: e = tid + 256 q → (γ = e >> 5, ρ = e & 31)
+  int64_t colA[4], colB[4];  // SMW: fixed column offsets J[·]*m for the a/b tiles
+  if (SMW) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t ga = o0 + ty + 8 * q, gb = o1 + ty + 8 * q;
+      colA[q] = ga < r ? (int64_t)J[ga] * m : -1;
+      colB[q] = gb < r ? (int64_t)J[gb] * m : -1;
+    }
+  }
+  double va[4], vb[4];
+  auto load = [&](int64_t ch) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (SMW) {
+        const int64_t k = ch * 32 + tx;
+        va[q] = (colA[q] >= 0 && k < m) ? __ldg(A + colA[q] + k) : 0.0;
+        vb[q] = (colB[q] >= 0 && k < m) ? __ldg(A + colB[q] + k) : 0.0;
+      } else {
+        const int64_t a = ch * 32 + ty + 8 * q;
+        const bool ok = a < r;
+        const int64_t cb = ok ? (int64_t)J[a] * m : 0;
+        va[q] = (ok && o0 + tx < m) ? __ldg(A + cb + o0 + tx) : 0.0;
+        vb[q] = (ok && o1 + tx < m) ? __ldg(A + cb + o1 + tx) : 0.0;
+      }
+    }
+  };
   double acc[4] = {0, 0, 0, 0};
-  for (int64_t k0 = 0; k0 < m; k0 += 32) {
-    for (int e = tid; e < 1024; e += 256) {
-      const int col = e >> 5, row = e & 31;
-      const int64_t k = k0 + row;
-      sA[row][col] = (a0 + col < r && k < m) ? __ldg(A + (int64_t)J[a0 + col] * m + k) : 0.0;
-      sB[row][col] = (b0 + col < r && k < m) ? __ldg(A + (int64_t)J[b0 + col] * m + k) : 0.0;
+  if (c_lo < c_hi) load(c_lo);
+  for (int64_t ch = c_lo; ch < c_hi; ++ch) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {  // sX[reduction idx][output idx]
+      if (SMW) {
+        sA[tx][ty + 8 * q] = va[q];
+        sB[tx][ty + 8 * q] = vb[q];
+      } else {
+        sA[ty + 8 * q][tx] = va[q];
+        sB[ty + 8 * q][tx] = vb[q];
+      }
     }
     __syncthreads();
+    if (ch + 1 < c_hi) load(ch + 1);
 #pragma unroll 8
     for (int kk = 0; kk < 32; ++kk) {
       const double bv = sB[kk][tx];
@@ -133,268 +182,427 @@ __global__ void __launch_bounds__(256) k_gram_smw(const double* __restrict__ A, 
     }
     __syncthreads();
   }
+  const int64_t nout = SMW ? r : m;
+  double* Ws = W + (size_t)s * wld * nout;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    const int a = a0 + ty * 4 + q, b = b0 + tx;
-    if (a < r && b < r && a >= b) M[(int64_t)a + (int64_t)b * r] = acc[q] + (a == b ? kinv : 0.0);
+    const int64_t i = o0 + ty * 4 + q, j = o1 + tx;
+    if (i < nout && j < nout && i >= j) Ws[i + j * wld] = acc[q];
   }
 }
 
-// W[s][k + l*m] = Σ_{a in split s} A[k,J_a] A[l,J_a], k ≥ l (lower tiles)
-__global__ void __launch_bounds__(256) k_gram_mm(const double* __restrict__ A, int64_t m,
-                                                 const int32_t* __restrict__ J, int64_t r,
-                                                 double* __restrict__ W) {
-  __shared__ double sA[32][33], sB[32][33];
-  int ti, tj;
-  tri_tile(blockIdx.x, &ti, &tj);
-  const int64_t k0 = ti * 32, l0 = tj * 32;
-  const int s = blockIdx.y, ns = gridDim.y;
-  const int64_t a_lo = (int64_t)s * r / ns, a_hi = (int64_t)(s + 1) * r / ns;
-  const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
-  double acc[4] = {0, 0, 0, 0};
-  for (int64_t a0 = a_lo; a0 < a_hi; a0 += 32) {
-    for (int e = tid; e < 1024; e += 256) {
-      const int ac = e >> 5, row = e & 31;  // column a0+ac, row offset
-      const bool ok = a0 + ac < a_hi;
-      const double* col = ok ? A + (int64_t)J[a0 + ac] * m : A;
-      sA[ac][row] = (ok && k0 + row < m) ? __ldg(col + k0 + row) : 0.0;
-      sB[ac][row] = (ok && l0 + row < m) ? __ldg(col + l0 + row) : 0.0;
-    }
-    __syncthreads();
-#pragma unroll 8
-    for (int aa = 0; aa < 32; ++aa) {
-      const double bv = sB[aa][tx];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) acc[q] = fma(sA[aa][ty * 4 + q], bv, acc[q]);
-    }
-    __syncthreads();
-  }
-  double* Ws = W + (size_t)s * m * m;
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const int64_t k = k0 + ty * 4 + q, l = l0 + tx;
-    if (k < m && l < m && k >= l) Ws[k + l * m] = acc[q];
-  }
-}
-
-// M[k + l*m] = (k == l) + κ Σ_s W[s][k + l*m]   (k ≥ l)
-__global__ void k_gram_mm_reduce(const double* __restrict__ W, int ns, int64_t m, double kappa,
-                                 double* __restrict__ M) {
+// M[i + j*ld] = diag·[i == j] + mult · Σ_s W[s][i + j*nout]   (i ≥ j)
+//   SMW:   diag = κ⁻¹, mult = 1          m × m:  diag = 1, mult = κ   (oracle: κ s + δ)
+__global__ void k_gram_reduce(const double* __restrict__ W, int ns, int64_t nout, double diag, double mult,
+                              double* __restrict__ M, int64_t ld) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= m * m) return;
-  const int64_t k = e % m, l = e / m;
-  if (k < l) return;
+  if (e >= nout * nout) return;
+  const int64_t i = e % nout, j = e / nout;
+  if (i < j) return;
   double s = 0.0;
-  for (int q = 0; q < ns; ++q) s += W[(size_t)q * m * m + e];
-  M[e] = kappa * s + (k == l ? 1.0 : 0.0);
+  for (int q = 0; q < ns; ++q) s += W[(size_t)q * nout * nout + e];
+  M[i + j * ld] = (mult == 1.0 ? s : mult * s) + (i == j ? diag : 0.0);
 }
 
 // ---------------------------------------------------------------------------
-// K4: Cholesky by one cluster.  M is N × N column-major (ld), lower used/overwritten.
-// Right-looking, 32 × 32 tiles kept in L2 (__ldcg), per panel k:
-//   B: L_ik = A_ik L_kk^{-T} for i > k           (warp per tile, all CTAs)   | cluster barrier
-//   C: A_ij −= L_ik L_jkᵀ for k < j ≤ i           (warp per tile, all CTAs)   | cluster barrier
-//      look-ahead: the warp that updates tile (k+1, k+1) factors it right away,
-//      so panel k+1 needs no separate diagonal phase.
+// K4: SPD solve by one thread-block cluster (Cholesky, right-looking, 32 × 32 tiles in L2).
+//
+// M is (N+1) × N column-major with ld ≥ N+1: rows 0..N-1 hold the SPD matrix (lower
+// triangle used and overwritten by L), row N holds the right-hand side.  Carrying the rhs
+// as an extra row through the factorisation yields z = L⁻¹ rhs in row N (the forward
+// substitution) for free.  Per panel k (W_k = L_kk⁻¹ is already in Winv):
+//   B: L_ik = A_ik W_kᵀ for row tiles i > k (rhs row included)   — DMMA tile GEMM, warp/tile
+//      | cluster barrier
+//   C: A_ij −= L_ik L_jkᵀ for k < j ≤ i                             — DMMA tile GEMM, warp/tile
+//      look-ahead: CTA 0 (warps 0-3) updates tile (k+1,k+1) first, factors it (4 warps) and
+//      inverts it (W_{k+1}); the other 8·CS − 4 warps take the remaining tiles
+//      | cluster barrier
+// Then CTA 0 runs the backward substitution v = L⁻ᵀ z with the stored W_k.
+// FP64 tensor cores: mma.sync.m8n8k4.f64 (SASS DMMA) — the tile updates are dense contractions.
+// out = scale · v; if dotv: *dot_out = Σ dotv · out.
 // ---------------------------------------------------------------------------
 constexpr int CHT = 32;  // tile edge
+constexpr int TLD = 33;  // smem tile leading dimension
 
-// Factor the 32×32 tile (k0, kn) of M in registers (lane = row), write L back.
-SSN_DEV void chol_diag_warp(double* M, int ld, int k0, int kn, int lane, int* info) {
-  double a[CHT];
+SSN_DEV void dmma(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+// acc[rb][cb] += sgn · Σ_p SA[r][p] · SB[c][p] over a 32 × 32 × 32 tile (rows r = 8rb + lane/4,
+// cols c = 8cb + 2(lane%4) + e in the C fragment layout of m8n8k4).
+SSN_DEV void tile_mma(const double* SA, const double* SB, double (&acc)[4][4][2], double sgn, int lane) {
+  const int g = lane >> 2, t = lane & 3;
 #pragma unroll
-  for (int c = 0; c < CHT; ++c)
-    a[c] = (lane < kn && c < kn) ? __ldcg(M + (int64_t)(k0 + lane) + (int64_t)(k0 + c) * ld)
-                                 : (lane == c ? 1.0 : 0.0);
+  for (int kk = 0; kk < 8; ++kk) {
+    double af[4], bf[4];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      af[b] = sgn * SA[(8 * b + g) * TLD + 4 * kk + t];
+      bf[b] = SB[(8 * b + g) * TLD + 4 * kk + t];
+    }
+#pragma unroll
+    for (int rb = 0; rb < 4; ++rb)
+#pragma unroll
+      for (int cb = 0; cb < 4; ++cb) dmma(acc[rb][cb], af[rb], bf[cb]);
+  }
+}
+
+// Warp loads rows [r0, r0+32) × cols [c0, c0+32) of M into S (row-major, TLD), zero outside
+// rows < nr and cols < nc.
+SSN_DEV void load_tile_rows(const double* M, int ld, int r0, int c0, int nr, int nc, double* S, int lane) {
+  double v[CHT];  // all 32 loads in flight before the smem stores
+#pragma unroll
+  for (int p = 0; p < CHT; ++p)
+    v[p] = (r0 + lane < nr && c0 + p < nc) ? __ldcg(M + (int64_t)(r0 + lane) + (int64_t)(c0 + p) * ld) : 0.0;
+#pragma unroll
+  for (int p = 0; p < CHT; ++p) S[lane * TLD + p] = v[p];
+}
+
+// Factor the diagonal tile held in smem T (32 × TLD, identity-padded beyond kn; rows up to
+// kn may include one rhs row at index kn) with 4 warps (128 threads, named barrier 2).
+// Warp w owns columns [8w, 8w+8); lane = row.  Then warp 0 computes W = L_diag⁻¹ into Wout.
+SSN_DEV void chol_diag_4w(double* T, int kn, int t128, int* info, double* colbuf, double* Wout) {
+  const int w = t128 >> 5, lane = t128 & 31;
+  double a[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) a[q] = T[lane * TLD + 8 * w + q];
+  bool bad = false;
 #pragma unroll
   for (int j = 0; j < CHT; ++j) {
-    double ajj = __shfl_sync(0xffffffffu, a[j], j);
-    if (!(ajj > 0.0)) {
-      if (lane == 0) atomicExch(info, 1);
-      ajj = 1.0;
+    double* cb = colbuf + (j & 1) * 40;
+    if (w == (j >> 3)) {  // warp-uniform: owner of column j
+      const int jl = j & 7;
+      if (lane == j) cb[33] = a[jl];
+      __syncwarp();
+      double ajj = cb[33];
+      const bool pv = j < kn;
+      bad |= pv && !(ajj > 0.0);
+      ajj = (pv && ajj > 0.0) ? ajj : 1.0;
+      const double d = sqrt(ajj);
+      const double lij = (lane > j) ? a[jl] / d : (lane == j ? d : 0.0);
+      if (lane >= j) a[jl] = lij;
+      cb[lane] = lij;
     }
+    asm volatile("bar.sync 2, 128;" ::: "memory");
+    const double li = cb[lane];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int c = 8 * w + q;
+      const double lc = (c > j) ? cb[c] : 0.0;
+      a[q] = fma(-li, lc, a[q]);
+    }
+  }
+  if (bad && lane == 0) atomicExch(info, 1);
+#pragma unroll
+  for (int q = 0; q < 8; ++q) T[lane * TLD + 8 * w + q] = a[q];
+  asm volatile("bar.sync 2, 128;" ::: "memory");
+  if (w == 0) {  // W = L⁻¹ (lane = column), forward substitution with 4 partial sums
+    double x[CHT];
+#pragma unroll
+    for (int i = 0; i < CHT; ++i) {
+      double s0 = (i == lane) ? 1.0 : 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+      for (int p = 0; p < i; ++p) {
+        const double v = T[i * TLD + p] * x[p];
+        if ((p & 3) == 0) s0 -= v;
+        else if ((p & 3) == 1) s1 -= v;
+        else if ((p & 3) == 2) s2 -= v;
+        else s3 -= v;
+      }
+      x[i] = ((s0 + s1) + (s2 + s3)) / T[i * TLD + i];
+    }
+#pragma unroll
+    for (int i = 0; i < CHT; ++i) Wout[i * CHT + lane] = (i < kn && lane < kn) ? x[i] : (i == lane ? 1.0 : 0.0);
+  }
+}
+
+// Single-warp variant (lane = row in registers; the scaled column is broadcast through smem).
+SSN_DEV void chol_diag_1w(double* T, int kn, int lane, int* info, double* colbuf, double* Wout) {
+  double a[CHT];
+#pragma unroll
+  for (int c = 0; c < CHT; ++c) a[c] = T[lane * TLD + c];
+  bool bad = false;
+#pragma unroll
+  for (int j = 0; j < CHT; ++j) {
+    double ajj = T[j * TLD + j];  // pivot row j, updated in smem by lane j below
+    const bool pv = j < kn;
+    bad |= pv && !(ajj > 0.0);
+    ajj = (pv && ajj > 0.0) ? ajj : 1.0;
     const double d = sqrt(ajj);
     const double inv = 1.0 / d;
     const double lij = (lane > j) ? a[j] * inv : (lane == j ? d : 0.0);
-    a[j] = lij;
+    if (lane >= j) a[j] = lij;
+    colbuf[lane] = lij;
+    __syncwarp();
+    double lc[CHT];
 #pragma unroll
-    for (int c = j + 1; c < CHT; ++c) {
-      const double lcj = __shfl_sync(0xffffffffu, lij, c);
-      if (lane >= c) a[c] = fma(-lij, lcj, a[c]);
+    for (int c = j + 1; c < CHT; ++c) lc[c] = colbuf[c];
+#pragma unroll
+    for (int c = j + 1; c < CHT; ++c) a[c] = fma(-lij, lc[c], a[c]);
+    if (j + 1 < CHT && lane == j + 1) T[(j + 1) * TLD + j + 1] = a[j + 1];
+    __syncwarp();
+  }
+  if (bad && lane == 0) atomicExch(info, 1);
+#pragma unroll
+  for (int c = 0; c < CHT; ++c) T[lane * TLD + c] = a[c];
+  __syncwarp();
+  double x[CHT];  // W = L⁻¹ restricted to the kn × kn factor (lane = column)
+#pragma unroll
+  for (int i = 0; i < CHT; ++i) {
+    double s0 = (i == lane) ? 1.0 : 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+    for (int p = 0; p < i; ++p) {
+      const double v = T[i * TLD + p] * x[p];
+      if ((p & 3) == 0) s0 -= v;
+      else if ((p & 3) == 1) s1 -= v;
+      else if ((p & 3) == 2) s2 -= v;
+      else s3 -= v;
     }
+    x[i] = ((s0 + s1) + (s2 + s3)) / T[i * TLD + i];
   }
-  if (lane < kn) {
 #pragma unroll
-    for (int c = 0; c < CHT; ++c)
-      if (c <= lane && c < kn) M[(int64_t)(k0 + lane) + (int64_t)(k0 + c) * ld] = a[c];
-  }
+  for (int i = 0; i < CHT; ++i) Wout[i * CHT + lane] = (i < kn && lane < kn) ? x[i] : (i == lane ? 1.0 : 0.0);
 }
 
-__global__ void __launch_bounds__(256, 1) k_chol_cluster(double* M, int N, int ld, int* info) {
+// CTA-0 look-ahead: factor the diagonal tile at n0 (kn columns, nrow rows incl. possibly the
+// rhs row) with warp 0 and store L (into M) and W = L⁻¹ (into Wout).  Latency-oriented:
+// lane = row in registers, each lane keeps a replica of the diagonal (updated with the same
+// fma as the owning lane, so bitwise equal) so the next pivot is local; 1/√pivot by rsqrt;
+// only the scaled column is broadcast (smem colbuf); the inverse uses the stored reciprocals.
+SSN_DEV void diag_block(double* M, int ld, int N, int NR, int n0, int t128, int* info, double* T, double* colbuf,
+                        double* Wout) {
+  if (t128 >= 32) return;
+  const int lane = t128;
+  const int kn = min(CHT, N - n0), nrow = min(CHT, NR - n0);
+  double a[CHT], dg[CHT];
+#pragma unroll
+  for (int c = 0; c < CHT; ++c)
+    a[c] = (lane < nrow && c < kn) ? __ldcg(M + (int64_t)(n0 + lane) + (int64_t)(n0 + c) * ld) : (lane == c ? 1.0 : 0.0);
+#pragma unroll
+  for (int c = 0; c < CHT; ++c) dg[c] = (c < kn) ? __ldcg(M + (int64_t)(n0 + c) * (ld + 1)) : 1.0;
+  double* invs = colbuf + 40;  // 1/L_jj
+  bool bad = false;
+#pragma unroll
+  for (int j = 0; j < CHT; ++j) {
+    double ajj = dg[j];
+    const bool pv = j < kn;
+    bad |= pv && !(ajj > 0.0);
+    ajj = (pv && ajj > 0.0) ? ajj : 1.0;
+    const double inv = rsqrt(ajj);
+    const double d = ajj * inv;
+    const double lij = (lane > j) ? a[j] * inv : (lane == j ? d : 0.0);
+    if (lane >= j) a[j] = lij;
+    colbuf[lane] = lij;
+    if (lane == 0) invs[j] = 1.0 / d;
+    __syncwarp();
+    double lc[CHT];
+#pragma unroll
+    for (int c = j + 1; c < CHT; ++c) lc[c] = colbuf[c];
+    if (j + 1 < CHT) dg[j + 1] = fma(-lc[j + 1], lc[j + 1], dg[j + 1]);  // next pivot first
+#pragma unroll
+    for (int c = j + 1; c < CHT; ++c) {
+      a[c] = fma(-lij, lc[c], a[c]);
+      if (c > j + 1) dg[c] = fma(-lc[c], lc[c], dg[c]);
+    }
+    __syncwarp();
+  }
+  if (bad && lane == 0) atomicExch(info, 1);
+  if (lane < nrow) {
+#pragma unroll
+    for (int c = 0; c < CHT; ++c)
+      if (c < kn && c <= lane) M[(int64_t)(n0 + lane) + (int64_t)(n0 + c) * ld] = a[c];
+  }
+#pragma unroll
+  for (int c = 0; c < CHT; ++c) T[lane * TLD + c] = a[c];
+  __syncwarp();
+  double x[CHT];  // W = L⁻¹ restricted to the kn × kn factor (lane = column)
+#pragma unroll
+  for (int i = 0; i < CHT; ++i) {
+    double s0 = (i == lane) ? 1.0 : 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+    for (int p = 0; p < i; ++p) {
+      const double v = T[i * TLD + p] * x[p];
+      if ((p & 3) == 0) s0 -= v;
+      else if ((p & 3) == 1) s1 -= v;
+      else if ((p & 3) == 2) s2 -= v;
+      else s3 -= v;
+    }
+    x[i] = ((s0 + s1) + (s2 + s3)) * invs[i];
+  }
+#pragma unroll
+  for (int i = 0; i < CHT; ++i) Wout[i * CHT + lane] = (i < kn && lane < kn) ? x[i] : (i == lane ? 1.0 : 0.0);
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(256, 1) k_chol_cluster(double* M, int N, int ld, double* __restrict__ out,
+                                                         double scale, const double* __restrict__ dotv,
+                                                         double* dot_out, double* Winv, int* info) {
   namespace cg = cooperative_groups;
   cg::cluster_group cl = cg::this_cluster();
   const int rank = (int)cl.block_rank(), CS = (int)cl.num_blocks();
   extern __shared__ double dsm[];
-  double(*D)[33] = reinterpret_cast<double(*)[33]>(dsm);  // L_kk
-  double* invd = dsm + 32 * 33;                            // 1 / L_kk[c][c]
-  double* wsm = invd + 32;                                 // 8 warps x 32 x 32
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int nt = (N + CHT - 1) / CHT;
-  const int gw = rank + CS * warp;  // global warp id in the cluster
+  double* SA = dsm + (size_t)warp * 2 * CHT * TLD;  // per-warp operand tiles
+  double* SB = SA + CHT * TLD;
+  double* T = dsm + (size_t)8 * 2 * CHT * TLD;      // CTA-0 diagonal tile
+  double* colbuf = T + CHT * TLD;                   // 80 doubles (col broadcast + reciprocals)
+  const int NR = N + 1;
+  const int ntc = (N + CHT - 1) / CHT, ntr = (NR + CHT - 1) / CHT;
   const int NWg = CS * 8;
-
-  if (gw == 0) chol_diag_warp(M, ld, 0, min(CHT, N), lane, info);
+  const int gw = rank + CS * warp;
+  // worker warps for phase C: all warps of CTAs 1..CS-1 (CTA 0 owns the look-ahead diagonal, so
+  // its factorisation does not compete for issue slots); with CS = 1 CTA 0's warps 4-7 work too.
+  const bool diag_team = (rank == 0 && warp < 4);
+  const int NWw = (CS > 1) ? NWg - 8 : 4;
+  const int wid = (CS > 1) ? ((rank == 0) ? -1 : (rank - 1) * 8 + warp) : warp - 4;
+#ifdef CHOL_PROBE
+#define STAMP(i) do { if (rank == 0 && tid == 0 && (i) < 64) { unsigned long long t_; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); g_t[i] = t_; } } while (0)
+#else
+#define STAMP(i) do {} while (0)
+#endif
+  STAMP(0);
+  if (diag_team) diag_block(M, ld, N, NR, 0, tid, info, T, colbuf, Winv);
   cl.sync();
-  for (int k = 0; k + 1 < nt; ++k) {
-    const int k0 = k * CHT;  // kn = 32 for every panel but the last
-    // ---- B: L_ik = A_ik L_kk^{-T}, i > k ----
-    const int ntiles = nt - k - 1;
-    if (rank < ntiles) {  // CTAs with at least one tile load L_kk
-      for (int e = tid; e < CHT * CHT; e += blockDim.x) {
-        const int i = e & 31, j = e >> 5;
-        D[i][j] = (i >= j) ? __ldcg(M + (int64_t)(k0 + i) + (int64_t)(k0 + j) * ld) : 0.0;
+  STAMP(1);
+  for (int k = 0; k < ntc; ++k) {
+    const int k0 = k * CHT;
+    const int kn = min(CHT, N - k0);
+    // ---- B: L_ik = A_ik W_kᵀ for row tiles i > k ----
+    const int nB = ntr - k - 1;
+    for (int q = gw; q < nB; q += NWg) {
+      const int i0 = (k + 1 + q) * CHT;
+      load_tile_rows(M, ld, i0, k0, NR, k0 + kn, SA, lane);
+      const double* Wk = Winv + (size_t)k * CHT * CHT;
+      {
+        double v[CHT];
+#pragma unroll
+        for (int p = 0; p < CHT; ++p) v[p] = __ldcg(Wk + lane * CHT + p);  // SB[c][p] = W[c][p]
+#pragma unroll
+        for (int p = 0; p < CHT; ++p) SB[lane * TLD + p] = v[p];
       }
-      __syncthreads();
-      if (tid < CHT) invd[tid] = 1.0 / D[tid][tid];
-      __syncthreads();
-      for (int q = gw; q < ntiles; q += NWg) {
-        const int row = (k + 1 + q) * CHT + lane;
-        double x[CHT];
+      __syncwarp();
+      double acc[4][4][2] = {};
+      tile_mma(SA, SB, acc, 1.0, lane);
+      const int g = lane >> 2, t = lane & 3;
 #pragma unroll
-        for (int c = 0; c < CHT; ++c) x[c] = (row < N) ? __ldcg(M + (int64_t)row + (int64_t)(k0 + c) * ld) : 0.0;
+      for (int rb = 0; rb < 4; ++rb)
 #pragma unroll
-        for (int c = 0; c < CHT; ++c) {
-          double s0 = x[c], s1 = 0.0;
+        for (int cb = 0; cb < 4; ++cb)
 #pragma unroll
-          for (int p = 0; p < c; ++p) {
-            if (p & 1) s1 = fma(-x[p], D[c][p], s1);
-            else s0 = fma(-x[p], D[c][p], s0);
+          for (int e = 0; e < 2; ++e) {
+            const int r = i0 + 8 * rb + g, c = 8 * cb + 2 * t + e;
+            if (r < NR && c < kn) M[(int64_t)r + (int64_t)(k0 + c) * ld] = acc[rb][cb][e];
           }
-          x[c] = (s0 + s1) * invd[c];
-        }
-        if (row < N) {
-#pragma unroll
-          for (int c = 0; c < CHT; ++c) M[(int64_t)row + (int64_t)(k0 + c) * ld] = x[c];
-        }
-      }
+      __syncwarp();
     }
     cl.sync();
-    // ---- C: A_ij −= L_ik L_jkᵀ, k < j ≤ i; tile (k+1,k+1) first, then factored ----
-    {
-      const int rem = nt - k - 1;
-      const int npairs = rem * (rem + 1) / 2;
-      double* S = wsm + (size_t)warp * CHT * CHT;  // S[p*32 + l] = L_jk[l][p]
-      for (int q = gw; q < npairs; q += NWg) {
-        int ii, jj;
-        tri_tile(q, &ii, &jj);  // q = 0 → (0,0) = tile (k+1, k+1)
-        const int i0 = (k + 1 + ii) * CHT, j0 = (k + 1 + jj) * CHT;
-        const int row = i0 + lane;
-        double a[CHT];
-#pragma unroll
-        for (int p = 0; p < CHT; ++p) {
-          a[p] = (row < N) ? __ldcg(M + (int64_t)row + (int64_t)(k0 + p) * ld) : 0.0;
-          S[p * CHT + lane] = (j0 + lane < N) ? __ldcg(M + (int64_t)(j0 + lane) + (int64_t)(k0 + p) * ld) : 0.0;
-        }
-        __syncwarp();
-        double c[CHT];
-#pragma unroll
-        for (int l = 0; l < CHT; ++l)
-          c[l] = (row < N && j0 + l < N) ? __ldcg(M + (int64_t)row + (int64_t)(j0 + l) * ld) : 0.0;
-#pragma unroll
-        for (int p = 0; p < CHT; ++p) {
-          const double ap = a[p];
-          const double2* Sp = reinterpret_cast<const double2*>(S + p * CHT);
-#pragma unroll
-          for (int l2 = 0; l2 < CHT / 2; ++l2) {
-            const double2 sv = Sp[l2];
-            c[2 * l2] = fma(-ap, sv.x, c[2 * l2]);
-            c[2 * l2 + 1] = fma(-ap, sv.y, c[2 * l2 + 1]);
-          }
-        }
-        if (row < N) {
-#pragma unroll
-          for (int l = 0; l < CHT; ++l)
-            if (j0 + l < N && (i0 != j0 || l <= lane)) M[(int64_t)row + (int64_t)(j0 + l) * ld] = c[l];
-        }
-        __syncwarp();
-        if (q == 0) {  // look-ahead: factor the next diagonal tile now
-          __threadfence_block();
-          chol_diag_warp(M, ld, (k + 1) * CHT, min(CHT, N - (k + 1) * CHT), lane, info);
-        }
+    STAMP(2 + 2 * k);
+    if (k + 1 >= ntc) break;
+    // ---- C: A_ij −= L_ik L_jkᵀ for k < j < ntc, j ≤ i < ntr ----
+    const int remc = ntc - k - 1, remr = ntr - k - 1;
+    const int ntri = remc * (remc + 1) / 2;
+    const int npairs = ntri + (remr - remc) * remc;
+    auto do_tile = [&](int q) {
+      int ii, jj;
+      if (q < ntri) tri_tile(q, &ii, &jj);
+      else {
+        ii = remc;
+        jj = q - ntri;
       }
+      const int i0 = (k + 1 + ii) * CHT, j0 = (k + 1 + jj) * CHT;
+      load_tile_rows(M, ld, i0, k0, NR, k0 + kn, SA, lane);
+      load_tile_rows(M, ld, j0, k0, N, k0 + kn, SB, lane);
+      if (k == 0 && q == 0) STAMP(53);
+      const int g = lane >> 2, t = lane & 3;
+      double acc[4][4][2];
+#pragma unroll
+      for (int rb = 0; rb < 4; ++rb)
+#pragma unroll
+        for (int cb = 0; cb < 4; ++cb)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int r = i0 + 8 * rb + g, c = j0 + 8 * cb + 2 * t + e;
+            acc[rb][cb][e] = (r < NR && c < N) ? __ldcg(M + (int64_t)r + (int64_t)c * ld) : 0.0;
+          }
+      __syncwarp();
+      if (k == 0 && q == 0) STAMP(54);
+      tile_mma(SA, SB, acc, -1.0, lane);
+      if (k == 0 && q == 0) STAMP(55);
+#pragma unroll
+      for (int rb = 0; rb < 4; ++rb)
+#pragma unroll
+        for (int cb = 0; cb < 4; ++cb)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int rl = 8 * rb + g, cl_ = 8 * cb + 2 * t + e;
+            const int r = i0 + rl, c = j0 + cl_;
+            if (r < NR && c < N && (i0 != j0 || cl_ <= rl)) M[(int64_t)r + (int64_t)c * ld] = acc[rb][cb][e];
+          }
+      __syncwarp();
+    };
+    if (diag_team) {
+      if (k == 0) STAMP(50);
+      if (warp == 0) do_tile(0);  // tile (k+1, k+1)
+      if (k == 0) STAMP(51);
+      asm volatile("bar.sync 2, 128;" ::: "memory");
+      __threadfence_block();
+      diag_block(M, ld, N, NR, (k + 1) * CHT, tid, info, T, colbuf, Winv + (size_t)(k + 1) * CHT * CHT);
+      if (k == 0) STAMP(52);
+    } else if (wid >= 0) {
+      for (int q = 1 + wid; q < npairs; q += NWw) do_tile(q);
     }
     cl.sync();
+    STAMP(3 + 2 * k);
   }
-}
-
-// Solve (L Lᵀ) v = rhs; out = scale * v; if dotv: *dot_out = Σ dotv · out.  Single CTA, N ≤ 4096.
-__global__ void __launch_bounds__(1024) k_chol_solve(const double* __restrict__ L, int N, int ld,
-                                                     const double* __restrict__ rhs, double scale,
-                                                     double* __restrict__ out, const double* __restrict__ dotv,
-                                                     double* dot_out) {
-  extern __shared__ double z[];
-  __shared__ double red[32];
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  for (int i = tid; i < N; i += blockDim.x) z[i] = rhs[i];
+  STAMP(40);
+  if (rank != 0) return;
+  // ---- backward substitution v = L⁻ᵀ z by CTA 0 (z = row N) ----
+  double* zv = dsm;  // N doubles (N ≤ 1024 < 16·32·33)
+  for (int i = tid; i < N; i += blockDim.x) zv[i] = __ldcg(M + (int64_t)N + (int64_t)i * ld);
   __syncthreads();
-  // forward: L y = z
-  for (int k0 = 0; k0 < N; k0 += 32) {
-    const int kn = min(32, N - k0);
-    if (warp == 0) {
-      const int c = lane;
-      double Lr[32];
+  for (int kb = ntc - 1; kb >= 0; --kb) {
+    const int b0 = kb * CHT, bn = min(CHT, N - b0);
+    if (warp == 0) {  // v_b = W_bᵀ z_b  (W identity-padded beyond bn)
+      const double* Wb = Winv + (size_t)kb * CHT * CHT;
+      double wv[CHT];
 #pragma unroll
-      for (int p = 0; p < 32; ++p) Lr[p] = (c < kn && p < c) ? L[(int64_t)(k0 + c) + (int64_t)(k0 + p) * ld] : 0.0;
-      const double dinv = (c < kn) ? 1.0 / L[(int64_t)(k0 + c) * (ld + 1)] : 1.0;
-      double zc = (c < kn) ? z[k0 + c] : 0.0;
+      for (int i = 0; i < CHT; ++i) wv[i] = __ldg(Wb + i * CHT + lane);
+      double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
 #pragma unroll
-      for (int p = 0; p < 32; ++p) {
-        if (lane == p) zc *= dinv;
-        const double zp = __shfl_sync(0xffffffffu, zc, p);
-        if (lane > p) zc = fma(-Lr[p], zp, zc);
+      for (int i = 0; i < CHT; i += 4) {
+        v0 = fma(wv[i], (i < bn) ? zv[b0 + i] : 0.0, v0);
+        v1 = fma(wv[i + 1], (i + 1 < bn) ? zv[b0 + i + 1] : 0.0, v1);
+        v2 = fma(wv[i + 2], (i + 2 < bn) ? zv[b0 + i + 2] : 0.0, v2);
+        v3 = fma(wv[i + 3], (i + 3 < bn) ? zv[b0 + i + 3] : 0.0, v3);
       }
-      if (c < kn) z[k0 + c] = zc;
+      __syncwarp();
+      if (lane < bn) zv[b0 + lane] = (v0 + v1) + (v2 + v3);
     }
     __syncthreads();
-    for (int i = k0 + kn + tid; i < N; i += blockDim.x) {
-      double s = 0.0;
-      for (int p = 0; p < kn; ++p) s = fma(L[(int64_t)i + (int64_t)(k0 + p) * ld], z[k0 + p], s);
-      z[i] -= s;
+    for (int p = tid; p < b0; p += blockDim.x) {  // z_p −= Σ_{c<bn} L[b0+c][p] v_c
+      const double* Lc = M + (int64_t)p * ld + b0;
+      double lv[CHT];
+#pragma unroll
+      for (int c = 0; c < CHT; ++c) lv[c] = (c < bn) ? __ldg(Lc + c) : 0.0;  // L1: no stale lines (.cg before)
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+      for (int c = 0; c < CHT; c += 4) {
+        s0 = fma(lv[c], (c < bn) ? zv[b0 + c] : 0.0, s0);
+        s1 = fma(lv[c + 1], (c + 1 < bn) ? zv[b0 + c + 1] : 0.0, s1);
+        s2 = fma(lv[c + 2], (c + 2 < bn) ? zv[b0 + c + 2] : 0.0, s2);
+        s3 = fma(lv[c + 3], (c + 3 < bn) ? zv[b0 + c + 3] : 0.0, s3);
+      }
+      zv[p] -= (s0 + s1) + (s2 + s3);
     }
     __syncthreads();
   }
-  // backward: Lᵀ v = y
-  const int nb = (N + 31) / 32;
-  for (int kb = nb - 1; kb >= 0; --kb) {
-    const int k0 = kb * 32, kn = min(32, N - k0);
-    if (warp == 0) {
-      const int c = lane;
-      double Lc[32];  // Lc[p] = L[k0+p][k0+c] for p > c
-#pragma unroll
-      for (int p = 0; p < 32; ++p)
-        Lc[p] = (c < kn && p < kn && p > c) ? L[(int64_t)(k0 + p) + (int64_t)(k0 + c) * ld] : 0.0;
-      const double dinv = (c < kn) ? 1.0 / L[(int64_t)(k0 + c) * (ld + 1)] : 1.0;
-      double zc = (c < kn) ? z[k0 + c] : 0.0;
-#pragma unroll
-      for (int p = 31; p >= 0; --p) {
-        if (lane == p) zc *= dinv;
-        const double zp = __shfl_sync(0xffffffffu, zc, p);
-        if (lane < p) zc = fma(-Lc[p], zp, zc);
-      }
-      if (c < kn) z[k0 + c] = zc;
-    }
-    __syncthreads();
-    for (int i = tid; i < k0; i += blockDim.x) {
-      double s = 0.0;
-      const double* Lcol = L + (int64_t)i * ld + k0;  // L[k0+p][i]
-      for (int p = 0; p < kn; ++p) s = fma(Lcol[p], z[k0 + p], s);
-      z[i] -= s;
-    }
-    __syncthreads();
-  }
+  STAMP(42);
+  __shared__ double red[8];
   double dot = 0.0;
   for (int i = tid; i < N; i += blockDim.x) {
-    const double v = scale * z[i];
+    const double v = scale * zv[i];
     out[i] = v;
     if (dotv) dot += dotv[i] * v;
   }
@@ -403,12 +611,15 @@ __global__ void __launch_bounds__(1024) k_chol_solve(const double* __restrict__ 
     if (lane == 0) red[warp] = dot;
     __syncthreads();
     if (tid == 0) {
-      double s = 0.0;
-      for (int wi = 0; wi < (int)(blockDim.x >> 5); ++wi) s += red[wi];
-      *dot_out = s;
+      double sacc = 0.0;
+      for (int wi = 0; wi < 8; ++wi) sacc += red[wi];
+      *dot_out = sacc;
     }
   }
 }
+
+// dynamic shared memory of k_chol_cluster (bytes)
+constexpr size_t kCholSmem = (size_t)(8 * 2 * CHT * TLD + CHT * TLD + 80) * sizeof(double);
 
 // y ← y + s·d  (m-vector) and small helpers
 __global__ void k_axpy_m(int64_t m, const double* y, double s, const double* d, double* out) {

@@ -206,6 +206,7 @@ struct ssnal_en_problem {
   double* u = nullptr;
   double* tmpm = nullptr;
   double* Mmat = nullptr;
+  double* Winv = nullptr;  // inverses of the 32 × 32 diagonal blocks of L
   double* W = nullptr;
   int W_splits = 0;
   int* info = nullptr;
@@ -273,10 +274,9 @@ int configure(ssnal_en_problem* P) {
   CK(cudaFuncSetAttribute(k1_for(P->MR), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->k1_smem));
   const size_t gsm = (size_t)8 * m * 8;
   CK(cudaFuncSetAttribute(gax_for(P->MR), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsm));
-  P->chol_smem = (size_t)(32 * 33 + 32 + 8 * 32 * 32) * 8;
+  P->chol_smem = kCholSmem;
   CK(cudaFuncSetAttribute(k_chol_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->chol_smem));
   CK(cudaFuncSetAttribute(k_chol_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-  CK(cudaFuncSetAttribute(k_chol_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(m * 8)));
   // cluster size: 16 (non-portable) when schedulable, else 8
   {
     int want = P->cluster > 0 ? P->cluster : 16;
@@ -323,7 +323,8 @@ int allocate(ssnal_en_problem* P) {
   AL(P->d, m * 8);
   AL(P->u, m * 8);
   AL(P->tmpm, m * 8);
-  AL(P->Mmat, (size_t)m * m * 8);
+  AL(P->Mmat, (size_t)(m + 1) * (m + 1) * 8);
+  AL(P->Winv, (size_t)((m + 31) / 32) * 32 * 32 * 8);
   P->W_splits = 16;
   AL(P->W, (size_t)P->W_splits * m * m * 8);
   AL(P->info, 64);
@@ -461,7 +462,9 @@ int fetch_eval(ssnal_en_problem* P, int slot, EvalOut* out) {
   return SSNAL_OK;
 }
 
-int launch_chol(ssnal_en_problem* P, double* M, int N) {
+// Cluster Cholesky + both triangular solves: M holds the matrix (ld = N+1) and the rhs in row N.
+int launch_chol(ssnal_en_problem* P, double* M, int N, double* out, double scale, const double* dotv,
+                double* dot_out) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(P->cluster);
   cfg.blockDim = dim3(256);
@@ -474,7 +477,7 @@ int launch_chol(ssnal_en_problem* P, double* M, int N) {
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  CK(cudaLaunchKernelEx(&cfg, k_chol_cluster, M, N, N, P->info));
+  CK(cudaLaunchKernelEx(&cfg, k_chol_cluster, M, N, N + 1, out, scale, dotv, dot_out, P->Winv, P->info));
   P->launches++;
   return SSNAL_OK;
 }
@@ -491,22 +494,31 @@ int newton_direction(ssnal_en_problem* P, const int32_t* J, int64_t r, const dou
     return SSNAL_OK;
   }
   CK(cudaMemsetAsync(P->info, 0, sizeof(int), P->st));
+  // K3: split-K Gram over enough CTAs to cover the GPU (2 per SM), ≤ W_splits slices
+  auto splits = [&](int tiles, int64_t K) {
+    int ns = (int)((2 * P->nsm + tiles - 1) / tiles);
+    const int64_t nch = (K + 31) / 32;
+    if (ns > nch) ns = (int)nch;
+    if (ns > P->W_splits) ns = P->W_splits;
+    return ns < 1 ? 1 : ns;
+  };
   if (r < m) {  // Sherman–Morrison–Woodbury, Eq. (19): factor κ⁻¹I_r + A_JᵀA_J (R13)
     const int N = (int)r;
-    const int nt = (N + 31) / 32;
-    k_gram_smw<<<nt * (nt + 1) / 2, 256, 0, P->st>>>(P->A, m, J, N, 1.0 / kappa, P->Mmat);
+    const int nt = (N + 31) / 32, tiles = nt * (nt + 1) / 2;
+    const int ns = splits(tiles, m);
+    k_gram<true><<<dim3(tiles, ns), 256, 0, P->st>>>(P->A, m, J, r, P->W, r);
+    P->launches++;
+    CKL();
+    k_gram_reduce<<<(unsigned)((r * r + 255) / 256), 256, 0, P->st>>>(P->W, ns, r, 1.0 / kappa, 1.0, P->Mmat, N + 1);
     P->launches++;
     CKL();
     int wg = (int)((r * 32 + 255) / 256);
     if (wg > 4 * P->nsm) wg = 4 * P->nsm;
-    k_jt_gemv<<<wg, 256, 0, P->st>>>(P->A, m, J, r, g, P->u);
+    k_jt_gemv<<<wg, 256, 0, P->st>>>(P->A, m, J, r, g, P->Mmat + N, N + 1);  // u = A_Jᵀ g → rhs row
     P->launches++;
     CKL();
-    int rc = launch_chol(P, P->Mmat, N);
+    int rc = launch_chol(P, P->Mmat, N, P->u, 1.0, nullptr, nullptr);  // v = (κ⁻¹I + G)⁻¹ u
     if (rc) return rc;
-    k_chol_solve<<<1, 1024, (size_t)N * 8, P->st>>>(P->Mmat, N, N, P->u, 1.0, P->u, nullptr, nullptr);
-    P->launches++;
-    CKL();
     int grid = 0;
     rc = launch_gather(P, J, P->u, r, &grid);
     if (rc) return rc;
@@ -517,24 +529,19 @@ int newton_direction(ssnal_en_problem* P, const int32_t* J, int64_t r, const dou
     return SSNAL_OK;
   }
   // r ≥ m: Eq. (18), M = I_m + κ A_J A_Jᵀ
-  const int nt = (int)((m + 31) / 32);
-  const int tiles = nt * (nt + 1) / 2;
-  int ns = (int)((2 * P->nsm + tiles - 1) / tiles);
-  int64_t maxs = (r + 63) / 64;
-  if (ns > maxs) ns = (int)maxs;
-  if (ns > P->W_splits) ns = P->W_splits;
-  if (ns < 1) ns = 1;
-  k_gram_mm<<<dim3(tiles, ns), 256, 0, P->st>>>(P->A, m, J, r, P->W);
+  const int nt = (int)((m + 31) / 32), tiles = nt * (nt + 1) / 2;
+  const int ns = splits(tiles, r);
+  k_gram<false><<<dim3(tiles, ns), 256, 0, P->st>>>(P->A, m, J, r, P->W, m);
   P->launches++;
   CKL();
-  k_gram_mm_reduce<<<(unsigned)((m * m + 255) / 256), 256, 0, P->st>>>(P->W, ns, m, kappa, P->Mmat);
+  k_gram_reduce<<<(unsigned)((m * m + 255) / 256), 256, 0, P->st>>>(P->W, ns, m, 1.0, kappa, P->Mmat, m + 1);
   P->launches++;
   CKL();
-  int rc = launch_chol(P, P->Mmat, (int)m);
+  k_copy_strided<<<(unsigned)((m + 255) / 256), 256, 0, P->st>>>(m, g, P->Mmat + m, m + 1);  // rhs row = g
+  P->launches++;
+  CKL();
+  int rc = launch_chol(P, P->Mmat, (int)m, d, -1.0, g, gd_dev);  // d = −M⁻¹ g, gd = gᵀd
   if (rc) return rc;
-  k_chol_solve<<<1, 1024, (size_t)m * 8, P->st>>>(P->Mmat, (int)m, (int)m, g, -1.0, d, g, gd_dev);
-  P->launches++;
-  CKL();
   *branch = 2;
   return SSNAL_OK;
 }
@@ -825,6 +832,7 @@ static void destroy_bufs(ssnal_en_problem* P) {
   cudaFree(P->u);
   cudaFree(P->tmpm);
   cudaFree(P->Mmat);
+  cudaFree(P->Winv);
   cudaFree(P->W);
   cudaFree(P->info);
   cudaFree(P->ev_dev);
