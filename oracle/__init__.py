@@ -42,7 +42,7 @@ class Stats(ctypes.Structure):
 
 class Trace(ctypes.Structure):
     _fields_ = [("outer", ctypes.c_int32), ("branch", ctypes.c_int32), ("r", ctypes.c_int64), ("s", _d),
-                ("psi", _d), ("res1", _d), ("gd", _d)]
+                ("psi", _d), ("res1", _d), ("gd", _d), ("jsum", ctypes.c_int64)]
 
 
 def lib():

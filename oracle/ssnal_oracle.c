@@ -340,6 +340,7 @@ typedef struct { /* one record per Newton step (debugging parity) */
   int32_t outer, branch;
   int64_t r;
   double s, psi, res1, gd;
+  int64_t jsum; /* checksum of J (Σ (i+1)·(a+1) mod 2^61) to see whether J changed */
 } orc_trace;
 
 typedef struct { /* EVAL(y, w): everything that depends on (x, σ, y) */
@@ -489,6 +490,9 @@ int orc_solve(const double* A, const double* b, i64 m, i64 n, double l1, double 
         trace[ntr].psi = ev.psi;
         trace[ntr].res1 = ev.res1;
         trace[ntr].gd = gd;
+        uint64_t js = 0;
+        for (i64 a = 0; a < ev.r; ++a) js = (js + (uint64_t)(J[a] + 1) * (uint64_t)(a + 1)) & ((1ULL << 61) - 1);
+        trace[ntr].jsum = (int64_t)js;
       }
       ntr++;
       /* y ← y + s d; z ← z̄(y) implicitly via P (Algorithm 1 steps (3)-(4)). */

@@ -460,9 +460,9 @@ struct EvalOut {
   double psi, psimag, res1;
   double yy, by, gg;
   double s[4];      // Σ P², Σ (x−P)², Σ z², Σ ((|w|−λ1)_+)²
-  double gd;        // gᵀd of the direction computed at this point (filled later)
+  double gd;        // gᵀd of the direction that produced this point (copied from gd_src)
   long long r;      // |J|
-  long long pad;
+  long long info;   // Cholesky status of that direction (copied from info_src)
 };
 
 constexpr int K5_THREADS = 256;  // 8 warps; CTA c owns rows [32c, 32c + 32)
@@ -477,7 +477,8 @@ __global__ void __launch_bounds__(K5_THREADS) k_eval_reduce(int64_t m, const dou
                                                             const double* __restrict__ part_scal, int nscal,
                                                             Scal sc, double nb, int with_grad,
                                                             double* __restrict__ g_out, const int64_t* r_in,
-                                                            EvalOut* out, double* blk, unsigned* ticket) {
+                                                            EvalOut* out, double* blk, unsigned* ticket,
+                                                            const double* gd_src, const int* info_src) {
   __shared__ double red[8][33];
   __shared__ bool last;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -528,17 +529,23 @@ __global__ void __launch_bounds__(K5_THREADS) k_eval_reduce(int64_t m, const dou
     }
   }
   __syncthreads();
-  if (!last || tid != 0) return;
+  if (!last || warp != 0) return;
   __threadfence();
+  // warp 0 of the last CTA: lane ℓ sums entries q ≡ ℓ (mod 32) in order, then a fixed butterfly
   double a = 0, bb = 0, c = 0;
-  for (unsigned q = 0; q < gridDim.x; ++q) {
+  for (unsigned q = lane; q < gridDim.x; q += 32) {
     a += __ldcg(blk + q * 3 + 0);
     bb += __ldcg(blk + q * 3 + 1);
     c += __ldcg(blk + q * 3 + 2);
   }
   double s[4] = {0, 0, 0, 0};
-  for (int q = 0; q < nscal; ++q)
-    for (int j = 0; j < 4; ++j) s[j] += part_scal[q * 4 + j];
+  for (int q = lane; q < nscal; q += 32)
+    for (int j = 0; j < 4; ++j) s[j] += __ldcg(part_scal + q * 4 + j);
+  a = warp_allsum(a);
+  bb = warp_allsum(bb);
+  c = warp_allsum(c);
+  for (int j = 0; j < 4; ++j) s[j] = warp_allsum(s[j]);
+  if (lane != 0) return;
   EvalOut o;
   o.yy = a;
   o.by = bb;
@@ -548,9 +555,9 @@ __global__ void __launch_bounds__(K5_THREADS) k_eval_reduce(int64_t m, const dou
   o.psi = __dadd_rn(__dadd_rn(__dmul_rn(0.5, a), bb), tprox);
   o.psimag = fabs(0.5 * a) + fabs(bb) + fabs(tprox);
   o.res1 = with_grad ? sqrt(c) / (1.0 + nb) : -1.0;
-  o.gd = 0.0;
+  o.gd = gd_src ? *gd_src : 0.0;
   o.r = r_in ? (long long)*r_in : -1;
-  o.pad = 0;
+  o.info = info_src ? (long long)*info_src : 0;
   *out = o;
   *ticket = 0u;  // ready for the next launch (stream-ordered)
 }

@@ -20,13 +20,19 @@ namespace ssn {
 // ---------------------------------------------------------------------------
 // K2: part_vec[b][k] = Σ_{a ∈ chunk b} coef[a] * A[k, J[a]]
 // ---------------------------------------------------------------------------
+// r is read from r_dev when r < 0 (device-resident count, fixed grid); valid[b] (nullable)
+// records whether CTA b had any column, so empty CTAs skip writing their partial row.
 template <int MR>
 __global__ void __launch_bounds__(256) k_gather_axpy(const double* __restrict__ A, int64_t m,
                                                      const int32_t* __restrict__ J, const double* __restrict__ coef,
-                                                     int64_t r, double* __restrict__ part_vec) {
+                                                     int64_t r, const int64_t* __restrict__ r_dev,
+                                                     double* __restrict__ part_vec, int* __restrict__ valid) {
   extern __shared__ double red[];  // 8 x m
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (r < 0) r = *r_dev;
   const int64_t a_lo = (int64_t)blockIdx.x * r / gridDim.x, a_hi = (int64_t)(blockIdx.x + 1) * r / gridDim.x;
+  if (valid && threadIdx.x == 0) valid[blockIdx.x] = a_hi > a_lo;
+  if (valid && a_hi <= a_lo) return;
   double acc[MR];
 #pragma unroll
   for (int t = 0; t < MR; ++t) acc[t] = 0.0;

@@ -80,7 +80,8 @@ int mr_bucket(int64_t m) {
 }
 
 typedef void (*k1_fn)(const K1Params);
-typedef void (*gax_fn)(const double*, int64_t, const int32_t*, const double*, int64_t, double*);
+typedef void (*gax_fn)(const double*, int64_t, const int32_t*, const double*, int64_t, const int64_t*, double*,
+                       int*);
 
 k1_fn k1_for(int mr) {
   switch (mr) {
@@ -216,6 +217,7 @@ struct ssnal_en_problem {
   double* scratch_host = nullptr;
   int* flags = nullptr;
   double* blk = nullptr;       // eval-reduce per-CTA partials
+  int* gax_valid = nullptr;    // device-r gather: CTA had columns
   unsigned* ticket = nullptr;  // eval-reduce last-block counter
   // state
   double lambda_max = 0, nb = 0;
@@ -333,6 +335,7 @@ int allocate(ssnal_en_problem* P) {
   AL(P->flags, 64);
   AL(P->blk, (size_t)((m + 31) / 32) * 3 * 8 + 64);
   AL(P->ticket, 64);
+  AL(P->gax_valid, 4 * 256);
   CK(cudaMemset(P->ticket, 0, 64));
   CK(cudaMallocHost((void**)&P->ev_host, sizeof(EvalOut) * 4));
   CK(cudaMallocHost((void**)&P->scratch_host, 64 * 8));
@@ -436,19 +439,30 @@ int launch_gather(ssnal_en_problem* P, const int32_t* J, const double* coef, int
   int grid = (int)((r + 63) / 64);
   if (grid > P->gax_grid) grid = P->gax_grid;
   if (grid < 1) grid = 1;
-  gax_for(P->MR)<<<grid, 256, (size_t)8 * P->m * 8, P->st>>>(P->A, P->m, J, coef, r, P->part_vec);
+  gax_for(P->MR)<<<grid, 256, (size_t)8 * P->m * 8, P->st>>>(P->A, P->m, J, coef, r, nullptr, P->part_vec, nullptr);
   P->launches++;
   *grid_out = grid;
   CKL();
   return SSNAL_OK;
 }
 
+// Same with r resident on the device (no host round trip): fixed grid, validity flags in gax_valid.
+constexpr int kGatherDevGrid = 128;
+int launch_gather_dev(ssnal_en_problem* P, const int32_t* J, const double* coef, const int64_t* r_dev) {
+  gax_for(P->MR)<<<kGatherDevGrid, 256, (size_t)8 * P->m * 8, P->st>>>(P->A, P->m, J, coef, -1, r_dev, P->part_vec,
+                                                                       P->gax_valid);
+  P->launches++;
+  CKL();
+  return SSNAL_OK;
+}
+
 int launch_eval(ssnal_en_problem* P, const double* y, const Scal& sc, int with_grad, const int* valid, int nparts,
-                double* g_out, const int64_t* r_dev, int slot) {
+                double* g_out, const int64_t* r_dev, int slot, const double* gd_src = nullptr,
+                const int* info_src = nullptr) {
   const unsigned nblk = (unsigned)((P->m + 31) / 32);
   k_eval_reduce<<<nblk, K5_THREADS, 0, P->st>>>(P->m, y, P->b, P->part_vec, valid, nparts, P->part_scal, P->G, sc,
                                                  P->nb, with_grad, g_out, r_dev, P->ev_dev + slot, P->blk,
-                                                 P->ticket);
+                                                 P->ticket, gd_src, info_src);
   P->launches++;
   CKL();
   return SSNAL_OK;
@@ -613,17 +627,10 @@ int solve_core(ssnal_en_problem* P, double l1, double l2, double sigma0, double 
     if ((rc = launch_k1e(P, P->w[wcur], nullptr, 0.0, P->x, sc, nullptr))) return rc;
     // partial scalars of K1e are in part_scal; they are reduced by the eval kernel
     if ((rc = launch_finalize(P, P->J[cur], P->PJ[cur], P->r_dev + cur))) return rc;
-    // r needed on the host to size the gather: read it first
-    CK(cudaMemcpyAsync(P->scratch_host, P->r_dev + cur, 8, cudaMemcpyDeviceToHost, P->st));
-    CK(cudaStreamSynchronize(P->st));
-    int64_t r;
-    memcpy(&r, P->scratch_host, 8);
-    int grid = 0;
-    if (r > 0) {
-      if ((rc = launch_gather(P, P->J[cur], P->PJ[cur], r, &grid))) return rc;
-    }
-    // K1e wrote G scalar partials; the gather wrote `grid` vector partials
-    if ((rc = launch_eval(P, P->y[cur], sc, 1, nullptr, grid, P->g[cur], P->r_dev + cur, 0))) return rc;
+    // ∇ψ needs A_J P_J for the re-thresholded J: gather with r read on the device
+    if ((rc = launch_gather_dev(P, P->J[cur], P->PJ[cur], P->r_dev + cur))) return rc;
+    // K1e wrote G scalar partials; the gather wrote kGatherDevGrid (flagged) vector partials
+    if ((rc = launch_eval(P, P->y[cur], sc, 1, P->gax_valid, kGatherDevGrid, P->g[cur], P->r_dev + cur, 0))) return rc;
     if ((rc = fetch_eval(P, 0, &ev))) return rc;
     S->psi_evals++;
 
@@ -642,15 +649,12 @@ int solve_core(ssnal_en_problem* P, double l1, double l2, double sigma0, double 
       if ((rc = launch_k1(P, P->y[tr], P->x, sc, 1, P->w[wtr]))) return rc;
       S->aty_passes++;
       if ((rc = launch_finalize(P, P->J[tr], P->PJ[tr], P->r_dev + tr))) return rc;
-      if ((rc = launch_eval(P, P->y[tr], sc, 1, P->cta_cnt, P->G, P->g[tr], P->r_dev + tr, 1))) return rc;
-      CK(cudaMemcpyAsync(&P->ev_dev[1].gd, gd_dev, 8, cudaMemcpyDeviceToDevice, P->st));
-      CK(cudaMemcpyAsync(P->scratch + 8, P->info, 4, cudaMemcpyDeviceToDevice, P->st));
-      CK(cudaMemcpyAsync(P->scratch_host + 8, P->scratch + 8, 8, cudaMemcpyDeviceToHost, P->st));
+      if ((rc = launch_eval(P, P->y[tr], sc, 1, P->cta_cnt, P->G, P->g[tr], P->r_dev + tr, 1, gd_dev,
+                            br > 0 ? P->info : nullptr)))
+        return rc;
       if ((rc = fetch_eval(P, 1, &evt))) return rc;
       S->psi_evals++;
-      int info_h = 0;
-      memcpy(&info_h, P->scratch_host + 8, 4);
-      if (br > 0 && info_h != 0) {
+      if (br > 0 && evt.info != 0) {
         numeric = 1;
         set_err("Cholesky pivot not positive (branch %d, r=%lld)", br, (long long)ev.r);
         break;
@@ -695,13 +699,10 @@ int solve_core(ssnal_en_problem* P, double l1, double l2, double sigma0, double 
         cur = tr;
         wcur = wbt;  // materialised w + s (w1 − w)
         // ∇ψ at the accepted point needs A_J P_J for the re-thresholded J (K2)
-        const int64_t r2 = evt.r;
-        int grid2 = 0;
-        if (r2 > 0) {
-          if ((rc = launch_gather(P, P->J[cur], P->PJ[cur], r2, &grid2))) return rc;
-        }
+        if ((rc = launch_gather_dev(P, P->J[cur], P->PJ[cur], P->r_dev + cur))) return rc;
         // scalar partials in part_scal still belong to the accepted K1e launch
-        if ((rc = launch_eval(P, P->y[cur], sc, 1, nullptr, grid2, P->g[cur], P->r_dev + cur, 0))) return rc;
+        if ((rc = launch_eval(P, P->y[cur], sc, 1, P->gax_valid, kGatherDevGrid, P->g[cur], P->r_dev + cur, 0)))
+          return rc;
         if ((rc = fetch_eval(P, 0, &ev))) return rc;
       }
       S->newton_iters++;
@@ -840,6 +841,7 @@ static void destroy_bufs(ssnal_en_problem* P) {
   cudaFree(P->flags);
   cudaFree(P->blk);
   cudaFree(P->ticket);
+  cudaFree(P->gax_valid);
   if (P->ev_host) cudaFreeHost(P->ev_host);
   if (P->scratch_host) cudaFreeHost(P->scratch_host);
   for (auto e : P->ev_pool) cudaEventDestroy(e);
