@@ -266,30 +266,37 @@ SSN_DEV void load_tile_rows(const double* M, int ld, int r0, int c0, int nr, int
   for (int p = 0; p < CHT; ++p) S[lane * TLD + p] = v[p];
 }
 
-// Factor the diagonal tile held in smem T (32 × TLD, identity-padded beyond kn; rows up to
-// kn may include one rhs row at index kn) with 4 warps (128 threads, named barrier 2).
-// Warp w owns columns [8w, 8w+8); lane = row.  Then warp 0 computes W = L_diag⁻¹ into Wout.
-SSN_DEV void chol_diag_4w(double* T, int kn, int t128, int* info, double* colbuf, double* Wout) {
+// CTA-0 look-ahead: factor the diagonal tile at n0 (kn columns, nrow rows incl. possibly the
+// rhs row) with the 4 warps of the diagonal team (t128 ∈ [0,128), named barrier 2) and store L
+// into M.  Warp w owns columns [8w, 8w+8) of every row (lane = row) and keeps a replica of its
+// 8 diagonal entries, updated with the same fma as the owning lane (bitwise equal), so the
+// owner of pivot j has it locally: per pivot only the scaled column goes through smem
+// (double-buffered colbuf) and one 128-thread barrier.  1/√pivot by rsqrt.
+SSN_DEV void diag_block(double* M, int ld, int N, int NR, int n0, int t128, int* info, double* colbuf,
+                        double* invg) {
   const int w = t128 >> 5, lane = t128 & 31;
-  double a[8];
+  const int kn = min(CHT, N - n0), nrow = min(CHT, NR - n0);
+  double a[8], dgw[8];
 #pragma unroll
-  for (int q = 0; q < 8; ++q) a[q] = T[lane * TLD + 8 * w + q];
+  for (int q = 0; q < 8; ++q) {
+    const int c = 8 * w + q;
+    a[q] = (lane < nrow && c < kn) ? __ldcg(M + (int64_t)(n0 + lane) + (int64_t)(n0 + c) * ld) : (lane == c ? 1.0 : 0.0);
+    dgw[q] = (c < kn) ? __ldcg(M + (int64_t)(n0 + c) * (ld + 1)) : 1.0;
+  }
   bool bad = false;
 #pragma unroll
   for (int j = 0; j < CHT; ++j) {
-    double* cb = colbuf + (j & 1) * 40;
+    double* cb = colbuf + (j & 1) * 32;
     if (w == (j >> 3)) {  // warp-uniform: owner of column j
       const int jl = j & 7;
-      if (lane == j) cb[33] = a[jl];
-      __syncwarp();
-      double ajj = cb[33];
-      const bool pv = j < kn;
-      bad |= pv && !(ajj > 0.0);
-      ajj = (pv && ajj > 0.0) ? ajj : 1.0;
-      const double d = sqrt(ajj);
-      const double lij = (lane > j) ? a[jl] / d : (lane == j ? d : 0.0);
+      double ajj = dgw[jl];
+      bad |= (j < kn) && !(ajj > 0.0);
+      ajj = (j < kn && ajj > 0.0) ? ajj : 1.0;
+      const double inv = rsqrt(ajj);
+      const double lij = (lane > j) ? a[jl] * inv : (lane == j ? ajj * inv : 0.0);
       if (lane >= j) a[jl] = lij;
       cb[lane] = lij;
+      if (lane == j) invg[j] = inv;  // 1/L_jj (= rsqrt of the pivot) for the block inverse
     }
     asm volatile("bar.sync 2, 128;" ::: "memory");
     const double li = cb[lane];
@@ -298,147 +305,50 @@ SSN_DEV void chol_diag_4w(double* T, int kn, int t128, int* info, double* colbuf
       const int c = 8 * w + q;
       const double lc = (c > j) ? cb[c] : 0.0;
       a[q] = fma(-li, lc, a[q]);
+      dgw[q] = fma(-lc, lc, dgw[q]);
     }
-  }
-  if (bad && lane == 0) atomicExch(info, 1);
-#pragma unroll
-  for (int q = 0; q < 8; ++q) T[lane * TLD + 8 * w + q] = a[q];
-  asm volatile("bar.sync 2, 128;" ::: "memory");
-  if (w == 0) {  // W = L⁻¹ (lane = column), forward substitution with 4 partial sums
-    double x[CHT];
-#pragma unroll
-    for (int i = 0; i < CHT; ++i) {
-      double s0 = (i == lane) ? 1.0 : 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-#pragma unroll
-      for (int p = 0; p < i; ++p) {
-        const double v = T[i * TLD + p] * x[p];
-        if ((p & 3) == 0) s0 -= v;
-        else if ((p & 3) == 1) s1 -= v;
-        else if ((p & 3) == 2) s2 -= v;
-        else s3 -= v;
-      }
-      x[i] = ((s0 + s1) + (s2 + s3)) / T[i * TLD + i];
-    }
-#pragma unroll
-    for (int i = 0; i < CHT; ++i) Wout[i * CHT + lane] = (i < kn && lane < kn) ? x[i] : (i == lane ? 1.0 : 0.0);
-  }
-}
-
-// Single-warp variant (lane = row in registers; the scaled column is broadcast through smem).
-SSN_DEV void chol_diag_1w(double* T, int kn, int lane, int* info, double* colbuf, double* Wout) {
-  double a[CHT];
-#pragma unroll
-  for (int c = 0; c < CHT; ++c) a[c] = T[lane * TLD + c];
-  bool bad = false;
-#pragma unroll
-  for (int j = 0; j < CHT; ++j) {
-    double ajj = T[j * TLD + j];  // pivot row j, updated in smem by lane j below
-    const bool pv = j < kn;
-    bad |= pv && !(ajj > 0.0);
-    ajj = (pv && ajj > 0.0) ? ajj : 1.0;
-    const double d = sqrt(ajj);
-    const double inv = 1.0 / d;
-    const double lij = (lane > j) ? a[j] * inv : (lane == j ? d : 0.0);
-    if (lane >= j) a[j] = lij;
-    colbuf[lane] = lij;
-    __syncwarp();
-    double lc[CHT];
-#pragma unroll
-    for (int c = j + 1; c < CHT; ++c) lc[c] = colbuf[c];
-#pragma unroll
-    for (int c = j + 1; c < CHT; ++c) a[c] = fma(-lij, lc[c], a[c]);
-    if (j + 1 < CHT && lane == j + 1) T[(j + 1) * TLD + j + 1] = a[j + 1];
-    __syncwarp();
-  }
-  if (bad && lane == 0) atomicExch(info, 1);
-#pragma unroll
-  for (int c = 0; c < CHT; ++c) T[lane * TLD + c] = a[c];
-  __syncwarp();
-  double x[CHT];  // W = L⁻¹ restricted to the kn × kn factor (lane = column)
-#pragma unroll
-  for (int i = 0; i < CHT; ++i) {
-    double s0 = (i == lane) ? 1.0 : 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-#pragma unroll
-    for (int p = 0; p < i; ++p) {
-      const double v = T[i * TLD + p] * x[p];
-      if ((p & 3) == 0) s0 -= v;
-      else if ((p & 3) == 1) s1 -= v;
-      else if ((p & 3) == 2) s2 -= v;
-      else s3 -= v;
-    }
-    x[i] = ((s0 + s1) + (s2 + s3)) / T[i * TLD + i];
-  }
-#pragma unroll
-  for (int i = 0; i < CHT; ++i) Wout[i * CHT + lane] = (i < kn && lane < kn) ? x[i] : (i == lane ? 1.0 : 0.0);
-}
-
-// CTA-0 look-ahead: factor the diagonal tile at n0 (kn columns, nrow rows incl. possibly the
-// rhs row) with warp 0 and store L (into M) and W = L⁻¹ (into Wout).  Latency-oriented:
-// lane = row in registers, each lane keeps a replica of the diagonal (updated with the same
-// fma as the owning lane, so bitwise equal) so the next pivot is local; 1/√pivot by rsqrt;
-// only the scaled column is broadcast (smem colbuf); the inverse uses the stored reciprocals.
-SSN_DEV void diag_block(double* M, int ld, int N, int NR, int n0, int t128, int* info, double* T, double* colbuf,
-                        double* Wout) {
-  if (t128 >= 32) return;
-  const int lane = t128;
-  const int kn = min(CHT, N - n0), nrow = min(CHT, NR - n0);
-  double a[CHT], dg[CHT];
-#pragma unroll
-  for (int c = 0; c < CHT; ++c)
-    a[c] = (lane < nrow && c < kn) ? __ldcg(M + (int64_t)(n0 + lane) + (int64_t)(n0 + c) * ld) : (lane == c ? 1.0 : 0.0);
-#pragma unroll
-  for (int c = 0; c < CHT; ++c) dg[c] = (c < kn) ? __ldcg(M + (int64_t)(n0 + c) * (ld + 1)) : 1.0;
-  double* invs = colbuf + 40;  // 1/L_jj
-  bool bad = false;
-#pragma unroll
-  for (int j = 0; j < CHT; ++j) {
-    double ajj = dg[j];
-    const bool pv = j < kn;
-    bad |= pv && !(ajj > 0.0);
-    ajj = (pv && ajj > 0.0) ? ajj : 1.0;
-    const double inv = rsqrt(ajj);
-    const double d = ajj * inv;
-    const double lij = (lane > j) ? a[j] * inv : (lane == j ? d : 0.0);
-    if (lane >= j) a[j] = lij;
-    colbuf[lane] = lij;
-    if (lane == 0) invs[j] = 1.0 / d;
-    __syncwarp();
-    double lc[CHT];
-#pragma unroll
-    for (int c = j + 1; c < CHT; ++c) lc[c] = colbuf[c];
-    if (j + 1 < CHT) dg[j + 1] = fma(-lc[j + 1], lc[j + 1], dg[j + 1]);  // next pivot first
-#pragma unroll
-    for (int c = j + 1; c < CHT; ++c) {
-      a[c] = fma(-lij, lc[c], a[c]);
-      if (c > j + 1) dg[c] = fma(-lc[c], lc[c], dg[c]);
-    }
-    __syncwarp();
   }
   if (bad && lane == 0) atomicExch(info, 1);
   if (lane < nrow) {
 #pragma unroll
-    for (int c = 0; c < CHT; ++c)
-      if (c < kn && c <= lane) M[(int64_t)(n0 + lane) + (int64_t)(n0 + c) * ld] = a[c];
+    for (int q = 0; q < 8; ++q) {
+      const int c = 8 * w + q;
+      if (c < kn && c <= lane) M[(int64_t)(n0 + lane) + (int64_t)(n0 + c) * ld] = a[q];
+    }
   }
+}
+
+// W = L_bb⁻¹ for diagonal block bb (lower, identity-padded beyond bn); one warp.  Rows are
+// loaded lane = row (coalesced per column), the solve runs lane = column with the stored
+// reciprocals invg[i] = 1/L_ii (no divisions on the chain).
+SSN_DEV void inv_block_warp(const double* M, int ld, int b0, int bn, double* S, const double* invg, double* W,
+                            int lane) {
+  double v[CHT];
 #pragma unroll
-  for (int c = 0; c < CHT; ++c) T[lane * TLD + c] = a[c];
+  for (int p = 0; p < CHT; ++p)
+    v[p] = (lane < bn && p < bn && p <= lane) ? __ldcg(M + (int64_t)(b0 + lane) + (int64_t)(b0 + p) * ld)
+                                              : (lane == p ? 1.0 : 0.0);
+  const double ri = (lane < bn) ? __ldcg(invg + lane) : 1.0;
+#pragma unroll
+  for (int p = 0; p < CHT; ++p) S[lane * TLD + p] = v[p];  // S[i][p] = L[i][p]
+  S[CHT * TLD + lane] = ri;
   __syncwarp();
-  double x[CHT];  // W = L⁻¹ restricted to the kn × kn factor (lane = column)
+  double x[CHT];
 #pragma unroll
   for (int i = 0; i < CHT; ++i) {
     double s0 = (i == lane) ? 1.0 : 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
 #pragma unroll
     for (int p = 0; p < i; ++p) {
-      const double v = T[i * TLD + p] * x[p];
-      if ((p & 3) == 0) s0 -= v;
-      else if ((p & 3) == 1) s1 -= v;
-      else if ((p & 3) == 2) s2 -= v;
-      else s3 -= v;
+      const double t = S[i * TLD + p] * x[p];
+      if ((p & 3) == 0) s0 -= t;
+      else if ((p & 3) == 1) s1 -= t;
+      else if ((p & 3) == 2) s2 -= t;
+      else s3 -= t;
     }
-    x[i] = ((s0 + s1) + (s2 + s3)) * invs[i];
+    x[i] = ((s0 + s1) + (s2 + s3)) * S[CHT * TLD + i];
   }
 #pragma unroll
-  for (int i = 0; i < CHT; ++i) Wout[i * CHT + lane] = (i < kn && lane < kn) ? x[i] : (i == lane ? 1.0 : 0.0);
+  for (int i = 0; i < CHT; ++i) W[i * CHT + lane] = x[i];
   __syncwarp();
 }
 
@@ -453,55 +363,71 @@ __global__ void __launch_bounds__(256, 1) k_chol_cluster(double* M, int N, int l
   double* SA = dsm + (size_t)warp * 2 * CHT * TLD;  // per-warp operand tiles
   double* SB = SA + CHT * TLD;
   double* T = dsm + (size_t)8 * 2 * CHT * TLD;      // CTA-0 diagonal tile
-  double* colbuf = T + CHT * TLD;                   // 80 doubles (col broadcast + reciprocals)
+  double* colbuf = T + CHT * TLD;                   // 80 doubles (column broadcast / reciprocals)
   const int NR = N + 1;
   const int ntc = (N + CHT - 1) / CHT, ntr = (NR + CHT - 1) / CHT;
   const int NWg = CS * 8;
   const int gw = rank + CS * warp;
   // worker warps for phase C: all warps of CTAs 1..CS-1 (CTA 0 owns the look-ahead diagonal, so
   // its factorisation does not compete for issue slots); with CS = 1 CTA 0's warps 4-7 work too.
+  // CTA 1's warp 0 (CTA 0's warp 4 when CS = 1) computes the block inverse W_k in phase C.
   const bool diag_team = (rank == 0 && warp < 4);
-  const int NWw = (CS > 1) ? NWg - 8 : 4;
-  const int wid = (CS > 1) ? ((rank == 0) ? -1 : (rank - 1) * 8 + warp) : warp - 4;
+  const bool inv_warp = (CS > 1) ? (rank == 1 && warp == 0) : (warp == 4);
+  const int NWw = (CS > 1) ? NWg - 9 : 3;
+  const int wid = (CS > 1) ? ((rank == 0 || inv_warp) ? -1 : (rank - 1) * 8 + warp - 1)
+                           : (warp > 4 ? warp - 5 : -1);
 #ifdef CHOL_PROBE
 #define STAMP(i) do { if (rank == 0 && tid == 0 && (i) < 64) { unsigned long long t_; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); g_t[i] = t_; } } while (0)
 #else
 #define STAMP(i) do {} while (0)
 #endif
   STAMP(0);
-  if (diag_team) diag_block(M, ld, N, NR, 0, tid, info, T, colbuf, Winv);
+  double* invg = Winv + (size_t)ntc * CHT * CHT;  // per-block reciprocals 1/L_jj (ntc × 32)
+  if (diag_team) diag_block(M, ld, N, NR, 0, tid, info, colbuf, invg);
   cl.sync();
   STAMP(1);
   for (int k = 0; k < ntc; ++k) {
     const int k0 = k * CHT;
     const int kn = min(CHT, N - k0);
-    // ---- B: L_ik = A_ik W_kᵀ for row tiles i > k ----
+    // ---- B: L_ik = A_ik L_kk^{-T} for row tiles i > k (substitution; warp per tile) ----
     const int nB = ntr - k - 1;
-    for (int q = gw; q < nB; q += NWg) {
-      const int i0 = (k + 1 + q) * CHT;
-      load_tile_rows(M, ld, i0, k0, NR, k0 + kn, SA, lane);
-      const double* Wk = Winv + (size_t)k * CHT * CHT;
-      {
-        double v[CHT];
+    if (nB > 0 && rank < nB) {
+      {  // T[c][p] = L_kk[c][p] (identity-padded); 4 independent loads per thread
+        double v[4];
 #pragma unroll
-        for (int p = 0; p < CHT; ++p) v[p] = __ldcg(Wk + lane * CHT + p);  // SB[c][p] = W[c][p]
+        for (int u = 0; u < 4; ++u) {
+          const int e = tid + 256 * u, c = e >> 5, p = e & 31;
+          v[u] = (c < kn && p < kn && p <= c) ? __ldcg(M + (int64_t)(k0 + c) + (int64_t)(k0 + p) * ld)
+                                              : (c == p ? 1.0 : 0.0);
+        }
 #pragma unroll
-        for (int p = 0; p < CHT; ++p) SB[lane * TLD + p] = v[p];
+        for (int u = 0; u < 4; ++u) {
+          const int e = tid + 256 * u;
+          T[(e >> 5) * TLD + (e & 31)] = v[u];
+        }
       }
-      __syncwarp();
-      double acc[4][4][2] = {};
-      tile_mma(SA, SB, acc, 1.0, lane);
-      const int g = lane >> 2, t = lane & 3;
+      __syncthreads();
+      if (tid < CHT) colbuf[tid] = 1.0 / T[tid * TLD + tid];
+      __syncthreads();
+      for (int q = gw; q < nB; q += NWg) {
+        const int row = (k + 1 + q) * CHT + lane;
+        double x[CHT];
 #pragma unroll
-      for (int rb = 0; rb < 4; ++rb)
+        for (int c = 0; c < CHT; ++c)
+          x[c] = (row < NR && c < kn) ? __ldcg(M + (int64_t)row + (int64_t)(k0 + c) * ld) : 0.0;
+        // right-looking within the row: x_c final after all p < c are applied
 #pragma unroll
-        for (int cb = 0; cb < 4; ++cb)
+        for (int c = 0; c < CHT; ++c) {
+          x[c] *= colbuf[c];
 #pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int r = i0 + 8 * rb + g, c = 8 * cb + 2 * t + e;
-            if (r < NR && c < kn) M[(int64_t)r + (int64_t)(k0 + c) * ld] = acc[rb][cb][e];
-          }
-      __syncwarp();
+          for (int c2 = c + 1; c2 < CHT; ++c2) x[c2] = fma(-x[c], T[c2 * TLD + c], x[c2]);
+        }
+        if (row < NR) {
+#pragma unroll
+          for (int c = 0; c < CHT; ++c)
+            if (c < kn) M[(int64_t)row + (int64_t)(k0 + c) * ld] = x[c];
+        }
+      }
     }
     cl.sync();
     STAMP(2 + 2 * k);
@@ -550,57 +476,104 @@ __global__ void __launch_bounds__(256, 1) k_chol_cluster(double* M, int N, int l
     };
     if (diag_team) {
       if (k == 0) STAMP(50);
-      if (warp == 0) do_tile(0);  // tile (k+1, k+1)
+      {  // tile (k+1, k+1), split over the 4 team warps: warp w updates rows 8w..8w+7
+        const int d0 = (k + 1) * CHT;
+        const int g = lane >> 2, t = lane & 3;
+        const int r = d0 + 8 * warp + g;
+        double af[8], bf[4][8], acc[4][2];
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const int p = k0 + 4 * kk + t;
+          af[kk] = (r < NR && 4 * kk + t < kn) ? -__ldcg(M + (int64_t)r + (int64_t)p * ld) : 0.0;
+#pragma unroll
+          for (int cb = 0; cb < 4; ++cb) {
+            const int rc = d0 + 8 * cb + g;
+            bf[cb][kk] = (rc < N && 4 * kk + t < kn) ? __ldcg(M + (int64_t)rc + (int64_t)p * ld) : 0.0;
+          }
+        }
+#pragma unroll
+        for (int cb = 0; cb < 4; ++cb)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int c = d0 + 8 * cb + 2 * t + e;
+            acc[cb][e] = (r < NR && c < N) ? __ldcg(M + (int64_t)r + (int64_t)c * ld) : 0.0;
+          }
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+#pragma unroll
+          for (int cb = 0; cb < 4; ++cb) dmma(acc[cb], af[kk], bf[cb][kk]);
+#pragma unroll
+        for (int cb = 0; cb < 4; ++cb)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int cl_ = 8 * cb + 2 * t + e, rl = 8 * warp + g;
+            if (r < NR && d0 + cl_ < N && cl_ <= rl) M[(int64_t)r + (int64_t)(d0 + cl_) * ld] = acc[cb][e];
+          }
+      }
       if (k == 0) STAMP(51);
       asm volatile("bar.sync 2, 128;" ::: "memory");
       __threadfence_block();
-      diag_block(M, ld, N, NR, (k + 1) * CHT, tid, info, T, colbuf, Winv + (size_t)(k + 1) * CHT * CHT);
+      diag_block(M, ld, N, NR, (k + 1) * CHT, tid, info, colbuf, invg + (size_t)(k + 1) * CHT);
       if (k == 0) STAMP(52);
     } else if (wid >= 0) {
       for (int q = 1 + wid; q < npairs; q += NWw) do_tile(q);
+    } else if (inv_warp) {  // W_k = L_kk⁻¹ for the backward solve, off the critical path
+      inv_block_warp(M, ld, k0, kn, SA, invg + (size_t)k * CHT, Winv + (size_t)k * CHT * CHT, lane);
     }
     cl.sync();
     STAMP(3 + 2 * k);
   }
   STAMP(40);
   if (rank != 0) return;
-  // ---- backward substitution v = L⁻ᵀ z by CTA 0 (z = row N) ----
-  double* zv = dsm;  // N doubles (N ≤ 1024 < 16·32·33)
+  if (warp == 0) {  // W of the last diagonal block (its panel has no phase C)
+    const int kl = ntc - 1;
+    inv_block_warp(M, ld, kl * CHT, min(CHT, N - kl * CHT), SA, invg + (size_t)kl * CHT,
+                   Winv + (size_t)kl * CHT * CHT, lane);
+  }
+  __syncthreads();
+  STAMP(41);
+  // ---- backward substitution v = L⁻ᵀ z by CTA 0 (z = row N), left-looking per block:
+  //      v_b = W_bᵀ (z_b − Σ_{i below block b} L[i][b-block]ᵀ v_i) ----
+  double* zv = dsm;                 // N doubles (N ≤ 1024)
+  double* sbuf = dsm + 1024;        // 32 doubles
   for (int i = tid; i < N; i += blockDim.x) zv[i] = __ldcg(M + (int64_t)N + (int64_t)i * ld);
   __syncthreads();
   for (int kb = ntc - 1; kb >= 0; --kb) {
-    const int b0 = kb * CHT, bn = min(CHT, N - b0);
-    if (warp == 0) {  // v_b = W_bᵀ z_b  (W identity-padded beyond bn)
+    const int b0 = kb * CHT, bn = min(CHT, N - b0), i_lo = b0 + bn;
+    double wv[CHT];
+    if (warp == 0) {  // issue the W_b loads first (independent of v)
       const double* Wb = Winv + (size_t)kb * CHT * CHT;
-      double wv[CHT];
 #pragma unroll
       for (int i = 0; i < CHT; ++i) wv[i] = __ldg(Wb + i * CHT + lane);
+    }
+    // s_j = Σ_{i ≥ i_lo} L[i][b0+j] v_i: warp w takes columns 4w..4w+3, lanes run down the rows
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 4
+    for (int i = i_lo + lane; i < N; i += 32) {
+      const double vi = zv[i];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int j = 4 * warp + q;
+        if (j < bn) acc[q] = fma(__ldg(M + (int64_t)i + (int64_t)(b0 + j) * ld), vi, acc[q]);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      acc[q] = warp_allsum(acc[q]);
+      if (lane == 0) sbuf[4 * warp + q] = acc[q];
+    }
+    __syncthreads();
+    if (warp == 0) {
+      const double t = (lane < bn) ? zv[b0 + lane] - sbuf[lane] : 0.0;
       double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
 #pragma unroll
       for (int i = 0; i < CHT; i += 4) {
-        v0 = fma(wv[i], (i < bn) ? zv[b0 + i] : 0.0, v0);
-        v1 = fma(wv[i + 1], (i + 1 < bn) ? zv[b0 + i + 1] : 0.0, v1);
-        v2 = fma(wv[i + 2], (i + 2 < bn) ? zv[b0 + i + 2] : 0.0, v2);
-        v3 = fma(wv[i + 3], (i + 3 < bn) ? zv[b0 + i + 3] : 0.0, v3);
+        v0 = fma(wv[i], __shfl_sync(0xffffffffu, t, i), v0);
+        v1 = fma(wv[i + 1], __shfl_sync(0xffffffffu, t, i + 1), v1);
+        v2 = fma(wv[i + 2], __shfl_sync(0xffffffffu, t, i + 2), v2);
+        v3 = fma(wv[i + 3], __shfl_sync(0xffffffffu, t, i + 3), v3);
       }
-      __syncwarp();
       if (lane < bn) zv[b0 + lane] = (v0 + v1) + (v2 + v3);
-    }
-    __syncthreads();
-    for (int p = tid; p < b0; p += blockDim.x) {  // z_p −= Σ_{c<bn} L[b0+c][p] v_c
-      const double* Lc = M + (int64_t)p * ld + b0;
-      double lv[CHT];
-#pragma unroll
-      for (int c = 0; c < CHT; ++c) lv[c] = (c < bn) ? __ldg(Lc + c) : 0.0;  // L1: no stale lines (.cg before)
-      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-#pragma unroll
-      for (int c = 0; c < CHT; c += 4) {
-        s0 = fma(lv[c], (c < bn) ? zv[b0 + c] : 0.0, s0);
-        s1 = fma(lv[c + 1], (c + 1 < bn) ? zv[b0 + c + 1] : 0.0, s1);
-        s2 = fma(lv[c + 2], (c + 2 < bn) ? zv[b0 + c + 2] : 0.0, s2);
-        s3 = fma(lv[c + 3], (c + 3 < bn) ? zv[b0 + c + 3] : 0.0, s3);
-      }
-      zv[p] -= (s0 + s1) + (s2 + s3);
     }
     __syncthreads();
   }

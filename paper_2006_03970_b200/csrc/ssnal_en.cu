@@ -326,7 +326,7 @@ int allocate(ssnal_en_problem* P) {
   AL(P->u, m * 8);
   AL(P->tmpm, m * 8);
   AL(P->Mmat, (size_t)(m + 1) * (m + 1) * 8);
-  AL(P->Winv, (size_t)((m + 31) / 32) * 32 * 32 * 8);
+  AL(P->Winv, (size_t)((m + 31) / 32) * 33 * 32 * 8);  // block inverses + reciprocals
   P->W_splits = 16;
   AL(P->W, (size_t)P->W_splits * m * m * 8);
   AL(P->info, 64);

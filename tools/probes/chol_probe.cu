@@ -16,7 +16,7 @@ __global__ void k_diag_only(double* M, int ld, int N, int* info, unsigned long l
   unsigned long long t0; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
   long long c0 = clock64();
   __shared__ double T[32 * 33 + 80];
-  if (threadIdx.x < 128) diag_block(M, ld, N, N + 1, 0, threadIdx.x, info, T, T + 32 * 33, M + 0 * 0 + (size_t)ld * N + 64);
+  if (threadIdx.x < 128) diag_block(M, ld, N, N + 1, 0, threadIdx.x, info, T, T + 64);
   __syncthreads();
   unsigned long long t1; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
   long long c1 = clock64();
@@ -43,7 +43,7 @@ int main() {
     for (int j = 0; j < N; ++j) for (int i = 0; i < ld; ++i) h[i + (size_t)j * ld] = (i == j) ? N + 1.0 : ((i < N) ? 0.01 * ((i * 7 + j * 13) % 11) : 1.0);
     for (int j = 0; j < N; ++j) for (int i = 0; i < N; ++i) h[i + (size_t)j * ld] = h[(i > j ? i : j) + (size_t)(i > j ? j : i) * ld];
     double *dM, *dout, *dW, *dd; int* info; unsigned long long* dt;
-    cudaMalloc(&dM, (h.size() + 4096) * 8); cudaMalloc(&dout, N * 8); cudaMalloc(&dW, 32 * 32 * 8 * ((N + 31) / 32)); cudaMalloc(&info, 4); cudaMalloc(&dt, 64 * 8); cudaMalloc(&dd, 8);
+    cudaMalloc(&dM, (h.size() + 4096) * 8); cudaMalloc(&dout, N * 8); cudaMalloc(&dW, 33 * 32 * 8 * ((N + 31) / 32)); cudaMalloc(&info, 4); cudaMalloc(&dt, 64 * 8); cudaMalloc(&dd, 8);
     size_t smem = kCholSmem;
     cudaFuncSetAttribute(k_chol_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(k_chol_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
