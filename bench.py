@@ -100,6 +100,19 @@ def lambdas(cfg, lmax_l1, c):
     return c * cfg.alpha * lmax, c * (1 - cfg.alpha) * lmax
 
 
+def max_over_ranks(v: float, device: str = "cuda") -> float:
+    """Max of a per-rank float over the process group (identity without one).  Works with
+    NCCL (device='cuda') and gloo (device='cpu')."""
+    import torch
+    import torch.distributed as dist
+
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(v)
+    t = torch.tensor([float(v)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def k1_bytes(m, n):
     """Algorithmic bytes of one fused K1 launch: A once (8mn), x read + w write (16n), y (8m)."""
     return 8 * m * n + 16 * n + 8 * m
@@ -171,16 +184,12 @@ def bench_ours(args, rank, world, local_rank):
         dist.barrier()
     P.set_option("time_k1", 0)
     elapsed = ev0.elapsed_time(ev1) * 1e-3
-    t_step = elapsed / args.steps
-    if world > 1:
-        t = torch.tensor([t_step], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        t_step = float(t.item())
+    t_step = max_over_ranks(elapsed / args.steps)
 
     # ---- e2e: through the C-ABI with HOST buffers (create + H2D + solves + D2H) ----
     A_host = None
     e2e = None
-    if rank == 0 or world > 1:
+    if not args.no_e2e:
         A_host = torch.empty((n, m), dtype=torch.float64, pin_memory=True)
         A_host.copy_(dA.cpu())
         A_np = A_host.numpy()
@@ -204,11 +213,7 @@ def bench_ours(args, rank, world, local_rank):
             if it > 0:  # first iteration is the e2e warm-up
                 e2e_times.append(dt)
             h2d, d2h = hb, db_
-        e2e_t = statistics.median(e2e_times)
-        if world > 1:
-            t = torch.tensor([e2e_t], dtype=torch.float64, device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_t = float(t.item())
+        e2e_t = max_over_ranks(statistics.median(e2e_times))
         e2e = {"value": e2e_t, "unit": "s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
 
     peak, peak_src = _peaks()
@@ -363,6 +368,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg2", choices=list(synth.CONFIGS))
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg (40 GB configs)")
     ap.add_argument("--sweep", action="store_true", help="K1 bandwidth sweep instead of the TTS bench")
     ap.add_argument("--sweep-n", default="100000,200000,500000,1000000,2000000,5000000,10000000")
     ap.add_argument("--sweep-reps", type=int, default=20)

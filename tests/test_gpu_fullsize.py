@@ -1,0 +1,160 @@
+"""Full-size checks at the BASELINE.json shapes (cfg3: 4 GB, cfg4: 12.8 GB, cfg5: 40 GB of A).
+
+A is generated directly in HBM by synth's device generator; any column can be regenerated
+bit-identically on the host, so the oracle checks GPU outputs one by one on sampled columns:
+  * device generator == host generator (bitwise) on sampled columns;
+  * K1 at full size: w_i on sampled and all active columns (reading R21), J membership;
+  * solves at full size: convergence, the KKT inclusion Aᵀ(b − Ax) − λ2x ∈ λ1∂‖x‖₁ on every
+    support column and 20 000 sampled columns, the duality gap, x = 0 above λmax;
+  * cfg3 additionally against a full oracle solve on the host (all three c values).
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from gpu_util import aty_errors, cuda_ok, solution_parity
+
+pytestmark = pytest.mark.gpu
+
+if cuda_ok():
+    import torch
+    from paper_2006_03970_b200 import Problem
+
+_cache = {}
+
+
+def device_problem(name):
+    """(cfg, dA tensor, b host, Problem) for a full-size config, built once per module."""
+    if name in _cache:
+        return _cache[name]
+    for k in list(_cache):  # keep one full-size A resident at a time
+        _cache[k][3].close()
+        del _cache[k]
+    torch.cuda.empty_cache()
+    cfg = synth.CONFIGS[name]
+    st = torch.cuda.current_stream()
+    dA = torch.empty((cfg.n, cfg.m), dtype=torch.float64, device="cuda")
+    synth.fill_device(cfg, dA.data_ptr(), st.cuda_stream)
+    b, _ = synth.response(cfg)
+    db = torch.from_numpy(b).cuda()
+    P = Problem.from_device(dA.data_ptr(), db.data_ptr(), cfg.m, cfg.n, st.cuda_stream, keep=(dA, db))
+    _cache[name] = (cfg, dA, b, P)
+    return _cache[name]
+
+
+def sample_idx(n, count, seed):
+    u = synth.uniforms(seed, 31, count)
+    idx = np.unique(np.minimum((u * n).astype(np.int64), n - 1))
+    return np.unique(np.concatenate([idx, [0, n - 1]]))
+
+
+def lambdas(cfg, lmax_l1, c):
+    lmax = lmax_l1 / cfg.alpha
+    return c * cfg.alpha * lmax, c * (1 - cfg.alpha) * lmax
+
+
+@pytest.mark.parametrize("name", ["cfg2", "cfg3", "cfg4", "cfg5"])
+def test_device_generator_bitwise(name):
+    cfg, dA, b, P = device_problem(name)
+    idx = sample_idx(cfg.n, 64, 1)
+    dev = dA[torch.from_numpy(idx).cuda()].cpu().numpy()
+    assert np.array_equal(dev, synth.columns(cfg, idx))
+
+
+@pytest.mark.parametrize("name", ["cfg3", "cfg4", "cfg5"])
+def test_k1_fullsize_sampled(name):
+    cfg, dA, b, P = device_problem(name)
+    m, n = cfg.m, cfg.n
+    y = synth.normals(7, 1, m)
+    x = np.zeros(n)
+    nz = sample_idx(n, 50, 2)
+    x[nz] = synth.normals(7, 2, len(nz))
+    sigma, l2 = 1.0, 0.3
+    dy, dx = torch.from_numpy(y).cuda(), torch.from_numpy(x).cuda()
+    w = torch.empty(n, dtype=torch.float64, device="cuda")
+    J = torch.empty(n, dtype=torch.int32, device="cuda")
+    PJ = torch.empty(n, dtype=torch.float64, device="cuda")
+    # λ1 at the (1 − 1e-4) quantile of |Aᵀy| (from a first pass) → r ≈ 1e-4 n
+    P.aty_fused(dy.data_ptr(), dx.data_ptr(), sigma, 1e30, l2, w.data_ptr(), J.data_ptr(), PJ.data_ptr())
+    l1 = float(torch.quantile(w.abs()[:16_000_000].float(), 1 - 1e-4).item())
+    r, part = P.aty_fused(dy.data_ptr(), dx.data_ptr(), sigma, l1, l2, w.data_ptr(), J.data_ptr(), PJ.data_ptr())
+    torch.cuda.synchronize()
+    Jg = J[:r].cpu().numpy().astype(np.int64)
+    assert r > 0 and np.all(np.diff(Jg) > 0)
+    idx = np.unique(np.concatenate([sample_idx(n, 4096, 3), Jg]))
+    cols = synth.columns(cfg, idx)
+    w_cpu = cols @ y  # (k, m) @ (m,): oracle-side products of regenerated columns
+    w_gpu = w[torch.from_numpy(idx).cuda()].cpu().numpy()
+    e1, e2 = aty_errors(w_gpu, w_cpu, cols, y)
+    assert e1 <= 1e-12 and e2 <= 1e-12, (e1, e2)
+    t = x[idx] - sigma * w_cpu
+    act_cpu = np.abs(t) > sigma * l1
+    margin = np.abs(np.abs(t) - sigma * l1) > 1e-12 * (1 + np.abs(t))
+    act_gpu = np.isin(idx, Jg)
+    assert np.array_equal(act_cpu[margin], act_gpu[margin])
+    PJc = oracle.prox(x[Jg] - sigma * w_gpu[np.searchsorted(idx, Jg)], sigma, l1, l2)
+    np.testing.assert_allclose(PJ[:r].cpu().numpy(), PJc, rtol=1e-12, atol=1e-15)
+    assert part[0] == pytest.approx(float(PJc @ PJc), rel=1e-10)
+
+
+def kkt_sampled(cfg, b, x, l1, l2, seed):
+    """max_i v_i of the KKT inclusion over the support and 20 000 sampled columns."""
+    supp = np.nonzero(x)[0]
+    cs = synth.columns(cfg, supp) if len(supp) else np.zeros((0, cfg.m))
+    res = b - (cs.T @ x[supp] if len(supp) else 0.0)
+    idx = np.unique(np.concatenate([sample_idx(cfg.n, 20_000, seed), supp]))
+    cols = synth.columns(cfg, idx)
+    c = cols @ res - l2 * x[idx]
+    xi = x[idx]
+    v = np.where(xi > 0, np.abs(c - l1), np.where(xi < 0, np.abs(c + l1), np.maximum(np.abs(c) - l1, 0.0)))
+    return float(v.max()), res
+
+
+@pytest.mark.parametrize("name", ["cfg3", "cfg4", "cfg5"])
+def test_solve_fullsize_properties(name):
+    cfg, dA, b, P = device_problem(name)
+    lm = P.lambda_max_l1
+    for c in cfg.cs:
+        l1, l2 = lambdas(cfg, lm, c)
+        x, st = P.solve(l1, l2, cfg.sigma0, cfg.tol)
+        assert st["status"] == 0 and st["res_kkt1"] <= cfg.tol and st["res_kkt3"] <= cfg.tol, st
+        assert st["outer_iters"] <= 8  # soft pin: "no more than 6 iteration(s)", allowance
+        assert st["gap"] >= -1e-9 * abs(st["primal_obj"])
+        v, _ = kkt_sampled(cfg, b, x, l1, l2, 5)
+        assert v <= 1e-3 * l1, (c, v / l1)
+        # tight tolerance: the KKT inclusion holds to 1e-7 λ1 on every checked column
+        xt, stt = P.solve(l1, l2, cfg.sigma0, 1e-10, x0=x)
+        vt, res = kkt_sampled(cfg, b, xt, l1, l2, 6)
+        assert vt <= 1e-7 * l1, (c, vt / l1)
+        # the GPU's objective report agrees with the host evaluation from regenerated columns
+        F = 0.5 * res @ res + l1 * np.abs(xt).sum() + 0.5 * l2 * xt @ xt
+        assert stt["primal_obj"] == pytest.approx(F, rel=1e-11)
+
+
+@pytest.mark.parametrize("name", ["cfg5"])
+def test_zero_above_lambda_max_fullsize(name):
+    cfg, dA, b, P = device_problem(name)
+    g = P.lambda_max_l1
+    x, st = P.solve(g, 0.3 * g, cfg.sigma0, cfg.tol)
+    assert np.all(x == 0) and st["newton_iters"] == 1 and st["aty_passes"] == 1
+
+
+def test_cfg3_fullsize_oracle_parity():
+    """cfg3 at full size (m=500, n=1e6) against the oracle on the host, all three c values."""
+    cfg, dA, b, P = device_problem("cfg3")
+    A = synth.design(cfg)  # 4 GB on the host, bitwise equal to dA
+    lm = float(np.max(np.abs(oracle.aty(A, b))))
+    assert P.lambda_max_l1 == pytest.approx(lm, rel=1e-13)
+    for c in cfg.cs:
+        l1, l2 = lambdas(cfg, lm, c)
+        xc, _, stc, _ = oracle.solve(A, b, l1, l2, sigma0=cfg.sigma0, tol=cfg.tol)
+        xg, stg = P.solve(l1, l2, cfg.sigma0, cfg.tol)
+        assert stc["status"] == 0 and stg["status"] == 0
+        Fg = oracle.primal_obj(A, b, xg, l1, l2)
+        Fc = oracle.primal_obj(A, b, xc, l1, l2)
+        par = solution_parity(xg, xc, Fg, Fc)
+        assert par["ok"], (c, par, stg, stc)
+        assert stg["outer_iters"] == stc["outer_iters"]
+        assert abs(stg["newton_iters"] - stc["newton_iters"]) <= 1
+    del A
