@@ -463,6 +463,8 @@ struct EvalOut {
   double gd;        // gᵀd of the direction that produced this point (copied from gd_src)
   long long r;      // |J|
   long long info;   // Cholesky status of that direction (copied from info_src)
+  unsigned long long seq;  // written last (mapped host copy: the host spins on it)
+  unsigned long long pad;
 };
 
 constexpr int K5_THREADS = 256;  // 8 warps; CTA c owns rows [32c, 32c + 32)
@@ -478,7 +480,8 @@ __global__ void __launch_bounds__(K5_THREADS) k_eval_reduce(int64_t m, const dou
                                                             Scal sc, double nb, int with_grad,
                                                             double* __restrict__ g_out, const int64_t* r_in,
                                                             EvalOut* out, double* blk, unsigned* ticket,
-                                                            const double* gd_src, const int* info_src) {
+                                                            const double* gd_src, const int* info_src,
+                                                            EvalOut* host_out, unsigned long long seq) {
   __shared__ double red[8][33];
   __shared__ bool last;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -558,7 +561,17 @@ __global__ void __launch_bounds__(K5_THREADS) k_eval_reduce(int64_t m, const dou
   o.gd = gd_src ? *gd_src : 0.0;
   o.r = r_in ? (long long)*r_in : -1;
   o.info = info_src ? (long long)*info_src : 0;
+  o.seq = seq;
+  o.pad = 0;
   *out = o;
+  if (host_out) {  // zero-copy to mapped pinned memory; seq last, after a system-scope fence
+    volatile EvalOut* h = host_out;
+    h->psi = o.psi; h->psimag = o.psimag; h->res1 = o.res1; h->yy = o.yy; h->by = o.by; h->gg = o.gg;
+    for (int j = 0; j < 4; ++j) h->s[j] = o.s[j];
+    h->gd = o.gd; h->r = o.r; h->info = o.info;
+    __threadfence_system();
+    h->seq = seq;
+  }
   *ticket = 0u;  // ready for the next launch (stream-ordered)
 }
 

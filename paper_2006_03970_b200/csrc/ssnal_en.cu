@@ -212,7 +212,9 @@ struct ssnal_en_problem {
   int W_splits = 0;
   int* info = nullptr;
   EvalOut* ev_dev = nullptr;   // slots
-  EvalOut* ev_host = nullptr;  // pinned mirror
+  EvalOut* ev_host = nullptr;  // mapped pinned mirror (GPU writes it directly)
+  EvalOut* ev_host_dev = nullptr;  // device alias of ev_host
+  unsigned long long ev_seq = 0;
   double* scratch = nullptr;   // small device scratch (objective, λmax)
   double* scratch_host = nullptr;
   int* flags = nullptr;
@@ -337,7 +339,9 @@ int allocate(ssnal_en_problem* P) {
   AL(P->ticket, 64);
   AL(P->gax_valid, 4 * 256);
   CK(cudaMemset(P->ticket, 0, 64));
-  CK(cudaMallocHost((void**)&P->ev_host, sizeof(EvalOut) * 4));
+  CK(cudaHostAlloc((void**)&P->ev_host, sizeof(EvalOut) * 4, cudaHostAllocMapped));
+  memset(P->ev_host, 0, sizeof(EvalOut) * 4);
+  CK(cudaHostGetDevicePointer((void**)&P->ev_host_dev, P->ev_host, 0));
   CK(cudaMallocHost((void**)&P->scratch_host, 64 * 8));
   return SSNAL_OK;
 }
@@ -357,6 +361,7 @@ cudaEvent_t take_event(ssnal_en_problem* P) {
 
 void harvest_k1(ssnal_en_problem* P) {  // call after a stream sync
   for (auto& pr : P->k1_pending) {
+    cudaEventSynchronize(pr.second);
     float ms = 0;
     cudaEventElapsedTime(&ms, pr.first, pr.second);
     P->k1_time += ms * 1e-3;
@@ -460,19 +465,40 @@ int launch_eval(ssnal_en_problem* P, const double* y, const Scal& sc, int with_g
                 double* g_out, const int64_t* r_dev, int slot, const double* gd_src = nullptr,
                 const int* info_src = nullptr) {
   const unsigned nblk = (unsigned)((P->m + 31) / 32);
+  ++P->ev_seq;
   k_eval_reduce<<<nblk, K5_THREADS, 0, P->st>>>(P->m, y, P->b, P->part_vec, valid, nparts, P->part_scal, P->G, sc,
                                                  P->nb, with_grad, g_out, r_dev, P->ev_dev + slot, P->blk,
-                                                 P->ticket, gd_src, info_src);
+                                                 P->ticket, gd_src, info_src, P->ev_host_dev + slot, P->ev_seq);
   P->launches++;
   CKL();
   return SSNAL_OK;
 }
 
+// Wait for the EvalOut of the most recent launch_eval on `slot`: spin on the mapped host copy's
+// sequence number (no stream synchronisation); poll the stream for errors now and then.
 int fetch_eval(ssnal_en_problem* P, int slot, EvalOut* out) {
-  CK(cudaMemcpyAsync(P->ev_host + slot, P->ev_dev + slot, sizeof(EvalOut), cudaMemcpyDeviceToHost, P->st));
-  CK(cudaStreamSynchronize(P->st));
-  harvest_k1(P);
-  *out = P->ev_host[slot];
+  volatile EvalOut* h = P->ev_host + slot;
+  const unsigned long long want = P->ev_seq;
+  for (uint64_t spin = 0; h->seq != want; ++spin) {
+    if ((spin & 0xFFFF) == 0xFFFF) {
+      cudaError_t e = cudaStreamQuery(P->st);
+      if (e != cudaSuccess && e != cudaErrorNotReady) {
+        set_err("stream error while waiting for an evaluation: %s", cudaGetErrorString(e));
+        return SSNAL_ECUDA;
+      }
+      if (e == cudaSuccess && h->seq != want) {
+        __sync_synchronize();
+        if (h->seq != want) {
+          set_err("evaluation record not delivered (seq %llu, want %llu)", (unsigned long long)h->seq, want);
+          return SSNAL_ECUDA;
+        }
+      }
+    }
+  }
+  __sync_synchronize();
+  out->psi = h->psi; out->psimag = h->psimag; out->res1 = h->res1; out->yy = h->yy; out->by = h->by; out->gg = h->gg;
+  for (int j = 0; j < 4; ++j) out->s[j] = h->s[j];
+  out->gd = h->gd; out->r = h->r; out->info = h->info; out->seq = h->seq; out->pad = 0;
   return SSNAL_OK;
 }
 
