@@ -29,16 +29,62 @@ __global__ void __launch_bounds__(256) k_gather_axpy(const double* __restrict__ 
                                                      double* __restrict__ part_vec, int* __restrict__ valid) {
   extern __shared__ double red[];  // 8 x m
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (r < 0) r = *r_dev;
-  const int64_t a_lo = (int64_t)blockIdx.x * r / gridDim.x, a_hi = (int64_t)(blockIdx.x + 1) * r / gridDim.x;
+  const bool devr = r < 0;
+  if (devr) r = *r_dev;
+  // host r: contiguous share; device r: chunks of 16 columns b, b + grid, ... (few CTAs for small r)
+  const int64_t a_lo = devr ? (int64_t)blockIdx.x * 16 : (int64_t)blockIdx.x * r / gridDim.x;
+  const int64_t a_hi = devr ? r : (int64_t)(blockIdx.x + 1) * r / gridDim.x;
   if (valid && threadIdx.x == 0) valid[blockIdx.x] = a_hi > a_lo;
   if (valid && a_hi <= a_lo) return;
   double acc[MR];
 #pragma unroll
   for (int t = 0; t < MR; ++t) acc[t] = 0.0;
+  const int64_t stride = devr ? (int64_t)gridDim.x * 16 : 0;
+  for (int64_t base = a_lo; base < a_hi; base += stride) {
+    const int64_t e_hi = devr ? min(base + 16, a_hi) : a_hi;
+    for (int64_t a = base + warp; a < e_hi; a += 8) {
+      const double* col = A + (int64_t)J[a] * m;
+      const double c = coef[a];
+#pragma unroll
+      for (int t = 0; t < MR; ++t) {
+        const int64_t row = lane + 32 * t;
+        if (row < m) acc[t] = fma(c, __ldg(col + row), acc[t]);
+      }
+    }
+    if (!devr) break;
+  }
+#pragma unroll
+  for (int t = 0; t < MR; ++t) {
+    const int64_t row = lane + 32 * t;
+    if (row < m) red[(size_t)warp * m + row] = acc[t];
+  }
+  __syncthreads();
+  for (int64_t k = threadIdx.x; k < m; k += blockDim.x) {
+    double v = red[k];
+    for (int wi = 1; wi < 8; ++wi) v += red[(size_t)wi * m + k];
+    part_vec[(size_t)blockIdx.x * m + k] = v;
+  }
+}
+
+// Fused SMW back-substitution (Eq. (19)): partials of A_J v over `grid` CTAs, then the last CTA
+// (ticket) forms d = −g + Σ_b parts[b] (b ascending), gᵀd, and the Armijo trial y_t = y + d.
+template <int MR>
+__global__ void __launch_bounds__(256) k_smw_backsub(const double* __restrict__ A, int64_t m,
+                                                     const int32_t* __restrict__ J, const double* __restrict__ v,
+                                                     int64_t r, double* __restrict__ parts, const double* __restrict__ g,
+                                                     const double* __restrict__ y, double* __restrict__ d,
+                                                     double* __restrict__ yt, double* gd_out, unsigned* ticket) {
+  extern __shared__ double red[];  // 8 x m
+  __shared__ bool last;
+  __shared__ double wsum[8];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t a_lo = (int64_t)blockIdx.x * r / gridDim.x, a_hi = (int64_t)(blockIdx.x + 1) * r / gridDim.x;
+  double acc[MR];
+#pragma unroll
+  for (int t = 0; t < MR; ++t) acc[t] = 0.0;
   for (int64_t a = a_lo + warp; a < a_hi; a += 8) {
     const double* col = A + (int64_t)J[a] * m;
-    const double c = coef[a];
+    const double c = v[a];
 #pragma unroll
     for (int t = 0; t < MR; ++t) {
       const int64_t row = lane + 32 * t;
@@ -52,9 +98,33 @@ __global__ void __launch_bounds__(256) k_gather_axpy(const double* __restrict__ 
   }
   __syncthreads();
   for (int64_t k = threadIdx.x; k < m; k += blockDim.x) {
-    double v = red[k];
-    for (int wi = 1; wi < 8; ++wi) v += red[(size_t)wi * m + k];
-    part_vec[(size_t)blockIdx.x * m + k] = v;
+    double sacc = red[k];
+    for (int wi = 1; wi < 8; ++wi) sacc += red[(size_t)wi * m + k];
+    parts[(size_t)blockIdx.x * m + k] = sacc;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = (atomicAdd(ticket, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double dot = 0.0;
+  for (int64_t k = threadIdx.x; k < m; k += blockDim.x) {
+    double sacc = 0.0;
+    for (unsigned b = 0; b < gridDim.x; ++b) sacc += __ldcg(parts + (size_t)b * m + k);
+    const double dk = -g[k] + sacc;
+    d[k] = dk;
+    yt[k] = __dadd_rn(y[k], __dmul_rn(1.0, dk));
+    dot += g[k] * dk;
+  }
+  dot = warp_allsum(dot);
+  if (lane == 0) wsum[warp] = dot;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double sacc = 0.0;
+    for (int wi = 0; wi < 8; ++wi) sacc += wsum[wi];
+    *gd_out = sacc;
+    *ticket = 0u;
   }
 }
 
@@ -128,7 +198,8 @@ SSN_DEV void tri_tile(int q, int* ti, int* tj) {  // q → (ti ≥ tj), row-majo
 template <bool SMW>
 __global__ void __launch_bounds__(256) k_gram(const double* __restrict__ A, int64_t m,
                                               const int32_t* __restrict__ J, int64_t r, double* __restrict__ W,
-                                              int64_t wld) {
+                                              int64_t wld, const double* __restrict__ gext) {
+  // SMW: index r (if gext) is the extra column g, so row r of the output is u = A_Jᵀg (Eq. (19) rhs)
   __shared__ double sA[32][33], sB[32][33];
   int ti, tj;
   tri_tile(blockIdx.x, &ti, &tj);
@@ -139,13 +210,14 @@ __global__ void __launch_bounds__(256) k_gram(const double* __restrict__ A, int6
   const int64_t c_lo = nch * s / ns, c_hi = nch * (s + 1) / ns;  // chunk slice
   const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
   // element q of this thread in a 32 × 32 block: e = tid + 256 q → (γ = e >> 5, ρ = e & 31)
-  int64_t colA[4], colB[4];  // SMW: fixed column offsets J[·]*m for the a/b tiles
+  const double* colA[4];  // SMW: fixed column pointers for the a/b tiles (g for index r)
+  const double* colB[4];
   if (SMW) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int64_t ga = o0 + ty + 8 * q, gb = o1 + ty + 8 * q;
-      colA[q] = ga < r ? (int64_t)J[ga] * m : -1;
-      colB[q] = gb < r ? (int64_t)J[gb] * m : -1;
+      colA[q] = ga < r ? A + (int64_t)J[ga] * m : ((ga == r && gext) ? gext : nullptr);
+      colB[q] = gb < r ? A + (int64_t)J[gb] * m : ((gb == r && gext) ? gext : nullptr);
     }
   }
   double va[4], vb[4];
@@ -154,8 +226,8 @@ __global__ void __launch_bounds__(256) k_gram(const double* __restrict__ A, int6
     for (int q = 0; q < 4; ++q) {
       if (SMW) {
         const int64_t k = ch * 32 + tx;
-        va[q] = (colA[q] >= 0 && k < m) ? __ldg(A + colA[q] + k) : 0.0;
-        vb[q] = (colB[q] >= 0 && k < m) ? __ldg(A + colB[q] + k) : 0.0;
+        va[q] = (colA[q] && k < m) ? __ldg(colA[q] + k) : 0.0;
+        vb[q] = (colB[q] && k < m) ? __ldg(colB[q] + k) : 0.0;
       } else {
         const int64_t a = ch * 32 + ty + 8 * q;
         const bool ok = a < r;
@@ -188,7 +260,7 @@ __global__ void __launch_bounds__(256) k_gram(const double* __restrict__ A, int6
     }
     __syncthreads();
   }
-  const int64_t nout = SMW ? r : m;
+  const int64_t nout = SMW ? r + (gext ? 1 : 0) : m;
   double* Ws = W + (size_t)s * wld * nout;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
@@ -197,17 +269,20 @@ __global__ void __launch_bounds__(256) k_gram(const double* __restrict__ A, int6
   }
 }
 
-// M[i + j*ld] = diag·[i == j] + mult · Σ_s W[s][i + j*nout]   (i ≥ j)
-//   SMW:   diag = κ⁻¹, mult = 1          m × m:  diag = 1, mult = κ   (oracle: κ s + δ)
-__global__ void k_gram_reduce(const double* __restrict__ W, int ns, int64_t nout, double diag, double mult,
-                              double* __restrict__ M, int64_t ld) {
+// M[i + j*ld] = diag·[i == j] + mult · Σ_s W[s][i + j*nout]   (i ≥ j, j < nmat)
+//   SMW:   diag = κ⁻¹, mult = 1; nout = nmat + 1: row nmat is the rhs u = A_Jᵀg (unscaled)
+//   m × m: diag = 1, mult = κ (oracle: κ s + δ); nout = nmat; rhs row ← g (if g)
+__global__ void k_gram_reduce(const double* __restrict__ W, int ns, int64_t nout, int64_t nmat, double diag,
+                              double mult, double* __restrict__ M, int64_t ld, const double* __restrict__ g) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g && e < nmat) M[nmat + e * ld] = g[e];
   if (e >= nout * nout) return;
   const int64_t i = e % nout, j = e / nout;
-  if (i < j) return;
+  if (i < j || j >= nmat) return;
   double s = 0.0;
   for (int q = 0; q < ns; ++q) s += W[(size_t)q * nout * nout + e];
-  M[i + j * ld] = (mult == 1.0 ? s : mult * s) + (i == j ? diag : 0.0);
+  if (i < nmat) M[i + j * ld] = (mult == 1.0 ? s : mult * s) + (i == j ? diag : 0.0);
+  else M[i + j * ld] = s;  // rhs row
 }
 
 // ---------------------------------------------------------------------------
@@ -354,7 +429,8 @@ SSN_DEV void inv_block_warp(const double* M, int ld, int b0, int bn, double* S, 
 
 __global__ void __launch_bounds__(256, 1) k_chol_cluster(double* M, int N, int ld, double* __restrict__ out,
                                                          double scale, const double* __restrict__ dotv,
-                                                         double* dot_out, double* Winv, int* info) {
+                                                         double* dot_out, double* Winv, int* info,
+                                                         const double* __restrict__ ybase, double* __restrict__ yt) {
   namespace cg = cooperative_groups;
   cg::cluster_group cl = cg::this_cluster();
   const int rank = (int)cl.block_rank(), CS = (int)cl.num_blocks();
@@ -583,6 +659,7 @@ __global__ void __launch_bounds__(256, 1) k_chol_cluster(double* M, int N, int l
   for (int i = tid; i < N; i += blockDim.x) {
     const double v = scale * zv[i];
     out[i] = v;
+    if (yt) yt[i] = __dadd_rn(ybase[i], __dmul_rn(1.0, v));  // Armijo trial y + d (m × m branch)
     if (dotv) dot += dotv[i] * v;
   }
   if (dotv) {
@@ -605,11 +682,13 @@ __global__ void k_axpy_m(int64_t m, const double* y, double s, const double* d, 
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k < m) out[k] = __dadd_rn(y[k], __dmul_rn(s, d[k]));
 }
-__global__ void k_neg_copy(int64_t m, const double* g, double* d, const double* dotv, double* dot_out) {
+__global__ void k_neg_copy(int64_t m, const double* g, double* d, const double* dotv, double* dot_out,
+                           const double* y, double* yt) {
   __shared__ double red[32];
   double dot = 0.0;
   for (int64_t k = threadIdx.x; k < m; k += blockDim.x) {
     d[k] = -g[k];
+    if (yt) yt[k] = __dadd_rn(y[k], __dmul_rn(1.0, -g[k]));
     dot += dotv[k] * (-g[k]);
   }
   dot = warp_allsum(dot);

@@ -94,6 +94,19 @@ k1_fn k1_for(int mr) {
     default: return k1_aty_fused<32>;
   }
 }
+typedef void (*bsub_fn)(const double*, int64_t, const int32_t*, const double*, int64_t, double*, const double*,
+                        const double*, double*, double*, double*, unsigned*);
+bsub_fn bsub_for(int mr) {
+  switch (mr) {
+    case 1: return k_smw_backsub<1>;
+    case 2: return k_smw_backsub<2>;
+    case 4: return k_smw_backsub<4>;
+    case 8: return k_smw_backsub<8>;
+    case 16: return k_smw_backsub<16>;
+    case 25: return k_smw_backsub<25>;
+    default: return k_smw_backsub<32>;
+  }
+}
 gax_fn gax_for(int mr) {
   switch (mr) {
     case 1: return k_gather_axpy<1>;
@@ -278,6 +291,7 @@ int configure(ssnal_en_problem* P) {
   CK(cudaFuncSetAttribute(k1_for(P->MR), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->k1_smem));
   const size_t gsm = (size_t)8 * m * 8;
   CK(cudaFuncSetAttribute(gax_for(P->MR), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsm));
+  CK(cudaFuncSetAttribute(bsub_for(P->MR), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsm));
   P->chol_smem = kCholSmem;
   CK(cudaFuncSetAttribute(k_chol_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->chol_smem));
   CK(cudaFuncSetAttribute(k_chol_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -504,7 +518,7 @@ int fetch_eval(ssnal_en_problem* P, int slot, EvalOut* out) {
 
 // Cluster Cholesky + both triangular solves: M holds the matrix (ld = N+1) and the rhs in row N.
 int launch_chol(ssnal_en_problem* P, double* M, int N, double* out, double scale, const double* dotv,
-                double* dot_out) {
+                double* dot_out, const double* ybase = nullptr, double* yt = nullptr) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(P->cluster);
   cfg.blockDim = dim3(256);
@@ -517,17 +531,18 @@ int launch_chol(ssnal_en_problem* P, double* M, int N, double* out, double scale
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  CK(cudaLaunchKernelEx(&cfg, k_chol_cluster, M, N, N + 1, out, scale, dotv, dot_out, P->Winv, P->info));
+  CK(cudaLaunchKernelEx(&cfg, k_chol_cluster, M, N, N + 1, out, scale, dotv, dot_out, P->Winv, P->info, ybase, yt));
   P->launches++;
   return SSNAL_OK;
 }
 
-// Newton direction for (J, r) at gradient g: d ← solution, *gd_dev ← gᵀd.  Eq. (18)/(19).
+// Newton direction for (J, r) at gradient g: d ← solution, *gd_dev ← gᵀd (Eq. (18)/(19)); if yt,
+// also the Armijo trial y_t = y + d (fused into the last kernel of each branch).
 int newton_direction(ssnal_en_problem* P, const int32_t* J, int64_t r, const double* g, double kappa, double* d,
-                     double* gd_dev, int* branch) {
+                     double* gd_dev, int* branch, const double* y = nullptr, double* yt = nullptr) {
   const int64_t m = P->m;
   if (r == 0) {
-    k_neg_copy<<<1, 1024, 0, P->st>>>(m, g, d, g, gd_dev);
+    k_neg_copy<<<1, 1024, 0, P->st>>>(m, g, d, g, gd_dev, y, yt);
     P->launches++;
     CKL();
     *branch = 0;
@@ -544,43 +559,39 @@ int newton_direction(ssnal_en_problem* P, const int32_t* J, int64_t r, const dou
   };
   if (r < m) {  // Sherman–Morrison–Woodbury, Eq. (19): factor κ⁻¹I_r + A_JᵀA_J (R13)
     const int N = (int)r;
-    const int nt = (N + 31) / 32, tiles = nt * (nt + 1) / 2;
+    const int64_t nout = r + 1;  // index r carries g: row r = u = A_Jᵀg (the rhs row)
+    const int nt = (int)((nout + 31) / 32), tiles = nt * (nt + 1) / 2;
     const int ns = splits(tiles, m);
-    k_gram<true><<<dim3(tiles, ns), 256, 0, P->st>>>(P->A, m, J, r, P->W, r);
+    k_gram<true><<<dim3(tiles, ns), 256, 0, P->st>>>(P->A, m, J, r, P->W, nout, g);
     P->launches++;
     CKL();
-    k_gram_reduce<<<(unsigned)((r * r + 255) / 256), 256, 0, P->st>>>(P->W, ns, r, 1.0 / kappa, 1.0, P->Mmat, N + 1);
-    P->launches++;
-    CKL();
-    int wg = (int)((r * 32 + 255) / 256);
-    if (wg > 4 * P->nsm) wg = 4 * P->nsm;
-    k_jt_gemv<<<wg, 256, 0, P->st>>>(P->A, m, J, r, g, P->Mmat + N, N + 1);  // u = A_Jᵀ g → rhs row
+    k_gram_reduce<<<(unsigned)((nout * nout + 255) / 256), 256, 0, P->st>>>(P->W, ns, nout, r, 1.0 / kappa, 1.0,
+                                                                            P->Mmat, N + 1, nullptr);
     P->launches++;
     CKL();
     int rc = launch_chol(P, P->Mmat, N, P->u, 1.0, nullptr, nullptr);  // v = (κ⁻¹I + G)⁻¹ u
     if (rc) return rc;
-    int grid = 0;
-    rc = launch_gather(P, J, P->u, r, &grid);
-    if (rc) return rc;
-    k_combine<<<1, 1024, 0, P->st>>>(m, g, -1.0, P->part_vec, grid, d, g, gd_dev);  // d = −g + A_J v
+    int grid = (int)((r + 63) / 64);
+    if (grid > P->gax_grid) grid = P->gax_grid;
+    if (grid < 1) grid = 1;
+    // d = −g + A_J v, gᵀd, y_t = y + d (last-CTA finalisation)
+    bsub_for(P->MR)<<<grid, 256, (size_t)8 * m * 8, P->st>>>(P->A, m, J, P->u, r, P->part_vec, g, y ? y : g, d,
+                                                             yt ? yt : P->tmpm, gd_dev, P->ticket);
     P->launches++;
     CKL();
     *branch = 1;
     return SSNAL_OK;
   }
-  // r ≥ m: Eq. (18), M = I_m + κ A_J A_Jᵀ
+  // r ≥ m: Eq. (18), M = I_m + κ A_J A_Jᵀ; the reduce also writes g into the rhs row
   const int nt = (int)((m + 31) / 32), tiles = nt * (nt + 1) / 2;
   const int ns = splits(tiles, r);
-  k_gram<false><<<dim3(tiles, ns), 256, 0, P->st>>>(P->A, m, J, r, P->W, m);
+  k_gram<false><<<dim3(tiles, ns), 256, 0, P->st>>>(P->A, m, J, r, P->W, m, nullptr);
   P->launches++;
   CKL();
-  k_gram_reduce<<<(unsigned)((m * m + 255) / 256), 256, 0, P->st>>>(P->W, ns, m, 1.0, kappa, P->Mmat, m + 1);
+  k_gram_reduce<<<(unsigned)((m * m + 255) / 256), 256, 0, P->st>>>(P->W, ns, m, m, 1.0, kappa, P->Mmat, m + 1, g);
   P->launches++;
   CKL();
-  k_copy_strided<<<(unsigned)((m + 255) / 256), 256, 0, P->st>>>(m, g, P->Mmat + m, m + 1);  // rhs row = g
-  P->launches++;
-  CKL();
-  int rc = launch_chol(P, P->Mmat, (int)m, d, -1.0, g, gd_dev);  // d = −M⁻¹ g, gd = gᵀd
+  int rc = launch_chol(P, P->Mmat, (int)m, d, -1.0, g, gd_dev, y, yt);  // d = −M⁻¹ g, gd = gᵀd
   if (rc) return rc;
   *branch = 2;
   return SSNAL_OK;
@@ -664,14 +675,12 @@ int solve_core(ssnal_en_problem* P, double l1, double l2, double sigma0, double 
       if (ev.res1 <= tol) break;  // inner stop, Eq. (20) res(kkt1) (R6)
       int br = 0;
       double* gd_dev = P->scratch;
-      if ((rc = newton_direction(P, P->J[cur], ev.r, P->g[cur], sc.kappa, P->d, gd_dev, &br))) return rc;
-      S->branch_steps[br]++;
-      // trial s = 1: y_t = y + d; K1 fused at y_t
+      // trial s = 1: y_t = y + d (written by the direction's last kernel); K1 fused at y_t
       const int tr = 1 - cur;
       const int wtr = (wcur + 1) % 3, wbt = (wcur + 2) % 3;
-      k_axpy_m<<<(unsigned)((m + 255) / 256), 256, 0, P->st>>>(m, P->y[cur], 1.0, P->d, P->y[tr]);
-      P->launches++;
-      CKL();
+      if ((rc = newton_direction(P, P->J[cur], ev.r, P->g[cur], sc.kappa, P->d, gd_dev, &br, P->y[cur], P->y[tr])))
+        return rc;
+      S->branch_steps[br]++;
       if ((rc = launch_k1(P, P->y[tr], P->x, sc, 1, P->w[wtr]))) return rc;
       S->aty_passes++;
       if ((rc = launch_finalize(P, P->J[tr], P->PJ[tr], P->r_dev + tr))) return rc;
