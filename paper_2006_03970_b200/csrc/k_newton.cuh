@@ -702,9 +702,22 @@ __global__ void k_neg_copy(int64_t m, const double* g, double* d, const double* 
 }
 
 // x ← P: zero x on the old support, then scatter (J, P_J).
-__global__ void k_zero_at(const int32_t* __restrict__ idx, int64_t cnt, double* x) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < cnt) x[idx[i]] = 0.0;
+__global__ void k_zero_at(const int32_t* __restrict__ idx, int64_t cnt, const int64_t* cnt_dev, double* x) {
+  if (cnt < 0) cnt = *cnt_dev;  // grid-stride with a device-resident count
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += (int64_t)gridDim.x * blockDim.x)
+    x[idx[i]] = 0.0;
+}
+
+// y = (*r_dev > 0) ? −b + Σ_{valid b'} parts[b'] : 0    (warm start y0 = A x0 − b, reading R8)
+__global__ void k_init_y(int64_t m, const double* __restrict__ bvec, const double* __restrict__ parts,
+                         const int* __restrict__ valid, int nparts, const int64_t* r_dev, double* __restrict__ y) {
+  const bool warm = *r_dev > 0;
+  for (int64_t k = threadIdx.x; k < m; k += blockDim.x) {
+    double s = 0.0;
+    for (int b = 0; b < nparts; ++b)
+      if (valid[b]) s += parts[(size_t)b * m + k];
+    y[k] = warm ? (-1.0 * bvec[k] + s) : 0.0;
+  }
 }
 __global__ void k_scatter(const int32_t* __restrict__ idx, const double* __restrict__ v, int64_t cnt, double* x) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;

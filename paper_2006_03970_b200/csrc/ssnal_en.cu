@@ -241,6 +241,9 @@ struct ssnal_en_problem {
   int max_outer = 100, max_inner = 100, max_bt = 50, init_mode = 1, time_k1 = 0;
   // counters for the current call
   int64_t launches = 0;
+  double stat_l1 = 0, stat_l2 = 0;
+  bool stat_warm_pass = false;
+  cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr;  // solve timing (persistent)
   std::vector<cudaEvent_t> ev_pool;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> k1_pending;
   double k1_time = 0;
@@ -629,28 +632,29 @@ int solve_core(ssnal_en_problem* P, double l1, double l2, double sigma0, double 
   EvalOut ev, evt;
 
   // Support of x (Jx, Px, rx): K1e with w = 0, σ = 1, λ = 0 selects x ≠ 0 and P = x.
+  // rx: size of supp(x) — host-known after the first outer step; before it (warm start) the count
+  // lives on the device only (rx = -1) and every consumer reads r_dev[2] there (no round trip).
   int64_t rx = 0;
   if (have_x0) {
     CK(cudaMemsetAsync(P->w[2], 0, n * 8, P->st));
     const Scal s0 = make_scal(1.0, 0.0, 0.0);
     if ((rc = launch_k1e(P, P->w[2], nullptr, 0.0, P->x, s0, nullptr))) return rc;
     if ((rc = launch_finalize(P, P->Jx, P->Px, P->r_dev + 2))) return rc;
-    CK(cudaMemcpyAsync(P->scratch_host, P->r_dev + 2, 8, cudaMemcpyDeviceToHost, P->st));
-    CK(cudaStreamSynchronize(P->st));
-    memcpy(&rx, P->scratch_host, 8);
+    CK(cudaMemcpyAsync(P->r_dev + 4, P->r_dev + 2, 8, cudaMemcpyDeviceToDevice, P->st));  // |supp x0| for stats
+    rx = -1;
   } else {
     CK(cudaMemsetAsync(P->x, 0, n * 8, P->st));
     CK(cudaMemsetAsync(P->r_dev + 2, 0, 8, P->st));
+    CK(cudaMemsetAsync(P->r_dev + 4, 0, 8, P->st));
   }
-  // Initial y, w (P:242 silent; reading R8)
-  if (rx > 0 && P->init_mode == 1) {
-    int grid = 0;
-    if ((rc = launch_gather(P, P->Jx, P->Px, rx, &grid))) return rc;
-    k_combine<<<1, 1024, 0, P->st>>>(m, P->b, -1.0, P->part_vec, grid, P->y[cur], nullptr, nullptr);  // A x0 − b
+  // Initial y, w (P:242 silent; reading R8): y0 = A x0 − b if x0 ≠ 0, else 0 (decided on the device)
+  if (have_x0 && P->init_mode == 1) {
+    if ((rc = launch_gather_dev(P, P->Jx, P->Px, P->r_dev + 2))) return rc;
+    k_init_y<<<1, 1024, 0, P->st>>>(m, P->b, P->part_vec, P->gax_valid, kGatherDevGrid, P->r_dev + 2, P->y[cur]);
     P->launches++;
     CKL();
     if ((rc = launch_k1(P, P->y[cur], nullptr, make_scal(1.0, 0.0, 0.0), 0, P->w[wcur]))) return rc;
-    S->aty_passes++;
+    S->aty_passes++;  // corrected at the end if x0 turned out to be zero (cold start, no pass)
   } else {
     CK(cudaMemsetAsync(P->y[cur], 0, m * 8, P->st));
     CK(cudaMemsetAsync(P->w[wcur], 0, n * 8, P->st));
@@ -748,7 +752,11 @@ int solve_core(ssnal_en_problem* P, double l1, double l2, double sigma0, double 
     S->res_kkt3 = res3;
     S->res_kkt1 = ev.res1;
     if (rx > 0) {
-      k_zero_at<<<(unsigned)((rx + 255) / 256), 256, 0, P->st>>>(P->Jx, rx, P->x);
+      k_zero_at<<<(unsigned)((rx + 255) / 256), 256, 0, P->st>>>(P->Jx, rx, nullptr, P->x);
+      P->launches++;
+      CKL();
+    } else if (rx < 0) {  // warm start: count on the device
+      k_zero_at<<<2 * P->nsm, 256, 0, P->st>>>(P->Jx, -1, P->r_dev + 2, P->x);
       P->launches++;
       CKL();
     }
@@ -785,15 +793,25 @@ int solve_core(ssnal_en_problem* P, double l1, double l2, double sigma0, double 
     P->launches++;
     CKL();
     CK(cudaMemcpyAsync(P->scratch_host + 16, P->scratch + 16, 4 * 8, cudaMemcpyDeviceToHost, P->st));
-    CK(cudaStreamSynchronize(P->st));
-    harvest_k1(P);
-    const double* o = P->scratch_host + 16;
-    S->primal_obj = o[0] + l1 * o[1] + 0.5 * l2 * o[2];
-    S->active = (int64_t)o[3];
+    CK(cudaMemcpyAsync(P->scratch_host + 20, P->r_dev + 4, 8, cudaMemcpyDeviceToHost, P->st));
+    // read after the caller's single end-of-solve synchronisation (finish_stats)
     S->dual_obj = (l2 > 0) ? (-(0.5 * ev.yy + ev.by) - ev.s[3] / (2.0 * l2)) : NAN;
-    S->gap = S->primal_obj - S->dual_obj;
+    P->stat_l1 = l1;
+    P->stat_l2 = l2;
+    P->stat_warm_pass = (have_x0 && P->init_mode == 1);
   }
   return S->status;
+}
+
+// Complete the stats from the objective pieces copied by solve_core (after a stream sync).
+void finish_stats(ssnal_en_problem* P, ssnal_en_stats* S) {
+  const double* o = P->scratch_host + 16;
+  S->primal_obj = o[0] + P->stat_l1 * o[1] + 0.5 * P->stat_l2 * o[2];
+  S->active = (int64_t)o[3];
+  S->gap = S->primal_obj - S->dual_obj;
+  int64_t rx0;
+  memcpy(&rx0, P->scratch_host + 20, 8);
+  if (P->stat_warm_pass && rx0 == 0) S->aty_passes--;  // x0 was all zero: cold start, no pass (R8)
 }
 
 }  // namespace
@@ -880,6 +898,8 @@ static void destroy_bufs(ssnal_en_problem* P) {
   if (P->ev_host) cudaFreeHost(P->ev_host);
   if (P->scratch_host) cudaFreeHost(P->scratch_host);
   for (auto e : P->ev_pool) cudaEventDestroy(e);
+  if (P->ev_t0) cudaEventDestroy(P->ev_t0);
+  if (P->ev_t1) cudaEventDestroy(P->ev_t1);
   for (auto& pr : P->k1_pending) {
     cudaEventDestroy(pr.first);
     cudaEventDestroy(pr.second);
@@ -1011,30 +1031,27 @@ static int solve_wrapped(ssnal_en_problem* P, double l1, double l2, double sigma
   P->launches = 0;
   P->k1_time = 0;
   P->k1_count = 0;
-  cudaEvent_t e0, e1;
-  CK(cudaEventCreate(&e0));
-  CK(cudaEventCreate(&e1));
+  if (!P->ev_t0) {
+    CK(cudaEventCreate(&P->ev_t0));
+    CK(cudaEventCreate(&P->ev_t1));
+  }
+  cudaEvent_t e0 = P->ev_t0, e1 = P->ev_t1;
   CK(cudaEventRecord(e0, P->st));
   if (x0) {
     CK(cudaMemcpyAsync(P->x, x0, P->n * 8, x0_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, P->st));
   }
   ssnal_en_stats S;
   rc = solve_core(P, l1, l2, sigma0, tol, x0 != nullptr, &S);
-  if (rc == SSNAL_ECUDA || rc == SSNAL_EINVAL) {
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-    return rc;
-  }
+  if (rc == SSNAL_ECUDA || rc == SSNAL_EINVAL) return rc;
   if (x_out) {
     CK(cudaMemcpyAsync(x_out, P->x, P->n * 8, xout_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, P->st));
   }
   CK(cudaEventRecord(e1, P->st));
   CK(cudaStreamSynchronize(P->st));
   harvest_k1(P);
+  finish_stats(P, &S);
   float ms = 0;
   cudaEventElapsedTime(&ms, e0, e1);
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
   S.time_device_s = ms * 1e-3;
   S.time_total_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   S.kernel_launches = P->launches;

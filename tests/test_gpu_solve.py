@@ -146,3 +146,27 @@ def test_invalid_arguments():
                 P.solve(*args)
         with pytest.raises(SsnalError):
             P.set_option("no_such_option", 1)
+
+
+EDGE = [  # (kind, m, n, c, alpha, seed): tiny / odd / largest-m shapes; small c pushes r ≥ m (Eq. (18) branch)
+    (synth.IID_STD, 2, 1, 0.5, 0.5, 61),
+    (synth.IID_STD, 3, 7, 0.3, 0.7, 62),
+    (synth.IID_STD, 33, 100, 0.2, 0.5, 63),
+    (synth.IID_UNIT_L2, 129, 5000, 0.1, 0.5, 64),
+    (synth.IID_STD, 1024, 2500, 0.1, 0.3, 65),
+    (synth.GENO_STD, 200, 3000, 0.05, 0.5, 66),  # genotype columns need enough rows to vary
+]
+
+
+@pytest.mark.parametrize("case", EDGE, ids=lambda c: f"m{c[1]}_n{c[2]}_c{c[3]}")
+def test_solve_edge_shapes(case):
+    kind, m, n, c, alpha, seed = case
+    cfg = synth.Config("edge", m, n, kind, min(5, n), 1.0, 2.0, 5.0, alpha, (c,), seed)
+    A = synth.design(cfg)
+    b, _ = synth.response(cfg)
+    lm = float(np.max(np.abs(oracle.aty(A, b))))
+    l1, l2 = lambdas(cfg, lm, c)
+    xc, stc, xg, stg = run_pair(A, b, l1, l2)
+    check_parity(xc, stc, xg, stg, A, b, l1, l2, f"edge {case}")
+    assert stg["outer_iters"] == stc["outer_iters"]
+    assert stg["branch_steps"][2] == stc["branch_steps"][2] or abs(stg["newton_iters"] - stc["newton_iters"]) <= 1
