@@ -4,9 +4,9 @@
 // (each column is m contiguous doubles); nothing is gathered into a copy.
 //
 // K2  k_gather_axpy    : per-CTA partials of Σ_a coef_a A[:, J_a]          (A_J v, A_J P_J)
+//     k_smw_backsub    : d = −g + A_J v, gᵀd and the trial y + d (last-CTA finalisation)
 //     k_combine        : out = bs·base + Σ parts (fixed order), optional dot
-//     k_jt_gemv        : u = A_Jᵀ g                                          (SMW rhs)
-// K3  k_gram<true>     : split-K partials of A_JᵀA_J (lower, r × r)            Eq. (19)
+// K3  k_gram<true>     : split-K partials of A_JᵀA_J (lower, r × r) and u = A_Jᵀg Eq. (19)
 //     k_gram<false>    : split-K partials of A_J A_Jᵀ (lower, m × m)            Eq. (18)
 //     k_gram_reduce    : κ⁻¹ I_r + Σ  /  I_m + κ Σ
 // K4  k_chol_cluster   : Cholesky by one thread-block cluster with the forward solve carried
@@ -153,29 +153,6 @@ __global__ void __launch_bounds__(1024) k_combine(int64_t m, const double* __res
       *dot_out = s;
     }
   }
-}
-
-// u[a] = Σ_k A[k, J[a]] g[k]   (one warp per column)
-__global__ void __launch_bounds__(256) k_jt_gemv(const double* __restrict__ A, int64_t m,
-                                                 const int32_t* __restrict__ J, int64_t r,
-                                                 const double* __restrict__ g, double* __restrict__ u,
-                                                 int64_t ustride) {
-  const int lane = threadIdx.x & 31;
-  const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t a = wid; a < r; a += nw) {
-    const double* col = A + (int64_t)J[a] * m;
-    double s = 0.0;
-    for (int64_t k = lane; k < m; k += 32) s = fma(__ldg(col + k), g[k], s);
-    s = warp_allsum(s);
-    if (lane == 0) u[a * ustride] = s;
-  }
-}
-
-// dst[i * stride] = src[i]
-__global__ void k_copy_strided(int64_t n, const double* __restrict__ src, double* __restrict__ dst, int64_t stride) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) dst[i * stride] = src[i];
 }
 
 // ---------------------------------------------------------------------------
