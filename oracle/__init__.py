@@ -73,6 +73,10 @@ def lib():
             "orc_solve": (ctypes.c_int, [_dp, _dp, _i64, _i64, _d, _d, _d, _d, _dp, ctypes.POINTER(Opts), _dp, _dp,
                                          ctypes.POINTER(Stats), ctypes.POINTER(Trace), _i64, _lp]),
             "orc_aty_fused": (_i64, [_dp, _dp, _i64, _i64, _dp, _dp, _d, _d, _d, _dp, _lp, _dp, _dp, _dp]),
+            "orc_dof": (_d, [_dp, _i64, _lp, _i64, _d]),
+            "orc_ols": (ctypes.c_int, [_dp, _dp, _i64, _lp, _i64, _dp, _dp]),
+            "orc_criteria": (None, [_d, _d, _i64, _i64, _dp, _dp]),
+            "orc_model_select": (ctypes.c_int, [_dp, _dp, _i64, _i64, _dp, _d, _dp, _dp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -270,3 +274,41 @@ def aty_fused(A, b, y, x, sigma, l1, l2, with_grad=True):
 def lambda_max_l1(A, b):
     """‖Aᵀb‖∞ (P:411, P:506)."""
     return float(np.max(np.abs(aty(A, b))))
+
+
+# --- Section 3.3: model selection along the path (SURVEY §8(f1)) -------------
+
+def dof(A, J, l2):
+    """ν = tr(A_J (A_JᵀA_J + λ2 I)⁻¹ A_Jᵀ)."""
+    A, m, n, Ap = _A(A)
+    J = np.ascontiguousarray(J, dtype=np.int64)
+    return lib().orc_dof(Ap, m, J.ctypes.data_as(_lp), len(J), l2)
+
+
+def ols(A, b, J):
+    """De-biased least squares on columns J.  Returns (v, rss, ok)."""
+    A, m, n, Ap = _A(A)
+    J = np.ascontiguousarray(J, dtype=np.int64)
+    b, bp = _f64(b)
+    v = np.empty(max(len(J), 1))
+    rss = ctypes.c_double(0)
+    rc = lib().orc_ols(Ap, bp, m, J.ctypes.data_as(_lp), len(J), v.ctypes.data_as(_dp), ctypes.byref(rss))
+    return v[:len(J)].copy(), rss.value, rc == 0
+
+
+def criteria(rss, nu, m, n):
+    """Eq. (21): (gcv, e-bic)."""
+    g, e = ctypes.c_double(0), ctypes.c_double(0)
+    lib().orc_criteria(rss, nu, m, n, ctypes.byref(g), ctypes.byref(e))
+    return g.value, e.value
+
+
+def model_select(A, b, x, l2):
+    """(r, ν, rss, gcv, e-bic, x_debiased) of a solution x."""
+    A, m, n, Ap = _A(A)
+    b, bp = _f64(b)
+    x, xp = _f64(x)
+    xdb = np.empty(n)
+    out = np.empty(5)
+    lib().orc_model_select(Ap, bp, m, n, xp, l2, xdb.ctypes.data_as(_dp), out.ctypes.data_as(_dp))
+    return int(out[0]), out[1], out[2], out[3], out[4], xdb

@@ -571,3 +571,96 @@ i64 orc_aty_fused(const double* A, const double* b, i64 m, i64 n, const double* 
   }
   return r;
 }
+
+/* ------------------------------------------------------------------------- */
+/* Model selection along the λ path (Section 3.3)    */
+/* ------------------------------------------------------------------------- */
+
+/* Degrees of freedom: ν = tr(A_J (A_JᵀA_J + λ2 I_r)⁻¹ A_Jᵀ) = tr((G + λ2 I)⁻¹ G),
+ * G = A_JᵀA_J; computed with the textbook Cholesky of G + λ2 I and r column solves. */
+double orc_dof(const double* A, i64 m, const i64* J, i64 r, double l2) {
+  if (r == 0) return 0.0;
+  double* G = (double*)malloc(sizeof(double) * (size_t)(r * r));
+  double* L = (double*)malloc(sizeof(double) * (size_t)(r * r));
+  double* c = (double*)malloc(sizeof(double) * (size_t)r);
+  for (i64 b = 0; b < r; ++b)
+    for (i64 a = 0; a < r; ++a) {
+      double s = 0.0;
+      for (i64 k = 0; k < m; ++k) s += A[k + J[a] * m] * A[k + J[b] * m];
+      G[a + b * r] = s;
+      L[a + b * r] = s + (a == b ? l2 : 0.0);
+    }
+  double nu = NAN;
+  if (orc_chol(L, r) == 0) {
+    nu = 0.0;
+    for (i64 j = 0; j < r; ++j) { /* column j of (G + λ2 I)⁻¹ G, keep entry j */
+      for (i64 a = 0; a < r; ++a) c[a] = G[a + j * r];
+      orc_chol_solve(L, r, c);
+      nu += c[j];
+    }
+  }
+  free(G); free(L); free(c);
+  return nu;
+}
+
+/* De-biasing by least squares on the selected features: v = argmin ‖A_J v − b‖²
+ * via the normal equations (Cholesky of A_JᵀA_J); *rss = ‖b − A_J v‖².  0 ok, −1 singular. */
+int orc_ols(const double* A, const double* b, i64 m, const i64* J, i64 r, double* v, double* rss) {
+  double* G = (double*)malloc(sizeof(double) * (size_t)((r > 0 ? r : 1) * (r > 0 ? r : 1)));
+  int rc = 0;
+  for (i64 bb = 0; bb < r; ++bb)
+    for (i64 a = 0; a < r; ++a) {
+      double s = 0.0;
+      for (i64 k = 0; k < m; ++k) s += A[k + J[a] * m] * A[k + J[bb] * m];
+      G[a + bb * r] = s;
+    }
+  for (i64 a = 0; a < r; ++a) {
+    double s = 0.0;
+    for (i64 k = 0; k < m; ++k) s += A[k + J[a] * m] * b[k];
+    v[a] = s;
+  }
+  if (r > 0) {
+    if (orc_chol(G, r) != 0) rc = -1;
+    else orc_chol_solve(G, r, v);
+  }
+  double q = 0.0;
+  for (i64 k = 0; k < m; ++k) {
+    double e = b[k];
+    for (i64 a = 0; a < r; ++a) e -= A[k + J[a] * m] * v[a];
+    q += e * e;
+  }
+  *rss = q;
+  free(G);
+  return rc;
+}
+
+/* Eq. (21): gcv = m⁻¹ rss / (1 − ν/m)²;  e-bic = log(rss/m) + (ν/m)(log m + log n). */
+void orc_criteria(double rss, double nu, i64 m, i64 n, double* gcv, double* ebic) {
+  const double dm = (double)m;
+  const double f = 1.0 - nu / dm;
+  *gcv = (rss / dm) / (f * f);
+  *ebic = log(rss / dm) + (nu / dm) * (log(dm) + log((double)n));
+}
+
+/* All model-selection quantities of a solution x: out = [r, ν, rss, gcv, ebic];
+ * xdb (n, nullable) = de-biased coefficients (OLS on supp x, zero elsewhere). */
+int orc_model_select(const double* A, const double* b, i64 m, i64 n, const double* x, double l2, double* xdb,
+                     double* out) {
+  i64* J = (i64*)malloc(sizeof(i64) * (size_t)(n > 0 ? n : 1));
+  i64 r = 0;
+  for (i64 i = 0; i < n; ++i)
+    if (x[i] != 0.0) J[r++] = i;
+  double* v = (double*)malloc(sizeof(double) * (size_t)(r > 0 ? r : 1));
+  double rss = 0.0;
+  int rc = orc_ols(A, b, m, J, r, v, &rss);
+  double nu = orc_dof(A, m, J, r, l2);
+  double gcv, ebic;
+  orc_criteria(rss, nu, m, n, &gcv, &ebic);
+  out[0] = (double)r; out[1] = nu; out[2] = rss; out[3] = gcv; out[4] = ebic;
+  if (xdb) {
+    for (i64 i = 0; i < n; ++i) xdb[i] = 0.0;
+    for (i64 a = 0; a < r; ++a) xdb[J[a]] = v[a];
+  }
+  free(J); free(v);
+  return rc;
+}

@@ -404,7 +404,10 @@ SSN_DEV void inv_block_warp(const double* M, int ld, int b0, int bn, double* S, 
   __syncwarp();
 }
 
-__global__ void __launch_bounds__(256, 1) k_chol_cluster(double* M, int N, int ld, double* __restrict__ out,
+// NR ≥ N + 1 rows: rows N..NR-1 are appended rows C, which leave the factorisation as C L⁻ᵀ.
+// With out != nullptr row N is the right-hand side and the backward solve runs; otherwise the
+// kernel stops after the factorisation (e.g. degrees of freedom from C = A_J).
+__global__ void __launch_bounds__(256, 1) k_chol_cluster(double* M, int N, int NR, int ld, double* __restrict__ out,
                                                          double scale, const double* __restrict__ dotv,
                                                          double* dot_out, double* Winv, int* info,
                                                          const double* __restrict__ ybase, double* __restrict__ yt) {
@@ -417,7 +420,6 @@ __global__ void __launch_bounds__(256, 1) k_chol_cluster(double* M, int N, int l
   double* SB = SA + CHT * TLD;
   double* T = dsm + (size_t)8 * 2 * CHT * TLD;      // CTA-0 diagonal tile
   double* colbuf = T + CHT * TLD;                   // 80 doubles (column broadcast / reciprocals)
-  const int NR = N + 1;
   const int ntc = (N + CHT - 1) / CHT, ntr = (NR + CHT - 1) / CHT;
   const int NWg = CS * 8;
   const int gw = rank + CS * warp;
@@ -577,7 +579,7 @@ __global__ void __launch_bounds__(256, 1) k_chol_cluster(double* M, int N, int l
     STAMP(3 + 2 * k);
   }
   STAMP(40);
-  if (rank != 0) return;
+  if (rank != 0 || out == nullptr) return;
   if (warp == 0) {  // W of the last diagonal block (its panel has no phase C)
     const int kl = ntc - 1;
     inv_block_warp(M, ld, kl * CHT, min(CHT, N - kl * CHT), SA, invg + (size_t)kl * CHT,

@@ -534,7 +534,8 @@ int launch_chol(ssnal_en_problem* P, double* M, int N, double* out, double scale
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  CK(cudaLaunchKernelEx(&cfg, k_chol_cluster, M, N, N + 1, out, scale, dotv, dot_out, P->Winv, P->info, ybase, yt));
+  CK(cudaLaunchKernelEx(&cfg, k_chol_cluster, M, N, N + 1, N + 1, out, scale, dotv, dot_out, P->Winv, P->info,
+                        ybase, yt));
   P->launches++;
   return SSNAL_OK;
 }
