@@ -49,7 +49,9 @@ def test_ols_empty_and_singular():
     A, b = _A(3)
     v, rss, ok = oracle.ols(A, b, np.array([], dtype=np.int64))
     assert ok and rss == pytest.approx(float(b @ b), rel=1e-14)
-    A2 = np.round(A * 4)  # small integers: the Gram of a duplicated column is exactly singular
+    A2 = A.copy()  # duplicated column with ‖a‖² = 25: the Cholesky pivot is exactly 0
+    A2[2] = 0.0
+    A2[2, :2] = [3.0, 4.0]
     A2[5] = A2[2]
     _, _, ok = oracle.ols(A2, b, np.array([2, 5]))
     assert not ok
