@@ -125,6 +125,24 @@ int ssnal_en_epilogue(ssnal_en_problem* p, const double* w0, const double* w1, d
 int ssnal_en_newton_direction(ssnal_en_problem* p, const int32_t* J, int64_t r, const double* g, double kappa,
                               double* d_out, double* gd_out, int32_t* branch_out);
 
+/* Model-selection quantities of the solution of the most recent ssnal_en_solve / _solve_device
+ * on this handle (Section 3.3):
+ *   active = r = |supp x|;
+ *   nu   = tr(A_J (A_JᵀA_J + λ2 I)⁻¹ A_Jᵀ), the Elastic Net degrees of freedom;
+ *   rss  = ‖b − A_J x_ols‖² after de-biasing by least squares on the selected features;
+ *   gcv  = m⁻¹ rss / (1 − ν/m)²,  ebic = log(rss/m) + (ν/m)(log m + log n)   (Eq. (21)).
+ * ols_ok = 0 (and rss, gcv, ebic = NaN) when A_JᵀA_J is not positive definite (r ≥ m or collinear
+ * columns).  xdb_out (host, n, nullable) receives the de-biased coefficients (zero off supp x).
+ * λ2 must equal the one the solution was computed with. */
+typedef struct {
+  int64_t active;
+  double nu, rss, gcv, ebic;
+  int32_t ols_ok;
+  int32_t reserved;
+} ssnal_en_criteria;
+
+int ssnal_en_model_select(ssnal_en_problem* p, double lambda2, double* xdb_out, ssnal_en_criteria* out);
+
 void ssnal_en_destroy(ssnal_en_problem* p);
 
 /* Thread-local message of the last failure on this thread ("" if none). */

@@ -494,9 +494,10 @@ __global__ void __launch_bounds__(256, 1) k_chol_cluster(double* M, int N, int N
     auto do_tile = [&](int q) {
       int ii, jj;
       if (q < ntri) tri_tile(q, &ii, &jj);
-      else {
-        ii = remc;
-        jj = q - ntri;
+      else {  // rectangular part: appended row tiles below the square (rhs row, C rows)
+        const int e = q - ntri;
+        ii = remc + e / remc;
+        jj = e % remc;
       }
       const int i0 = (k + 1 + ii) * CHT, j0 = (k + 1 + jj) * CHT;
       load_tile_rows(M, ld, i0, k0, NR, k0 + kn, SA, lane);
@@ -701,6 +702,67 @@ __global__ void k_init_y(int64_t m, const double* __restrict__ bvec, const doubl
 __global__ void k_scatter(const int32_t* __restrict__ idx, const double* __restrict__ v, int64_t cnt, double* x) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < cnt) x[idx[i]] = v[i];
+}
+
+}  // namespace ssn
+
+// ---------------------------------------------------------------------------
+// Model selection along the λ path (Section 3.3)
+// ---------------------------------------------------------------------------
+namespace ssn {
+
+// Appended rows for the degrees-of-freedom factorisation: rows [row0, row0+m) of M.
+//   ident = 0: C = A_J (M[row0 + k, a] = A[k, J_a], a < r)        (r < m)
+//   ident = 1: C = I_m (M[row0 + k, a] = δ_ka, a < m)              (r ≥ m)
+__global__ void k_fill_rows(double* __restrict__ M, int64_t ld, int64_t row0, const double* __restrict__ A,
+                            int64_t m, const int32_t* __restrict__ J, int64_t ncol, int ident) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= m * ncol) return;
+  const int64_t k = e % m, a = e / m;
+  M[row0 + k + a * ld] = ident ? (k == a ? 1.0 : 0.0) : A[(int64_t)J[a] * m + k];
+}
+
+// Deterministic Σ M[row0+i, j]² over i < nr, j < nc (single CTA, fixed per-thread order + tree).
+__global__ void __launch_bounds__(1024) k_frob(const double* __restrict__ M, int64_t ld, int64_t row0, int64_t nr,
+                                               int64_t nc, double* out) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int64_t e = threadIdx.x; e < nr * nc; e += blockDim.x) {
+    const double v = M[row0 + e % nr + (e / nr) * ld];
+    s += v * v;
+  }
+  s = warp_allsum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    *out = t;
+  }
+}
+
+// ν from the Frobenius sum, rss from the residual, then Eq. (21): out = [ν, rss, gcv, ebic].
+//   r < m:  ν = ‖A_J L⁻ᵀ‖_F²;   r ≥ m: ν = m − λ2 ‖L⁻¹‖_F²   (push-through identity)
+__global__ void k_criteria(const double* __restrict__ frob, int ident, double l2, const double* __restrict__ resid,
+                           int64_t m, int64_t n, const int* ols_info, double* out) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int64_t k = threadIdx.x; k < m; k += blockDim.x) s += resid[k] * resid[k];
+  s = warp_allsum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double rss = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) rss += red[w];
+    if (ols_info == nullptr || *ols_info != 0) rss = nan("");  // OLS undefined / not positive definite
+    const double dm = (double)m;
+    const double nu = ident ? dm - l2 * (*frob) : *frob;
+    const double f = 1.0 - nu / dm;
+    out[0] = nu;
+    out[1] = rss;
+    out[2] = (rss / dm) / (f * f);
+    out[3] = log(rss / dm) + (nu / dm) * (log(dm) + log((double)n));
+  }
 }
 
 }  // namespace ssn

@@ -220,6 +220,7 @@ struct ssnal_en_problem {
   double* u = nullptr;
   double* tmpm = nullptr;
   double* Mmat = nullptr;
+  double* Msel = nullptr;  // model selection: (2m) × m with appended rows (allocated on first use)
   double* Winv = nullptr;  // inverses of the 32 × 32 diagonal blocks of L
   double* W = nullptr;
   int W_splits = 0;
@@ -516,6 +517,27 @@ int fetch_eval(ssnal_en_problem* P, int slot, EvalOut* out) {
   out->psi = h->psi; out->psimag = h->psimag; out->res1 = h->res1; out->yy = h->yy; out->by = h->by; out->gg = h->gg;
   for (int j = 0; j < 4; ++j) out->s[j] = h->s[j];
   out->gd = h->gd; out->r = h->r; out->info = h->info; out->seq = h->seq; out->pad = 0;
+  return SSNAL_OK;
+}
+
+// Cluster Cholesky of the N × N lower part of M with NR − N appended rows (ld ≥ NR); with `out`
+// the first appended row is the right-hand side and the solve (L Lᵀ)⁻¹ rhs is written to out.
+int launch_chol_ex(ssnal_en_problem* P, double* M, int N, int NR, int ld, double* out, double scale,
+                   const double* dotv, double* dot_out, const double* ybase, double* yt, int* info) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(P->cluster);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = P->chol_smem;
+  cfg.stream = P->st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = P->cluster;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, k_chol_cluster, M, N, NR, ld, out, scale, dotv, dot_out, P->Winv, info, ybase, yt));
+  P->launches++;
   return SSNAL_OK;
 }
 
@@ -887,6 +909,7 @@ static void destroy_bufs(ssnal_en_problem* P) {
   cudaFree(P->u);
   cudaFree(P->tmpm);
   cudaFree(P->Mmat);
+  cudaFree(P->Msel);
   cudaFree(P->Winv);
   cudaFree(P->W);
   cudaFree(P->info);
@@ -1137,6 +1160,117 @@ int ssnal_en_newton_direction(ssnal_en_problem* P, const int32_t* J, int64_t r, 
   memcpy(&info, P->scratch_host + 1, 4);
   if (br > 0 && info) {
     set_err("Cholesky pivot not positive");
+    return SSNAL_ENUMERIC;
+  }
+  return SSNAL_OK;
+}
+
+// Section 3.3: ν, OLS de-biasing, rss, GCV, e-BIC for the latest solution.
+int ssnal_en_model_select(ssnal_en_problem* P, double l2, double* xdb_out, ssnal_en_criteria* out) {
+  if (!P || !out || !(l2 >= 0)) {
+    set_err("invalid argument");
+    return SSNAL_EINVAL;
+  }
+  const int64_t m = P->m, n = P->n;
+  CK(cudaMemcpyAsync(P->scratch_host, P->r_dev + 2, 8, cudaMemcpyDeviceToHost, P->st));
+  CK(cudaStreamSynchronize(P->st));
+  int64_t r;
+  memcpy(&r, P->scratch_host, 8);
+  if (!P->Msel) {
+    int rc = alloc((void**)&P->Msel, (size_t)2 * m * m * 8 + 64);
+    if (rc) return rc;
+  }
+  auto splits = [&](int tiles, int64_t K) {
+    int ns = (int)((2 * P->nsm + tiles - 1) / tiles);
+    const int64_t nch = (K + 31) / 32;
+    if (ns > nch) ns = (int)nch;
+    if (ns > P->W_splits) ns = P->W_splits;
+    return ns < 1 ? 1 : ns;
+  };
+  int* info_nu = P->info + 2;
+  int* info_ols = P->info + 3;
+  CK(cudaMemsetAsync(P->info + 2, 0, 2 * sizeof(int), P->st));
+  double* frob = P->scratch + 24;
+  double* crit = P->scratch + 28;
+  const int32_t* J = P->Jx;
+  int rc;
+  int ident = 0;
+  bool ols_possible = false;
+  if (r == 0) {
+    CK(cudaMemsetAsync(frob, 0, 8, P->st));
+  } else if (r < m) {
+    // ν: factor A_JᵀA_J + λ2 I with A_J appended as m rows: ν = ‖A_J L⁻ᵀ‖_F²
+    const int N = (int)r, NR = (int)(r + m);
+    const int nt = (N + 31) / 32, tiles = nt * (nt + 1) / 2, ns = splits(tiles, m);
+    k_gram<true><<<dim3(tiles, ns), 256, 0, P->st>>>(P->A, m, J, r, P->W, r, nullptr);
+    k_gram_reduce<<<(unsigned)((r * r + 255) / 256), 256, 0, P->st>>>(P->W, ns, r, r, l2, 1.0, P->Msel, NR, nullptr);
+    k_fill_rows<<<(unsigned)((m * r + 255) / 256), 256, 0, P->st>>>(P->Msel, NR, r, P->A, m, J, r, 0);
+    P->launches += 3;
+    CKL();
+    if ((rc = launch_chol_ex(P, P->Msel, N, NR, NR, nullptr, 1.0, nullptr, nullptr, nullptr, nullptr, info_nu)))
+      return rc;
+    k_frob<<<1, 1024, 0, P->st>>>(P->Msel, NR, r, m, r, frob);
+    // OLS de-biasing: factor A_JᵀA_J with rhs row A_Jᵀb; v → P->u
+    const int64_t nout = r + 1;
+    const int nt2 = (int)((nout + 31) / 32), tiles2 = nt2 * (nt2 + 1) / 2, ns2 = splits(tiles2, m);
+    k_gram<true><<<dim3(tiles2, ns2), 256, 0, P->st>>>(P->A, m, J, r, P->W, nout, P->b);
+    k_gram_reduce<<<(unsigned)((nout * nout + 255) / 256), 256, 0, P->st>>>(P->W, ns2, nout, r, 0.0, 1.0, P->Mmat,
+                                                                            N + 1, nullptr);
+    P->launches += 3;
+    CKL();
+    if ((rc = launch_chol_ex(P, P->Mmat, N, N + 1, N + 1, P->u, 1.0, nullptr, nullptr, nullptr, nullptr, info_ols)))
+      return rc;
+    int grid = 0;
+    if ((rc = launch_gather(P, J, P->u, r, &grid))) return rc;
+    k_combine<<<1, 1024, 0, P->st>>>(m, P->b, -1.0, P->part_vec, grid, P->tmpm, nullptr, nullptr);  // A_J v − b
+    P->launches++;
+    CKL();
+    ols_possible = true;
+  } else {
+    // r ≥ m: ν = tr(K (K + λ2 I)⁻¹), K = A_J A_Jᵀ, = m − λ2 ‖L⁻¹‖_F² with I_m appended
+    const int N = (int)m, NR = (int)(2 * m);
+    const int nt = (int)((m + 31) / 32), tiles = nt * (nt + 1) / 2, ns = splits(tiles, r);
+    k_gram<false><<<dim3(tiles, ns), 256, 0, P->st>>>(P->A, m, J, r, P->W, m, nullptr);
+    k_gram_reduce<<<(unsigned)((m * m + 255) / 256), 256, 0, P->st>>>(P->W, ns, m, m, l2, 1.0, P->Msel, NR, nullptr);
+    k_fill_rows<<<(unsigned)((m * m + 255) / 256), 256, 0, P->st>>>(P->Msel, NR, m, P->A, m, J, m, 1);
+    P->launches += 3;
+    CKL();
+    if ((rc = launch_chol_ex(P, P->Msel, N, NR, NR, nullptr, 1.0, nullptr, nullptr, nullptr, nullptr, info_nu)))
+      return rc;
+    k_frob<<<1, 1024, 0, P->st>>>(P->Msel, NR, m, m, m, frob);
+    ident = 1;
+  }
+  if (r == 0) {  // x_ols = 0: residual = −b
+    k_combine<<<1, 1024, 0, P->st>>>(m, P->b, -1.0, P->part_vec, 0, P->tmpm, nullptr, nullptr);
+    CK(cudaMemsetAsync(info_ols, 0, sizeof(int), P->st));
+    ols_possible = true;
+  }
+  k_criteria<<<1, 1024, 0, P->st>>>(frob, ident, l2, P->tmpm, m, n, ols_possible ? info_ols : nullptr, crit);
+  P->launches += 2;
+  CKL();
+  CK(cudaMemcpyAsync(P->scratch_host + 28, crit, 4 * 8, cudaMemcpyDeviceToHost, P->st));
+  CK(cudaMemcpyAsync(P->scratch_host + 32, P->info + 2, 2 * sizeof(int), cudaMemcpyDeviceToHost, P->st));
+  if (xdb_out) {
+    CK(cudaMemsetAsync(P->w[2], 0, n * 8, P->st));
+    if (ols_possible && r > 0) {
+      k_scatter<<<(unsigned)((r + 255) / 256), 256, 0, P->st>>>(J, P->u, r, P->w[2]);
+      CKL();
+    }
+    CK(cudaMemcpyAsync(xdb_out, P->w[2], n * 8, cudaMemcpyDeviceToHost, P->st));
+  }
+  CK(cudaStreamSynchronize(P->st));
+  const double* c = P->scratch_host + 28;
+  int infos[2];
+  memcpy(infos, P->scratch_host + 32, 8);
+  out->active = r;
+  out->nu = c[0];
+  out->rss = c[1];
+  out->gcv = c[2];
+  out->ebic = c[3];
+  out->ols_ok = (ols_possible && infos[1] == 0) ? 1 : 0;
+  out->reserved = 0;
+  if (infos[0] != 0) {
+    set_err("degrees-of-freedom factorisation not positive definite");
     return SSNAL_ENUMERIC;
   }
   return SSNAL_OK;

@@ -1,0 +1,42 @@
+"""λ path with warm starts, a max-active cap and model selection (Section 3.3).
+
+Orchestration only: every solve and every criterion (ν, OLS de-biasing, rss, GCV, e-BIC) is
+computed by the C-ABI (ssnal_en_solve / ssnal_en_model_select); this module loops over the grid
+and picks the minimiser of each criterion.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+
+def lambda_grid(n_points: int = 100, c_max: float = 1.0, c_min: float = 0.1) -> np.ndarray:
+    """Log-spaced c values from c_max down to c_min (Table D.4 protocol: 100 points, 1 → 0.1)."""
+    return np.logspace(math.log10(c_max), math.log10(c_min), n_points)
+
+
+def solve_path(P, alpha: float, cs, sigma0: float = 5e-3, tol: float = 1e-6, max_active: int | None = None,
+               select: bool = True, debias: bool = False):
+    """Solve along c ∈ cs with λ1 = c α λmax, λ2 = c (1 − α) λmax, λmax = ‖Aᵀb‖∞/α,
+    warm-starting each point at the previous solution.  The path stops once a
+    solution has at least `max_active` nonzeros.  Returns (points, best) where best maps
+    'gcv' / 'ebic' to the index of the minimising point (None without selection)."""
+    lmax = P.lambda_max_l1 / alpha
+    points = []
+    x = None
+    for c in cs:
+        l1, l2 = c * alpha * lmax, c * (1 - alpha) * lmax
+        x, st = P.solve(l1, l2, sigma0, tol, x0=x)
+        crit, xdb = P.model_select(l2, debias) if select else (None, None)
+        points.append({"c": float(c), "lambda1": l1, "lambda2": l2, "x": x, "stats": st, "criteria": crit,
+                       "x_debiased": xdb})
+        if max_active is not None and st["active"] >= max_active:
+            break
+    best = {}
+    if select:
+        for key in ("gcv", "ebic"):
+            vals = [p["criteria"][key] for p in points]
+            finite = [i for i, v in enumerate(vals) if v == v]
+            best[key] = min(finite, key=lambda i: vals[i]) if finite else None
+    return points, best

@@ -40,6 +40,16 @@ class Stats(ctypes.Structure):
         return d
 
 
+class Criteria(ctypes.Structure):
+    """Mirror of ssnal_en_criteria."""
+
+    _fields_ = [("active", _i64), ("nu", _d), ("rss", _d), ("gcv", _d), ("ebic", _d), ("ols_ok", _i32),
+                ("reserved", _i32)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_ if f != "reserved"}
+
+
 class SsnalError(RuntimeError):
     def __init__(self, code, msg):
         super().__init__(f"ssnal_en error {code}: {msg}")
@@ -69,6 +79,8 @@ def load_library():
         L.ssnal_en_aty_fused.argtypes = [_vp, _vp, _vp, _d, _d, _d, _vp, _vp, _vp, P(_i64), _dp, _vp]
         L.ssnal_en_epilogue.argtypes = [_vp, _vp, _vp, _d, _vp, _d, _d, _d, _vp, _vp, _vp, P(_i64), _dp]
         L.ssnal_en_newton_direction.argtypes = [_vp, _vp, _i64, _vp, _d, _vp, _dp, P(_i32)]
+        L.ssnal_en_model_select.argtypes = [_vp, _d, _dp, P(Criteria)]
+        L.ssnal_en_model_select.restype = ctypes.c_int
         L.ssnal_en_destroy.argtypes = [_vp]
         L.ssnal_en_destroy.restype = None
         L.ssnal_en_last_error.restype = ctypes.c_char_p
@@ -150,6 +162,16 @@ class Problem:
                                              _vp(x0_ptr) if x0_ptr else None, _vp(x_out_ptr), ctypes.byref(st))
         _check(rc, (SSNAL_OK, SSNAL_NOT_CONVERGED, SSNAL_ENUMERIC))
         return st.as_dict()
+
+    def model_select(self, lambda2, debias=False):
+        """ν, rss (after OLS de-biasing), GCV, e-BIC of the latest solution.
+        Returns (criteria dict, de-biased x or None)."""
+        c = Criteria()
+        xdb = np.empty(self.n) if debias else None
+        rc = self._lib.ssnal_en_model_select(self._h, lambda2, xdb.ctypes.data_as(_dp) if debias else None,
+                                             ctypes.byref(c))
+        _check(rc)
+        return c.as_dict(), xdb
 
     # -- kernel hooks (device pointers) --
     def aty_fused(self, y, x, sigma, l1, l2, w_out, J_out, PJ_out, grad_out=0):
