@@ -315,6 +315,52 @@ def bench_reference(args, rank, world):
             "e2e": {"value": t, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
+def bench_select(args):
+    """the Table D.4 protocol on cfg2 — 100 log-spaced c from 1 to 0.1,
+    warm-started, stopping at 100 active features, with ν / OLS de-biasing / GCV / e-BIC at
+    every point.  GPU device time per path vs the oracle doing the same on the host."""
+    import torch
+
+    from paper_2006_03970_b200 import Problem
+    from paper_2006_03970_b200.path import lambda_grid, solve_path
+
+    cfg = synth.CONFIGS["cfg2"]
+    A = synth.design(cfg)
+    b, _ = synth.response(cfg)
+    cs = lambda_grid(100)
+    P = Problem(A, b)
+    for _ in range(max(args.warmup, 1)):
+        solve_path(P, cfg.alpha, cs, max_active=100)
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        pts, best = solve_path(P, cfg.alpha, cs, max_active=100)
+        ts.append(time.perf_counter() - t0)
+    P.close()
+    t_gpu = statistics.median(ts)
+    res = {"metric": "lambda-path with model selection: time per path (s)", "value": t_gpu, "unit": "s",
+           "higher_is_better": False, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "dtype": "f64",
+           "data": "synthetic (synth/, seeded)",
+           "config": {"workload": "cfg2 path: 100 log-spaced c in [0.1, 1], max 100 actives (Table D.4 protocol)",
+                      "points": len(pts), "best_gcv": best["gcv"], "best_ebic": best["ebic"]}}
+    if not args.no_cpu:
+        import oracle
+
+        lm = float(np.max(np.abs(oracle.aty(A, b)))) / cfg.alpha
+        t0 = time.perf_counter()
+        x = None
+        for c in cs:
+            l1, l2 = c * cfg.alpha * lm, c * (1 - cfg.alpha) * lm
+            x, _, st, _ = oracle.solve(A, b, l1, l2, x0=x)
+            oracle.model_select(A, b, x, l2)
+            if st["active"] >= 100:
+                break
+        res["cpu_baseline"] = {"value": time.perf_counter() - t0, "unit": "s", "cores": os.cpu_count(),
+                               "kind": "oracle", "sample": "the same path with the same criteria"}
+    print(json.dumps(res), flush=True)
+
+
 def sweep(args):
     """K1 bandwidth sweep: m = 500, n = 1e5 … 1e7, r ≈ 1e-4 n."""
     import torch
@@ -370,6 +416,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg (40 GB configs)")
     ap.add_argument("--sweep", action="store_true", help="K1 bandwidth sweep instead of the TTS bench")
+    ap.add_argument("--select", action="store_true", help="lambda path with model selection (SURVEY 8(f1))")
     ap.add_argument("--sweep-n", default="100000,200000,500000,1000000,2000000,5000000,10000000")
     ap.add_argument("--sweep-reps", type=int, default=20)
     args = ap.parse_args()
@@ -388,6 +435,9 @@ def main():
 
     if args.sweep:
         sweep(args)
+        return
+    if args.select:
+        bench_select(args)
         return
 
     import torch.distributed as dist
