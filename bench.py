@@ -150,6 +150,7 @@ def bench_ours(args, rank, world, local_rank):
     db = torch.from_numpy(b_host).cuda()
     torch.cuda.synchronize()
     P = Problem.from_device(dA.data_ptr(), db.data_ptr(), m, n, stream.cuda_stream, keep=(dA, db))
+    P.set_option("graph", 1 if args.control == "graph" else 0)
     lm = P.lambda_max_l1
     x_buf = torch.zeros(n, dtype=torch.float64, device="cuda")
 
@@ -198,6 +199,7 @@ def bench_ours(args, rank, world, local_rank):
         for it in range(max(1, min(args.steps, 3)) + 1):
             t0 = time.perf_counter()
             Q = Problem(A_np, b_host)
+            Q.set_option("graph", 1 if args.control == "graph" else 0)
             lmq = Q.lambda_max_l1
             x_prev = None
             hb = 8 * m * n + 8 * m
@@ -244,7 +246,9 @@ def bench_ours(args, rank, world, local_rank):
                                                               if cfg.path else "c=" + ",".join(str(c) for c in cfg.cs)),
                    "m": m, "n": n, "alpha": cfg.alpha, "tol": cfg.tol, "sigma0": cfg.sigma0,
                    "l2_policy": f"A = {8 * m * n / 1e6:.0f} MB > 126 MB L2 (no flush needed)",
-                   "parallelism": f"replicas x{world}"},
+                   "parallelism": f"replicas x{world}",
+                   "control": ("device-resident, one CUDA graph per solve (nested conditional WHILE)"
+                               if args.control == "graph" else "host-driven (per-evaluation readback)")},
         "roofline": {"bound": "hbm", "achieved": k1_gbs, "peak": peak, "unit": "GB/s",
                      "frac": (k1_gbs / peak) if k1_gbs else None, "traffic": traffic,
                      "kernel": "k1_aty_fused", "bytes_per_launch": k1_bytes(m, n), "launches": k1_launches,
@@ -414,6 +418,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg2", choices=list(synth.CONFIGS))
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--control", default="graph", choices=["graph", "host"],
+                    help="graph: Algorithm 1 control on the device in one CUDA graph; host: CPU decisions")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg (40 GB configs)")
     ap.add_argument("--sweep", action="store_true", help="K1 bandwidth sweep instead of the TTS bench")
     ap.add_argument("--select", action="store_true", help="lambda path with model selection (SURVEY 8(f1))")

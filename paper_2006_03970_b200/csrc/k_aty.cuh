@@ -42,6 +42,8 @@ struct K1Params {
   double* part_scal;    // G x 4
   double* part_vec;     // G x m (fused mode; rows Σ P_i a_i)
   Scal sc;
+  const Scal* scp;      // graph mode: σ-dependent scalars on the device (overrides sc)
+  unsigned long long* tstamp;  // nullable: [0] ← min CTA start, [1] ← max CTA end (globaltimer ns)
   int C;                // columns per tile (multiple of 8)
   int64_t T;            // tiles
   int stages;
@@ -96,6 +98,7 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_aty_fused(const K1Params p) 
   const int64_t ntiles = (c_hi - c_lo + C - 1) / C;
 
   if (threadIdx.x == 0) {
+    if (p.tstamp) atomicMin(p.tstamp, global_ns());
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -143,7 +146,7 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_aty_fused(const K1Params p) 
     yr[t] = row < m ? p.y[row] : 0.0;
     gacc[t] = 0.0;
   }
-  const Scal sc = p.sc;
+  const Scal sc = p.scp ? *p.scp : p.sc;
   const bool leader = (lane & 3) == 0;
   const int gcol = lane >> 2;  // column of the 8-group this lane ends up holding
   double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;  // per leader lane, its columns in order
@@ -271,8 +274,16 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_aty_fused(const K1Params p) 
       for (int j = 0; j < 4; ++j) q[j] = p.fused ? __dadd_rn(q[j], rs[wi * 4 + j]) : fmax(q[j], rs[wi * 4 + j]);
     for (int j = 0; j < 4; ++j) p.part_scal[b * 4 + j] = q[j];
   }
+  // kernel-duration stamp: all consumer warps of this CTA are past their last write
+  auto stamp_end = [&]() {
+    if (p.tstamp) {
+      named_bar_sync(1, K1_NWC * 32);
+      if (tid == 0) atomicMax(p.tstamp + 1, global_ns());
+    }
+  };
   if (!p.fused) {
     if (tid == 0) p.cta_cnt[b] = 0;
+    stamp_end();
     return;
   }
   int anyv = 0;
@@ -287,6 +298,7 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_aty_fused(const K1Params p) 
   }
   if (!anyv) {
     if (tid == 0) p.cta_cnt[b] = 0;
+    stamp_end();
     return;
   }
   // ordered compaction: warp wi scans bytes [bw0, bw1) of this CTA's mask range
@@ -326,6 +338,7 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_aty_fused(const K1Params p) 
     }
     off += __shfl_sync(0xffffffffu, incl, 31);
   }
+  stamp_end();
 }
 
 // ---------------------------------------------------------------------------
@@ -345,6 +358,8 @@ struct K1eParams {
   int* cta_cnt;
   double* part_scal;
   Scal sc;
+  const Scal* scp;   // graph mode: device scalars (overrides sc)
+  const double* sp;  // graph mode: device step length (overrides s)
   int C;
   int64_t T;
 };
@@ -355,7 +370,8 @@ __global__ void __launch_bounds__(K1E_THREADS) k1e_epilogue(const K1eParams p) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   int64_t c_lo, c_hi;
   cta_cols(blockIdx.x, gridDim.x, p.T, p.C, p.n, &c_lo, &c_hi);
-  const Scal sc = p.sc;
+  const Scal sc = p.scp ? *p.scp : p.sc;
+  const double step = p.sp ? *p.sp : p.s;
   double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
   int64_t cnt = 0;
   for (int64_t base = c_lo; base < c_hi; base += K1E_THREADS) {
@@ -364,7 +380,7 @@ __global__ void __launch_bounds__(K1E_THREADS) k1e_epilogue(const K1eParams p) {
     double P = 0.0;
     if (i < c_hi) {
       double w = p.w0[i];
-      if (p.w1) w = __dadd_rn(w, __dmul_rn(p.s, __dsub_rn(p.w1[i], w)));
+      if (p.w1) w = __dadd_rn(w, __dmul_rn(step, __dsub_rn(p.w1[i], w)));
       if (p.w_out) p.w_out[i] = w;
       const double xi = p.x[i];
       const double tt = __dsub_rn(xi, __dmul_rn(sc.sigma, w));
@@ -481,9 +497,12 @@ __global__ void __launch_bounds__(K5_THREADS) k_eval_reduce(int64_t m, const dou
                                                             double* __restrict__ g_out, const int64_t* r_in,
                                                             EvalOut* out, double* blk, unsigned* ticket,
                                                             const double* gd_src, const int* info_src,
-                                                            EvalOut* host_out, unsigned long long seq) {
+                                                            EvalOut* host_out, unsigned long long seq,
+                                                            const Scal* scp, const int* pred) {
   __shared__ double red[8][33];
   __shared__ bool last;
+  if (pred && *pred == 0) return;  // graph mode: predicated off (uniform over the grid)
+  if (scp) sc = *scp;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t k = (int64_t)blockIdx.x * 32 + lane;
   if (with_grad) {

@@ -18,6 +18,70 @@
 namespace ssn {
 
 // ---------------------------------------------------------------------------
+// Geometry of the Newton direction for an active set of size r (Eq. (18) / (19)).  Computed by
+// the same function on the host (host-driven mode) and on the device (graph mode), so both
+// modes launch identical work decompositions and produce bitwise-identical results.
+// ---------------------------------------------------------------------------
+struct DirGeo {
+  int branch;          // 0: r = 0 (d = −g), 1: 0 < r < m (SMW, Eq. (19)), 2: r ≥ m (Eq. (18))
+  int N, NR, ld;       // factor order, rows incl. the rhs row, leading dimension of Mmat
+  int tiles, ns;       // Gram lower 32 × 32 tiles and split-K slices
+  int bgrid;           // SMW back-substitution CTAs
+  int pad;
+  long long r, nout, nmat;
+  double diag, mult;   // reduce: M = diag·I + mult·Σ_s W[s]
+};
+
+// split-K slices: enough (tile, slice) items to cover 2 CTAs per SM, ≤ one slice per 32-chunk
+SSN_HD int gram_splits(int nsm, int tiles, long long K, int wsplits) {
+  int ns = (2 * nsm + tiles - 1) / tiles;
+  const long long nch = (K + 31) / 32;
+  if (ns > nch) ns = (int)nch;
+  if (ns > wsplits) ns = wsplits;
+  return ns < 1 ? 1 : ns;
+}
+
+SSN_HD DirGeo make_geo(long long r, long long m, int nsm, int wsplits, double kappa, double kinv) {
+  DirGeo g;
+  g.r = r;
+  g.pad = 0;
+  g.bgrid = 1;
+  if (r == 0) {
+    g.branch = 0;
+    g.N = g.NR = g.ld = g.tiles = g.ns = 0;
+    g.nout = g.nmat = 0;
+    g.diag = g.mult = 0.0;
+  } else if (r < m) {
+    g.branch = 1;
+    g.N = (int)r;
+    g.NR = g.N + 1;
+    g.ld = g.N + 1;
+    g.nout = r + 1;  // index r carries g: row r = u = A_Jᵀg (the rhs row)
+    g.nmat = r;
+    const int nt = (int)((g.nout + 31) / 32);
+    g.tiles = nt * (nt + 1) / 2;
+    g.ns = gram_splits(nsm, g.tiles, m, wsplits);
+    g.diag = kinv;  // κ⁻¹ I_r + A_JᵀA_J (R13)
+    g.mult = 1.0;
+    long long bg = (r + 63) / 64;
+    if (bg > nsm) bg = nsm;
+    g.bgrid = bg < 1 ? 1 : (int)bg;
+  } else {
+    g.branch = 2;
+    g.N = (int)m;
+    g.NR = g.N + 1;
+    g.ld = g.N + 1;
+    g.nout = g.nmat = m;
+    const int nt = (int)((m + 31) / 32);
+    g.tiles = nt * (nt + 1) / 2;
+    g.ns = gram_splits(nsm, g.tiles, r, wsplits);
+    g.diag = 1.0;  // I_m + κ A_J A_Jᵀ
+    g.mult = kappa;
+  }
+  return g;
+}
+
+// ---------------------------------------------------------------------------
 // K2: part_vec[b][k] = Σ_{a ∈ chunk b} coef[a] * A[k, J[a]]
 // ---------------------------------------------------------------------------
 // r is read from r_dev when r < 0 (device-resident count, fixed grid); valid[b] (nullable)
@@ -26,8 +90,10 @@ template <int MR>
 __global__ void __launch_bounds__(256) k_gather_axpy(const double* __restrict__ A, int64_t m,
                                                      const int32_t* __restrict__ J, const double* __restrict__ coef,
                                                      int64_t r, const int64_t* __restrict__ r_dev,
-                                                     double* __restrict__ part_vec, int* __restrict__ valid) {
+                                                     double* __restrict__ part_vec, int* __restrict__ valid,
+                                                     const int* __restrict__ pred) {
   extern __shared__ double red[];  // 8 x m
+  if (pred && *pred == 0) return;  // graph mode: predicated off (the consumer is predicated too)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool devr = r < 0;
   if (devr) r = *r_dev;
@@ -73,12 +139,19 @@ __global__ void __launch_bounds__(256) k_smw_backsub(const double* __restrict__ 
                                                      const int32_t* __restrict__ J, const double* __restrict__ v,
                                                      int64_t r, double* __restrict__ parts, const double* __restrict__ g,
                                                      const double* __restrict__ y, double* __restrict__ d,
-                                                     double* __restrict__ yt, double* gd_out, unsigned* ticket) {
+                                                     double* __restrict__ yt, double* gd_out, unsigned* ticket,
+                                                     int grid_eff, const DirGeo* geo) {
   extern __shared__ double red[];  // 8 x m
   __shared__ bool last;
   __shared__ double wsum[8];
+  if (geo) {  // graph mode: r and the CTA count from the device-computed geometry
+    if (geo->branch != 1) return;
+    r = geo->r;
+    grid_eff = geo->bgrid;
+  }
+  if ((int)blockIdx.x >= grid_eff) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t a_lo = (int64_t)blockIdx.x * r / gridDim.x, a_hi = (int64_t)(blockIdx.x + 1) * r / gridDim.x;
+  const int64_t a_lo = (int64_t)blockIdx.x * r / grid_eff, a_hi = (int64_t)(blockIdx.x + 1) * r / grid_eff;
   double acc[MR];
 #pragma unroll
   for (int t = 0; t < MR; ++t) acc[t] = 0.0;
@@ -104,14 +177,14 @@ __global__ void __launch_bounds__(256) k_smw_backsub(const double* __restrict__ 
   }
   __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) last = (atomicAdd(ticket, 1u) == gridDim.x - 1);
+  if (threadIdx.x == 0) last = (atomicAdd(ticket, 1u) == (unsigned)grid_eff - 1);
   __syncthreads();
   if (!last) return;
   __threadfence();
   double dot = 0.0;
   for (int64_t k = threadIdx.x; k < m; k += blockDim.x) {
     double sacc = 0.0;
-    for (unsigned b = 0; b < gridDim.x; ++b) sacc += __ldcg(parts + (size_t)b * m + k);
+    for (int b = 0; b < grid_eff; ++b) sacc += __ldcg(parts + (size_t)b * m + k);
     const double dk = -g[k] + sacc;
     d[k] = dk;
     yt[k] = __dadd_rn(y[k], __dmul_rn(1.0, dk));
@@ -132,13 +205,14 @@ __global__ void __launch_bounds__(256) k_smw_backsub(const double* __restrict__ 
 __global__ void __launch_bounds__(1024) k_combine(int64_t m, const double* __restrict__ base, double bs,
                                                   const double* __restrict__ parts, int nparts,
                                                   double* __restrict__ out, const double* __restrict__ dotv,
-                                                  double* dot_out) {
+                                                  double* dot_out, const int* __restrict__ valid) {
   __shared__ double red[32];
   const int tid = threadIdx.x;
   double dot = 0.0;
   for (int64_t k = tid; k < m; k += blockDim.x) {
     double s = 0.0;
-    for (int b = 0; b < nparts; ++b) s += parts[(size_t)b * m + k];
+    for (int b = 0; b < nparts; ++b)
+      if (!valid || valid[b]) s += parts[(size_t)b * m + k];
     const double v = (base ? bs * base[k] : 0.0) + s;
     out[k] = v;
     if (dotv) dot += dotv[k] * v;
@@ -169,97 +243,121 @@ SSN_DEV void tri_tile(int q, int* ti, int* tj) {  // q → (ti ≥ tj), row-majo
 // Split-K Gram tiles.  A 32 × 32 operand block element (row ρ, col γ) is A[rowbase+ρ, J[colbase+γ]]:
 //   SMW   (Eq. (19)): out(a, b) = Σ_k A[k,J_a] A[k,J_b]   — blocks over rows k, columns a / b tiles
 //   m × m (Eq. (18)): out(k, l) = Σ_a A[k,J_a] A[l,J_a]   — blocks over row tiles k / l, columns a
-// Each CTA owns one lower tile and one contiguous slice of the reduction index, double-buffers
-// the next 32-slice in registers while computing the current one from smem, and writes its
-// partial tile to W[split]; a reduce kernel sums the splits in order.
+// Work items (lower tile q, slice s), item = q + tiles·s, are taken by persistent CTAs in a
+// grid-stride loop (results do not depend on the grid).  An item owns one contiguous slice of
+// the reduction index, double-buffers the next 32-slice in registers while computing the
+// current one from smem, and writes its partial tile to W[s]; a reduce kernel sums the slices
+// in order.  Graph mode: r, tiles, ns come from the device geometry (predicated on the branch).
 template <bool SMW>
 __global__ void __launch_bounds__(256) k_gram(const double* __restrict__ A, int64_t m,
                                               const int32_t* __restrict__ J, int64_t r, double* __restrict__ W,
-                                              int64_t wld, const double* __restrict__ gext) {
+                                              const double* __restrict__ gext, int tiles, int ns,
+                                              const DirGeo* geo) {
   // SMW: index r (if gext) is the extra column g, so row r of the output is u = A_Jᵀg (Eq. (19) rhs)
   __shared__ double sA[32][33], sB[32][33];
-  int ti, tj;
-  tri_tile(blockIdx.x, &ti, &tj);
-  const int64_t o0 = (int64_t)ti * 32, o1 = (int64_t)tj * 32;   // output tile origin
-  const int s = blockIdx.y, ns = gridDim.y;
-  const int64_t K = SMW ? m : r;                                 // reduction length
+  if (geo) {
+    if (geo->branch != (SMW ? 1 : 2)) return;
+    r = geo->r;
+    tiles = geo->tiles;
+    ns = geo->ns;
+  }
+  const int64_t K = SMW ? m : r;  // reduction length
   const int64_t nch = (K + 31) / 32;
-  const int64_t c_lo = nch * s / ns, c_hi = nch * (s + 1) / ns;  // chunk slice
-  const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
-  // element q of this thread in a 32 × 32 block: e = tid + 256 q → (γ = e >> 5, ρ = e & 31)
-  const double* colA[4];  // SMW: fixed column pointers for the a/b tiles (g for index r)
-  const double* colB[4];
-  if (SMW) {
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int64_t ga = o0 + ty + 8 * q, gb = o1 + ty + 8 * q;
-      colA[q] = ga < r ? A + (int64_t)J[ga] * m : ((ga == r && gext) ? gext : nullptr);
-      colB[q] = gb < r ? A + (int64_t)J[gb] * m : ((gb == r && gext) ? gext : nullptr);
-    }
-  }
-  double va[4], vb[4];
-  auto load = [&](int64_t ch) {
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      if (SMW) {
-        const int64_t k = ch * 32 + tx;
-        va[q] = (colA[q] && k < m) ? __ldg(colA[q] + k) : 0.0;
-        vb[q] = (colB[q] && k < m) ? __ldg(colB[q] + k) : 0.0;
-      } else {
-        const int64_t a = ch * 32 + ty + 8 * q;
-        const bool ok = a < r;
-        const int64_t cb = ok ? (int64_t)J[a] * m : 0;
-        va[q] = (ok && o0 + tx < m) ? __ldg(A + cb + o0 + tx) : 0.0;
-        vb[q] = (ok && o1 + tx < m) ? __ldg(A + cb + o1 + tx) : 0.0;
-      }
-    }
-  };
-  double acc[4] = {0, 0, 0, 0};
-  if (c_lo < c_hi) load(c_lo);
-  for (int64_t ch = c_lo; ch < c_hi; ++ch) {
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {  // sX[reduction idx][output idx]
-      if (SMW) {
-        sA[tx][ty + 8 * q] = va[q];
-        sB[tx][ty + 8 * q] = vb[q];
-      } else {
-        sA[ty + 8 * q][tx] = va[q];
-        sB[ty + 8 * q][tx] = vb[q];
-      }
-    }
-    __syncthreads();
-    if (ch + 1 < c_hi) load(ch + 1);
-#pragma unroll 8
-    for (int kk = 0; kk < 32; ++kk) {
-      const double bv = sB[kk][tx];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) acc[q] = fma(sA[kk][ty * 4 + q], bv, acc[q]);
-    }
-    __syncthreads();
-  }
   const int64_t nout = SMW ? r + (gext ? 1 : 0) : m;
-  double* Ws = W + (size_t)s * wld * nout;
+  const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
+  for (int item = blockIdx.x; item < tiles * ns; item += gridDim.x) {
+    int ti, tj;
+    tri_tile(item % tiles, &ti, &tj);
+    const int s = item / tiles;
+    const int64_t o0 = (int64_t)ti * 32, o1 = (int64_t)tj * 32;   // output tile origin
+    const int64_t c_lo = nch * s / ns, c_hi = nch * (s + 1) / ns;  // chunk slice
+    // element q of this thread in a 32 × 32 block: e = tid + 256 q → (γ = e >> 5, ρ = e & 31)
+    const double* colA[4];  // SMW: fixed column pointers for the a/b tiles (g for index r)
+    const double* colB[4];
+    if (SMW) {
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const int64_t i = o0 + ty * 4 + q, j = o1 + tx;
-    if (i < nout && j < nout && i >= j) Ws[i + j * wld] = acc[q];
+      for (int q = 0; q < 4; ++q) {
+        const int64_t ga = o0 + ty + 8 * q, gb = o1 + ty + 8 * q;
+        colA[q] = ga < r ? A + (int64_t)J[ga] * m : ((ga == r && gext) ? gext : nullptr);
+        colB[q] = gb < r ? A + (int64_t)J[gb] * m : ((gb == r && gext) ? gext : nullptr);
+      }
+    }
+    double va[4], vb[4];
+    auto load = [&](int64_t ch) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (SMW) {
+          const int64_t k = ch * 32 + tx;
+          va[q] = (colA[q] && k < m) ? __ldg(colA[q] + k) : 0.0;
+          vb[q] = (colB[q] && k < m) ? __ldg(colB[q] + k) : 0.0;
+        } else {
+          const int64_t a = ch * 32 + ty + 8 * q;
+          const bool ok = a < r;
+          const int64_t cb = ok ? (int64_t)J[a] * m : 0;
+          va[q] = (ok && o0 + tx < m) ? __ldg(A + cb + o0 + tx) : 0.0;
+          vb[q] = (ok && o1 + tx < m) ? __ldg(A + cb + o1 + tx) : 0.0;
+        }
+      }
+    };
+    double acc[4] = {0, 0, 0, 0};
+    if (c_lo < c_hi) load(c_lo);
+    for (int64_t ch = c_lo; ch < c_hi; ++ch) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {  // sX[reduction idx][output idx]
+        if (SMW) {
+          sA[tx][ty + 8 * q] = va[q];
+          sB[tx][ty + 8 * q] = vb[q];
+        } else {
+          sA[ty + 8 * q][tx] = va[q];
+          sB[ty + 8 * q][tx] = vb[q];
+        }
+      }
+      __syncthreads();
+      if (ch + 1 < c_hi) load(ch + 1);
+#pragma unroll 8
+      for (int kk = 0; kk < 32; ++kk) {
+        const double bv = sB[kk][tx];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[q] = fma(sA[kk][ty * 4 + q], bv, acc[q]);
+      }
+      __syncthreads();
+    }
+    double* Ws = W + (size_t)s * nout * nout;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t i = o0 + ty * 4 + q, j = o1 + tx;
+      if (i < nout && j < nout && i >= j) Ws[i + j * nout] = acc[q];
+    }
   }
 }
 
 // M[i + j*ld] = diag·[i == j] + mult · Σ_s W[s][i + j*nout]   (i ≥ j, j < nmat)
 //   SMW:   diag = κ⁻¹, mult = 1; nout = nmat + 1: row nmat is the rhs u = A_Jᵀg (unscaled)
 //   m × m: diag = 1, mult = κ (oracle: κ s + δ); nout = nmat; rhs row ← g (if g)
+// Grid-stride; graph mode reads the sizes from the device geometry (predicated on the branch).
 __global__ void k_gram_reduce(const double* __restrict__ W, int ns, int64_t nout, int64_t nmat, double diag,
-                              double mult, double* __restrict__ M, int64_t ld, const double* __restrict__ g) {
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (g && e < nmat) M[nmat + e * ld] = g[e];
-  if (e >= nout * nout) return;
-  const int64_t i = e % nout, j = e / nout;
-  if (i < j || j >= nmat) return;
-  double s = 0.0;
-  for (int q = 0; q < ns; ++q) s += W[(size_t)q * nout * nout + e];
-  if (i < nmat) M[i + j * ld] = (mult == 1.0 ? s : mult * s) + (i == j ? diag : 0.0);
-  else M[i + j * ld] = s;  // rhs row
+                              double mult, double* __restrict__ M, int64_t ld, const double* __restrict__ g,
+                              const DirGeo* geo, int want) {
+  if (geo) {
+    if (geo->branch != want) return;
+    ns = geo->ns;
+    nout = geo->nout;
+    nmat = geo->nmat;
+    diag = geo->diag;
+    mult = geo->mult;
+    ld = geo->ld;
+  }
+  const int64_t tot = nout * nout > nmat ? nout * nout : nmat;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+    if (g && e < nmat) M[nmat + e * ld] = g[e];
+    if (e >= nout * nout) continue;
+    const int64_t i = e % nout, j = e / nout;
+    if (i < j || j >= nmat) continue;
+    double s = 0.0;
+    for (int q = 0; q < ns; ++q) s += W[(size_t)q * nout * nout + e];
+    if (i < nmat) M[i + j * ld] = (mult == 1.0 ? s : mult * s) + (i == j ? diag : 0.0);
+    else M[i + j * ld] = s;  // rhs row
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -410,8 +508,15 @@ SSN_DEV void inv_block_warp(const double* M, int ld, int b0, int bn, double* S, 
 __global__ void __launch_bounds__(256, 1) k_chol_cluster(double* M, int N, int NR, int ld, double* __restrict__ out,
                                                          double scale, const double* __restrict__ dotv,
                                                          double* dot_out, double* Winv, int* info,
-                                                         const double* __restrict__ ybase, double* __restrict__ yt) {
+                                                         const double* __restrict__ ybase, double* __restrict__ yt,
+                                                         const DirGeo* geo, int want) {
   namespace cg = cooperative_groups;
+  if (geo) {  // graph mode: order from the device geometry; whole cluster exits together
+    if (geo->branch != want) return;
+    N = geo->N;
+    NR = geo->NR;
+    ld = geo->ld;
+  }
   cg::cluster_group cl = cg::this_cluster();
   const int rank = (int)cl.block_rank(), CS = (int)cl.num_blocks();
   extern __shared__ double dsm[];
@@ -658,13 +763,15 @@ __global__ void __launch_bounds__(256, 1) k_chol_cluster(double* M, int N, int N
 constexpr size_t kCholSmem = (size_t)(8 * 2 * CHT * TLD + CHT * TLD + 80) * sizeof(double);
 
 // y ← y + s·d  (m-vector) and small helpers
-__global__ void k_axpy_m(int64_t m, const double* y, double s, const double* d, double* out) {
+__global__ void k_axpy_m(int64_t m, const double* y, double s, const double* d, double* out, const double* sp) {
+  if (sp) s = *sp;
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k < m) out[k] = __dadd_rn(y[k], __dmul_rn(s, d[k]));
 }
 __global__ void k_neg_copy(int64_t m, const double* g, double* d, const double* dotv, double* dot_out,
-                           const double* y, double* yt) {
+                           const double* y, double* yt, const DirGeo* geo) {
   __shared__ double red[32];
+  if (geo && geo->branch != 0) return;
   double dot = 0.0;
   for (int64_t k = threadIdx.x; k < m; k += blockDim.x) {
     d[k] = -g[k];
@@ -682,7 +789,9 @@ __global__ void k_neg_copy(int64_t m, const double* g, double* d, const double* 
 }
 
 // x ← P: zero x on the old support, then scatter (J, P_J).
-__global__ void k_zero_at(const int32_t* __restrict__ idx, int64_t cnt, const int64_t* cnt_dev, double* x) {
+__global__ void k_zero_at(const int32_t* __restrict__ idx, int64_t cnt, const int64_t* cnt_dev, double* x,
+                          const int* skip) {
+  if (skip && *skip) return;
   if (cnt < 0) cnt = *cnt_dev;  // grid-stride with a device-resident count
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += (int64_t)gridDim.x * blockDim.x)
     x[idx[i]] = 0.0;

@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "k_aty.cuh"
+#include "k_ctl.cuh"
 #include "k_newton.cuh"
 #include "ssnal_en.h"
 
@@ -81,7 +82,7 @@ int mr_bucket(int64_t m) {
 
 typedef void (*k1_fn)(const K1Params);
 typedef void (*gax_fn)(const double*, int64_t, const int32_t*, const double*, int64_t, const int64_t*, double*,
-                       int*);
+                       int*, const int*);
 
 k1_fn k1_for(int mr) {
   switch (mr) {
@@ -95,7 +96,7 @@ k1_fn k1_for(int mr) {
   }
 }
 typedef void (*bsub_fn)(const double*, int64_t, const int32_t*, const double*, int64_t, double*, const double*,
-                        const double*, double*, double*, double*, unsigned*);
+                        const double*, double*, double*, double*, unsigned*, int, const DirGeo*);
 bsub_fn bsub_for(int mr) {
   switch (mr) {
     case 1: return k_smw_backsub<1>;
@@ -249,6 +250,18 @@ struct ssnal_en_problem {
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> k1_pending;
   double k1_time = 0;
   int k1_count = 0;
+  // graph mode (device-resident control, k_ctl.cuh)
+  int use_graph = 1;
+  ssn::DevCtl* ctl = nullptr;       // device control block
+  ssn::DevCtl* ctl_host = nullptr;  // pinned staging (inputs in, results back)
+  EvalOut* ev_out_host = nullptr;   // pinned: final EvalOut of the current point
+  bool capturing = false;
+  int cap_depth = 0;
+  cudaStream_t cap[3] = {nullptr, nullptr, nullptr};
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  int seg_kernels[5] = {0, 0, 0, 0, 0};
+  bool graph_pending = false;
 };
 
 namespace {
@@ -361,6 +374,9 @@ int allocate(ssnal_en_problem* P) {
   memset(P->ev_host, 0, sizeof(EvalOut) * 4);
   CK(cudaHostGetDevicePointer((void**)&P->ev_host_dev, P->ev_host, 0));
   CK(cudaMallocHost((void**)&P->scratch_host, 64 * 8));
+  AL(P->ctl, sizeof(DevCtl));
+  CK(cudaMallocHost((void**)&P->ctl_host, sizeof(DevCtl)));
+  CK(cudaMallocHost((void**)&P->ev_out_host, sizeof(EvalOut)));
   return SSNAL_OK;
 }
 
@@ -391,7 +407,8 @@ void harvest_k1(ssnal_en_problem* P) {  // call after a stream sync
 }
 
 // K1 at y (device, m).  fused=0: plain w = Aᵀy into w_out (+ per-CTA max|w|).
-int launch_k1(ssnal_en_problem* P, const double* y, const double* x, const Scal& sc, int fused, double* w_out) {
+int launch_k1(ssnal_en_problem* P, const double* y, const double* x, const Scal& sc, int fused, double* w_out,
+              const Scal* scp = nullptr, unsigned long long* tstamp = nullptr) {
   K1Params k;
   k.A = P->A;
   k.m = P->m;
@@ -406,6 +423,8 @@ int launch_k1(ssnal_en_problem* P, const double* y, const double* x, const Scal&
   k.part_scal = P->part_scal;
   k.part_vec = fused ? P->part_vec : nullptr;
   k.sc = sc;
+  k.scp = scp;
+  k.tstamp = tstamp;
   k.C = P->C;
   k.T = P->T;
   k.stages = P->S;
@@ -413,14 +432,15 @@ int launch_k1(ssnal_en_problem* P, const double* y, const double* x, const Scal&
   k.stage_elems = P->stage_elems;
   k.xstage_elems = P->xstage_elems;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
-  if (P->time_k1) {
+  const bool ev_time = P->time_k1 && !P->capturing;
+  if (ev_time) {
     e0 = take_event(P);
     e1 = take_event(P);
     cudaEventRecord(e0, P->st);
   }
   k1_for(P->MR)<<<P->G, K1_THREADS, P->k1_smem, P->st>>>(k);
   P->launches++;
-  if (P->time_k1) {
+  if (ev_time) {
     cudaEventRecord(e1, P->st);
     P->k1_pending.push_back({e0, e1});
   }
@@ -429,7 +449,7 @@ int launch_k1(ssnal_en_problem* P, const double* y, const double* x, const Scal&
 }
 
 int launch_k1e(ssnal_en_problem* P, const double* w0, const double* w1, double s, const double* x, const Scal& sc,
-               double* w_out) {
+               double* w_out, const Scal* scp = nullptr, const double* sp = nullptr) {
   K1eParams k;
   k.n = P->n;
   k.w0 = w0;
@@ -442,6 +462,8 @@ int launch_k1e(ssnal_en_problem* P, const double* w0, const double* w1, double s
   k.cta_cnt = P->cta_cnt;
   k.part_scal = P->part_scal;
   k.sc = sc;
+  k.scp = scp;
+  k.sp = sp;
   k.C = P->C;
   k.T = P->T;
   k1e_epilogue<<<P->G, K1E_THREADS, 0, P->st>>>(k);
@@ -462,7 +484,8 @@ int launch_gather(ssnal_en_problem* P, const int32_t* J, const double* coef, int
   int grid = (int)((r + 63) / 64);
   if (grid > P->gax_grid) grid = P->gax_grid;
   if (grid < 1) grid = 1;
-  gax_for(P->MR)<<<grid, 256, (size_t)8 * P->m * 8, P->st>>>(P->A, P->m, J, coef, r, nullptr, P->part_vec, nullptr);
+  gax_for(P->MR)<<<grid, 256, (size_t)8 * P->m * 8, P->st>>>(P->A, P->m, J, coef, r, nullptr, P->part_vec, nullptr,
+                                                                          nullptr);
   P->launches++;
   *grid_out = grid;
   CKL();
@@ -471,9 +494,10 @@ int launch_gather(ssnal_en_problem* P, const int32_t* J, const double* coef, int
 
 // Same with r resident on the device (no host round trip): fixed grid, validity flags in gax_valid.
 constexpr int kGatherDevGrid = 128;
-int launch_gather_dev(ssnal_en_problem* P, const int32_t* J, const double* coef, const int64_t* r_dev) {
+int launch_gather_dev(ssnal_en_problem* P, const int32_t* J, const double* coef, const int64_t* r_dev,
+                      const int* pred = nullptr) {
   gax_for(P->MR)<<<kGatherDevGrid, 256, (size_t)8 * P->m * 8, P->st>>>(P->A, P->m, J, coef, -1, r_dev, P->part_vec,
-                                                                       P->gax_valid);
+                                                                       P->gax_valid, pred);
   P->launches++;
   CKL();
   return SSNAL_OK;
@@ -481,12 +505,14 @@ int launch_gather_dev(ssnal_en_problem* P, const int32_t* J, const double* coef,
 
 int launch_eval(ssnal_en_problem* P, const double* y, const Scal& sc, int with_grad, const int* valid, int nparts,
                 double* g_out, const int64_t* r_dev, int slot, const double* gd_src = nullptr,
-                const int* info_src = nullptr) {
+                const int* info_src = nullptr, const Scal* scp = nullptr, const int* pred = nullptr) {
   const unsigned nblk = (unsigned)((P->m + 31) / 32);
-  ++P->ev_seq;
+  if (!P->capturing) ++P->ev_seq;
+  // graph mode: no mapped host mirror (decisions are taken on the device)
   k_eval_reduce<<<nblk, K5_THREADS, 0, P->st>>>(P->m, y, P->b, P->part_vec, valid, nparts, P->part_scal, P->G, sc,
                                                  P->nb, with_grad, g_out, r_dev, P->ev_dev + slot, P->blk,
-                                                 P->ticket, gd_src, info_src, P->ev_host_dev + slot, P->ev_seq);
+                                                 P->ticket, gd_src, info_src,
+                                                 P->capturing ? nullptr : P->ev_host_dev + slot, P->ev_seq, scp, pred);
   P->launches++;
   CKL();
   return SSNAL_OK;
@@ -536,14 +562,17 @@ int launch_chol_ex(ssnal_en_problem* P, double* M, int N, int NR, int ld, double
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  CK(cudaLaunchKernelEx(&cfg, k_chol_cluster, M, N, NR, ld, out, scale, dotv, dot_out, P->Winv, info, ybase, yt));
+  const DirGeo* nog = nullptr;
+  CK(cudaLaunchKernelEx(&cfg, k_chol_cluster, M, N, NR, ld, out, scale, dotv, dot_out, P->Winv, info, ybase, yt, nog,
+                        0));
   P->launches++;
   return SSNAL_OK;
 }
 
 // Cluster Cholesky + both triangular solves: M holds the matrix (ld = N+1) and the rhs in row N.
 int launch_chol(ssnal_en_problem* P, double* M, int N, double* out, double scale, const double* dotv,
-                double* dot_out, const double* ybase = nullptr, double* yt = nullptr) {
+                double* dot_out, const double* ybase = nullptr, double* yt = nullptr, const DirGeo* geo = nullptr,
+                int want = 0) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(P->cluster);
   cfg.blockDim = dim3(256);
@@ -557,9 +586,17 @@ int launch_chol(ssnal_en_problem* P, double* M, int N, double* out, double scale
   cfg.attrs = at;
   cfg.numAttrs = 1;
   CK(cudaLaunchKernelEx(&cfg, k_chol_cluster, M, N, N + 1, N + 1, out, scale, dotv, dot_out, P->Winv, P->info,
-                        ybase, yt));
+                        ybase, yt, geo, want));
   P->launches++;
   return SSNAL_OK;
+}
+
+// Gram / reduce grids: persistent CTAs (results do not depend on the grid; DirGeo fixes the work)
+int gram_grid(ssnal_en_problem* P, int items) { return items < 2 * P->nsm ? (items < 1 ? 1 : items) : 2 * P->nsm; }
+unsigned reduce_grid(ssnal_en_problem* P, int64_t tot) {
+  int64_t g = (tot + 255) / 256;
+  if (g > 4 * P->nsm) g = 4 * P->nsm;
+  return (unsigned)(g < 1 ? 1 : g);
 }
 
 // Newton direction for (J, r) at gradient g: d ← solution, *gd_dev ← gᵀd (Eq. (18)/(19)); if yt,
@@ -567,60 +604,69 @@ int launch_chol(ssnal_en_problem* P, double* M, int N, double* out, double scale
 int newton_direction(ssnal_en_problem* P, const int32_t* J, int64_t r, const double* g, double kappa, double* d,
                      double* gd_dev, int* branch, const double* y = nullptr, double* yt = nullptr) {
   const int64_t m = P->m;
-  if (r == 0) {
-    k_neg_copy<<<1, 1024, 0, P->st>>>(m, g, d, g, gd_dev, y, yt);
+  const DirGeo geo = make_geo(r, m, P->nsm, P->W_splits, kappa, 1.0 / kappa);
+  *branch = geo.branch;
+  if (geo.branch == 0) {
+    k_neg_copy<<<1, 1024, 0, P->st>>>(m, g, d, g, gd_dev, y, yt, nullptr);
     P->launches++;
     CKL();
-    *branch = 0;
     return SSNAL_OK;
   }
   CK(cudaMemsetAsync(P->info, 0, sizeof(int), P->st));
-  // K3: split-K Gram over enough CTAs to cover the GPU (2 per SM), ≤ W_splits slices
-  auto splits = [&](int tiles, int64_t K) {
-    int ns = (int)((2 * P->nsm + tiles - 1) / tiles);
-    const int64_t nch = (K + 31) / 32;
-    if (ns > nch) ns = (int)nch;
-    if (ns > P->W_splits) ns = P->W_splits;
-    return ns < 1 ? 1 : ns;
-  };
-  if (r < m) {  // Sherman–Morrison–Woodbury, Eq. (19): factor κ⁻¹I_r + A_JᵀA_J (R13)
-    const int N = (int)r;
-    const int64_t nout = r + 1;  // index r carries g: row r = u = A_Jᵀg (the rhs row)
-    const int nt = (int)((nout + 31) / 32), tiles = nt * (nt + 1) / 2;
-    const int ns = splits(tiles, m);
-    k_gram<true><<<dim3(tiles, ns), 256, 0, P->st>>>(P->A, m, J, r, P->W, nout, g);
+  if (geo.branch == 1) {  // Sherman–Morrison–Woodbury, Eq. (19): factor κ⁻¹I_r + A_JᵀA_J (R13)
+    k_gram<true><<<gram_grid(P, geo.tiles * geo.ns), 256, 0, P->st>>>(P->A, m, J, r, P->W, g, geo.tiles, geo.ns,
+                                                                      nullptr);
     P->launches++;
     CKL();
-    k_gram_reduce<<<(unsigned)((nout * nout + 255) / 256), 256, 0, P->st>>>(P->W, ns, nout, r, 1.0 / kappa, 1.0,
-                                                                            P->Mmat, N + 1, nullptr);
+    k_gram_reduce<<<reduce_grid(P, geo.nout * geo.nout), 256, 0, P->st>>>(P->W, geo.ns, geo.nout, geo.nmat, geo.diag,
+                                                                          geo.mult, P->Mmat, geo.ld, nullptr, nullptr, 0);
     P->launches++;
     CKL();
-    int rc = launch_chol(P, P->Mmat, N, P->u, 1.0, nullptr, nullptr);  // v = (κ⁻¹I + G)⁻¹ u
+    int rc = launch_chol(P, P->Mmat, geo.N, P->u, 1.0, nullptr, nullptr);  // v = (κ⁻¹I + G)⁻¹ u
     if (rc) return rc;
-    int grid = (int)((r + 63) / 64);
-    if (grid > P->gax_grid) grid = P->gax_grid;
-    if (grid < 1) grid = 1;
     // d = −g + A_J v, gᵀd, y_t = y + d (last-CTA finalisation)
-    bsub_for(P->MR)<<<grid, 256, (size_t)8 * m * 8, P->st>>>(P->A, m, J, P->u, r, P->part_vec, g, y ? y : g, d,
-                                                             yt ? yt : P->tmpm, gd_dev, P->ticket);
+    bsub_for(P->MR)<<<geo.bgrid, 256, (size_t)8 * m * 8, P->st>>>(P->A, m, J, P->u, r, P->part_vec, g, y ? y : g, d,
+                                                                  yt ? yt : P->tmpm, gd_dev, P->ticket, geo.bgrid,
+                                                                  nullptr);
     P->launches++;
     CKL();
-    *branch = 1;
     return SSNAL_OK;
   }
   // r ≥ m: Eq. (18), M = I_m + κ A_J A_Jᵀ; the reduce also writes g into the rhs row
-  const int nt = (int)((m + 31) / 32), tiles = nt * (nt + 1) / 2;
-  const int ns = splits(tiles, r);
-  k_gram<false><<<dim3(tiles, ns), 256, 0, P->st>>>(P->A, m, J, r, P->W, m, nullptr);
+  k_gram<false><<<gram_grid(P, geo.tiles * geo.ns), 256, 0, P->st>>>(P->A, m, J, r, P->W, nullptr, geo.tiles,
+                                                                     geo.ns, nullptr);
   P->launches++;
   CKL();
-  k_gram_reduce<<<(unsigned)((m * m + 255) / 256), 256, 0, P->st>>>(P->W, ns, m, m, 1.0, kappa, P->Mmat, m + 1, g);
+  k_gram_reduce<<<reduce_grid(P, m * m), 256, 0, P->st>>>(P->W, geo.ns, m, m, geo.diag, geo.mult, P->Mmat, geo.ld, g,
+                                                          nullptr, 0);
   P->launches++;
   CKL();
-  int rc = launch_chol(P, P->Mmat, (int)m, d, -1.0, g, gd_dev, y, yt);  // d = −M⁻¹ g, gd = gᵀd
+  return launch_chol(P, P->Mmat, (int)m, d, -1.0, g, gd_dev, y, yt);  // d = −M⁻¹ g, gd = gᵀd
+}
+
+// Graph mode: every branch's kernels, predicated on the device geometry C->geo (computed by the
+// control kernels from r); worst-case grids, surplus CTAs exit.  Same work decomposition as
+// newton_direction for the same r.  Reads J[0], g[0], y[0]; writes d, y[1], gᵀd → scratch[0].
+int newton_direction_graph(ssnal_en_problem* P) {
+  const int64_t m = P->m;
+  const DirGeo* geo = &P->ctl->geo;
+  const int32_t* J = P->J[0];
+  const double* g = P->g[0];
+  double* gd = P->scratch;
+  k_neg_copy<<<1, 1024, 0, P->st>>>(m, g, P->d, g, gd, P->y[0], P->y[1], geo);
+  k_gram<true><<<2 * P->nsm, 256, 0, P->st>>>(P->A, m, J, 0, P->W, g, 0, 0, geo);
+  k_gram_reduce<<<reduce_grid(P, m * m), 256, 0, P->st>>>(P->W, 0, 0, 0, 0.0, 0.0, P->Mmat, 0, nullptr, geo, 1);
+  P->launches += 3;
+  CKL();
+  int rc = launch_chol(P, P->Mmat, 0, P->u, 1.0, nullptr, nullptr, nullptr, nullptr, geo, 1);
   if (rc) return rc;
-  *branch = 2;
-  return SSNAL_OK;
+  bsub_for(P->MR)<<<P->nsm, 256, (size_t)8 * m * 8, P->st>>>(P->A, m, J, P->u, 0, P->part_vec, g, P->y[0], P->d,
+                                                             P->y[1], gd, P->ticket, 0, geo);
+  k_gram<false><<<2 * P->nsm, 256, 0, P->st>>>(P->A, m, J, 0, P->W, nullptr, 0, 0, geo);
+  k_gram_reduce<<<reduce_grid(P, m * m), 256, 0, P->st>>>(P->W, 0, 0, 0, 0.0, 0.0, P->Mmat, 0, g, geo, 2);
+  P->launches += 3;
+  CKL();
+  return launch_chol(P, P->Mmat, 0, P->d, -1.0, g, gd, P->y[0], P->y[1], geo, 2);
 }
 
 int check_args(ssnal_en_problem* P, double l1, double l2, double sigma0, double tol) {
@@ -644,27 +690,21 @@ int check_args(ssnal_en_problem* P, double l1, double l2, double sigma0, double 
 }
 
 // ---------------- Algorithm 1 ----------------
-// x (P->x) holds x0 on entry (device); on exit P->x holds the solution.
-int solve_core(ssnal_en_problem* P, double l1, double l2, double sigma0, double tol, int have_x0,
-               ssnal_en_stats* S) {
+// Start point (both modes).  x (P->x) holds x0 on entry (device).  Writes the support of x
+// (Jx, Px, r_dev[2]), y0 into y[0] and w0 = Aᵀy0 into w[0].  *rx = host-known |supp x| (0 cold,
+// −1 = on the device only).
+int init_point(ssnal_en_problem* P, int have_x0, ssnal_en_stats* S, int64_t* rx) {
   const int64_t m = P->m, n = P->n;
-  memset(S, 0, sizeof(*S));
   int rc;
-  int cur = 0;  // index of current J/PJ/y/g
-  int wcur = 0; // index of current w buffer (0..2)
-  EvalOut ev, evt;
-
   // Support of x (Jx, Px, rx): K1e with w = 0, σ = 1, λ = 0 selects x ≠ 0 and P = x.
-  // rx: size of supp(x) — host-known after the first outer step; before it (warm start) the count
-  // lives on the device only (rx = -1) and every consumer reads r_dev[2] there (no round trip).
-  int64_t rx = 0;
+  *rx = 0;
   if (have_x0) {
     CK(cudaMemsetAsync(P->w[2], 0, n * 8, P->st));
     const Scal s0 = make_scal(1.0, 0.0, 0.0);
     if ((rc = launch_k1e(P, P->w[2], nullptr, 0.0, P->x, s0, nullptr))) return rc;
     if ((rc = launch_finalize(P, P->Jx, P->Px, P->r_dev + 2))) return rc;
     CK(cudaMemcpyAsync(P->r_dev + 4, P->r_dev + 2, 8, cudaMemcpyDeviceToDevice, P->st));  // |supp x0| for stats
-    rx = -1;
+    *rx = -1;
   } else {
     CK(cudaMemsetAsync(P->x, 0, n * 8, P->st));
     CK(cudaMemsetAsync(P->r_dev + 2, 0, 8, P->st));
@@ -673,15 +713,46 @@ int solve_core(ssnal_en_problem* P, double l1, double l2, double sigma0, double 
   // Initial y, w (P:242 silent; reading R8): y0 = A x0 − b if x0 ≠ 0, else 0 (decided on the device)
   if (have_x0 && P->init_mode == 1) {
     if ((rc = launch_gather_dev(P, P->Jx, P->Px, P->r_dev + 2))) return rc;
-    k_init_y<<<1, 1024, 0, P->st>>>(m, P->b, P->part_vec, P->gax_valid, kGatherDevGrid, P->r_dev + 2, P->y[cur]);
+    k_init_y<<<1, 1024, 0, P->st>>>(m, P->b, P->part_vec, P->gax_valid, kGatherDevGrid, P->r_dev + 2, P->y[0]);
     P->launches++;
     CKL();
-    if ((rc = launch_k1(P, P->y[cur], nullptr, make_scal(1.0, 0.0, 0.0), 0, P->w[wcur]))) return rc;
+    if ((rc = launch_k1(P, P->y[0], nullptr, make_scal(1.0, 0.0, 0.0), 0, P->w[0]))) return rc;
     S->aty_passes++;  // corrected at the end if x0 turned out to be zero (cold start, no pass)
   } else {
-    CK(cudaMemsetAsync(P->y[cur], 0, m * 8, P->st));
-    CK(cudaMemsetAsync(P->w[wcur], 0, n * 8, P->st));
+    CK(cudaMemsetAsync(P->y[0], 0, m * 8, P->st));
+    CK(cudaMemsetAsync(P->w[0], 0, n * 8, P->st));
   }
+  return SSNAL_OK;
+}
+
+// Objective pieces at the final x (both modes): resid = A x − b from the support (Jx, Px, r_dev[2])
+// → scratch_host[16..19] = [½‖resid‖², Σ|x|, Σx², nnz], scratch_host[20] = |supp x0| (after a sync).
+int launch_objective(ssnal_en_problem* P) {
+  int rc;
+  if ((rc = launch_gather_dev(P, P->Jx, P->Px, P->r_dev + 2))) return rc;
+  k_combine<<<1, 1024, 0, P->st>>>(P->m, P->b, -1.0, P->part_vec, kGatherDevGrid, P->tmpm, nullptr, nullptr,
+                                   P->gax_valid);
+  P->launches++;
+  CKL();
+  k_objective<<<1, 1024, 0, P->st>>>(P->m, P->tmpm, P->Px, P->r_dev + 2, P->scratch + 16);
+  P->launches++;
+  CKL();
+  CK(cudaMemcpyAsync(P->scratch_host + 16, P->scratch + 16, 4 * 8, cudaMemcpyDeviceToHost, P->st));
+  CK(cudaMemcpyAsync(P->scratch_host + 20, P->r_dev + 4, 8, cudaMemcpyDeviceToHost, P->st));
+  return SSNAL_OK;
+}
+
+// Host-driven mode: control decisions on the CPU from the EvalOut records (mapped memory).
+int solve_core(ssnal_en_problem* P, double l1, double l2, double sigma0, double tol, int have_x0,
+               ssnal_en_stats* S) {
+  const int64_t m = P->m;
+  memset(S, 0, sizeof(*S));
+  int rc;
+  int cur = 0;  // index of current J/PJ/y/g
+  int wcur = 0; // index of current w buffer (0..2)
+  EvalOut ev, evt;
+  int64_t rx = 0;
+  if ((rc = init_point(P, have_x0, S, &rx))) return rc;
 
   double sigma = sigma0;
   int converged = 0, numeric = 0, k;
@@ -739,7 +810,7 @@ int solve_core(ssnal_en_problem* P, double l1, double l2, double sigma0, double 
         s *= P->beta;
         nbt++;
         // trial y + s d; w_s = w + s (w1 − w) (linearity of Aᵀ, R14)
-        k_axpy_m<<<(unsigned)((m + 255) / 256), 256, 0, P->st>>>(m, P->y[cur], s, P->d, P->y[tr]);
+        k_axpy_m<<<(unsigned)((m + 255) / 256), 256, 0, P->st>>>(m, P->y[cur], s, P->d, P->y[tr], nullptr);
         P->launches++;
         CKL();
         if ((rc = launch_k1e(P, P->w[wcur], P->w[wtr], s, P->x, sc, P->w[wbt]))) return rc;
@@ -775,11 +846,11 @@ int solve_core(ssnal_en_problem* P, double l1, double l2, double sigma0, double 
     S->res_kkt3 = res3;
     S->res_kkt1 = ev.res1;
     if (rx > 0) {
-      k_zero_at<<<(unsigned)((rx + 255) / 256), 256, 0, P->st>>>(P->Jx, rx, nullptr, P->x);
+      k_zero_at<<<(unsigned)((rx + 255) / 256), 256, 0, P->st>>>(P->Jx, rx, nullptr, P->x, nullptr);
       P->launches++;
       CKL();
     } else if (rx < 0) {  // warm start: count on the device
-      k_zero_at<<<2 * P->nsm, 256, 0, P->st>>>(P->Jx, -1, P->r_dev + 2, P->x);
+      k_zero_at<<<2 * P->nsm, 256, 0, P->st>>>(P->Jx, -1, P->r_dev + 2, P->x, nullptr);
       P->launches++;
       CKL();
     }
@@ -804,30 +875,252 @@ int solve_core(ssnal_en_problem* P, double l1, double l2, double sigma0, double 
   S->sigma_final = sigma;
   S->status = numeric ? SSNAL_ENUMERIC : (converged ? SSNAL_OK : SSNAL_NOT_CONVERGED);
   // Stats: F(x) (Eq. (1)) via resid = A x − b; D(y) = −½yᵀy − bᵀy − Σ(|w|−λ1)²₊/(2λ2)
-  {
-    int grid = 0;
-    if (rx > 0) {
-      if ((rc = launch_gather(P, P->Jx, P->Px, rx, &grid))) return rc;
-    }
-    k_combine<<<1, 1024, 0, P->st>>>(m, P->b, -1.0, P->part_vec, grid, P->tmpm, nullptr, nullptr);
-    P->launches++;
-    CKL();
-    k_objective<<<1, 1024, 0, P->st>>>(m, P->tmpm, P->Px, P->r_dev + 2, P->scratch + 16);
-    P->launches++;
-    CKL();
-    CK(cudaMemcpyAsync(P->scratch_host + 16, P->scratch + 16, 4 * 8, cudaMemcpyDeviceToHost, P->st));
-    CK(cudaMemcpyAsync(P->scratch_host + 20, P->r_dev + 4, 8, cudaMemcpyDeviceToHost, P->st));
-    // read after the caller's single end-of-solve synchronisation (finish_stats)
-    S->dual_obj = (l2 > 0) ? (-(0.5 * ev.yy + ev.by) - ev.s[3] / (2.0 * l2)) : NAN;
-    P->stat_l1 = l1;
-    P->stat_l2 = l2;
-    P->stat_warm_pass = (have_x0 && P->init_mode == 1);
-  }
+  if ((rc = launch_objective(P))) return rc;
+  S->dual_obj = (l2 > 0) ? (-(0.5 * ev.yy + ev.by) - ev.s[3] / (2.0 * l2)) : NAN;
+  P->stat_l1 = l1;
+  P->stat_l2 = l2;
+  P->stat_warm_pass = (have_x0 && P->init_mode == 1);
+  P->graph_pending = false;
   return S->status;
+}
+
+// ---------------- graph mode ----------------
+// Append a conditional WHILE node (handle h) to the graph being captured on st; returns its body.
+int add_while(cudaStream_t st, cudaGraphConditionalHandle h, cudaGraph_t* body) {
+  cudaStreamCaptureStatus cs;
+  cudaGraph_t g;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t nd = 0;
+  CK(cudaStreamGetCaptureInfo(st, &cs, nullptr, &g, &deps, &nd));
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t node;
+  CK(cudaGraphAddNode(&node, g, deps, nd, &cp));
+  CK(cudaStreamUpdateCaptureDependencies(st, &node, 1, cudaStreamSetCaptureDependencies));
+  *body = cp.conditional.phGraph_out[0];
+  return SSNAL_OK;
+}
+
+// Captures the three loop levels into the bodies of nested WHILE nodes (see k_ctl.cuh).
+int capture_graph(ssnal_en_problem* P, cudaGraph_t G) {
+  const int64_t m = P->m, n = P->n;
+  DevCtl* C = P->ctl;
+  const Scal none = make_scal(1.0, 0.0, 0.0);  // placeholder: every kernel reads C->sc
+  int rc;
+  cudaGraphConditionalHandle h_outer, h_inner, h_bt;
+  CK(cudaGraphConditionalHandleCreate(&h_outer, G, 1, cudaGraphCondAssignDefault));
+  cudaGraph_t body_o, body_i, body_b;
+  {
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h_outer;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t node;
+    CK(cudaGraphAddNode(&node, G, nullptr, 0, &cp));
+    body_o = cp.conditional.phGraph_out[0];
+  }
+  // ---- outer body: σ-scalars, EVAL(y, x), first inner test ----
+  CK(cudaStreamBeginCaptureToGraph(P->cap[0], body_o, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  P->cap_depth = 1;
+  P->st = P->cap[0];
+  CK(cudaGraphConditionalHandleCreate(&h_inner, body_o, 0, 0));
+  int64_t L = P->launches;
+  k_ctl_outer_begin<<<1, 1, 0, P->st>>>(C);
+  P->launches++;
+  if ((rc = launch_k1e(P, P->w[0], nullptr, 0.0, P->x, none, nullptr, &C->sc, nullptr))) return rc;
+  if ((rc = launch_finalize(P, P->J[0], P->PJ[0], P->r_dev + 0))) return rc;
+  if ((rc = launch_gather_dev(P, P->J[0], P->PJ[0], P->r_dev + 0))) return rc;
+  if ((rc = launch_eval(P, P->y[0], none, 1, P->gax_valid, kGatherDevGrid, P->g[0], P->r_dev + 0, 0, nullptr,
+                        nullptr, &C->sc)))
+    return rc;
+  k_ctl_inner_begin<<<1, 1, 0, P->st>>>(C, P->ev_dev + 0, m, P->nsm, P->W_splits, P->info, h_inner);
+  P->launches++;
+  CKL();
+  P->seg_kernels[0] = (int)(P->launches - L);
+  if ((rc = add_while(P->cap[0], h_inner, &body_i))) return rc;
+  {
+    // ---- inner body: direction, trial K1 at y + d, Armijo ----
+    CK(cudaStreamBeginCaptureToGraph(P->cap[1], body_i, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    P->cap_depth = 2;
+    P->st = P->cap[1];
+    CK(cudaGraphConditionalHandleCreate(&h_bt, body_i, 0, 0));
+    L = P->launches;
+    if ((rc = newton_direction_graph(P))) return rc;
+    if ((rc = launch_k1(P, P->y[1], P->x, none, 1, P->w[1], &C->sc, C->tstamp))) return rc;
+    if ((rc = launch_finalize(P, P->J[1], P->PJ[1], P->r_dev + 1))) return rc;
+    if ((rc = launch_eval(P, P->y[1], none, 1, P->cta_cnt, P->G, P->g[1], P->r_dev + 1, 1, P->scratch, P->info,
+                          &C->sc)))
+      return rc;
+    k_ctl_armijo<<<1, 1, 0, P->st>>>(C, P->ev_dev + 0, P->ev_dev + 1, h_bt);
+    P->launches++;
+    CKL();
+    P->seg_kernels[1] = (int)(P->launches - L);
+    if ((rc = add_while(P->cap[1], h_bt, &body_b))) return rc;
+    {
+      // ---- backtrack body: y + s d, K1e from w + s (w1 − w), Armijo ----
+      CK(cudaStreamBeginCaptureToGraph(P->cap[2], body_b, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+      P->cap_depth = 3;
+      P->st = P->cap[2];
+      L = P->launches;
+      k_axpy_m<<<(unsigned)((m + 255) / 256), 256, 0, P->st>>>(m, P->y[0], 0.0, P->d, P->y[1], &C->s);
+      P->launches++;
+      if ((rc = launch_k1e(P, P->w[0], P->w[1], 0.0, P->x, none, P->w[2], &C->sc, &C->s))) return rc;
+      if ((rc = launch_finalize(P, P->J[1], P->PJ[1], P->r_dev + 1))) return rc;
+      if ((rc = launch_eval(P, P->y[1], none, 0, nullptr, 0, nullptr, P->r_dev + 1, 2, nullptr, nullptr, &C->sc)))
+        return rc;
+      k_ctl_bt<<<1, 1, 0, P->st>>>(C, P->ev_dev + 0, P->ev_dev + 2, h_bt);
+      P->launches++;
+      CKL();
+      P->seg_kernels[2] = (int)(P->launches - L);
+      cudaGraph_t tmp;
+      CK(cudaStreamEndCapture(P->cap[2], &tmp));
+      P->cap_depth = 2;
+      P->st = P->cap[1];
+    }
+    // ---- accept (trial → current), gradient after a backtrack, next inner test ----
+    L = P->launches;
+    k_accept<<<2 * P->nsm, 256, 0, P->st>>>(C, m, n, P->y[0], P->y[1], P->g[0], P->g[1], P->J[0], P->J[1],
+                                              P->PJ[0], P->PJ[1], P->r_dev, P->w[0], P->w[1], P->w[2], P->ev_dev);
+    P->launches++;
+    if ((rc = launch_gather_dev(P, P->J[0], P->PJ[0], P->r_dev + 0, &C->need_grad))) return rc;
+    if ((rc = launch_eval(P, P->y[0], none, 1, P->gax_valid, kGatherDevGrid, P->g[0], P->r_dev + 0, 0, nullptr,
+                          nullptr, &C->sc, &C->need_grad)))
+      return rc;
+    k_ctl_inner_end<<<1, 1, 0, P->st>>>(C, P->ev_dev + 0, m, P->nsm, P->W_splits, P->info, h_inner);
+    P->launches++;
+    CKL();
+    P->seg_kernels[3] = (int)(P->launches - L);
+    cudaGraph_t tmp;
+    CK(cudaStreamEndCapture(P->cap[1], &tmp));
+    P->cap_depth = 1;
+    P->st = P->cap[0];
+  }
+  // ---- multiplier update x ← P, KKT stop, σ update ----
+  L = P->launches;
+  k_zero_at<<<2 * P->nsm, 256, 0, P->st>>>(P->Jx, -1, P->r_dev + 2, P->x, &C->numeric);
+  k_xupdate<<<2 * P->nsm, 256, 0, P->st>>>(C, P->J[0], P->PJ[0], P->r_dev, P->x, P->Jx, P->Px);
+  k_ctl_outer_end<<<1, 1, 0, P->st>>>(C, P->ev_dev + 0, h_outer);
+  P->launches += 3;
+  CKL();
+  P->seg_kernels[4] = (int)(P->launches - L);
+  cudaGraph_t tmp;
+  CK(cudaStreamEndCapture(P->cap[0], &tmp));
+  P->cap_depth = 0;
+  return SSNAL_OK;
+}
+
+int build_graph(ssnal_en_problem* P) {
+  if (P->gexec) return SSNAL_OK;
+  for (int i = 0; i < 3; ++i)
+    if (!P->cap[i]) CK(cudaStreamCreateWithFlags(&P->cap[i], cudaStreamNonBlocking));
+  cudaGraph_t G;
+  CK(cudaGraphCreate(&G, 0));
+  cudaStream_t saved = P->st;
+  const int64_t L0 = P->launches;
+  P->capturing = true;
+  int rc = capture_graph(P, G);
+  // unwind any capture left open by a failure
+  for (int d = P->cap_depth; d > 0; --d) {
+    cudaGraph_t tmp;
+    cudaStreamEndCapture(P->cap[d - 1], &tmp);
+  }
+  P->cap_depth = 0;
+  P->capturing = false;
+  P->st = saved;
+  P->launches = L0;
+  if (rc == SSNAL_OK) {
+    cudaError_t e = cudaGraphInstantiate(&P->gexec, G, 0);
+    if (e != cudaSuccess) {
+      set_err("cudaGraphInstantiate: %s", cudaGetErrorString(e));
+      rc = SSNAL_ECUDA;
+      P->gexec = nullptr;
+    }
+  }
+  if (rc) {
+    cudaGetLastError();
+    cudaGraphDestroy(G);
+    return rc;
+  }
+  P->graph = G;
+  return SSNAL_OK;
+}
+
+void drop_graph(ssnal_en_problem* P) {
+  if (P->gexec) cudaGraphExecDestroy(P->gexec);
+  if (P->graph) cudaGraphDestroy(P->graph);
+  P->gexec = nullptr;
+  P->graph = nullptr;
+}
+
+// Graph mode: the whole Algorithm 1 loop nest is one graph launch; stats are read back with the
+// objective after the caller's synchronisation (finish_stats).
+int solve_graph_core(ssnal_en_problem* P, double l1, double l2, double sigma0, double tol, int have_x0,
+                     ssnal_en_stats* S) {
+  memset(S, 0, sizeof(*S));
+  int rc;
+  if ((rc = build_graph(P))) return rc;
+  int64_t rx = 0;
+  if ((rc = init_point(P, have_x0, S, &rx))) return rc;
+  DevCtl* h = P->ctl_host;
+  memset(h, 0, sizeof(DevCtl));
+  h->l1 = l1;
+  h->l2 = l2;
+  h->tol = tol;
+  h->sigma = sigma0;
+  h->sigma_factor = P->sigma_factor;
+  h->sigma_max = P->sigma_max;
+  h->mu = P->mu;
+  h->beta = P->beta;
+  h->max_outer = P->max_outer;
+  h->max_inner = P->max_inner;
+  h->max_bt = P->max_bt;
+  h->tstamp[0] = ~0ull;
+  h->tstamp[1] = 0ull;
+  CK(cudaMemcpyAsync(P->ctl, h, sizeof(DevCtl), cudaMemcpyHostToDevice, P->st));
+  CK(cudaGraphLaunch(P->gexec, P->st));
+  if ((rc = launch_objective(P))) return rc;
+  CK(cudaMemcpyAsync(h, P->ctl, sizeof(DevCtl), cudaMemcpyDeviceToHost, P->st));
+  CK(cudaMemcpyAsync(P->ev_out_host, P->ev_dev, sizeof(EvalOut), cudaMemcpyDeviceToHost, P->st));
+  P->stat_l1 = l1;
+  P->stat_l2 = l2;
+  P->stat_warm_pass = (have_x0 && P->init_mode == 1);
+  P->graph_pending = true;
+  return SSNAL_OK;
 }
 
 // Complete the stats from the objective pieces copied by solve_core (after a stream sync).
 void finish_stats(ssnal_en_problem* P, ssnal_en_stats* S) {
+  if (P->graph_pending) {  // graph mode: counters and decisions from the device control block
+    const DevCtl* C = P->ctl_host;
+    const EvalOut* ev = P->ev_out_host;
+    S->outer_iters = C->outer_iters;
+    S->newton_iters = C->newton_iters;
+    S->psi_evals = C->psi_evals;
+    S->backtracks = C->backtracks;
+    S->aty_passes += C->aty_passes;
+    for (int b = 0; b < 3; ++b) S->branch_steps[b] = C->branch_steps[b];
+    S->line_search_stalled = C->stalled;
+    S->res_kkt1 = C->res1;
+    S->res_kkt3 = C->res3;
+    S->sigma_final = C->sigma_final;
+    S->status = C->numeric ? SSNAL_ENUMERIC : (C->converged ? SSNAL_OK : SSNAL_NOT_CONVERGED);
+    if (C->numeric && C->numeric_kind == 1) set_err("Cholesky pivot not positive (r=%lld)", (long long)C->numeric_r);
+    else if (C->numeric) set_err("non-finite psi/gd");
+    const double l2 = P->stat_l2;
+    S->dual_obj = (l2 > 0) ? (-(0.5 * ev->yy + ev->by) - ev->s[3] / (2.0 * l2)) : NAN;
+    P->launches += (int64_t)C->seg_outer * (P->seg_kernels[0] + P->seg_kernels[4]) +
+                   (int64_t)C->seg_inner * (P->seg_kernels[1] + P->seg_kernels[3]) +
+                   (int64_t)C->seg_bt * P->seg_kernels[2];
+    if (P->time_k1) {  // in-kernel globaltimer stamps (events cannot sit inside conditional bodies)
+      P->k1_time += C->k1_ns * 1e-9;
+      P->k1_count += C->k1_cnt;
+    }
+    P->graph_pending = false;
+  }
   const double* o = P->scratch_host + 16;
   S->primal_obj = o[0] + P->stat_l1 * o[1] + 0.5 * P->stat_l2 * o[2];
   S->active = (int64_t)o[3];
@@ -921,6 +1214,12 @@ static void destroy_bufs(ssnal_en_problem* P) {
   cudaFree(P->gax_valid);
   if (P->ev_host) cudaFreeHost(P->ev_host);
   if (P->scratch_host) cudaFreeHost(P->scratch_host);
+  drop_graph(P);
+  for (int i = 0; i < 3; ++i)
+    if (P->cap[i]) cudaStreamDestroy(P->cap[i]);
+  cudaFree(P->ctl);
+  if (P->ctl_host) cudaFreeHost(P->ctl_host);
+  if (P->ev_out_host) cudaFreeHost(P->ev_out_host);
   for (auto e : P->ev_pool) cudaEventDestroy(e);
   if (P->ev_t0) cudaEventDestroy(P->ev_t0);
   if (P->ev_t1) cudaEventDestroy(P->ev_t1);
@@ -1024,8 +1323,10 @@ int ssnal_en_set_option(ssnal_en_problem* P, const char* key, double v) {
   else if (k == "max_backtracks" && v >= 0) P->max_bt = (int)v;
   else if (k == "init_mode" && (v == 0 || v == 1)) P->init_mode = (int)v;
   else if (k == "time_k1") P->time_k1 = v != 0;
+  else if (k == "graph" && (v == 0 || v == 1)) P->use_graph = (int)v;
   else if (k == "cluster_size" && (v == 1 || v == 2 || v == 4 || v == 8 || v == 16)) {
     P->cluster = (int)v;
+    drop_graph(P);  // the cluster launch configuration is baked into the graph
   } else {
     set_err("unknown option or bad value: %s=%g", key, v);
     return SSNAL_EINVAL;
@@ -1044,6 +1345,7 @@ double ssnal_en_get_info(const ssnal_en_problem* P, const char* key) {
   if (k == "k1_smem") return (double)P->k1_smem;
   if (k == "cluster_size") return P->cluster;
   if (k == "num_sms") return P->nsm;
+  if (k == "graph") return P->use_graph;
   return NAN;
 }
 
@@ -1065,7 +1367,8 @@ static int solve_wrapped(ssnal_en_problem* P, double l1, double l2, double sigma
     CK(cudaMemcpyAsync(P->x, x0, P->n * 8, x0_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, P->st));
   }
   ssnal_en_stats S;
-  rc = solve_core(P, l1, l2, sigma0, tol, x0 != nullptr, &S);
+  rc = P->use_graph ? solve_graph_core(P, l1, l2, sigma0, tol, x0 != nullptr, &S)
+                    : solve_core(P, l1, l2, sigma0, tol, x0 != nullptr, &S);
   if (rc == SSNAL_ECUDA || rc == SSNAL_EINVAL) return rc;
   if (x_out) {
     CK(cudaMemcpyAsync(x_out, P->x, P->n * 8, xout_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, P->st));
@@ -1180,13 +1483,7 @@ int ssnal_en_model_select(ssnal_en_problem* P, double l2, double* xdb_out, ssnal
     int rc = alloc((void**)&P->Msel, (size_t)2 * m * m * 8 + 64);
     if (rc) return rc;
   }
-  auto splits = [&](int tiles, int64_t K) {
-    int ns = (int)((2 * P->nsm + tiles - 1) / tiles);
-    const int64_t nch = (K + 31) / 32;
-    if (ns > nch) ns = (int)nch;
-    if (ns > P->W_splits) ns = P->W_splits;
-    return ns < 1 ? 1 : ns;
-  };
+  auto splits = [&](int tiles, int64_t K) { return gram_splits(P->nsm, tiles, K, P->W_splits); };
   int* info_nu = P->info + 2;
   int* info_ols = P->info + 3;
   CK(cudaMemsetAsync(P->info + 2, 0, 2 * sizeof(int), P->st));
@@ -1202,8 +1499,8 @@ int ssnal_en_model_select(ssnal_en_problem* P, double l2, double* xdb_out, ssnal
     // ν: factor A_JᵀA_J + λ2 I with A_J appended as m rows: ν = ‖A_J L⁻ᵀ‖_F²
     const int N = (int)r, NR = (int)(r + m);
     const int nt = (N + 31) / 32, tiles = nt * (nt + 1) / 2, ns = splits(tiles, m);
-    k_gram<true><<<dim3(tiles, ns), 256, 0, P->st>>>(P->A, m, J, r, P->W, r, nullptr);
-    k_gram_reduce<<<(unsigned)((r * r + 255) / 256), 256, 0, P->st>>>(P->W, ns, r, r, l2, 1.0, P->Msel, NR, nullptr);
+    k_gram<true><<<gram_grid(P, tiles * ns), 256, 0, P->st>>>(P->A, m, J, r, P->W, nullptr, tiles, ns, nullptr);
+    k_gram_reduce<<<reduce_grid(P, r * r), 256, 0, P->st>>>(P->W, ns, r, r, l2, 1.0, P->Msel, NR, nullptr, nullptr, 0);
     k_fill_rows<<<(unsigned)((m * r + 255) / 256), 256, 0, P->st>>>(P->Msel, NR, r, P->A, m, J, r, 0);
     P->launches += 3;
     CKL();
@@ -1213,16 +1510,17 @@ int ssnal_en_model_select(ssnal_en_problem* P, double l2, double* xdb_out, ssnal
     // OLS de-biasing: factor A_JᵀA_J with rhs row A_Jᵀb; v → P->u
     const int64_t nout = r + 1;
     const int nt2 = (int)((nout + 31) / 32), tiles2 = nt2 * (nt2 + 1) / 2, ns2 = splits(tiles2, m);
-    k_gram<true><<<dim3(tiles2, ns2), 256, 0, P->st>>>(P->A, m, J, r, P->W, nout, P->b);
-    k_gram_reduce<<<(unsigned)((nout * nout + 255) / 256), 256, 0, P->st>>>(P->W, ns2, nout, r, 0.0, 1.0, P->Mmat,
-                                                                            N + 1, nullptr);
+    k_gram<true><<<gram_grid(P, tiles2 * ns2), 256, 0, P->st>>>(P->A, m, J, r, P->W, P->b, tiles2, ns2, nullptr);
+    k_gram_reduce<<<reduce_grid(P, nout * nout), 256, 0, P->st>>>(P->W, ns2, nout, r, 0.0, 1.0, P->Mmat, N + 1, nullptr,
+                                                                  nullptr, 0);
     P->launches += 3;
     CKL();
     if ((rc = launch_chol_ex(P, P->Mmat, N, N + 1, N + 1, P->u, 1.0, nullptr, nullptr, nullptr, nullptr, info_ols)))
       return rc;
     int grid = 0;
     if ((rc = launch_gather(P, J, P->u, r, &grid))) return rc;
-    k_combine<<<1, 1024, 0, P->st>>>(m, P->b, -1.0, P->part_vec, grid, P->tmpm, nullptr, nullptr);  // A_J v − b
+    k_combine<<<1, 1024, 0, P->st>>>(m, P->b, -1.0, P->part_vec, grid, P->tmpm, nullptr, nullptr,
+                                     nullptr);  // A_J v − b
     P->launches++;
     CKL();
     ols_possible = true;
@@ -1230,8 +1528,8 @@ int ssnal_en_model_select(ssnal_en_problem* P, double l2, double* xdb_out, ssnal
     // r ≥ m: ν = tr(K (K + λ2 I)⁻¹), K = A_J A_Jᵀ, = m − λ2 ‖L⁻¹‖_F² with I_m appended
     const int N = (int)m, NR = (int)(2 * m);
     const int nt = (int)((m + 31) / 32), tiles = nt * (nt + 1) / 2, ns = splits(tiles, r);
-    k_gram<false><<<dim3(tiles, ns), 256, 0, P->st>>>(P->A, m, J, r, P->W, m, nullptr);
-    k_gram_reduce<<<(unsigned)((m * m + 255) / 256), 256, 0, P->st>>>(P->W, ns, m, m, l2, 1.0, P->Msel, NR, nullptr);
+    k_gram<false><<<gram_grid(P, tiles * ns), 256, 0, P->st>>>(P->A, m, J, r, P->W, nullptr, tiles, ns, nullptr);
+    k_gram_reduce<<<reduce_grid(P, m * m), 256, 0, P->st>>>(P->W, ns, m, m, l2, 1.0, P->Msel, NR, nullptr, nullptr, 0);
     k_fill_rows<<<(unsigned)((m * m + 255) / 256), 256, 0, P->st>>>(P->Msel, NR, m, P->A, m, J, m, 1);
     P->launches += 3;
     CKL();
@@ -1241,7 +1539,7 @@ int ssnal_en_model_select(ssnal_en_problem* P, double l2, double* xdb_out, ssnal
     ident = 1;
   }
   if (r == 0) {  // x_ols = 0: residual = −b
-    k_combine<<<1, 1024, 0, P->st>>>(m, P->b, -1.0, P->part_vec, 0, P->tmpm, nullptr, nullptr);
+    k_combine<<<1, 1024, 0, P->st>>>(m, P->b, -1.0, P->part_vec, 0, P->tmpm, nullptr, nullptr, nullptr);
     CK(cudaMemsetAsync(info_ols, 0, sizeof(int), P->st));
     ols_possible = true;
   }

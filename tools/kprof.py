@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--config", default="cfg2")
     ap.add_argument("--reps", type=int, default=1)
     ap.add_argument("--n", type=int, default=0)
+    ap.add_argument("--control", default="graph", choices=["graph", "host"])
     ap.add_argument("--newton", default="", help="comma list of r: time the Newton direction hook (m=500)")
     args = ap.parse_args()
     if args.newton:
@@ -41,6 +42,7 @@ def main():
     b, _ = synth.response(cfg)
     db = torch.from_numpy(b).cuda()
     P = Problem.from_device(dA.data_ptr(), db.data_ptr(), m, n, st.cuda_stream, keep=(dA, db))
+    P.set_option("graph", 1 if args.control == "graph" else 0)
     lm = P.lambda_max_l1 / cfg.alpha
     x = torch.zeros(n, dtype=torch.float64, device="cuda")
 
@@ -66,7 +68,7 @@ def main():
             agg[k][1] += e.device_time_total if hasattr(e, "device_time_total") else e.cuda_time_total
     tot = sum(v[1] for v in agg.values())
     print(f"wall per step {wall * 1e3:.2f} ms; kernel time per step {tot / 1e3 / args.reps:.2f} ms")
-    for k, (c, t) in sorted(agg.items(), key=lambda kv: -kv[1][1])[:20]:
+    for k, (c, t) in sorted(agg.items(), key=lambda kv: -kv[1][1])[:40]:
         print(f"{k:48s} {c // args.reps:6d} {t / 1e3 / args.reps:8.3f} ms  {100 * t / tot:5.1f}%  avg {t / c:8.2f} us")
 
 
