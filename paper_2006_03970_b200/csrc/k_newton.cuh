@@ -363,19 +363,19 @@ __global__ void k_gram_reduce(const double* __restrict__ W, int ns, int64_t nout
 // ---------------------------------------------------------------------------
 // K4: SPD solve by one thread-block cluster (Cholesky, right-looking, 32 × 32 tiles in L2).
 //
-// M is (N+1) × N column-major with ld ≥ N+1: rows 0..N-1 hold the SPD matrix (lower
-// triangle used and overwritten by L), row N holds the right-hand side.  Carrying the rhs
-// as an extra row through the factorisation yields z = L⁻¹ rhs in row N (the forward
-// substitution) for free.  Per panel k (W_k = L_kk⁻¹ is already in Winv):
-//   B: L_ik = A_ik W_kᵀ for row tiles i > k (rhs row included)   — DMMA tile GEMM, warp/tile
+// M is NR × N column-major with ld ≥ NR: rows 0..N-1 hold the SPD matrix (lower triangle used
+// and overwritten by L), rows N..NR-1 are appended rows C that leave the factorisation as
+// C L⁻ᵀ; with `out` row N is the right-hand side, so the factorisation performs the forward
+// substitution z = L⁻¹ rhs for free.  Per panel k (W_k = L_kk⁻¹ already in Winv):
+//   B: L_ik = A_ik W_kᵀ for row tiles i > k (appended rows included) — DMMA tile GEMM, warp/tile
 //      | cluster barrier
-//   C: A_ij −= L_ik L_jkᵀ for k < j ≤ i                             — DMMA tile GEMM, warp/tile
-//      look-ahead: CTA 0 (warps 0-3) updates tile (k+1,k+1) first, factors it (4 warps) and
-//      inverts it (W_{k+1}); the other 8·CS − 4 warps take the remaining tiles
+//   C: A_ij −= L_ik L_jkᵀ for k < j ≤ i                                — DMMA tile GEMM, warp/tile
+//      look-ahead: CTA 0 warps 0-3 update tile (k+1,k+1) into smem, then warp 0 factors it and
+//      inverts it in one register-resident sweep (W_{k+1}); the other warps take the rest
 //      | cluster barrier
-// Then CTA 0 runs the backward substitution v = L⁻ᵀ z with the stored W_k.
+// Then CTA 0 runs the backward substitution v = L⁻ᵀ z right-looking over the blocks.
 // FP64 tensor cores: mma.sync.m8n8k4.f64 (SASS DMMA) — the tile updates are dense contractions.
-// out = scale · v; if dotv: *dot_out = Σ dotv · out.
+// out = scale · v; if dotv: *dot_out = Σ dotv · out; if yt: yt = ybase + out.
 // ---------------------------------------------------------------------------
 constexpr int CHT = 32;  // tile edge
 constexpr int TLD = 33;  // smem tile leading dimension
@@ -406,100 +406,203 @@ SSN_DEV void tile_mma(const double* SA, const double* SB, double (&acc)[4][4][2]
 }
 
 // Warp loads rows [r0, r0+32) × cols [c0, c0+32) of M into S (row-major, TLD), zero outside
-// rows < nr and cols < nc.
+// rows < nr and cols < nc.  One 256-B coalesced load per column (lane = row).
 SSN_DEV void load_tile_rows(const double* M, int ld, int r0, int c0, int nr, int nc, double* S, int lane) {
+  const bool rok = r0 + lane < nr;
+  const double* col = M + (int64_t)c0 * ld + (rok ? r0 + lane : 0);
+  const int ncl = nc - c0;
   double v[CHT];  // all 32 loads in flight before the smem stores
 #pragma unroll
-  for (int p = 0; p < CHT; ++p)
-    v[p] = (r0 + lane < nr && c0 + p < nc) ? __ldcg(M + (int64_t)(r0 + lane) + (int64_t)(c0 + p) * ld) : 0.0;
+  for (int p = 0; p < CHT; ++p) v[p] = (rok && p < ncl) ? __ldcg(col + p * ld) : 0.0;
 #pragma unroll
   for (int p = 0; p < CHT; ++p) S[lane * TLD + p] = v[p];
 }
 
-// CTA-0 look-ahead: factor the diagonal tile at n0 (kn columns, nrow rows incl. possibly the
-// rhs row) with the 4 warps of the diagonal team (t128 ∈ [0,128), named barrier 2) and store L
-// into M.  Warp w owns columns [8w, 8w+8) of every row (lane = row) and keeps a replica of its
-// 8 diagonal entries, updated with the same fma as the owning lane (bitwise equal), so the
-// owner of pivot j has it locally: per pivot only the scaled column goes through smem
-// (double-buffered colbuf) and one 128-thread barrier.  1/√pivot by rsqrt.
-SSN_DEV void diag_block(double* M, int ld, int N, int NR, int n0, int t128, int* info, double* colbuf,
-                        double* invg) {
+// The diagonal team (CTA 0 warps 0-3, t128 ∈ [0,128), named barrier 2) factors the diagonal tile
+// S (smem, row-major: S[r][c] = A[n0+r][n0+c]) and inverts the factor, blocked by 8 columns.
+// Warp w owns columns [8w, 8w+8) of every row (lane = row: a[q] = L[lane][8w+q]), a replica of
+// their diagonal entries (dgw, updated with the same fma as the owning lane — bitwise equal), and
+// rows [8w, 8w+8) of W = L⁻¹ (lane = column: wr[q] = W[8w+q][lane]).
+//   block b = 0..3: warp b factors its 8 columns with intra-warp shuffles (per pivot j: rsqrt →
+//   scale column → shuffle → rank-1 update of its later columns; W row j /= L_jj, later rows
+//   −= L_kj · row j — column-oriented forward substitution on I), publishes the 8 columns of L
+//   and 8 rows of W to smem (double-buffered), one 128-thread barrier.  The next owner (b + 1)
+//   applies block b's rank-8 update lazily, one column right before its pivot (off the chain);
+//   warps > b + 1 apply it eagerly while the next block is factored.
+// Rows ≥ kn (appended rows / padding) are identity-padded and never pivot.  Writes L (rows <
+// nrow, cols < kn, c ≤ r) into M at (n0, n0), W (row-major 32 × 32) to Wout and to Wsm (smem,
+// row stride TLD).  Compact code (block loop rolled): it runs once per panel.
+// smem scratch `cb`: 2 × (32 × 9 + 8 × 33) doubles.
+constexpr int kDiagScratch = 2 * (CHT * 9 + 8 * 33);
+SSN_DEV void diag_factor4(const double* S, double* M, int ld, int n0, int kn, int nrow, double* Wout, double* Wsm,
+                          int* info, double* cb, int t128) {
   const int w = t128 >> 5, lane = t128 & 31;
-  const int kn = min(CHT, N - n0), nrow = min(CHT, NR - n0);
-  double a[8], dgw[8];
+  double a[8], dgw[8], wr[8];
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
     const int c = 8 * w + q;
-    a[q] = (lane < nrow && c < kn) ? __ldcg(M + (int64_t)(n0 + lane) + (int64_t)(n0 + c) * ld) : (lane == c ? 1.0 : 0.0);
-    dgw[q] = (c < kn) ? __ldcg(M + (int64_t)(n0 + c) * (ld + 1)) : 1.0;
+    a[q] = (lane < nrow && c < kn) ? S[lane * TLD + c] : (lane == c ? 1.0 : 0.0);
+    dgw[q] = (c < kn) ? S[c * TLD + c] : 1.0;
+    wr[q] = (lane == c) ? 1.0 : 0.0;
   }
   bool bad = false;
+#pragma unroll 1
+  for (int blk = 0; blk < 4; ++blk) {
+    double* Lb = cb + (blk & 1) * (CHT * 9 + 8 * 33);  // Lb[r * 9 + p] = L[r][8blk + p]
+    double* Wb = Lb + CHT * 9;                          // Wb[p * 33 + c] = W[8blk + p][c]
+    if (w == blk) {
+      const double* Lp = cb + ((blk + 1) & 1) * (CHT * 9 + 8 * 33);  // block blk − 1
+      const double* Wp = Lp + CHT * 9;
+      double lrp[8], wbp[8];
+      if (blk > 0) {
 #pragma unroll
-  for (int j = 0; j < CHT; ++j) {
-    double* cb = colbuf + (j & 1) * 32;
-    if (w == (j >> 3)) {  // warp-uniform: owner of column j
-      const int jl = j & 7;
-      double ajj = dgw[jl];
-      bad |= (j < kn) && !(ajj > 0.0);
-      ajj = (j < kn && ajj > 0.0) ? ajj : 1.0;
-      const double inv = rsqrt(ajj);
-      const double lij = (lane > j) ? a[jl] * inv : (lane == j ? ajj * inv : 0.0);
-      if (lane >= j) a[jl] = lij;
-      cb[lane] = lij;
-      if (lane == j) invg[j] = inv;  // 1/L_jj (= rsqrt of the pivot) for the block inverse
+        for (int pp = 0; pp < 8; ++pp) {
+          lrp[pp] = Lp[lane * 9 + pp];
+          wbp[pp] = Wp[pp * 33 + lane];
+        }
+      }
+#pragma unroll
+      for (int p = 0; p < 8; ++p) {
+        if (blk > 0) {  // lazy rank-8 update of column p from block blk − 1
+#pragma unroll
+          for (int pp = 0; pp < 8; ++pp) {
+            const double l = Lp[(8 * w + p) * 9 + pp];
+            dgw[p] = fma(-l, l, dgw[p]);
+            a[p] = fma(-lrp[pp], l, a[p]);
+            wr[p] = fma(-l, wbp[pp], wr[p]);
+          }
+        }
+        const int j = 8 * blk + p;
+        double d = dgw[p];
+        bad |= (j < kn) && !(d > 0.0);
+        d = (j < kn && d > 0.0) ? d : 1.0;
+        const double inv = rsqrt_pos(d);
+        const double lij = (lane > j) ? a[p] * inv : (lane == j ? d * inv : 0.0);
+        const double wj = wr[p] * inv;  // W row j scaled (final)
+#pragma unroll
+        for (int q = p + 1; q < 8; ++q) {
+          const double lq = __shfl_sync(0xffffffffu, lij, 8 * blk + q);  // L[8blk+q][j]
+          dgw[q] = fma(-lq, lq, dgw[q]);
+          a[q] = fma(-lij, lq, a[q]);
+          wr[q] = fma(-lq, wj, wr[q]);
+        }
+        a[p] = lij;
+        wr[p] = wj;
+      }
+#pragma unroll
+      for (int p = 0; p < 8; ++p) {
+        Lb[lane * 9 + p] = a[p];
+        Wb[p * 33 + lane] = wr[p];
+      }
     }
     asm volatile("bar.sync 2, 128;" ::: "memory");
-    const double li = cb[lane];
+    if (w > blk + 1) {  // eager rank-8 update from block blk
+      double lr[8], wb[8];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int c = 8 * w + q;
-      const double lc = (c > j) ? cb[c] : 0.0;
-      a[q] = fma(-li, lc, a[q]);
-      dgw[q] = fma(-lc, lc, dgw[q]);
+      for (int p = 0; p < 8; ++p) {
+        lr[p] = Lb[lane * 9 + p];
+        wb[p] = Wb[p * 33 + lane];
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const double* lc = Lb + (8 * w + q) * 9;
+#pragma unroll
+        for (int p = 0; p < 8; ++p) {
+          const double l = lc[p];  // L[8w+q][8blk+p]
+          dgw[q] = fma(-l, l, dgw[q]);
+          a[q] = fma(-lr[p], l, a[q]);
+          wr[q] = fma(-l, wb[p], wr[q]);
+        }
+      }
     }
   }
   if (bad && lane == 0) atomicExch(info, 1);
-  if (lane < nrow) {
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int c = 8 * w + q;
-      if (c < kn && c <= lane) M[(int64_t)(n0 + lane) + (int64_t)(n0 + c) * ld] = a[q];
-    }
+  for (int q = 0; q < 8; ++q) {
+    const int c = 8 * w + q;
+    if (lane < nrow && c < kn && c <= lane) M[(int64_t)(n0 + lane) + (int64_t)(n0 + c) * ld] = a[q];
+    const double wv = (c < kn && lane < kn) ? wr[q] : (lane == c ? 1.0 : 0.0);  // pad: identity
+    Wout[c * CHT + lane] = wv;
+    if (Wsm) Wsm[c * TLD + lane] = wv;
   }
 }
 
-// W = L_bb⁻¹ for diagonal block bb (lower, identity-padded beyond bn); one warp.  Rows are
-// loaded lane = row (coalesced per column), the solve runs lane = column with the stored
-// reciprocals invg[i] = 1/L_ii (no divisions on the chain).
-SSN_DEV void inv_block_warp(const double* M, int ld, int b0, int bn, double* S, const double* invg, double* W,
-                            int lane) {
-  double v[CHT];
+// Backward substitution v = L⁻ᵀ z by one CTA (8 warps), right-looking over 32-blocks:
+//   for b = last … 0:  v_b = W_bᵀ z_b  (warp 0)  |  z_a −= L_baᵀ v_b for a < b (warp a mod 8)
+// z (smem, N) holds the forward-substitution result on entry and v on exit.  W blocks are staged
+// in a smem ring (≤ 16 blocks).  Each warp prefetches its first L tile of the next step into
+// registers (coalesced: lane = row) while the current step runs and transposes it through its
+// own smem tile (lane = column for the dot products); further tiles (N > 256) load on demand.
+constexpr int kBwdRing = 16;
+SSN_DEV void bwd_tile_load(const double* M, int ld, int N, int b, int a, double (&t)[CHT], int lane) {
+  const int row = b * CHT + lane;
+  const bool rok = row < N;
+  const double* src = M + (int64_t)a * CHT * ld + (rok ? row : 0);
 #pragma unroll
-  for (int p = 0; p < CHT; ++p)
-    v[p] = (lane < bn && p < bn && p <= lane) ? __ldcg(M + (int64_t)(b0 + lane) + (int64_t)(b0 + p) * ld)
-                                              : (lane == p ? 1.0 : 0.0);
-  const double ri = (lane < bn) ? __ldcg(invg + lane) : 1.0;
+  for (int c = 0; c < CHT; ++c) t[c] = rok ? __ldcg(src + c * ld) : 0.0;
+}
+SSN_DEV void backward_solve(const double* M, int ld, int N, const double* Winv, double* z, double* Wring, double* Tw,
+                            int tid) {
+  const int warp = tid >> 5, lane = tid & 31;
+  const int ntc = (N + CHT - 1) / CHT;
+  double* Ts = Tw + (size_t)warp * CHT * TLD;  // this warp's transpose tile
+  auto stage_w = [&](int b) {  // W_b → ring slot b % kBwdRing (all threads)
+    double* dst = Wring + (size_t)(b % kBwdRing) * CHT * CHT;
+    const double* src = Winv + (size_t)b * CHT * CHT;
+    for (int e = tid; e < CHT * CHT; e += blockDim.x) dst[e] = __ldcg(src + e);
+  };
+  for (int b = ntc - 1; b >= 0 && b >= ntc - kBwdRing; --b) stage_w(b);
+  double cur[CHT], nxt[CHT];  // tile (b, warp): cur[c] = L[b0 + lane][a0 + c]
+  if (warp < ntc - 1) bwd_tile_load(M, ld, N, ntc - 1, warp, cur, lane);
+  __syncthreads();
+  // z_a −= L_baᵀ v_b for one tile held as t[c] = L[b0 + lane][a0 + c] (zero rows ≥ N)
+  auto upd = [&](int a, int b0, const double (&t)[CHT]) {
 #pragma unroll
-  for (int p = 0; p < CHT; ++p) S[lane * TLD + p] = v[p];  // S[i][p] = L[i][p]
-  S[CHT * TLD + lane] = ri;
-  __syncwarp();
-  double x[CHT];
+    for (int c = 0; c < CHT; ++c) Ts[lane * TLD + c] = t[c];
+    __syncwarp();
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
 #pragma unroll
-  for (int i = 0; i < CHT; ++i) {
-    double s0 = (i == lane) ? 1.0 : 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-#pragma unroll
-    for (int p = 0; p < i; ++p) {
-      const double t = S[i * TLD + p] * x[p];
-      if ((p & 3) == 0) s0 -= t;
-      else if ((p & 3) == 1) s1 -= t;
-      else if ((p & 3) == 2) s2 -= t;
-      else s3 -= t;
+    for (int r = 0; r < CHT; r += 4) {  // lane = column: Σ_r L[b0+r][a0+lane] v[b0+r]
+      s0 = fma(Ts[r * TLD + lane], z[b0 + r], s0);
+      s1 = fma(Ts[(r + 1) * TLD + lane], z[b0 + r + 1], s1);
+      s2 = fma(Ts[(r + 2) * TLD + lane], z[b0 + r + 2], s2);
+      s3 = fma(Ts[(r + 3) * TLD + lane], z[b0 + r + 3], s3);
     }
-    x[i] = ((s0 + s1) + (s2 + s3)) * S[CHT * TLD + i];
-  }
+    z[a * CHT + lane] -= (s0 + s1) + (s2 + s3);  // a < b: full block
+    __syncwarp();
+  };
+#pragma unroll 1
+  for (int b = ntc - 1; b >= 0; --b) {
+    const int b0 = b * CHT, bn = min(CHT, N - b0);
+    if (warp < b - 1) bwd_tile_load(M, ld, N, b - 1, warp, nxt, lane);  // prefetch
+    if (warp == 0) {  // v_b[c] = Σ_r W_b[r][c] z_b[r]   (W_b lower triangular)
+      const double* Wb = Wring + (size_t)(b % kBwdRing) * CHT * CHT;
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
 #pragma unroll
-  for (int i = 0; i < CHT; ++i) W[i * CHT + lane] = x[i];
-  __syncwarp();
+      for (int r = 0; r < CHT; r += 4) {
+        const double z0 = (r < bn) ? z[b0 + r] : 0.0, z1 = (r + 1 < bn) ? z[b0 + r + 1] : 0.0;
+        const double z2 = (r + 2 < bn) ? z[b0 + r + 2] : 0.0, z3 = (r + 3 < bn) ? z[b0 + r + 3] : 0.0;
+        s0 = fma(Wb[r * CHT + lane], z0, s0);
+        s1 = fma(Wb[(r + 1) * CHT + lane], z1, s1);
+        s2 = fma(Wb[(r + 2) * CHT + lane], z2, s2);
+        s3 = fma(Wb[(r + 3) * CHT + lane], z3, s3);
+      }
+      __syncwarp();
+      z[b0 + lane] = (lane < bn) ? (s0 + s1) + (s2 + s3) : 0.0;  // zero pad beyond N (z has 1024 slots)
+    }
+    __syncthreads();
+    if (b - kBwdRing >= 0) stage_w(b - kBwdRing);  // ring slot of b is free now
+    if (warp < b) upd(warp, b0, cur);
+#pragma unroll 1
+    for (int a = warp + 8; a < b; a += 8) {  // further tiles of this warp: on demand
+      double t[CHT];
+      bwd_tile_load(M, ld, N, b, a, t, lane);
+      upd(a, b0, t);
+    }
+#pragma unroll
+    for (int c = 0; c < CHT; ++c) cur[c] = nxt[c];
+    __syncthreads();
+  }
 }
 
 // NR ≥ N + 1 rows: rows N..NR-1 are appended rows C, which leave the factorisation as C L⁻ᵀ.
@@ -521,223 +624,184 @@ __global__ void __launch_bounds__(256, 1) k_chol_cluster(double* M, int N, int N
   const int rank = (int)cl.block_rank(), CS = (int)cl.num_blocks();
   extern __shared__ double dsm[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  double* SA = dsm + (size_t)warp * 2 * CHT * TLD;  // per-warp operand tiles
+  const int quad = warp >> 2, qw = warp & 3;
+  double* SA = dsm + (size_t)warp * 2 * CHT * TLD;  // per-warp operand tiles (phase C)
   double* SB = SA + CHT * TLD;
-  double* T = dsm + (size_t)8 * 2 * CHT * TLD;      // CTA-0 diagonal tile
-  double* colbuf = T + CHT * TLD;                   // 80 doubles (column broadcast / reciprocals)
+  double* SQ = dsm + (size_t)quad * 2 * CHT * TLD;  // per-quad tile (phase B; aliases SA/SB)
+  double* T = dsm + (size_t)8 * 2 * CHT * TLD;      // W_k (phase B operand)
+  double* T2 = T + CHT * TLD;                        // CTA-0 diagonal tile (look-ahead)
+  double* T3 = T2 + CHT * TLD;                       // CTA-0: L_{k+1,k} from phase B
+  double* dscr = T3 + CHT * TLD;                     // diag_factor4 scratch
   const int ntc = (N + CHT - 1) / CHT, ntr = (NR + CHT - 1) / CHT;
-  const int NWg = CS * 8;
-  const int gw = rank + CS * warp;
-  // worker warps for phase C: all warps of CTAs 1..CS-1 (CTA 0 owns the look-ahead diagonal, so
-  // its factorisation does not compete for issue slots); with CS = 1 CTA 0's warps 4-7 work too.
-  // CTA 1's warp 0 (CTA 0's warp 4 when CS = 1) computes the block inverse W_k in phase C.
-  const bool diag_team = (rank == 0 && warp < 4);
-  const bool inv_warp = (CS > 1) ? (rank == 1 && warp == 0) : (warp == 4);
-  const int NWw = (CS > 1) ? NWg - 9 : 3;
-  const int wid = (CS > 1) ? ((rank == 0 || inv_warp) ? -1 : (rank - 1) * 8 + warp - 1)
-                           : (warp > 4 ? warp - 5 : -1);
+  // Roles.  CTA 0 quad 0 = the diagonal team: the whole critical chain factor(k) → L_{k+1,k} →
+  // update (k+1,k+1) → factor(k+1) runs there with operands in its smem; SM 0 takes no other tiles
+  // when the cluster has more CTAs.  Other quads take the remaining phase-B tiles; the other CTAs'
+  // warps the phase-C trailing updates.
+  const bool diag_team = (rank == 0 && quad == 0);
+  const int NQ = (CS > 1) ? 2 * (CS - 1) : 1;  // phase-B worker quads
+  const int gq = (CS > 1) ? ((rank == 0) ? -1 : 2 * (rank - 1) + quad) : (quad == 1 ? 0 : -1);
+  const int NWw = (CS > 1) ? 8 * (CS - 1) : 4;  // phase-C worker warps
+  const int wid = (CS > 1) ? ((rank == 0) ? -1 : 8 * (rank - 1) + warp) : (warp >= 4 ? warp - 4 : -1);
 #ifdef CHOL_PROBE
-#define STAMP(i) do { if (rank == 0 && tid == 0 && (i) < 64) { unsigned long long t_; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); g_t[i] = t_; } } while (0)
+#define STAMP(i) do { if (rank == 0 && tid == 0 && (i) < 64) { unsigned long long t_; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); g_t[i] = t_; g_c[i] = clock64(); } } while (0)
 #else
 #define STAMP(i) do {} while (0)
 #endif
   STAMP(0);
-  double* invg = Winv + (size_t)ntc * CHT * CHT;  // per-block reciprocals 1/L_jj (ntc × 32)
-  if (diag_team) diag_block(M, ld, N, NR, 0, tid, info, colbuf, invg);
-  cl.sync();
-  STAMP(1);
-  for (int k = 0; k < ntc; ++k) {
+  // k = −1: the diagonal team factors tile (0,0); k ≥ 0: phase B(k), then phase C(k) with the
+  // look-ahead factor of tile (k+1,k+1) — one call site of diag_factor4 (I-cache).
+  for (int k = -1; k < ntc; ++k) {
     const int k0 = k * CHT;
     const int kn = min(CHT, N - k0);
-    // ---- B: L_ik = A_ik L_kk^{-T} for row tiles i > k (substitution; warp per tile) ----
-    const int nB = ntr - k - 1;
-    if (nB > 0 && rank < nB) {
-      {  // T[c][p] = L_kk[c][p] (identity-padded); 4 independent loads per thread
-        double v[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int e = tid + 256 * u, c = e >> 5, p = e & 31;
-          v[u] = (c < kn && p < kn && p <= c) ? __ldcg(M + (int64_t)(k0 + c) + (int64_t)(k0 + p) * ld)
-                                              : (c == p ? 1.0 : 0.0);
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int e = tid + 256 * u;
-          T[(e >> 5) * TLD + (e & 31)] = v[u];
-        }
-      }
-      __syncthreads();
-      if (tid < CHT) colbuf[tid] = 1.0 / T[tid * TLD + tid];
-      __syncthreads();
-      for (int q = gw; q < nB; q += NWg) {
-        const int row = (k + 1 + q) * CHT + lane;
-        double x[CHT];
-#pragma unroll
-        for (int c = 0; c < CHT; ++c)
-          x[c] = (row < NR && c < kn) ? __ldcg(M + (int64_t)row + (int64_t)(k0 + c) * ld) : 0.0;
-        // right-looking within the row: x_c final after all p < c are applied
-#pragma unroll
-        for (int c = 0; c < CHT; ++c) {
-          x[c] *= colbuf[c];
-#pragma unroll
-          for (int c2 = c + 1; c2 < CHT; ++c2) x[c2] = fma(-x[c], T[c2 * TLD + c], x[c2]);
-        }
-        if (row < NR) {
-#pragma unroll
-          for (int c = 0; c < CHT; ++c)
-            if (c < kn) M[(int64_t)row + (int64_t)(k0 + c) * ld] = x[c];
-        }
-      }
-    }
-    cl.sync();
-    STAMP(2 + 2 * k);
-    if (k + 1 >= ntc) break;
-    // ---- C: A_ij −= L_ik L_jkᵀ for k < j < ntc, j ≤ i < ntr ----
-    const int remc = ntc - k - 1, remr = ntr - k - 1;
-    const int ntri = remc * (remc + 1) / 2;
-    const int npairs = ntri + (remr - remc) * remc;
-    auto do_tile = [&](int q) {
-      int ii, jj;
-      if (q < ntri) tri_tile(q, &ii, &jj);
-      else {  // rectangular part: appended row tiles below the square (rhs row, C rows)
-        const int e = q - ntri;
-        ii = remc + e / remc;
-        jj = e % remc;
-      }
-      const int i0 = (k + 1 + ii) * CHT, j0 = (k + 1 + jj) * CHT;
-      load_tile_rows(M, ld, i0, k0, NR, k0 + kn, SA, lane);
-      load_tile_rows(M, ld, j0, k0, N, k0 + kn, SB, lane);
-      if (k == 0 && q == 0) STAMP(53);
-      const int g = lane >> 2, t = lane & 3;
-      double acc[4][4][2];
-#pragma unroll
-      for (int rb = 0; rb < 4; ++rb)
-#pragma unroll
-        for (int cb = 0; cb < 4; ++cb)
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int r = i0 + 8 * rb + g, c = j0 + 8 * cb + 2 * t + e;
-            acc[rb][cb][e] = (r < NR && c < N) ? __ldcg(M + (int64_t)r + (int64_t)c * ld) : 0.0;
-          }
-      __syncwarp();
-      if (k == 0 && q == 0) STAMP(54);
-      tile_mma(SA, SB, acc, -1.0, lane);
-      if (k == 0 && q == 0) STAMP(55);
-#pragma unroll
-      for (int rb = 0; rb < 4; ++rb)
-#pragma unroll
-        for (int cb = 0; cb < 4; ++cb)
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int rl = 8 * rb + g, cl_ = 8 * cb + 2 * t + e;
-            const int r = i0 + rl, c = j0 + cl_;
-            if (r < NR && c < N && (i0 != j0 || cl_ <= rl)) M[(int64_t)r + (int64_t)c * ld] = acc[rb][cb][e];
-          }
-      __syncwarp();
-    };
-    if (diag_team) {
-      if (k == 0) STAMP(50);
-      {  // tile (k+1, k+1), split over the 4 team warps: warp w updates rows 8w..8w+7
-        const int d0 = (k + 1) * CHT;
-        const int g = lane >> 2, t = lane & 3;
-        const int r = d0 + 8 * warp + g;
-        double af[8], bf[4][8], acc[4][2];
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          const int p = k0 + 4 * kk + t;
-          af[kk] = (r < NR && 4 * kk + t < kn) ? -__ldcg(M + (int64_t)r + (int64_t)p * ld) : 0.0;
-#pragma unroll
-          for (int cb = 0; cb < 4; ++cb) {
-            const int rc = d0 + 8 * cb + g;
-            bf[cb][kk] = (rc < N && 4 * kk + t < kn) ? __ldcg(M + (int64_t)rc + (int64_t)p * ld) : 0.0;
-          }
-        }
+    const int g = lane >> 2, t = lane & 3;
+    double pre[4][2];  // diagonal team: A_{k+1,k+1} fragment, prefetched during phase B
+    if (k >= 0) {
+      // ---- B: L_ik = A_ik W_kᵀ for row tiles i > k; a quad of 4 warps per tile (8 rows each) ----
+      const int nB = ntr - k - 1;
+      if (diag_team && k + 1 < ntc) {
+        const int d0 = (k + 1) * CHT, r = d0 + 8 * qw + g;
 #pragma unroll
         for (int cb = 0; cb < 4; ++cb)
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const int c = d0 + 8 * cb + 2 * t + e;
-            acc[cb][e] = (r < NR && c < N) ? __ldcg(M + (int64_t)r + (int64_t)c * ld) : 0.0;
+            pre[cb][e] = (r < NR && c < N) ? __ldcg(M + (int64_t)r + (int64_t)c * ld) : 0.0;
           }
+      }
+      // CTA-uniform: quad 0 of a worker CTA has the lower quad index (gq0 = 2(rank − 1))
+      const bool cta_has_b = (rank == 0) ? (nB > 0) : (2 * (rank - 1) < nB - 1);
+      if (rank != 0 && cta_has_b) {  // T[c][p] = W_k[c][p] (CTA 0 has it from the factor)
+        const double* Wk = Winv + (size_t)k * CHT * CHT;
+        double v[4];
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
+        for (int u = 0; u < 4; ++u) v[u] = __ldcg(Wk + tid + 256 * u);
 #pragma unroll
-          for (int cb = 0; cb < 4; ++cb) dmma(acc[cb], af[kk], bf[cb][kk]);
+        for (int u = 0; u < 4; ++u) {
+          const int e = tid + 256 * u;
+          T[(e >> 5) * TLD + (e & 31)] = v[u];
+        }
+        __syncthreads();
+      }
+      if (k == 1) STAMP(44);
+      // tile 0 (= L_{k+1,k}) → diagonal team; tiles 1.. → worker quads
+#pragma unroll 1
+      for (int q = diag_team ? 0 : 1 + gq; q < nB && (diag_team || gq >= 0); q += diag_team ? nB : NQ) {
+        const int r0 = (k + 1 + q) * CHT;
+        {  // rows 8qw..8qw+7: lane ℓ loads row 8qw + ℓ/4, columns 8(ℓ%4)..+7
+          const int rr = 8 * qw + g, cc = 8 * t;
+          const bool rok = r0 + rr < NR;
+          const double* src = M + (int64_t)(k0 + cc) * ld + (rok ? r0 + rr : 0);
+          double v[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) v[e] = (rok && cc + e < kn) ? __ldcg(src + e * ld) : 0.0;
+#pragma unroll
+          for (int e = 0; e < 8; ++e) SQ[rr * TLD + cc + e] = v[e];
+        }
+        asm volatile("bar.sync %0, 128;" ::"r"(3 + quad) : "memory");
+        if (k == 1) STAMP(45);
+        double acc[4][2];
+#pragma unroll
+        for (int cb = 0; cb < 4; ++cb) acc[cb][0] = acc[cb][1] = 0.0;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const double af = SQ[(8 * qw + g) * TLD + 4 * kk + t];
+#pragma unroll
+          for (int cb = 0; cb < 4; ++cb) dmma(acc[cb], af, T[(8 * cb + g) * TLD + 4 * kk + t]);
+        }
+        if (k == 1) STAMP(46);
+        const int r = r0 + 8 * qw + g;
 #pragma unroll
         for (int cb = 0; cb < 4; ++cb)
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
-            const int cl_ = 8 * cb + 2 * t + e, rl = 8 * warp + g;
-            if (r < NR && d0 + cl_ < N && cl_ <= rl) M[(int64_t)r + (int64_t)(d0 + cl_) * ld] = acc[cb][e];
+            const int c = 8 * cb + 2 * t + e;
+            if (r < NR && c < kn) M[(int64_t)r + (int64_t)(k0 + c) * ld] = acc[cb][e];
+            if (diag_team) T3[(8 * qw + g) * TLD + c] = (r < NR && c < kn) ? acc[cb][e] : 0.0;
           }
+        asm volatile("bar.sync %0, 128;" ::"r"(3 + quad) : "memory");  // SQ reuse
       }
-      if (k == 0) STAMP(51);
+      cl.sync();
+      STAMP(2 + 2 * k);
+      if (k + 1 >= ntc) break;
+    }
+    // ---- C: A_ij −= L_ik L_jkᵀ for k < j < ntc, j ≤ i < ntr ----
+    if (diag_team) {
+      if (k < 0) {  // tile (0,0) as loaded
+        if (warp == 0) load_tile_rows(M, ld, 0, 0, NR, N, T2, lane);
+      } else {  // tile (k+1,k+1) = prefetched A − L_{k+1,k} L_{k+1,k}ᵀ, operands in smem (T3)
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const double af = -T3[(8 * qw + g) * TLD + 4 * kk + t];
+#pragma unroll
+          for (int cb = 0; cb < 4; ++cb) dmma(pre[cb], af, T3[(8 * cb + g) * TLD + 4 * kk + t]);
+        }
+#pragma unroll
+        for (int cb = 0; cb < 4; ++cb)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) T2[(8 * qw + g) * TLD + 8 * cb + 2 * t + e] = pre[cb][e];
+      }
       asm volatile("bar.sync 2, 128;" ::: "memory");
-      __threadfence_block();
-      diag_block(M, ld, N, NR, (k + 1) * CHT, tid, info, colbuf, invg + (size_t)(k + 1) * CHT);
-      if (k == 0) STAMP(52);
-    } else if (wid >= 0) {
-      for (int q = 1 + wid; q < npairs; q += NWw) do_tile(q);
-    } else if (inv_warp) {  // W_k = L_kk⁻¹ for the backward solve, off the critical path
-      inv_block_warp(M, ld, k0, kn, SA, invg + (size_t)k * CHT, Winv + (size_t)k * CHT * CHT, lane);
+      if (k == 1) STAMP(48);
+      {
+        const int n0 = (k + 1) * CHT;
+        diag_factor4(T2, M, ld, n0, min(CHT, N - n0), min(CHT, NR - n0), Winv + (size_t)(k + 1) * CHT * CHT, T,
+                     info, dscr, tid);
+        if (k == 1) STAMP(49);
+      }
+    } else if (wid >= 0 && k >= 0) {
+      const int remc = ntc - k - 1, remr = ntr - k - 1;
+      const int ntri = remc * (remc + 1) / 2;
+      const int npairs = ntri + (remr - remc) * remc;
+#pragma unroll 1
+      for (int q = 1 + wid; q < npairs; q += NWw) {  // tile 0 = (k+1, k+1) is the diagonal team's
+        int ii, jj;
+        if (q < ntri) tri_tile(q, &ii, &jj);
+        else {  // rectangular part: appended row tiles below the square (rhs row, C rows)
+          const int e = q - ntri;
+          ii = remc + e / remc;
+          jj = e % remc;
+        }
+        const int i0 = (k + 1 + ii) * CHT, j0 = (k + 1 + jj) * CHT;
+        load_tile_rows(M, ld, i0, k0, NR, k0 + kn, SA, lane);
+        load_tile_rows(M, ld, j0, k0, N, k0 + kn, SB, lane);
+        double acc[4][4][2];
+#pragma unroll
+        for (int rb = 0; rb < 4; ++rb)
+#pragma unroll
+          for (int cb = 0; cb < 4; ++cb)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int r = i0 + 8 * rb + g, c = j0 + 8 * cb + 2 * t + e;
+              acc[rb][cb][e] = (r < NR && c < N) ? __ldcg(M + (int64_t)r + (int64_t)c * ld) : 0.0;
+            }
+        __syncwarp();
+        tile_mma(SA, SB, acc, -1.0, lane);
+#pragma unroll
+        for (int rb = 0; rb < 4; ++rb)
+#pragma unroll
+          for (int cb = 0; cb < 4; ++cb)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int rl = 8 * rb + g, cl_ = 8 * cb + 2 * t + e;
+              const int r = i0 + rl, c = j0 + cl_;
+              if (r < NR && c < N && (i0 != j0 || cl_ <= rl)) M[(int64_t)r + (int64_t)c * ld] = acc[rb][cb][e];
+            }
+        __syncwarp();
+      }
     }
     cl.sync();
     STAMP(3 + 2 * k);
   }
   STAMP(40);
   if (rank != 0 || out == nullptr) return;
-  if (warp == 0) {  // W of the last diagonal block (its panel has no phase C)
-    const int kl = ntc - 1;
-    inv_block_warp(M, ld, kl * CHT, min(CHT, N - kl * CHT), SA, invg + (size_t)kl * CHT,
-                   Winv + (size_t)kl * CHT * CHT, lane);
-  }
-  __syncthreads();
-  STAMP(41);
-  // ---- backward substitution v = L⁻ᵀ z by CTA 0 (z = row N), left-looking per block:
-  //      v_b = W_bᵀ (z_b − Σ_{i below block b} L[i][b-block]ᵀ v_i) ----
-  double* zv = dsm;                 // N doubles (N ≤ 1024)
-  double* sbuf = dsm + 1024;        // 32 doubles
+  // ---- backward substitution v = L⁻ᵀ z by CTA 0 (z = row N) ----
+  double* zv = dsm;                          // N doubles (N ≤ 1024)
+  double* Wring = dsm + 1024;                // kBwdRing × 32 × 32 doubles
+  double* Tw = Wring + kBwdRing * CHT * CHT;  // 8 warps × 32 × TLD transpose tiles
   for (int i = tid; i < N; i += blockDim.x) zv[i] = __ldcg(M + (int64_t)N + (int64_t)i * ld);
   __syncthreads();
-  for (int kb = ntc - 1; kb >= 0; --kb) {
-    const int b0 = kb * CHT, bn = min(CHT, N - b0), i_lo = b0 + bn;
-    double wv[CHT];
-    if (warp == 0) {  // issue the W_b loads first (independent of v)
-      const double* Wb = Winv + (size_t)kb * CHT * CHT;
-#pragma unroll
-      for (int i = 0; i < CHT; ++i) wv[i] = __ldg(Wb + i * CHT + lane);
-    }
-    // s_j = Σ_{i ≥ i_lo} L[i][b0+j] v_i: warp w takes columns 4w..4w+3, lanes run down the rows
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll 4
-    for (int i = i_lo + lane; i < N; i += 32) {
-      const double vi = zv[i];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int j = 4 * warp + q;
-        if (j < bn) acc[q] = fma(__ldg(M + (int64_t)i + (int64_t)(b0 + j) * ld), vi, acc[q]);
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      acc[q] = warp_allsum(acc[q]);
-      if (lane == 0) sbuf[4 * warp + q] = acc[q];
-    }
-    __syncthreads();
-    if (warp == 0) {
-      const double t = (lane < bn) ? zv[b0 + lane] - sbuf[lane] : 0.0;
-      double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
-#pragma unroll
-      for (int i = 0; i < CHT; i += 4) {
-        v0 = fma(wv[i], __shfl_sync(0xffffffffu, t, i), v0);
-        v1 = fma(wv[i + 1], __shfl_sync(0xffffffffu, t, i + 1), v1);
-        v2 = fma(wv[i + 2], __shfl_sync(0xffffffffu, t, i + 2), v2);
-        v3 = fma(wv[i + 3], __shfl_sync(0xffffffffu, t, i + 3), v3);
-      }
-      if (lane < bn) zv[b0 + lane] = (v0 + v1) + (v2 + v3);
-    }
-    __syncthreads();
-  }
+  STAMP(41);
+  backward_solve(M, ld, N, Winv, zv, Wring, Tw, tid);
   STAMP(42);
   __shared__ double red[8];
   double dot = 0.0;
@@ -759,8 +823,11 @@ __global__ void __launch_bounds__(256, 1) k_chol_cluster(double* M, int N, int N
   }
 }
 
-// dynamic shared memory of k_chol_cluster (bytes)
-constexpr size_t kCholSmem = (size_t)(8 * 2 * CHT * TLD + CHT * TLD + 80) * sizeof(double);
+// dynamic shared memory of k_chol_cluster (bytes): factorisation operands, or in the backward
+// solve z (1024) + the W ring
+constexpr size_t kCholSmemFact = (size_t)(8 * 2 * CHT * TLD + 3 * CHT * TLD + kDiagScratch) * sizeof(double);
+constexpr size_t kCholSmemBwd = (size_t)(1024 + kBwdRing * CHT * CHT + 8 * CHT * TLD) * sizeof(double);
+constexpr size_t kCholSmem = kCholSmemFact > kCholSmemBwd ? kCholSmemFact : kCholSmemBwd;
 
 // y ← y + s·d  (m-vector) and small helpers
 __global__ void k_axpy_m(int64_t m, const double* y, double s, const double* d, double* out, const double* sp) {

@@ -5,6 +5,13 @@
 #include <cmath>
 #define CHOL_PROBE 1
 __device__ unsigned long long g_t[64];
+__device__ long long g_c[64];
+__global__ void k_timer_res(unsigned long long* out) {
+  unsigned long long prev, t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(prev));
+  unsigned long long mind = ~0ull; int changes = 0; long long c0 = clock64();
+  while (changes < 100) { asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); if (t != prev) { if (t - prev < mind) mind = t - prev; prev = t; ++changes; } }
+  out[0] = mind; out[1] = clock64() - c0;
+}
 #include "../../paper_2006_03970_b200/csrc/k_newton.cuh"
 using namespace ssn;
 
@@ -15,8 +22,10 @@ __global__ void k_empty_cluster() {
 __global__ void k_diag_only(double* M, int ld, int N, int* info, unsigned long long* t) {
   unsigned long long t0; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
   long long c0 = clock64();
-  __shared__ double T[32 * 33 + 80];
-  if (threadIdx.x < 128) diag_block(M, ld, N, N + 1, 0, threadIdx.x, info, T, T + 64);
+  __shared__ double T[32 * 33 + kDiagScratch];  // diag tile + factor scratch
+  if (threadIdx.x < 32) load_tile_rows(M, ld, 0, 0, N + 1, N, T, threadIdx.x);
+  __syncthreads();
+  if (threadIdx.x < 128) diag_factor4(T, M, ld, 0, N < 32 ? N : 32, N + 1 < 32 ? N + 1 : 32, M + (size_t)ld * N, nullptr, info, T + 32 * 33, threadIdx.x);
   __syncthreads();
   unsigned long long t1; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
   long long c1 = clock64();
@@ -35,6 +44,7 @@ __global__ void k_chain(double* out, unsigned long long* t) {
 }
 
 int main() {
+  { unsigned long long* d; cudaMalloc(&d, 16); k_timer_res<<<1,1>>>(d); unsigned long long h[2]; cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost); printf("globaltimer: min step %llu ns, 100 changes in %llu cycles\n", h[0], h[1]); }
   for (int N : {8, 32, 64, 200, 500}) {
     int ld = N + 1;
     std::vector<double> h((size_t)ld * N);
@@ -63,11 +73,14 @@ int main() {
       }
       printf("N=%4d cluster=%2d chol_cluster %8.1f us  err=%s\n", N, cs, best * 1e3, cudaGetErrorString(cudaGetLastError()));
       unsigned long long ts[64]; cudaMemcpyFromSymbol(ts, g_t, sizeof(ts));
+      long long cs_[64]; cudaMemcpyFromSymbol(cs_, g_c, sizeof(cs_));
+      printf("   cycles(k from start):");
+      for (int q = 1; q < 60; ++q) if (ts[q] > ts[0] && ts[q] - ts[0] < 100000000ull) printf(" [%d]%.1f", q, (cs_[q] - cs_[0]) / 1000.0);
+      printf("\n");
       printf("   stamps(us from start):");
       for (int q = 1; q < 60; ++q) if (ts[q] > ts[0] && ts[q] - ts[0] < 100000000ull) printf(" [%d]%.1f", q, (ts[q] - ts[0]) / 1000.0);
       printf("\n");
-      cudaMemset(g_t, 0, 0);
-      { unsigned long long z[64] = {0}; cudaMemcpyToSymbol(g_t, z, sizeof(z)); }
+            { unsigned long long z[64] = {0}; cudaMemcpyToSymbol(g_t, z, sizeof(z)); }
       float bestE = 1e9;
       for (int rep = 0; rep < 5; ++rep) {
         cudaEventRecord(e0);
