@@ -29,14 +29,16 @@ _lp = ctypes.POINTER(ctypes.c_int64)
 
 class Opts(ctypes.Structure):
     _fields_ = [("sigma_factor", _d), ("sigma_max", _d), ("mu", _d), ("beta", _d), ("max_outer", ctypes.c_int32),
-                ("max_inner", ctypes.c_int32), ("max_bt", ctypes.c_int32), ("init_mode", ctypes.c_int32)]
+                ("max_inner", ctypes.c_int32), ("max_bt", ctypes.c_int32), ("init_mode", ctypes.c_int32),
+                ("cg_ratio", _d), ("cg_threshold", _d), ("cg_tol", _d), ("cg_maxit", ctypes.c_int32),
+                ("pad", ctypes.c_int32)]
 
 
 class Stats(ctypes.Structure):
     _fields_ = [("status", ctypes.c_int32), ("outer_iters", ctypes.c_int32), ("newton_iters", ctypes.c_int32),
                 ("backtracks", ctypes.c_int32), ("aty_passes", ctypes.c_int32),
-                ("branch_steps", ctypes.c_int32 * 3), ("line_search_stalled", ctypes.c_int32),
-                ("active", ctypes.c_int64), ("res_kkt1", _d), ("res_kkt3", _d), ("primal_obj", _d),
+                ("branch_steps", ctypes.c_int32 * 4), ("line_search_stalled", ctypes.c_int32),
+                ("cg_iters", ctypes.c_int32), ("active", ctypes.c_int64), ("res_kkt1", _d), ("res_kkt3", _d), ("primal_obj", _d),
                 ("dual_obj", _d), ("gap", _d), ("sigma_final", _d)]
 
 
@@ -66,6 +68,7 @@ def lib():
             "orc_chol": (ctypes.c_int, [_dp, _i64]),
             "orc_chol_solve": (None, [_dp, _i64, _dp]),
             "orc_newton_direction": (ctypes.c_int, [_dp, _i64, _lp, _i64, _dp, _d, _dp]),
+            "orc_cg_direction": (ctypes.c_int, [_dp, _i64, _lp, _i64, _dp, _d, _d, ctypes.c_int, _dp]),
             "orc_primal_obj": (_d, [_dp, _dp, _i64, _i64, _dp, _d, _d]),
             "orc_dual_obj": (_d, [_dp, _i64, _dp, _dp, _i64, _d, _d]),
             "orc_kkt_violation": (_d, [_dp, _dp, _i64, _i64, _dp, _d, _d]),
@@ -191,6 +194,17 @@ def newton_direction(A, J, g, kappa):
     if br < 0:
         raise FloatingPointError("oracle Cholesky failed")
     return d, br
+
+
+def cg_direction(A, J, g, kappa, tol=1e-10, maxit=1000):
+    """Algorithm 1 step (1) by conjugate gradient, matrix-free V u = u + κA_J(A_Jᵀu),
+    d0 = 0, stop at ‖Vd + g‖ ≤ tol‖g‖ (R32).  Returns (d, iterations)."""
+    A, m, n, Ap = _A(A)
+    J = np.ascontiguousarray(J, dtype=np.int64)
+    g, gp = _f64(g)
+    d = np.empty(m)
+    it = lib().orc_cg_direction(Ap, m, J.ctypes.data_as(_lp), len(J), gp, kappa, tol, maxit, d.ctypes.data_as(_dp))
+    return d, it
 
 
 def chol(M):

@@ -271,6 +271,57 @@ int orc_newton_direction(const double* A, i64 m, const i64* J, i64 r, const doub
   return 2;
 }
 
+/* Newton direction by the conjugate-gradient method (Algorithm 1 step (1): "solving exactly or
+ * by conjugate gradient"; "approximately with the conjugate gradient method"),
+ * matrix-free: V u = u + κ A_J (A_Jᵀ u).  Textbook CG from d0 = 0 (reading R32): stop when
+ * ‖V d + g‖ ≤ tol·‖g‖ or after maxit iterations.  Returns the number of iterations. */
+int orc_cg_direction(const double* A, i64 m, const i64* J, i64 r, const double* g, double kappa, double tol,
+                     int maxit, double* d) {
+  double* res = (double*)malloc(sizeof(double) * (size_t)m);
+  double* p = (double*)malloc(sizeof(double) * (size_t)m);
+  double* q = (double*)malloc(sizeof(double) * (size_t)m);
+  double* t = (double*)malloc(sizeof(double) * (size_t)(r > 0 ? r : 1));
+  double gg = 0.0, rr = 0.0;
+  for (i64 k = 0; k < m; ++k) {
+    d[k] = 0.0;
+    res[k] = -g[k];
+    p[k] = res[k];
+    gg += g[k] * g[k];
+    rr += res[k] * res[k];
+  }
+  const double thr = tol * tol * gg;
+  int it = 0;
+  while (it < maxit && rr > thr) {
+    /* q = V p = p + κ A_J (A_Jᵀ p) */
+    for (i64 a = 0; a < r; ++a) {
+      const double* aa = A + J[a] * m;
+      double s = 0.0;
+      for (i64 k = 0; k < m; ++k) s += aa[k] * p[k];
+      t[a] = s;
+    }
+    for (i64 k = 0; k < m; ++k) {
+      double s = 0.0;
+      for (i64 a = 0; a < r; ++a) s += A[k + J[a] * m] * t[a];
+      q[k] = p[k] + kappa * s;
+    }
+    double pq = 0.0;
+    for (i64 k = 0; k < m; ++k) pq += p[k] * q[k];
+    const double alpha = rr / pq;
+    double rr_new = 0.0;
+    for (i64 k = 0; k < m; ++k) {
+      d[k] += alpha * p[k];
+      res[k] -= alpha * q[k];
+      rr_new += res[k] * res[k];
+    }
+    const double beta = rr_new / rr;
+    for (i64 k = 0; k < m; ++k) p[k] = res[k] + beta * p[k];
+    rr = rr_new;
+    ++it;
+  }
+  free(res); free(p); free(q); free(t);
+  return it;
+}
+
 /* ------------------------------------------------------------------------- */
 /* Objectives and certificates (used for stats and pins)                       */
 /* ------------------------------------------------------------------------- */
@@ -325,13 +376,19 @@ typedef struct {
   int32_t max_inner;   /* 100 (R10)                         */
   int32_t max_bt;      /* 50 (R30)                          */
   int32_t init_mode;   /* 1: y0 = A x0 − b when x0 ≠ 0, else 0; 0: always y0 = 0 (R8) */
+  double cg_ratio;     /* > 0: CG when r > cg_ratio·m (R32); 0: off                */
+  double cg_threshold; /* CG when min(m, r) > cg_threshold (10⁴)          */
+  double cg_tol;       /* CG relative residual (R32)                               */
+  int32_t cg_maxit;
+  int32_t pad;
 } orc_opts;
 
 typedef struct {
   int32_t status; /* 0 converged, 1 not converged, 4 numeric */
   int32_t outer_iters, newton_iters, backtracks, aty_passes;
-  int32_t branch_steps[3];
+  int32_t branch_steps[4]; /* r = 0, SMW, m × m, CG */
   int32_t line_search_stalled;
+  int32_t cg_iters;
   int64_t active;
   double res_kkt1, res_kkt3, primal_obj, dual_obj, gap, sigma_final;
 } orc_stats;
@@ -411,6 +468,11 @@ void orc_default_opts(orc_opts* o) {
   o->max_inner = 100;
   o->max_bt = 50;
   o->init_mode = 1;
+  o->cg_ratio = 0.0;
+  o->cg_threshold = 1e4;
+  o->cg_tol = 1e-10;
+  o->cg_maxit = 1000;
+  o->pad = 0;
 }
 
 /* SsNAL-EN (Algorithm 1).  x0 may be NULL (cold start).  x_out (n) and y_out (m,
@@ -463,7 +525,17 @@ int orc_solve(const double* A, const double* b, i64 m, i64 n, double l1, double 
     for (int j = 0; j < o.max_inner; ++j) {
       if (ev.res1 <= tol) break; /* inner stop, Eq. (20) res(kkt1) (R6) */
       double kappa = sigma / (1.0 + sigma * l2);
-      int br = orc_newton_direction(A, m, J, ev.r, g, kappa, d);
+      /* strategy (R12, R32): CG iff r > cg_ratio·m (cg_ratio > 0) or min(m, r) > cg_threshold */
+      const i64 mr_min = ev.r < m ? ev.r : m;
+      const int use_cg = ev.r > 0 && ((o.cg_ratio > 0.0 && (double)ev.r > o.cg_ratio * (double)m) ||
+                                      (double)mr_min > o.cg_threshold);
+      int br;
+      if (use_cg) {
+        S.cg_iters += orc_cg_direction(A, m, J, ev.r, g, kappa, o.cg_tol, o.cg_maxit, d);
+        br = 3;
+      } else {
+        br = orc_newton_direction(A, m, J, ev.r, g, kappa, d);
+      }
       if (br < 0) { numeric = 1; break; }
       S.branch_steps[br]++;
       double gd = 0.0;
