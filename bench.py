@@ -151,6 +151,7 @@ def bench_ours(args, rank, world, local_rank):
     torch.cuda.synchronize()
     P = Problem.from_device(dA.data_ptr(), db.data_ptr(), m, n, stream.cuda_stream, keep=(dA, db))
     P.set_option("graph", 1 if args.control == "graph" else 0)
+    P.set_option("cg_ratio", args.cg_ratio)
     lm = P.lambda_max_l1
     x_buf = torch.zeros(n, dtype=torch.float64, device="cuda")
 
@@ -200,6 +201,7 @@ def bench_ours(args, rank, world, local_rank):
             t0 = time.perf_counter()
             Q = Problem(A_np, b_host)
             Q.set_option("graph", 1 if args.control == "graph" else 0)
+            Q.set_option("cg_ratio", args.cg_ratio)
             lmq = Q.lambda_max_l1
             x_prev = None
             hb = 8 * m * n + 8 * m
@@ -248,7 +250,9 @@ def bench_ours(args, rank, world, local_rank):
                    "l2_policy": f"A = {8 * m * n / 1e6:.0f} MB > 126 MB L2 (no flush needed)",
                    "parallelism": f"replicas x{world}",
                    "control": ("device-resident, one CUDA graph per solve (nested conditional WHILE)"
-                               if args.control == "graph" else "host-driven (per-evaluation readback)")},
+                               if args.control == "graph" else "host-driven (per-evaluation readback)"),
+                   "newton_strategy": ("exact (Eq. 18/19); CG when min(m, r) > 1e4 (P:379)" if args.cg_ratio == 0
+                                       else f"CG (K6) when r > {args.cg_ratio:g} m, else exact (Eq. 18/19)")},
         "roofline": {"bound": "hbm", "achieved": k1_gbs, "peak": peak, "unit": "GB/s",
                      "frac": (k1_gbs / peak) if k1_gbs else None, "traffic": traffic,
                      "kernel": "k1_aty_fused", "bytes_per_launch": k1_bytes(m, n), "launches": k1_launches,
@@ -259,6 +263,7 @@ def bench_ours(args, rank, world, local_rank):
         "clocks": clk.summary(),
         "iterations": [{"c": round(c, 4), "outer": s["outer_iters"], "newton": s["newton_iters"],
                         "passes": s["aty_passes"], "backtracks": s["backtracks"], "r": s["active"],
+                        "branches": s["branch_steps"], "cg_iters": s["cg_iters"],
                         "res1": s["res_kkt1"], "res3": s["res_kkt3"], "gap": s["gap"]}
                        for c, s in zip(cfg.cs, last_stats)],
     }
@@ -418,6 +423,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg2", choices=list(synth.CONFIGS))
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--cg-ratio", type=float, default=0.0,
+                    help="Newton strategy: CG when r > ratio*m (0: the paper's rule, min(m, r) > 1e4)")
     ap.add_argument("--control", default="graph", choices=["graph", "host"],
                     help="graph: Algorithm 1 control on the device in one CUDA graph; host: CPU decisions")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg (40 GB configs)")

@@ -44,8 +44,9 @@ typedef struct {
   int32_t psi_evals;       /* ψ evaluations (Armijo trials incl. backtracks)              */
   int32_t backtracks;      /* step halvings                                               */
   int32_t aty_passes;      /* full passes over A (K1 launches)                            */
-  int32_t branch_steps[3]; /* Newton steps with r = 0, 0 < r < m (Eq. 19), r ≥ m (Eq. 18) */
+  int32_t branch_steps[4]; /* Newton steps with r = 0, 0 < r < m (Eq. 19), r ≥ m (Eq. 18), CG (R32) */
   int32_t line_search_stalled; /* max_backtracks reached at least once (R30)              */
+  int32_t cg_iters;        /* conjugate-gradient iterations, summed over CG steps             */
   int64_t active;          /* nnz(x) at return                                            */
   double res_kkt1;         /* ‖y + b − Ax‖/(1 + ‖b‖) at the last evaluation, Eq. (20)    */
   double res_kkt3;         /* ‖Aᵀy + z‖/(1 + ‖y‖ + ‖z‖) at the last outer step, Eq. (20) */
@@ -78,8 +79,15 @@ double ssnal_en_lambda_max_l1(const ssnal_en_problem* p);
 /* Options (defaults from P:497 and DESIGN.md readings):
  *   sigma_factor=5, sigma_max=1e8, mu=0.2, beta=0.5, max_outer=100, max_inner=100,
  *   max_backtracks=50, init_mode=1 (y0 = A x0 − b when x0 ≠ 0, else y0 = 0; 0: always y0 = 0),
- *   time_k1=0 (1: time every K1 launch with CUDA events → stats.k1_time_s),
- *   cluster_size=0 (auto: 16 if the device allows, else 8).  EINVAL for unknown keys. */
+ *   time_k1=0 (1: time every K1 launch → stats.k1_time_s; CUDA events in host-driven mode,
+ *     in-kernel %globaltimer stamps inside the graph),
+ *   cluster_size=0 (auto: 16 if the device allows, else 8),
+ *   graph=1 (Algorithm 1 control on the device, the whole solve one CUDA graph; 0: host-driven
+ *     control with one evaluation record read per ψ evaluation — identical results),
+ *   Newton-system strategy (Algorithm 1 step (1); reading R32): conjugate gradient
+ *     when r > cg_ratio·m (cg_ratio=0: off) or min(m, r) > cg_threshold (=1e4), else the
+ *     exact branches; cg_tol=1e-10 (stop at ‖V d + ∇ψ‖ ≤ cg_tol‖∇ψ‖), cg_maxit=1000.
+ *   EINVAL for unknown keys. */
 int ssnal_en_set_option(ssnal_en_problem* p, const char* key, double value);
 
 /* Read-only introspection: "m", "n", "k1_cols", "k1_stages", "k1_grid", "k1_smem",
@@ -118,10 +126,11 @@ int ssnal_en_epilogue(ssnal_en_problem* p, const double* w0, const double* w1, d
                       double sigma, double lambda1, double lambda2, double* w_out, int32_t* J_out,
                       double* PJ_out, int64_t* r_out, double partials_out[4]);
 
-/* K2–K4 hook: the Newton direction d (device, m) solving (I_m + κ A_J A_Jᵀ) d = −g for the
+/* K2–K4/K6 hook: the Newton direction d (device, m) solving (I_m + κ A_J A_Jᵀ) d = −g for the
  * active set J (device int32, r entries, ascending) and g (device, m): r = 0 → d = −g;
- * 0 < r < m → SMW Eq. (19); r ≥ m → m × m Cholesky Eq. (18).  *gd_out (host) = gᵀd,
- * *branch_out (host) ∈ {0, 1, 2}.  SSNAL_ENUMERIC if a Cholesky pivot is not positive. */
+ * 0 < r < m → SMW Eq. (19); r ≥ m → m × m Cholesky Eq. (18); CG (K6) when the cg_* options
+ * select it.  *gd_out (host) = gᵀd, *branch_out (host) ∈ {0, 1, 2, 3}.  SSNAL_ENUMERIC if a
+ * Cholesky pivot is not positive. */
 int ssnal_en_newton_direction(ssnal_en_problem* p, const int32_t* J, int64_t r, const double* g, double kappa,
                               double* d_out, double* gd_out, int32_t* branch_out);
 

@@ -14,12 +14,14 @@
 #include "common.cuh"
 #include "k_aty.cuh"
 #include "k_newton.cuh"
+#include "k_cg.cuh"
 
 namespace ssn {
 
 struct DevCtl {
   // per-solve settings (host-written before the graph launch)
   double l1, l2, tol, sigma, sigma_factor, sigma_max, mu, beta;
+  double cg_ratio, cg_threshold;  // Newton strategy (R32)
   int max_outer, max_inner, max_bt, pad0;
   // state
   Scal sc;           // σ-dependent scalars of the current outer iteration
@@ -29,7 +31,7 @@ struct DevCtl {
   int converged, numeric, numeric_kind, stalled;
   DirGeo geo;        // direction geometry for the current r
   // statistics (same meaning as ssnal_en_stats)
-  int outer_iters, newton_iters, psi_evals, backtracks, aty_passes, branch_steps[3];
+  int outer_iters, newton_iters, psi_evals, backtracks, aty_passes, branch_steps[4], cg_iters;
   int seg_outer, seg_inner, seg_bt, seg_grad;  // segment executions (kernel-launch accounting)
   double res1, res3, sigma_final;
   long long numeric_r;
@@ -76,7 +78,7 @@ SSN_DEV int bt_next(DevCtl* C, bool ok) {
 SSN_DEV int inner_next(DevCtl* C, const EvalOut* ev0, int64_t m, int nsm, int wsplits, int* info) {
   const int go = (C->numeric == 0) && (C->j < C->max_inner) && !(ev0->res1 <= C->tol);
   if (go) {
-    C->geo = make_geo(ev0->r, m, nsm, wsplits, C->sc.kappa, C->kinv);
+    C->geo = make_geo(ev0->r, m, nsm, wsplits, C->sc.kappa, C->kinv, C->cg_ratio, C->cg_threshold);
     *info = 0;
   }
   return go;
@@ -111,7 +113,7 @@ __global__ void k_ctl_armijo(DevCtl* C, const EvalOut* ev0, const EvalOut* ev1, 
   C->tstamp[1] = 0ull;
   C->nbt = 0;
   C->s = 1.0;
-  if (C->geo.branch > 0 && ev1->info != 0) {
+  if ((C->geo.branch == 1 || C->geo.branch == 2) && ev1->info != 0) {
     C->numeric = 1;
     C->numeric_kind = 1;
     C->numeric_r = C->geo.r;

@@ -23,14 +23,20 @@ namespace ssn {
 // modes launch identical work decompositions and produce bitwise-identical results.
 // ---------------------------------------------------------------------------
 struct DirGeo {
-  int branch;          // 0: r = 0 (d = −g), 1: 0 < r < m (SMW, Eq. (19)), 2: r ≥ m (Eq. (18))
+  int branch;          // 0: r = 0 (d = −g), 1: 0 < r < m (SMW, Eq. (19)), 2: r ≥ m (Eq. (18)), 3: CG (R32)
   int N, NR, ld;       // factor order, rows incl. the rhs row, leading dimension of Mmat
   int tiles, ns;       // Gram lower 32 × 32 tiles and split-K slices
   int bgrid;           // SMW back-substitution CTAs
   int pad;
   long long r, nout, nmat;
-  double diag, mult;   // reduce: M = diag·I + mult·Σ_s W[s]
+  double diag, mult;   // reduce: M = diag·I + mult·Σ_s W[s]; CG: mult = κ
 };
+
+// Strategy (R12, R32): CG iff r > cg_ratio·m (cg_ratio > 0) or min(m, r) > cg_threshold.
+SSN_HD bool use_cg(long long r, long long m, double cg_ratio, double cg_threshold) {
+  const long long mn = r < m ? r : m;
+  return r > 0 && ((cg_ratio > 0.0 && (double)r > cg_ratio * (double)m) || (double)mn > cg_threshold);
+}
 
 // split-K slices: enough (tile, slice) items to cover 2 CTAs per SM, ≤ one slice per 32-chunk
 SSN_HD int gram_splits(int nsm, int tiles, long long K, int wsplits) {
@@ -41,12 +47,19 @@ SSN_HD int gram_splits(int nsm, int tiles, long long K, int wsplits) {
   return ns < 1 ? 1 : ns;
 }
 
-SSN_HD DirGeo make_geo(long long r, long long m, int nsm, int wsplits, double kappa, double kinv) {
+SSN_HD DirGeo make_geo(long long r, long long m, int nsm, int wsplits, double kappa, double kinv, double cg_ratio,
+                       double cg_threshold) {
   DirGeo g;
   g.r = r;
   g.pad = 0;
   g.bgrid = 1;
-  if (r == 0) {
+  if (use_cg(r, m, cg_ratio, cg_threshold)) {
+    g.branch = 3;
+    g.N = g.NR = g.ld = g.tiles = g.ns = 0;
+    g.nout = g.nmat = 0;
+    g.diag = 0.0;
+    g.mult = kappa;
+  } else if (r == 0) {
     g.branch = 0;
     g.N = g.NR = g.ld = g.tiles = g.ns = 0;
     g.nout = g.nmat = 0;

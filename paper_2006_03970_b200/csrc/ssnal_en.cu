@@ -108,6 +108,18 @@ bsub_fn bsub_for(int mr) {
     default: return k_smw_backsub<32>;
   }
 }
+typedef void (*cg_fn)(const CgParams);
+cg_fn cg_for(int mr) {
+  switch (mr) {
+    case 1: return k_cg_newton<1>;
+    case 2: return k_cg_newton<2>;
+    case 4: return k_cg_newton<4>;
+    case 8: return k_cg_newton<8>;
+    case 16: return k_cg_newton<16>;
+    case 25: return k_cg_newton<25>;
+    default: return k_cg_newton<32>;
+  }
+}
 gax_fn gax_for(int mr) {
   switch (mr) {
     case 1: return k_gather_axpy<1>;
@@ -235,12 +247,18 @@ struct ssnal_en_problem {
   int* flags = nullptr;
   double* blk = nullptr;       // eval-reduce per-CTA partials
   int* gax_valid = nullptr;    // device-r gather: CTA had columns
+  double* cg_res = nullptr;    // K6: residual (m), per-CTA partials (nsm × m), scalars (2 nsm)
+  double* cg_parts = nullptr;
+  double* cg_scal = nullptr;
+  size_t cg_smem_bytes = 0;
   unsigned* ticket = nullptr;  // eval-reduce last-block counter
   // state
   double lambda_max = 0, nb = 0;
   // options
   double sigma_factor = 5.0, sigma_max = 1e8, mu = 0.2, beta = 0.5;
   int max_outer = 100, max_inner = 100, max_bt = 50, init_mode = 1, time_k1 = 0;
+  double cg_ratio = 0.0, cg_threshold = 1e4, cg_tol = 1e-10;  // Newton strategy (R32)
+  int cg_maxit = 1000;
   // counters for the current call
   int64_t launches = 0;
   double stat_l1 = 0, stat_l2 = 0;
@@ -309,6 +327,8 @@ int configure(ssnal_en_problem* P) {
   const size_t gsm = (size_t)8 * m * 8;
   CK(cudaFuncSetAttribute(gax_for(P->MR), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsm));
   CK(cudaFuncSetAttribute(bsub_for(P->MR), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsm));
+  P->cg_smem_bytes = cg_smem(m);
+  CK(cudaFuncSetAttribute(cg_for(P->MR), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->cg_smem_bytes));
   P->chol_smem = kCholSmem;
   CK(cudaFuncSetAttribute(k_chol_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->chol_smem));
   CK(cudaFuncSetAttribute(k_chol_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -369,6 +389,9 @@ int allocate(ssnal_en_problem* P) {
   AL(P->blk, (size_t)((m + 31) / 32) * 3 * 8 + 64);
   AL(P->ticket, 64);
   AL(P->gax_valid, 4 * 256);
+  AL(P->cg_res, m * 8);
+  AL(P->cg_parts, (size_t)P->nsm * m * 8);
+  AL(P->cg_scal, (size_t)P->nsm * 2 * 8 + 64);
   CK(cudaMemset(P->ticket, 0, 64));
   CK(cudaHostAlloc((void**)&P->ev_host, sizeof(EvalOut) * 4, cudaHostAllocMapped));
   memset(P->ev_host, 0, sizeof(EvalOut) * 4);
@@ -591,6 +614,42 @@ int launch_chol(ssnal_en_problem* P, double* M, int N, double* out, double scale
   return SSNAL_OK;
 }
 
+// K6: CG Newton direction, one cooperative launch (nsm CTAs, grid barriers); host values or geo.
+int launch_cg(ssnal_en_problem* P, const int32_t* J, int64_t r, const double* g, double kappa, double* d,
+              double* gd_dev, const double* y, double* yt, const DirGeo* geo) {
+  CgParams c;
+  c.A = P->A;
+  c.m = P->m;
+  c.J = J;
+  c.r = r;
+  c.g = g;
+  c.kappa = kappa;
+  c.tol = P->cg_tol;
+  c.maxit = P->cg_maxit;
+  c.y = y;
+  c.d = d;
+  c.yt = yt;
+  c.gd_out = gd_dev;
+  c.res = P->cg_res;
+  c.parts = P->cg_parts;
+  c.scal = P->cg_scal;
+  c.iters_out = &P->ctl->cg_iters;
+  c.geo = geo;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(P->nsm);
+  cfg.blockDim = dim3(K6_THREADS);
+  cfg.dynamicSmemBytes = P->cg_smem_bytes;
+  cfg.stream = P->st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, cg_for(P->MR), c));
+  P->launches++;
+  return SSNAL_OK;
+}
+
 // Gram / reduce grids: persistent CTAs (results do not depend on the grid; DirGeo fixes the work)
 int gram_grid(ssnal_en_problem* P, int items) { return items < 2 * P->nsm ? (items < 1 ? 1 : items) : 2 * P->nsm; }
 unsigned reduce_grid(ssnal_en_problem* P, int64_t tot) {
@@ -604,8 +663,10 @@ unsigned reduce_grid(ssnal_en_problem* P, int64_t tot) {
 int newton_direction(ssnal_en_problem* P, const int32_t* J, int64_t r, const double* g, double kappa, double* d,
                      double* gd_dev, int* branch, const double* y = nullptr, double* yt = nullptr) {
   const int64_t m = P->m;
-  const DirGeo geo = make_geo(r, m, P->nsm, P->W_splits, kappa, 1.0 / kappa);
+  const DirGeo geo = make_geo(r, m, P->nsm, P->W_splits, kappa, 1.0 / kappa, P->cg_ratio, P->cg_threshold);
   *branch = geo.branch;
+  if (geo.branch == 3)  // K6: conjugate gradient (R32)
+    return launch_cg(P, J, r, g, kappa, d, gd_dev, y, yt, nullptr);
   if (geo.branch == 0) {
     k_neg_copy<<<1, 1024, 0, P->st>>>(m, g, d, g, gd_dev, y, yt, nullptr);
     P->launches++;
@@ -666,7 +727,9 @@ int newton_direction_graph(ssnal_en_problem* P) {
   k_gram_reduce<<<reduce_grid(P, m * m), 256, 0, P->st>>>(P->W, 0, 0, 0, 0.0, 0.0, P->Mmat, 0, g, geo, 2);
   P->launches += 3;
   CKL();
-  return launch_chol(P, P->Mmat, 0, P->d, -1.0, g, gd, P->y[0], P->y[1], geo, 2);
+  rc = launch_chol(P, P->Mmat, 0, P->d, -1.0, g, gd, P->y[0], P->y[1], geo, 2);
+  if (rc) return rc;
+  return launch_cg(P, J, 0, g, 0.0, P->d, gd, P->y[0], P->y[1], geo);  // predicated on branch 3
 }
 
 int check_args(ssnal_en_problem* P, double l1, double l2, double sigma0, double tol) {
@@ -752,6 +815,7 @@ int solve_core(ssnal_en_problem* P, double l1, double l2, double sigma0, double 
   int wcur = 0; // index of current w buffer (0..2)
   EvalOut ev, evt;
   int64_t rx = 0;
+  CK(cudaMemsetAsync(&P->ctl->cg_iters, 0, sizeof(int), P->st));
   if ((rc = init_point(P, have_x0, S, &rx))) return rc;
 
   double sigma = sigma0;
@@ -783,11 +847,11 @@ int solve_core(ssnal_en_problem* P, double l1, double l2, double sigma0, double 
       S->aty_passes++;
       if ((rc = launch_finalize(P, P->J[tr], P->PJ[tr], P->r_dev + tr))) return rc;
       if ((rc = launch_eval(P, P->y[tr], sc, 1, P->cta_cnt, P->G, P->g[tr], P->r_dev + tr, 1, gd_dev,
-                            br > 0 ? P->info : nullptr)))
+                            (br == 1 || br == 2) ? P->info : nullptr)))
         return rc;
       if ((rc = fetch_eval(P, 1, &evt))) return rc;
       S->psi_evals++;
-      if (br > 0 && evt.info != 0) {
+      if ((br == 1 || br == 2) && evt.info != 0) {
         numeric = 1;
         set_err("Cholesky pivot not positive (branch %d, r=%lld)", br, (long long)ev.r);
         break;
@@ -877,6 +941,7 @@ int solve_core(ssnal_en_problem* P, double l1, double l2, double sigma0, double 
   // Stats: F(x) (Eq. (1)) via resid = A x − b; D(y) = −½yᵀy − bᵀy − Σ(|w|−λ1)²₊/(2λ2)
   if ((rc = launch_objective(P))) return rc;
   S->dual_obj = (l2 > 0) ? (-(0.5 * ev.yy + ev.by) - ev.s[3] / (2.0 * l2)) : NAN;
+  CK(cudaMemcpyAsync(P->scratch_host + 40, &P->ctl->cg_iters, sizeof(int), cudaMemcpyDeviceToHost, P->st));
   P->stat_l1 = l1;
   P->stat_l2 = l2;
   P->stat_warm_pass = (have_x0 && P->init_mode == 1);
@@ -1078,6 +1143,8 @@ int solve_graph_core(ssnal_en_problem* P, double l1, double l2, double sigma0, d
   h->max_outer = P->max_outer;
   h->max_inner = P->max_inner;
   h->max_bt = P->max_bt;
+  h->cg_ratio = P->cg_ratio;
+  h->cg_threshold = P->cg_threshold;
   h->tstamp[0] = ~0ull;
   h->tstamp[1] = 0ull;
   CK(cudaMemcpyAsync(P->ctl, h, sizeof(DevCtl), cudaMemcpyHostToDevice, P->st));
@@ -1102,7 +1169,8 @@ void finish_stats(ssnal_en_problem* P, ssnal_en_stats* S) {
     S->psi_evals = C->psi_evals;
     S->backtracks = C->backtracks;
     S->aty_passes += C->aty_passes;
-    for (int b = 0; b < 3; ++b) S->branch_steps[b] = C->branch_steps[b];
+    for (int b = 0; b < 4; ++b) S->branch_steps[b] = C->branch_steps[b];
+    S->cg_iters = C->cg_iters;
     S->line_search_stalled = C->stalled;
     S->res_kkt1 = C->res1;
     S->res_kkt3 = C->res3;
@@ -1120,6 +1188,10 @@ void finish_stats(ssnal_en_problem* P, ssnal_en_stats* S) {
       P->k1_count += C->k1_cnt;
     }
     P->graph_pending = false;
+  } else {
+    int it = 0;
+    memcpy(&it, P->scratch_host + 40, sizeof(int));
+    S->cg_iters = it;
   }
   const double* o = P->scratch_host + 16;
   S->primal_obj = o[0] + P->stat_l1 * o[1] + 0.5 * P->stat_l2 * o[2];
@@ -1212,6 +1284,9 @@ static void destroy_bufs(ssnal_en_problem* P) {
   cudaFree(P->blk);
   cudaFree(P->ticket);
   cudaFree(P->gax_valid);
+  cudaFree(P->cg_res);
+  cudaFree(P->cg_parts);
+  cudaFree(P->cg_scal);
   if (P->ev_host) cudaFreeHost(P->ev_host);
   if (P->scratch_host) cudaFreeHost(P->scratch_host);
   drop_graph(P);
@@ -1324,6 +1399,10 @@ int ssnal_en_set_option(ssnal_en_problem* P, const char* key, double v) {
   else if (k == "init_mode" && (v == 0 || v == 1)) P->init_mode = (int)v;
   else if (k == "time_k1") P->time_k1 = v != 0;
   else if (k == "graph" && (v == 0 || v == 1)) P->use_graph = (int)v;
+  else if (k == "cg_ratio" && v >= 0) P->cg_ratio = v;
+  else if (k == "cg_threshold" && v >= 0) P->cg_threshold = v;
+  else if (k == "cg_tol" && v > 0 && v < 1) P->cg_tol = v;
+  else if (k == "cg_maxit" && v >= 1) P->cg_maxit = (int)v;
   else if (k == "cluster_size" && (v == 1 || v == 2 || v == 4 || v == 8 || v == 16)) {
     P->cluster = (int)v;
     drop_graph(P);  // the cluster launch configuration is baked into the graph
@@ -1346,6 +1425,8 @@ double ssnal_en_get_info(const ssnal_en_problem* P, const char* key) {
   if (k == "cluster_size") return P->cluster;
   if (k == "num_sms") return P->nsm;
   if (k == "graph") return P->use_graph;
+  if (k == "cg_ratio") return P->cg_ratio;
+  if (k == "cg_threshold") return P->cg_threshold;
   return NAN;
 }
 
@@ -1461,7 +1542,7 @@ int ssnal_en_newton_direction(ssnal_en_problem* P, const int32_t* J, int64_t r, 
   if (branch_out) *branch_out = br;
   int info = 0;
   memcpy(&info, P->scratch_host + 1, 4);
-  if (br > 0 && info) {
+  if ((br == 1 || br == 2) && info) {
     set_err("Cholesky pivot not positive");
     return SSNAL_ENUMERIC;
   }

@@ -28,8 +28,8 @@ class Stats(ctypes.Structure):
     """Mirror of ssnal_en_stats."""
 
     _fields_ = [("status", _i32), ("outer_iters", _i32), ("newton_iters", _i32), ("psi_evals", _i32),
-                ("backtracks", _i32), ("aty_passes", _i32), ("branch_steps", _i32 * 3),
-                ("line_search_stalled", _i32), ("active", _i64), ("res_kkt1", _d), ("res_kkt3", _d),
+                ("backtracks", _i32), ("aty_passes", _i32), ("branch_steps", _i32 * 4),
+                ("line_search_stalled", _i32), ("cg_iters", _i32), ("active", _i64), ("res_kkt1", _d), ("res_kkt3", _d),
                 ("primal_obj", _d), ("dual_obj", _d), ("gap", _d), ("sigma_final", _d),
                 ("time_device_s", _d), ("time_total_s", _d), ("kernel_launches", _i64), ("k1_time_s", _d),
                 ("k1_launches", _i32), ("reserved", _i32)]

@@ -4,6 +4,8 @@ import ctypes
 import os
 import re
 
+import pytest
+
 import paper_2006_03970_b200 as pkg
 from paper_2006_03970_b200 import ssnal_en as binding
 
@@ -30,14 +32,32 @@ def test_version_and_error_without_gpu():
     assert isinstance(lib.ssnal_en_last_error(), bytes)
 
 
-def test_stats_struct_layout_matches_header():
-    # header: 10 int32 (incl. 3-array) + int64 + 8 doubles + int64 + double + 2 int32
-    assert ctypes.sizeof(binding.Stats) == 10 * 4 + 8 + 8 * 8 + 8 + 8 + 2 * 4
-    fields = [f for f, _ in binding.Stats._fields_]
-    hdr = open(os.path.join(ROOT, "include", "ssnal_en.h")).read()
-    body = hdr[hdr.index("typedef struct {"):hdr.index("} ssnal_en_stats;")]
+def _c_layout(struct, fields):
+    """sizeof and offsetof of a header struct, compiled with gcc from include/ssnal_en.h."""
+    import subprocess
+    import tempfile
+    src = "#include <stdio.h>\n#include <stddef.h>\n#include \"ssnal_en.h\"\nint main(void){printf(\"%zu\", sizeof(" + struct + "));"
     for f in fields:
-        assert re.search(r"\b" + f + r"\b", body), f
+        src += 'printf(" %zu", offsetof(' + struct + ", " + f + "));"
+    src += "return 0;}\n"
+    with tempfile.TemporaryDirectory() as d:
+        c, exe = os.path.join(d, "l.c"), os.path.join(d, "l")
+        open(c, "w").write(src)
+        subprocess.run(["gcc", "-I" + os.path.join(ROOT, "include"), c, "-o", exe], check=True)
+        out = subprocess.run([exe], check=True, capture_output=True, text=True).stdout.split()
+    return int(out[0]), [int(v) for v in out[1:]]
+
+
+@pytest.mark.parametrize("name,cls", [("ssnal_en_stats", "Stats"), ("ssnal_en_criteria", "Criteria")])
+def test_struct_layout_matches_header(name, cls):
+    """ctypes mirrors have the header's size and every field at the header's offset."""
+    C = getattr(binding, cls)
+    fields = [f for f, _ in C._fields_]
+    size, offs = _c_layout(name, fields)
+    assert ctypes.sizeof(C) == size
+    for f, off in zip(fields, offs):
+        assert getattr(C, f).offset == off, f
+
 
 
 def test_no_cpu_fallback_in_product():
