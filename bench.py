@@ -113,9 +113,23 @@ def max_over_ranks(v: float, device: str = "cuda") -> float:
     return float(t.item())
 
 
-def k1_bytes(m, n):
-    """Algorithmic bytes of one fused K1 launch: A once (8mn), x read + w write (16n), y (8m)."""
-    return 8 * m * n + 16 * n + 8 * m
+def k1_bytes(m, n, geno=False):
+    """Algorithmic bytes of one fused K1 launch: A once (8mn fp64, or packed codes n·stride + 24n
+    tables for the §8(f4) genotype storage), x read + w write (16n), y (8m)."""
+    a = n * synth.geno_stride(m) + 24 * n if geno else 8 * m * n
+    return a + 16 * n + 8 * m
+
+
+def geno_roofline(m, n, k1_avg, k1_gbs, hbm_peak, traffic):
+    """K1g (packed genotype codes) moves 32x fewer bytes than K1 and is bound by the
+    FP64 pipe, not HBM: per decoded element two bucket adds (DADD) — peak = 64 FP64 ops/clk/SM
+    (measured, tools/probes/mma_probe) x 148 SMs x 1.965 GHz / 2 elements/s.  Also reports the HBM view."""
+    peak_el = 64 * 148 * 1.965e9 / 2 / 1e9  # Gelem/s
+    ach = m * n / k1_avg / 1e9 if k1_avg else None
+    return {"bound": "alu", "achieved": ach, "peak": peak_el, "unit": "Gelem/s",
+            "frac": (ach / peak_el) if ach else None, "traffic": traffic,
+            "peak_source": "derived: FP64 add rate (measured 64/clk/SM) / 2 adds per element",
+            "hbm_view": {"achieved_GBps": k1_gbs, "peak_GBps": hbm_peak}}
 
 
 def run_path_device(P, cfg, lm, x_buf, x_prev_ptr=None):
@@ -144,12 +158,23 @@ def bench_ours(args, rank, world, local_rank):
     cfg = synth.CONFIGS[args.config]
     m, n = cfg.m, cfg.n
     stream = torch.cuda.current_stream()
-    dA = torch.empty((n, m), dtype=torch.float64, device="cuda")
-    synth.fill_device(cfg, dA.data_ptr(), stream.cuda_stream)
     b_host, _ = synth.response(cfg)
     db = torch.from_numpy(b_host).cuda()
-    torch.cuda.synchronize()
-    P = Problem.from_device(dA.data_ptr(), db.data_ptr(), m, n, stream.cuda_stream, keep=(dA, db))
+    if args.geno:  # §8(f4): A as packed 2-bit genotype codes + per-column tables
+        if cfg.kind != synth.GENO_STD:
+            raise SystemExit("--geno needs a genotype config (cfg4)")
+        stride = synth.geno_stride(m)
+        dA = torch.empty((n, stride), dtype=torch.uint8, device="cuda")
+        dtab = torch.empty((n, 3), dtype=torch.float64, device="cuda")
+        synth.fill_device_geno(cfg, dA.data_ptr(), dtab.data_ptr(), stream.cuda_stream)
+        torch.cuda.synchronize()
+        P = Problem.from_geno_device(dA.data_ptr(), stride, dtab.data_ptr(), db.data_ptr(), m, n, stream.cuda_stream,
+                                     keep=(dA, dtab, db))
+    else:
+        dA = torch.empty((n, m), dtype=torch.float64, device="cuda")
+        synth.fill_device(cfg, dA.data_ptr(), stream.cuda_stream)
+        torch.cuda.synchronize()
+        P = Problem.from_device(dA.data_ptr(), db.data_ptr(), m, n, stream.cuda_stream, keep=(dA, db))
     P.set_option("graph", 1 if args.control == "graph" else 0)
     P.set_option("cg_ratio", args.cg_ratio)
     lm = P.lambda_max_l1
@@ -191,7 +216,25 @@ def bench_ours(args, rank, world, local_rank):
     # ---- e2e: through the C-ABI with HOST buffers (create + H2D + solves + D2H) ----
     A_host = None
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and args.geno:
+        codes_h, tab_h = synth.geno_codes(cfg)
+        e2e_times = []
+        for it in range(max(1, min(args.steps, 3)) + 1):
+            t0 = time.perf_counter()
+            Q = Problem.from_geno(codes_h, tab_h, b_host)
+            Q.set_option("graph", 1 if args.control == "graph" else 0)
+            lmq = Q.lambda_max_l1
+            x_prev = None
+            for i, c in enumerate(cfg.cs):
+                l1, l2 = lambdas(cfg, lmq, c)
+                x_prev, st = Q.solve(l1, l2, cfg.sigma0, cfg.tol, x0=x_prev if cfg.path else None)
+            Q.close()
+            if it > 0:
+                e2e_times.append(time.perf_counter() - t0)
+        e2e = {"value": max_over_ranks(statistics.median(e2e_times)), "unit": "s",
+               "h2d_bytes_per_step": int(codes_h.nbytes + tab_h.nbytes + 8 * m),
+               "d2h_bytes_per_step": 8 * n * len(cfg.cs)}
+    elif not args.no_e2e:
         A_host = torch.empty((n, m), dtype=torch.float64, pin_memory=True)
         A_host.copy_(dA.cpu())
         A_np = A_host.numpy()
@@ -222,13 +265,13 @@ def bench_ours(args, rank, world, local_rank):
 
     peak, peak_src = _peaks()
     k1_avg = k1_time / max(k1_launches, 1)
-    k1_gbs = k1_bytes(m, n) / k1_avg / 1e9 if k1_launches else None
+    k1_gbs = k1_bytes(m, n, args.geno) / k1_avg / 1e9 if k1_launches else None
     traffic = None
     tp = os.path.join(ROOT, "profiles", "k1_traffic.json")
     if os.path.exists(tp):
         try:
             tj = json.load(open(tp))
-            traffic = tj.get(args.config)
+            traffic = tj.get(args.config + ("_geno" if args.geno else ""))
         except Exception:
             traffic = None
     res = {
@@ -251,13 +294,16 @@ def bench_ours(args, rank, world, local_rank):
                    "parallelism": f"replicas x{world}",
                    "control": ("device-resident, one CUDA graph per solve (nested conditional WHILE)"
                                if args.control == "graph" else "host-driven (per-evaluation readback)"),
+                   "storage": ("packed 2-bit genotype codes + per-column tables (SURVEY 8(f4))" if args.geno
+                               else "fp64 column-major"),
                    "newton_strategy": ("exact (Eq. 18/19); CG when min(m, r) > 1e4 (P:379)" if args.cg_ratio == 0
                                        else f"CG (K6) when r > {args.cg_ratio:g} m, else exact (Eq. 18/19)")},
-        "roofline": {"bound": "hbm", "achieved": k1_gbs, "peak": peak, "unit": "GB/s",
-                     "frac": (k1_gbs / peak) if k1_gbs else None, "traffic": traffic,
-                     "kernel": "k1_aty_fused", "bytes_per_launch": k1_bytes(m, n), "launches": k1_launches,
-                     "mean_launch_us": k1_avg * 1e6, "share_of_step": k1_time / max(elapsed, 1e-30),
-                     "peak_source": peak_src},
+        "roofline": {**({"bound": "hbm", "achieved": k1_gbs, "peak": peak, "unit": "GB/s",
+                         "frac": (k1_gbs / peak) if k1_gbs else None, "traffic": traffic, "peak_source": peak_src}
+                        if not args.geno else geno_roofline(m, n, k1_avg, k1_gbs, peak, traffic)),
+                     "kernel": "k1g_aty_fused" if args.geno else "k1_aty_fused",
+                     "bytes_per_launch": k1_bytes(m, n, args.geno), "launches": k1_launches,
+                     "mean_launch_us": k1_avg * 1e6, "share_of_step": k1_time / max(elapsed, 1e-30)},
         "e2e": e2e,
         "gpu_launches": launches // max(args.steps, 1),
         "clocks": clk.summary(),
@@ -267,7 +313,7 @@ def bench_ours(args, rank, world, local_rank):
                         "res1": s["res_kkt1"], "res3": s["res_kkt3"], "gap": s["gap"]}
                        for c, s in zip(cfg.cs, last_stats)],
     }
-    if rank == 0 and not args.no_cpu and world == 1:
+    if rank == 0 and not args.no_cpu and world == 1 and not args.geno:
         res["cpu_baseline"] = cpu_baseline(cfg, b_host, A_host.numpy() if A_host is not None else dA.cpu().numpy())
     P.close()
     return res
@@ -423,6 +469,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg2", choices=list(synth.CONFIGS))
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--geno", action="store_true",
+                    help="cfg4 from packed 2-bit genotype codes (SURVEY 8(f4)) instead of fp64")
     ap.add_argument("--cg-ratio", type=float, default=0.0,
                     help="Newton strategy: CG when r > ratio*m (0: the paper's rule, min(m, r) > 1e4)")
     ap.add_argument("--control", default="graph", choices=["graph", "host"],

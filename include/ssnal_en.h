@@ -8,6 +8,8 @@
  * Sherman–Morrison–Woodbury form Eq. (19), Armijo line search Eq. (13)
  * (μ = 0.2 at P:497), KKT residuals Eq. (20), σ ← 5σ.
  * Readings of garbled / silent passages are listed in DESIGN.md ("Readings").
+ * A is either fp64 column-major (ssnal_en_create*) or packed 2-bit genotype codes with
+ * per-column tables (ssnal_en_create_geno*).
  *
  * Conventions (all entry points):
  *   - fp64 throughout; A is column-major m × n with lda = m (column i = A + i*m).
@@ -72,6 +74,22 @@ int ssnal_en_create(const double* A_colmajor, const double* b, int64_t m, int64_
  * is used for every launch.  Inputs are validated on the device (NaN/Inf, zero columns). */
 int ssnal_en_create_device(const double* dA, const double* db, int64_t m, int64_t n, void* cuda_stream,
                            ssnal_en_problem** out);
+
+/* Compressed genotype storage (not in the paper): A given as 2-bit codes
+ * g ∈ {0, 1, 2} with a per-column table, a_kj = tab[3j + g_kj] (e.g. the standardised value
+ * (g − mean_j)/sd_j, which synth/ computes bit-exactly with its fp64 design).  Column j is
+ * `stride` bytes at codes + j·stride (stride a multiple of 16, ≥ ceil(m/4)); row k lives in
+ * bits 2(k mod 4)..2(k mod 4)+1 of byte k/4, padding bits zero.  K1 streams 32× fewer bytes
+ * than fp64; every other kernel decodes the columns it touches.  Everything else (options,
+ * solve, hooks, model selection) is as for the fp64 handle.
+ *   _device: codes, tab, db are device pointers borrowed until destroy (codes 16-B aligned).
+ *   host:    copies codes (n·stride bytes), tab (3n doubles) and b to the device.
+ * EINVAL: bad sizes/stride, a code of value 3, a non-finite table entry or b, or a column
+ * whose decoded entries are all zero. */
+int ssnal_en_create_geno_device(const uint8_t* codes, int64_t stride, const double* tab, const double* db, int64_t m,
+                                int64_t n, void* cuda_stream, ssnal_en_problem** out);
+int ssnal_en_create_geno(const uint8_t* codes, int64_t stride, const double* tab, const double* b, int64_t m,
+                         int64_t n, ssnal_en_problem** out);
 
 /* ‖Aᵀb‖∞ computed at create (plain K1 pass).  λ1 ≥ this value gives x = 0. */
 double ssnal_en_lambda_max_l1(const ssnal_en_problem* p);

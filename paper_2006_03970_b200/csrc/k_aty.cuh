@@ -50,6 +50,10 @@ struct K1Params {
   int fused;            // 0: plain w = Aᵀy (+ max|w|), 1: full epilogue
   uint32_t stage_elems; // doubles per A stage buffer (≥ C*m, multiple of 16)
   uint32_t xstage_elems;// doubles per x stage buffer (≥ C, multiple of 16)
+  // packed genotype storage (K1g); A == nullptr
+  const uint8_t* codes; // n × cstride bytes: 2-bit codes, row k in bits 2(k%4) of byte k/4
+  const double* tab;    // n × 3: decoded value of codes 0, 1, 2 for each column
+  int64_t cstride;      // bytes per column (multiple of 16)
 };
 
 // Reduce-scatter of 8 per-lane partial sums a[0..7] across the warp: afterwards every
@@ -78,6 +82,109 @@ SSN_DEV double reduce8(double (&a)[8], int lane) {
   a[0] += __shfl_xor_sync(0xffffffffu, a[0], 2);
   a[0] += __shfl_xor_sync(0xffffffffu, a[0], 1);
   return a[0];
+}
+
+// CTA end of K1 / K1g (consumer warps only; the ring is idle and holds the warps' ∇ψ partial
+// rows rv[warp][0..m) when fused): fixed-order reductions of the partial scalars and rows, then
+// the ordered compaction of this CTA's active columns from the bitmap (P recomputed from w).
+SSN_DEV void k1_cta_end(const K1Params& p, const Scal& sc, double* ring, int* sh, int64_t c_lo, int64_t c_hi,
+                        double s0, double s1, double s2, double s3, bool any_active) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t m = p.m;
+  double* rv = ring;                       // K1_NWC x m
+  double* rs = ring + (size_t)K1_NWC * m;  // K1_NWC x 4
+  int* ract = reinterpret_cast<int*>(rs + K1_NWC * 4);
+  // warp partial scalars: leader lanes 0,4,...,28 in lane order (plain mode: max over lanes)
+  double q4[4] = {s0, s1, s2, s3};
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    double acc = 0.0;
+    for (int l = 0; l < 32; l += 4) {
+      const double v = __shfl_sync(0xffffffffu, q4[j], l);
+      acc = p.fused ? __dadd_rn(acc, v) : fmax(acc, v);
+    }
+    if (!p.fused) acc = warp_allmax(q4[j]);
+    q4[j] = acc;
+  }
+  const bool wact = __any_sync(0xffffffffu, any_active);
+  if (lane == 0) {
+    for (int j = 0; j < 4; ++j) rs[warp * 4 + j] = q4[j];
+    ract[warp] = wact ? 1 : 0;
+  }
+  named_bar_sync(1, K1_NWC * 32);
+  const int tid = threadIdx.x;
+  const int b = blockIdx.x;
+  if (tid == 0) {
+    double q[4] = {rs[0], rs[1], rs[2], rs[3]};
+    for (int wi = 1; wi < K1_NWC; ++wi)
+      for (int j = 0; j < 4; ++j) q[j] = p.fused ? __dadd_rn(q[j], rs[wi * 4 + j]) : fmax(q[j], rs[wi * 4 + j]);
+    for (int j = 0; j < 4; ++j) p.part_scal[b * 4 + j] = q[j];
+  }
+  // kernel-duration stamp: all consumer warps of this CTA are past their last write
+  auto stamp_end = [&]() {
+    if (p.tstamp) {
+      named_bar_sync(1, K1_NWC * 32);
+      if (tid == 0) atomicMax(p.tstamp + 1, global_ns());
+    }
+  };
+  if (!p.fused) {
+    if (tid == 0) p.cta_cnt[b] = 0;
+    stamp_end();
+    return;
+  }
+  int anyv = 0;
+  for (int wi = 0; wi < K1_NWC; ++wi) anyv |= ract[wi];
+  if (p.part_vec && anyv) {
+    for (int64_t k = tid; k < m; k += K1_NWC * 32) {
+      double v = 0.0;
+      for (int wi = 0; wi < K1_NWC; ++wi)
+        if (ract[wi]) v += rv[(size_t)wi * m + k];
+      p.part_vec[(size_t)b * m + k] = v;
+    }
+  }
+  if (!anyv) {
+    if (tid == 0) p.cta_cnt[b] = 0;
+    stamp_end();
+    return;
+  }
+  // ordered compaction: warp wi scans bytes [bw0, bw1) of this CTA's mask range
+  const int64_t byte_lo = c_lo >> 3, nbytes = (c_hi - c_lo + 7) >> 3;
+  const int64_t bw0 = byte_lo + nbytes * warp / K1_NWC, bw1 = byte_lo + nbytes * (warp + 1) / K1_NWC;
+  int cnt = 0;
+  for (int64_t q = bw0 + lane; q < bw1; q += 32) cnt += __popc((unsigned)p.mask[q]);
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  if (lane == 0) sh[warp] = cnt;
+  named_bar_sync(1, K1_NWC * 32);
+  int off = 0, tot = 0;
+  for (int wi = 0; wi < K1_NWC; ++wi) {
+    off += (wi < warp) ? sh[wi] : 0;
+    tot += sh[wi];
+  }
+  if (tid == 0) p.cta_cnt[b] = tot;
+  for (int64_t q0 = bw0; q0 < bw1; q0 += 32) {
+    const int64_t q = q0 + lane;
+    const unsigned byte = (q < bw1) ? (unsigned)p.mask[q] : 0u;
+    const int pc = __popc(byte);
+    int incl = pc;  // inclusive warp scan
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    int pos = off + incl - pc;
+    unsigned bb = byte;
+    while (bb) {
+      const int bit = __ffs(bb) - 1;
+      bb &= bb - 1;
+      const int64_t i = (q << 3) + bit;
+      const double w = p.w_out[i];
+      const double tt = __dsub_rn(p.x[i], __dmul_rn(sc.sigma, w));
+      p.seg_idx[c_lo + pos] = (int32_t)i;
+      p.seg_P[c_lo + pos] = prox_en(tt, sc.thr, sc.den);
+      ++pos;
+    }
+    off += __shfl_sync(0xffffffffu, incl, 31);
+  }
+  stamp_end();
 }
 
 template <int MR>
@@ -238,107 +345,244 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_aty_fused(const K1Params p) 
 
   // ---------------- CTA epilogue: fixed-order reductions, then ordered compaction ----------------
   named_bar_sync(1, K1_NWC * 32);  // ring idle; this CTA's w / mask writes are visible CTA-wide
-  double* rv = ring;                       // K1_NWC x m
-  double* rs = ring + (size_t)K1_NWC * m;  // K1_NWC x 4
-  int* ract = reinterpret_cast<int*>(rs + K1_NWC * 4);
-  // warp partial scalars: leader lanes 0,4,...,28 in lane order (plain mode: max over lanes)
-  double q4[4] = {s0, s1, s2, s3};
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    double acc = 0.0;
-    for (int l = 0; l < 32; l += 4) {
-      const double v = __shfl_sync(0xffffffffu, q4[j], l);
-      acc = p.fused ? __dadd_rn(acc, v) : fmax(acc, v);
-    }
-    if (!p.fused) acc = warp_allmax(q4[j]);
-    q4[j] = acc;
-  }
   if (p.fused && p.part_vec) {
 #pragma unroll
     for (int t = 0; t < MR; ++t) {
       const int64_t row = lane + 32 * t;
-      if (row < m) rv[(size_t)warp * m + row] = gacc[t];
+      if (row < m) ring[(size_t)warp * m + row] = gacc[t];
     }
   }
-  const bool wact = __any_sync(0xffffffffu, any_active);
-  if (lane == 0) {
-    for (int j = 0; j < 4; ++j) rs[warp * 4 + j] = q4[j];
-    ract[warp] = wact ? 1 : 0;
-  }
-  named_bar_sync(1, K1_NWC * 32);
-  const int tid = threadIdx.x;
-  const int b = blockIdx.x;
-  if (tid == 0) {
-    double q[4] = {rs[0], rs[1], rs[2], rs[3]};
-    for (int wi = 1; wi < K1_NWC; ++wi)
-      for (int j = 0; j < 4; ++j) q[j] = p.fused ? __dadd_rn(q[j], rs[wi * 4 + j]) : fmax(q[j], rs[wi * 4 + j]);
-    for (int j = 0; j < 4; ++j) p.part_scal[b * 4 + j] = q[j];
-  }
-  // kernel-duration stamp: all consumer warps of this CTA are past their last write
-  auto stamp_end = [&]() {
-    if (p.tstamp) {
-      named_bar_sync(1, K1_NWC * 32);
-      if (tid == 0) atomicMax(p.tstamp + 1, global_ns());
+  k1_cta_end(p, sc, ring, sh, c_lo, c_hi, s0, s1, s2, s3, any_active);
+}
+
+// acc += v when (word & bit) != 0 — a predicated add, no branch (K1g's inner loop)
+SSN_DEV void add_if_bit(double& acc, double v, uint32_t word, uint32_t bit) {
+  asm("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\tand.b32 t, %2, %3;\n\tsetp.ne.u32 p, t, 0;\n\t@p add.f64 %0, %0, %1;\n\t}"
+      : "+d"(acc)
+      : "d"(v), "r"(word), "r"(bit));
+}
+// x = v when (word & bit) != 0 — a predicated move
+SSN_DEV void sel_if_bit(double& x, double v, uint32_t word, uint32_t bit) {
+  asm("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\tand.b32 t, %2, %3;\n\tsetp.ne.u32 p, t, 0;\n\t@p mov.f64 %0, %1;\n\t}"
+      : "+d"(x)
+      : "d"(v), "r"(word), "r"(bit));
+}
+
+// ---------------------------------------------------------------------------
+// K1g: K1 over packed 2-bit genotype codes.  Column j is cstride bytes of
+// codes g ∈ {0,1,2} and a 3-entry table v_j[g] (the standardised value, bit-exact with the
+// fp64 design); a_kj = v_j[g_kj].  The A tile of a stage is C × cstride bytes of codes plus
+// C × 3 table doubles, streamed by the same 1D bulk-copy ring (32× fewer bytes than fp64).
+// Lane ℓ owns 32-bit words ℓ + 32t of every column (rows 16(ℓ + 32t) + 0..15, y in
+// registers).  Since a_kj takes three values per column, a_jᵀy = v0 ΣY + (v1−v0) S1 + (v2−v0) S2
+// with the bucket sums S_g = Σ_{k: g_kj = g} y_k: per element two bit-tested predicated adds.
+// The 8-column transpose-reduce, the epilogue and the CTA end are K1's.
+// ---------------------------------------------------------------------------
+template <int TW>
+__global__ void __launch_bounds__(K1_THREADS, 1) k1g_aty_fused(const K1Params p) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int S = p.stages, C = p.C;
+  const int64_t m = p.m, cs = p.cstride;
+  const int nwords = (int)(cs >> 2);
+  double* ring = reinterpret_cast<double*>(smem);  // per stage: codes (cs·C bytes) then table (3C doubles)
+  double* xring = ring + (size_t)S * p.stage_elems;
+  uint64_t* full = reinterpret_cast<uint64_t*>(xring + (size_t)S * p.xstage_elems);
+  uint64_t* empty = full + S;
+  int* sh = reinterpret_cast<int*>(empty + S);
+  volatile int* slot_seq = sh + 16;
+  const uint32_t code_elems = (uint32_t)((cs * C + 7) / 8);  // doubles occupied by a stage's codes
+
+  int64_t c_lo, c_hi;
+  cta_cols(blockIdx.x, gridDim.x, p.T, C, p.n, &c_lo, &c_hi);
+  const int64_t ntiles = (c_hi - c_lo + C - 1) / C;
+  if (threadIdx.x == 0) {
+    if (p.tstamp) atomicMin(p.tstamp, global_ns());
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+      slot_seq[s] = -1;
     }
-  };
-  if (!p.fused) {
-    if (tid == 0) p.cta_cnt[b] = 0;
-    stamp_end();
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == K1_NWC) {  // ---------------- producer warp ----------------
+    if (lane == 0) {
+      for (int64_t it = 0; it < ntiles; ++it) {
+        const int s = (int)(it % S);
+        if (it >= S) mbar_wait(&empty[s], (uint32_t)(((it / S) - 1) & 1));
+        const int64_t c0 = c_lo + it * C;
+        const int nc = (int)((c_hi - c0) < C ? (c_hi - c0) : C);
+        double* dst = ring + (size_t)s * p.stage_elems;
+        double* dT = dst + code_elems;
+        double* dX = xring + (size_t)s * p.xstage_elems;
+        const uint32_t bytesC = (uint32_t)(nc * cs);  // multiple of 16
+        const uint32_t bytesT = (uint32_t)nc * 24u, t16 = bytesT & ~15u;
+        if (t16 != bytesT) dT[3 * nc - 1] = __ldg(p.tab + (c0 + nc) * 3 - 1);  // 8-B tail
+        uint32_t x16 = 0;
+        if (p.fused) {
+          const uint32_t bytesX = (uint32_t)nc * 8u;
+          x16 = bytesX & ~15u;
+          if (x16 != bytesX) dX[nc - 1] = __ldg(p.x + c0 + nc - 1);
+        }
+        fence_proxy_async();
+        mbar_arrive_expect_tx(&full[s], bytesC + t16 + x16);
+        bulk_g2s(dst, p.codes + c0 * cs, bytesC, &full[s]);
+        if (t16) bulk_g2s(dT, p.tab + c0 * 3, t16, &full[s]);
+        if (x16) bulk_g2s(dX, p.x + c0, x16, &full[s]);
+        slot_seq[s] = (int)it;
+      }
+    }
     return;
   }
-  int anyv = 0;
-  for (int wi = 0; wi < K1_NWC; ++wi) anyv |= ract[wi];
-  if (p.part_vec && anyv) {
-    for (int64_t k = tid; k < m; k += K1_NWC * 32) {
-      double v = 0.0;
-      for (int wi = 0; wi < K1_NWC; ++wi)
-        if (ract[wi]) v += rv[(size_t)wi * m + k];
-      p.part_vec[(size_t)b * m + k] = v;
+
+  // ---------------- consumer warps ----------------
+  double yr[TW][16], gacc[TW][16];
+#pragma unroll
+  for (int t = 0; t < TW; ++t)
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int64_t row = 16 * (lane + 32 * t) + q;
+      yr[t][q] = row < m ? p.y[row] : 0.0;
+      gacc[t][q] = 0.0;
     }
-  }
-  if (!anyv) {
-    if (tid == 0) p.cta_cnt[b] = 0;
-    stamp_end();
-    return;
-  }
-  // ordered compaction: warp wi scans bytes [bw0, bw1) of this CTA's mask range
-  const int64_t byte_lo = c_lo >> 3, nbytes = (c_hi - c_lo + 7) >> 3;
-  const int64_t bw0 = byte_lo + nbytes * warp / K1_NWC, bw1 = byte_lo + nbytes * (warp + 1) / K1_NWC;
-  int cnt = 0;
-  for (int64_t q = bw0 + lane; q < bw1; q += 32) cnt += __popc((unsigned)p.mask[q]);
-  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-  if (lane == 0) sh[warp] = cnt;
-  named_bar_sync(1, K1_NWC * 32);
-  int off = 0, tot = 0;
-  for (int wi = 0; wi < K1_NWC; ++wi) {
-    off += (wi < warp) ? sh[wi] : 0;
-    tot += sh[wi];
-  }
-  if (tid == 0) p.cta_cnt[b] = tot;
-  for (int64_t q0 = bw0; q0 < bw1; q0 += 32) {
-    const int64_t q = q0 + lane;
-    const unsigned byte = (q < bw1) ? (unsigned)p.mask[q] : 0u;
-    const int pc = __popc(byte);
-    int incl = pc;  // inclusive warp scan
-    for (int o = 1; o < 32; o <<= 1) {
-      const int v = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += v;
+  double ysum = 0.0;  // Σ y over this lane's rows (the g = 0 bucket is ΣY − S1 − S2)
+#pragma unroll
+  for (int t = 0; t < TW; ++t)
+#pragma unroll
+    for (int q = 0; q < 16; ++q) ysum += yr[t][q];
+  const Scal sc = p.scp ? *p.scp : p.sc;
+  const bool leader = (lane & 3) == 0;
+  const int gcol = lane >> 2;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  bool any_active = false;
+
+  for (int64_t it = warp; it < ntiles; it += K1_NWC) {
+    const int s = (int)(it % S);
+    if (lane == 0)
+      while (slot_seq[s] != (int)it) __nanosleep(32);
+    __syncwarp();
+    mbar_wait(&full[s], (uint32_t)((it / S) & 1));
+    const int64_t c0 = c_lo + it * C;
+    const int nc = (int)((c_hi - c0) < C ? (c_hi - c0) : C);
+    const unsigned char* Cs = reinterpret_cast<const unsigned char*>(ring + (size_t)s * p.stage_elems);
+    const double* Ts = ring + (size_t)s * p.stage_elems + code_elems;
+    const double* Xs = xring + (size_t)s * p.xstage_elems;
+    for (int g = 0; g * K1_GRP < nc; ++g) {
+      // bucket sums S1 = Σ y [g = 1], S2 = Σ y [g = 2] over this lane's rows (code 3 is rejected at
+      // create, so g = 1 ⇔ bit 0 and g = 2 ⇔ bit 1): two bit-tested predicated adds per element
+      double b1[K1_GRP], b2[K1_GRP];
+#pragma unroll
+      for (int c = 0; c < K1_GRP; ++c) b1[c] = b2[c] = 0.0;
+#pragma unroll
+      for (int t = 0; t < TW; ++t) {
+        const int wi = lane + 32 * t;
+        uint32_t wd[K1_GRP];
+#pragma unroll
+        for (int c = 0; c < K1_GRP; ++c) {
+          const int cc = g * K1_GRP + c;
+          wd[c] = (cc < nc && wi < nwords) ? reinterpret_cast<const uint32_t*>(Cs + (size_t)cc * cs)[wi] : 0u;
+        }
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          const double yv = yr[t][q];
+#pragma unroll
+          for (int c = 0; c < K1_GRP; ++c) {
+            add_if_bit(b1[c], yv, wd[c], 1u << (2 * q));
+            add_if_bit(b2[c], yv, wd[c], 2u << (2 * q));
+          }
+        }
+      }
+      // lane partial of column c: v0 ΣY + (v1 − v0) S1 + (v2 − v0) S2
+      double a[K1_GRP];
+#pragma unroll
+      for (int c = 0; c < K1_GRP; ++c) {
+        const int cc = g * K1_GRP + c;
+        const bool cv = cc < nc;
+        const double v0 = cv ? Ts[3 * cc] : 0.0, v1 = cv ? Ts[3 * cc + 1] : 0.0, v2 = cv ? Ts[3 * cc + 2] : 0.0;
+        a[c] = fma(v2 - v0, b2[c], fma(v1 - v0, b1[c], v0 * ysum));
+      }
+      const double w = reduce8(a, lane);
+      const int c = g * K1_GRP + gcol;
+      const bool valid = c < nc;
+      if (p.fused) {
+        bool act = false;
+        double P = 0.0;
+        if (valid) {
+          const double xi = Xs[c];
+          const double tt = __dsub_rn(xi, __dmul_rn(sc.sigma, w));
+          act = fabs(tt) > sc.thr;
+          const double e = __dsub_rn(fabs(w), sc.l1);
+          if (xi == 0.0 && !act) {
+            if (leader) {
+              s2 = __dadd_rn(s2, __dmul_rn(w, w));
+              if (e > 0.0) s3 = __dadd_rn(s3, __dmul_rn(e, e));
+            }
+          } else {
+            P = prox_en(tt, sc.thr, sc.den);
+            const double dx = __dsub_rn(xi, P);
+            const double z = __dsub_rn(__ddiv_rn(dx, sc.sigma), w);
+            if (leader) {
+              s0 = __dadd_rn(s0, __dmul_rn(P, P));
+              s1 = __dadd_rn(s1, __dmul_rn(dx, dx));
+              s2 = __dadd_rn(s2, __dmul_rn(z, z));
+              if (e > 0.0) s3 = __dadd_rn(s3, __dmul_rn(e, e));
+            }
+          }
+          if (leader) p.w_out[c0 + c] = w;
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, act && leader);
+        unsigned m8 = 0;
+#pragma unroll
+        for (int q = 0; q < K1_GRP; ++q) m8 |= ((bal >> (4 * q)) & 1u) << q;
+        if (lane == 0) p.mask[(c0 >> 3) + g] = (uint8_t)m8;
+        if (m8) {
+          any_active = true;
+          unsigned mm = m8;
+          while (mm) {
+            const int q8 = __ffs(mm) - 1;
+            mm &= mm - 1;
+            const double Pq = __shfl_sync(0xffffffffu, P, 4 * q8);
+            const int cq = g * K1_GRP + q8;
+            const double v0 = Ts[3 * cq], v1 = Ts[3 * cq + 1], v2 = Ts[3 * cq + 2];
+            const uint32_t* wcol = reinterpret_cast<const uint32_t*>(Cs + (size_t)cq * cs);
+#pragma unroll
+            for (int t = 0; t < TW; ++t) {
+              const int wi = lane + 32 * t;
+              const uint32_t word = (wi < nwords) ? wcol[wi] : 0u;
+#pragma unroll
+              for (int q = 0; q < 16; ++q) {
+                double v = v0;
+                sel_if_bit(v, v1, word, 1u << (2 * q));
+                sel_if_bit(v, v2, word, 2u << (2 * q));
+                gacc[t][q] = fma(Pq, v, gacc[t][q]);
+              }
+            }
+          }
+        }
+      } else {
+        if (valid) {
+          s0 = fmax(s0, fabs(w));
+          if (leader) p.w_out[c0 + c] = w;
+        }
+      }
     }
-    int pos = off + incl - pc;
-    unsigned bb = byte;
-    while (bb) {
-      const int bit = __ffs(bb) - 1;
-      bb &= bb - 1;
-      const int64_t i = (q << 3) + bit;
-      const double w = p.w_out[i];
-      const double tt = __dsub_rn(p.x[i], __dmul_rn(sc.sigma, w));
-      p.seg_idx[c_lo + pos] = (int32_t)i;
-      p.seg_P[c_lo + pos] = prox_en(tt, sc.thr, sc.den);
-      ++pos;
-    }
-    off += __shfl_sync(0xffffffffu, incl, 31);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
   }
-  stamp_end();
+
+  named_bar_sync(1, K1_NWC * 32);  // ring idle
+  if (p.fused && p.part_vec) {
+#pragma unroll
+    for (int t = 0; t < TW; ++t)
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const int64_t row = 16 * (lane + 32 * t) + q;
+        if (row < m) ring[(size_t)warp * m + row] = gacc[t][q];
+      }
+  }
+  k1_cta_end(p, sc, ring, sh, c_lo, c_hi, s0, s1, s2, s3, any_active);
 }
 
 // ---------------------------------------------------------------------------

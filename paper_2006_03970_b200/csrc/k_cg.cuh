@@ -24,7 +24,6 @@ namespace ssn {
 constexpr int K6_THREADS = 256;
 
 struct CgParams {
-  const double* A;
   int64_t m;
   const int32_t* J;
   int64_t r;            // overridden by geo
@@ -54,8 +53,8 @@ SSN_DEV double block_sum(double v, double* red, int tid) {
   return s;
 }
 
-template <int MR>
-__global__ void __launch_bounds__(K6_THREADS, 1) k_cg_newton(const CgParams prm) {
+template <class Acc, int MR>
+__global__ void __launch_bounds__(K6_THREADS, 1) k_cg_newton(const CgParams prm, const Acc A) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   int64_t r = prm.r;
@@ -101,13 +100,13 @@ __global__ void __launch_bounds__(K6_THREADS, 1) k_cg_newton(const CgParams prm)
     }
     double tt = 0.0;
     for (int64_t a = a_lo + warp; a < a_hi; a += 8) {
-      const double* col = prm.A + (int64_t)prm.J[a] * m;
+      const int64_t col = prm.J[a];
       double cv[MR];
       double s = 0.0;
 #pragma unroll
       for (int t = 0; t < MR; ++t) {
         const int64_t row = lane + 32 * t;
-        cv[t] = row < m ? __ldg(col + row) : 0.0;
+        cv[t] = row < m ? A.ld(col, row) : 0.0;
         s = fma(cv[t], pr[t], s);
       }
       s = warp_allsum(s);  // t_a (bitwise identical in all lanes)

@@ -99,8 +99,8 @@ SSN_HD DirGeo make_geo(long long r, long long m, int nsm, int wsplits, double ka
 // ---------------------------------------------------------------------------
 // r is read from r_dev when r < 0 (device-resident count, fixed grid); valid[b] (nullable)
 // records whether CTA b had any column, so empty CTAs skip writing their partial row.
-template <int MR>
-__global__ void __launch_bounds__(256) k_gather_axpy(const double* __restrict__ A, int64_t m,
+template <class Acc, int MR>
+__global__ void __launch_bounds__(256) k_gather_axpy(const Acc A, int64_t m,
                                                      const int32_t* __restrict__ J, const double* __restrict__ coef,
                                                      int64_t r, const int64_t* __restrict__ r_dev,
                                                      double* __restrict__ part_vec, int* __restrict__ valid,
@@ -122,12 +122,12 @@ __global__ void __launch_bounds__(256) k_gather_axpy(const double* __restrict__ 
   for (int64_t base = a_lo; base < a_hi; base += stride) {
     const int64_t e_hi = devr ? min(base + 16, a_hi) : a_hi;
     for (int64_t a = base + warp; a < e_hi; a += 8) {
-      const double* col = A + (int64_t)J[a] * m;
+      const int64_t col = J[a];
       const double c = coef[a];
 #pragma unroll
       for (int t = 0; t < MR; ++t) {
         const int64_t row = lane + 32 * t;
-        if (row < m) acc[t] = fma(c, __ldg(col + row), acc[t]);
+        if (row < m) acc[t] = fma(c, A.ld(col, row), acc[t]);
       }
     }
     if (!devr) break;
@@ -147,8 +147,8 @@ __global__ void __launch_bounds__(256) k_gather_axpy(const double* __restrict__ 
 
 // Fused SMW back-substitution (Eq. (19)): partials of A_J v over `grid` CTAs, then the last CTA
 // (ticket) forms d = −g + Σ_b parts[b] (b ascending), gᵀd, and the Armijo trial y_t = y + d.
-template <int MR>
-__global__ void __launch_bounds__(256) k_smw_backsub(const double* __restrict__ A, int64_t m,
+template <class Acc, int MR>
+__global__ void __launch_bounds__(256) k_smw_backsub(const Acc A, int64_t m,
                                                      const int32_t* __restrict__ J, const double* __restrict__ v,
                                                      int64_t r, double* __restrict__ parts, const double* __restrict__ g,
                                                      const double* __restrict__ y, double* __restrict__ d,
@@ -169,12 +169,12 @@ __global__ void __launch_bounds__(256) k_smw_backsub(const double* __restrict__ 
 #pragma unroll
   for (int t = 0; t < MR; ++t) acc[t] = 0.0;
   for (int64_t a = a_lo + warp; a < a_hi; a += 8) {
-    const double* col = A + (int64_t)J[a] * m;
+    const int64_t col = J[a];
     const double c = v[a];
 #pragma unroll
     for (int t = 0; t < MR; ++t) {
       const int64_t row = lane + 32 * t;
-      if (row < m) acc[t] = fma(c, __ldg(col + row), acc[t]);
+      if (row < m) acc[t] = fma(c, A.ld(col, row), acc[t]);
     }
   }
 #pragma unroll
@@ -261,8 +261,8 @@ SSN_DEV void tri_tile(int q, int* ti, int* tj) {  // q → (ti ≥ tj), row-majo
 // the reduction index, double-buffers the next 32-slice in registers while computing the
 // current one from smem, and writes its partial tile to W[s]; a reduce kernel sums the slices
 // in order.  Graph mode: r, tiles, ns come from the device geometry (predicated on the branch).
-template <bool SMW>
-__global__ void __launch_bounds__(256) k_gram(const double* __restrict__ A, int64_t m,
+template <bool SMW, class Acc>
+__global__ void __launch_bounds__(256) k_gram(const Acc A, int64_t m,
                                               const int32_t* __restrict__ J, int64_t r, double* __restrict__ W,
                                               const double* __restrict__ gext, int tiles, int ns,
                                               const DirGeo* geo) {
@@ -285,14 +285,13 @@ __global__ void __launch_bounds__(256) k_gram(const double* __restrict__ A, int6
     const int64_t o0 = (int64_t)ti * 32, o1 = (int64_t)tj * 32;   // output tile origin
     const int64_t c_lo = nch * s / ns, c_hi = nch * (s + 1) / ns;  // chunk slice
     // element q of this thread in a 32 × 32 block: e = tid + 256 q → (γ = e >> 5, ρ = e & 31)
-    const double* colA[4];  // SMW: fixed column pointers for the a/b tiles (g for index r)
-    const double* colB[4];
+    int64_t colA[4], colB[4];  // SMW: column of A for the a/b tiles; −1: the extra column g; −2: none
     if (SMW) {
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int64_t ga = o0 + ty + 8 * q, gb = o1 + ty + 8 * q;
-        colA[q] = ga < r ? A + (int64_t)J[ga] * m : ((ga == r && gext) ? gext : nullptr);
-        colB[q] = gb < r ? A + (int64_t)J[gb] * m : ((gb == r && gext) ? gext : nullptr);
+        colA[q] = ga < r ? (int64_t)J[ga] : ((ga == r && gext) ? -1 : -2);
+        colB[q] = gb < r ? (int64_t)J[gb] : ((gb == r && gext) ? -1 : -2);
       }
     }
     double va[4], vb[4];
@@ -301,14 +300,14 @@ __global__ void __launch_bounds__(256) k_gram(const double* __restrict__ A, int6
       for (int q = 0; q < 4; ++q) {
         if (SMW) {
           const int64_t k = ch * 32 + tx;
-          va[q] = (colA[q] && k < m) ? __ldg(colA[q] + k) : 0.0;
-          vb[q] = (colB[q] && k < m) ? __ldg(colB[q] + k) : 0.0;
+          va[q] = (k < m && colA[q] >= 0) ? A.ld(colA[q], k) : ((k < m && colA[q] == -1) ? __ldg(gext + k) : 0.0);
+          vb[q] = (k < m && colB[q] >= 0) ? A.ld(colB[q], k) : ((k < m && colB[q] == -1) ? __ldg(gext + k) : 0.0);
         } else {
           const int64_t a = ch * 32 + ty + 8 * q;
           const bool ok = a < r;
-          const int64_t cb = ok ? (int64_t)J[a] * m : 0;
-          va[q] = (ok && o0 + tx < m) ? __ldg(A + cb + o0 + tx) : 0.0;
-          vb[q] = (ok && o1 + tx < m) ? __ldg(A + cb + o1 + tx) : 0.0;
+          const int64_t cb = ok ? (int64_t)J[a] : 0;
+          va[q] = (ok && o0 + tx < m) ? A.ld(cb, o0 + tx) : 0.0;
+          vb[q] = (ok && o1 + tx < m) ? A.ld(cb, o1 + tx) : 0.0;
         }
       }
     };
@@ -903,12 +902,13 @@ namespace ssn {
 // Appended rows for the degrees-of-freedom factorisation: rows [row0, row0+m) of M.
 //   ident = 0: C = A_J (M[row0 + k, a] = A[k, J_a], a < r)        (r < m)
 //   ident = 1: C = I_m (M[row0 + k, a] = δ_ka, a < m)              (r ≥ m)
-__global__ void k_fill_rows(double* __restrict__ M, int64_t ld, int64_t row0, const double* __restrict__ A,
+template <class Acc>
+__global__ void k_fill_rows(double* __restrict__ M, int64_t ld, int64_t row0, const Acc A,
                             int64_t m, const int32_t* __restrict__ J, int64_t ncol, int ident) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= m * ncol) return;
   const int64_t k = e % m, a = e / m;
-  M[row0 + k + a * ld] = ident ? (k == a ? 1.0 : 0.0) : A[(int64_t)J[a] * m + k];
+  M[row0 + k + a * ld] = ident ? (k == a ? 1.0 : 0.0) : A.ld(J[a], k);
 }
 
 // Deterministic Σ M[row0+i, j]² over i < nr, j < nc (single CTA, fixed per-thread order + tree).

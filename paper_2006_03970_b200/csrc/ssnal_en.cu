@@ -81,8 +81,6 @@ int mr_bucket(int64_t m) {
 }
 
 typedef void (*k1_fn)(const K1Params);
-typedef void (*gax_fn)(const double*, int64_t, const int32_t*, const double*, int64_t, const int64_t*, double*,
-                       int*, const int*);
 
 k1_fn k1_for(int mr) {
   switch (mr) {
@@ -95,40 +93,85 @@ k1_fn k1_for(int mr) {
     default: return k1_aty_fused<32>;
   }
 }
-typedef void (*bsub_fn)(const double*, int64_t, const int32_t*, const double*, int64_t, double*, const double*,
-                        const double*, double*, double*, double*, unsigned*, int, const DirGeo*);
-bsub_fn bsub_for(int mr) {
+k1_fn k1g_for(int tw) { return tw <= 1 ? k1g_aty_fused<1> : k1g_aty_fused<2>; }
+
+// Kernels that read individual columns are templated on the column accessor (AccA: fp64 design,
+// AccG: packed genotype codes, §8(f4)); these tables pick the register-tile variant.
+template <class Acc>
+using gax_fn = void (*)(const Acc, int64_t, const int32_t*, const double*, int64_t, const int64_t*, double*, int*,
+                        const int*);
+template <class Acc>
+gax_fn<Acc> gax_for(int mr) {
   switch (mr) {
-    case 1: return k_smw_backsub<1>;
-    case 2: return k_smw_backsub<2>;
-    case 4: return k_smw_backsub<4>;
-    case 8: return k_smw_backsub<8>;
-    case 16: return k_smw_backsub<16>;
-    case 25: return k_smw_backsub<25>;
-    default: return k_smw_backsub<32>;
+    case 1: return k_gather_axpy<Acc, 1>;
+    case 2: return k_gather_axpy<Acc, 2>;
+    case 4: return k_gather_axpy<Acc, 4>;
+    case 8: return k_gather_axpy<Acc, 8>;
+    case 16: return k_gather_axpy<Acc, 16>;
+    case 25: return k_gather_axpy<Acc, 25>;
+    default: return k_gather_axpy<Acc, 32>;
   }
 }
-typedef void (*cg_fn)(const CgParams);
-cg_fn cg_for(int mr) {
+template <class Acc>
+using bsub_fn = void (*)(const Acc, int64_t, const int32_t*, const double*, int64_t, double*, const double*,
+                         const double*, double*, double*, double*, unsigned*, int, const DirGeo*);
+template <class Acc>
+bsub_fn<Acc> bsub_for(int mr) {
   switch (mr) {
-    case 1: return k_cg_newton<1>;
-    case 2: return k_cg_newton<2>;
-    case 4: return k_cg_newton<4>;
-    case 8: return k_cg_newton<8>;
-    case 16: return k_cg_newton<16>;
-    case 25: return k_cg_newton<25>;
-    default: return k_cg_newton<32>;
+    case 1: return k_smw_backsub<Acc, 1>;
+    case 2: return k_smw_backsub<Acc, 2>;
+    case 4: return k_smw_backsub<Acc, 4>;
+    case 8: return k_smw_backsub<Acc, 8>;
+    case 16: return k_smw_backsub<Acc, 16>;
+    case 25: return k_smw_backsub<Acc, 25>;
+    default: return k_smw_backsub<Acc, 32>;
   }
 }
-gax_fn gax_for(int mr) {
+template <class Acc>
+using cg_fn = void (*)(const CgParams, const Acc);
+template <class Acc>
+cg_fn<Acc> cg_for(int mr) {
   switch (mr) {
-    case 1: return k_gather_axpy<1>;
-    case 2: return k_gather_axpy<2>;
-    case 4: return k_gather_axpy<4>;
-    case 8: return k_gather_axpy<8>;
-    case 16: return k_gather_axpy<16>;
-    case 25: return k_gather_axpy<25>;
-    default: return k_gather_axpy<32>;
+    case 1: return k_cg_newton<Acc, 1>;
+    case 2: return k_cg_newton<Acc, 2>;
+    case 4: return k_cg_newton<Acc, 4>;
+    case 8: return k_cg_newton<Acc, 8>;
+    case 16: return k_cg_newton<Acc, 16>;
+    case 25: return k_cg_newton<Acc, 25>;
+    default: return k_cg_newton<Acc, 32>;
+  }
+}
+
+// Packed genotype validation: one warp per column; flag[0] = codes of value 3 or non-finite
+// table entries, flag[1] = columns whose decoded entries are all zero.
+__global__ void k_validate_geno(const uint8_t* codes, int64_t cs, const double* tab, int64_t m, int64_t n,
+                                const double* b, int* flag) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const AccG acc{codes, cs, tab};
+  for (int64_t i = wid; i < n; i += nw) {
+    int bad = 0, nz = 0;
+    for (int64_t k = lane; k < m; k += 32) {
+      const unsigned g = (codes[i * cs + (k >> 2)] >> (2 * (int)(k & 3))) & 3u;
+      if (g == 3u) bad = 1;
+      const double v = acc.ld(i, k);
+      if (!isfinite(v)) bad = 1;
+      if (v != 0.0) nz = 1;
+    }
+    bad = __any_sync(0xffffffffu, bad);
+    nz = __any_sync(0xffffffffu, nz);
+    if (lane == 0) {
+      if (bad) atomicAdd(&flag[0], 1);
+      if (!nz) atomicAdd(&flag[1], 1);
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x < 32) {
+    int bad = 0;
+    for (int64_t k = threadIdx.x; k < m; k += 32)
+      if (!isfinite(b[k])) bad = 1;
+    bad = __any_sync(0xffffffffu, bad);
+    if (threadIdx.x == 0 && bad) atomicAdd(&flag[0], 1);
   }
 }
 
@@ -203,6 +246,14 @@ struct ssnal_en_problem {
   const double* A = nullptr;
   const double* b = nullptr;
   double* A_own = nullptr;
+  // packed genotype storage (§8(f4)); fmt = 1 when A is given as codes + tables
+  int fmt = 0;
+  const uint8_t* codes = nullptr;
+  const double* tab = nullptr;
+  int64_t cstride = 0;
+  uint8_t* codes_own = nullptr;
+  double* tab_own = nullptr;
+  int TW = 1;
   double* b_own = nullptr;
   cudaStream_t st = nullptr;
   // K1 configuration
@@ -302,12 +353,19 @@ int alloc(void** p, size_t bytes) {
 int configure(ssnal_en_problem* P) {
   const int64_t m = P->m, n = P->n;
   P->MR = mr_bucket(m);
-  const int64_t bytes_col = 8 * m;
+  // bytes of A per column in a K1 stage: fp64 (8m) or packed codes + table (cstride + 24)
+  const int64_t bytes_col = P->fmt ? P->cstride + 24 : 8 * m;
   int k = (int)(32768 / (K1_GRP * bytes_col));  // ~32 KB of A per tile
   if (k < 1) k = 1;
   if (k > 32) k = 32;  // ≤ 256 columns per tile
   P->C = K1_GRP * k;   // multiple of 8: one mask byte per 8 columns, 16-B aligned tiles
-  P->stage_elems = (uint32_t)(((int64_t)P->C * m + 15) / 16 * 16);
+  if (P->fmt) {
+    P->TW = (int)((P->cstride / 4 + 31) / 32);
+    const int64_t code_elems = (P->cstride * P->C + 7) / 8;  // = cstride·C/8 (cstride % 16 == 0)
+    P->stage_elems = (uint32_t)((code_elems + 3 * P->C + 15) / 16 * 16);
+  } else {
+    P->stage_elems = (uint32_t)(((int64_t)P->C * m + 15) / 16 * 16);
+  }
   P->xstage_elems = (uint32_t)((P->C + 15) / 16 * 16);
   const size_t per_stage = (size_t)(P->stage_elems + P->xstage_elems) * 8;
   int S = (int)((200 * 1024) / per_stage);
@@ -323,12 +381,21 @@ int configure(ssnal_en_problem* P) {
     set_err("K1 shared memory %zu exceeds 227 KB (m=%lld)", P->k1_smem, (long long)m);
     return SSNAL_EINVAL;
   }
-  CK(cudaFuncSetAttribute(k1_for(P->MR), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->k1_smem));
+  CK(cudaFuncSetAttribute(P->fmt ? k1g_for(P->TW) : k1_for(P->MR), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)P->k1_smem));
   const size_t gsm = (size_t)8 * m * 8;
-  CK(cudaFuncSetAttribute(gax_for(P->MR), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsm));
-  CK(cudaFuncSetAttribute(bsub_for(P->MR), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsm));
   P->cg_smem_bytes = cg_smem(m);
-  CK(cudaFuncSetAttribute(cg_for(P->MR), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->cg_smem_bytes));
+  if (P->fmt) {
+    CK(cudaFuncSetAttribute(gax_for<AccG>(P->MR), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsm));
+    CK(cudaFuncSetAttribute(bsub_for<AccG>(P->MR), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsm));
+    CK(cudaFuncSetAttribute(cg_for<AccG>(P->MR), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)P->cg_smem_bytes));
+  } else {
+    CK(cudaFuncSetAttribute(gax_for<AccA>(P->MR), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsm));
+    CK(cudaFuncSetAttribute(bsub_for<AccA>(P->MR), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsm));
+    CK(cudaFuncSetAttribute(cg_for<AccA>(P->MR), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)P->cg_smem_bytes));
+  }
   P->chol_smem = kCholSmem;
   CK(cudaFuncSetAttribute(k_chol_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->chol_smem));
   CK(cudaFuncSetAttribute(k_chol_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -405,6 +472,13 @@ int allocate(ssnal_en_problem* P) {
 
 // ---------------- launch wrappers ----------------
 
+// Calls f(acc) with the handle's column accessor (fp64 design or packed genotype codes).
+template <class F>
+int with_acc(ssnal_en_problem* P, F&& f) {
+  if (P->fmt) return f(AccG{P->codes, P->cstride, P->tab});
+  return f(AccA{P->A, P->m});
+}
+
 cudaEvent_t take_event(ssnal_en_problem* P) {
   if (!P->ev_pool.empty()) {
     cudaEvent_t e = P->ev_pool.back();
@@ -454,6 +528,9 @@ int launch_k1(ssnal_en_problem* P, const double* y, const double* x, const Scal&
   k.fused = fused;
   k.stage_elems = P->stage_elems;
   k.xstage_elems = P->xstage_elems;
+  k.codes = P->codes;
+  k.tab = P->tab;
+  k.cstride = P->cstride;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   const bool ev_time = P->time_k1 && !P->capturing;
   if (ev_time) {
@@ -461,7 +538,7 @@ int launch_k1(ssnal_en_problem* P, const double* y, const double* x, const Scal&
     e1 = take_event(P);
     cudaEventRecord(e0, P->st);
   }
-  k1_for(P->MR)<<<P->G, K1_THREADS, P->k1_smem, P->st>>>(k);
+  (P->fmt ? k1g_for(P->TW) : k1_for(P->MR))<<<P->G, K1_THREADS, P->k1_smem, P->st>>>(k);
   P->launches++;
   if (ev_time) {
     cudaEventRecord(e1, P->st);
@@ -507,8 +584,11 @@ int launch_gather(ssnal_en_problem* P, const int32_t* J, const double* coef, int
   int grid = (int)((r + 63) / 64);
   if (grid > P->gax_grid) grid = P->gax_grid;
   if (grid < 1) grid = 1;
-  gax_for(P->MR)<<<grid, 256, (size_t)8 * P->m * 8, P->st>>>(P->A, P->m, J, coef, r, nullptr, P->part_vec, nullptr,
-                                                                          nullptr);
+  with_acc(P, [&](auto acc) {
+    gax_for<decltype(acc)>(P->MR)<<<grid, 256, (size_t)8 * P->m * 8, P->st>>>(acc, P->m, J, coef, r, nullptr,
+                                                                               P->part_vec, nullptr, nullptr);
+    return 0;
+  });
   P->launches++;
   *grid_out = grid;
   CKL();
@@ -519,8 +599,11 @@ int launch_gather(ssnal_en_problem* P, const int32_t* J, const double* coef, int
 constexpr int kGatherDevGrid = 128;
 int launch_gather_dev(ssnal_en_problem* P, const int32_t* J, const double* coef, const int64_t* r_dev,
                       const int* pred = nullptr) {
-  gax_for(P->MR)<<<kGatherDevGrid, 256, (size_t)8 * P->m * 8, P->st>>>(P->A, P->m, J, coef, -1, r_dev, P->part_vec,
-                                                                       P->gax_valid, pred);
+  with_acc(P, [&](auto acc) {
+    gax_for<decltype(acc)>(P->MR)<<<kGatherDevGrid, 256, (size_t)8 * P->m * 8, P->st>>>(
+        acc, P->m, J, coef, -1, r_dev, P->part_vec, P->gax_valid, pred);
+    return 0;
+  });
   P->launches++;
   CKL();
   return SSNAL_OK;
@@ -618,7 +701,6 @@ int launch_chol(ssnal_en_problem* P, double* M, int N, double* out, double scale
 int launch_cg(ssnal_en_problem* P, const int32_t* J, int64_t r, const double* g, double kappa, double* d,
               double* gd_dev, const double* y, double* yt, const DirGeo* geo) {
   CgParams c;
-  c.A = P->A;
   c.m = P->m;
   c.J = J;
   c.r = r;
@@ -645,7 +727,10 @@ int launch_cg(ssnal_en_problem* P, const int32_t* J, int64_t r, const double* g,
   at[0].val.cooperative = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  CK(cudaLaunchKernelEx(&cfg, cg_for(P->MR), c));
+  cudaError_t e = (cudaError_t)with_acc(P, [&](auto acc) {
+    return (int)cudaLaunchKernelEx(&cfg, cg_for<decltype(acc)>(P->MR), c, acc);
+  });
+  CK(e);
   P->launches++;
   return SSNAL_OK;
 }
@@ -675,8 +760,11 @@ int newton_direction(ssnal_en_problem* P, const int32_t* J, int64_t r, const dou
   }
   CK(cudaMemsetAsync(P->info, 0, sizeof(int), P->st));
   if (geo.branch == 1) {  // Sherman–Morrison–Woodbury, Eq. (19): factor κ⁻¹I_r + A_JᵀA_J (R13)
-    k_gram<true><<<gram_grid(P, geo.tiles * geo.ns), 256, 0, P->st>>>(P->A, m, J, r, P->W, g, geo.tiles, geo.ns,
-                                                                      nullptr);
+    with_acc(P, [&](auto acc) {
+      k_gram<true><<<gram_grid(P, geo.tiles * geo.ns), 256, 0, P->st>>>(acc, m, J, r, P->W, g, geo.tiles, geo.ns,
+                                                                        nullptr);
+      return 0;
+    });
     P->launches++;
     CKL();
     k_gram_reduce<<<reduce_grid(P, geo.nout * geo.nout), 256, 0, P->st>>>(P->W, geo.ns, geo.nout, geo.nmat, geo.diag,
@@ -686,16 +774,21 @@ int newton_direction(ssnal_en_problem* P, const int32_t* J, int64_t r, const dou
     int rc = launch_chol(P, P->Mmat, geo.N, P->u, 1.0, nullptr, nullptr);  // v = (κ⁻¹I + G)⁻¹ u
     if (rc) return rc;
     // d = −g + A_J v, gᵀd, y_t = y + d (last-CTA finalisation)
-    bsub_for(P->MR)<<<geo.bgrid, 256, (size_t)8 * m * 8, P->st>>>(P->A, m, J, P->u, r, P->part_vec, g, y ? y : g, d,
-                                                                  yt ? yt : P->tmpm, gd_dev, P->ticket, geo.bgrid,
-                                                                  nullptr);
+    with_acc(P, [&](auto acc) {
+      bsub_for<decltype(acc)>(P->MR)<<<geo.bgrid, 256, (size_t)8 * m * 8, P->st>>>(
+          acc, m, J, P->u, r, P->part_vec, g, y ? y : g, d, yt ? yt : P->tmpm, gd_dev, P->ticket, geo.bgrid, nullptr);
+      return 0;
+    });
     P->launches++;
     CKL();
     return SSNAL_OK;
   }
   // r ≥ m: Eq. (18), M = I_m + κ A_J A_Jᵀ; the reduce also writes g into the rhs row
-  k_gram<false><<<gram_grid(P, geo.tiles * geo.ns), 256, 0, P->st>>>(P->A, m, J, r, P->W, nullptr, geo.tiles,
-                                                                     geo.ns, nullptr);
+  with_acc(P, [&](auto acc) {
+    k_gram<false><<<gram_grid(P, geo.tiles * geo.ns), 256, 0, P->st>>>(acc, m, J, r, P->W, nullptr, geo.tiles,
+                                                                       geo.ns, nullptr);
+    return 0;
+  });
   P->launches++;
   CKL();
   k_gram_reduce<<<reduce_grid(P, m * m), 256, 0, P->st>>>(P->W, geo.ns, m, m, geo.diag, geo.mult, P->Mmat, geo.ld, g,
@@ -715,15 +808,22 @@ int newton_direction_graph(ssnal_en_problem* P) {
   const double* g = P->g[0];
   double* gd = P->scratch;
   k_neg_copy<<<1, 1024, 0, P->st>>>(m, g, P->d, g, gd, P->y[0], P->y[1], geo);
-  k_gram<true><<<2 * P->nsm, 256, 0, P->st>>>(P->A, m, J, 0, P->W, g, 0, 0, geo);
+  with_acc(P, [&](auto acc) {
+    k_gram<true><<<2 * P->nsm, 256, 0, P->st>>>(acc, m, J, 0, P->W, g, 0, 0, geo);
+    return 0;
+  });
   k_gram_reduce<<<reduce_grid(P, m * m), 256, 0, P->st>>>(P->W, 0, 0, 0, 0.0, 0.0, P->Mmat, 0, nullptr, geo, 1);
   P->launches += 3;
   CKL();
   int rc = launch_chol(P, P->Mmat, 0, P->u, 1.0, nullptr, nullptr, nullptr, nullptr, geo, 1);
   if (rc) return rc;
-  bsub_for(P->MR)<<<P->nsm, 256, (size_t)8 * m * 8, P->st>>>(P->A, m, J, P->u, 0, P->part_vec, g, P->y[0], P->d,
-                                                             P->y[1], gd, P->ticket, 0, geo);
-  k_gram<false><<<2 * P->nsm, 256, 0, P->st>>>(P->A, m, J, 0, P->W, nullptr, 0, 0, geo);
+  with_acc(P, [&](auto acc) {
+    bsub_for<decltype(acc)>(P->MR)<<<P->nsm, 256, (size_t)8 * m * 8, P->st>>>(acc, m, J, P->u, 0, P->part_vec, g,
+                                                                               P->y[0], P->d, P->y[1], gd, P->ticket,
+                                                                               0, geo);
+    k_gram<false><<<2 * P->nsm, 256, 0, P->st>>>(acc, m, J, 0, P->W, nullptr, 0, 0, geo);
+    return 0;
+  });
   k_gram_reduce<<<reduce_grid(P, m * m), 256, 0, P->st>>>(P->W, 0, 0, 0, 0.0, 0.0, P->Mmat, 0, g, geo, 2);
   P->launches += 3;
   CKL();
@@ -1220,14 +1320,18 @@ static int create_common(ssnal_en_problem* P) {
   if (rc) return rc;
   // validate inputs on the device
   CK(cudaMemsetAsync(P->flags, 0, 8, P->st));
-  k_validate<<<4 * P->nsm, 256, 0, P->st>>>(P->A, P->m, P->n, P->b, P->flags);
+  if (P->fmt)
+    k_validate_geno<<<4 * P->nsm, 256, 0, P->st>>>(P->codes, P->cstride, P->tab, P->m, P->n, P->b, P->flags);
+  else
+    k_validate<<<4 * P->nsm, 256, 0, P->st>>>(P->A, P->m, P->n, P->b, P->flags);
   CKL();
   int hf[2] = {0, 0};
   CK(cudaMemcpyAsync(P->scratch_host, P->flags, 8, cudaMemcpyDeviceToHost, P->st));
   CK(cudaStreamSynchronize(P->st));
   memcpy(hf, P->scratch_host, 8);
   if (hf[0]) {
-    set_err("A or b contains NaN/Inf (%d columns)", hf[0]);
+    set_err(P->fmt ? "invalid genotype codes / table or non-finite b (%d columns)" : "A or b contains NaN/Inf (%d columns)",
+            hf[0]);
     return SSNAL_EINVAL;
   }
   if (hf[1]) {
@@ -1303,6 +1407,8 @@ static void destroy_bufs(ssnal_en_problem* P) {
     cudaEventDestroy(pr.second);
   }
   cudaFree(P->A_own);
+  cudaFree(P->codes_own);
+  cudaFree(P->tab_own);
   cudaFree(P->b_own);
 }
 
@@ -1381,6 +1487,94 @@ int ssnal_en_create_device(const double* dA, const double* db, int64_t m, int64_
   return SSNAL_OK;
 }
 
+static int geno_common(ssnal_en_problem* P, int64_t stride) {
+  if (stride < (P->m + 3) / 4 || stride % 16 != 0) {
+    set_err("genotype stride %lld must be a multiple of 16 and >= ceil(m/4)", (long long)stride);
+    return SSNAL_EINVAL;
+  }
+  P->fmt = 1;
+  P->cstride = stride;
+  return SSNAL_OK;
+}
+
+int ssnal_en_create_geno_device(const uint8_t* codes, int64_t stride, const double* tab, const double* db, int64_t m,
+                                int64_t n, void* cuda_stream, ssnal_en_problem** out) {
+  if (!out || !codes || !tab || !db) {
+    set_err("null argument");
+    return SSNAL_EINVAL;
+  }
+  *out = nullptr;
+  int rc = check_dims(m, n);
+  if (rc) return rc;
+  if (((uintptr_t)codes & 15) != 0 || ((uintptr_t)tab & 15) != 0) {
+    set_err("codes and tab must be 16-byte aligned");
+    return SSNAL_EINVAL;
+  }
+  ssnal_en_problem* P = new ssnal_en_problem();
+  P->m = m;
+  P->n = n;
+  P->codes = codes;
+  P->tab = tab;
+  P->b = db;
+  P->st = (cudaStream_t)cuda_stream;
+  rc = geno_common(P, stride);
+  if (!rc) rc = create_common(P);
+  if (rc) {
+    destroy_bufs(P);
+    delete P;
+    return rc;
+  }
+  *out = P;
+  return SSNAL_OK;
+}
+
+int ssnal_en_create_geno(const uint8_t* codes, int64_t stride, const double* tab, const double* b, int64_t m,
+                         int64_t n, ssnal_en_problem** out) {
+  if (!out || !codes || !tab || !b) {
+    set_err("null argument");
+    return SSNAL_EINVAL;
+  }
+  *out = nullptr;
+  int rc = check_dims(m, n);
+  if (rc) return rc;
+  ssnal_en_problem* P = new ssnal_en_problem();
+  P->m = m;
+  P->n = n;
+  rc = geno_common(P, stride);
+  if (rc) {
+    delete P;
+    return rc;
+  }
+  if (cudaMalloc((void**)&P->codes_own, (size_t)n * stride + 64) != cudaSuccess ||
+      cudaMalloc((void**)&P->tab_own, (size_t)n * 3 * 8 + 64) != cudaSuccess ||
+      cudaMalloc((void**)&P->b_own, (size_t)m * 8 + 64) != cudaSuccess) {
+    set_err("cudaMalloc for genotype codes failed");
+    destroy_bufs(P);
+    delete P;
+    return SSNAL_ECUDA;
+  }
+  if (cudaMemcpy(P->codes_own, codes, (size_t)n * stride, cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemcpy(P->tab_own, tab, (size_t)n * 3 * 8, cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemcpy(P->b_own, b, (size_t)m * 8, cudaMemcpyHostToDevice) != cudaSuccess) {
+    set_err("H2D copy failed");
+    destroy_bufs(P);
+    delete P;
+    return SSNAL_ECUDA;
+  }
+  P->codes = P->codes_own;
+  P->tab = P->tab_own;
+  P->b = P->b_own;
+  P->st = nullptr;
+  rc = create_common(P);
+  if (rc) {
+    destroy_bufs(P);
+    delete P;
+    return rc;
+  }
+  *out = P;
+  return SSNAL_OK;
+}
+
 double ssnal_en_lambda_max_l1(const ssnal_en_problem* p) { return p ? p->lambda_max : NAN; }
 
 int ssnal_en_set_option(ssnal_en_problem* P, const char* key, double v) {
@@ -1425,6 +1619,7 @@ double ssnal_en_get_info(const ssnal_en_problem* P, const char* key) {
   if (k == "cluster_size") return P->cluster;
   if (k == "num_sms") return P->nsm;
   if (k == "graph") return P->use_graph;
+  if (k == "format") return P->fmt;
   if (k == "cg_ratio") return P->cg_ratio;
   if (k == "cg_threshold") return P->cg_threshold;
   return NAN;
@@ -1580,9 +1775,15 @@ int ssnal_en_model_select(ssnal_en_problem* P, double l2, double* xdb_out, ssnal
     // ν: factor A_JᵀA_J + λ2 I with A_J appended as m rows: ν = ‖A_J L⁻ᵀ‖_F²
     const int N = (int)r, NR = (int)(r + m);
     const int nt = (N + 31) / 32, tiles = nt * (nt + 1) / 2, ns = splits(tiles, m);
-    k_gram<true><<<gram_grid(P, tiles * ns), 256, 0, P->st>>>(P->A, m, J, r, P->W, nullptr, tiles, ns, nullptr);
+    with_acc(P, [&](auto acc) {
+      k_gram<true><<<gram_grid(P, tiles * ns), 256, 0, P->st>>>(acc, m, J, r, P->W, nullptr, tiles, ns, nullptr);
+      return 0;
+    });
     k_gram_reduce<<<reduce_grid(P, r * r), 256, 0, P->st>>>(P->W, ns, r, r, l2, 1.0, P->Msel, NR, nullptr, nullptr, 0);
-    k_fill_rows<<<(unsigned)((m * r + 255) / 256), 256, 0, P->st>>>(P->Msel, NR, r, P->A, m, J, r, 0);
+    with_acc(P, [&](auto acc) {
+      k_fill_rows<<<(unsigned)((m * r + 255) / 256), 256, 0, P->st>>>(P->Msel, NR, r, acc, m, J, r, 0);
+      return 0;
+    });
     P->launches += 3;
     CKL();
     if ((rc = launch_chol_ex(P, P->Msel, N, NR, NR, nullptr, 1.0, nullptr, nullptr, nullptr, nullptr, info_nu)))
@@ -1591,7 +1792,10 @@ int ssnal_en_model_select(ssnal_en_problem* P, double l2, double* xdb_out, ssnal
     // OLS de-biasing: factor A_JᵀA_J with rhs row A_Jᵀb; v → P->u
     const int64_t nout = r + 1;
     const int nt2 = (int)((nout + 31) / 32), tiles2 = nt2 * (nt2 + 1) / 2, ns2 = splits(tiles2, m);
-    k_gram<true><<<gram_grid(P, tiles2 * ns2), 256, 0, P->st>>>(P->A, m, J, r, P->W, P->b, tiles2, ns2, nullptr);
+    with_acc(P, [&](auto acc) {
+      k_gram<true><<<gram_grid(P, tiles2 * ns2), 256, 0, P->st>>>(acc, m, J, r, P->W, P->b, tiles2, ns2, nullptr);
+      return 0;
+    });
     k_gram_reduce<<<reduce_grid(P, nout * nout), 256, 0, P->st>>>(P->W, ns2, nout, r, 0.0, 1.0, P->Mmat, N + 1, nullptr,
                                                                   nullptr, 0);
     P->launches += 3;
@@ -1609,9 +1813,15 @@ int ssnal_en_model_select(ssnal_en_problem* P, double l2, double* xdb_out, ssnal
     // r ≥ m: ν = tr(K (K + λ2 I)⁻¹), K = A_J A_Jᵀ, = m − λ2 ‖L⁻¹‖_F² with I_m appended
     const int N = (int)m, NR = (int)(2 * m);
     const int nt = (int)((m + 31) / 32), tiles = nt * (nt + 1) / 2, ns = splits(tiles, r);
-    k_gram<false><<<gram_grid(P, tiles * ns), 256, 0, P->st>>>(P->A, m, J, r, P->W, nullptr, tiles, ns, nullptr);
+    with_acc(P, [&](auto acc) {
+      k_gram<false><<<gram_grid(P, tiles * ns), 256, 0, P->st>>>(acc, m, J, r, P->W, nullptr, tiles, ns, nullptr);
+      return 0;
+    });
     k_gram_reduce<<<reduce_grid(P, m * m), 256, 0, P->st>>>(P->W, ns, m, m, l2, 1.0, P->Msel, NR, nullptr, nullptr, 0);
-    k_fill_rows<<<(unsigned)((m * m + 255) / 256), 256, 0, P->st>>>(P->Msel, NR, m, P->A, m, J, m, 1);
+    with_acc(P, [&](auto acc) {
+      k_fill_rows<<<(unsigned)((m * m + 255) / 256), 256, 0, P->st>>>(P->Msel, NR, m, acc, m, J, m, 1);
+      return 0;
+    });
     P->launches += 3;
     CKL();
     if ((rc = launch_chol_ex(P, P->Msel, N, NR, NR, nullptr, 1.0, nullptr, nullptr, nullptr, nullptr, info_nu)))

@@ -69,6 +69,8 @@ def load_library():
         P = ctypes.POINTER
         L.ssnal_en_create.argtypes = [_dp, _dp, _i64, _i64, P(_vp)]
         L.ssnal_en_create_device.argtypes = [_vp, _vp, _i64, _i64, _vp, P(_vp)]
+        L.ssnal_en_create_geno.argtypes = [_vp, _i64, _dp, _dp, _i64, _i64, P(_vp)]
+        L.ssnal_en_create_geno_device.argtypes = [_vp, _i64, _vp, _vp, _i64, _i64, _vp, P(_vp)]
         L.ssnal_en_lambda_max_l1.argtypes = [_vp]
         L.ssnal_en_lambda_max_l1.restype = _d
         L.ssnal_en_set_option.argtypes = [_vp, ctypes.c_char_p, _d]
@@ -85,7 +87,7 @@ def load_library():
         L.ssnal_en_destroy.restype = None
         L.ssnal_en_last_error.restype = ctypes.c_char_p
         L.ssnal_en_version.restype = ctypes.c_char_p
-        for f in ("create", "create_device", "set_option", "solve", "solve_device", "aty_fused", "epilogue",
+        for f in ("create", "create_device", "create_geno", "create_geno_device", "set_option", "solve", "solve_device", "aty_fused", "epilogue",
                   "newton_direction"):
             getattr(L, "ssnal_en_" + f).restype = ctypes.c_int
         _lib = L
@@ -108,6 +110,8 @@ class Problem:
 
     Problem(A, b)                          host arrays; A is (n, m) C-contiguous = column-major m x n
     Problem.from_device(dA, db, m, n, s)   device pointers (borrowed), s = cudaStream_t as int
+    Problem.from_geno(codes, tab, b)       packed 2-bit genotype codes (n, stride) uint8 + tables (n, 3)
+    Problem.from_geno_device(dcodes, stride, dtab, db, m, n, s)   the same, device pointers (borrowed)
     """
 
     def __init__(self, A=None, b=None, _handle=None, _keep=None):
@@ -130,6 +134,27 @@ class Problem:
         lib = load_library()
         h = _vp()
         _check(lib.ssnal_en_create_device(_vp(dA), _vp(db), m, n, _vp(stream), ctypes.byref(h)))
+        return cls(_handle=h, _keep=keep)
+
+    @classmethod
+    def from_geno(cls, codes, tab, b):
+        """Compressed genotype storage (SURVEY §8(f4)): a_kj = tab[j, (codes[j, k//4] >> 2(k%4)) & 3]."""
+        lib = load_library()
+        codes = np.ascontiguousarray(codes, dtype=np.uint8)
+        tab, tp = _f64(tab)
+        b, bp = _f64(b)
+        n, stride = codes.shape
+        h = _vp()
+        _check(lib.ssnal_en_create_geno(_vp(codes.ctypes.data), stride, tp, bp, len(b), n, ctypes.byref(h)))
+        return cls(_handle=h)
+
+    @classmethod
+    def from_geno_device(cls, dcodes: int, stride: int, dtab: int, db: int, m: int, n: int, stream: int = 0,
+                         keep=None):
+        lib = load_library()
+        h = _vp()
+        _check(lib.ssnal_en_create_geno_device(_vp(dcodes), stride, _vp(dtab), _vp(db), m, n, _vp(stream),
+                                               ctypes.byref(h)))
         return cls(_handle=h, _keep=keep)
 
     # -- introspection / options --

@@ -91,6 +91,8 @@ def host_lib():
         lib.synth_normals.restype = None
         lib.synth_uniforms.argtypes = [u64, u64, i64, dp]
         lib.synth_uniforms.restype = None
+        lib.synth_geno_codes.argtypes = [u64, i64, i64, i64, i64, ctypes.c_void_p, i64, dp]
+        lib.synth_geno_codes.restype = ctypes.c_int
         _host = lib
     return _host
 
@@ -104,6 +106,10 @@ def dev_lib():
         lib.synth_fill_A_device.argtypes = [ctypes.c_int, ctypes.c_uint64, ctypes.c_int64, ctypes.c_int64,
                                             ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]
         lib.synth_fill_A_device.restype = ctypes.c_int
+        lib.synth_geno_codes_device.argtypes = [ctypes.c_uint64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                                                ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
+                                                ctypes.c_void_p]
+        lib.synth_geno_codes_device.restype = ctypes.c_int
         _dev = lib
     return _dev
 
@@ -177,3 +183,38 @@ def fill_device(cfg: Config, dptr: int, stream: int = 0, j0: int = 0, j1: int | 
                                        ctypes.c_void_p(stream))
     if rc != 0:
         raise RuntimeError(f"synth_fill_A_device returned {rc}")
+
+
+def geno_stride(m: int) -> int:
+    """Bytes per packed genotype column: ceil(m/4) rounded up to 16 (TMA-aligned tiles)."""
+    return ((m + 3) // 4 + 15) // 16 * 16
+
+
+def geno_codes(cfg: Config, j0: int = 0, j1: int | None = None):
+    """Compressed storage of a GENO_STD design: (codes uint8 (ncols, stride), tab (ncols, 3)).
+    decode_geno(codes, tab, m) equals design(cfg) bit for bit."""
+    assert cfg.kind == GENO_STD
+    j1 = cfg.n if j1 is None else j1
+    stride = geno_stride(cfg.m)
+    codes = np.empty((j1 - j0, stride), dtype=np.uint8)
+    tab = np.empty((j1 - j0, 3), dtype=np.float64)
+    rc = host_lib().synth_geno_codes(cfg.seed, cfg.m, cfg.n, j0, j1, codes.ctypes.data, stride, _dp(tab))
+    if rc < 0:
+        raise RuntimeError(f"synth_geno_codes returned {rc}")
+    return codes, tab
+
+
+def decode_geno(codes: np.ndarray, tab: np.ndarray, m: int) -> np.ndarray:
+    """(ncols, m) fp64 design from packed codes: entry (j, k) = tab[j, (codes[j, k//4] >> 2(k%4)) & 3]."""
+    k = np.arange(m)
+    g = (codes[:, k // 4] >> (2 * (k % 4))) & 3
+    return np.take_along_axis(tab, g.astype(np.int64), axis=1)
+
+
+def fill_device_geno(cfg: Config, dcodes: int, dtab: int, stream: int = 0, j0: int = 0, j1: int | None = None):
+    """Device twin of geno_codes: packed codes (stride geno_stride(m)) and tables into device memory."""
+    j1 = cfg.n if j1 is None else j1
+    rc = dev_lib().synth_geno_codes_device(cfg.seed, cfg.m, cfg.n, j0, j1, ctypes.c_void_p(dcodes),
+                                           geno_stride(cfg.m), ctypes.c_void_p(dtab), ctypes.c_void_p(stream))
+    if rc < 0:
+        raise RuntimeError(f"synth_geno_codes_device returned {rc}")

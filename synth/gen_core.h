@@ -241,4 +241,32 @@ SX_HD int sx_standardise(double* col, int64_t m, int unit_l2) {
   return 1;
 }
 
+/* ---- compressed genotype storage ------------------------------
+ * Column j of a SX_GENO_STD design as 2-bit codes g ∈ {0,1,2}, four rows per byte
+ * (row k in bits 2(k%4)..2(k%4)+1 of byte k/4), plus the 3-entry table
+ * v[g] = (g − mean_j) / nrm_j computed with sx_standardise's exact operations, so that
+ * v[code(k, j)] equals the standardised fp64 design entry bit for bit (zero-variance
+ * column: v[g] = g − mean_j, as the generator writes it).  `codes` has `stride` bytes
+ * (≥ ceil(m/4), padding zero).  Returns 1, or 0 for a zero-variance column. */
+SX_HD int sx_geno_packed(uint64_t seed, int64_t m, int64_t n, int64_t j, uint8_t* codes, int64_t stride,
+                         double* v) {
+  for (int64_t q = 0; q < stride; ++q) codes[q] = 0;
+  double s = 0.0;
+  for (int64_t k = 0; k < m; ++k) {
+    const double g = sx_geno_entry(seed, m, n, k, j);
+    codes[k >> 2] = (uint8_t)(codes[k >> 2] | ((int)g << (2 * (int)(k & 3))));
+    s = SX_ADD(s, g);
+  }
+  const double mean = SX_DIV(s, (double)m);
+  double ss = 0.0;
+  for (int64_t k = 0; k < m; ++k) {
+    const double c = SX_SUB((double)((codes[k >> 2] >> (2 * (int)(k & 3))) & 3), mean);
+    ss = SX_ADD(ss, SX_MUL(c, c));
+  }
+  const int ok = ss > 0.0;
+  const double nrm = SX_SQRT(SX_DIV(ss, (double)m));
+  for (int g = 0; g < 3; ++g) v[g] = ok ? SX_DIV(SX_SUB((double)g, mean), nrm) : SX_SUB((double)g, mean);
+  return ok;
+}
+
 #endif /* SYNTH_GEN_CORE_H */

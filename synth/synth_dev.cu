@@ -60,6 +60,14 @@ __global__ void k_standardise(int64_t m, int64_t ncols, double* out, int* bad) {
   if (!sx_standardise(out + j * m, m, 0)) atomicAdd(bad, 1);
 }
 
+/* Packed genotype codes, one thread per column (gen_core.h sx_geno_packed). */
+__global__ void k_gen_geno_packed(uint64_t seed, int64_t m, int64_t n, int64_t j0, int64_t j1, uint8_t* codes,
+                                  int64_t stride, double* tab, int* bad) {
+  int64_t j = j0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= j1) return;
+  if (!sx_geno_packed(seed, m, n, j, codes + (j - j0) * stride, stride, tab + (j - j0) * 3)) atomicAdd(bad, 1);
+}
+
 extern "C" {
 
 /* Same contract as synth_fill_A (host) but out is a device pointer.
@@ -88,6 +96,25 @@ int synth_fill_A_device(int kind, uint64_t seed, int64_t m, int64_t n, int64_t j
     }
     default: cudaFreeAsync(dbad, st); return -1;
   }
+  int hbad = 0;
+  cudaMemcpyAsync(&hbad, dbad, sizeof(int), cudaMemcpyDeviceToHost, st);
+  cudaFreeAsync(dbad, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess) return -2;
+  if (cudaGetLastError() != cudaSuccess) return -2;
+  return hbad;
+}
+
+/* Device twin of synth_geno_codes (codes, tab are device pointers). */
+int synth_geno_codes_device(uint64_t seed, int64_t m, int64_t n, int64_t j0, int64_t j1, uint8_t* codes,
+                            int64_t stride, double* tab, void* stream) {
+  if (m < 1 || n < 1 || j0 < 0 || j1 > n || j0 > j1 || stride < (m + 3) / 4) return -1;
+  if (j1 == j0) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  int* dbad = nullptr;
+  if (cudaMallocAsync((void**)&dbad, sizeof(int), st) != cudaSuccess) return -2;
+  cudaMemsetAsync(dbad, 0, sizeof(int), st);
+  const int T = 128;
+  k_gen_geno_packed<<<(unsigned)((j1 - j0 + T - 1) / T), T, 0, st>>>(seed, m, n, j0, j1, codes, stride, tab, dbad);
   int hbad = 0;
   cudaMemcpyAsync(&hbad, dbad, sizeof(int), cudaMemcpyDeviceToHost, st);
   cudaFreeAsync(dbad, st);

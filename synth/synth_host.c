@@ -132,3 +132,16 @@ void synth_uniforms(uint64_t seed, uint64_t sub, int64_t count, double* out) {
 #pragma omp parallel for schedule(static)
   for (int64_t i = 0; i < count; ++i) out[i] = sx_u01(key, (uint64_t)i);
 }
+
+/* Packed 2-bit genotype codes of columns [j0, j1) of a SX_GENO_STD design (gen_core.h
+ * sx_geno_packed): codes ((j1-j0) × stride bytes), tab ((j1-j0) × 3 doubles).
+ * Returns 0, the number of zero-variance columns, or -1 for bad arguments. */
+int synth_geno_codes(uint64_t seed, int64_t m, int64_t n, int64_t j0, int64_t j1, uint8_t* codes, int64_t stride,
+                     double* tab) {
+  if (m < 1 || n < 1 || j0 < 0 || j1 > n || j0 > j1 || stride < (m + 3) / 4) return -1;
+  int64_t bad = 0;
+#pragma omp parallel for schedule(static) reduction(+ : bad)
+  for (int64_t j = j0; j < j1; ++j)
+    if (!sx_geno_packed(seed, m, n, j, codes + (j - j0) * stride, stride, tab + (j - j0) * 3)) bad++;
+  return (int)bad;
+}
