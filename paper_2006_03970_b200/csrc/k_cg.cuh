@@ -100,13 +100,13 @@ __global__ void __launch_bounds__(K6_THREADS, 1) k_cg_newton(const CgParams prm,
     }
     double tt = 0.0;
     for (int64_t a = a_lo + warp; a < a_hi; a += 8) {
-      const int64_t col = prm.J[a];
+      const auto col = A.col(prm.J[a]);
       double cv[MR];
       double s = 0.0;
 #pragma unroll
       for (int t = 0; t < MR; ++t) {
         const int64_t row = lane + 32 * t;
-        cv[t] = row < m ? A.ld(col, row) : 0.0;
+        cv[t] = row < m ? col.ld(row) : 0.0;
         s = fma(cv[t], pr[t], s);
       }
       s = warp_allsum(s);  // t_a (bitwise identical in all lanes)

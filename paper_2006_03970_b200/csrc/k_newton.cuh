@@ -13,6 +13,7 @@
 //                        as an extra matrix row and a block backward solve (one launch)
 #pragma once
 #include <cooperative_groups.h>
+#include <type_traits>
 #include "common.cuh"
 
 namespace ssn {
@@ -122,12 +123,12 @@ __global__ void __launch_bounds__(256) k_gather_axpy(const Acc A, int64_t m,
   for (int64_t base = a_lo; base < a_hi; base += stride) {
     const int64_t e_hi = devr ? min(base + 16, a_hi) : a_hi;
     for (int64_t a = base + warp; a < e_hi; a += 8) {
-      const int64_t col = J[a];
+      const auto col = A.col(J[a]);
       const double c = coef[a];
 #pragma unroll
       for (int t = 0; t < MR; ++t) {
         const int64_t row = lane + 32 * t;
-        if (row < m) acc[t] = fma(c, A.ld(col, row), acc[t]);
+        if (row < m) acc[t] = fma(c, col.ld(row), acc[t]);
       }
     }
     if (!devr) break;
@@ -169,12 +170,12 @@ __global__ void __launch_bounds__(256) k_smw_backsub(const Acc A, int64_t m,
 #pragma unroll
   for (int t = 0; t < MR; ++t) acc[t] = 0.0;
   for (int64_t a = a_lo + warp; a < a_hi; a += 8) {
-    const int64_t col = J[a];
+    const auto col = A.col(J[a]);
     const double c = v[a];
 #pragma unroll
     for (int t = 0; t < MR; ++t) {
       const int64_t row = lane + 32 * t;
-      if (row < m) acc[t] = fma(c, A.ld(col, row), acc[t]);
+      if (row < m) acc[t] = fma(c, col.ld(row), acc[t]);
     }
   }
 #pragma unroll
@@ -286,12 +287,18 @@ __global__ void __launch_bounds__(256) k_gram(const Acc A, int64_t m,
     const int64_t c_lo = nch * s / ns, c_hi = nch * (s + 1) / ns;  // chunk slice
     // element q of this thread in a 32 × 32 block: e = tid + 256 q → (γ = e >> 5, ρ = e & 31)
     int64_t colA[4], colB[4];  // SMW: column of A for the a/b tiles; −1: the extra column g; −2: none
+    const double* pA[4];       // fp64 design: the column pointers themselves (g for index r)
+    const double* pB[4];
     if (SMW) {
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int64_t ga = o0 + ty + 8 * q, gb = o1 + ty + 8 * q;
         colA[q] = ga < r ? (int64_t)J[ga] : ((ga == r && gext) ? -1 : -2);
         colB[q] = gb < r ? (int64_t)J[gb] : ((gb == r && gext) ? -1 : -2);
+        if constexpr (std::is_same<Acc, AccA>::value) {
+          pA[q] = colA[q] >= 0 ? A.A + colA[q] * m : (colA[q] == -1 ? gext : nullptr);
+          pB[q] = colB[q] >= 0 ? A.A + colB[q] * m : (colB[q] == -1 ? gext : nullptr);
+        }
       }
     }
     double va[4], vb[4];
@@ -300,8 +307,13 @@ __global__ void __launch_bounds__(256) k_gram(const Acc A, int64_t m,
       for (int q = 0; q < 4; ++q) {
         if (SMW) {
           const int64_t k = ch * 32 + tx;
-          va[q] = (k < m && colA[q] >= 0) ? A.ld(colA[q], k) : ((k < m && colA[q] == -1) ? __ldg(gext + k) : 0.0);
-          vb[q] = (k < m && colB[q] >= 0) ? A.ld(colB[q], k) : ((k < m && colB[q] == -1) ? __ldg(gext + k) : 0.0);
+          if constexpr (std::is_same<Acc, AccA>::value) {
+            va[q] = (pA[q] && k < m) ? __ldg(pA[q] + k) : 0.0;
+            vb[q] = (pB[q] && k < m) ? __ldg(pB[q] + k) : 0.0;
+          } else {
+            va[q] = (k < m && colA[q] >= 0) ? A.ld(colA[q], k) : ((k < m && colA[q] == -1) ? __ldg(gext + k) : 0.0);
+            vb[q] = (k < m && colB[q] >= 0) ? A.ld(colB[q], k) : ((k < m && colB[q] == -1) ? __ldg(gext + k) : 0.0);
+          }
         } else {
           const int64_t a = ch * 32 + ty + 8 * q;
           const bool ok = a < r;
