@@ -326,3 +326,47 @@ def model_select(A, b, x, l2):
     out = np.empty(5)
     lib().orc_model_select(Ap, bp, m, n, xp, l2, xdb.ctypes.data_as(_dp), out.ctypes.data_as(_dp))
     return int(out[0]), out[1], out[2], out[3], out[4], xdb
+
+
+# --- k-fold cross-validation along the λ path (Section 3.3) ----------
+
+def cv_folds(m, k):
+    """Fold f holds rows r with r ≡ f (mod k) (reading R35: interleaved, deterministic)."""
+    return [np.arange(f, m, k) for f in range(k)]
+
+
+def residual_ss(A, b, x):
+    """‖A x − b‖² by its definition (A is (n, m): row i is column a_i)."""
+    r = oracle_ax(A, x) - np.asarray(b, dtype=np.float64)
+    return float(r @ r)
+
+
+def oracle_ax(A, x):
+    A, m, n, Ap = _A(A)
+    x, xp = _f64(x)
+    out = np.empty(m)
+    lib().orc_ax(Ap, m, n, xp, out.ctypes.data_as(_dp))
+    return out
+
+
+def cv_path(A, b, alpha, cs, k=5, sigma0=5e-3, tol=1e-6):
+    """k-fold CV error along c ∈ cs ("cross-validation ... along the path"): λ from the FULL
+    data (λmax = ‖Aᵀb‖∞/α) so every fold uses the same grid; for each fold the
+    warm-started path on the training rows, and the held-out squared error.
+    Returns cv[c] = Σ_folds ‖b_test − A_test x_fold(c)‖² / m (reading R35) and the minimising index."""
+    A = np.ascontiguousarray(A, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    n, m = A.shape
+    lm = float(np.max(np.abs(aty(A, b)))) / alpha
+    err = np.zeros(len(cs))
+    for test in cv_folds(m, k):
+        train = np.setdiff1d(np.arange(m), test)
+        Atr, btr = np.ascontiguousarray(A[:, train]), b[train]
+        Ate, bte = np.ascontiguousarray(A[:, test]), b[test]
+        x = None
+        for i, c in enumerate(cs):
+            l1, l2 = c * alpha * lm, c * (1 - alpha) * lm
+            x, _, st, _ = solve(Atr, btr, l1, l2, sigma0=sigma0, tol=tol, x0=x)
+            err[i] += residual_ss(Ate, bte, x)
+    err /= m
+    return err, int(np.argmin(err))
