@@ -392,6 +392,7 @@ def bench_select(args):
         t0 = time.perf_counter()
         pts, best = solve_path(P, cfg.alpha, cs, max_active=100)
         ts.append(time.perf_counter() - t0)
+    lm_l1 = P.lambda_max_l1  # ‖Aᵀb‖∞ from the handle's own K1 pass (the CV grid is the full-data one)
     P.close()
     t_gpu = statistics.median(ts)
     res = {"metric": "lambda-path with model selection: time per path (s)", "value": t_gpu, "unit": "s",
@@ -413,6 +414,33 @@ def bench_select(args):
                 break
         res["cpu_baseline"] = {"value": time.perf_counter() - t0, "unit": "s", "cores": os.cpu_count(),
                                "kind": "oracle", "sample": "the same path with the same criteria"}
+    if args.cv > 0:  # k-fold CV along a 20-point grid (reading R35)
+        from paper_2006_03970_b200.path import cv_path
+
+        dA = torch.from_numpy(A).cuda()
+        st = torch.cuda.current_stream()
+
+        def make(rows):
+            sub = dA[:, torch.from_numpy(rows).cuda()].contiguous()
+            bs = torch.from_numpy(np.ascontiguousarray(b[rows])).cuda()
+            return Problem.from_device(sub.data_ptr(), bs.data_ptr(), len(rows), cfg.n, st.cuda_stream,
+                                       keep=(sub, bs))
+
+        cs_cv = lambda_grid(20)
+        cv_path(make, cfg.m, cfg.alpha, cs_cv, lm_l1, k=args.cv)  # warm-up
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        cv, best = cv_path(make, cfg.m, cfg.alpha, cs_cv, lm_l1, k=args.cv)
+        torch.cuda.synchronize()
+        res["cv"] = {"k": args.cv, "points": len(cs_cv), "seconds": time.perf_counter() - t0, "best": best,
+                     "best_c": float(cs_cv[best])}
+        if not args.no_cpu:
+            import oracle
+
+            t0 = time.perf_counter()
+            cvc, bestc = oracle.cv_path(A, b, cfg.alpha, cs_cv, k=args.cv)
+            res["cv"]["cpu_baseline"] = {"value": time.perf_counter() - t0, "unit": "s", "kind": "oracle",
+                                         "best": bestc, "max_rel_diff": float(np.max(np.abs(cv - cvc) / cvc))}
     print(json.dumps(res), flush=True)
 
 
@@ -478,6 +506,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg (40 GB configs)")
     ap.add_argument("--sweep", action="store_true", help="K1 bandwidth sweep instead of the TTS bench")
     ap.add_argument("--select", action="store_true", help="lambda path with model selection (SURVEY 8(f1))")
+    ap.add_argument("--cv", type=int, default=0, help="with --select: k-fold cross-validation over a 20-point grid")
     ap.add_argument("--sweep-n", default="100000,200000,500000,1000000,2000000,5000000,10000000")
     ap.add_argument("--sweep-reps", type=int, default=20)
     args = ap.parse_args()

@@ -170,6 +170,13 @@ typedef struct {
 
 int ssnal_en_model_select(ssnal_en_problem* p, double lambda2, double* xdb_out, ssnal_en_criteria* out);
 
+/* Held-out residual for cross-validation (Section 3.3): *rss_out = ‖A x − b‖²
+ * for this handle's A and b (e.g. the test rows of a fold) and a given x (n; host for
+ * ssnal_en_residual, device for _device).  Uses only the support of x (gathered columns).  Does not
+ * touch the handle's last solution.  EINVAL for null arguments. */
+int ssnal_en_residual(ssnal_en_problem* p, const double* x, double* rss_out);
+int ssnal_en_residual_device(ssnal_en_problem* p, const double* x_dev, double* rss_out);
+
 void ssnal_en_destroy(ssnal_en_problem* p);
 
 /* Thread-local message of the last failure on this thread ("" if none). */

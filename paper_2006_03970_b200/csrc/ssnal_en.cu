@@ -1865,6 +1865,36 @@ int ssnal_en_model_select(ssnal_en_problem* P, double l2, double* xdb_out, ssnal
   return SSNAL_OK;
 }
 
+// ‖A x − b‖² for an external x: support of x by K1e (w = 0, σ = 1, λ = 0 selects x ≠ 0 with P = x)
+// into the trial set (J[1], PJ[1], r_dev[3]) — free outside a solve — then K2 + combine + norm.
+static int residual_impl(ssnal_en_problem* P, const double* x, int x_dev, double* rss_out) {
+  if (!P || !x || !rss_out) {
+    set_err("null argument");
+    return SSNAL_EINVAL;
+  }
+  const int64_t n = P->n;
+  int rc;
+  CK(cudaMemcpyAsync(P->w[1], x, n * 8, x_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, P->st));
+  CK(cudaMemsetAsync(P->w[2], 0, n * 8, P->st));
+  if ((rc = launch_k1e(P, P->w[2], nullptr, 0.0, P->w[1], make_scal(1.0, 0.0, 0.0), nullptr))) return rc;
+  if ((rc = launch_finalize(P, P->J[1], P->PJ[1], P->r_dev + 3))) return rc;
+  if ((rc = launch_gather_dev(P, P->J[1], P->PJ[1], P->r_dev + 3))) return rc;
+  k_combine<<<1, 1024, 0, P->st>>>(P->m, P->b, -1.0, P->part_vec, kGatherDevGrid, P->tmpm, nullptr, nullptr,
+                                   P->gax_valid);
+  k_objective<<<1, 1024, 0, P->st>>>(P->m, P->tmpm, P->PJ[1], P->r_dev + 3, P->scratch + 36);
+  CKL();
+  CK(cudaMemcpyAsync(P->scratch_host + 36, P->scratch + 36, 8, cudaMemcpyDeviceToHost, P->st));
+  CK(cudaStreamSynchronize(P->st));
+  *rss_out = 2.0 * P->scratch_host[36];  // k_objective reports ½‖resid‖²
+  return SSNAL_OK;
+}
+
+int ssnal_en_residual(ssnal_en_problem* P, const double* x, double* rss_out) { return residual_impl(P, x, 0, rss_out); }
+
+int ssnal_en_residual_device(ssnal_en_problem* P, const double* x, double* rss_out) {
+  return residual_impl(P, x, 1, rss_out);
+}
+
 void ssnal_en_destroy(ssnal_en_problem* P) {
   if (!P) return;
   if (P->st) cudaStreamSynchronize(P->st);

@@ -40,3 +40,31 @@ def solve_path(P, alpha: float, cs, sigma0: float = 5e-3, tol: float = 1e-6, max
             finite = [i for i, v in enumerate(vals) if v == v]
             best[key] = min(finite, key=lambda i: vals[i]) if finite else None
     return points, best
+
+
+def cv_path(make_problem, m: int, alpha: float, cs, lambda_max_l1: float, k: int = 5, sigma0: float = 5e-3,
+            tol: float = 1e-6):
+    """k-fold cross-validation along the path (Section 3.3; reading R35).
+
+    make_problem(rows) must return a Problem over the given rows of (A, b) (e.g. a handle created
+    from a row subset in device memory).  Folds are interleaved (row r in fold r mod k); the grid
+    uses the full-data λmax = lambda_max_l1/α for every fold.  Each fold solves the
+    warm-started path on its training rows; the held-out error ‖b_test − A_test x‖² is computed by
+    the test handle (ssnal_en_residual).  Returns (cv, best) with cv[i] = Σ_folds err / m."""
+    lmax = lambda_max_l1 / alpha
+    cv = np.zeros(len(cs))
+    for f in range(k):
+        test = np.arange(f, m, k)
+        train = np.setdiff1d(np.arange(m), test)
+        Ptr, Pte = make_problem(train), make_problem(test)
+        try:
+            x = None
+            for i, c in enumerate(cs):
+                l1, l2 = c * alpha * lmax, c * (1 - alpha) * lmax
+                x, _ = Ptr.solve(l1, l2, sigma0, tol, x0=x)
+                cv[i] += Pte.residual(x)
+        finally:
+            Ptr.close()
+            Pte.close()
+    cv /= m
+    return cv, int(np.argmin(cv))

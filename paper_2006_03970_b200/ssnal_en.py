@@ -83,11 +83,14 @@ def load_library():
         L.ssnal_en_newton_direction.argtypes = [_vp, _vp, _i64, _vp, _d, _vp, _dp, P(_i32)]
         L.ssnal_en_model_select.argtypes = [_vp, _d, _dp, P(Criteria)]
         L.ssnal_en_model_select.restype = ctypes.c_int
+        L.ssnal_en_residual.argtypes = [_vp, _dp, _dp]
+        L.ssnal_en_residual_device.argtypes = [_vp, _vp, _dp]
         L.ssnal_en_destroy.argtypes = [_vp]
         L.ssnal_en_destroy.restype = None
         L.ssnal_en_last_error.restype = ctypes.c_char_p
         L.ssnal_en_version.restype = ctypes.c_char_p
-        for f in ("create", "create_device", "create_geno", "create_geno_device", "set_option", "solve", "solve_device", "aty_fused", "epilogue",
+        for f in ("create", "create_device", "create_geno", "create_geno_device", "residual", "residual_device",
+                  "set_option", "solve", "solve_device", "aty_fused", "epilogue",
                   "newton_direction"):
             getattr(L, "ssnal_en_" + f).restype = ctypes.c_int
         _lib = L
@@ -180,6 +183,18 @@ class Problem:
                                       ctypes.byref(st))
         _check(rc, (SSNAL_OK, SSNAL_NOT_CONVERGED, SSNAL_ENUMERIC))
         return x, st.as_dict()
+
+    def residual(self, x) -> float:
+        """‖A x − b‖² for this handle's A, b and a host x (cross-validation test folds)."""
+        x, xp = _f64(x)
+        out = ctypes.c_double(0.0)
+        _check(self._lib.ssnal_en_residual(self._h, xp, ctypes.byref(out)))
+        return out.value
+
+    def residual_device(self, x_ptr: int) -> float:
+        out = ctypes.c_double(0.0)
+        _check(self._lib.ssnal_en_residual_device(self._h, _vp(x_ptr), ctypes.byref(out)))
+        return out.value
 
     def solve_device(self, lambda1, lambda2, sigma0, tol, x0_ptr, x_out_ptr):
         st = Stats()
