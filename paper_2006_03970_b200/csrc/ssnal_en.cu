@@ -312,6 +312,8 @@ struct ssnal_en_problem {
   int cg_maxit = 1000;
   // counters for the current call
   int64_t launches = 0;
+  void* arena = nullptr;    // all device buffers above (one allocation)
+  void* arena_h = nullptr;  // mapped pinned host buffers (one allocation)
   double stat_l1 = 0, stat_l2 = 0;
   bool stat_warm_pass = false;
   cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr;  // solve timing (persistent)
@@ -334,6 +336,36 @@ struct ssnal_en_problem {
 };
 
 namespace {
+
+// Large per-handle allocations (the owned copy of A, the buffer arena) come from the device's
+// stream-ordered memory pool with an unlimited release threshold: destroy returns them to the
+// pool and the next create reuses them without mapping / unmapping device memory.
+void* pool_alloc(size_t bytes) {
+  static bool init = false;
+  if (!init) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    init = true;
+  }
+  void* p = nullptr;
+  if (cudaMallocAsync(&p, bytes, 0) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  if (cudaStreamSynchronize(0) != cudaSuccess) return nullptr;
+  return p;
+}
+void pool_free(void* p) {
+  if (p) {
+    cudaFreeAsync(p, 0);
+    cudaStreamSynchronize(0);
+  }
+}
 
 int alloc(void** p, size_t bytes) {
   cudaError_t e = cudaMalloc(p, bytes > 0 ? bytes : 16);
@@ -423,50 +455,74 @@ int configure(ssnal_en_problem* P) {
   return SSNAL_OK;
 }
 
+// All per-handle buffers live in one device arena and one mapped pinned host arena: create and
+// destroy cost two allocations instead of ~40 (cudaFree / cudaFreeHost synchronise the device).
+struct Arena {
+  std::vector<std::pair<void**, size_t>> req;
+  size_t total = 0;
+  void add(void** p, size_t bytes) {
+    req.push_back({p, total});
+    total += (bytes + 255) / 256 * 256;
+  }
+  void assign(char* base) {
+    for (auto& r : req) *r.first = base + r.second;
+  }
+};
+
 int allocate(ssnal_en_problem* P) {
   const int64_t m = P->m, n = P->n;
-  for (int i = 0; i < 3; ++i) AL(P->w[i], n * 8);
-  AL(P->x, n * 8);
-  AL(P->seg_idx, n * 4);
-  AL(P->mask, n / 8 + 64);
-  AL(P->seg_P, n * 8);
-  AL(P->cta_cnt, (size_t)P->nsm * 4 + 64);
-  AL(P->part_scal, (size_t)P->nsm * 4 * 8 + 64);
-  AL(P->part_vec, (size_t)P->nsm * m * 8);
+  Arena d;
+  for (int i = 0; i < 3; ++i) d.add((void**)&P->w[i], n * 8);
+  d.add((void**)&P->x, n * 8);
+  d.add((void**)&P->seg_idx, n * 4);
+  d.add((void**)&P->mask, n / 8 + 64);
+  d.add((void**)&P->seg_P, n * 8);
+  d.add((void**)&P->cta_cnt, (size_t)P->nsm * 4 + 64);
+  d.add((void**)&P->part_scal, (size_t)P->nsm * 4 * 8 + 64);
+  d.add((void**)&P->part_vec, (size_t)P->nsm * m * 8);
   for (int i = 0; i < 2; ++i) {
-    AL(P->J[i], n * 4);
-    AL(P->PJ[i], n * 8);
-    AL(P->y[i], m * 8);
-    AL(P->g[i], m * 8);
+    d.add((void**)&P->J[i], n * 4);
+    d.add((void**)&P->PJ[i], n * 8);
+    d.add((void**)&P->y[i], m * 8);
+    d.add((void**)&P->g[i], m * 8);
   }
-  AL(P->r_dev, 8 * 8);
-  AL(P->Jx, n * 4);
-  AL(P->Px, n * 8);
-  AL(P->d, m * 8);
-  AL(P->u, m * 8);
-  AL(P->tmpm, m * 8);
-  AL(P->Mmat, (size_t)(m + 1) * (m + 1) * 8);
-  AL(P->Winv, (size_t)((m + 31) / 32) * 33 * 32 * 8);  // block inverses + reciprocals
+  d.add((void**)&P->r_dev, 8 * 8);
+  d.add((void**)&P->Jx, n * 4);
+  d.add((void**)&P->Px, n * 8);
+  d.add((void**)&P->d, m * 8);
+  d.add((void**)&P->u, m * 8);
+  d.add((void**)&P->tmpm, m * 8);
+  d.add((void**)&P->Mmat, (size_t)(m + 1) * (m + 1) * 8);
+  d.add((void**)&P->Winv, (size_t)((m + 31) / 32) * 33 * 32 * 8);  // block inverses
   P->W_splits = 16;
-  AL(P->W, (size_t)P->W_splits * m * m * 8);
-  AL(P->info, 64);
-  AL(P->ev_dev, sizeof(EvalOut) * 4);
-  AL(P->scratch, 64 * 8);
-  AL(P->flags, 64);
-  AL(P->blk, (size_t)((m + 31) / 32) * 3 * 8 + 64);
-  AL(P->ticket, 64);
-  AL(P->gax_valid, 4 * 256);
-  AL(P->cg_res, m * 8);
-  AL(P->cg_parts, (size_t)P->nsm * m * 8);
-  AL(P->cg_scal, (size_t)P->nsm * 2 * 8 + 64);
+  d.add((void**)&P->W, (size_t)P->W_splits * m * m * 8);
+  d.add((void**)&P->info, 64);
+  d.add((void**)&P->ev_dev, sizeof(EvalOut) * 4);
+  d.add((void**)&P->scratch, 64 * 8);
+  d.add((void**)&P->flags, 64);
+  d.add((void**)&P->blk, (size_t)((m + 31) / 32) * 3 * 8 + 64);
+  d.add((void**)&P->ticket, 64);
+  d.add((void**)&P->gax_valid, 4 * 256);
+  d.add((void**)&P->cg_res, m * 8);
+  d.add((void**)&P->cg_parts, (size_t)P->nsm * m * 8);
+  d.add((void**)&P->cg_scal, (size_t)P->nsm * 2 * 8 + 64);
+  d.add((void**)&P->ctl, sizeof(DevCtl));
+  P->arena = pool_alloc(d.total);
+  if (!P->arena) {
+    set_err("device allocation of %zu bytes failed", d.total);
+    return SSNAL_ECUDA;
+  }
+  d.assign((char*)P->arena);
   CK(cudaMemset(P->ticket, 0, 64));
-  CK(cudaHostAlloc((void**)&P->ev_host, sizeof(EvalOut) * 4, cudaHostAllocMapped));
-  memset(P->ev_host, 0, sizeof(EvalOut) * 4);
+  Arena h;
+  h.add((void**)&P->ev_host, sizeof(EvalOut) * 4);
+  h.add((void**)&P->scratch_host, 64 * 8);
+  h.add((void**)&P->ctl_host, sizeof(DevCtl));
+  h.add((void**)&P->ev_out_host, sizeof(EvalOut));
+  CK(cudaHostAlloc(&P->arena_h, h.total, cudaHostAllocMapped));
+  memset(P->arena_h, 0, h.total);
+  h.assign((char*)P->arena_h);
   CK(cudaHostGetDevicePointer((void**)&P->ev_host_dev, P->ev_host, 0));
-  CK(cudaMallocHost((void**)&P->scratch_host, 64 * 8));
-  AL(P->ctl, sizeof(DevCtl));
-  CK(cudaMallocHost((void**)&P->ctl_host, sizeof(DevCtl)));
-  CK(cudaMallocHost((void**)&P->ev_out_host, sizeof(EvalOut)));
   return SSNAL_OK;
 }
 
@@ -1357,48 +1413,12 @@ static int create_common(ssnal_en_problem* P) {
 
 static void destroy_bufs(ssnal_en_problem* P) {
   if (!P) return;
-  for (int i = 0; i < 3; ++i) cudaFree(P->w[i]);
-  cudaFree(P->x);
-  cudaFree(P->seg_idx);
-  cudaFree(P->seg_P);
-  cudaFree(P->mask);
-  cudaFree(P->cta_cnt);
-  cudaFree(P->part_scal);
-  cudaFree(P->part_vec);
-  for (int i = 0; i < 2; ++i) {
-    cudaFree(P->J[i]);
-    cudaFree(P->PJ[i]);
-    cudaFree(P->y[i]);
-    cudaFree(P->g[i]);
-  }
-  cudaFree(P->r_dev);
-  cudaFree(P->Jx);
-  cudaFree(P->Px);
-  cudaFree(P->d);
-  cudaFree(P->u);
-  cudaFree(P->tmpm);
-  cudaFree(P->Mmat);
+  pool_free(P->arena);
   cudaFree(P->Msel);
-  cudaFree(P->Winv);
-  cudaFree(P->W);
-  cudaFree(P->info);
-  cudaFree(P->ev_dev);
-  cudaFree(P->scratch);
-  cudaFree(P->flags);
-  cudaFree(P->blk);
-  cudaFree(P->ticket);
-  cudaFree(P->gax_valid);
-  cudaFree(P->cg_res);
-  cudaFree(P->cg_parts);
-  cudaFree(P->cg_scal);
-  if (P->ev_host) cudaFreeHost(P->ev_host);
-  if (P->scratch_host) cudaFreeHost(P->scratch_host);
+  if (P->arena_h) cudaFreeHost(P->arena_h);
   drop_graph(P);
   for (int i = 0; i < 3; ++i)
     if (P->cap[i]) cudaStreamDestroy(P->cap[i]);
-  cudaFree(P->ctl);
-  if (P->ctl_host) cudaFreeHost(P->ctl_host);
-  if (P->ev_out_host) cudaFreeHost(P->ev_out_host);
   for (auto e : P->ev_pool) cudaEventDestroy(e);
   if (P->ev_t0) cudaEventDestroy(P->ev_t0);
   if (P->ev_t1) cudaEventDestroy(P->ev_t1);
@@ -1406,10 +1426,10 @@ static void destroy_bufs(ssnal_en_problem* P) {
     cudaEventDestroy(pr.first);
     cudaEventDestroy(pr.second);
   }
-  cudaFree(P->A_own);
-  cudaFree(P->codes_own);
-  cudaFree(P->tab_own);
-  cudaFree(P->b_own);
+  pool_free(P->A_own);
+  pool_free(P->codes_own);
+  pool_free(P->tab_own);
+  pool_free(P->b_own);
 }
 
 static int check_dims(int64_t m, int64_t n) {
@@ -1431,8 +1451,9 @@ int ssnal_en_create(const double* A_colmajor, const double* b, int64_t m, int64_
   ssnal_en_problem* P = new ssnal_en_problem();
   P->m = m;
   P->n = n;
-  if (cudaMalloc((void**)&P->A_own, (size_t)m * n * 8 + 64) != cudaSuccess ||
-      cudaMalloc((void**)&P->b_own, (size_t)m * 8 + 64) != cudaSuccess) {
+  P->A_own = (double*)pool_alloc((size_t)m * n * 8 + 64);
+  P->b_own = (double*)pool_alloc((size_t)m * 8 + 64);
+  if (!P->A_own || !P->b_own) {
     set_err("cudaMalloc for A (%zu bytes) failed", (size_t)m * n * 8);
     destroy_bufs(P);
     delete P;
@@ -1545,9 +1566,10 @@ int ssnal_en_create_geno(const uint8_t* codes, int64_t stride, const double* tab
     delete P;
     return rc;
   }
-  if (cudaMalloc((void**)&P->codes_own, (size_t)n * stride + 64) != cudaSuccess ||
-      cudaMalloc((void**)&P->tab_own, (size_t)n * 3 * 8 + 64) != cudaSuccess ||
-      cudaMalloc((void**)&P->b_own, (size_t)m * 8 + 64) != cudaSuccess) {
+  P->codes_own = (uint8_t*)pool_alloc((size_t)n * stride + 64);
+  P->tab_own = (double*)pool_alloc((size_t)n * 3 * 8 + 64);
+  P->b_own = (double*)pool_alloc((size_t)m * 8 + 64);
+  if (!P->codes_own || !P->tab_own || !P->b_own) {
     set_err("cudaMalloc for genotype codes failed");
     destroy_bufs(P);
     delete P;
