@@ -403,6 +403,7 @@ __global__ void k_gram_reduce(const double* __restrict__ W, int ns, int64_t nout
 // ---------------------------------------------------------------------------
 constexpr int CHT = 32;  // tile edge
 constexpr int TLD = 33;  // smem tile leading dimension
+constexpr int kColSlots = 3;  // column tiles a worker quad holds for the TRSM (≤ 3 × 30 quads ≥ 64 row tiles)
 
 SSN_DEV void dmma(double (&d)[2], double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -629,6 +630,13 @@ SSN_DEV void backward_solve(const double* M, int ld, int N, const double* Winv, 
   }
 }
 
+// dynamic shared memory of k_chol_cluster (bytes): factorisation operands, or in the backward
+// solve z (1024) + the W ring
+constexpr size_t kCholSmemFact =
+    (size_t)(2 * (3 + kColSlots) * CHT * TLD + 2 * CHT * TLD + kDiagScratch) * sizeof(double);
+constexpr size_t kCholSmemBwd = (size_t)(1024 + kBwdRing * CHT * CHT + 8 * CHT * TLD) * sizeof(double);
+constexpr size_t kCholSmem = kCholSmemFact > kCholSmemBwd ? kCholSmemFact : kCholSmemBwd;
+
 // NR ≥ N + 1 rows: rows N..NR-1 are appended rows C, which leave the factorisation as C L⁻ᵀ.
 // With out != nullptr row N is the right-hand side and the backward solve runs; otherwise the
 // kernel stops after the factorisation (e.g. degrees of freedom from C = A_J).
@@ -636,7 +644,7 @@ __global__ void __launch_bounds__(256, 1) k_chol_cluster(double* M, int N, int N
                                                          double scale, const double* __restrict__ dotv,
                                                          double* dot_out, double* Winv, int* info,
                                                          const double* __restrict__ ybase, double* __restrict__ yt,
-                                                         const DirGeo* geo, int want) {
+                                                         const DirGeo* geo, int want, int* kflag) {
   namespace cg = cooperative_groups;
   if (geo) {  // graph mode: order from the device geometry; whole cluster exits together
     if (geo->branch != want) return;
@@ -649,176 +657,388 @@ __global__ void __launch_bounds__(256, 1) k_chol_cluster(double* M, int N, int N
   extern __shared__ double dsm[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int quad = warp >> 2, qw = warp & 3;
-  double* SA = dsm + (size_t)warp * 2 * CHT * TLD;  // per-warp operand tiles (phase C)
-  double* SB = SA + CHT * TLD;
-  double* SQ = dsm + (size_t)quad * 2 * CHT * TLD;  // per-quad tile (phase B; aliases SA/SB)
-  double* T = dsm + (size_t)8 * 2 * CHT * TLD;      // W_k (phase B operand)
-  double* T2 = T + CHT * TLD;                        // CTA-0 diagonal tile (look-ahead)
-  double* T3 = T2 + CHT * TLD;                       // CTA-0: L_{k+1,k} from phase B
-  double* dscr = T3 + CHT * TLD;                     // diag_factor4 scratch
+  const int g = lane >> 2, t = lane & 3;
+  // smem: per quad [SA, SB, Wq, slots × kColSlots] (tiles 32 × TLD); CTA 0 adds T2, T3, scratch
+  double* QB = dsm + (size_t)quad * (3 + kColSlots) * CHT * TLD;
+  double* SA = QB;                       // L_ik rows of the tile being updated
+  double* SB = QB + CHT * TLD;           // L_jk rows
+  double* Wq = QB + 2 * CHT * TLD;       // W_{k+1} for this quad's TRSMs
+  double* slots = QB + 3 * CHT * TLD;    // updated column-(k+1) tiles awaiting W_{k+1}
+  double* T2 = dsm + (size_t)2 * (3 + kColSlots) * CHT * TLD;  // CTA-0 diagonal tile
+  double* T3 = T2 + CHT * TLD;                                  // CTA-0: L_{k+1,k}
+  double* dscr = T3 + CHT * TLD;                                // diag_factor4 scratch
   const int ntc = (N + CHT - 1) / CHT, ntr = (NR + CHT - 1) / CHT;
-  // Roles.  CTA 0 quad 0 = the diagonal team: the whole critical chain factor(k) → L_{k+1,k} →
-  // update (k+1,k+1) → factor(k+1) runs there with operands in its smem; SM 0 takes no other tiles
-  // when the cluster has more CTAs.  Other quads take the remaining phase-B tiles; the other CTAs'
-  // warps the phase-C trailing updates.
+  // Roles.  CTA 0 quad 0 = the diagonal team (the critical chain).  Worker quads: every quad of
+  // the other CTAs (CTA 0 quad 1 too when the cluster has one CTA).
   const bool diag_team = (rank == 0 && quad == 0);
-  const int NQ = (CS > 1) ? 2 * (CS - 1) : 1;  // phase-B worker quads
+  const int NQ = (CS > 1) ? 2 * (CS - 1) : 1;
   const int gq = (CS > 1) ? ((rank == 0) ? -1 : 2 * (rank - 1) + quad) : (quad == 1 ? 0 : -1);
-  const int NWw = (CS > 1) ? 8 * (CS - 1) : 4;  // phase-C worker warps
-  const int wid = (CS > 1) ? ((rank == 0) ? -1 : 8 * (rank - 1) + warp) : (warp >= 4 ? warp - 4 : -1);
+  const int qbar = 3 + quad;  // named barrier of this quad (128 threads)
 #ifdef CHOL_PROBE
 #define STAMP(i) do { if (rank == 0 && tid == 0 && (i) < 64) { unsigned long long t_; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); g_t[i] = t_; g_c[i] = clock64(); } } while (0)
+#define STAMPW(i) do { if (rank == 1 && tid == 0 && (i) < 64) { unsigned long long t_; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); g_t[i] = t_; g_c[i] = clock64(); } } while (0)
 #else
 #define STAMP(i) do {} while (0)
+#define STAMPW(i) do {} while (0)
 #endif
   STAMP(0);
-  // k = −1: the diagonal team factors tile (0,0); k ≥ 0: phase B(k), then phase C(k) with the
-  // look-ahead factor of tile (k+1,k+1) — one call site of diag_factor4 (I-cache).
-  for (int k = -1; k < ntc; ++k) {
-    const int k0 = k * CHT;
-    const int kn = min(CHT, N - k0);
-    const int g = lane >> 2, t = lane & 3;
-    double pre[4][2];  // diagonal team: A_{k+1,k+1} fragment, prefetched during phase B
-    if (k >= 0) {
-      // ---- B: L_ik = A_ik W_kᵀ for row tiles i > k; a quad of 4 warps per tile (8 rows each) ----
-      const int nB = ntr - k - 1;
-      if (diag_team && k + 1 < ntc) {
-        const int d0 = (k + 1) * CHT, r = d0 + 8 * qw + g;
-#pragma unroll
-        for (int cb = 0; cb < 4; ++cb)
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int c = d0 + 8 * cb + 2 * t + e;
-            pre[cb][e] = (r < NR && c < N) ? __ldcg(M + (int64_t)r + (int64_t)c * ld) : 0.0;
-          }
-      }
-      // CTA-uniform: quad 0 of a worker CTA has the lower quad index (gq0 = 2(rank − 1))
-      const bool cta_has_b = (rank == 0) ? (nB > 0) : (2 * (rank - 1) < nB - 1);
-      if (rank != 0 && cta_has_b) {  // T[c][p] = W_k[c][p] (CTA 0 has it from the factor)
-        const double* Wk = Winv + (size_t)k * CHT * CHT;
-        double v[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) v[u] = __ldcg(Wk + tid + 256 * u);
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int e = tid + 256 * u;
-          T[(e >> 5) * TLD + (e & 31)] = v[u];
-        }
-        __syncthreads();
-      }
-      if (k == 1) STAMP(44);
-      // tile 0 (= L_{k+1,k}) → diagonal team; tiles 1.. → worker quads
-#pragma unroll 1
-      for (int q = diag_team ? 0 : 1 + gq; q < nB && (diag_team || gq >= 0); q += diag_team ? nB : NQ) {
-        const int r0 = (k + 1 + q) * CHT;
-        {  // rows 8qw..8qw+7: lane ℓ loads row 8qw + ℓ/4, columns 8(ℓ%4)..+7
-          const int rr = 8 * qw + g, cc = 8 * t;
-          const bool rok = r0 + rr < NR;
-          const double* src = M + (int64_t)(k0 + cc) * ld + (rok ? r0 + rr : 0);
+  if (rank == 0 && tid < ntc + 1) kflag[tid] = 0;  // W-ready flags of this launch
+  cl.sync();
+  // One phase per panel.  M(k), k = −1 … ntc−2:
+  //   diagonal team: A_{k+1,k+1} −= L_{k+1,k} L_{k+1,k}ᵀ (k ≥ 0), factor it → L, W_{k+1}; publish
+  //                  W_{k+1} (global) with a release flag
+  //   worker quads:  column-(k+1) tiles (i ≥ k+2): A_{i,k+1} −= L_ik L_{k+1,k}ᵀ into a smem slot;
+  //                  trailing tiles (i, j ≥ k+2): A_ij −= L_ik L_jkᵀ in place;
+  //                  then wait for W_{k+1} (acquire) and TRSM the slots: L_{i,k+1} = A_{i,k+1} W_{k+1}ᵀ
+  //   cluster barrier (column k+1 of L complete in M)
+  for (int k = -1; k + 1 < ntc; ++k) {
+    const int k0 = k * CHT, kn = (k >= 0) ? min(CHT, N - k0) : 0;
+    const int c0 = (k + 1) * CHT, cn = min(CHT, N - c0);  // the column being factored / TRSM'd
+    if (diag_team) {
+      if (k < 0) {
+        if (warp == 0) load_tile_rows(M, ld, 0, 0, NR, N, T2, lane);
+      } else {
+        // L_{k+1,k} (rows c0.., panel k) and A_{k+1,k+1}, then the DMMA update (8 rows per warp)
+        {  // coalesced: lane = row, warp qw takes columns 8qw .. 8qw+7
+          const bool rok = c0 + lane < NR;
+          const double* src = M + (int64_t)(k0 + 8 * qw) * ld + (rok ? c0 + lane : 0);
           double v[8];
 #pragma unroll
-          for (int e = 0; e < 8; ++e) v[e] = (rok && cc + e < kn) ? __ldcg(src + e * ld) : 0.0;
+          for (int e = 0; e < 8; ++e) v[e] = (rok && 8 * qw + e < kn) ? __ldcg(src + e * ld) : 0.0;
 #pragma unroll
-          for (int e = 0; e < 8; ++e) SQ[rr * TLD + cc + e] = v[e];
+          for (int e = 0; e < 8; ++e) T3[lane * TLD + 8 * qw + e] = v[e];
         }
-        asm volatile("bar.sync %0, 128;" ::"r"(3 + quad) : "memory");
-        if (k == 1) STAMP(45);
         double acc[4][2];
-#pragma unroll
-        for (int cb = 0; cb < 4; ++cb) acc[cb][0] = acc[cb][1] = 0.0;
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          const double af = SQ[(8 * qw + g) * TLD + 4 * kk + t];
-#pragma unroll
-          for (int cb = 0; cb < 4; ++cb) dmma(acc[cb], af, T[(8 * cb + g) * TLD + 4 * kk + t]);
-        }
-        if (k == 1) STAMP(46);
-        const int r = r0 + 8 * qw + g;
+        const int r = c0 + 8 * qw + g;
 #pragma unroll
         for (int cb = 0; cb < 4; ++cb)
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
-            const int c = 8 * cb + 2 * t + e;
-            if (r < NR && c < kn) M[(int64_t)r + (int64_t)(k0 + c) * ld] = acc[cb][e];
-            if (diag_team) T3[(8 * qw + g) * TLD + c] = (r < NR && c < kn) ? acc[cb][e] : 0.0;
+            const int c = c0 + 8 * cb + 2 * t + e;
+            acc[cb][e] = (r < NR && c < N) ? __ldcg(M + (int64_t)r + (int64_t)c * ld) : 0.0;
           }
-        asm volatile("bar.sync %0, 128;" ::"r"(3 + quad) : "memory");  // SQ reuse
-      }
-      cl.sync();
-      STAMP(2 + 2 * k);
-      if (k + 1 >= ntc) break;
-    }
-    // ---- C: A_ij −= L_ik L_jkᵀ for k < j < ntc, j ≤ i < ntr ----
-    if (diag_team) {
-      if (k < 0) {  // tile (0,0) as loaded
-        if (warp == 0) load_tile_rows(M, ld, 0, 0, NR, N, T2, lane);
-      } else {  // tile (k+1,k+1) = prefetched A − L_{k+1,k} L_{k+1,k}ᵀ, operands in smem (T3)
+        asm volatile("bar.sync 2, 128;" ::: "memory");
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           const double af = -T3[(8 * qw + g) * TLD + 4 * kk + t];
 #pragma unroll
-          for (int cb = 0; cb < 4; ++cb) dmma(pre[cb], af, T3[(8 * cb + g) * TLD + 4 * kk + t]);
+          for (int cb = 0; cb < 4; ++cb) dmma(acc[cb], af, T3[(8 * cb + g) * TLD + 4 * kk + t]);
         }
 #pragma unroll
         for (int cb = 0; cb < 4; ++cb)
 #pragma unroll
-          for (int e = 0; e < 2; ++e) T2[(8 * qw + g) * TLD + 8 * cb + 2 * t + e] = pre[cb][e];
+          for (int e = 0; e < 2; ++e) T2[(8 * qw + g) * TLD + 8 * cb + 2 * t + e] = acc[cb][e];
       }
       asm volatile("bar.sync 2, 128;" ::: "memory");
       if (k == 1) STAMP(48);
-      {
-        const int n0 = (k + 1) * CHT;
-        diag_factor4(T2, M, ld, n0, min(CHT, N - n0), min(CHT, NR - n0), Winv + (size_t)(k + 1) * CHT * CHT, T,
-                     info, dscr, tid);
-        if (k == 1) STAMP(49);
+#if defined(CHOL_EXPERIMENT) && CHOL_EXPERIMENT == 3
+      if (false)
+#endif
+      diag_factor4(T2, M, ld, c0, cn, min(CHT, NR - c0), Winv + (size_t)(k + 1) * CHT * CHT, nullptr, info, dscr,
+                   tid);
+      __threadfence();                                 // this thread's W_{k+1} / L stores, gpu scope
+      asm volatile("bar.sync 2, 128;" ::: "memory");  // … for all 128 threads before the release
+      if (tid == 0) {
+        __threadfence();
+        asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(kflag + k + 1), "r"(1) : "memory");
       }
-    } else if (wid >= 0 && k >= 0) {
-      const int remc = ntc - k - 1, remr = ntr - k - 1;
-      const int ntri = remc * (remc + 1) / 2;
-      const int npairs = ntri + (remr - remc) * remc;
-#pragma unroll 1
-      for (int q = 1 + wid; q < npairs; q += NWw) {  // tile 0 = (k+1, k+1) is the diagonal team's
-        int ii, jj;
-        if (q < ntri) tri_tile(q, &ii, &jj);
-        else {  // rectangular part: appended row tiles below the square (rhs row, C rows)
-          const int e = q - ntri;
-          ii = remc + e / remc;
-          jj = e % remc;
+      if (k == 1) STAMP(49);
+    } else if (gq >= 0) {
+      const int ncol = ntr - k - 2;                       // column-(k+1) tiles i = k+2 …
+      const int remc = ntc - k - 2, remr = ntr - k - 2;   // trailing: columns k+2 … ntc−1
+      const int ntri = remc > 0 ? remc * (remc + 1) / 2 : 0;
+      const int ntrail = (k >= 0 && remc > 0) ? ntri + (remr - remc) * remc : 0;
+      int nslot = 0;
+      // job q → tile (i0, j0); column jobs (q < ncol) first.  Software-pipelined: the operands of
+      // job q + NQ are loaded into registers while job q computes.
+      auto job_tile = [&](int q, int& i0, int& j0) {
+        if (q < ncol) {
+          i0 = (k + 2 + q) * CHT;
+          j0 = c0;
+        } else {
+          const int e = q - ncol;
+          int ii, jj;
+          if (e < ntri) tri_tile(e, &ii, &jj);
+          else {
+            const int f = e - ntri;
+            ii = remc + f / remc;
+            jj = f % remc;
+          }
+          i0 = (k + 2 + ii) * CHT;
+          j0 = (k + 2 + jj) * CHT;
         }
-        const int i0 = (k + 1 + ii) * CHT, j0 = (k + 1 + jj) * CHT;
-        load_tile_rows(M, ld, i0, k0, NR, k0 + kn, SA, lane);
-        load_tile_rows(M, ld, j0, k0, N, k0 + kn, SB, lane);
-        double acc[4][4][2];
+      };
+      double va[8], vb[8], acc[4][2];
+      auto fetch = [&](int q) {  // A_ij fragment + this thread's rows of L_ik, L_jk
+        int i0, j0;
+        job_tile(q, i0, j0);
+        const int r = i0 + 8 * qw + g;
 #pragma unroll
-        for (int rb = 0; rb < 4; ++rb)
+        for (int cb = 0; cb < 4; ++cb)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int c = j0 + 8 * cb + 2 * t + e;
+            acc[cb][e] = (r < NR && c < N) ? __ldcg(M + (int64_t)r + (int64_t)c * ld) : 0.0;
+          }
+        if (k >= 0) {  // coalesced: lane = row, warp qw takes columns 8qw .. 8qw+7 of both tiles
+          const bool ra = i0 + lane < NR, rb = j0 + lane < N;
+          const double* sa = M + (int64_t)(k0 + 8 * qw) * ld + (ra ? i0 + lane : 0);
+          const double* sb = M + (int64_t)(k0 + 8 * qw) * ld + (rb ? j0 + lane : 0);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            va[e] = (ra && 8 * qw + e < kn) ? __ldcg(sa + e * ld) : 0.0;
+            vb[e] = (rb && 8 * qw + e < kn) ? __ldcg(sb + e * ld) : 0.0;
+          }
+        }
+      };
+      if (k == 1) STAMPW(50);
+      if (gq < ncol + ntrail) fetch(gq);
+#pragma unroll 1
+      for (int q = gq; q < ncol + ntrail; q += NQ) {
+        int i0, j0;
+        job_tile(q, i0, j0);
+        const bool colj = q < ncol;
+        double cur[4][2];
+#pragma unroll
+        for (int cb = 0; cb < 4; ++cb) cur[cb][0] = acc[cb][0], cur[cb][1] = acc[cb][1];
+        if (k >= 0) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            SA[lane * TLD + 8 * qw + e] = va[e];
+            SB[lane * TLD + 8 * qw + e] = vb[e];
+          }
+        }
+        asm volatile("bar.sync %0, 128;" ::"r"(qbar) : "memory");
+        if (k == 1 && q == gq) STAMPW(51);
+#if defined(CHOL_EXPERIMENT) && CHOL_EXPERIMENT == 2
+        if (false)
+#endif
+        if (q + NQ < ncol + ntrail) fetch(q + NQ);  // next job's loads in flight during the DMMAs
+        if (k == 1 && q == gq) STAMPW(52);
+#if defined(CHOL_EXPERIMENT) && CHOL_EXPERIMENT == 1
+        if (false)
+#endif
+        if (k >= 0) {
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            const double af = -SA[(8 * qw + g) * TLD + 4 * kk + t];
+#pragma unroll
+            for (int cb = 0; cb < 4; ++cb) dmma(cur[cb], af, SB[(8 * cb + g) * TLD + 4 * kk + t]);
+          }
+        }
+        if (k == 1 && q == gq) STAMPW(53);
+        // column tiles beyond the slots (small clusters, many appended rows) go back to M in place
+        double* dst = (colj && nslot < kColSlots) ? slots + (size_t)nslot * CHT * TLD : nullptr;
+        if (colj) ++nslot;
+        const int r = i0 + 8 * qw + g;
+        if (dst) {  // keep for the TRSM (full tile, zero outside)
+#pragma unroll
+          for (int cb = 0; cb < 4; ++cb)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) dst[(8 * qw + g) * TLD + 8 * cb + 2 * t + e] = cur[cb][e];
+        } else {
 #pragma unroll
           for (int cb = 0; cb < 4; ++cb)
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
-              const int r = i0 + 8 * rb + g, c = j0 + 8 * cb + 2 * t + e;
-              acc[rb][cb][e] = (r < NR && c < N) ? __ldcg(M + (int64_t)r + (int64_t)c * ld) : 0.0;
+              const int rl = 8 * qw + g, cl_ = 8 * cb + 2 * t + e;
+              const int c = j0 + cl_;
+              if (r < NR && c < N && (i0 != j0 || cl_ <= rl)) M[(int64_t)r + (int64_t)c * ld] = cur[cb][e];
             }
-        __syncwarp();
-        tile_mma(SA, SB, acc, -1.0, lane);
+        }
+        asm volatile("bar.sync %0, 128;" ::"r"(qbar) : "memory");  // SA/SB reuse
+        if (k == 1 && q == gq) STAMPW(54);
+        if (k == 1 && q == gq + NQ) STAMPW(55);
+      }
+      if (k == 1) STAMPW(56);
+      if (nslot > 0) {  // TRSM of this quad's column tiles with W_{k+1}
+        if (tid % 128 == 0) {
+          int f;
+          do {
+            asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(f) : "l"(kflag + k + 1) : "memory");
+            if (!f) __nanosleep(64);
+          } while (!f);
+        }
+        asm volatile("bar.sync %0, 128;" ::"r"(qbar) : "memory");
+        if (k == 1) STAMPW(57);
+        {
+          const double* Wk = Winv + (size_t)(k + 1) * CHT * CHT;
+          const int tq = tid & 127;
+          double v[8];
 #pragma unroll
-        for (int rb = 0; rb < 4; ++rb)
+          for (int u = 0; u < 8; ++u) v[u] = __ldcg(Wk + tq + 128 * u);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int e = tq + 128 * u;
+            Wq[(e >> 5) * TLD + (e & 31)] = v[u];
+          }
+        }
+        asm volatile("bar.sync %0, 128;" ::"r"(qbar) : "memory");
+        int s = 0;
+#pragma unroll 1
+        for (int q = gq; q < ncol; q += NQ, ++s) {
+          const int r0 = (k + 2 + q) * CHT;
+          const double* src = slots + (size_t)s * CHT * TLD;
+          if (s >= kColSlots) {  // overflow tile: reload the updated A_{i,k+1} from M into SA
+            const bool rok = r0 + lane < NR;
+            const double* sp = M + (int64_t)(c0 + 8 * qw) * ld + (rok ? r0 + lane : 0);
+            double v[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) v[e] = (rok && 8 * qw + e < cn) ? __ldcg(sp + e * ld) : 0.0;
+            asm volatile("bar.sync %0, 128;" ::"r"(qbar) : "memory");  // previous SA readers done
+#pragma unroll
+            for (int e = 0; e < 8; ++e) SA[lane * TLD + 8 * qw + e] = v[e];
+            asm volatile("bar.sync %0, 128;" ::"r"(qbar) : "memory");
+            src = SA;
+          }
+          double acc[4][2];
+#pragma unroll
+          for (int cb = 0; cb < 4; ++cb) acc[cb][0] = acc[cb][1] = 0.0;
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            const double af = src[(8 * qw + g) * TLD + 4 * kk + t];
+#pragma unroll
+            for (int cb = 0; cb < 4; ++cb) dmma(acc[cb], af, Wq[(8 * cb + g) * TLD + 4 * kk + t]);
+          }
+          const int r = r0 + 8 * qw + g;
 #pragma unroll
           for (int cb = 0; cb < 4; ++cb)
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
-              const int rl = 8 * rb + g, cl_ = 8 * cb + 2 * t + e;
-              const int r = i0 + rl, c = j0 + cl_;
-              if (r < NR && c < N && (i0 != j0 || cl_ <= rl)) M[(int64_t)r + (int64_t)c * ld] = acc[rb][cb][e];
+              const int c = 8 * cb + 2 * t + e;
+              if (r < NR && c < cn) M[(int64_t)r + (int64_t)(c0 + c) * ld] = acc[cb][e];
             }
-        __syncwarp();
+        }
       }
     }
+    if (k == 1) STAMPW(58);
     cl.sync();
-    STAMP(3 + 2 * k);
+    STAMP(2 + k);
   }
   STAMP(40);
-  if (rank != 0 || out == nullptr) return;
-  // ---- backward substitution v = L⁻ᵀ z by CTA 0 (z = row N) ----
+  if (out == nullptr) return;
+  // ---- backward substitution v = L⁻ᵀ z (z = row N) ----
+  // Cluster version when every CTA can stage its share in smem: CTA c owns the column blocks
+  // a ≡ c (mod CS) and holds z_a, W_a and the tiles L_ba (b > a).  Step b (descending): the owner of
+  // block b computes v_b = W_bᵀ z_b and writes it into every CTA's v buffer (DSMEM) | cluster barrier
+  // | every CTA applies z_a −= L_baᵀ v_b to its blocks a < b.  Otherwise CTA 0 alone (backward_solve).
+  int own_tiles = 0;  // rank 0 owns the most: blocks 0, CS, 2CS, …
+  for (int a = 0; a < ntc; a += CS) own_tiles += ntc - a;  // tiles below + W_a
+  const int kBwdTileBudget = (int)((kCholSmem / sizeof(double) - 1024 - 64 * CHT) / (CHT * TLD));
+  if (CS > 1 && own_tiles <= kBwdTileBudget) {
+    double* vfull = dsm;                        // 1024: v, filled block by block (broadcast)
+    double* zl = dsm + 1024;                    // 64 × 32: z of the owned blocks (≤ 64 blocks)
+    double* tl = zl + 64 * CHT;                 // staged tiles (TLD layout)
+    // staging: for owned block a: W_a, then L_ba for b = a+1 … ntc−1, as one flat list of tiles
+    // (8 independent loads in flight per thread)
+    int nt = 0;
+    for (int a = rank; a < ntc; a += CS) {
+      const int a0 = a * CHT, an = min(CHT, N - a0);
+      for (int e = tid; e < CHT; e += blockDim.x) zl[(a / CS) * CHT + e] = (e < an) ? __ldcg(M + (int64_t)N + (int64_t)(a0 + e) * ld) : 0.0;
+      nt += ntc - a;
+    }
+    {
+      const int total = nt * CHT * CHT;
+      for (int base = tid; base < total; base += 8 * (int)blockDim.x) {
+        double v[8];
+        int dsti[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int idx = base + u * (int)blockDim.x;
+          v[u] = 0.0;
+          dsti[u] = -1;
+          if (idx < total) {
+            int tt = idx >> 10, e = idx & 1023;
+            // tile tt → (a, b): walk the owned blocks
+            int a = rank;
+            while (tt >= ntc - a) {
+              tt -= ntc - a;
+              a += CS;
+            }
+            const int b = a + tt;  // tt = 0 → W_a
+            const int r = e & 31, c = e >> 5;
+            const int ti = idx >> 10;
+            if (b == a) {
+              v[u] = __ldcg(Winv + (size_t)a * CHT * CHT + (size_t)c * CHT + r);  // W_a[c][r]
+              dsti[u] = ti * CHT * TLD + c * TLD + r;
+            } else {
+              const int row = b * CHT + r;
+              v[u] = (row < N) ? __ldcg(M + (int64_t)row + (int64_t)(a * CHT + c) * ld) : 0.0;
+              dsti[u] = ti * CHT * TLD + r * TLD + c;
+            }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (dsti[u] >= 0) tl[dsti[u]] = v[u];
+      }
+    }
+    __syncthreads();
+    STAMP(41);
+    // tile index of (b, a) for owned a: block offset of a + 1 + (b − a − 1)
+    auto tile_of = [&](int a, int b) {
+      int off = 0;
+      for (int a2 = rank; a2 < a; a2 += CS) off += ntc - a2;
+      return tl + (size_t)(off + (b - a)) * CHT * TLD;  // b == a → W_a
+    };
+    for (int b = ntc - 1; b >= 0; --b) {
+      const int b0 = b * CHT, bn = min(CHT, N - b0);
+      if (b % CS == rank && warp == 0) {  // v_b = W_bᵀ z_b, broadcast to every CTA
+        const double* Wt = tile_of(b, b);
+        const double* zb = zl + (b / CS) * CHT;
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+        for (int r = 0; r < CHT; r += 4) {
+          s0 = fma(Wt[r * TLD + lane], zb[r], s0);
+          s1 = fma(Wt[(r + 1) * TLD + lane], zb[r + 1], s1);
+          s2 = fma(Wt[(r + 2) * TLD + lane], zb[r + 2], s2);
+          s3 = fma(Wt[(r + 3) * TLD + lane], zb[r + 3], s3);
+        }
+        const double v = (lane < bn) ? (s0 + s1) + (s2 + s3) : 0.0;
+        for (int q = 0; q < CS; ++q) cl.map_shared_rank(vfull, q)[b0 + lane] = v;
+      }
+      cl.sync();
+      // z_a −= L_baᵀ v_b for owned a < b (one warp per owned block)
+      int ia = 0;
+      for (int a = rank; a < b; a += CS, ++ia) {
+        if (warp != ia) continue;
+        const double* Tt = tile_of(a, b);
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+        for (int r = 0; r < CHT; r += 4) {
+          s0 = fma(Tt[r * TLD + lane], vfull[b0 + r], s0);
+          s1 = fma(Tt[(r + 1) * TLD + lane], vfull[b0 + r + 1], s1);
+          s2 = fma(Tt[(r + 2) * TLD + lane], vfull[b0 + r + 2], s2);
+          s3 = fma(Tt[(r + 3) * TLD + lane], vfull[b0 + r + 3], s3);
+        }
+        zl[(a / CS) * CHT + lane] -= (s0 + s1) + (s2 + s3);
+      }
+      __syncthreads();
+    }
+    STAMP(42);
+    if (rank != 0) return;
+    double* zv = vfull;
+    __shared__ double redc[8];
+    double dot = 0.0;
+    for (int i = tid; i < N; i += blockDim.x) {
+      const double v = scale * zv[i];
+      out[i] = v;
+      if (yt) yt[i] = __dadd_rn(ybase[i], __dmul_rn(1.0, v));  // Armijo trial y + d (m × m branch)
+      if (dotv) dot += dotv[i] * v;
+    }
+    if (dotv) {
+      dot = warp_allsum(dot);
+      if (lane == 0) redc[warp] = dot;
+      __syncthreads();
+      if (tid == 0) {
+        double sacc = 0.0;
+        for (int wi = 0; wi < 8; ++wi) sacc += redc[wi];
+        *dot_out = sacc;
+      }
+    }
+    return;
+  }
+  if (rank != 0) return;
   double* zv = dsm;                          // N doubles (N ≤ 1024)
   double* Wring = dsm + 1024;                // kBwdRing × 32 × 32 doubles
   double* Tw = Wring + kBwdRing * CHT * CHT;  // 8 warps × 32 × TLD transpose tiles
@@ -847,11 +1067,6 @@ __global__ void __launch_bounds__(256, 1) k_chol_cluster(double* M, int N, int N
   }
 }
 
-// dynamic shared memory of k_chol_cluster (bytes): factorisation operands, or in the backward
-// solve z (1024) + the W ring
-constexpr size_t kCholSmemFact = (size_t)(8 * 2 * CHT * TLD + 3 * CHT * TLD + kDiagScratch) * sizeof(double);
-constexpr size_t kCholSmemBwd = (size_t)(1024 + kBwdRing * CHT * CHT + 8 * CHT * TLD) * sizeof(double);
-constexpr size_t kCholSmem = kCholSmemFact > kCholSmemBwd ? kCholSmemFact : kCholSmemBwd;
 
 // y ← y + s·d  (m-vector) and small helpers
 __global__ void k_axpy_m(int64_t m, const double* y, double s, const double* d, double* out, const double* sp) {

@@ -289,6 +289,7 @@ struct ssnal_en_problem {
   double* W = nullptr;
   int W_splits = 0;
   int* info = nullptr;
+  int* kflag = nullptr;  // K4 W-ready flags (one per panel)
   EvalOut* ev_dev = nullptr;   // slots
   EvalOut* ev_host = nullptr;  // mapped pinned mirror (GPU writes it directly)
   EvalOut* ev_host_dev = nullptr;  // device alias of ev_host
@@ -507,6 +508,7 @@ int allocate(ssnal_en_problem* P) {
   d.add((void**)&P->cg_parts, (size_t)P->nsm * m * 8);
   d.add((void**)&P->cg_scal, (size_t)P->nsm * 2 * 8 + 64);
   d.add((void**)&P->ctl, sizeof(DevCtl));
+  d.add((void**)&P->kflag, 256 * sizeof(int));
   P->arena = pool_alloc(d.total);
   if (!P->arena) {
     set_err("device allocation of %zu bytes failed", d.total);
@@ -726,7 +728,7 @@ int launch_chol_ex(ssnal_en_problem* P, double* M, int N, int NR, int ld, double
   cfg.numAttrs = 1;
   const DirGeo* nog = nullptr;
   CK(cudaLaunchKernelEx(&cfg, k_chol_cluster, M, N, NR, ld, out, scale, dotv, dot_out, P->Winv, info, ybase, yt, nog,
-                        0));
+                        0, P->kflag));
   P->launches++;
   return SSNAL_OK;
 }
@@ -748,7 +750,7 @@ int launch_chol(ssnal_en_problem* P, double* M, int N, double* out, double scale
   cfg.attrs = at;
   cfg.numAttrs = 1;
   CK(cudaLaunchKernelEx(&cfg, k_chol_cluster, M, N, N + 1, N + 1, out, scale, dotv, dot_out, P->Winv, P->info,
-                        ybase, yt, geo, want));
+                        ybase, yt, geo, want, P->kflag));
   P->launches++;
   return SSNAL_OK;
 }

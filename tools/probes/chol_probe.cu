@@ -53,7 +53,7 @@ int main() {
     for (int j = 0; j < N; ++j) for (int i = 0; i < ld; ++i) h[i + (size_t)j * ld] = (i == j) ? N + 1.0 : ((i < N) ? 0.01 * ((i * 7 + j * 13) % 11) : 1.0);
     for (int j = 0; j < N; ++j) for (int i = 0; i < N; ++i) h[i + (size_t)j * ld] = h[(i > j ? i : j) + (size_t)(i > j ? j : i) * ld];
     double *dM, *dout, *dW, *dd; int* info; unsigned long long* dt;
-    cudaMalloc(&dM, (h.size() + 4096) * 8); cudaMalloc(&dout, N * 8); cudaMalloc(&dW, 33 * 32 * 8 * ((N + 31) / 32)); cudaMalloc(&info, 4); cudaMalloc(&dt, 64 * 8); cudaMalloc(&dd, 8);
+    cudaMalloc(&dM, (h.size() + 4096) * 8); cudaMalloc(&dout, N * 8); cudaMalloc(&dW, 33 * 32 * 8 * ((N + 31) / 32)); cudaMalloc(&info, 4); cudaMalloc(&dt, 64 * 8); cudaMalloc(&dd, 8); int* kf; cudaMalloc(&kf, 1024); cudaMemset(kf, 0, 1024);
     size_t smem = kCholSmem;
     cudaFuncSetAttribute(k_chol_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(k_chol_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -67,7 +67,7 @@ int main() {
       for (int rep = 0; rep < 5; ++rep) {
         cudaMemcpy(dM, h.data(), h.size() * 8, cudaMemcpyHostToDevice);
         cudaEventRecord(e0);
-        cudaLaunchKernelEx(&cfg, k_chol_cluster, dM, N, N + 1, ld, dout, 1.0, (const double*)nullptr, (double*)nullptr, dW, info, (const double*)nullptr, (double*)nullptr, (const DirGeo*)nullptr, 0);
+        cudaLaunchKernelEx(&cfg, k_chol_cluster, dM, N, N + 1, ld, dout, 1.0, (const double*)nullptr, (double*)nullptr, dW, info, (const double*)nullptr, (double*)nullptr, (const DirGeo*)nullptr, 0, kf);
         cudaEventRecord(e1); cudaEventSynchronize(e1);
         float ms; cudaEventElapsedTime(&ms, e0, e1); if (ms < best) best = ms;
       }
