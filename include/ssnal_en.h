@@ -62,6 +62,10 @@ typedef struct {
   double k1_time_s;        /* Σ device time of K1 launches (option time_k1 = 1), else 0   */
   int32_t k1_launches;     /* K1 launches timed                                           */
   int32_t reserved;
+  double primal_viol;      /* option certify=1: max_i v_i of the KKT inclusion c = Aᵀ(b − Ax) − λ2x ∈
+                              λ1∂‖x‖₁ over ALL n columns (v_i = |c_i − λ1 sign x_i| on the support, else
+                              (|c_i| − λ1)₊); one extra Aᵀ pass after the solve, outside time_device_s.
+                              NaN when certify = 0. */
 } ssnal_en_stats;
 
 /* Copy A (host, column-major m × n) and b (host, m) to the current device; the handle owns
@@ -100,6 +104,7 @@ double ssnal_en_lambda_max_l1(const ssnal_en_problem* p);
  *   time_k1=0 (1: time every K1 launch → stats.k1_time_s; CUDA events in host-driven mode,
  *     in-kernel %globaltimer stamps inside the graph),
  *   cluster_size=0 (auto: 16 if the device allows, else 8),
+ *   certify=0 (1: after each solve compute stats.primal_viol with one extra Aᵀ pass),
  *   graph=1 (Algorithm 1 control on the device, the whole solve one CUDA graph; 0: host-driven
  *     control with one evaluation record read per ψ evaluation — identical results),
  *   Newton-system strategy (Algorithm 1 step (1); reading R32): conjugate gradient

@@ -237,6 +237,35 @@ __global__ void k_objective(int64_t m, const double* resid, const double* Px, co
   }
 }
 
+// KKT certificate: with w = Aᵀ(Ax − b), c_i = −w_i − λ2 x_i and
+// v_i = |c_i − λ1 sign x_i| (x_i ≠ 0) or (|c_i| − λ1)₊; per-block max → out[blockIdx] (max is exact).
+__global__ void __launch_bounds__(256) k_kkt_viol(int64_t n, const double* __restrict__ w, const double* __restrict__ x,
+                                                  double l1, double l2, double* out) {
+  __shared__ double red[8];
+  double v = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double xi = x[i];
+    const double c = -w[i] - l2 * xi;
+    const double vi = xi > 0.0 ? fabs(c - l1) : (xi < 0.0 ? fabs(c + l1) : fmax(fabs(c) - l1, 0.0));
+    v = fmax(v, vi);
+  }
+  v = warp_allmax(v);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = red[0];
+    for (int q = 1; q < 8; ++q) m = fmax(m, red[q]);
+    out[blockIdx.x] = m;
+  }
+}
+
+__global__ void k_max_reduce(const double* in, int cnt, double* out) {
+  double v = 0.0;
+  for (int q = threadIdx.x; q < cnt; q += 32) v = fmax(v, in[q]);
+  v = warp_allmax(v);
+  if (threadIdx.x == 0) *out = v;
+}
+
 }  // namespace
 
 // ===========================================================================
@@ -308,7 +337,7 @@ struct ssnal_en_problem {
   double lambda_max = 0, nb = 0;
   // options
   double sigma_factor = 5.0, sigma_max = 1e8, mu = 0.2, beta = 0.5;
-  int max_outer = 100, max_inner = 100, max_bt = 50, init_mode = 1, time_k1 = 0;
+  int max_outer = 100, max_inner = 100, max_bt = 50, init_mode = 1, time_k1 = 0, certify = 0;
   double cg_ratio = 0.0, cg_threshold = 1e4, cg_tol = 1e-10;  // Newton strategy (R32)
   int cg_maxit = 1000;
   // counters for the current call
@@ -1616,6 +1645,7 @@ int ssnal_en_set_option(ssnal_en_problem* P, const char* key, double v) {
   else if (k == "max_backtracks" && v >= 0) P->max_bt = (int)v;
   else if (k == "init_mode" && (v == 0 || v == 1)) P->init_mode = (int)v;
   else if (k == "time_k1") P->time_k1 = v != 0;
+  else if (k == "certify" && (v == 0 || v == 1)) P->certify = (int)v;
   else if (k == "graph" && (v == 0 || v == 1)) P->use_graph = (int)v;
   else if (k == "cg_ratio" && v >= 0) P->cg_ratio = v;
   else if (k == "cg_threshold" && v >= 0) P->cg_threshold = v;
@@ -1677,6 +1707,21 @@ static int solve_wrapped(ssnal_en_problem* P, double l1, double l2, double sigma
   CK(cudaStreamSynchronize(P->st));
   harvest_k1(P);
   finish_stats(P, &S);
+  S.primal_viol = NAN;
+  if (P->certify) {  // one extra Aᵀ pass at Ax − b (tmpm holds it from the objective), outside TTS
+    const int keep = P->time_k1;
+    P->time_k1 = 0;
+    rc = launch_k1(P, P->tmpm, nullptr, make_scal(1.0, 0.0, 0.0), 0, P->w[2]);
+    P->time_k1 = keep;
+    if (rc) return rc;
+    const int nb = 2 * P->nsm;  // block maxima into cg_scal (2·nsm + 8 doubles)
+    k_kkt_viol<<<nb, 256, 0, P->st>>>(P->n, P->w[2], P->x, P->stat_l1, P->stat_l2, P->cg_scal);
+    k_max_reduce<<<1, 32, 0, P->st>>>(P->cg_scal, nb, P->scratch + 40);
+    CKL();
+    CK(cudaMemcpyAsync(P->scratch_host + 42, P->scratch + 40, 8, cudaMemcpyDeviceToHost, P->st));
+    CK(cudaStreamSynchronize(P->st));
+    S.primal_viol = P->scratch_host[42];
+  }
   float ms = 0;
   cudaEventElapsedTime(&ms, e0, e1);
   S.time_device_s = ms * 1e-3;

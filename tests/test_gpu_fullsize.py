@@ -123,10 +123,15 @@ def test_solve_fullsize_properties(name):
         assert st["gap"] >= -1e-9 * abs(st["primal_obj"])
         v, _ = kkt_sampled(cfg, b, x, l1, l2, 5)
         assert v <= 1e-3 * l1, (c, v / l1)
-        # tight tolerance: the KKT inclusion holds to 1e-7 λ1 on every checked column
+        # tight tolerance: the KKT inclusion holds to 1e-7 λ1 on every checked column, and on ALL n
+        # columns per the GPU's own certificate (option certify: one extra Aᵀ pass)
+        P.set_option("certify", 1)
         xt, stt = P.solve(l1, l2, cfg.sigma0, 1e-10, x0=x)
+        P.set_option("certify", 0)
+        assert stt["primal_viol"] <= 1e-7 * l1, (c, stt["primal_viol"] / l1)
         vt, res = kkt_sampled(cfg, b, xt, l1, l2, 6)
         assert vt <= 1e-7 * l1, (c, vt / l1)
+        assert vt <= stt["primal_viol"] * (1 + 1e-6) + 1e-12 * l1  # the sample cannot exceed the max
         # the GPU's objective report agrees with the host evaluation from regenerated columns
         F = 0.5 * res @ res + l1 * np.abs(xt).sum() + 0.5 * l2 * xt @ xt
         assert stt["primal_obj"] == pytest.approx(F, rel=1e-11)

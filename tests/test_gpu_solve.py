@@ -170,3 +170,23 @@ def test_solve_edge_shapes(case):
     check_parity(xc, stc, xg, stg, A, b, l1, l2, f"edge {case}")
     assert stg["outer_iters"] == stc["outer_iters"]
     assert stg["branch_steps"][2] == stc["branch_steps"][2] or abs(stg["newton_iters"] - stc["newton_iters"]) <= 1
+
+
+@pytest.mark.parametrize("name,n", [("cfg1", None), ("cfg3", 20_000)])
+def test_certify_primal_violation(name, n):
+    """Option certify: stats.primal_viol = max_i v_i over all n columns (one extra Aᵀ pass), against the
+    oracle's definition of the KKT-inclusion violation at the GPU's own x; NaN without the option."""
+    cfg = synth.CONFIGS[name] if n is None else synth.scaled(synth.CONFIGS[name], n=n)
+    A = synth.design(cfg)
+    b, _ = synth.response(cfg)
+    lm = float(np.max(np.abs(oracle.aty(A, b))))
+    l1, l2 = lambdas(cfg, lm, cfg.cs[0])
+    with Problem(A, b) as P:
+        x, st = P.solve(l1, l2, cfg.sigma0, cfg.tol)
+        assert np.isnan(st["primal_viol"])
+        P.set_option("certify", 1)
+        for tol in (cfg.tol, 1e-10):
+            x, st = P.solve(l1, l2, cfg.sigma0, tol)
+            ref = oracle.kkt_violation(A, b, x, l1, l2)
+            assert st["primal_viol"] == pytest.approx(ref, rel=1e-6, abs=1e-12 * l1)
+        assert st["primal_viol"] <= 1e-7 * l1
