@@ -411,6 +411,29 @@ SSN_DEV void dmma(double (&d)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
+// One warp's 8 × 32 strip of a 32 × 32 × 32 product: acc[cb] += sgn · Σ_p SA[8w + g][p] SB[8cb + ·][p].
+// DMMA latency is ~270 cycles (tools/probes/mma_probe), so the K loop is split over 4 accumulator
+// groups (16 independent chains instead of 4), summed at the end.
+SSN_DEV void strip_mma(const double* SA, const double* SB, double (&acc)[4][2], double sgn, int w, int lane) {
+  const int g = lane >> 2, t = lane & 3;
+  double part[4][4][2];
+#pragma unroll
+  for (int h = 0; h < 4; ++h)
+#pragma unroll
+    for (int cb = 0; cb < 4; ++cb) part[h][cb][0] = part[h][cb][1] = 0.0;
+#pragma unroll
+  for (int kk = 0; kk < 8; ++kk) {
+    const int h = kk & 3;
+    const double af = sgn * SA[(8 * w + g) * TLD + 4 * kk + t];
+#pragma unroll
+    for (int cb = 0; cb < 4; ++cb) dmma(part[h][cb], af, SB[(8 * cb + g) * TLD + 4 * kk + t]);
+  }
+#pragma unroll
+  for (int cb = 0; cb < 4; ++cb)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) acc[cb][e] += (part[0][cb][e] + part[1][cb][e]) + (part[2][cb][e] + part[3][cb][e]);
+}
+
 // acc[rb][cb] += sgn · Σ_p SA[r][p] · SB[c][p] over a 32 × 32 × 32 tile (rows r = 8rb + lane/4,
 // cols c = 8cb + 2(lane%4) + e in the C fragment layout of m8n8k4).
 SSN_DEV void tile_mma(const double* SA, const double* SB, double (&acc)[4][4][2], double sgn, int lane) {
@@ -632,8 +655,9 @@ SSN_DEV void backward_solve(const double* M, int ld, int N, const double* Winv, 
 
 // dynamic shared memory of k_chol_cluster (bytes): factorisation operands, or in the backward
 // solve z (1024) + the W ring
+constexpr int kQuadTiles = 7 + kColSlots;  // per quad: 2 stages × (L_ik, L_jk, A_ij), W_{k+1}, slots
 constexpr size_t kCholSmemFact =
-    (size_t)(2 * (3 + kColSlots) * CHT * TLD + 2 * CHT * TLD + kDiagScratch) * sizeof(double);
+    (size_t)(2 * kQuadTiles * CHT * TLD + 2 * CHT * TLD + kDiagScratch) * sizeof(double);
 constexpr size_t kCholSmemBwd = (size_t)(1024 + kBwdRing * CHT * CHT + 8 * CHT * TLD) * sizeof(double);
 constexpr size_t kCholSmem = kCholSmemFact > kCholSmemBwd ? kCholSmemFact : kCholSmemBwd;
 
@@ -659,12 +683,11 @@ __global__ void __launch_bounds__(256, 1) k_chol_cluster(double* M, int N, int N
   const int quad = warp >> 2, qw = warp & 3;
   const int g = lane >> 2, t = lane & 3;
   // smem: per quad [SA, SB, Wq, slots × kColSlots] (tiles 32 × TLD); CTA 0 adds T2, T3, scratch
-  double* QB = dsm + (size_t)quad * (3 + kColSlots) * CHT * TLD;
-  double* SA = QB;                       // L_ik rows of the tile being updated
-  double* SB = QB + CHT * TLD;           // L_jk rows
-  double* Wq = QB + 2 * CHT * TLD;       // W_{k+1} for this quad's TRSMs
-  double* slots = QB + 3 * CHT * TLD;    // updated column-(k+1) tiles awaiting W_{k+1}
-  double* T2 = dsm + (size_t)2 * (3 + kColSlots) * CHT * TLD;  // CTA-0 diagonal tile
+  double* QB = dsm + (size_t)quad * kQuadTiles * CHT * TLD;
+  double* SA = QB;                       // stage s: QB + 3s tiles = L_ik, + 1 = L_jk, + 2 = A_ij
+  double* Wq = QB + 6 * CHT * TLD;       // W_{k+1} for this quad's TRSMs
+  double* slots = QB + 7 * CHT * TLD;    // updated column-(k+1) tiles awaiting W_{k+1}
+  double* T2 = dsm + (size_t)2 * kQuadTiles * CHT * TLD;  // CTA-0 diagonal tile
   double* T3 = T2 + CHT * TLD;                                  // CTA-0: L_{k+1,k}
   double* dscr = T3 + CHT * TLD;                                // diag_factor4 scratch
   const int ntc = (N + CHT - 1) / CHT, ntr = (NR + CHT - 1) / CHT;
@@ -718,12 +741,7 @@ __global__ void __launch_bounds__(256, 1) k_chol_cluster(double* M, int N, int N
             acc[cb][e] = (r < NR && c < N) ? __ldcg(M + (int64_t)r + (int64_t)c * ld) : 0.0;
           }
         asm volatile("bar.sync 2, 128;" ::: "memory");
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          const double af = -T3[(8 * qw + g) * TLD + 4 * kk + t];
-#pragma unroll
-          for (int cb = 0; cb < 4; ++cb) dmma(acc[cb], af, T3[(8 * cb + g) * TLD + 4 * kk + t]);
-        }
+        strip_mma(T3, T3, acc, -1.0, qw, lane);
 #pragma unroll
         for (int cb = 0; cb < 4; ++cb)
 #pragma unroll
@@ -749,8 +767,8 @@ __global__ void __launch_bounds__(256, 1) k_chol_cluster(double* M, int N, int N
       const int ntri = remc > 0 ? remc * (remc + 1) / 2 : 0;
       const int ntrail = (k >= 0 && remc > 0) ? ntri + (remr - remc) * remc : 0;
       int nslot = 0;
-      // job q → tile (i0, j0); column jobs (q < ncol) first.  Software-pipelined: the operands of
-      // job q + NQ are loaded into registers while job q computes.
+      // job q → tile (i0, j0); column jobs (q < ncol) first.  The three operand tiles of job q + NQ
+      // stream global → smem with cp.async (no register staging) while job q computes; two stages.
       auto job_tile = [&](int q, int& i0, int& j0) {
         if (q < ncol) {
           i0 = (k + 2 + q) * CHT;
@@ -768,64 +786,65 @@ __global__ void __launch_bounds__(256, 1) k_chol_cluster(double* M, int N, int N
           j0 = (k + 2 + jj) * CHT;
         }
       };
-      double va[8], vb[8], acc[4][2];
-      auto fetch = [&](int q) {  // A_ij fragment + this thread's rows of L_ik, L_jk
-        int i0, j0;
-        job_tile(q, i0, j0);
-        const int r = i0 + 8 * qw + g;
-#pragma unroll
-        for (int cb = 0; cb < 4; ++cb)
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int c = j0 + 8 * cb + 2 * t + e;
-            acc[cb][e] = (r < NR && c < N) ? __ldcg(M + (int64_t)r + (int64_t)c * ld) : 0.0;
-          }
-        if (k >= 0) {  // coalesced: lane = row, warp qw takes columns 8qw .. 8qw+7 of both tiles
-          const bool ra = i0 + lane < NR, rb = j0 + lane < N;
-          const double* sa = M + (int64_t)(k0 + 8 * qw) * ld + (ra ? i0 + lane : 0);
-          const double* sb = M + (int64_t)(k0 + 8 * qw) * ld + (rb ? j0 + lane : 0);
-#pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            va[e] = (ra && 8 * qw + e < kn) ? __ldcg(sa + e * ld) : 0.0;
-            vb[e] = (rb && 8 * qw + e < kn) ? __ldcg(sb + e * ld) : 0.0;
-          }
+      const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(SA);
+      auto cp8 = [&](double* dst, const double* src, bool ok) {  // 8-byte async copy or a zero
+        if (ok) {
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+                       "l"(src)
+                       : "memory");
+        } else {
+          *dst = 0.0;
         }
       };
+      (void)sbase;
+      // issue: lane = row, warp qw takes columns 8qw .. 8qw+7 of the three tiles
+      auto issue = [&](int q, int st) {
+        int i0, j0;
+        job_tile(q, i0, j0);
+        double* tA = SA + (size_t)(3 * st) * CHT * TLD;
+        double* tB = tA + CHT * TLD;
+        double* tC = tB + CHT * TLD;
+        const bool ra = i0 + lane < NR, rb = j0 + lane < N;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const int c = 8 * qw + e;
+          cp8(tC + lane * TLD + c, M + (int64_t)(j0 + c) * ld + i0 + lane, ra && j0 + c < N);
+          if (k >= 0) {
+            cp8(tA + lane * TLD + c, M + (int64_t)(k0 + c) * ld + i0 + lane, ra && c < kn);
+            cp8(tB + lane * TLD + c, M + (int64_t)(k0 + c) * ld + j0 + lane, rb && c < kn);
+          }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+      };
+      const int njobs = ncol + ntrail;
+      if (gq < njobs) issue(gq, 0);
       if (k == 1) STAMPW(50);
-      if (gq < ncol + ntrail) fetch(gq);
+      int st = 0;
 #pragma unroll 1
-      for (int q = gq; q < ncol + ntrail; q += NQ) {
+      for (int q = gq; q < njobs; q += NQ, st ^= 1) {
         int i0, j0;
         job_tile(q, i0, j0);
         const bool colj = q < ncol;
-        double cur[4][2];
-#pragma unroll
-        for (int cb = 0; cb < 4; ++cb) cur[cb][0] = acc[cb][0], cur[cb][1] = acc[cb][1];
-        if (k >= 0) {
-#pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            SA[lane * TLD + 8 * qw + e] = va[e];
-            SB[lane * TLD + 8 * qw + e] = vb[e];
-          }
+        if (q + NQ < njobs) {
+          issue(q + NQ, st ^ 1);
+          asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+          asm volatile("cp.async.wait_group 0;" ::: "memory");
         }
         asm volatile("bar.sync %0, 128;" ::"r"(qbar) : "memory");
         if (k == 1 && q == gq) STAMPW(51);
-#if defined(CHOL_EXPERIMENT) && CHOL_EXPERIMENT == 2
-        if (false)
-#endif
-        if (q + NQ < ncol + ntrail) fetch(q + NQ);  // next job's loads in flight during the DMMAs
-        if (k == 1 && q == gq) STAMPW(52);
+        const double* tA = SA + (size_t)(3 * st) * CHT * TLD;
+        const double* tB = tA + CHT * TLD;
+        const double* tC = tB + CHT * TLD;
+        double cur[4][2];
+#pragma unroll
+        for (int cb = 0; cb < 4; ++cb)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) cur[cb][e] = tC[(8 * qw + g) * TLD + 8 * cb + 2 * t + e];
 #if defined(CHOL_EXPERIMENT) && CHOL_EXPERIMENT == 1
         if (false)
 #endif
-        if (k >= 0) {
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk) {
-            const double af = -SA[(8 * qw + g) * TLD + 4 * kk + t];
-#pragma unroll
-            for (int cb = 0; cb < 4; ++cb) dmma(cur[cb], af, SB[(8 * cb + g) * TLD + 4 * kk + t]);
-          }
-        }
+        if (k >= 0) strip_mma(tA, tB, cur, -1.0, qw, lane);
         if (k == 1 && q == gq) STAMPW(53);
         // column tiles beyond the slots (small clusters, many appended rows) go back to M in place
         double* dst = (colj && nslot < kColSlots) ? slots + (size_t)nslot * CHT * TLD : nullptr;
@@ -846,7 +865,7 @@ __global__ void __launch_bounds__(256, 1) k_chol_cluster(double* M, int N, int N
               if (r < NR && c < N && (i0 != j0 || cl_ <= rl)) M[(int64_t)r + (int64_t)c * ld] = cur[cb][e];
             }
         }
-        asm volatile("bar.sync %0, 128;" ::"r"(qbar) : "memory");  // SA/SB reuse
+        asm volatile("bar.sync %0, 128;" ::"r"(qbar) : "memory");  // stage reuse
         if (k == 1 && q == gq) STAMPW(54);
         if (k == 1 && q == gq + NQ) STAMPW(55);
       }
@@ -894,12 +913,7 @@ __global__ void __launch_bounds__(256, 1) k_chol_cluster(double* M, int N, int N
           double acc[4][2];
 #pragma unroll
           for (int cb = 0; cb < 4; ++cb) acc[cb][0] = acc[cb][1] = 0.0;
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk) {
-            const double af = src[(8 * qw + g) * TLD + 4 * kk + t];
-#pragma unroll
-            for (int cb = 0; cb < 4; ++cb) dmma(acc[cb], af, Wq[(8 * cb + g) * TLD + 4 * kk + t]);
-          }
+          strip_mma(src, Wq, acc, 1.0, qw, lane);
           const int r = r0 + 8 * qw + g;
 #pragma unroll
           for (int cb = 0; cb < 4; ++cb)
