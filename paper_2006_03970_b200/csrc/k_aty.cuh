@@ -742,11 +742,12 @@ __global__ void __launch_bounds__(K5_THREADS) k_eval_reduce(int64_t m, const dou
                                                             EvalOut* out, double* blk, unsigned* ticket,
                                                             const double* gd_src, const int* info_src,
                                                             EvalOut* host_out, unsigned long long seq,
-                                                            const Scal* scp, const int* pred) {
+                                                            const Scal* scp, const int* pred, const double* nbp) {
   __shared__ double red[8][33];
   __shared__ bool last;
   if (pred && *pred == 0) return;  // graph mode: predicated off (uniform over the grid)
   if (scp) sc = *scp;
+  if (nbp) nb = *nbp;  // graph mode: ‖b‖ from the control block (the graph may predate it)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t k = (int64_t)blockIdx.x * 32 + lane;
   if (with_grad) {

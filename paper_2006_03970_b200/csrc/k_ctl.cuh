@@ -22,6 +22,7 @@ struct DevCtl {
   // per-solve settings (host-written before the graph launch)
   double l1, l2, tol, sigma, sigma_factor, sigma_max, mu, beta;
   double cg_ratio, cg_threshold;  // Newton strategy (R32)
+  double nb;                      // ‖b‖ (res1 denominator, Eq. (15))
   int max_outer, max_inner, max_bt, pad0;
   // state
   Scal sc;           // σ-dependent scalars of the current outer iteration

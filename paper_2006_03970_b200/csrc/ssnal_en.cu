@@ -705,7 +705,8 @@ int launch_eval(ssnal_en_problem* P, const double* y, const Scal& sc, int with_g
   k_eval_reduce<<<nblk, K5_THREADS, 0, P->st>>>(P->m, y, P->b, P->part_vec, valid, nparts, P->part_scal, P->G, sc,
                                                  P->nb, with_grad, g_out, r_dev, P->ev_dev + slot, P->blk,
                                                  P->ticket, gd_src, info_src,
-                                                 P->capturing ? nullptr : P->ev_host_dev + slot, P->ev_seq, scp, pred);
+                                                 P->capturing ? nullptr : P->ev_host_dev + slot, P->ev_seq, scp, pred,
+                                                 P->capturing ? &P->ctl->nb : nullptr);
   P->launches++;
   CKL();
   return SSNAL_OK;
@@ -1290,6 +1291,9 @@ int build_graph(ssnal_en_problem* P) {
       set_err("cudaGraphInstantiate: %s", cudaGetErrorString(e));
       rc = SSNAL_ECUDA;
       P->gexec = nullptr;
+    } else if ((e = cudaGraphUpload(P->gexec, P->st)) != cudaSuccess) {  // device-side setup off the first solve
+      set_err("cudaGraphUpload: %s", cudaGetErrorString(e));
+      rc = SSNAL_ECUDA;
     }
   }
   if (rc) {
@@ -1332,6 +1336,7 @@ int solve_graph_core(ssnal_en_problem* P, double l1, double l2, double sigma0, d
   h->max_bt = P->max_bt;
   h->cg_ratio = P->cg_ratio;
   h->cg_threshold = P->cg_threshold;
+  h->nb = P->nb;
   h->tstamp[0] = ~0ull;
   h->tstamp[1] = 0ull;
   CK(cudaMemcpyAsync(P->ctl, h, sizeof(DevCtl), cudaMemcpyHostToDevice, P->st));
@@ -1405,6 +1410,9 @@ static int create_common(ssnal_en_problem* P) {
   if (rc) return rc;
   rc = allocate(P);
   if (rc) return rc;
+  // Capture + instantiate the solve graph now: host work that overlaps the asynchronous upload of A
+  // (ssnal_en_create with pinned input) instead of delaying the first solve.
+  if (P->use_graph && (rc = build_graph(P))) return rc;
   // validate inputs on the device
   CK(cudaMemsetAsync(P->flags, 0, 8, P->st));
   if (P->fmt)
@@ -1490,8 +1498,9 @@ int ssnal_en_create(const double* A_colmajor, const double* b, int64_t m, int64_
     delete P;
     return SSNAL_ECUDA;
   }
-  if (cudaMemcpy(P->A_own, A_colmajor, (size_t)m * n * 8, cudaMemcpyHostToDevice) != cudaSuccess ||
-      cudaMemcpy(P->b_own, b, (size_t)m * 8, cudaMemcpyHostToDevice) != cudaSuccess) {
+  // asynchronous for pinned input (overlaps the graph build in create_common); staged otherwise
+  if (cudaMemcpyAsync(P->A_own, A_colmajor, (size_t)m * n * 8, cudaMemcpyHostToDevice, 0) != cudaSuccess ||
+      cudaMemcpyAsync(P->b_own, b, (size_t)m * 8, cudaMemcpyHostToDevice, 0) != cudaSuccess) {
     set_err("H2D copy failed");
     destroy_bufs(P);
     delete P;
@@ -1606,9 +1615,9 @@ int ssnal_en_create_geno(const uint8_t* codes, int64_t stride, const double* tab
     delete P;
     return SSNAL_ECUDA;
   }
-  if (cudaMemcpy(P->codes_own, codes, (size_t)n * stride, cudaMemcpyHostToDevice) != cudaSuccess ||
-      cudaMemcpy(P->tab_own, tab, (size_t)n * 3 * 8, cudaMemcpyHostToDevice) != cudaSuccess ||
-      cudaMemcpy(P->b_own, b, (size_t)m * 8, cudaMemcpyHostToDevice) != cudaSuccess) {
+  if (cudaMemcpyAsync(P->codes_own, codes, (size_t)n * stride, cudaMemcpyHostToDevice, 0) != cudaSuccess ||
+      cudaMemcpyAsync(P->tab_own, tab, (size_t)n * 3 * 8, cudaMemcpyHostToDevice, 0) != cudaSuccess ||
+      cudaMemcpyAsync(P->b_own, b, (size_t)m * 8, cudaMemcpyHostToDevice, 0) != cudaSuccess) {
     set_err("H2D copy failed");
     destroy_bufs(P);
     delete P;
@@ -1649,8 +1658,13 @@ int ssnal_en_set_option(ssnal_en_problem* P, const char* key, double v) {
   else if (k == "graph" && (v == 0 || v == 1)) P->use_graph = (int)v;
   else if (k == "cg_ratio" && v >= 0) P->cg_ratio = v;
   else if (k == "cg_threshold" && v >= 0) P->cg_threshold = v;
-  else if (k == "cg_tol" && v > 0 && v < 1) P->cg_tol = v;
-  else if (k == "cg_maxit" && v >= 1) P->cg_maxit = (int)v;
+  else if (k == "cg_tol" && v > 0 && v < 1) {
+    P->cg_tol = v;
+    drop_graph(P);  // baked into the captured CG launch
+  } else if (k == "cg_maxit" && v >= 1) {
+    P->cg_maxit = (int)v;
+    drop_graph(P);
+  }
   else if (k == "cluster_size" && (v == 1 || v == 2 || v == 4 || v == 8 || v == 16)) {
     P->cluster = (int)v;
     drop_graph(P);  // the cluster launch configuration is baked into the graph

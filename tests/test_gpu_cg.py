@@ -147,3 +147,26 @@ def test_cg_graph_equals_host():
             for k in ("outer_iters", "newton_iters", "branch_steps", "cg_iters", "backtracks", "res_kkt1",
                       "res_kkt3", "primal_obj"):
                 assert sh[k] == sg[k], (k, sh[k], sg[k])
+
+
+def test_cg_options_after_graph_build():
+    """cg_tol / cg_maxit set after the handle's graph exists still reach the CG kernel (the graph is
+    rebuilt): graph ≡ host with a truncated CG (R32)."""
+    cfg = synth.scaled(synth.CONFIGS["cfg2"], n=20_000)
+    A = synth.design(cfg)
+    b, _ = synth.response(cfg)
+    lm = float(np.max(np.abs(oracle.aty(A, b)))) / cfg.alpha
+    l1, l2 = 0.2 * cfg.alpha * lm, 0.2 * (1 - cfg.alpha) * lm
+    with Problem(A, b) as P:
+        P.set_option("cg_ratio", 1e-9)
+        P.set_option("graph", 1)
+        _, s0 = P.solve(l1, l2, cfg.sigma0, cfg.tol)  # graph built with the default cg options
+        P.set_option("cg_maxit", 3)
+        P.set_option("cg_tol", 1e-6)
+        xg, sg = P.solve(l1, l2, cfg.sigma0, cfg.tol)
+        P.set_option("graph", 0)
+        xh, sh = P.solve(l1, l2, cfg.sigma0, cfg.tol)
+        assert np.array_equal(xh, xg)
+        assert sg["cg_iters"] == sh["cg_iters"] and sg["newton_iters"] == sh["newton_iters"]
+        assert sg["branch_steps"][3] > 0
+        assert sg["cg_iters"] <= 3 * sg["branch_steps"][3] < s0["cg_iters"]
