@@ -61,7 +61,7 @@ typedef struct {
   int64_t kernel_launches; /* kernels launched by this call                              */
   double k1_time_s;        /* Σ device time of K1 launches (option time_k1 = 1), else 0   */
   int32_t k1_launches;     /* K1 launches timed                                           */
-  int32_t reserved;
+  int32_t jitter_retries;  /* Newton steps whose factor was redone with the jitter (R36) */
   double primal_viol;      /* option certify=1: max_i v_i of the KKT inclusion c = Aᵀ(b − Ax) − λ2x ∈
                               λ1∂‖x‖₁ over ALL n columns (v_i = |c_i − λ1 sign x_i| on the support, else
                               (|c_i| − λ1)₊); one extra Aᵀ pass after the solve, outside time_device_s.
@@ -110,6 +110,11 @@ double ssnal_en_lambda_max_l1(const ssnal_en_problem* p);
  *   Newton-system strategy (Algorithm 1 step (1); reading R32): conjugate gradient
  *     when r > cg_ratio·m (cg_ratio=0: off) or min(m, r) > cg_threshold (=1e4), else the
  *     exact branches; cg_tol=1e-10 (stop at ‖V d + ∇ψ‖ ≤ cg_tol‖∇ψ‖), cg_maxit=1000.
+ *   jitter=1e-10 (R36): a non-positive Cholesky pivot redoes that Newton step once from
+ *     the same y with the factored matrix's diagonal scaled by (1 + jitter) — the step is not
+ *     counted, stats.jitter_retries is; a second failure returns SSNAL_ENUMERIC.  0: no retry.
+ *   test_fail_factor=0 (test hook: each solve treats its first N Cholesky factorisations as
+ *     failed, to exercise the retry and SSNAL_ENUMERIC paths),
  *   EINVAL for unknown keys. */
 int ssnal_en_set_option(ssnal_en_problem* p, const char* key, double value);
 
@@ -152,8 +157,9 @@ int ssnal_en_epilogue(ssnal_en_problem* p, const double* w0, const double* w1, d
 /* K2–K4/K6 hook: the Newton direction d (device, m) solving (I_m + κ A_J A_Jᵀ) d = −g for the
  * active set J (device int32, r entries, ascending) and g (device, m): r = 0 → d = −g;
  * 0 < r < m → SMW Eq. (19); r ≥ m → m × m Cholesky Eq. (18); CG (K6) when the cg_* options
- * select it.  *gd_out (host) = gᵀd, *branch_out (host) ∈ {0, 1, 2, 3}.  SSNAL_ENUMERIC if a
- * Cholesky pivot is not positive. */
+ * select it.  *gd_out (host) = gᵀd, *branch_out (host) ∈ {0, 1, 2, 3}.  A non-positive Cholesky
+ * pivot is retried once with the factored matrix's diagonal scaled by (1 + jitter) (option
+ * "jitter", R36); SSNAL_ENUMERIC if the retry fails too (or jitter = 0). */
 int ssnal_en_newton_direction(ssnal_en_problem* p, const int32_t* J, int64_t r, const double* g, double kappa,
                               double* d_out, double* gd_out, int32_t* branch_out);
 

@@ -31,14 +31,14 @@ class Opts(ctypes.Structure):
     _fields_ = [("sigma_factor", _d), ("sigma_max", _d), ("mu", _d), ("beta", _d), ("max_outer", ctypes.c_int32),
                 ("max_inner", ctypes.c_int32), ("max_bt", ctypes.c_int32), ("init_mode", ctypes.c_int32),
                 ("cg_ratio", _d), ("cg_threshold", _d), ("cg_tol", _d), ("cg_maxit", ctypes.c_int32),
-                ("pad", ctypes.c_int32)]
+                ("pad", ctypes.c_int32), ("jitter", _d)]
 
 
 class Stats(ctypes.Structure):
     _fields_ = [("status", ctypes.c_int32), ("outer_iters", ctypes.c_int32), ("newton_iters", ctypes.c_int32),
                 ("backtracks", ctypes.c_int32), ("aty_passes", ctypes.c_int32),
                 ("branch_steps", ctypes.c_int32 * 4), ("line_search_stalled", ctypes.c_int32),
-                ("cg_iters", ctypes.c_int32), ("active", ctypes.c_int64), ("res_kkt1", _d), ("res_kkt3", _d), ("primal_obj", _d),
+                ("cg_iters", ctypes.c_int32), ("jitter_retries", ctypes.c_int32), ("active", ctypes.c_int64), ("res_kkt1", _d), ("res_kkt3", _d), ("primal_obj", _d),
                 ("dual_obj", _d), ("gap", _d), ("sigma_final", _d)]
 
 
@@ -67,7 +67,7 @@ def lib():
             "orc_active_set": (_i64, [_dp, _i64, _d, _d, _lp]),
             "orc_chol": (ctypes.c_int, [_dp, _i64]),
             "orc_chol_solve": (None, [_dp, _i64, _dp]),
-            "orc_newton_direction": (ctypes.c_int, [_dp, _i64, _lp, _i64, _dp, _d, _dp]),
+            "orc_newton_direction": (ctypes.c_int, [_dp, _i64, _lp, _i64, _dp, _d, _d, _dp]),
             "orc_cg_direction": (ctypes.c_int, [_dp, _i64, _lp, _i64, _dp, _d, _d, ctypes.c_int, _dp]),
             "orc_primal_obj": (_d, [_dp, _dp, _i64, _i64, _dp, _d, _d]),
             "orc_dual_obj": (_d, [_dp, _i64, _dp, _dp, _i64, _d, _d]),
@@ -184,13 +184,14 @@ def active_set(t, sigma, l1):
     return J[:r].copy()
 
 
-def newton_direction(A, J, g, kappa):
-    """Eq. (18)/(19): d solving (I + κ A_J A_Jᵀ) d = −g.  Returns (d, branch)."""
+def newton_direction(A, J, g, kappa, jitter=0.0):
+    """Eq. (18)/(19): d solving (I + κ A_J A_Jᵀ) d = −g.  Returns (d, branch).  jitter > 0 scales the
+    factored matrix's diagonal by (1 + jitter) (the retry of S:227, reading R36)."""
     A, m, n, Ap = _A(A)
     J = np.ascontiguousarray(J, dtype=np.int64)
     g, gp = _f64(g)
     d = np.empty(m)
-    br = lib().orc_newton_direction(Ap, m, J.ctypes.data_as(_lp), len(J), gp, kappa, d.ctypes.data_as(_dp))
+    br = lib().orc_newton_direction(Ap, m, J.ctypes.data_as(_lp), len(J), gp, kappa, jitter, d.ctypes.data_as(_dp))
     if br < 0:
         raise FloatingPointError("oracle Cholesky failed")
     return d, br

@@ -215,7 +215,8 @@ void orc_chol_solve(const double* L, i64 N, double* v) {
  * κ = σ/(1+σλ2).  Branch rule (R12): r = 0 → d = −g;
  * 0 < r < m → Sherman–Morrison–Woodbury Eq. (19), factoring κ⁻¹I_r + A_JᵀA_J (R13);
  * r ≥ m → Cholesky of the m × m matrix Eq. (18).  Returns the branch (0,1,2) or −1. */
-int orc_newton_direction(const double* A, i64 m, const i64* J, i64 r, const double* g, double kappa, double* d) {
+int orc_newton_direction(const double* A, i64 m, const i64* J, i64 r, const double* g, double kappa, double jitter,
+                         double* d) {
   if (r == 0) {
     for (i64 k = 0; k < m; ++k) d[k] = -g[k];
     return 0;
@@ -236,6 +237,7 @@ int orc_newton_direction(const double* A, i64 m, const i64* J, i64 r, const doub
     }
     double kinv = 1.0 / kappa;
     for (i64 a = 0; a < r; ++a) M[a + a * r] += kinv;
+    for (i64 a = 0; a < r; ++a) M[a + a * r] += jitter * M[a + a * r]; /* retry (R36) */
     for (i64 a = 0; a < r; ++a) {
       const double* aa = A + J[a] * m;
       double s = 0.0;
@@ -264,6 +266,7 @@ int orc_newton_direction(const double* A, i64 m, const i64* J, i64 r, const doub
       M[l + k * m] = v;
     }
   }
+  for (i64 k = 0; k < m; ++k) M[k + k * m] += jitter * M[k + k * m]; /* retry (R36) */
   if (orc_chol(M, m) != 0) { free(M); return -1; }
   for (i64 k = 0; k < m; ++k) d[k] = -g[k];
   orc_chol_solve(M, m, d);
@@ -381,6 +384,7 @@ typedef struct {
   double cg_tol;       /* CG relative residual (R32)                               */
   int32_t cg_maxit;
   int32_t pad;
+  double jitter;       /* factor retry: diagonal × (1 + jitter) after a non-positive pivot (R36) */
 } orc_opts;
 
 typedef struct {
@@ -389,6 +393,7 @@ typedef struct {
   int32_t branch_steps[4]; /* r = 0, SMW, m × m, CG */
   int32_t line_search_stalled;
   int32_t cg_iters;
+  int32_t jitter_retries;
   int64_t active;
   double res_kkt1, res_kkt3, primal_obj, dual_obj, gap, sigma_final;
 } orc_stats;
@@ -473,6 +478,7 @@ void orc_default_opts(orc_opts* o) {
   o->cg_tol = 1e-10;
   o->cg_maxit = 1000;
   o->pad = 0;
+  o->jitter = 1e-10;
 }
 
 /* SsNAL-EN (Algorithm 1).  x0 may be NULL (cold start).  x_out (n) and y_out (m,
@@ -534,7 +540,11 @@ int orc_solve(const double* A, const double* b, i64 m, i64 n, double l1, double 
         S.cg_iters += orc_cg_direction(A, m, J, ev.r, g, kappa, o.cg_tol, o.cg_maxit, d);
         br = 3;
       } else {
-        br = orc_newton_direction(A, m, J, ev.r, g, kappa, d);
+        br = orc_newton_direction(A, m, J, ev.r, g, kappa, 0.0, d);
+        if (br < 0 && o.jitter > 0.0) { /* one retry with the jittered factor (R36) */
+          S.jitter_retries++;
+          br = orc_newton_direction(A, m, J, ev.r, g, kappa, o.jitter, d);
+        }
       }
       if (br < 0) { numeric = 1; break; }
       S.branch_steps[br]++;

@@ -23,6 +23,7 @@ struct DevCtl {
   double l1, l2, tol, sigma, sigma_factor, sigma_max, mu, beta;
   double cg_ratio, cg_threshold;  // Newton strategy (R32)
   double nb;                      // ‖b‖ (res1 denominator, Eq. (15))
+  double jitter;                  // factor retry scale (R36); 0 = no retry
   int max_outer, max_inner, max_bt, pad0;
   // state
   Scal sc;           // σ-dependent scalars of the current outer iteration
@@ -30,6 +31,8 @@ struct DevCtl {
   double s, gd;      // Armijo step length and gᵀd of the current direction
   int k, j, nbt, need_grad;
   int converged, numeric, numeric_kind, stalled;
+  int retry, skip;   // retry: this step's factor failed once; skip: redo the step (no accept)
+  int inject, pad2;  // test hook: treat the next `inject` factorisations as failed
   DirGeo geo;        // direction geometry for the current r
   // statistics (same meaning as ssnal_en_stats)
   int outer_iters, newton_iters, psi_evals, backtracks, aty_passes, branch_steps[4], cg_iters;
@@ -37,7 +40,7 @@ struct DevCtl {
   double res1, res3, sigma_final;
   long long numeric_r;
   unsigned long long k1_ns;  // Σ K1 durations from the in-kernel globaltimer stamps
-  int k1_cnt, pad1;
+  int k1_cnt, jitter_retries;
   unsigned long long tstamp[2];
 };
 
@@ -80,6 +83,7 @@ SSN_DEV int inner_next(DevCtl* C, const EvalOut* ev0, int64_t m, int nsm, int ws
   const int go = (C->numeric == 0) && (C->j < C->max_inner) && !(ev0->res1 <= C->tol);
   if (go) {
     C->geo = make_geo(ev0->r, m, nsm, wsplits, C->sc.kappa, C->kinv, C->cg_ratio, C->cg_threshold);
+    C->geo.jit = C->retry ? C->jitter : 0.0;
     *info = 0;
   }
   return go;
@@ -114,7 +118,18 @@ __global__ void k_ctl_armijo(DevCtl* C, const EvalOut* ev0, const EvalOut* ev1, 
   C->tstamp[1] = 0ull;
   C->nbt = 0;
   C->s = 1.0;
-  if ((C->geo.branch == 1 || C->geo.branch == 2) && ev1->info != 0) {
+  const bool fac = C->geo.branch == 1 || C->geo.branch == 2;
+  const bool failed = fac && (ev1->info != 0 || C->inject > 0);
+  if (fac && C->inject > 0) C->inject--;
+  if (failed && !C->retry && C->jitter > 0.0) {
+    C->retry = 1;  // redo this step from the same y with the jittered factor (R36)
+    C->skip = 1;
+    C->need_grad = 0;
+    C->jitter_retries++;
+    cudaGraphSetConditional(h_bt, 0);
+    return;
+  }
+  if (failed) {
     C->numeric = 1;
     C->numeric_kind = 1;
     C->numeric_r = C->geo.r;
@@ -147,7 +162,7 @@ __global__ void __launch_bounds__(256) k_accept(DevCtl* C, int64_t m, int64_t n,
                                                 const double* __restrict__ P1, int64_t* r_dev,
                                                 double* __restrict__ w0, const double* __restrict__ w1,
                                                 const double* __restrict__ w2, EvalOut* ev) {
-  if (C->numeric) return;
+  if (C->numeric || C->skip) return;
   const int nb = C->nbt;
   const int64_t r1 = r_dev[1];
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nth = (int64_t)gridDim.x * blockDim.x;
@@ -166,6 +181,7 @@ __global__ void __launch_bounds__(256) k_accept(DevCtl* C, int64_t m, int64_t n,
     if (nb == 0) ev[0] = ev[1];
     C->backtracks += nb;
     C->newton_iters++;
+    C->retry = 0;
     C->need_grad = nb > 0;
     if (nb > 0) C->seg_grad++;
   }
@@ -174,7 +190,8 @@ __global__ void __launch_bounds__(256) k_accept(DevCtl* C, int64_t m, int64_t n,
 // end of a Newton step: next inner test
 __global__ void k_ctl_inner_end(DevCtl* C, const EvalOut* ev0, int64_t m, int nsm, int wsplits, int* info,
                                 cudaGraphConditionalHandle h_inner) {
-  if (C->numeric == 0) C->j++;
+  if (C->skip) C->skip = 0;  // a retried step does not advance j (host: --j)
+  else if (C->numeric == 0) C->j++;
   cudaGraphSetConditional(h_inner, inner_next(C, ev0, m, nsm, wsplits, info));
 }
 

@@ -31,6 +31,7 @@ struct DirGeo {
   int pad;
   long long r, nout, nmat;
   double diag, mult;   // reduce: M = diag·I + mult·Σ_s W[s]; CG: mult = κ
+  double jit;          // factor retry (R36): M_ii ← M_ii (1 + jit); 0 on a first attempt
 };
 
 // Strategy (R12, R32): CG iff r > cg_ratio·m (cg_ratio > 0) or min(m, r) > cg_threshold.
@@ -53,6 +54,7 @@ SSN_HD DirGeo make_geo(long long r, long long m, int nsm, int wsplits, double ka
   DirGeo g;
   g.r = r;
   g.pad = 0;
+  g.jit = 0.0;
   g.bgrid = 1;
   if (use_cg(r, m, cg_ratio, cg_threshold)) {
     g.branch = 3;
@@ -356,12 +358,13 @@ __global__ void __launch_bounds__(256) k_gram(const Acc A, int64_t m,
 }
 
 // M[i + j*ld] = diag·[i == j] + mult · Σ_s W[s][i + j*nout]   (i ≥ j, j < nmat)
+//   retry after a failed factor (R36): M_ii ← M_ii + jit·M_ii
 //   SMW:   diag = κ⁻¹, mult = 1; nout = nmat + 1: row nmat is the rhs u = A_Jᵀg (unscaled)
 //   m × m: diag = 1, mult = κ (oracle: κ s + δ); nout = nmat; rhs row ← g (if g)
 // Grid-stride; graph mode reads the sizes from the device geometry (predicated on the branch).
 __global__ void k_gram_reduce(const double* __restrict__ W, int ns, int64_t nout, int64_t nmat, double diag,
                               double mult, double* __restrict__ M, int64_t ld, const double* __restrict__ g,
-                              const DirGeo* geo, int want) {
+                              const DirGeo* geo, int want, double jit) {
   if (geo) {
     if (geo->branch != want) return;
     ns = geo->ns;
@@ -370,6 +373,7 @@ __global__ void k_gram_reduce(const double* __restrict__ W, int ns, int64_t nout
     diag = geo->diag;
     mult = geo->mult;
     ld = geo->ld;
+    jit = geo->jit;
   }
   const int64_t tot = nout * nout > nmat ? nout * nout : nmat;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
@@ -379,8 +383,13 @@ __global__ void k_gram_reduce(const double* __restrict__ W, int ns, int64_t nout
     if (i < j || j >= nmat) continue;
     double s = 0.0;
     for (int q = 0; q < ns; ++q) s += W[(size_t)q * nout * nout + e];
-    if (i < nmat) M[i + j * ld] = (mult == 1.0 ? s : mult * s) + (i == j ? diag : 0.0);
-    else M[i + j * ld] = s;  // rhs row
+    if (i < nmat) {
+      double v = (mult == 1.0 ? s : mult * s) + (i == j ? diag : 0.0);
+      if (i == j && jit != 0.0) v = __fma_rn(v, jit, v);
+      M[i + j * ld] = v;
+    } else {
+      M[i + j * ld] = s;  // rhs row
+    }
   }
 }
 

@@ -340,6 +340,8 @@ struct ssnal_en_problem {
   int max_outer = 100, max_inner = 100, max_bt = 50, init_mode = 1, time_k1 = 0, certify = 0;
   double cg_ratio = 0.0, cg_threshold = 1e4, cg_tol = 1e-10;  // Newton strategy (R32)
   int cg_maxit = 1000;
+  int inject_fail = 0;    // test hook: the next N factorisations of a solve report failure
+  double jitter = 1e-10;  // factor retry M_ii ← M_ii (1 + jitter) after a non-positive pivot (R36)
   // counters for the current call
   int64_t launches = 0;
   void* arena = nullptr;    // all device buffers above (one allocation)
@@ -834,9 +836,11 @@ unsigned reduce_grid(ssnal_en_problem* P, int64_t tot) {
 // Newton direction for (J, r) at gradient g: d ← solution, *gd_dev ← gᵀd (Eq. (18)/(19)); if yt,
 // also the Armijo trial y_t = y + d (fused into the last kernel of each branch).
 int newton_direction(ssnal_en_problem* P, const int32_t* J, int64_t r, const double* g, double kappa, double* d,
-                     double* gd_dev, int* branch, const double* y = nullptr, double* yt = nullptr) {
+                     double* gd_dev, int* branch, const double* y = nullptr, double* yt = nullptr,
+                     double jit = 0.0) {
   const int64_t m = P->m;
-  const DirGeo geo = make_geo(r, m, P->nsm, P->W_splits, kappa, 1.0 / kappa, P->cg_ratio, P->cg_threshold);
+  DirGeo geo = make_geo(r, m, P->nsm, P->W_splits, kappa, 1.0 / kappa, P->cg_ratio, P->cg_threshold);
+  geo.jit = jit;
   *branch = geo.branch;
   if (geo.branch == 3)  // K6: conjugate gradient (R32)
     return launch_cg(P, J, r, g, kappa, d, gd_dev, y, yt, nullptr);
@@ -856,7 +860,7 @@ int newton_direction(ssnal_en_problem* P, const int32_t* J, int64_t r, const dou
     P->launches++;
     CKL();
     k_gram_reduce<<<reduce_grid(P, geo.nout * geo.nout), 256, 0, P->st>>>(P->W, geo.ns, geo.nout, geo.nmat, geo.diag,
-                                                                          geo.mult, P->Mmat, geo.ld, nullptr, nullptr, 0);
+                                                                          geo.mult, P->Mmat, geo.ld, nullptr, nullptr, 0, geo.jit);
     P->launches++;
     CKL();
     int rc = launch_chol(P, P->Mmat, geo.N, P->u, 1.0, nullptr, nullptr);  // v = (κ⁻¹I + G)⁻¹ u
@@ -880,7 +884,7 @@ int newton_direction(ssnal_en_problem* P, const int32_t* J, int64_t r, const dou
   P->launches++;
   CKL();
   k_gram_reduce<<<reduce_grid(P, m * m), 256, 0, P->st>>>(P->W, geo.ns, m, m, geo.diag, geo.mult, P->Mmat, geo.ld, g,
-                                                          nullptr, 0);
+                                                          nullptr, 0, geo.jit);
   P->launches++;
   CKL();
   return launch_chol(P, P->Mmat, (int)m, d, -1.0, g, gd_dev, y, yt);  // d = −M⁻¹ g, gd = gᵀd
@@ -900,7 +904,7 @@ int newton_direction_graph(ssnal_en_problem* P) {
     k_gram<true><<<2 * P->nsm, 256, 0, P->st>>>(acc, m, J, 0, P->W, g, 0, 0, geo);
     return 0;
   });
-  k_gram_reduce<<<reduce_grid(P, m * m), 256, 0, P->st>>>(P->W, 0, 0, 0, 0.0, 0.0, P->Mmat, 0, nullptr, geo, 1);
+  k_gram_reduce<<<reduce_grid(P, m * m), 256, 0, P->st>>>(P->W, 0, 0, 0, 0.0, 0.0, P->Mmat, 0, nullptr, geo, 1, 0.0);
   P->launches += 3;
   CKL();
   int rc = launch_chol(P, P->Mmat, 0, P->u, 1.0, nullptr, nullptr, nullptr, nullptr, geo, 1);
@@ -912,7 +916,7 @@ int newton_direction_graph(ssnal_en_problem* P) {
     k_gram<false><<<2 * P->nsm, 256, 0, P->st>>>(acc, m, J, 0, P->W, nullptr, 0, 0, geo);
     return 0;
   });
-  k_gram_reduce<<<reduce_grid(P, m * m), 256, 0, P->st>>>(P->W, 0, 0, 0, 0.0, 0.0, P->Mmat, 0, g, geo, 2);
+  k_gram_reduce<<<reduce_grid(P, m * m), 256, 0, P->st>>>(P->W, 0, 0, 0, 0.0, 0.0, P->Mmat, 0, g, geo, 2, 0.0);
   P->launches += 3;
   CKL();
   rc = launch_chol(P, P->Mmat, 0, P->d, -1.0, g, gd, P->y[0], P->y[1], geo, 2);
@@ -1008,6 +1012,7 @@ int solve_core(ssnal_en_problem* P, double l1, double l2, double sigma0, double 
 
   double sigma = sigma0;
   int converged = 0, numeric = 0, k;
+  int inject = P->inject_fail;
   for (k = 0; k < P->max_outer && !numeric; ++k) {
     const Scal sc = make_scal(sigma, l1, l2);
     // EVAL(y, w) with the new (x, σ): K1e + finalize + gather (∇ψ) + reduce
@@ -1021,6 +1026,7 @@ int solve_core(ssnal_en_problem* P, double l1, double l2, double sigma0, double 
     if ((rc = fetch_eval(P, 0, &ev))) return rc;
     S->psi_evals++;
 
+    int retry = 0;  // the current step's factor failed once: recompute it with the jitter (R36)
     for (int j = 0; j < P->max_inner; ++j) {
       if (ev.res1 <= tol) break;  // inner stop, Eq. (20) res(kkt1) (R6)
       int br = 0;
@@ -1028,7 +1034,8 @@ int solve_core(ssnal_en_problem* P, double l1, double l2, double sigma0, double 
       // trial s = 1: y_t = y + d (written by the direction's last kernel); K1 fused at y_t
       const int tr = 1 - cur;
       const int wtr = (wcur + 1) % 3, wbt = (wcur + 2) % 3;
-      if ((rc = newton_direction(P, P->J[cur], ev.r, P->g[cur], sc.kappa, P->d, gd_dev, &br, P->y[cur], P->y[tr])))
+      if ((rc = newton_direction(P, P->J[cur], ev.r, P->g[cur], sc.kappa, P->d, gd_dev, &br, P->y[cur], P->y[tr],
+                                 retry ? P->jitter : 0.0)))
         return rc;
       S->branch_steps[br]++;
       if ((rc = launch_k1(P, P->y[tr], P->x, sc, 1, P->w[wtr]))) return rc;
@@ -1039,6 +1046,16 @@ int solve_core(ssnal_en_problem* P, double l1, double l2, double sigma0, double 
         return rc;
       if ((rc = fetch_eval(P, 1, &evt))) return rc;
       S->psi_evals++;
+      if ((br == 1 || br == 2) && inject > 0) {
+        inject--;
+        evt.info = 1;
+      }
+      if ((br == 1 || br == 2) && evt.info != 0 && !retry && P->jitter > 0.0) {
+        retry = 1;  // same y, same step index: redo the direction with the jittered factor
+        S->jitter_retries++;
+        --j;
+        continue;
+      }
       if ((br == 1 || br == 2) && evt.info != 0) {
         numeric = 1;
         set_err("Cholesky pivot not positive (branch %d, r=%lld)", br, (long long)ev.r);
@@ -1091,6 +1108,7 @@ int solve_core(ssnal_en_problem* P, double l1, double l2, double sigma0, double 
         if ((rc = fetch_eval(P, 0, &ev))) return rc;
       }
       S->newton_iters++;
+      retry = 0;
     }
     if (numeric) break;
     // Multiplier update Eq. (10): x ← x − σ(Aᵀy + z̄) = P (Moreau); res(kkt3) Eq. (20)
@@ -1337,6 +1355,8 @@ int solve_graph_core(ssnal_en_problem* P, double l1, double l2, double sigma0, d
   h->cg_ratio = P->cg_ratio;
   h->cg_threshold = P->cg_threshold;
   h->nb = P->nb;
+  h->jitter = P->jitter;
+  h->inject = P->inject_fail;
   h->tstamp[0] = ~0ull;
   h->tstamp[1] = 0ull;
   CK(cudaMemcpyAsync(P->ctl, h, sizeof(DevCtl), cudaMemcpyHostToDevice, P->st));
@@ -1363,6 +1383,7 @@ void finish_stats(ssnal_en_problem* P, ssnal_en_stats* S) {
     S->aty_passes += C->aty_passes;
     for (int b = 0; b < 4; ++b) S->branch_steps[b] = C->branch_steps[b];
     S->cg_iters = C->cg_iters;
+    S->jitter_retries = C->jitter_retries;
     S->line_search_stalled = C->stalled;
     S->res_kkt1 = C->res1;
     S->res_kkt3 = C->res3;
@@ -1658,6 +1679,8 @@ int ssnal_en_set_option(ssnal_en_problem* P, const char* key, double v) {
   else if (k == "graph" && (v == 0 || v == 1)) P->use_graph = (int)v;
   else if (k == "cg_ratio" && v >= 0) P->cg_ratio = v;
   else if (k == "cg_threshold" && v >= 0) P->cg_threshold = v;
+  else if (k == "jitter" && v >= 0 && v < 1) P->jitter = v;
+  else if (k == "test_fail_factor" && v >= 0) P->inject_fail = (int)v;
   else if (k == "cg_tol" && v > 0 && v < 1) {
     P->cg_tol = v;
     drop_graph(P);  // baked into the captured CG launch
@@ -1810,16 +1833,18 @@ int ssnal_en_newton_direction(ssnal_en_problem* P, const int32_t* J, int64_t r, 
     set_err("invalid argument");
     return SSNAL_EINVAL;
   }
-  int br = 0;
-  int rc = newton_direction(P, J, r, g, kappa, d_out, P->scratch, &br);
-  if (rc) return rc;
-  CK(cudaMemcpyAsync(P->scratch_host, P->scratch, 8, cudaMemcpyDeviceToHost, P->st));
-  CK(cudaMemcpyAsync(P->scratch_host + 1, P->info, 4, cudaMemcpyDeviceToHost, P->st));
-  CK(cudaStreamSynchronize(P->st));
+  int br = 0, info = 0;
+  for (int attempt = 0; attempt < 2; ++attempt) {  // a failed factor is retried once with the jitter (R36)
+    int rc = newton_direction(P, J, r, g, kappa, d_out, P->scratch, &br, nullptr, nullptr, attempt ? P->jitter : 0.0);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(P->scratch_host, P->scratch, 8, cudaMemcpyDeviceToHost, P->st));
+    CK(cudaMemcpyAsync(P->scratch_host + 1, P->info, 4, cudaMemcpyDeviceToHost, P->st));
+    CK(cudaStreamSynchronize(P->st));
+    memcpy(&info, P->scratch_host + 1, 4);
+    if (!((br == 1 || br == 2) && info) || !(P->jitter > 0.0)) break;
+  }
   if (gd_out) *gd_out = P->scratch_host[0];
   if (branch_out) *branch_out = br;
-  int info = 0;
-  memcpy(&info, P->scratch_host + 1, 4);
   if ((br == 1 || br == 2) && info) {
     set_err("Cholesky pivot not positive");
     return SSNAL_ENUMERIC;
@@ -1862,7 +1887,7 @@ int ssnal_en_model_select(ssnal_en_problem* P, double l2, double* xdb_out, ssnal
       k_gram<true><<<gram_grid(P, tiles * ns), 256, 0, P->st>>>(acc, m, J, r, P->W, nullptr, tiles, ns, nullptr);
       return 0;
     });
-    k_gram_reduce<<<reduce_grid(P, r * r), 256, 0, P->st>>>(P->W, ns, r, r, l2, 1.0, P->Msel, NR, nullptr, nullptr, 0);
+    k_gram_reduce<<<reduce_grid(P, r * r), 256, 0, P->st>>>(P->W, ns, r, r, l2, 1.0, P->Msel, NR, nullptr, nullptr, 0, 0.0);
     with_acc(P, [&](auto acc) {
       k_fill_rows<<<(unsigned)((m * r + 255) / 256), 256, 0, P->st>>>(P->Msel, NR, r, acc, m, J, r, 0);
       return 0;
@@ -1880,7 +1905,7 @@ int ssnal_en_model_select(ssnal_en_problem* P, double l2, double* xdb_out, ssnal
       return 0;
     });
     k_gram_reduce<<<reduce_grid(P, nout * nout), 256, 0, P->st>>>(P->W, ns2, nout, r, 0.0, 1.0, P->Mmat, N + 1, nullptr,
-                                                                  nullptr, 0);
+                                                                  nullptr, 0, 0.0);
     P->launches += 3;
     CKL();
     if ((rc = launch_chol_ex(P, P->Mmat, N, N + 1, N + 1, P->u, 1.0, nullptr, nullptr, nullptr, nullptr, info_ols)))
@@ -1900,7 +1925,7 @@ int ssnal_en_model_select(ssnal_en_problem* P, double l2, double* xdb_out, ssnal
       k_gram<false><<<gram_grid(P, tiles * ns), 256, 0, P->st>>>(acc, m, J, r, P->W, nullptr, tiles, ns, nullptr);
       return 0;
     });
-    k_gram_reduce<<<reduce_grid(P, m * m), 256, 0, P->st>>>(P->W, ns, m, m, l2, 1.0, P->Msel, NR, nullptr, nullptr, 0);
+    k_gram_reduce<<<reduce_grid(P, m * m), 256, 0, P->st>>>(P->W, ns, m, m, l2, 1.0, P->Msel, NR, nullptr, nullptr, 0, 0.0);
     with_acc(P, [&](auto acc) {
       k_fill_rows<<<(unsigned)((m * m + 255) / 256), 256, 0, P->st>>>(P->Msel, NR, m, acc, m, J, m, 1);
       return 0;

@@ -32,7 +32,7 @@ class Stats(ctypes.Structure):
                 ("line_search_stalled", _i32), ("cg_iters", _i32), ("active", _i64), ("res_kkt1", _d), ("res_kkt3", _d),
                 ("primal_obj", _d), ("dual_obj", _d), ("gap", _d), ("sigma_final", _d),
                 ("time_device_s", _d), ("time_total_s", _d), ("kernel_launches", _i64), ("k1_time_s", _d),
-                ("k1_launches", _i32), ("reserved", _i32), ("primal_viol", _d)]
+                ("k1_launches", _i32), ("jitter_retries", _i32), ("primal_viol", _d)]
 
     def as_dict(self):
         d = {f: getattr(self, f) for f, _ in self._fields_ if f != "reserved"}
