@@ -113,6 +113,8 @@ double ssnal_en_lambda_max_l1(const ssnal_en_problem* p);
  *   jitter=1e-10 (R36): a non-positive Cholesky pivot redoes that Newton step once from
  *     the same y with the factored matrix's diagonal scaled by (1 + jitter) — the step is not
  *     counted, stats.jitter_retries is; a second failure returns SSNAL_ENUMERIC.  0: no retry.
+ *   inner_tol_mode=0 (inner stop res1 ≤ tol, R6; 1: res1 ≤ max(tol, 0.1·res3) with res3 of Eq. (20)
+ *     at the point each outer iteration starts from — SPEC's schedule, reading R37),
  *   test_fail_factor=0 (test hook: each solve treats its first N Cholesky factorisations as
  *     failed, to exercise the retry and SSNAL_ENUMERIC paths),
  *   EINVAL for unknown keys. */

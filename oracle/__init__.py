@@ -31,7 +31,7 @@ class Opts(ctypes.Structure):
     _fields_ = [("sigma_factor", _d), ("sigma_max", _d), ("mu", _d), ("beta", _d), ("max_outer", ctypes.c_int32),
                 ("max_inner", ctypes.c_int32), ("max_bt", ctypes.c_int32), ("init_mode", ctypes.c_int32),
                 ("cg_ratio", _d), ("cg_threshold", _d), ("cg_tol", _d), ("cg_maxit", ctypes.c_int32),
-                ("pad", ctypes.c_int32), ("jitter", _d)]
+                ("inner_tol_mode", ctypes.c_int32), ("jitter", _d)]
 
 
 class Stats(ctypes.Structure):

@@ -383,7 +383,7 @@ typedef struct {
   double cg_threshold; /* CG when min(m, r) > cg_threshold (10⁴)          */
   double cg_tol;       /* CG relative residual (R32)                               */
   int32_t cg_maxit;
-  int32_t pad;
+  int32_t inner_tol_mode; /* 0: tol_in = tol (R6); 1: max(tol, 0.1·res3 at the outer start) (R37) */
   double jitter;       /* factor retry: diagonal × (1 + jitter) after a non-positive pivot (R36) */
 } orc_opts;
 
@@ -477,7 +477,7 @@ void orc_default_opts(orc_opts* o) {
   o->cg_threshold = 1e4;
   o->cg_tol = 1e-10;
   o->cg_maxit = 1000;
-  o->pad = 0;
+  o->inner_tol_mode = 0;
   o->jitter = 1e-10;
 }
 
@@ -527,9 +527,24 @@ int orc_solve(const double* A, const double* b, i64 m, i64 n, double l1, double 
   int k;
   for (k = 0; k < o.max_outer && !numeric; ++k) {
     eval_point(A, b, m, n, x, y, w, sigma, l1, l2, nb, P, J, g, &ev);
+    /* inner tolerance: tol (R6), or SPEC's schedule max(tol, 0.1·res(kkt3)) with res(kkt3) of
+     * Eq. (20) at the point this outer iteration starts from (reading R37) */
+    double tol_in = tol;
+    if (o.inner_tol_mode) {
+      double dx2 = 0.0, zz = 0.0, yy = 0.0;
+      for (i64 i = 0; i < n; ++i) {
+        double dx = x[i] - P[i];
+        double z = dx / sigma - w[i];
+        dx2 += dx * dx;
+        zz += z * z;
+      }
+      for (i64 q = 0; q < m; ++q) yy += y[q] * y[q];
+      double res3_0 = (sqrt(dx2) / sigma) / (1.0 + sqrt(yy) + sqrt(zz));
+      tol_in = fmax(tol, 0.1 * res3_0);
+    }
     /* Semi-smooth Newton inner loop. */
     for (int j = 0; j < o.max_inner; ++j) {
-      if (ev.res1 <= tol) break; /* inner stop, Eq. (20) res(kkt1) (R6) */
+      if (ev.res1 <= tol_in) break; /* inner stop, Eq. (20) res(kkt1) (R6) */
       double kappa = sigma / (1.0 + sigma * l2);
       /* strategy (R12, R32): CG iff r > cg_ratio·m (cg_ratio > 0) or min(m, r) > cg_threshold */
       const i64 mr_min = ev.r < m ? ev.r : m;

@@ -32,7 +32,9 @@ struct DevCtl {
   int k, j, nbt, need_grad;
   int converged, numeric, numeric_kind, stalled;
   int retry, skip;   // retry: this step's factor failed once; skip: redo the step (no accept)
-  int inject, pad2;  // test hook: treat the next `inject` factorisations as failed
+  int inject;        // test hook: treat the next `inject` factorisations as failed
+  int inner_tol_mode;  // 0: tol_in = tol (R6); 1: tol_in = max(tol, 0.1 res3 at the outer start) (R37)
+  double tol_in;     // inner stop of the current outer iteration
   DirGeo geo;        // direction geometry for the current r
   // statistics (same meaning as ssnal_en_stats)
   int outer_iters, newton_iters, psi_evals, backtracks, aty_passes, branch_steps[4], cg_iters;
@@ -80,7 +82,7 @@ SSN_DEV int bt_next(DevCtl* C, bool ok) {
 
 // Inner-loop test (R6: res(kkt1) ≤ tol stops) and, if continuing, the next direction's setup.
 SSN_DEV int inner_next(DevCtl* C, const EvalOut* ev0, int64_t m, int nsm, int wsplits, int* info) {
-  const int go = (C->numeric == 0) && (C->j < C->max_inner) && !(ev0->res1 <= C->tol);
+  const int go = (C->numeric == 0) && (C->j < C->max_inner) && !(ev0->res1 <= C->tol_in);
   if (go) {
     C->geo = make_geo(ev0->r, m, nsm, wsplits, C->sc.kappa, C->kinv, C->cg_ratio, C->cg_threshold);
     C->geo.jit = C->retry ? C->jitter : 0.0;
@@ -101,6 +103,12 @@ __global__ void k_ctl_outer_begin(DevCtl* C) {
 __global__ void k_ctl_inner_begin(DevCtl* C, const EvalOut* ev0, int64_t m, int nsm, int wsplits, int* info,
                                   cudaGraphConditionalHandle h_inner) {
   C->psi_evals++;
+  C->tol_in = C->tol;
+  if (C->inner_tol_mode) {  // res(kkt3), Eq. (20), of the point the outer iteration starts from
+    const double res3 = __ddiv_rn(__ddiv_rn(__dsqrt_rn(ev0->s[1]), C->sigma),
+                                  __dadd_rn(__dadd_rn(1.0, __dsqrt_rn(ev0->yy)), __dsqrt_rn(ev0->s[2])));
+    C->tol_in = fmax(C->tol, __dmul_rn(0.1, res3));
+  }
   cudaGraphSetConditional(h_inner, inner_next(C, ev0, m, nsm, wsplits, info));
 }
 

@@ -340,6 +340,7 @@ struct ssnal_en_problem {
   int max_outer = 100, max_inner = 100, max_bt = 50, init_mode = 1, time_k1 = 0, certify = 0;
   double cg_ratio = 0.0, cg_threshold = 1e4, cg_tol = 1e-10;  // Newton strategy (R32)
   int cg_maxit = 1000;
+  int inner_tol_mode = 0;  // 1: tol_in = max(tol, 0.1 res3 at the outer start) (R37)
   int inject_fail = 0;    // test hook: the next N factorisations of a solve report failure
   double jitter = 1e-10;  // factor retry M_ii ← M_ii (1 + jitter) after a non-positive pivot (R36)
   // counters for the current call
@@ -1026,9 +1027,14 @@ int solve_core(ssnal_en_problem* P, double l1, double l2, double sigma0, double 
     if ((rc = fetch_eval(P, 0, &ev))) return rc;
     S->psi_evals++;
 
+    double tol_in = tol;  // inner stop (R6); adaptive schedule (R37)
+    if (P->inner_tol_mode) {
+      const double res3_0 = (sqrt(ev.s[1]) / sigma) / (1.0 + sqrt(ev.yy) + sqrt(ev.s[2]));
+      tol_in = fmax(tol, 0.1 * res3_0);
+    }
     int retry = 0;  // the current step's factor failed once: recompute it with the jitter (R36)
     for (int j = 0; j < P->max_inner; ++j) {
-      if (ev.res1 <= tol) break;  // inner stop, Eq. (20) res(kkt1) (R6)
+      if (ev.res1 <= tol_in) break;  // inner stop, Eq. (20) res(kkt1) (R6)
       int br = 0;
       double* gd_dev = P->scratch;
       // trial s = 1: y_t = y + d (written by the direction's last kernel); K1 fused at y_t
@@ -1357,6 +1363,7 @@ int solve_graph_core(ssnal_en_problem* P, double l1, double l2, double sigma0, d
   h->nb = P->nb;
   h->jitter = P->jitter;
   h->inject = P->inject_fail;
+  h->inner_tol_mode = P->inner_tol_mode;
   h->tstamp[0] = ~0ull;
   h->tstamp[1] = 0ull;
   CK(cudaMemcpyAsync(P->ctl, h, sizeof(DevCtl), cudaMemcpyHostToDevice, P->st));
@@ -1681,6 +1688,7 @@ int ssnal_en_set_option(ssnal_en_problem* P, const char* key, double v) {
   else if (k == "cg_threshold" && v >= 0) P->cg_threshold = v;
   else if (k == "jitter" && v >= 0 && v < 1) P->jitter = v;
   else if (k == "test_fail_factor" && v >= 0) P->inject_fail = (int)v;
+  else if (k == "inner_tol_mode" && (v == 0 || v == 1)) P->inner_tol_mode = (int)v;
   else if (k == "cg_tol" && v > 0 && v < 1) {
     P->cg_tol = v;
     drop_graph(P);  // baked into the captured CG launch
