@@ -21,6 +21,7 @@
 // K1f k1_finalize    : concatenates the per-CTA segments in CTA order → ascending J.
 // K5  k_eval_reduce  : g = y + b − Σ parts, ψ (Prop. 2), res1 (Eq. (20)).
 #pragma once
+#include <cooperative_groups.h>
 #include "common.cuh"
 
 namespace ssn {
@@ -729,10 +730,14 @@ struct EvalOut {
 
 constexpr int K5_THREADS = 256;  // 8 warps; CTA c owns rows [32c, 32c + 32)
 
-// Multi-CTA, deterministic: warp w of CTA c sums partial rows b ∈ [w·np/8, (w+1)·np/8)
-// in ascending b for its 32 rows; the 8 warp sums are added in warp order; the last CTA
-// (ticket counter) adds the per-CTA scalar partials in CTA order and writes EvalOut.
-__global__ void __launch_bounds__(K5_THREADS) k_eval_reduce(int64_t m, const double* __restrict__ y,
+// Multi-CTA, deterministic.  Clusters of kEvalCS CTAs per 32-row block rb: with the gradient,
+// CTA q of the cluster sums the partial rows b ∈ [q·np/8, (q+1)·np/8) (warp w a contiguous
+// eighth of that, ascending b) for the block's 32 rows; the warp sums are added in warp order
+// and rank 0 adds the cluster's CTA sums in rank order through DSMEM.  Rank 0 then forms g and
+// the block's scalar partials; the last row block (ticket counter) adds them in block order,
+// adds the per-CTA scalar partials of K1/K1e in CTA order and writes EvalOut.
+constexpr int kEvalCS = 8;
+__global__ void __cluster_dims__(kEvalCS, 1, 1) __launch_bounds__(K5_THREADS) k_eval_reduce(int64_t m, const double* __restrict__ y,
                                                             const double* __restrict__ bvec,
                                                             const double* __restrict__ part_vec,
                                                             const int* __restrict__ part_valid, int nparts,
@@ -748,26 +753,51 @@ __global__ void __launch_bounds__(K5_THREADS) k_eval_reduce(int64_t m, const dou
   if (pred && *pred == 0) return;  // graph mode: predicated off (uniform over the grid)
   if (scp) sc = *scp;
   if (nbp) nb = *nbp;  // graph mode: ‖b‖ from the control block (the graph may predate it)
+  namespace cg = cooperative_groups;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t k = (int64_t)blockIdx.x * 32 + lane;
+  const int cs = (int)(blockIdx.x % kEvalCS), rb = (int)(blockIdx.x / kEvalCS), nrb = (int)(gridDim.x / kEvalCS);
+  const int64_t k = (int64_t)rb * 32 + lane;
+  __shared__ double gsum[32];
   if (with_grad) {
-    const int b0 = (int)((int64_t)nparts * warp / 8), b1 = (int)((int64_t)nparts * (warp + 1) / 8);
+    const int q0 = (int)((int64_t)nparts * cs / kEvalCS), q1 = (int)((int64_t)nparts * (cs + 1) / kEvalCS);
+    const int b0 = q0 + (int)((int64_t)(q1 - q0) * warp / 8), b1 = q0 + (int)((int64_t)(q1 - q0) * (warp + 1) / 8);
     double gp = 0.0;
-    if (k < m) {
-      int b = b0;
-      for (; b + 4 <= b1; b += 4) {
-        double v[4];
+    // 32 partials at a time: one coalesced load of their flags, a ballot, then the valid ones in
+    // ascending b, 8 independent loads per round trip (adding +0.0 for the unused slots)
+    for (int c0 = b0; c0 < b1; c0 += 32) {
+      const int cn = min(32, b1 - c0);
+      unsigned mask;
+      if (part_valid) mask = __ballot_sync(0xffffffffu, lane < cn && part_valid[c0 + lane] != 0);
+      else mask = cn == 32 ? 0xffffffffu : ((1u << cn) - 1u);
+      while (mask) {
+        double v[8];
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-          v[u] = (!part_valid || part_valid[b + u]) ? part_vec[(size_t)(b + u) * m + k] : 0.0;
+        for (int u = 0; u < 8; ++u) {
+          const int bit = mask ? __ffs(mask) - 1 : -1;
+          mask &= mask - 1u;
+          v[u] = (bit >= 0 && k < m) ? part_vec[(size_t)(c0 + bit) * m + k] : 0.0;
+        }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) gp += v[u];
+        for (int u = 0; u < 8; ++u) gp += v[u];
       }
-      for (; b < b1; ++b)
-        if (!part_valid || part_valid[b]) gp += part_vec[(size_t)b * m + k];
     }
     red[warp][lane] = gp;
+    __syncthreads();
+    if (warp == 0) {
+      double t = red[0][lane];
+      for (int wi = 1; wi < 8; ++wi) t += red[wi][lane];
+      gsum[lane] = t;
+    }
+    cg::cluster_group cluster = cg::this_cluster();
+    cluster.sync();
+    if (cs == 0 && warp == 0) {
+      double t = gsum[lane];
+      for (int q = 1; q < kEvalCS; ++q) t += cluster.map_shared_rank(gsum, q)[lane];
+      red[0][lane] = t;
+    }
+    cluster.sync();  // rank 0 has read every CTA's sums
   }
+  if (cs != 0) return;
   __syncthreads();
   if (warp == 0) {
     double yy = 0.0, by = 0.0, gg = 0.0;
@@ -776,8 +806,7 @@ __global__ void __launch_bounds__(K5_THREADS) k_eval_reduce(int64_t m, const dou
       yy = yk * yk;
       by = bk * yk;
       if (with_grad) {
-        double gp = red[0][lane];
-        for (int wi = 1; wi < 8; ++wi) gp += red[wi][lane];
+        const double gp = red[0][lane];
         const double g = __dsub_rn(__dadd_rn(yk, bk), gp);
         g_out[k] = g;
         gg = g * g;
@@ -787,12 +816,12 @@ __global__ void __launch_bounds__(K5_THREADS) k_eval_reduce(int64_t m, const dou
     by = warp_allsum(by);
     gg = warp_allsum(gg);
     if (lane == 0) {
-      blk[blockIdx.x * 3 + 0] = yy;
-      blk[blockIdx.x * 3 + 1] = by;
-      blk[blockIdx.x * 3 + 2] = gg;
+      blk[rb * 3 + 0] = yy;
+      blk[rb * 3 + 1] = by;
+      blk[rb * 3 + 2] = gg;
       __threadfence();
       const unsigned t = atomicAdd(ticket, 1u);
-      last = (t == gridDim.x - 1);
+      last = (t == (unsigned)nrb - 1);
     }
   }
   __syncthreads();
@@ -800,14 +829,23 @@ __global__ void __launch_bounds__(K5_THREADS) k_eval_reduce(int64_t m, const dou
   __threadfence();
   // warp 0 of the last CTA: lane ℓ sums entries q ≡ ℓ (mod 32) in order, then a fixed butterfly
   double a = 0, bb = 0, c = 0;
-  for (unsigned q = lane; q < gridDim.x; q += 32) {
+  for (int q = lane; q < nrb; q += 32) {
     a += __ldcg(blk + q * 3 + 0);
     bb += __ldcg(blk + q * 3 + 1);
     c += __ldcg(blk + q * 3 + 2);
   }
   double s[4] = {0, 0, 0, 0};
-  for (int q = lane; q < nscal; q += 32)
-    for (int j = 0; j < 4; ++j) s[j] += __ldcg(part_scal + q * 4 + j);
+  for (int q0 = lane; q0 < nscal; q0 += 32 * 8) {  // lane sums q ≡ lane (mod 32) ascending; 8 in flight
+    double v[8][4];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) v[u][j] = q0 + 32 * u < nscal ? __ldcg(part_scal + (q0 + 32 * u) * 4 + j) : 0.0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) s[j] += v[u][j];
+  }
   a = warp_allsum(a);
   bb = warp_allsum(bb);
   c = warp_allsum(c);

@@ -4,7 +4,7 @@
 // (each column is m contiguous doubles); nothing is gathered into a copy.
 //
 // K2  k_gather_axpy    : per-CTA partials of Σ_a coef_a A[:, J_a]          (A_J v, A_J P_J)
-//     k_smw_backsub    : d = −g + A_J v, gᵀd and the trial y + d (last-CTA finalisation)
+//     k_gather_rows    : row-block clusters: A_J coef (∇ψ) or d = −g + A_J v, gᵀd, y + d (SMW)
 //     k_combine        : out = bs·base + Σ parts (fixed order), optional dot
 // K3  k_gram<true>     : split-K partials of A_JᵀA_J (lower, r × r) and u = A_Jᵀg Eq. (19)
 //     k_gram<false>    : split-K partials of A_J A_Jᵀ (lower, m × m)            Eq. (18)
@@ -27,7 +27,7 @@ struct DirGeo {
   int branch;          // 0: r = 0 (d = −g), 1: 0 < r < m (SMW, Eq. (19)), 2: r ≥ m (Eq. (18)), 3: CG (R32)
   int N, NR, ld;       // factor order, rows incl. the rhs row, leading dimension of Mmat
   int tiles, ns;       // Gram lower 32 × 32 tiles and split-K slices
-  int bgrid;           // SMW back-substitution CTAs
+  int pad0;
   int pad;
   long long r, nout, nmat;
   double diag, mult;   // reduce: M = diag·I + mult·Σ_s W[s]; CG: mult = κ
@@ -38,6 +38,13 @@ struct DirGeo {
 SSN_HD bool use_cg(long long r, long long m, double cg_ratio, double cg_threshold) {
   const long long mn = r < m ? r : m;
   return r > 0 && ((cg_ratio > 0.0 && (double)r > cg_ratio * (double)m) || (double)mn > cg_threshold);
+}
+
+// K3 Gram: lower 64 × 64 output tiles of an nout × nout matrix
+constexpr int GT = 64;  // Gram output tile edge
+SSN_HD int gram_tiles(long long nout) {
+  const int nt = (int)((nout + GT - 1) / GT);
+  return nt * (nt + 1) / 2;
 }
 
 // split-K slices: enough (tile, slice) items to cover 2 CTAs per SM, ≤ one slice per 32-chunk
@@ -53,9 +60,8 @@ SSN_HD DirGeo make_geo(long long r, long long m, int nsm, int wsplits, double ka
                        double cg_threshold) {
   DirGeo g;
   g.r = r;
-  g.pad = 0;
+  g.pad0 = g.pad = 0;
   g.jit = 0.0;
-  g.bgrid = 1;
   if (use_cg(r, m, cg_ratio, cg_threshold)) {
     g.branch = 3;
     g.N = g.NR = g.ld = g.tiles = g.ns = 0;
@@ -74,22 +80,17 @@ SSN_HD DirGeo make_geo(long long r, long long m, int nsm, int wsplits, double ka
     g.ld = g.N + 1;
     g.nout = r + 1;  // index r carries g: row r = u = A_Jᵀg (the rhs row)
     g.nmat = r;
-    const int nt = (int)((g.nout + 31) / 32);
-    g.tiles = nt * (nt + 1) / 2;
+    g.tiles = gram_tiles(g.nout);
     g.ns = gram_splits(nsm, g.tiles, m, wsplits);
     g.diag = kinv;  // κ⁻¹ I_r + A_JᵀA_J (R13)
     g.mult = 1.0;
-    long long bg = (r + 63) / 64;
-    if (bg > nsm) bg = nsm;
-    g.bgrid = bg < 1 ? 1 : (int)bg;
   } else {
     g.branch = 2;
     g.N = (int)m;
     g.NR = g.N + 1;
     g.ld = g.N + 1;
     g.nout = g.nmat = m;
-    const int nt = (int)((m + 31) / 32);
-    g.tiles = nt * (nt + 1) / 2;
+    g.tiles = gram_tiles(m);
     g.ns = gram_splits(nsm, g.tiles, r, wsplits);
     g.diag = 1.0;  // I_m + κ A_J A_Jᵀ
     g.mult = kappa;
@@ -148,73 +149,102 @@ __global__ void __launch_bounds__(256) k_gather_axpy(const Acc A, int64_t m,
   }
 }
 
-// Fused SMW back-substitution (Eq. (19)): partials of A_J v over `grid` CTAs, then the last CTA
-// (ticket) forms d = −g + Σ_b parts[b] (b ascending), gᵀd, and the Armijo trial y_t = y + d.
-template <class Acc, int MR>
-__global__ void __launch_bounds__(256) k_smw_backsub(const Acc A, int64_t m,
-                                                     const int32_t* __restrict__ J, const double* __restrict__ v,
-                                                     int64_t r, double* __restrict__ parts, const double* __restrict__ g,
-                                                     const double* __restrict__ y, double* __restrict__ d,
-                                                     double* __restrict__ yt, double* gd_out, unsigned* ticket,
-                                                     int grid_eff, const DirGeo* geo) {
-  extern __shared__ double red[];  // 8 x m
+// K2 by row blocks (the hot gathers): lane ℓ of every warp owns row k = 32·rb + ℓ of the row block
+// rb = cluster index; the 8 CTAs of a cluster split the r columns in 8 contiguous ranges, each
+// CTA stages its J / coef in smem and its warps issue 8 independent column loads per round trip.
+// The cluster's rank-0 CTA sums the 8 per-CTA partials through DSMEM in rank order, so one
+// launch yields the finished m-vector (no partial vectors in HBM, no second kernel):
+//   kGatherVec: out = Σ_a coef_a A[:, J_a]                      (∇ψ's A_J P_J, Eq. (15))
+//   kGatherSmw: out = d = −g + Σ_a v_a A[:, J_a], yt = y + d, *gd_out = gᵀd   (Eq. (19))
+// r: host value (≥ 0), else *r_dev; graph mode: pred (nullable) / geo (SMW branch) predicate.
+constexpr int kGatherCS = 8;  // cluster size = column splits per row block
+enum { kGatherVec = 0, kGatherSmw = 1 };
+template <class Acc>
+__global__ void __cluster_dims__(kGatherCS, 1, 1) __launch_bounds__(256)
+    k_gather_rows(const Acc A, int64_t m, const int32_t* __restrict__ J, const double* __restrict__ coef, int64_t r,
+                  const int64_t* __restrict__ r_dev, const int* __restrict__ pred, const DirGeo* geo, int mode,
+                  double* __restrict__ out, const double* __restrict__ g, const double* __restrict__ y,
+                  double* __restrict__ yt, double* gd_out, double* gdpart, unsigned* ticket) {
+  __shared__ int32_t sJ[256];
+  __shared__ double sC[256];
+  __shared__ double red[8][32];
+  __shared__ double part[32];
   __shared__ bool last;
-  __shared__ double wsum[8];
-  if (geo) {  // graph mode: r and the CTA count from the device-computed geometry
+  if (pred && *pred == 0) return;  // uniform over the grid
+  if (geo) {
     if (geo->branch != 1) return;
     r = geo->r;
-    grid_eff = geo->bgrid;
+  } else if (r < 0) {
+    r = *r_dev;
   }
-  if ((int)blockIdx.x >= grid_eff) return;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t a_lo = (int64_t)blockIdx.x * r / grid_eff, a_hi = (int64_t)(blockIdx.x + 1) * r / grid_eff;
-  double acc[MR];
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int cs = (int)cluster.block_rank();
+  const int rb = (int)(blockIdx.x / kGatherCS);
+  const int64_t row = (int64_t)rb * 32 + lane;
+  const int64_t lo = r * cs / kGatherCS, hi = r * (cs + 1) / kGatherCS;
+  double acc = 0.0;
+  for (int64_t c0 = lo; c0 < hi; c0 += 256) {
+    const int cn = (int)min((int64_t)256, hi - c0);
+    if (tid < cn) {
+      sJ[tid] = J[c0 + tid];
+      sC[tid] = coef[c0 + tid];
+    }
+    __syncthreads();
+    for (int e0 = warp; e0 < cn; e0 += 64) {  // this warp: columns e0, e0 + 8, …, e0 + 56
+      double v[8];
 #pragma unroll
-  for (int t = 0; t < MR; ++t) acc[t] = 0.0;
-  for (int64_t a = a_lo + warp; a < a_hi; a += 8) {
-    const auto col = A.col(J[a]);
-    const double c = v[a];
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + 8 * u;
+        v[u] = (e < cn && row < m) ? A.col(sJ[e]).ld(row) : 0.0;
+      }
 #pragma unroll
-    for (int t = 0; t < MR; ++t) {
-      const int64_t row = lane + 32 * t;
-      if (row < m) acc[t] = fma(c, col.ld(row), acc[t]);
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + 8 * u;
+        if (e < cn) acc = fma(sC[e], v[u], acc);
+      }
+    }
+    __syncthreads();
+  }
+  red[warp][lane] = acc;
+  __syncthreads();
+  if (warp == 0) {
+    double t = red[0][lane];
+    for (int wi = 1; wi < 8; ++wi) t += red[wi][lane];
+    part[lane] = t;
+  }
+  cluster.sync();
+  if (cs == 0 && warp == 0) {
+    double tot = part[lane];
+    for (int q = 1; q < kGatherCS; ++q) tot += cluster.map_shared_rank(part, q)[lane];
+    if (mode == kGatherVec) {
+      if (row < m) out[row] = tot;
+    } else {
+      double dot = 0.0;
+      if (row < m) {
+        const double dk = -g[row] + tot;
+        out[row] = dk;
+        yt[row] = __dadd_rn(y[row], dk);
+        dot = g[row] * dk;
+      }
+      dot = warp_allsum(dot);
+      if (lane == 0) {
+        gdpart[rb] = dot;
+        __threadfence();
+        last = atomicAdd(ticket, 1u) == (unsigned)(gridDim.x / kGatherCS) - 1;
+      }
+      __syncwarp();
+      if (last && lane == 0) {  // gᵀd = Σ_rb partials in row-block order
+        __threadfence();
+        double sdot = 0.0;
+        for (unsigned q = 0; q < gridDim.x / kGatherCS; ++q) sdot += __ldcg(gdpart + q);
+        *gd_out = sdot;
+        *ticket = 0u;
+      }
     }
   }
-#pragma unroll
-  for (int t = 0; t < MR; ++t) {
-    const int64_t row = lane + 32 * t;
-    if (row < m) red[(size_t)warp * m + row] = acc[t];
-  }
-  __syncthreads();
-  for (int64_t k = threadIdx.x; k < m; k += blockDim.x) {
-    double sacc = red[k];
-    for (int wi = 1; wi < 8; ++wi) sacc += red[(size_t)wi * m + k];
-    parts[(size_t)blockIdx.x * m + k] = sacc;
-  }
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) last = (atomicAdd(ticket, 1u) == (unsigned)grid_eff - 1);
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  double dot = 0.0;
-  for (int64_t k = threadIdx.x; k < m; k += blockDim.x) {
-    double sacc = 0.0;
-    for (int b = 0; b < grid_eff; ++b) sacc += __ldcg(parts + (size_t)b * m + k);
-    const double dk = -g[k] + sacc;
-    d[k] = dk;
-    yt[k] = __dadd_rn(y[k], __dmul_rn(1.0, dk));
-    dot += g[k] * dk;
-  }
-  dot = warp_allsum(dot);
-  if (lane == 0) wsum[warp] = dot;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double sacc = 0.0;
-    for (int wi = 0; wi < 8; ++wi) sacc += wsum[wi];
-    *gd_out = sacc;
-    *ticket = 0u;
-  }
+  cluster.sync();  // the partials stay resident until rank 0 has read them
 }
 
 // out[k] = bs*base[k] + Σ_{b<nparts} parts[b][k] (b ascending); if dotv: *dot_out = Σ dotv·out
@@ -254,107 +284,6 @@ SSN_DEV void tri_tile(int q, int* ti, int* tj) {  // q → (ti ≥ tj), row-majo
   while (i * (i + 1) / 2 > q) --i;
   *ti = i;
   *tj = q - i * (i + 1) / 2;
-}
-
-// Split-K Gram tiles.  A 32 × 32 operand block element (row ρ, col γ) is A[rowbase+ρ, J[colbase+γ]]:
-//   SMW   (Eq. (19)): out(a, b) = Σ_k A[k,J_a] A[k,J_b]   — blocks over rows k, columns a / b tiles
-//   m × m (Eq. (18)): out(k, l) = Σ_a A[k,J_a] A[l,J_a]   — blocks over row tiles k / l, columns a
-// Work items (lower tile q, slice s), item = q + tiles·s, are taken by persistent CTAs in a
-// grid-stride loop (results do not depend on the grid).  An item owns one contiguous slice of
-// the reduction index, double-buffers the next 32-slice in registers while computing the
-// current one from smem, and writes its partial tile to W[s]; a reduce kernel sums the slices
-// in order.  Graph mode: r, tiles, ns come from the device geometry (predicated on the branch).
-template <bool SMW, class Acc>
-__global__ void __launch_bounds__(256) k_gram(const Acc A, int64_t m,
-                                              const int32_t* __restrict__ J, int64_t r, double* __restrict__ W,
-                                              const double* __restrict__ gext, int tiles, int ns,
-                                              const DirGeo* geo) {
-  // SMW: index r (if gext) is the extra column g, so row r of the output is u = A_Jᵀg (Eq. (19) rhs)
-  __shared__ double sA[32][33], sB[32][33];
-  if (geo) {
-    if (geo->branch != (SMW ? 1 : 2)) return;
-    r = geo->r;
-    tiles = geo->tiles;
-    ns = geo->ns;
-  }
-  const int64_t K = SMW ? m : r;  // reduction length
-  const int64_t nch = (K + 31) / 32;
-  const int64_t nout = SMW ? r + (gext ? 1 : 0) : m;
-  const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
-  for (int item = blockIdx.x; item < tiles * ns; item += gridDim.x) {
-    int ti, tj;
-    tri_tile(item % tiles, &ti, &tj);
-    const int s = item / tiles;
-    const int64_t o0 = (int64_t)ti * 32, o1 = (int64_t)tj * 32;   // output tile origin
-    const int64_t c_lo = nch * s / ns, c_hi = nch * (s + 1) / ns;  // chunk slice
-    // element q of this thread in a 32 × 32 block: e = tid + 256 q → (γ = e >> 5, ρ = e & 31)
-    int64_t colA[4], colB[4];  // SMW: column of A for the a/b tiles; −1: the extra column g; −2: none
-    const double* pA[4];       // fp64 design: the column pointers themselves (g for index r)
-    const double* pB[4];
-    if (SMW) {
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int64_t ga = o0 + ty + 8 * q, gb = o1 + ty + 8 * q;
-        colA[q] = ga < r ? (int64_t)J[ga] : ((ga == r && gext) ? -1 : -2);
-        colB[q] = gb < r ? (int64_t)J[gb] : ((gb == r && gext) ? -1 : -2);
-        if constexpr (std::is_same<Acc, AccA>::value) {
-          pA[q] = colA[q] >= 0 ? A.A + colA[q] * m : (colA[q] == -1 ? gext : nullptr);
-          pB[q] = colB[q] >= 0 ? A.A + colB[q] * m : (colB[q] == -1 ? gext : nullptr);
-        }
-      }
-    }
-    double va[4], vb[4];
-    auto load = [&](int64_t ch) {
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        if (SMW) {
-          const int64_t k = ch * 32 + tx;
-          if constexpr (std::is_same<Acc, AccA>::value) {
-            va[q] = (pA[q] && k < m) ? __ldg(pA[q] + k) : 0.0;
-            vb[q] = (pB[q] && k < m) ? __ldg(pB[q] + k) : 0.0;
-          } else {
-            va[q] = (k < m && colA[q] >= 0) ? A.ld(colA[q], k) : ((k < m && colA[q] == -1) ? __ldg(gext + k) : 0.0);
-            vb[q] = (k < m && colB[q] >= 0) ? A.ld(colB[q], k) : ((k < m && colB[q] == -1) ? __ldg(gext + k) : 0.0);
-          }
-        } else {
-          const int64_t a = ch * 32 + ty + 8 * q;
-          const bool ok = a < r;
-          const int64_t cb = ok ? (int64_t)J[a] : 0;
-          va[q] = (ok && o0 + tx < m) ? A.ld(cb, o0 + tx) : 0.0;
-          vb[q] = (ok && o1 + tx < m) ? A.ld(cb, o1 + tx) : 0.0;
-        }
-      }
-    };
-    double acc[4] = {0, 0, 0, 0};
-    if (c_lo < c_hi) load(c_lo);
-    for (int64_t ch = c_lo; ch < c_hi; ++ch) {
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {  // sX[reduction idx][output idx]
-        if (SMW) {
-          sA[tx][ty + 8 * q] = va[q];
-          sB[tx][ty + 8 * q] = vb[q];
-        } else {
-          sA[ty + 8 * q][tx] = va[q];
-          sB[ty + 8 * q][tx] = vb[q];
-        }
-      }
-      __syncthreads();
-      if (ch + 1 < c_hi) load(ch + 1);
-#pragma unroll 8
-      for (int kk = 0; kk < 32; ++kk) {
-        const double bv = sB[kk][tx];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) acc[q] = fma(sA[kk][ty * 4 + q], bv, acc[q]);
-      }
-      __syncthreads();
-    }
-    double* Ws = W + (size_t)s * nout * nout;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int64_t i = o0 + ty * 4 + q, j = o1 + tx;
-      if (i < nout && j < nout && i >= j) Ws[i + j * nout] = acc[q];
-    }
-  }
 }
 
 // M[i + j*ld] = diag·[i == j] + mult · Σ_s W[s][i + j*nout]   (i ≥ j, j < nmat)
@@ -459,6 +388,114 @@ SSN_DEV void tile_mma(const double* SA, const double* SB, double (&acc)[4][4][2]
     for (int rb = 0; rb < 4; ++rb)
 #pragma unroll
       for (int cb = 0; cb < 4; ++cb) dmma(acc[rb][cb], af[rb], bf[cb]);
+  }
+}
+
+// K3: split-K Gram tiles on the FP64 tensor cores.  64 × 64 output tiles; the reduction runs in
+// 32-chunks staged through shared memory (register double buffer), 8 warps × (16 × 32) blocks of
+// m8n8k4 DMMAs (8 independent accumulator chains per warp).  Operand element (output idx ω, κ):
+//   SMW   (Eq. (19)): out(a, b) = Σ_k A[k,J_a] A[k,J_b];  ω = a, κ = k − 32·chunk; index r = g
+//   m × m (Eq. (18)): out(k, l) = Σ_a A[k,J_a] A[l,J_a];  ω = k, κ = a − 32·chunk
+// Shared layouts are chosen for conflict-free fragment reads and coalesced global loads: SMW
+// [ω][κ] (ld 36: a warp loads one column's 32 consecutive rows), m × m [κ][ω] (ld 68: a warp
+// loads 64 consecutive rows of one column).  Work items (lower tile q, slice s), item = q + tiles·s,
+// are taken by persistent CTAs in a grid-stride loop (results do not depend on the grid); each
+// writes its partial tile (lower part) to W[s] and k_gram_reduce sums the slices in order.
+// Graph mode: r, tiles, ns from the device geometry (predicated on the branch).
+template <bool SMW, class Acc>
+__global__ void __launch_bounds__(256) k_gram(const Acc A, int64_t m, const int32_t* __restrict__ J, int64_t r,
+                                              double* __restrict__ W, const double* __restrict__ gext, int tiles,
+                                              int ns, const DirGeo* geo) {
+  constexpr int LD = SMW ? 36 : 68;
+  constexpr int SZ = SMW ? GT * 36 : 32 * 68;
+  __shared__ double sA[SZ], sB[SZ];
+  if (geo) {
+    if (geo->branch != (SMW ? 1 : 2)) return;
+    r = geo->r;
+    tiles = geo->tiles;
+    ns = geo->ns;
+  }
+  const int64_t K = SMW ? m : r;  // reduction length
+  const int64_t nch = (K + 31) / 32;
+  const int64_t nout = SMW ? r + (gext ? 1 : 0) : m;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int wr = warp >> 1, wc = warp & 1;  // this warp's block: rows 16 wr …, cols 32 wc …
+  auto at = [&](int w, int k) { return SMW ? w * LD + k : k * LD + w; };
+  for (int item = blockIdx.x; item < tiles * ns; item += gridDim.x) {
+    int ti, tj;
+    tri_tile(item % tiles, &ti, &tj);
+    const int s = item / tiles;
+    const bool dg = ti == tj;
+    const int64_t o0 = (int64_t)ti * GT, o1 = (int64_t)tj * GT;
+    const int64_t c_lo = nch * s / ns, c_hi = nch * (s + 1) / ns;
+    double va[8], vb[8];
+    // SMW: value q is (ω = warp + 8q, κ = lane); m × m: (ω = lane + 32(q & 1), κ = warp + 8(q >> 1))
+    auto load = [&](int64_t ch) {
+      if (SMW) {
+        const int64_t k = ch * 32 + lane;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int64_t a = o0 + warp + 8 * q, b = o1 + warp + 8 * q;
+          va[q] = k >= m ? 0.0 : (a < r ? A.col(J[a]).ld(k) : ((a == r && gext) ? __ldg(gext + k) : 0.0));
+          vb[q] = (dg || k >= m) ? 0.0 : (b < r ? A.col(J[b]).ld(k) : ((b == r && gext) ? __ldg(gext + k) : 0.0));
+        }
+      } else {
+#pragma unroll
+        for (int q2 = 0; q2 < 4; ++q2) {
+          const int64_t a = ch * 32 + warp + 8 * q2;
+          const bool ok = a < r;
+          const auto col = A.col(ok ? (int64_t)J[a] : 0);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int64_t ra = o0 + lane + 32 * h, rb = o1 + lane + 32 * h;
+            va[2 * q2 + h] = (ok && ra < m) ? col.ld(ra) : 0.0;
+            vb[2 * q2 + h] = (ok && !dg && rb < m) ? col.ld(rb) : 0.0;
+          }
+        }
+      }
+    };
+    double acc[2][4][2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    if (c_lo < c_hi) load(c_lo);
+    for (int64_t ch = c_lo; ch < c_hi; ++ch) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int w = SMW ? warp + 8 * q : lane + 32 * (q & 1);
+        const int k = SMW ? lane : warp + 8 * (q >> 1);
+        sA[at(w, k)] = va[q];
+        if (!dg) sB[at(w, k)] = vb[q];
+      }
+      __syncthreads();
+      if (ch + 1 < c_hi) load(ch + 1);
+      const double* SB = dg ? sA : sB;
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        double af[2], bf[4];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) af[i] = sA[at(16 * wr + 8 * i + g, 4 * kk + t)];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) bf[j] = SB[at(32 * wc + 8 * j + g, 4 * kk + t)];
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) dmma(acc[i][j], af[i], bf[j]);
+      }
+      __syncthreads();
+    }
+    double* Ws = W + (size_t)s * nout * nout;
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int64_t oi = o0 + 16 * wr + 8 * i + g, oj = o1 + 32 * wc + 8 * j + 2 * t + e;
+          if (oi < nout && oj < nout && oi >= oj) Ws[oi + oj * nout] = acc[i][j][e];
+        }
   }
 }
 

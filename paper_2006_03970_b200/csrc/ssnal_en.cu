@@ -113,21 +113,6 @@ gax_fn<Acc> gax_for(int mr) {
   }
 }
 template <class Acc>
-using bsub_fn = void (*)(const Acc, int64_t, const int32_t*, const double*, int64_t, double*, const double*,
-                         const double*, double*, double*, double*, unsigned*, int, const DirGeo*);
-template <class Acc>
-bsub_fn<Acc> bsub_for(int mr) {
-  switch (mr) {
-    case 1: return k_smw_backsub<Acc, 1>;
-    case 2: return k_smw_backsub<Acc, 2>;
-    case 4: return k_smw_backsub<Acc, 4>;
-    case 8: return k_smw_backsub<Acc, 8>;
-    case 16: return k_smw_backsub<Acc, 16>;
-    case 25: return k_smw_backsub<Acc, 25>;
-    default: return k_smw_backsub<Acc, 32>;
-  }
-}
-template <class Acc>
 using cg_fn = void (*)(const CgParams, const Acc);
 template <class Acc>
 cg_fn<Acc> cg_for(int mr) {
@@ -452,12 +437,10 @@ int configure(ssnal_en_problem* P) {
   P->cg_smem_bytes = cg_smem(m);
   if (P->fmt) {
     CK(cudaFuncSetAttribute(gax_for<AccG>(P->MR), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsm));
-    CK(cudaFuncSetAttribute(bsub_for<AccG>(P->MR), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsm));
     CK(cudaFuncSetAttribute(cg_for<AccG>(P->MR), cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)P->cg_smem_bytes));
   } else {
     CK(cudaFuncSetAttribute(gax_for<AccA>(P->MR), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsm));
-    CK(cudaFuncSetAttribute(bsub_for<AccA>(P->MR), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsm));
     CK(cudaFuncSetAttribute(cg_for<AccA>(P->MR), cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)P->cg_smem_bytes));
   }
@@ -685,6 +668,24 @@ int launch_gather(ssnal_en_problem* P, const int32_t* J, const double* coef, int
   return SSNAL_OK;
 }
 
+// The hot gathers: row-block clusters (k_gather_rows), grid ⌈m/32⌉ × 8 whatever r is.
+unsigned gather_rows_grid(const ssnal_en_problem* P) { return (unsigned)((P->m + 31) / 32) * kGatherCS; }
+
+// part_vec row 0 = A_J coef with r on the device (∇ψ, Eq. (15)); consumed by launch_eval with
+// nparts = 1 and no validity flags.
+int launch_gather_vec(ssnal_en_problem* P, const int32_t* J, const double* coef, const int64_t* r_dev,
+                      const int* pred = nullptr) {
+  with_acc(P, [&](auto acc) {
+    k_gather_rows<<<gather_rows_grid(P), 256, 0, P->st>>>(acc, P->m, J, coef, -1, r_dev, pred, nullptr, kGatherVec,
+                                                           P->part_vec, nullptr, nullptr, nullptr, nullptr, nullptr,
+                                                           nullptr);
+    return 0;
+  });
+  P->launches++;
+  CKL();
+  return SSNAL_OK;
+}
+
 // Same with r resident on the device (no host round trip): fixed grid, validity flags in gax_valid.
 constexpr int kGatherDevGrid = 128;
 int launch_gather_dev(ssnal_en_problem* P, const int32_t* J, const double* coef, const int64_t* r_dev,
@@ -705,7 +706,7 @@ int launch_eval(ssnal_en_problem* P, const double* y, const Scal& sc, int with_g
   const unsigned nblk = (unsigned)((P->m + 31) / 32);
   if (!P->capturing) ++P->ev_seq;
   // graph mode: no mapped host mirror (decisions are taken on the device)
-  k_eval_reduce<<<nblk, K5_THREADS, 0, P->st>>>(P->m, y, P->b, P->part_vec, valid, nparts, P->part_scal, P->G, sc,
+  k_eval_reduce<<<nblk * kEvalCS, K5_THREADS, 0, P->st>>>(P->m, y, P->b, P->part_vec, valid, nparts, P->part_scal, P->G, sc,
                                                  P->nb, with_grad, g_out, r_dev, P->ev_dev + slot, P->blk,
                                                  P->ticket, gd_src, info_src,
                                                  P->capturing ? nullptr : P->ev_host_dev + slot, P->ev_seq, scp, pred,
@@ -868,8 +869,9 @@ int newton_direction(ssnal_en_problem* P, const int32_t* J, int64_t r, const dou
     if (rc) return rc;
     // d = −g + A_J v, gᵀd, y_t = y + d (last-CTA finalisation)
     with_acc(P, [&](auto acc) {
-      bsub_for<decltype(acc)>(P->MR)<<<geo.bgrid, 256, (size_t)8 * m * 8, P->st>>>(
-          acc, m, J, P->u, r, P->part_vec, g, y ? y : g, d, yt ? yt : P->tmpm, gd_dev, P->ticket, geo.bgrid, nullptr);
+      k_gather_rows<<<gather_rows_grid(P), 256, 0, P->st>>>(acc, m, J, P->u, r, nullptr, nullptr, nullptr, kGatherSmw,
+                                                             d, g, y ? y : g, yt ? yt : P->tmpm, gd_dev, P->blk,
+                                                             P->ticket);
       return 0;
     });
     P->launches++;
@@ -911,9 +913,8 @@ int newton_direction_graph(ssnal_en_problem* P) {
   int rc = launch_chol(P, P->Mmat, 0, P->u, 1.0, nullptr, nullptr, nullptr, nullptr, geo, 1);
   if (rc) return rc;
   with_acc(P, [&](auto acc) {
-    bsub_for<decltype(acc)>(P->MR)<<<P->nsm, 256, (size_t)8 * m * 8, P->st>>>(acc, m, J, P->u, 0, P->part_vec, g,
-                                                                               P->y[0], P->d, P->y[1], gd, P->ticket,
-                                                                               0, geo);
+    k_gather_rows<<<gather_rows_grid(P), 256, 0, P->st>>>(acc, m, J, P->u, 0, nullptr, nullptr, geo, kGatherSmw, P->d,
+                                                           g, P->y[0], P->y[1], gd, P->blk, P->ticket);
     k_gram<false><<<2 * P->nsm, 256, 0, P->st>>>(acc, m, J, 0, P->W, nullptr, 0, 0, geo);
     return 0;
   });
@@ -1021,9 +1022,9 @@ int solve_core(ssnal_en_problem* P, double l1, double l2, double sigma0, double 
     // partial scalars of K1e are in part_scal; they are reduced by the eval kernel
     if ((rc = launch_finalize(P, P->J[cur], P->PJ[cur], P->r_dev + cur))) return rc;
     // ∇ψ needs A_J P_J for the re-thresholded J: gather with r read on the device
-    if ((rc = launch_gather_dev(P, P->J[cur], P->PJ[cur], P->r_dev + cur))) return rc;
-    // K1e wrote G scalar partials; the gather wrote kGatherDevGrid (flagged) vector partials
-    if ((rc = launch_eval(P, P->y[cur], sc, 1, P->gax_valid, kGatherDevGrid, P->g[cur], P->r_dev + cur, 0))) return rc;
+    if ((rc = launch_gather_vec(P, P->J[cur], P->PJ[cur], P->r_dev + cur))) return rc;
+    // K1e wrote G scalar partials; the gather wrote the finished vector A_J P_J (part_vec row 0)
+    if ((rc = launch_eval(P, P->y[cur], sc, 1, nullptr, 1, P->g[cur], P->r_dev + cur, 0))) return rc;
     if ((rc = fetch_eval(P, 0, &ev))) return rc;
     S->psi_evals++;
 
@@ -1107,9 +1108,9 @@ int solve_core(ssnal_en_problem* P, double l1, double l2, double sigma0, double 
         cur = tr;
         wcur = wbt;  // materialised w + s (w1 − w)
         // ∇ψ at the accepted point needs A_J P_J for the re-thresholded J (K2)
-        if ((rc = launch_gather_dev(P, P->J[cur], P->PJ[cur], P->r_dev + cur))) return rc;
+        if ((rc = launch_gather_vec(P, P->J[cur], P->PJ[cur], P->r_dev + cur))) return rc;
         // scalar partials in part_scal still belong to the accepted K1e launch
-        if ((rc = launch_eval(P, P->y[cur], sc, 1, P->gax_valid, kGatherDevGrid, P->g[cur], P->r_dev + cur, 0)))
+        if ((rc = launch_eval(P, P->y[cur], sc, 1, nullptr, 1, P->g[cur], P->r_dev + cur, 0)))
           return rc;
         if ((rc = fetch_eval(P, 0, &ev))) return rc;
       }
@@ -1210,9 +1211,8 @@ int capture_graph(ssnal_en_problem* P, cudaGraph_t G) {
   P->launches++;
   if ((rc = launch_k1e(P, P->w[0], nullptr, 0.0, P->x, none, nullptr, &C->sc, nullptr))) return rc;
   if ((rc = launch_finalize(P, P->J[0], P->PJ[0], P->r_dev + 0))) return rc;
-  if ((rc = launch_gather_dev(P, P->J[0], P->PJ[0], P->r_dev + 0))) return rc;
-  if ((rc = launch_eval(P, P->y[0], none, 1, P->gax_valid, kGatherDevGrid, P->g[0], P->r_dev + 0, 0, nullptr,
-                        nullptr, &C->sc)))
+  if ((rc = launch_gather_vec(P, P->J[0], P->PJ[0], P->r_dev + 0))) return rc;
+  if ((rc = launch_eval(P, P->y[0], none, 1, nullptr, 1, P->g[0], P->r_dev + 0, 0, nullptr, nullptr, &C->sc)))
     return rc;
   k_ctl_inner_begin<<<1, 1, 0, P->st>>>(C, P->ev_dev + 0, m, P->nsm, P->W_splits, P->info, h_inner);
   P->launches++;
@@ -1263,9 +1263,9 @@ int capture_graph(ssnal_en_problem* P, cudaGraph_t G) {
     k_accept<<<2 * P->nsm, 256, 0, P->st>>>(C, m, n, P->y[0], P->y[1], P->g[0], P->g[1], P->J[0], P->J[1],
                                               P->PJ[0], P->PJ[1], P->r_dev, P->w[0], P->w[1], P->w[2], P->ev_dev);
     P->launches++;
-    if ((rc = launch_gather_dev(P, P->J[0], P->PJ[0], P->r_dev + 0, &C->need_grad))) return rc;
-    if ((rc = launch_eval(P, P->y[0], none, 1, P->gax_valid, kGatherDevGrid, P->g[0], P->r_dev + 0, 0, nullptr,
-                          nullptr, &C->sc, &C->need_grad)))
+    if ((rc = launch_gather_vec(P, P->J[0], P->PJ[0], P->r_dev + 0, &C->need_grad))) return rc;
+    if ((rc = launch_eval(P, P->y[0], none, 1, nullptr, 1, P->g[0], P->r_dev + 0, 0, nullptr, nullptr, &C->sc,
+                          &C->need_grad)))
       return rc;
     k_ctl_inner_end<<<1, 1, 0, P->st>>>(C, P->ev_dev + 0, m, P->nsm, P->W_splits, P->info, h_inner);
     P->launches++;
@@ -1890,7 +1890,7 @@ int ssnal_en_model_select(ssnal_en_problem* P, double l2, double* xdb_out, ssnal
   } else if (r < m) {
     // ν: factor A_JᵀA_J + λ2 I with A_J appended as m rows: ν = ‖A_J L⁻ᵀ‖_F²
     const int N = (int)r, NR = (int)(r + m);
-    const int nt = (N + 31) / 32, tiles = nt * (nt + 1) / 2, ns = splits(tiles, m);
+    const int tiles = gram_tiles(N), ns = splits(tiles, m);
     with_acc(P, [&](auto acc) {
       k_gram<true><<<gram_grid(P, tiles * ns), 256, 0, P->st>>>(acc, m, J, r, P->W, nullptr, tiles, ns, nullptr);
       return 0;
@@ -1907,7 +1907,7 @@ int ssnal_en_model_select(ssnal_en_problem* P, double l2, double* xdb_out, ssnal
     k_frob<<<1, 1024, 0, P->st>>>(P->Msel, NR, r, m, r, frob);
     // OLS de-biasing: factor A_JᵀA_J with rhs row A_Jᵀb; v → P->u
     const int64_t nout = r + 1;
-    const int nt2 = (int)((nout + 31) / 32), tiles2 = nt2 * (nt2 + 1) / 2, ns2 = splits(tiles2, m);
+    const int tiles2 = gram_tiles(nout), ns2 = splits(tiles2, m);
     with_acc(P, [&](auto acc) {
       k_gram<true><<<gram_grid(P, tiles2 * ns2), 256, 0, P->st>>>(acc, m, J, r, P->W, P->b, tiles2, ns2, nullptr);
       return 0;
@@ -1928,7 +1928,7 @@ int ssnal_en_model_select(ssnal_en_problem* P, double l2, double* xdb_out, ssnal
   } else {
     // r ≥ m: ν = tr(K (K + λ2 I)⁻¹), K = A_J A_Jᵀ, = m − λ2 ‖L⁻¹‖_F² with I_m appended
     const int N = (int)m, NR = (int)(2 * m);
-    const int nt = (int)((m + 31) / 32), tiles = nt * (nt + 1) / 2, ns = splits(tiles, r);
+    const int tiles = gram_tiles(m), ns = splits(tiles, r);
     with_acc(P, [&](auto acc) {
       k_gram<false><<<gram_grid(P, tiles * ns), 256, 0, P->st>>>(acc, m, J, r, P->W, nullptr, tiles, ns, nullptr);
       return 0;
