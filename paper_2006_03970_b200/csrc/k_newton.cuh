@@ -611,12 +611,17 @@ SSN_DEV void diag_factor4(const double* S, double* M, int ld, int n0, int kn, in
     }
   }
   if (bad && lane == 0) atomicExch(info, 1);
+  if (!M) asm volatile("bar.sync 2, 128;" ::: "memory");  // every warp has read S before L overwrites it
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
     const int c = 8 * w + q;
-    if (lane < nrow && c < kn && c <= lane) M[(int64_t)(n0 + lane) + (int64_t)(n0 + c) * ld] = a[q];
+    if (M) {
+      if (lane < nrow && c < kn && c <= lane) M[(int64_t)(n0 + lane) + (int64_t)(n0 + c) * ld] = a[q];
+    } else {  // L into the smem tile itself (DSMEM-resident factor): rows < nrow, cols < kn, else 0
+      const_cast<double*>(S)[lane * TLD + c] = (lane < nrow && c < kn && c <= lane) ? a[q] : 0.0;
+    }
     const double wv = (c < kn && lane < kn) ? wr[q] : (lane == c ? 1.0 : 0.0);  // pad: identity
-    Wout[c * CHT + lane] = wv;
+    if (Wout) Wout[c * CHT + lane] = wv;
     if (Wsm) Wsm[c * TLD + lane] = wv;
   }
 }
@@ -714,10 +719,10 @@ __global__ void __launch_bounds__(256, 1) k_chol_cluster(double* M, int N, int N
                                                          double scale, const double* __restrict__ dotv,
                                                          double* dot_out, double* Winv, int* info,
                                                          const double* __restrict__ ybase, double* __restrict__ yt,
-                                                         const DirGeo* geo, int want, int* kflag) {
+                                                         const DirGeo* geo, int want, int* kflag, int nmin) {
   namespace cg = cooperative_groups;
   if (geo) {  // graph mode: order from the device geometry; whole cluster exits together
-    if (geo->branch != want) return;
+    if (geo->branch != want || geo->N < nmin) return;
     N = geo->N;
     NR = geo->NR;
     ld = geo->ld;

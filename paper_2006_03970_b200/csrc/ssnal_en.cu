@@ -19,6 +19,7 @@
 #include "k_aty.cuh"
 #include "k_ctl.cuh"
 #include "k_newton.cuh"
+#include "k_chol_dsm.cuh"
 #include "ssnal_en.h"
 
 using namespace ssn;
@@ -277,6 +278,9 @@ struct ssnal_en_problem {
   uint32_t stage_elems = 0, xstage_elems = 0;
   int cluster = 16;
   size_t chol_smem = 0;
+  int use_dsm = 1;   // option chol_dsm: DSMEM-resident K4 for N ≤ 512 when schedulable
+  int dsm_ok = 0;    // … schedulable on this device
+  int chol_dsm = 0;  // use_dsm && dsm_ok
   int gax_grid = 0;
   // device buffers
   double* w[3] = {nullptr, nullptr, nullptr};  // current / trial / backtrack
@@ -468,6 +472,27 @@ int configure(ssnal_en_problem* P) {
     }
     P->cluster = want < 1 ? 1 : want;
   }
+  // DSMEM-resident K4 (N ≤ 512): needs a schedulable 16-CTA cluster with ~175 KB smem per CTA
+  P->dsm_ok = 0;
+  {
+    CK(cudaFuncSetAttribute(k_chol_dsm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDsmSmem));
+    CK(cudaFuncSetAttribute(k_chol_dsm, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(kDsmCS);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = kDsmSmem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = kDsmCS;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int nclus = 0;
+    if (cudaOccupancyMaxActiveClusters(&nclus, k_chol_dsm, &cfg) == cudaSuccess && nclus >= 1) P->dsm_ok = 1;
+    cudaGetLastError();
+  }
+  P->chol_dsm = P->use_dsm && P->dsm_ok;
   return SSNAL_OK;
 }
 
@@ -762,15 +787,50 @@ int launch_chol_ex(ssnal_en_problem* P, double* M, int N, int NR, int ld, double
   cfg.numAttrs = 1;
   const DirGeo* nog = nullptr;
   CK(cudaLaunchKernelEx(&cfg, k_chol_cluster, M, N, NR, ld, out, scale, dotv, dot_out, P->Winv, info, ybase, yt, nog,
-                        0, P->kflag));
+                        0, P->kflag, 0));
+  P->launches++;
+  return SSNAL_OK;
+}
+
+// DSMEM-resident K4 (k_chol_dsm.cuh): same contract as the k_chol_cluster launch below.  Used for
+// N ≤ kDsmUseMax, where it is faster (N = 100: 35 vs 47 µs; crossover near N = 192, and N = 500
+// takes ~300 vs ~211 µs: its per-owner update load is uneven).
+constexpr int kDsmUseMax = 160;
+int launch_chol_dsm(ssnal_en_problem* P, double* M, int N, double* out, double scale, const double* dotv,
+                    double* dot_out, const double* ybase, double* yt, const DirGeo* geo, int want) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(kDsmCS);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = kDsmSmem;
+  cfg.stream = P->st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = kDsmCS;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, k_chol_dsm, (const double*)M, N, N + 1, out, scale, dotv, dot_out, P->info, ybase, yt,
+                        geo, want, kDsmUseMax));
   P->launches++;
   return SSNAL_OK;
 }
 
 // Cluster Cholesky + both triangular solves: M holds the matrix (ld = N+1) and the rhs in row N.
+// Host mode: the DSMEM-resident kernel for N ≤ 512, else k_chol_cluster.  Graph mode (geo): the
+// DSMEM kernel predicated on N ≤ 512 and, when m > 512, k_chol_cluster predicated on N > 512.
 int launch_chol(ssnal_en_problem* P, double* M, int N, double* out, double scale, const double* dotv,
                 double* dot_out, const double* ybase = nullptr, double* yt = nullptr, const DirGeo* geo = nullptr,
                 int want = 0) {
+  int nmin = 0;
+  if (P->chol_dsm) {
+    if (geo || N <= kDsmUseMax) {
+      int rc = launch_chol_dsm(P, M, N, out, scale, dotv, dot_out, ybase, yt, geo, want);
+      if (rc) return rc;
+    }
+    if (geo ? P->m <= kDsmUseMax : N <= kDsmUseMax) return SSNAL_OK;
+    nmin = kDsmUseMax + 1;
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(P->cluster);
   cfg.blockDim = dim3(256);
@@ -784,7 +844,7 @@ int launch_chol(ssnal_en_problem* P, double* M, int N, double* out, double scale
   cfg.attrs = at;
   cfg.numAttrs = 1;
   CK(cudaLaunchKernelEx(&cfg, k_chol_cluster, M, N, N + 1, N + 1, out, scale, dotv, dot_out, P->Winv, P->info,
-                        ybase, yt, geo, want, P->kflag));
+                        ybase, yt, geo, want, P->kflag, nmin));
   P->launches++;
   return SSNAL_OK;
 }
@@ -1696,7 +1756,11 @@ int ssnal_en_set_option(ssnal_en_problem* P, const char* key, double v) {
     P->cg_maxit = (int)v;
     drop_graph(P);
   }
-  else if (k == "cluster_size" && (v == 1 || v == 2 || v == 4 || v == 8 || v == 16)) {
+  else if (k == "chol_dsm" && (v == 0 || v == 1)) {
+    P->use_dsm = (int)v;
+    P->chol_dsm = P->use_dsm && P->dsm_ok;
+    drop_graph(P);  // the K4 variant is baked into the graph
+  } else if (k == "cluster_size" && (v == 1 || v == 2 || v == 4 || v == 8 || v == 16)) {
     P->cluster = (int)v;
     drop_graph(P);  // the cluster launch configuration is baked into the graph
   } else {
@@ -1716,6 +1780,7 @@ double ssnal_en_get_info(const ssnal_en_problem* P, const char* key) {
   if (k == "k1_grid") return P->G;
   if (k == "k1_smem") return (double)P->k1_smem;
   if (k == "cluster_size") return P->cluster;
+  if (k == "chol_dsm") return P->chol_dsm;
   if (k == "num_sms") return P->nsm;
   if (k == "graph") return P->use_graph;
   if (k == "format") return P->fmt;
