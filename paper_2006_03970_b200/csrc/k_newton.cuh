@@ -555,9 +555,10 @@ SSN_DEV void diag_factor4(const double* S, double* M, int ld, int n0, int kn, in
           wbp[pp] = Wp[pp * 33 + lane];
         }
       }
+      if (blk > 0) {  // rank-8 update of this block's columns from block blk − 1, before any pivot:
+                      // eight independent chains, so only pivot 0 waits for one of them
 #pragma unroll
-      for (int p = 0; p < 8; ++p) {
-        if (blk > 0) {  // lazy rank-8 update of column p from block blk − 1
+        for (int p = 0; p < 8; ++p)
 #pragma unroll
           for (int pp = 0; pp < 8; ++pp) {
             const double l = Lp[(8 * w + p) * 9 + pp];
@@ -565,7 +566,9 @@ SSN_DEV void diag_factor4(const double* S, double* M, int ld, int n0, int kn, in
             a[p] = fma(-lrp[pp], l, a[p]);
             wr[p] = fma(-l, wbp[pp], wr[p]);
           }
-        }
+      }
+#pragma unroll
+      for (int p = 0; p < 8; ++p) {
         const int j = 8 * blk + p;
         double d = dgw[p];
         bad |= (j < kn) && !(d > 0.0);
