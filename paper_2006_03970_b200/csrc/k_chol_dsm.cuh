@@ -235,15 +235,11 @@ __global__ void __launch_bounds__(256, 1) k_chol_dsm(const double* __restrict__ 
       const int s = bcast[quad];
       qbar();
       if (s >= nt) break;
-      if (s == 2) DCLK(10);
       lwait(upd + s, j);
-      if (s == 2) DCLK(11);
       double af[8];
       load_af(T + s * kTileD, af);
       strip_af(T + s * kTileD, af, Wj, 1.0, false);
-      if (s == 2) DCLK(12);
       qrelease(ready + s);
-      if (s == 2) DCLK(13);
     }
     if (quad == 0) DSTAMP(5); else DSTAMP(9);
   }

@@ -38,8 +38,7 @@ int main() {
     const int ntc = (N + 31) / 32;
     for (int j = 0; j < ntc; ++j) {
       auto f = [&](int i) { return t[j][i] >= t0 ? (t[j][i] - t0) * 1e-3 : -1.0; };
-      printf("  %2d: %5.1f %5.1f | %6.1f %6.1f %6.1f %6.1f %6.1f %6.1f %6.1f %6.1f | trsm(s=2) cycles: wait %lld strip %lld release %lld\n", j, f(0), f(1), f(2), f(8), f(3), f(4), f(5), f(9), f(6), f(7),
-             (long long)(t[j][11] - t[j][10]), (long long)(t[j][12] - t[j][11]), (long long)(t[j][13] - t[j][12]));
+      printf("  %2d: %5.1f %5.1f | %6.1f %6.1f %6.1f %6.1f %6.1f %6.1f %6.1f %6.1f\n", j, f(0), f(1), f(2), f(8), f(3), f(4), f(5), f(9), f(6), f(7));
     }
     cudaFree(dM); cudaFree(dout); cudaFree(info);
   }
