@@ -18,8 +18,9 @@ this host, rank 0 only), clocks sampled during the timed region, gpu_launches.
 
 --impl reference: the base contract's reference arm is, for this paper-only tier, the CPU
 oracle (oracle/), timed on the host cores on the same workload (rank 0 only).
-Multi-GPU (torchrun): the path does not shard; each rank solves
-its own replica; value = max over ranks; scaling "weak".
+Multi-GPU (torchrun): by default each rank solves its own replica (value = max over ranks,
+scaling "weak"); with --shard the ranks split the columns of one problem and
+exchange the cross-column sums by NCCL all-reduce (scaling "strong").
 """
 from __future__ import annotations
 
@@ -170,6 +171,16 @@ def bench_ours(args, rank, world, local_rank):
         torch.cuda.synchronize()
         P = Problem.from_geno_device(dA.data_ptr(), stride, dtab.data_ptr(), db.data_ptr(), m, n, stream.cuda_stream,
                                      keep=(dA, dtab, db))
+    elif args.shard:  # §8(f3): this rank owns columns [j0, j1); cross-column sums by NCCL all-reduce
+        from paper_2006_03970_b200.shard import column_range, torch_allreduce
+
+        j0, j1 = column_range(cfg.n, rank, world)
+        n = j1 - j0
+        dA = torch.empty((n, m), dtype=torch.float64, device="cuda")
+        synth.fill_device(cfg, dA.data_ptr(), stream.cuda_stream, j0, j1)
+        torch.cuda.synchronize()
+        P = Problem.from_device(dA.data_ptr(), db.data_ptr(), m, n, stream.cuda_stream, keep=(dA, db))
+        P.set_comm(torch_allreduce(), rank, world)
     else:
         dA = torch.empty((n, m), dtype=torch.float64, device="cuda")
         synth.fill_device(cfg, dA.data_ptr(), stream.cuda_stream)
@@ -234,7 +245,7 @@ def bench_ours(args, rank, world, local_rank):
         e2e = {"value": max_over_ranks(statistics.median(e2e_times)), "unit": "s",
                "h2d_bytes_per_step": int(codes_h.nbytes + tab_h.nbytes + 8 * m),
                "d2h_bytes_per_step": 8 * n * len(cfg.cs)}
-    elif not args.no_e2e:
+    elif not args.no_e2e and not args.shard:
         A_host = torch.empty((n, m), dtype=torch.float64, pin_memory=True)
         A_host.copy_(dA.cpu())
         A_np = A_host.numpy()
@@ -283,17 +294,19 @@ def bench_ours(args, rank, world, local_rank):
         "warmup": args.warmup,
         "ms_per_step": t_step * 1e3,
         "higher_is_better": False,
-        "scaling": "weak",
+        "scaling": "strong" if args.shard else "weak",
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (synth/, seeded; generated in HBM)",
-        "config": {"workload": f"{cfg.name}: m={m} n={n} " + ("warm-started path c=" + ",".join(f"{c:.3g}" for c in cfg.cs)
+        "config": {"workload": f"{cfg.name}: m={m} n={cfg.n} " + ("warm-started path c=" + ",".join(f"{c:.3g}" for c in cfg.cs)
                                                               if cfg.path else "c=" + ",".join(str(c) for c in cfg.cs)),
-                   "m": m, "n": n, "alpha": cfg.alpha, "tol": cfg.tol, "sigma0": cfg.sigma0,
+                   "m": m, "n": cfg.n, "alpha": cfg.alpha, "tol": cfg.tol, "sigma0": cfg.sigma0,
                    "l2_policy": f"A = {8 * m * n / 1e6:.0f} MB > 126 MB L2 (no flush needed)",
-                   "parallelism": f"replicas x{world}",
+                   "parallelism": (f"column-sharded x{world}: rank q owns n/{world} columns, NCCL all-reduce of the "
+                                   "per-evaluation partials and the Newton-system exchange (SURVEY 8(f3))"
+                                   if args.shard else f"replicas x{world}"),
                    "control": ("device-resident, one CUDA graph per solve (nested conditional WHILE)"
-                               if args.control == "graph" else "host-driven (per-evaluation readback)"),
+                               if args.control == "graph" and not args.shard else "host-driven (per-evaluation readback)"),
                    "storage": ("packed 2-bit genotype codes + per-column tables (SURVEY 8(f4))" if args.geno
                                else "fp64 column-major"),
                    "newton_strategy": ("exact (Eq. 18/19); CG when min(m, r) > 1e4 (P:379)" if args.cg_ratio == 0
@@ -313,7 +326,9 @@ def bench_ours(args, rank, world, local_rank):
                         "res1": s["res_kkt1"], "res3": s["res_kkt3"], "gap": s["gap"]}
                        for c, s in zip(cfg.cs, last_stats)],
     }
-    if rank == 0 and not args.no_cpu and world == 1 and not args.geno:
+    if args.shard:
+        res["config"]["n_local"] = n
+    if rank == 0 and not args.no_cpu and world == 1 and not args.geno and not args.shard:
         res["cpu_baseline"] = cpu_baseline(cfg, b_host, A_host.numpy() if A_host is not None else dA.cpu().numpy())
     P.close()
     return res
@@ -507,6 +522,8 @@ def main():
     ap.add_argument("--sweep", action="store_true", help="K1 bandwidth sweep instead of the TTS bench")
     ap.add_argument("--select", action="store_true", help="lambda path with model selection (SURVEY 8(f1))")
     ap.add_argument("--cv", type=int, default=0, help="with --select: k-fold cross-validation over a 20-point grid")
+    ap.add_argument("--shard", action="store_true",
+                    help="column-sharded solve across the ranks (SURVEY 8(f3)) instead of replicas")
     ap.add_argument("--sweep-n", default="100000,200000,500000,1000000,2000000,5000000,10000000")
     ap.add_argument("--sweep-reps", type=int, default=20)
     args = ap.parse_args()
@@ -532,15 +549,23 @@ def main():
 
     import torch.distributed as dist
 
-    if world > 1:
+    if world > 1 or args.shard:
         import torch
 
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl")
+        if world > 1:
+            dist.init_process_group("nccl")
+        else:  # a one-rank NCCL group, so the sharded path runs its real all-reduces
+            import socket
+
+            with socket.socket() as so:
+                so.bind(("127.0.0.1", 0))
+                port = so.getsockname()[1]
+            dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
     res = bench_ours(args, rank, world, local_rank)
     if rank == 0:
         print(json.dumps(res), flush=True)
-    if world > 1:
+    if dist.is_initialized():
         dist.destroy_process_group()
 
 

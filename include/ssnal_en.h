@@ -39,6 +39,9 @@ enum {
 
 typedef struct ssnal_en_problem ssnal_en_problem; /* opaque handle */
 
+/* Caller-supplied all-reduce for column-sharded handles (see ssnal_en_set_comm). */
+typedef int (*ssnal_en_allreduce_fn)(void* ctx, double* buf, int64_t count, int op, void* stream);
+
 typedef struct {
   int32_t status;          /* SSNAL_OK / SSNAL_NOT_CONVERGED / SSNAL_ENUMERIC            */
   int32_t outer_iters;     /* augmented-Lagrangian iterations (the paper's "(k)", R23)   */
@@ -189,6 +192,26 @@ int ssnal_en_model_select(ssnal_en_problem* p, double lambda2, double* xdb_out, 
  * touch the handle's last solution.  EINVAL for null arguments. */
 int ssnal_en_residual(ssnal_en_problem* p, const double* x, double* rss_out);
 int ssnal_en_residual_device(ssnal_en_problem* p, const double* x_dev, double* rss_out);
+
+/* Column-sharded solves ("the path shards naturally by column blocks of A").
+ * Rank q of nranks owns a contiguous block of columns; its handle is created on that block alone
+ * (n = the block's column count, any create call).  Every cross-column quantity of Algorithm 1 is
+ * a sum over the blocks and goes through the caller's all-reduce, called on the handle's stream
+ * order: per ψ evaluation the partial m-vector A_J P_J, four scalar partial sums and |J| (m + 5
+ * doubles); per Newton step either the active columns (0 < r < m: each rank's A_J placed at its
+ * prefix offset of an r × m buffer, so the sum is an all-gather; SMW Eq. (19) on the result) or
+ * the partial m × m Gram A_J A_Jᵀ (r ≥ m, Eq. (18)); plus the warm-start A x0, the objective and
+ * λmax.  All ranks therefore hold identical reduced values and take identical control decisions;
+ * solves run host-driven (graph mode and the CG strategy are not used on a sharded handle).
+ *   fn(ctx, buf, count, op, stream): all-reduce count doubles at the DEVICE pointer buf in place,
+ *     op 0 = sum, 1 = max, ordered after the work already queued on `stream` (cudaStream_t) and
+ *     complete before work queued after the call; return 0 on success.  Called only from inside
+ *     this library's calls, on the calling thread.
+ *   Each rank must call ssnal_en_solve* with the same λ1, λ2, σ0, tol and options; x0 / x_out are
+ *   the rank's slices (x0 may be NULL on some ranks: missing slices count as zero).
+ * set_comm exchanges λmax (lambda_max_l1 becomes the global value).  rank ∈ [0, nranks).  Stats:
+ * active, primal_obj, gap, res_kkt* are global.  Returns SSNAL_EINVAL for bad arguments. */
+int ssnal_en_set_comm(ssnal_en_problem* p, ssnal_en_allreduce_fn fn, void* ctx, int rank, int nranks);
 
 void ssnal_en_destroy(ssnal_en_problem* p);
 

@@ -1178,10 +1178,63 @@ __global__ void k_init_y(int64_t m, const double* __restrict__ bvec, const doubl
   for (int64_t k = threadIdx.x; k < m; k += blockDim.x) {
     double s = 0.0;
     for (int b = 0; b < nparts; ++b)
-      if (valid[b]) s += parts[(size_t)b * m + k];
+      if (!valid || valid[b]) s += parts[(size_t)b * m + k];
     y[k] = warm ? (-1.0 * bvec[k] + s) : 0.0;
   }
 }
+// §8(f3) exchange record of one evaluation: out[0, m) = Σ_b part_vec[b] (ascending b, valid ones;
+// none if nparts = 0), out[m, m+4) = Σ_q part_scal[q][·] (ascending q), out[m+4] = r (local count).
+__global__ void __launch_bounds__(1024) k_prereduce(int64_t m, const double* __restrict__ part_vec,
+                                                    const int* __restrict__ valid, int nparts,
+                                                    const double* __restrict__ part_scal, int nscal,
+                                                    const int64_t* __restrict__ r_dev, double* __restrict__ out) {
+  for (int64_t k = threadIdx.x; k < m; k += blockDim.x) {
+    double s = 0.0;
+    for (int b = 0; b < nparts; ++b)
+      if (!valid || valid[b]) s += part_vec[(size_t)b * m + k];
+    out[k] = s;
+  }
+  if (threadIdx.x < 4) {
+    double s = 0.0;
+    for (int q = 0; q < nscal; ++q) s += part_scal[q * 4 + threadIdx.x];
+    out[m + threadIdx.x] = s;
+  }
+  if (threadIdx.x == 4) out[m + 4] = r_dev ? (double)*r_dev : 0.0;
+}
+__global__ void k_to_i64(const double* src, int64_t* dst) { *dst = (int64_t)*src; }
+// columns A[:, J[a]], a < r, densely into out (column-major, m × r) — the local share of a gather
+template <class Acc>
+__global__ void k_pack_cols(const Acc A, int64_t m, const int32_t* __restrict__ J, int64_t r, double* __restrict__ out) {
+  for (int64_t a = blockIdx.x; a < r; a += gridDim.x) {
+    const auto col = A.col(J[a]);
+    for (int64_t k = threadIdx.x; k < m; k += blockDim.x) out[a * m + k] = col.ld(k);
+  }
+}
+__global__ void k_iota(int32_t* v, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) v[i] = (int32_t)i;
+}
+
+// x[J[i]] = P[i] for i < *r_dev, and (Jx, Px, *rx_dev) ← (J, P, *r_dev): the x-update with the
+// count on the device (sharded handles)
+__global__ void k_scatter_dev(const int32_t* __restrict__ J, const double* __restrict__ PJ, const int64_t* r_dev,
+                              double* __restrict__ x, int32_t* __restrict__ Jx, double* __restrict__ Px,
+                              int64_t* rx_dev) {
+  const int64_t r = *r_dev;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nth = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = tid; i < r; i += nth) {
+    const int32_t j = J[i];
+    const double v = PJ[i];
+    x[j] = v;
+    Jx[i] = j;
+    Px[i] = v;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    *rx_dev = r;
+  }
+}
+
 __global__ void k_scatter(const int32_t* __restrict__ idx, const double* __restrict__ v, int64_t cnt, double* x) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < cnt) x[idx[i]] = v[i];

@@ -329,6 +329,15 @@ struct ssnal_en_problem {
   int max_outer = 100, max_inner = 100, max_bt = 50, init_mode = 1, time_k1 = 0, certify = 0;
   double cg_ratio = 0.0, cg_threshold = 1e4, cg_tol = 1e-10;  // Newton strategy (R32)
   int cg_maxit = 1000;
+  // §8(f3) column sharding: this handle holds one block of columns; every cross-column sum goes
+  // through the caller's all-reduce (host-driven control, identical decisions on every rank)
+  ssnal_en_allreduce_fn comm_fn = nullptr;
+  void* comm_ctx = nullptr;
+  int comm_rank = 0, comm_size = 0;  // comm_size > 0: sharded
+  double* xbuf = nullptr;            // exchange buffer, m² + 2m + 64 doubles (device)
+  int64_t* rg_dev = nullptr;         // global r for the eval record
+  int32_t* iota = nullptr;           // 0 … m−1: indices of the gathered active columns
+  double* comm_host = nullptr;       // pinned staging (nranks + 8 doubles)
   int inner_tol_mode = 0;  // 1: tol_in = max(tol, 0.1 res3 at the outer start) (R37)
   int inject_fail = 0;    // test hook: the next N factorisations of a solve report failure
   double jitter = 1e-10;  // factor retry M_ii ← M_ii (1 + jitter) after a non-positive pivot (R36)
@@ -727,11 +736,17 @@ int launch_gather_dev(ssnal_en_problem* P, const int32_t* J, const double* coef,
 
 int launch_eval(ssnal_en_problem* P, const double* y, const Scal& sc, int with_grad, const int* valid, int nparts,
                 double* g_out, const int64_t* r_dev, int slot, const double* gd_src = nullptr,
-                const int* info_src = nullptr, const Scal* scp = nullptr, const int* pred = nullptr) {
+                const int* info_src = nullptr, const Scal* scp = nullptr, const int* pred = nullptr,
+                const double* vec = nullptr, const double* scal = nullptr, int nscal = 0) {
   const unsigned nblk = (unsigned)((P->m + 31) / 32);
   if (!P->capturing) ++P->ev_seq;
+  if (!vec) vec = P->part_vec;
+  if (!scal) {
+    scal = P->part_scal;
+    nscal = P->G;
+  }
   // graph mode: no mapped host mirror (decisions are taken on the device)
-  k_eval_reduce<<<nblk * kEvalCS, K5_THREADS, 0, P->st>>>(P->m, y, P->b, P->part_vec, valid, nparts, P->part_scal, P->G, sc,
+  k_eval_reduce<<<nblk * kEvalCS, K5_THREADS, 0, P->st>>>(P->m, y, P->b, vec, valid, nparts, scal, nscal, sc,
                                                  P->nb, with_grad, g_out, r_dev, P->ev_dev + slot, P->blk,
                                                  P->ticket, gd_src, info_src,
                                                  P->capturing ? nullptr : P->ev_host_dev + slot, P->ev_seq, scp, pred,
@@ -739,6 +754,44 @@ int launch_eval(ssnal_en_problem* P, const double* y, const Scal& sc, int with_g
   P->launches++;
   CKL();
   return SSNAL_OK;
+}
+
+// ---- §8(f3) column sharding: exchanges through the caller's all-reduce ----
+bool sharded(const ssnal_en_problem* P) { return P->comm_size > 0; }
+
+int comm_allreduce(ssnal_en_problem* P, double* buf, int64_t count, int op) {
+  CKL();
+  const int rc = P->comm_fn(P->comm_ctx, buf, count, op, (void*)P->st);
+  if (rc) {
+    set_err("all-reduce callback failed (%d)", rc);
+    return SSNAL_ECUDA;
+  }
+  return SSNAL_OK;
+}
+
+// xbuf = [Σ local partial vectors (m) | Σ local scalar partials (4) | local r] summed over the ranks;
+// rg_dev = the global r.  vec/nparts/valid: the partial m-vectors (nparts = 0: none).
+int exchange_eval(ssnal_en_problem* P, const double* vec, const int* valid, int nparts, const double* scal, int nscal,
+                  const int64_t* r_local) {
+  k_prereduce<<<1, 1024, 0, P->st>>>(P->m, vec, valid, nparts, scal, nscal, r_local, P->xbuf);
+  P->launches++;
+  int rc = comm_allreduce(P, P->xbuf, P->m + 5, 0);
+  if (rc) return rc;
+  k_to_i64<<<1, 1, 0, P->st>>>(P->xbuf + P->m + 4, P->rg_dev);
+  P->launches++;
+  CKL();
+  return SSNAL_OK;
+}
+
+// launch_eval on the global sums when sharded (partial vectors: part_vec rows, `valid` flags)
+int eval_g(ssnal_en_problem* P, const double* y, const Scal& sc, int with_grad, const int* valid, int nparts,
+           double* g_out, const int64_t* r_dev, int slot, const double* gd_src = nullptr,
+           const int* info_src = nullptr) {
+  if (!sharded(P)) return launch_eval(P, y, sc, with_grad, valid, nparts, g_out, r_dev, slot, gd_src, info_src);
+  int rc = exchange_eval(P, nparts ? P->part_vec : nullptr, valid, nparts, P->part_scal, P->G, r_dev);
+  if (rc) return rc;
+  return launch_eval(P, y, sc, with_grad, nullptr, nparts ? 1 : 0, g_out, P->rg_dev, slot, gd_src, info_src, nullptr,
+                     nullptr, P->xbuf, P->xbuf + P->m, 1);
 }
 
 // Wait for the EvalOut of the most recent launch_eval on `slot`: spin on the mapped host copy's
@@ -897,9 +950,94 @@ unsigned reduce_grid(ssnal_en_problem* P, int64_t tot) {
 
 // Newton direction for (J, r) at gradient g: d ← solution, *gd_dev ← gᵀd (Eq. (18)/(19)); if yt,
 // also the Armijo trial y_t = y + d (fused into the last kernel of each branch).
+// §8(f3): the Newton direction of a sharded handle from the global r.  0 < r < m: the ranks' active
+// columns are all-gathered (each placed at its prefix offset of an r × m buffer, summed) and the
+// SMW form Eq. (19) runs on them; r ≥ m: the partial Grams A_J A_Jᵀ are summed (Eq. (18)).
+int newton_direction_sharded(ssnal_en_problem* P, const int32_t* J, int64_t rg, const int64_t* r_loc_dev,
+                             const double* g, double kappa, double* d, double* gd_dev, int* branch, const double* y,
+                             double* yt, double jit) {
+  const int64_t m = P->m;
+  int rc;
+  if (rg == 0) {
+    *branch = 0;
+    k_neg_copy<<<1, 1024, 0, P->st>>>(m, g, d, g, gd_dev, y, yt, nullptr);
+    P->launches++;
+    CKL();
+    return SSNAL_OK;
+  }
+  CK(cudaMemcpyAsync(P->comm_host, r_loc_dev, 8, cudaMemcpyDeviceToHost, P->st));
+  CK(cudaStreamSynchronize(P->st));
+  int64_t rl;
+  memcpy(&rl, P->comm_host, 8);
+  CK(cudaMemsetAsync(P->info, 0, sizeof(int), P->st));
+  if (rg < m) {
+    *branch = 1;
+    const int R = P->comm_size;
+    CK(cudaMemsetAsync(P->xbuf, 0, (size_t)R * 8, P->st));
+    P->comm_host[0] = (double)rl;
+    CK(cudaMemcpyAsync(P->xbuf + P->comm_rank, P->comm_host, 8, cudaMemcpyHostToDevice, P->st));
+    if ((rc = comm_allreduce(P, P->xbuf, R, 0))) return rc;
+    CK(cudaMemcpyAsync(P->comm_host + 8, P->xbuf, (size_t)R * 8, cudaMemcpyDeviceToHost, P->st));
+    CK(cudaStreamSynchronize(P->st));
+    int64_t off = 0, tot = 0;
+    for (int q = 0; q < R; ++q) {
+      const int64_t c = (int64_t)P->comm_host[8 + q];
+      if (q < P->comm_rank) off += c;
+      tot += c;
+    }
+    if (tot != rg) {
+      set_err("sharded active counts disagree (%lld vs %lld)", (long long)tot, (long long)rg);
+      return SSNAL_ECUDA;
+    }
+    double* GA = P->xbuf;  // gathered A_J, column-major m × rg
+    CK(cudaMemsetAsync(GA, 0, (size_t)rg * m * 8, P->st));
+    if (rl > 0) {
+      with_acc(P, [&](auto acc) {
+        k_pack_cols<<<(unsigned)(rl < 2 * P->nsm ? rl : 2 * P->nsm), 256, 0, P->st>>>(acc, m, J, rl, GA + off * m);
+        return 0;
+      });
+      P->launches++;
+    }
+    if ((rc = comm_allreduce(P, GA, rg * m, 0))) return rc;
+    DirGeo geo = make_geo(rg, m, P->nsm, P->W_splits, kappa, 1.0 / kappa, 0.0, INFINITY);
+    geo.jit = jit;
+    const AccA ga{GA, m};
+    k_gram<true><<<gram_grid(P, geo.tiles * geo.ns), 256, 0, P->st>>>(ga, m, P->iota, rg, P->W, g, geo.tiles, geo.ns,
+                                                                      nullptr);
+    k_gram_reduce<<<reduce_grid(P, geo.nout * geo.nout), 256, 0, P->st>>>(P->W, geo.ns, geo.nout, geo.nmat, geo.diag,
+                                                                          geo.mult, P->Mmat, geo.ld, nullptr, nullptr, 0,
+                                                                          geo.jit);
+    P->launches += 2;
+    CKL();
+    if ((rc = launch_chol(P, P->Mmat, geo.N, P->u, 1.0, nullptr, nullptr))) return rc;
+    k_gather_rows<<<gather_rows_grid(P), 256, 0, P->st>>>(ga, m, P->iota, P->u, rg, nullptr, nullptr, nullptr,
+                                                           kGatherSmw, d, g, y ? y : g, yt ? yt : P->tmpm, gd_dev, P->blk,
+                                                           P->ticket);
+    P->launches++;
+    CKL();
+    return SSNAL_OK;
+  }
+  *branch = 2;
+  const int tiles = gram_tiles(m), ns = gram_splits(P->nsm, tiles, rl, P->W_splits);
+  with_acc(P, [&](auto acc) {
+    k_gram<false><<<gram_grid(P, tiles * ns), 256, 0, P->st>>>(acc, m, J, rl, P->W, nullptr, tiles, ns, nullptr);
+    return 0;
+  });
+  CK(cudaMemsetAsync(P->xbuf, 0, (size_t)m * m * 8, P->st));
+  k_gram_reduce<<<reduce_grid(P, m * m), 256, 0, P->st>>>(P->W, ns, m, m, 0.0, 1.0, P->xbuf, m, nullptr, nullptr, 0, 0.0);
+  P->launches += 2;
+  if ((rc = comm_allreduce(P, P->xbuf, m * m, 0))) return rc;
+  k_gram_reduce<<<reduce_grid(P, m * m), 256, 0, P->st>>>(P->xbuf, 1, m, m, 1.0, kappa, P->Mmat, m + 1, g, nullptr, 0,
+                                                          jit);
+  P->launches++;
+  CKL();
+  return launch_chol(P, P->Mmat, (int)m, d, -1.0, g, gd_dev, y, yt);
+}
+
 int newton_direction(ssnal_en_problem* P, const int32_t* J, int64_t r, const double* g, double kappa, double* d,
                      double* gd_dev, int* branch, const double* y = nullptr, double* yt = nullptr,
-                     double jit = 0.0) {
+                     double jit = 0.0, const int64_t* r_loc_dev = nullptr) {
+  if (sharded(P)) return newton_direction_sharded(P, J, r, r_loc_dev, g, kappa, d, gd_dev, branch, y, yt, jit);
   const int64_t m = P->m;
   DirGeo geo = make_geo(r, m, P->nsm, P->W_splits, kappa, 1.0 / kappa, P->cg_ratio, P->cg_threshold);
   geo.jit = jit;
@@ -1030,7 +1168,13 @@ int init_point(ssnal_en_problem* P, int have_x0, ssnal_en_stats* S, int64_t* rx)
   // Initial y, w (P:242 silent; reading R8): y0 = A x0 − b if x0 ≠ 0, else 0 (decided on the device)
   if (have_x0 && P->init_mode == 1) {
     if ((rc = launch_gather_dev(P, P->Jx, P->Px, P->r_dev + 2))) return rc;
-    k_init_y<<<1, 1024, 0, P->st>>>(m, P->b, P->part_vec, P->gax_valid, kGatherDevGrid, P->r_dev + 2, P->y[0]);
+    if (sharded(P)) {  // y0 = Σ_ranks A_S x0_S − b; warm iff the global support is non-empty
+      if ((rc = exchange_eval(P, P->part_vec, P->gax_valid, kGatherDevGrid, nullptr, 0, P->r_dev + 2))) return rc;
+      k_init_y<<<1, 1024, 0, P->st>>>(m, P->b, P->xbuf, nullptr, 1, P->rg_dev, P->y[0]);
+      CK(cudaMemcpyAsync(P->r_dev + 4, P->rg_dev, 8, cudaMemcpyDeviceToDevice, P->st));
+    } else {
+      k_init_y<<<1, 1024, 0, P->st>>>(m, P->b, P->part_vec, P->gax_valid, kGatherDevGrid, P->r_dev + 2, P->y[0]);
+    }
     P->launches++;
     CKL();
     if ((rc = launch_k1(P, P->y[0], nullptr, make_scal(1.0, 0.0, 0.0), 0, P->w[0]))) return rc;
@@ -1047,13 +1191,24 @@ int init_point(ssnal_en_problem* P, int have_x0, ssnal_en_stats* S, int64_t* rx)
 int launch_objective(ssnal_en_problem* P) {
   int rc;
   if ((rc = launch_gather_dev(P, P->Jx, P->Px, P->r_dev + 2))) return rc;
-  k_combine<<<1, 1024, 0, P->st>>>(P->m, P->b, -1.0, P->part_vec, kGatherDevGrid, P->tmpm, nullptr, nullptr,
-                                   P->gax_valid);
-  P->launches++;
-  CKL();
-  k_objective<<<1, 1024, 0, P->st>>>(P->m, P->tmpm, P->Px, P->r_dev + 2, P->scratch + 16);
-  P->launches++;
-  CKL();
+  if (sharded(P)) {  // resid = Σ_ranks A_S x_S − b; Σ|x|, Σx², nnz summed over the ranks
+    if ((rc = exchange_eval(P, P->part_vec, P->gax_valid, kGatherDevGrid, nullptr, 0, P->r_dev + 2))) return rc;
+    k_combine<<<1, 1024, 0, P->st>>>(P->m, P->b, -1.0, P->xbuf, 1, P->tmpm, nullptr, nullptr, nullptr);
+    k_objective<<<1, 1024, 0, P->st>>>(P->m, P->tmpm, P->Px, P->r_dev + 2, P->scratch + 16);
+    P->launches += 2;
+    CKL();
+    CK(cudaMemcpyAsync(P->xbuf, P->scratch + 17, 3 * 8, cudaMemcpyDeviceToDevice, P->st));
+    if ((rc = comm_allreduce(P, P->xbuf, 3, 0))) return rc;
+    CK(cudaMemcpyAsync(P->scratch + 17, P->xbuf, 3 * 8, cudaMemcpyDeviceToDevice, P->st));
+  } else {
+    k_combine<<<1, 1024, 0, P->st>>>(P->m, P->b, -1.0, P->part_vec, kGatherDevGrid, P->tmpm, nullptr, nullptr,
+                                     P->gax_valid);
+    P->launches++;
+    CKL();
+    k_objective<<<1, 1024, 0, P->st>>>(P->m, P->tmpm, P->Px, P->r_dev + 2, P->scratch + 16);
+    P->launches++;
+    CKL();
+  }
   CK(cudaMemcpyAsync(P->scratch_host + 16, P->scratch + 16, 4 * 8, cudaMemcpyDeviceToHost, P->st));
   CK(cudaMemcpyAsync(P->scratch_host + 20, P->r_dev + 4, 8, cudaMemcpyDeviceToHost, P->st));
   return SSNAL_OK;
@@ -1084,7 +1239,7 @@ int solve_core(ssnal_en_problem* P, double l1, double l2, double sigma0, double 
     // ∇ψ needs A_J P_J for the re-thresholded J: gather with r read on the device
     if ((rc = launch_gather_vec(P, P->J[cur], P->PJ[cur], P->r_dev + cur))) return rc;
     // K1e wrote G scalar partials; the gather wrote the finished vector A_J P_J (part_vec row 0)
-    if ((rc = launch_eval(P, P->y[cur], sc, 1, nullptr, 1, P->g[cur], P->r_dev + cur, 0))) return rc;
+    if ((rc = eval_g(P, P->y[cur], sc, 1, nullptr, 1, P->g[cur], P->r_dev + cur, 0))) return rc;
     if ((rc = fetch_eval(P, 0, &ev))) return rc;
     S->psi_evals++;
 
@@ -1102,13 +1257,13 @@ int solve_core(ssnal_en_problem* P, double l1, double l2, double sigma0, double 
       const int tr = 1 - cur;
       const int wtr = (wcur + 1) % 3, wbt = (wcur + 2) % 3;
       if ((rc = newton_direction(P, P->J[cur], ev.r, P->g[cur], sc.kappa, P->d, gd_dev, &br, P->y[cur], P->y[tr],
-                                 retry ? P->jitter : 0.0)))
+                                 retry ? P->jitter : 0.0, P->r_dev + cur)))
         return rc;
       S->branch_steps[br]++;
       if ((rc = launch_k1(P, P->y[tr], P->x, sc, 1, P->w[wtr]))) return rc;
       S->aty_passes++;
       if ((rc = launch_finalize(P, P->J[tr], P->PJ[tr], P->r_dev + tr))) return rc;
-      if ((rc = launch_eval(P, P->y[tr], sc, 1, P->cta_cnt, P->G, P->g[tr], P->r_dev + tr, 1, gd_dev,
+      if ((rc = eval_g(P, P->y[tr], sc, 1, P->cta_cnt, P->G, P->g[tr], P->r_dev + tr, 1, gd_dev,
                             (br == 1 || br == 2) ? P->info : nullptr)))
         return rc;
       if ((rc = fetch_eval(P, 1, &evt))) return rc;
@@ -1151,7 +1306,7 @@ int solve_core(ssnal_en_problem* P, double l1, double l2, double sigma0, double 
         CKL();
         if ((rc = launch_k1e(P, P->w[wcur], P->w[wtr], s, P->x, sc, P->w[wbt]))) return rc;
         if ((rc = launch_finalize(P, P->J[tr], P->PJ[tr], P->r_dev + tr))) return rc;
-        if ((rc = launch_eval(P, P->y[tr], sc, 0, nullptr, 0, nullptr, P->r_dev + tr, 2))) return rc;
+        if ((rc = eval_g(P, P->y[tr], sc, 0, nullptr, 0, nullptr, P->r_dev + tr, 2))) return rc;
         EvalOut eb;
         if ((rc = fetch_eval(P, 2, &eb))) return rc;
         S->psi_evals++;
@@ -1170,7 +1325,7 @@ int solve_core(ssnal_en_problem* P, double l1, double l2, double sigma0, double 
         // ∇ψ at the accepted point needs A_J P_J for the re-thresholded J (K2)
         if ((rc = launch_gather_vec(P, P->J[cur], P->PJ[cur], P->r_dev + cur))) return rc;
         // scalar partials in part_scal still belong to the accepted K1e launch
-        if ((rc = launch_eval(P, P->y[cur], sc, 1, nullptr, 1, P->g[cur], P->r_dev + cur, 0)))
+        if ((rc = eval_g(P, P->y[cur], sc, 1, nullptr, 1, P->g[cur], P->r_dev + cur, 0)))
           return rc;
         if ((rc = fetch_eval(P, 0, &ev))) return rc;
       }
@@ -1190,6 +1345,21 @@ int solve_core(ssnal_en_problem* P, double l1, double l2, double sigma0, double 
       k_zero_at<<<2 * P->nsm, 256, 0, P->st>>>(P->Jx, -1, P->r_dev + 2, P->x, nullptr);
       P->launches++;
       CKL();
+    }
+    if (sharded(P)) {  // ev.r is the global count: the local support lives on the device only
+      k_zero_at<<<2 * P->nsm, 256, 0, P->st>>>(P->Jx, -1, P->r_dev + 2, P->x, nullptr);
+      k_scatter_dev<<<2 * P->nsm, 256, 0, P->st>>>(P->J[cur], P->PJ[cur], P->r_dev + cur, P->x, P->Jx, P->Px,
+                                                    P->r_dev + 2);
+      P->launches += 2;
+      CKL();
+      rx = -1;
+      if (res3 <= tol && ev.res1 <= tol) {
+        converged = 1;
+        k++;
+        break;
+      }
+      sigma = fmin(P->sigma_factor * sigma, P->sigma_max);
+      continue;
     }
     const int64_t rnew = ev.r;
     if (rnew > 0) {
@@ -1553,6 +1723,10 @@ static void destroy_bufs(ssnal_en_problem* P) {
     cudaEventDestroy(pr.first);
     cudaEventDestroy(pr.second);
   }
+  cudaFree(P->xbuf);
+  cudaFree(P->rg_dev);
+  cudaFree(P->iota);
+  if (P->comm_host) cudaFreeHost(P->comm_host);
   pool_free(P->A_own);
   pool_free(P->codes_own);
   pool_free(P->tab_own);
@@ -1806,9 +1980,19 @@ static int solve_wrapped(ssnal_en_problem* P, double l1, double l2, double sigma
   if (x0) {
     CK(cudaMemcpyAsync(P->x, x0, P->n * 8, x0_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, P->st));
   }
+  int have_x0 = x0 != nullptr;
+  if (sharded(P)) {  // warm start iff any rank has an x0 slice (the others count as zero)
+    P->comm_host[0] = have_x0;
+    CK(cudaMemcpyAsync(P->xbuf, P->comm_host, 8, cudaMemcpyHostToDevice, P->st));
+    if ((rc = comm_allreduce(P, P->xbuf, 1, 0))) return rc;
+    CK(cudaMemcpyAsync(P->comm_host + 1, P->xbuf, 8, cudaMemcpyDeviceToHost, P->st));
+    CK(cudaStreamSynchronize(P->st));
+    if (P->comm_host[1] > 0 && !have_x0) CK(cudaMemsetAsync(P->x, 0, P->n * 8, P->st));
+    have_x0 = P->comm_host[1] > 0;
+  }
   ssnal_en_stats S;
-  rc = P->use_graph ? solve_graph_core(P, l1, l2, sigma0, tol, x0 != nullptr, &S)
-                    : solve_core(P, l1, l2, sigma0, tol, x0 != nullptr, &S);
+  rc = (P->use_graph && !sharded(P)) ? solve_graph_core(P, l1, l2, sigma0, tol, have_x0, &S)
+                                     : solve_core(P, l1, l2, sigma0, tol, have_x0, &S);
   if (rc == SSNAL_ECUDA || rc == SSNAL_EINVAL) return rc;
   if (x_out) {
     CK(cudaMemcpyAsync(x_out, P->x, P->n * 8, xout_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, P->st));
@@ -1828,6 +2012,7 @@ static int solve_wrapped(ssnal_en_problem* P, double l1, double l2, double sigma
     k_kkt_viol<<<nb, 256, 0, P->st>>>(P->n, P->w[2], P->x, P->stat_l1, P->stat_l2, P->cg_scal);
     k_max_reduce<<<1, 32, 0, P->st>>>(P->cg_scal, nb, P->scratch + 40);
     CKL();
+    if (sharded(P) && (rc = comm_allreduce(P, P->scratch + 40, 1, 1))) return rc;
     CK(cudaMemcpyAsync(P->scratch_host + 42, P->scratch + 40, 8, cudaMemcpyDeviceToHost, P->st));
     CK(cudaStreamSynchronize(P->st));
     S.primal_viol = P->scratch_host[42];
@@ -1902,6 +2087,10 @@ int ssnal_en_epilogue(ssnal_en_problem* P, const double* w0, const double* w1, d
 
 int ssnal_en_newton_direction(ssnal_en_problem* P, const int32_t* J, int64_t r, const double* g, double kappa,
                               double* d_out, double* gd_out, int32_t* branch_out) {
+  if (P && sharded(P)) {
+    set_err("not available on a column-sharded handle");
+    return SSNAL_EINVAL;
+  }
   if (!P || (r > 0 && !J) || !g || !d_out || !(kappa > 0) || r < 0 || r > P->n) {
     set_err("invalid argument");
     return SSNAL_EINVAL;
@@ -1927,6 +2116,10 @@ int ssnal_en_newton_direction(ssnal_en_problem* P, const int32_t* J, int64_t r, 
 
 // Section 3.3: ν, OLS de-biasing, rss, GCV, e-BIC for the latest solution.
 int ssnal_en_model_select(ssnal_en_problem* P, double l2, double* xdb_out, ssnal_en_criteria* out) {
+  if (P && sharded(P)) {
+    set_err("not available on a column-sharded handle");
+    return SSNAL_EINVAL;
+  }
   if (!P || !out || !(l2 >= 0)) {
     set_err("invalid argument");
     return SSNAL_EINVAL;
@@ -2049,6 +2242,10 @@ int ssnal_en_model_select(ssnal_en_problem* P, double l2, double* xdb_out, ssnal
 // ‖A x − b‖² for an external x: support of x by K1e (w = 0, σ = 1, λ = 0 selects x ≠ 0 with P = x)
 // into the trial set (J[1], PJ[1], r_dev[3]) — free outside a solve — then K2 + combine + norm.
 static int residual_impl(ssnal_en_problem* P, const double* x, int x_dev, double* rss_out) {
+  if (P && sharded(P)) {
+    set_err("not available on a column-sharded handle");
+    return SSNAL_EINVAL;
+  }
   if (!P || !x || !rss_out) {
     set_err("null argument");
     return SSNAL_EINVAL;
@@ -2074,6 +2271,38 @@ int ssnal_en_residual(ssnal_en_problem* P, const double* x, double* rss_out) { r
 
 int ssnal_en_residual_device(ssnal_en_problem* P, const double* x, double* rss_out) {
   return residual_impl(P, x, 1, rss_out);
+}
+
+int ssnal_en_set_comm(ssnal_en_problem* P, ssnal_en_allreduce_fn fn, void* ctx, int rank, int nranks) {
+  if (!P || !fn || nranks < 1 || rank < 0 || rank >= nranks) {
+    set_err("invalid argument");
+    return SSNAL_EINVAL;
+  }
+  const int64_t m = P->m;
+  if (!P->xbuf) {
+    int rc;
+    if ((rc = alloc((void**)&P->xbuf, (size_t)(m * m + 2 * m + 64 + nranks) * 8))) return rc;
+    if ((rc = alloc((void**)&P->rg_dev, 64))) return rc;
+    if ((rc = alloc((void**)&P->iota, (size_t)(m + 1) * 4))) return rc;
+  }
+  if (P->comm_host) cudaFreeHost(P->comm_host);
+  P->comm_host = nullptr;
+  CK(cudaHostAlloc((void**)&P->comm_host, (size_t)(nranks + 16) * 8, cudaHostAllocDefault));
+  P->comm_fn = fn;
+  P->comm_ctx = ctx;
+  P->comm_rank = rank;
+  P->comm_size = nranks;
+  k_iota<<<1, 1024, 0, P->st>>>(P->iota, m);
+  CKL();
+  // λmax = max over the ranks of the local ‖A_qᵀb‖∞
+  P->comm_host[0] = P->lambda_max;
+  CK(cudaMemcpyAsync(P->xbuf, P->comm_host, 8, cudaMemcpyHostToDevice, P->st));
+  int rc = comm_allreduce(P, P->xbuf, 1, 1);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(P->comm_host + 1, P->xbuf, 8, cudaMemcpyDeviceToHost, P->st));
+  CK(cudaStreamSynchronize(P->st));
+  P->lambda_max = P->comm_host[1];
+  return SSNAL_OK;
 }
 
 void ssnal_en_destroy(ssnal_en_problem* P) {

@@ -58,6 +58,10 @@ class SsnalError(RuntimeError):
 
 _lib = None
 
+# int (*)(void* ctx, double* buf, int64_t count, int op, void* stream) — ssnal_en_allreduce_fn
+ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int,
+                                ctypes.c_void_p)
+
 
 def load_library():
     global _lib
@@ -85,13 +89,14 @@ def load_library():
         L.ssnal_en_model_select.restype = ctypes.c_int
         L.ssnal_en_residual.argtypes = [_vp, _dp, _dp]
         L.ssnal_en_residual_device.argtypes = [_vp, _vp, _dp]
+        L.ssnal_en_set_comm.argtypes = [_vp, ALLREDUCE_FN, _vp, ctypes.c_int, ctypes.c_int]
         L.ssnal_en_destroy.argtypes = [_vp]
         L.ssnal_en_destroy.restype = None
         L.ssnal_en_last_error.restype = ctypes.c_char_p
         L.ssnal_en_version.restype = ctypes.c_char_p
         for f in ("create", "create_device", "create_geno", "create_geno_device", "residual", "residual_device",
                   "set_option", "solve", "solve_device", "aty_fused", "epilogue",
-                  "newton_direction"):
+                  "newton_direction", "set_comm"):
             getattr(L, "ssnal_en_" + f).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -235,6 +240,23 @@ class Problem:
         _check(self._lib.ssnal_en_newton_direction(self._h, _vp(J) if J else None, r, _vp(g), kappa, _vp(d_out),
                                                    ctypes.byref(gd), ctypes.byref(br)))
         return gd.value, br.value
+
+    def set_comm(self, fn, rank: int, nranks: int):
+        """Make this handle rank `rank` of a column-sharded solve (§8(f3)); fn(buf_ptr, count, op,
+        stream) -> None all-reduces `count` doubles at the device pointer in place (op 0 sum, 1 max),
+        stream-ordered.  See ssnal_en_set_comm in include/ssnal_en.h."""
+
+        def cb(ctx, buf, count, op, stream):
+            try:
+                fn(buf, count, op, stream)
+                return 0
+            except Exception:  # reported as SSNAL_ECUDA by the library
+                import traceback
+                traceback.print_exc()
+                return 1
+
+        self._comm_cb = ALLREDUCE_FN(cb)  # kept alive with the handle
+        _check(self._lib.ssnal_en_set_comm(self._h, self._comm_cb, None, rank, nranks))
 
     def close(self):
         if getattr(self, "_h", None):
