@@ -319,6 +319,7 @@ def bench_ours(args, rank, world, local_rank):
                      "mean_launch_us": k1_avg * 1e6, "share_of_step": k1_time / max(elapsed, 1e-30)},
         "e2e": e2e,
         "gpu_launches": launches // max(args.steps, 1),
+        "solves_device_s_per_step": dev_sum / max(args.steps, 1),
         "clocks": clk.summary(),
         "iterations": [{"c": round(c, 4), "outer": s["outer_iters"], "newton": s["newton_iters"],
                         "passes": s["aty_passes"], "backtracks": s["backtracks"], "r": s["active"],

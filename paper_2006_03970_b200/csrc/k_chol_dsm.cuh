@@ -55,10 +55,19 @@ __global__ void __launch_bounds__(256, 1) k_chol_dsm(const double* __restrict__ 
                                                      double* __restrict__ out, double scale,
                                                      const double* __restrict__ dotv, double* dot_out, int* info,
                                                      const double* __restrict__ ybase, double* __restrict__ yt,
-                                                     const DirGeo* geo, int want, int nmax) {
+                                                     const DirGeo* geo, int want, int nmax, const CholArgs* ca) {
   namespace cg = cooperative_groups;
   if (geo) {  // graph mode: predicated on the branch and on N ≤ nmax ≤ 512 (uniform over the cluster)
-    if (geo->branch != want || geo->N > nmax) return;
+    if ((want >= 0 ? geo->branch != want : (geo->branch != 1 && geo->branch != 2)) || geo->N > nmax) return;
+    if (ca) {  // want < 0: the outputs of whichever exact branch this step took
+      const CholArgs& c = ca[geo->branch - 1];
+      out = c.out;
+      scale = c.scale;
+      dotv = c.dotv;
+      dot_out = c.dot_out;
+      ybase = c.ybase;
+      yt = c.yt;
+    }
     N = geo->N;
     ld = geo->ld;
   }

@@ -171,9 +171,9 @@ __global__ void __cluster_dims__(kGatherCS, 1, 1) __launch_bounds__(256)
   __shared__ double part[32];
   __shared__ bool last;
   if (pred && *pred == 0) return;  // uniform over the grid
-  if (geo) {
-    if (geo->branch != 1) return;
-    r = geo->r;
+  if (geo) {  // SMW back-substitution (branch 1), or d = −g for r = 0 (branch 0: no columns)
+    if (geo->branch != 1 && geo->branch != 0) return;
+    r = geo->branch == 1 ? geo->r : 0;
   } else if (r < 0) {
     r = *r_dev;
   }
@@ -294,8 +294,9 @@ SSN_DEV void tri_tile(int q, int* ti, int* tj) {  // q → (ti ≥ tj), row-majo
 __global__ void k_gram_reduce(const double* __restrict__ W, int ns, int64_t nout, int64_t nmat, double diag,
                               double mult, double* __restrict__ M, int64_t ld, const double* __restrict__ g,
                               const DirGeo* geo, int want, double jit) {
-  if (geo) {
-    if (geo->branch != want) return;
+  if (geo) {  // want < 0: either exact branch (the rhs row g only for r ≥ m)
+    if (want >= 0 ? geo->branch != want : (geo->branch != 1 && geo->branch != 2)) return;
+    if (want < 0 && geo->branch != 2) g = nullptr;
     ns = geo->ns;
     nout = geo->nout;
     nmat = geo->nmat;
@@ -339,6 +340,17 @@ __global__ void k_gram_reduce(const double* __restrict__ W, int ns, int64_t nout
 // FP64 tensor cores: mma.sync.m8n8k4.f64 (SASS DMMA) — the tile updates are dense contractions.
 // out = scale · v; if dotv: *dot_out = Σ dotv · out; if yt: yt = ybase + out.
 // ---------------------------------------------------------------------------
+// Per-branch outputs of a K4 launch that serves both exact branches (graph mode, want < 0):
+// [0] SMW (v → u), [1] m × m (d = −M⁻¹g, gᵀd, y + d)
+struct CholArgs {
+  double* out;
+  double scale;
+  const double* dotv;
+  double* dot_out;
+  const double* ybase;
+  double* yt;
+};
+
 constexpr int CHT = 32;  // tile edge
 constexpr int TLD = 33;  // smem tile leading dimension
 constexpr int kColSlots = 3;  // column tiles a worker quad holds for the TRSM (≤ 3 × 30 quads ≥ 64 row tiles)
@@ -402,19 +414,11 @@ SSN_DEV void tile_mma(const double* SA, const double* SB, double (&acc)[4][4][2]
 // are taken by persistent CTAs in a grid-stride loop (results do not depend on the grid); each
 // writes its partial tile (lower part) to W[s] and k_gram_reduce sums the slices in order.
 // Graph mode: r, tiles, ns from the device geometry (predicated on the branch).
+constexpr int kGramSmem = GT * 36;  // doubles per operand buffer (≥ 32 · 68 of the m × m layout)
 template <bool SMW, class Acc>
-__global__ void __launch_bounds__(256) k_gram(const Acc A, int64_t m, const int32_t* __restrict__ J, int64_t r,
-                                              double* __restrict__ W, const double* __restrict__ gext, int tiles,
-                                              int ns, const DirGeo* geo) {
+SSN_DEV void gram_body(const Acc& A, int64_t m, const int32_t* __restrict__ J, int64_t r, double* __restrict__ W,
+                       const double* __restrict__ gext, int tiles, int ns, double* sA, double* sB) {
   constexpr int LD = SMW ? 36 : 68;
-  constexpr int SZ = SMW ? GT * 36 : 32 * 68;
-  __shared__ double sA[SZ], sB[SZ];
-  if (geo) {
-    if (geo->branch != (SMW ? 1 : 2)) return;
-    r = geo->r;
-    tiles = geo->tiles;
-    ns = geo->ns;
-  }
   const int64_t K = SMW ? m : r;  // reduction length
   const int64_t nch = (K + 31) / 32;
   const int64_t nout = SMW ? r + (gext ? 1 : 0) : m;
@@ -497,6 +501,29 @@ __global__ void __launch_bounds__(256) k_gram(const Acc A, int64_t m, const int3
           if (oi < nout && oj < nout && oi >= oj) Ws[oi + oj * nout] = acc[i][j][e];
         }
   }
+}
+template <bool SMW, class Acc>
+__global__ void __launch_bounds__(256) k_gram(const Acc A, int64_t m, const int32_t* __restrict__ J, int64_t r,
+                                              double* __restrict__ W, const double* __restrict__ gext, int tiles,
+                                              int ns, const DirGeo* geo) {
+  __shared__ double sA[kGramSmem], sB[kGramSmem];
+  if (geo) {
+    if (geo->branch != (SMW ? 1 : 2)) return;
+    r = geo->r;
+    tiles = geo->tiles;
+    ns = geo->ns;
+  }
+  gram_body<SMW>(A, m, J, r, W, gext, tiles, ns, sA, sB);
+}
+// graph mode: one launch for both exact branches (SMW with the extra column g, or m × m)
+template <class Acc>
+__global__ void __launch_bounds__(256) k_gram_any(const Acc A, int64_t m, const int32_t* __restrict__ J,
+                                                  double* __restrict__ W, const double* __restrict__ g,
+                                                  const DirGeo* geo) {
+  __shared__ double sA[kGramSmem], sB[kGramSmem];
+  const int br = geo->branch;
+  if (br == 1) gram_body<true>(A, m, J, geo->r, W, g, geo->tiles, geo->ns, sA, sB);
+  else if (br == 2) gram_body<false>(A, m, J, geo->r, W, nullptr, geo->tiles, geo->ns, sA, sB);
 }
 
 // Warp loads rows [r0, r0+32) × cols [c0, c0+32) of M into S (row-major, TLD), zero outside
@@ -722,10 +749,20 @@ __global__ void __launch_bounds__(256, 1) k_chol_cluster(double* M, int N, int N
                                                          double scale, const double* __restrict__ dotv,
                                                          double* dot_out, double* Winv, int* info,
                                                          const double* __restrict__ ybase, double* __restrict__ yt,
-                                                         const DirGeo* geo, int want, int* kflag, int nmin) {
+                                                         const DirGeo* geo, int want, int* kflag, int nmin,
+                                                         const CholArgs* ca) {
   namespace cg = cooperative_groups;
   if (geo) {  // graph mode: order from the device geometry; whole cluster exits together
-    if (geo->branch != want || geo->N < nmin) return;
+    if ((want >= 0 ? geo->branch != want : (geo->branch != 1 && geo->branch != 2)) || geo->N < nmin) return;
+    if (ca) {
+      const CholArgs& c = ca[geo->branch - 1];
+      out = c.out;
+      scale = c.scale;
+      dotv = c.dotv;
+      dot_out = c.dot_out;
+      ybase = c.ybase;
+      yt = c.yt;
+    }
     N = geo->N;
     NR = geo->NR;
     ld = geo->ld;

@@ -338,6 +338,7 @@ struct ssnal_en_problem {
   int64_t* rg_dev = nullptr;         // global r for the eval record
   int32_t* iota = nullptr;           // 0 … m−1: indices of the gathered active columns
   double* comm_host = nullptr;       // pinned staging (nranks + 8 doubles)
+  CholArgs* chol_args = nullptr;  // graph mode: K4 outputs per exact branch (device, 2 entries)
   int inner_tol_mode = 0;  // 1: tol_in = max(tol, 0.1 res3 at the outer start) (R37)
   int inject_fail = 0;    // test hook: the next N factorisations of a solve report failure
   double jitter = 1e-10;  // factor retry M_ii ← M_ii (1 + jitter) after a non-positive pivot (R36)
@@ -552,6 +553,7 @@ int allocate(ssnal_en_problem* P) {
   d.add((void**)&P->flags, 64);
   d.add((void**)&P->blk, (size_t)((m + 31) / 32) * 3 * 8 + 64);
   d.add((void**)&P->ticket, 64);
+  d.add((void**)&P->chol_args, 2 * sizeof(CholArgs));
   d.add((void**)&P->gax_valid, 4 * 256);
   d.add((void**)&P->cg_res, m * 8);
   d.add((void**)&P->cg_parts, (size_t)P->nsm * m * 8);
@@ -840,7 +842,7 @@ int launch_chol_ex(ssnal_en_problem* P, double* M, int N, int NR, int ld, double
   cfg.numAttrs = 1;
   const DirGeo* nog = nullptr;
   CK(cudaLaunchKernelEx(&cfg, k_chol_cluster, M, N, NR, ld, out, scale, dotv, dot_out, P->Winv, info, ybase, yt, nog,
-                        0, P->kflag, 0));
+                        0, P->kflag, 0, (const CholArgs*)nullptr));
   P->launches++;
   return SSNAL_OK;
 }
@@ -863,8 +865,9 @@ int launch_chol_dsm(ssnal_en_problem* P, double* M, int N, double* out, double s
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
+  const CholArgs* ca = want < 0 ? P->chol_args : nullptr;
   CK(cudaLaunchKernelEx(&cfg, k_chol_dsm, (const double*)M, N, N + 1, out, scale, dotv, dot_out, P->info, ybase, yt,
-                        geo, want, kDsmUseMax));
+                        geo, want, kDsmUseMax, ca));
   P->launches++;
   return SSNAL_OK;
 }
@@ -896,8 +899,9 @@ int launch_chol(ssnal_en_problem* P, double* M, int N, double* out, double scale
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
+  const CholArgs* ca = want < 0 ? P->chol_args : nullptr;
   CK(cudaLaunchKernelEx(&cfg, k_chol_cluster, M, N, N + 1, N + 1, out, scale, dotv, dot_out, P->Winv, P->info,
-                        ybase, yt, geo, want, P->kflag, nmin));
+                        ybase, yt, geo, want, P->kflag, nmin, ca));
   P->launches++;
   return SSNAL_OK;
 }
@@ -1044,8 +1048,13 @@ int newton_direction(ssnal_en_problem* P, const int32_t* J, int64_t r, const dou
   *branch = geo.branch;
   if (geo.branch == 3)  // K6: conjugate gradient (R32)
     return launch_cg(P, J, r, g, kappa, d, gd_dev, y, yt, nullptr);
-  if (geo.branch == 0) {
-    k_neg_copy<<<1, 1024, 0, P->st>>>(m, g, d, g, gd_dev, y, yt, nullptr);
+  if (geo.branch == 0) {  // d = −g, gᵀd, y + d: the SMW back-substitution kernel with no columns
+    with_acc(P, [&](auto acc) {
+      k_gather_rows<<<gather_rows_grid(P), 256, 0, P->st>>>(acc, m, J, g, 0, nullptr, nullptr, nullptr, kGatherSmw, d,
+                                                             g, y ? y : g, yt ? yt : P->tmpm, gd_dev, P->blk,
+                                                             P->ticket);
+      return 0;
+    });
     P->launches++;
     CKL();
     return SSNAL_OK;
@@ -1100,27 +1109,22 @@ int newton_direction_graph(ssnal_en_problem* P) {
   const int32_t* J = P->J[0];
   const double* g = P->g[0];
   double* gd = P->scratch;
-  k_neg_copy<<<1, 1024, 0, P->st>>>(m, g, P->d, g, gd, P->y[0], P->y[1], geo);
   with_acc(P, [&](auto acc) {
-    k_gram<true><<<2 * P->nsm, 256, 0, P->st>>>(acc, m, J, 0, P->W, g, 0, 0, geo);
+    k_gram_any<<<2 * P->nsm, 256, 0, P->st>>>(acc, m, J, P->W, g, geo);
     return 0;
   });
-  k_gram_reduce<<<reduce_grid(P, m * m), 256, 0, P->st>>>(P->W, 0, 0, 0, 0.0, 0.0, P->Mmat, 0, nullptr, geo, 1, 0.0);
-  P->launches += 3;
+  k_gram_reduce<<<reduce_grid(P, m * m), 256, 0, P->st>>>(P->W, 0, 0, 0, 0.0, 0.0, P->Mmat, 0, g, geo, -1, 0.0);
+  P->launches += 2;
   CKL();
-  int rc = launch_chol(P, P->Mmat, 0, P->u, 1.0, nullptr, nullptr, nullptr, nullptr, geo, 1);
+  int rc = launch_chol(P, P->Mmat, 0, nullptr, 0.0, nullptr, nullptr, nullptr, nullptr, geo, -1);
   if (rc) return rc;
-  with_acc(P, [&](auto acc) {
+  with_acc(P, [&](auto acc) {  // SMW back-substitution, or d = −g when r = 0
     k_gather_rows<<<gather_rows_grid(P), 256, 0, P->st>>>(acc, m, J, P->u, 0, nullptr, nullptr, geo, kGatherSmw, P->d,
                                                            g, P->y[0], P->y[1], gd, P->blk, P->ticket);
-    k_gram<false><<<2 * P->nsm, 256, 0, P->st>>>(acc, m, J, 0, P->W, nullptr, 0, 0, geo);
     return 0;
   });
-  k_gram_reduce<<<reduce_grid(P, m * m), 256, 0, P->st>>>(P->W, 0, 0, 0, 0.0, 0.0, P->Mmat, 0, g, geo, 2, 0.0);
-  P->launches += 3;
+  P->launches++;
   CKL();
-  rc = launch_chol(P, P->Mmat, 0, P->d, -1.0, g, gd, P->y[0], P->y[1], geo, 2);
-  if (rc) return rc;
   return launch_cg(P, J, 0, g, 0.0, P->d, gd, P->y[0], P->y[1], geo);  // predicated on branch 3
 }
 
@@ -1522,6 +1526,12 @@ int capture_graph(ssnal_en_problem* P, cudaGraph_t G) {
 
 int build_graph(ssnal_en_problem* P) {
   if (P->gexec) return SSNAL_OK;
+  {  // K4 outputs per exact branch for the graph's branch-agnostic launch (k_chol_* with want < 0):
+     // [0] SMW v → u; [1] m × m d = −M⁻¹g, gᵀd = scratch[0], y[1] = y[0] + d
+    const CholArgs ca[2] = {{P->u, 1.0, nullptr, nullptr, nullptr, nullptr},
+                            {P->d, -1.0, P->g[0], P->scratch, P->y[0], P->y[1]}};
+    CK(cudaMemcpy(P->chol_args, ca, sizeof(ca), cudaMemcpyHostToDevice));
+  }
   for (int i = 0; i < 3; ++i)
     if (!P->cap[i]) CK(cudaStreamCreateWithFlags(&P->cap[i], cudaStreamNonBlocking));
   cudaGraph_t G;

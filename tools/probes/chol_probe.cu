@@ -67,7 +67,7 @@ int main() {
       for (int rep = 0; rep < 5; ++rep) {
         cudaMemcpy(dM, h.data(), h.size() * 8, cudaMemcpyHostToDevice);
         cudaEventRecord(e0);
-        cudaLaunchKernelEx(&cfg, k_chol_cluster, dM, N, N + 1, ld, dout, 1.0, (const double*)nullptr, (double*)nullptr, dW, info, (const double*)nullptr, (double*)nullptr, (const DirGeo*)nullptr, 0, kf, 0);
+        cudaLaunchKernelEx(&cfg, k_chol_cluster, dM, N, N + 1, ld, dout, 1.0, (const double*)nullptr, (double*)nullptr, dW, info, (const double*)nullptr, (double*)nullptr, (const DirGeo*)nullptr, 0, kf, 0, (const CholArgs*)nullptr);
         cudaEventRecord(e1); cudaEventSynchronize(e1);
         float ms; cudaEventElapsedTime(&ms, e0, e1); if (ms < best) best = ms;
       }

@@ -24,9 +24,9 @@ int main() {
     cfg.attrs = at; cfg.numAttrs = 1;
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
     const DirGeo* nog = nullptr;
-    for (int it = 0; it < 3; ++it) cudaLaunchKernelEx(&cfg, k_chol_dsm, (const double*)dM, N, ld, dout, 1.0, (const double*)nullptr, (double*)nullptr, info, (const double*)nullptr, (double*)nullptr, nog, 0, kDsmMaxN);
+    for (int it = 0; it < 3; ++it) cudaLaunchKernelEx(&cfg, k_chol_dsm, (const double*)dM, N, ld, dout, 1.0, (const double*)nullptr, (double*)nullptr, info, (const double*)nullptr, (double*)nullptr, nog, 0, kDsmMaxN, (const CholArgs*)nullptr);
     cudaEventRecord(e0);
-    for (int it = 0; it < 20; ++it) cudaLaunchKernelEx(&cfg, k_chol_dsm, (const double*)dM, N, ld, dout, 1.0, (const double*)nullptr, (double*)nullptr, info, (const double*)nullptr, (double*)nullptr, nog, 0, kDsmMaxN);
+    for (int it = 0; it < 20; ++it) cudaLaunchKernelEx(&cfg, k_chol_dsm, (const double*)dM, N, ld, dout, 1.0, (const double*)nullptr, (double*)nullptr, info, (const double*)nullptr, (double*)nullptr, nog, 0, kDsmMaxN, (const CholArgs*)nullptr);
     cudaEventRecord(e1); cudaEventSynchronize(e1);
     float ms; cudaEventElapsedTime(&ms, e0, e1);
     printf("N=%d: %.1f us per call (%s)\n", N, ms * 1e3 / 20, cudaGetErrorString(cudaGetLastError()));
