@@ -12,6 +12,7 @@
 
 #include <stdarg.h>
 
+#include <algorithm>
 #include <chrono>
 #include <string>
 #include <vector>
@@ -1125,6 +1126,8 @@ int newton_direction_graph(ssnal_en_problem* P) {
   });
   P->launches++;
   CKL();
+  // K6 only when the strategy can select it (the options drop the graph when they change)
+  if (!(P->cg_ratio > 0.0) && !((double)std::min<int64_t>(m, P->n) > P->cg_threshold)) return SSNAL_OK;
   return launch_cg(P, J, 0, g, 0.0, P->d, gd, P->y[0], P->y[1], geo);  // predicated on branch 3
 }
 
@@ -1928,8 +1931,13 @@ int ssnal_en_set_option(ssnal_en_problem* P, const char* key, double v) {
   else if (k == "time_k1") P->time_k1 = v != 0;
   else if (k == "certify" && (v == 0 || v == 1)) P->certify = (int)v;
   else if (k == "graph" && (v == 0 || v == 1)) P->use_graph = (int)v;
-  else if (k == "cg_ratio" && v >= 0) P->cg_ratio = v;
-  else if (k == "cg_threshold" && v >= 0) P->cg_threshold = v;
+  else if (k == "cg_ratio" && v >= 0) {
+    if ((v > 0) != (P->cg_ratio > 0)) drop_graph(P);  // the graph holds K6 only when CG can be chosen
+    P->cg_ratio = v;
+  } else if (k == "cg_threshold" && v >= 0) {
+    P->cg_threshold = v;
+    drop_graph(P);
+  }
   else if (k == "jitter" && v >= 0 && v < 1) P->jitter = v;
   else if (k == "test_fail_factor" && v >= 0) P->inject_fail = (int)v;
   else if (k == "inner_tol_mode" && (v == 0 || v == 1)) P->inner_tol_mode = (int)v;
