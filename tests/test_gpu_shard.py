@@ -113,3 +113,31 @@ def test_sharded_warm_start_and_branches():
     finally:
         for P, _, _ in shards:
             P.close()
+
+
+def test_sharded_genotype_handles():
+    """Packed 2-bit genotype shards (§8(f4) storage) exchange like fp64 ones: the gathered active
+    columns and the summed Grams are decoded through the column accessor."""
+    m, n, G = 300, 9000, 2
+    cfg = synth.Config("gs", m, n, synth.GENO_STD, 10, 0.1, 0.3, 1.0, 0.5, (0.3,), 19)
+    codes, tab = synth.geno_codes(cfg)
+    A = synth.decode_geno(codes, tab, m)
+    b, _ = synth.response(cfg)
+    lm = float(np.max(np.abs(oracle.aty(A, b)))) / cfg.alpha
+    grp = ThreadGroup(G)
+    shards = []
+    for q in range(G):
+        j0, j1 = column_range(n, q, G)
+        shards.append((Problem.from_geno(np.ascontiguousarray(codes[j0:j1]), np.ascontiguousarray(tab[j0:j1]), b),
+                       j0, j1))
+    try:
+        run_threads([(lambda q=q: shards[q][0].set_comm(grp.member(q), q, G)) for q in range(G)], grp)
+        for c in (0.3, 0.05):
+            l1, l2 = c * cfg.alpha * lm, c * (1 - cfg.alpha) * lm
+            xs, sts = sharded_solve(grp, shards, l1, l2, cfg.sigma0, cfg.tol)
+            xc, _, sc, _ = oracle.solve(A, b, l1, l2, sigma0=cfg.sigma0, tol=cfg.tol)
+            assert sts[0]["status"] == 0 and sts[0]["outer_iters"] == sc["outer_iters"]
+            assert solution_parity(xs, xc, oracle.primal_obj(A, b, xs, l1, l2), oracle.primal_obj(A, b, xc, l1, l2))["ok"]
+    finally:
+        for P, _, _ in shards:
+            P.close()
