@@ -737,7 +737,9 @@ constexpr int K5_THREADS = 256;  // 8 warps; CTA c owns rows [32c, 32c + 32)
 // the block's scalar partials; the last row block (ticket counter) adds them in block order,
 // adds the per-CTA scalar partials of K1/K1e in CTA order and writes EvalOut.
 constexpr int kEvalCS = 8;
-__global__ void __cluster_dims__(kEvalCS, 1, 1) __launch_bounds__(K5_THREADS) k_eval_reduce(int64_t m, const double* __restrict__ y,
+// The evaluation as a device function: true on the one thread that finishes (after *out is
+// written), so control epilogues can follow in the same launch (k_ctl.cuh).
+SSN_DEV bool eval_body(int64_t m, const double* __restrict__ y,
                                                             const double* __restrict__ bvec,
                                                             const double* __restrict__ part_vec,
                                                             const int* __restrict__ part_valid, int nparts,
@@ -748,9 +750,10 @@ __global__ void __cluster_dims__(kEvalCS, 1, 1) __launch_bounds__(K5_THREADS) k_
                                                             const double* gd_src, const int* info_src,
                                                             EvalOut* host_out, unsigned long long seq,
                                                             const Scal* scp, const int* pred, const double* nbp) {
+
   __shared__ double red[8][33];
   __shared__ bool last;
-  if (pred && *pred == 0) return;  // graph mode: predicated off (uniform over the grid)
+  if (pred && *pred == 0) return false;  // graph mode: predicated off (uniform over the grid)
   if (scp) sc = *scp;
   if (nbp) nb = *nbp;  // graph mode: ‖b‖ from the control block (the graph may predate it)
   namespace cg = cooperative_groups;
@@ -797,7 +800,7 @@ __global__ void __cluster_dims__(kEvalCS, 1, 1) __launch_bounds__(K5_THREADS) k_
     }
     cluster.sync();  // rank 0 has read every CTA's sums
   }
-  if (cs != 0) return;
+  if (cs != 0) return false;
   __syncthreads();
   if (warp == 0) {
     double yy = 0.0, by = 0.0, gg = 0.0;
@@ -825,7 +828,7 @@ __global__ void __cluster_dims__(kEvalCS, 1, 1) __launch_bounds__(K5_THREADS) k_
     }
   }
   __syncthreads();
-  if (!last || warp != 0) return;
+  if (!last || warp != 0) return false;
   __threadfence();
   // warp 0 of the last CTA: lane ℓ sums entries q ≡ ℓ (mod 32) in order, then a fixed butterfly
   double a = 0, bb = 0, c = 0;
@@ -850,7 +853,7 @@ __global__ void __cluster_dims__(kEvalCS, 1, 1) __launch_bounds__(K5_THREADS) k_
   bb = warp_allsum(bb);
   c = warp_allsum(c);
   for (int j = 0; j < 4; ++j) s[j] = warp_allsum(s[j]);
-  if (lane != 0) return;
+  if (lane != 0) return false;
   EvalOut o;
   o.yy = a;
   o.by = bb;
@@ -875,6 +878,22 @@ __global__ void __cluster_dims__(kEvalCS, 1, 1) __launch_bounds__(K5_THREADS) k_
     h->seq = seq;
   }
   *ticket = 0u;  // ready for the next launch (stream-ordered)
+  return true;  // the finishing thread (EvalOut written)
+}
+
+__global__ void __cluster_dims__(kEvalCS, 1, 1) __launch_bounds__(K5_THREADS) k_eval_reduce(int64_t m, const double* __restrict__ y,
+                                                            const double* __restrict__ bvec,
+                                                            const double* __restrict__ part_vec,
+                                                            const int* __restrict__ part_valid, int nparts,
+                                                            const double* __restrict__ part_scal, int nscal,
+                                                            Scal sc, double nb, int with_grad,
+                                                            double* __restrict__ g_out, const int64_t* r_in,
+                                                            EvalOut* out, double* blk, unsigned* ticket,
+                                                            const double* gd_src, const int* info_src,
+                                                            EvalOut* host_out, unsigned long long seq,
+                                                            const Scal* scp, const int* pred, const double* nbp) {
+  eval_body(m, y, bvec, part_vec, part_valid, nparts, part_scal, nscal, sc, nb, with_grad, g_out, r_in, out, blk,
+            ticket, gd_src, info_src, host_out, seq, scp, pred, nbp);
 }
 
 // max over G plain-mode partials (λmax = ‖Aᵀb‖∞)

@@ -100,8 +100,8 @@ __global__ void k_ctl_outer_begin(DevCtl* C) {
 }
 
 // after EVAL at the outer start: first inner test
-__global__ void k_ctl_inner_begin(DevCtl* C, const EvalOut* ev0, int64_t m, int nsm, int wsplits, int* info,
-                                  cudaGraphConditionalHandle h_inner) {
+SSN_DEV void ctl_inner_begin(DevCtl* C, const EvalOut* ev0, int64_t m, int nsm, int wsplits, int* info,
+                             cudaGraphConditionalHandle h_inner) {
   C->psi_evals++;
   C->tol_in = C->tol;
   if (C->inner_tol_mode) {  // res(kkt3), Eq. (20), of the point the outer iteration starts from
@@ -113,7 +113,7 @@ __global__ void k_ctl_inner_begin(DevCtl* C, const EvalOut* ev0, int64_t m, int 
 }
 
 // after the trial evaluation at s = 1: numeric checks, first Armijo test, K1 timing
-__global__ void k_ctl_armijo(DevCtl* C, const EvalOut* ev0, const EvalOut* ev1, cudaGraphConditionalHandle h_bt) {
+SSN_DEV void ctl_armijo(DevCtl* C, const EvalOut* ev0, const EvalOut* ev1, cudaGraphConditionalHandle h_bt) {
   C->seg_inner++;
   C->psi_evals++;
   C->aty_passes++;
@@ -154,7 +154,7 @@ __global__ void k_ctl_armijo(DevCtl* C, const EvalOut* ev0, const EvalOut* ev1, 
 }
 
 // after a backtrack evaluation (no gradient) at the current s
-__global__ void k_ctl_bt(DevCtl* C, const EvalOut* ev0, const EvalOut* evb, cudaGraphConditionalHandle h_bt) {
+SSN_DEV void ctl_bt(DevCtl* C, const EvalOut* ev0, const EvalOut* evb, cudaGraphConditionalHandle h_bt) {
   C->seg_bt++;
   C->psi_evals++;
   cudaGraphSetConditional(h_bt, bt_next(C, armijo_ok(C, evb->psi, ev0->psi, ev0->psimag)));
@@ -196,8 +196,8 @@ __global__ void __launch_bounds__(256) k_accept(DevCtl* C, int64_t m, int64_t n,
 }
 
 // end of a Newton step: next inner test
-__global__ void k_ctl_inner_end(DevCtl* C, const EvalOut* ev0, int64_t m, int nsm, int wsplits, int* info,
-                                cudaGraphConditionalHandle h_inner) {
+SSN_DEV void ctl_inner_end(DevCtl* C, const EvalOut* ev0, int64_t m, int nsm, int wsplits, int* info,
+                           cudaGraphConditionalHandle h_inner) {
   if (C->skip) C->skip = 0;  // a retried step does not advance j (host: --j)
   else if (C->numeric == 0) C->j++;
   cudaGraphSetConditional(h_inner, inner_next(C, ev0, m, nsm, wsplits, info));
@@ -248,6 +248,42 @@ __global__ void k_ctl_outer_end(DevCtl* C, const EvalOut* ev0, cudaGraphConditio
   const int go = C->k < C->max_outer;
   if (!go) C->outer_iters = C->k;
   cudaGraphSetConditional(h_outer, go);
+}
+
+// ---- ψ evaluation fused with the control decision that consumes it (one graph node instead of
+// two; each dependent node costs ~1-1.5 µs).  The finishing thread of the evaluation (EvalOut
+// written) runs the decision; with KIND = kHookInnerEnd and the gradient recompute predicated
+// off, thread 0 runs the decision alone.
+struct CtlHook {
+  DevCtl* C;
+  const EvalOut* ev0;  // current point's record
+  const EvalOut* ev1;  // this evaluation's record (Armijo trial / backtrack)
+  int64_t m;
+  int nsm, wsplits;
+  int* info;
+  cudaGraphConditionalHandle h;
+};
+enum { kHookInnerBegin = 1, kHookArmijo = 2, kHookBacktrack = 3, kHookInnerEnd = 4 };
+
+template <int KIND>
+__global__ void __cluster_dims__(kEvalCS, 1, 1) __launch_bounds__(K5_THREADS)
+    k_eval_ctl(int64_t m, const double* __restrict__ y, const double* __restrict__ bvec,
+               const double* __restrict__ part_vec, const int* __restrict__ part_valid, int nparts,
+               const double* __restrict__ part_scal, int nscal, Scal sc, double nb, int with_grad,
+               double* __restrict__ g_out, const int64_t* r_in, EvalOut* out, double* blk, unsigned* ticket,
+               const double* gd_src, const int* info_src, EvalOut* host_out, unsigned long long seq, const Scal* scp,
+               const int* pred, const double* nbp, CtlHook hk) {
+  if (KIND == kHookInnerEnd && pred && *pred == 0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) ctl_inner_end(hk.C, hk.ev0, hk.m, hk.nsm, hk.wsplits, hk.info, hk.h);
+    return;
+  }
+  if (!eval_body(m, y, bvec, part_vec, part_valid, nparts, part_scal, nscal, sc, nb, with_grad, g_out, r_in, out, blk,
+                 ticket, gd_src, info_src, host_out, seq, scp, pred, nbp))
+    return;
+  if (KIND == kHookInnerBegin) ctl_inner_begin(hk.C, hk.ev0, hk.m, hk.nsm, hk.wsplits, hk.info, hk.h);
+  if (KIND == kHookArmijo) ctl_armijo(hk.C, hk.ev0, hk.ev1, hk.h);
+  if (KIND == kHookBacktrack) ctl_bt(hk.C, hk.ev0, hk.ev1, hk.h);
+  if (KIND == kHookInnerEnd) ctl_inner_end(hk.C, hk.ev0, hk.m, hk.nsm, hk.wsplits, hk.info, hk.h);
 }
 
 }  // namespace ssn

@@ -740,7 +740,8 @@ int launch_gather_dev(ssnal_en_problem* P, const int32_t* J, const double* coef,
 int launch_eval(ssnal_en_problem* P, const double* y, const Scal& sc, int with_grad, const int* valid, int nparts,
                 double* g_out, const int64_t* r_dev, int slot, const double* gd_src = nullptr,
                 const int* info_src = nullptr, const Scal* scp = nullptr, const int* pred = nullptr,
-                const double* vec = nullptr, const double* scal = nullptr, int nscal = 0) {
+                const double* vec = nullptr, const double* scal = nullptr, int nscal = 0, int hook = 0,
+                const CtlHook* hk = nullptr) {
   const unsigned nblk = (unsigned)((P->m + 31) / 32);
   if (!P->capturing) ++P->ev_seq;
   if (!vec) vec = P->part_vec;
@@ -748,12 +749,20 @@ int launch_eval(ssnal_en_problem* P, const double* y, const Scal& sc, int with_g
     scal = P->part_scal;
     nscal = P->G;
   }
-  // graph mode: no mapped host mirror (decisions are taken on the device)
-  k_eval_reduce<<<nblk * kEvalCS, K5_THREADS, 0, P->st>>>(P->m, y, P->b, vec, valid, nparts, scal, nscal, sc,
-                                                 P->nb, with_grad, g_out, r_dev, P->ev_dev + slot, P->blk,
-                                                 P->ticket, gd_src, info_src,
-                                                 P->capturing ? nullptr : P->ev_host_dev + slot, P->ev_seq, scp, pred,
-                                                 P->capturing ? &P->ctl->nb : nullptr);
+  EvalOut* hout = P->capturing ? nullptr : P->ev_host_dev + slot;  // graph mode: decisions on the device
+  const double* nbp = P->capturing ? &P->ctl->nb : nullptr;
+  const dim3 grid(nblk * kEvalCS);
+#define SSN_EVAL_ARGS                                                                                              \
+  P->m, y, P->b, vec, valid, nparts, scal, nscal, sc, P->nb, with_grad, g_out, r_dev, P->ev_dev + slot, P->blk,   \
+      P->ticket, gd_src, info_src, hout, P->ev_seq, scp, pred, nbp
+  switch (hook) {  // graph mode: the control decision that consumes this evaluation, in the same launch
+    case kHookInnerBegin: k_eval_ctl<kHookInnerBegin><<<grid, K5_THREADS, 0, P->st>>>(SSN_EVAL_ARGS, *hk); break;
+    case kHookArmijo: k_eval_ctl<kHookArmijo><<<grid, K5_THREADS, 0, P->st>>>(SSN_EVAL_ARGS, *hk); break;
+    case kHookBacktrack: k_eval_ctl<kHookBacktrack><<<grid, K5_THREADS, 0, P->st>>>(SSN_EVAL_ARGS, *hk); break;
+    case kHookInnerEnd: k_eval_ctl<kHookInnerEnd><<<grid, K5_THREADS, 0, P->st>>>(SSN_EVAL_ARGS, *hk); break;
+    default: k_eval_reduce<<<grid, K5_THREADS, 0, P->st>>>(SSN_EVAL_ARGS);
+  }
+#undef SSN_EVAL_ARGS
   P->launches++;
   CKL();
   return SSNAL_OK;
@@ -1449,11 +1458,10 @@ int capture_graph(ssnal_en_problem* P, cudaGraph_t G) {
   if ((rc = launch_k1e(P, P->w[0], nullptr, 0.0, P->x, none, nullptr, &C->sc, nullptr))) return rc;
   if ((rc = launch_finalize(P, P->J[0], P->PJ[0], P->r_dev + 0))) return rc;
   if ((rc = launch_gather_vec(P, P->J[0], P->PJ[0], P->r_dev + 0))) return rc;
-  if ((rc = launch_eval(P, P->y[0], none, 1, nullptr, 1, P->g[0], P->r_dev + 0, 0, nullptr, nullptr, &C->sc)))
+  CtlHook hk{C, P->ev_dev + 0, nullptr, m, P->nsm, P->W_splits, P->info, h_inner};
+  if ((rc = launch_eval(P, P->y[0], none, 1, nullptr, 1, P->g[0], P->r_dev + 0, 0, nullptr, nullptr, &C->sc, nullptr,
+                        nullptr, nullptr, 0, kHookInnerBegin, &hk)))
     return rc;
-  k_ctl_inner_begin<<<1, 1, 0, P->st>>>(C, P->ev_dev + 0, m, P->nsm, P->W_splits, P->info, h_inner);
-  P->launches++;
-  CKL();
   P->seg_kernels[0] = (int)(P->launches - L);
   if ((rc = add_while(P->cap[0], h_inner, &body_i))) return rc;
   {
@@ -1466,12 +1474,10 @@ int capture_graph(ssnal_en_problem* P, cudaGraph_t G) {
     if ((rc = newton_direction_graph(P))) return rc;
     if ((rc = launch_k1(P, P->y[1], P->x, none, 1, P->w[1], &C->sc, C->tstamp))) return rc;
     if ((rc = launch_finalize(P, P->J[1], P->PJ[1], P->r_dev + 1))) return rc;
+    CtlHook ha{C, P->ev_dev + 0, P->ev_dev + 1, m, P->nsm, P->W_splits, P->info, h_bt};
     if ((rc = launch_eval(P, P->y[1], none, 1, P->cta_cnt, P->G, P->g[1], P->r_dev + 1, 1, P->scratch, P->info,
-                          &C->sc)))
+                          &C->sc, nullptr, nullptr, nullptr, 0, kHookArmijo, &ha)))
       return rc;
-    k_ctl_armijo<<<1, 1, 0, P->st>>>(C, P->ev_dev + 0, P->ev_dev + 1, h_bt);
-    P->launches++;
-    CKL();
     P->seg_kernels[1] = (int)(P->launches - L);
     if ((rc = add_while(P->cap[1], h_bt, &body_b))) return rc;
     {
@@ -1484,11 +1490,10 @@ int capture_graph(ssnal_en_problem* P, cudaGraph_t G) {
       P->launches++;
       if ((rc = launch_k1e(P, P->w[0], P->w[1], 0.0, P->x, none, P->w[2], &C->sc, &C->s))) return rc;
       if ((rc = launch_finalize(P, P->J[1], P->PJ[1], P->r_dev + 1))) return rc;
-      if ((rc = launch_eval(P, P->y[1], none, 0, nullptr, 0, nullptr, P->r_dev + 1, 2, nullptr, nullptr, &C->sc)))
+      CtlHook hb{C, P->ev_dev + 0, P->ev_dev + 2, m, P->nsm, P->W_splits, P->info, h_bt};
+      if ((rc = launch_eval(P, P->y[1], none, 0, nullptr, 0, nullptr, P->r_dev + 1, 2, nullptr, nullptr, &C->sc,
+                            nullptr, nullptr, nullptr, 0, kHookBacktrack, &hb)))
         return rc;
-      k_ctl_bt<<<1, 1, 0, P->st>>>(C, P->ev_dev + 0, P->ev_dev + 2, h_bt);
-      P->launches++;
-      CKL();
       P->seg_kernels[2] = (int)(P->launches - L);
       cudaGraph_t tmp;
       CK(cudaStreamEndCapture(P->cap[2], &tmp));
@@ -1501,12 +1506,10 @@ int capture_graph(ssnal_en_problem* P, cudaGraph_t G) {
                                               P->PJ[0], P->PJ[1], P->r_dev, P->w[0], P->w[1], P->w[2], P->ev_dev);
     P->launches++;
     if ((rc = launch_gather_vec(P, P->J[0], P->PJ[0], P->r_dev + 0, &C->need_grad))) return rc;
+    CtlHook he{C, P->ev_dev + 0, nullptr, m, P->nsm, P->W_splits, P->info, h_inner};
     if ((rc = launch_eval(P, P->y[0], none, 1, nullptr, 1, P->g[0], P->r_dev + 0, 0, nullptr, nullptr, &C->sc,
-                          &C->need_grad)))
+                          &C->need_grad, nullptr, nullptr, 0, kHookInnerEnd, &he)))
       return rc;
-    k_ctl_inner_end<<<1, 1, 0, P->st>>>(C, P->ev_dev + 0, m, P->nsm, P->W_splits, P->info, h_inner);
-    P->launches++;
-    CKL();
     P->seg_kernels[3] = (int)(P->launches - L);
     cudaGraph_t tmp;
     CK(cudaStreamEndCapture(P->cap[1], &tmp));
