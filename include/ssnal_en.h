@@ -107,6 +107,9 @@ double ssnal_en_lambda_max_l1(const ssnal_en_problem* p);
  *   time_k1=0 (1: time every K1 launch → stats.k1_time_s; CUDA events in host-driven mode,
  *     in-kernel %globaltimer stamps inside the graph),
  *   cluster_size=0 (auto: 16 if the device allows, else 8),
+ *   K4 variants (identical contract, results equal up to rounding): chol_dsm=1 (DSMEM-resident
+ *     16-CTA cluster Cholesky for N ≤ 160; 0: the L2-tiled k_chol_cluster for every N), chol_d2=1
+ *     (split-ownership DSMEM Cholesky k_chol_d2 for 160 < N ≤ 512; needs chol_dsm=1),
  *   certify=0 (1: after each solve compute stats.primal_viol with one extra Aᵀ pass),
  *   graph=1 (Algorithm 1 control on the device, the whole solve one CUDA graph; 0: host-driven
  *     control with one evaluation record read per ψ evaluation — identical results),

@@ -21,6 +21,7 @@
 #include "k_ctl.cuh"
 #include "k_newton.cuh"
 #include "k_chol_dsm.cuh"
+#include "k_chol_d2.cuh"
 #include "ssnal_en.h"
 
 using namespace ssn;
@@ -282,6 +283,8 @@ struct ssnal_en_problem {
   int use_dsm = 1;   // option chol_dsm: DSMEM-resident K4 for N ≤ 512 when schedulable
   int dsm_ok = 0;    // … schedulable on this device
   int chol_dsm = 0;  // use_dsm && dsm_ok
+  int use_d2 = 1;    // option chol_d2: split-ownership DSMEM K4 (k_chol_d2) for 160 < N ≤ 512
+  int d2_ok = 0;     // … schedulable on this device
   int gax_grid = 0;
   // device buffers
   double* w[3] = {nullptr, nullptr, nullptr};  // current / trial / backtrack
@@ -504,6 +507,25 @@ int configure(ssnal_en_problem* P) {
     cudaGetLastError();
   }
   P->chol_dsm = P->use_dsm && P->dsm_ok;
+  P->d2_ok = 0;
+  if (P->dsm_ok) {
+    CK(cudaFuncSetAttribute(k_chol_d2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kD2Smem));
+    CK(cudaFuncSetAttribute(k_chol_d2, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(kDsmCS);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = kD2Smem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = kDsmCS;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int nclus = 0;
+    if (cudaOccupancyMaxActiveClusters(&nclus, k_chol_d2, &cfg) == cudaSuccess && nclus >= 1) P->d2_ok = 1;
+    cudaGetLastError();
+  }
   return SSNAL_OK;
 }
 
@@ -882,9 +904,31 @@ int launch_chol_dsm(ssnal_en_problem* P, double* M, int N, double* out, double s
   return SSNAL_OK;
 }
 
+// Split-ownership DSMEM K4 (k_chol_d2.cuh) for kDsmUseMax < N ≤ kDsmMaxN: same contract.
+int launch_chol_d2(ssnal_en_problem* P, double* M, int N, double* out, double scale, const double* dotv,
+                   double* dot_out, const double* ybase, double* yt, const DirGeo* geo, int want) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(kDsmCS);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = kD2Smem;
+  cfg.stream = P->st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = kDsmCS;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  const CholArgs* ca = want < 0 ? P->chol_args : nullptr;
+  CK(cudaLaunchKernelEx(&cfg, k_chol_d2, (const double*)M, N, N + 1, out, scale, dotv, dot_out, P->info, ybase, yt,
+                        geo, want, kDsmUseMax + 1, kDsmMaxN, ca));
+  P->launches++;
+  return SSNAL_OK;
+}
+
 // Cluster Cholesky + both triangular solves: M holds the matrix (ld = N+1) and the rhs in row N.
-// Host mode: the DSMEM-resident kernel for N ≤ 512, else k_chol_cluster.  Graph mode (geo): the
-// DSMEM kernel predicated on N ≤ 512 and, when m > 512, k_chol_cluster predicated on N > 512.
+// Host mode: k_chol_dsm for N ≤ 160, k_chol_d2 for 160 < N ≤ 512, else k_chol_cluster.  Graph
+// mode (geo): each kernel that can occur for this m, predicated on its N range.
 int launch_chol(ssnal_en_problem* P, double* M, int N, double* out, double scale, const double* dotv,
                 double* dot_out, const double* ybase = nullptr, double* yt = nullptr, const DirGeo* geo = nullptr,
                 int want = 0) {
@@ -896,6 +940,14 @@ int launch_chol(ssnal_en_problem* P, double* M, int N, double* out, double scale
     }
     if (geo ? P->m <= kDsmUseMax : N <= kDsmUseMax) return SSNAL_OK;
     nmin = kDsmUseMax + 1;
+    if (P->use_d2 && P->d2_ok) {
+      if (geo || N <= kDsmMaxN) {
+        int rc = launch_chol_d2(P, M, N, out, scale, dotv, dot_out, ybase, yt, geo, want);
+        if (rc) return rc;
+      }
+      if (geo ? P->m <= kDsmMaxN : N <= kDsmMaxN) return SSNAL_OK;
+      nmin = kDsmMaxN + 1;
+    }
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(P->cluster);
@@ -1951,6 +2003,10 @@ int ssnal_en_set_option(ssnal_en_problem* P, const char* key, double v) {
     P->cg_maxit = (int)v;
     drop_graph(P);
   }
+  else if (k == "chol_d2" && (v == 0 || v == 1)) {
+    P->use_d2 = (int)v;
+    drop_graph(P);  // the K4 variant is baked into the graph
+  }
   else if (k == "chol_dsm" && (v == 0 || v == 1)) {
     P->use_dsm = (int)v;
     P->chol_dsm = P->use_dsm && P->dsm_ok;
@@ -1976,6 +2032,7 @@ double ssnal_en_get_info(const ssnal_en_problem* P, const char* key) {
   if (k == "k1_smem") return (double)P->k1_smem;
   if (k == "cluster_size") return P->cluster;
   if (k == "chol_dsm") return P->chol_dsm;
+  if (k == "chol_d2") return P->chol_dsm && P->use_d2 && P->d2_ok;
   if (k == "num_sms") return P->nsm;
   if (k == "graph") return P->use_graph;
   if (k == "format") return P->fmt;

@@ -1,7 +1,8 @@
 """K4 variants (Eq. (18)/(19) factor and solves): the DSMEM-resident cluster
-Cholesky (k_chol_dsm, used for N ≤ 160) against the L2-tiled cluster Cholesky (k_chol_cluster)
-and the oracle, through the Newton-direction hook, across tile edges and the switch point; and
-whole solves with either variant, graph-mode control ≡ host-mode control."""
+Cholesky (k_chol_dsm, N ≤ 160) and the split-ownership DSMEM Cholesky (k_chol_d2, 160 < N ≤ 512)
+against the L2-tiled cluster Cholesky (k_chol_cluster) and the oracle, through the
+Newton-direction hook, across tile edges and the switch points; and whole solves with each
+variant, graph-mode control ≡ host-mode control."""
 import numpy as np
 import pytest
 
@@ -25,7 +26,9 @@ def direction(P, J, g, kappa):
 
 
 @pytest.mark.parametrize("m,r", [(500, 1), (500, 31), (500, 32), (500, 33), (500, 100), (500, 160), (500, 161),
-                                 (500, 300), (160, 159), (160, 400), (161, 400), (40, 7), (64, 1000)])
+                                 (500, 300), (160, 159), (160, 400), (161, 400), (40, 7), (64, 1000),
+                                 (500, 192), (500, 255), (500, 256), (500, 257), (500, 435), (500, 499),
+                                 (500, 500), (500, 700), (511, 900), (512, 1000), (513, 1000), (400, 2000)])
 def test_dsm_vs_cluster_vs_oracle(m, r):
     n = max(2 * r, 1500)
     cfg = synth.Config("k4", m, n, synth.IID_STD, 5, 1.0, 2.0, 5.0, 0.7, (0.5,), m + r)
@@ -37,21 +40,25 @@ def test_dsm_vs_cluster_vs_oracle(m, r):
     d_c, br_c = oracle.newton_direction(A, J, g, kappa)
     with Problem(A, b) as P:
         out = {}
-        for v in (1, 0):
+        for v, v2 in ((1, 1), (1, 0), (0, 0)):
             P.set_option("chol_dsm", v)
-            out[v] = direction(P, J, g, kappa)
-    (d1, gd1, b1), (d0, gd0, b0) = out[1], out[0]
-    assert b1 == b0 == br_c
+            P.set_option("chol_d2", v2)
+            out[v, v2] = direction(P, J, g, kappa)
+    (d0, gd0, b0) = out[0, 0]
     scale = np.max(np.abs(d_c))
-    assert np.max(np.abs(d1 - d0)) <= 1e-12 * scale
-    assert np.max(np.abs(d1 - d_c)) <= 1e-10 * scale
-    assert gd1 == pytest.approx(gd0, rel=1e-12)
+    for key in ((1, 1), (1, 0)):
+        (d1, gd1, b1) = out[key]
+        assert b1 == b0 == br_c
+        assert np.max(np.abs(d1 - d0)) <= 1e-12 * scale, key
+        assert np.max(np.abs(d1 - d_c)) <= 1e-10 * scale, key
+        assert gd1 == pytest.approx(gd0, rel=1e-12)
 
 
-@pytest.mark.parametrize("m,n", [(150, 4000), (300, 8000)])
+@pytest.mark.parametrize("m,n", [(150, 4000), (300, 8000), (500, 20000)])
 def test_solves_with_both_variants(m, n):
-    """m = 150: every factor on the DSMEM kernel; m = 300: both kernels, switching on N inside the
-    graph.  Same iteration as the other variant up to rounding; graph ≡ host bitwise."""
+    """m = 150: every factor on the DSMEM kernel; m = 300 / 500: k_chol_dsm and k_chol_d2, switching
+    on N inside the graph.  Same iteration as the L2-tiled variant up to rounding; graph ≡ host
+    bitwise."""
     cfg = synth.Config("k4s", m, n, synth.AR1_STD, 10, 1.0, 2.0, 5.0, 0.7, (0.5,), 11)
     A = synth.design(cfg)
     b, _ = synth.response(cfg)
