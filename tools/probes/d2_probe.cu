@@ -117,14 +117,16 @@ int main(int argc, char** argv) {
            ms2 * 1e3 / 20, ms1 * 1e3 / 20, e2 / xm, e1r / xm, xm, dotv, dref, hinfo, cudaGetErrorString(err),
            ok ? "OK" : "FAIL");
     if (getenv("D2_TIMELINE")) {
-      unsigned long long tl[18][8];
+      unsigned long long tl[18][12];
       cudaMemcpyFromSymbol(tl, g_d2, sizeof(tl));
       const unsigned long long t0 = tl[17][0];
       auto f = [&](unsigned long long v) { return v >= t0 && v - t0 < 10000000ull ? (v - t0) * 1e-3 : -1.0; };
       printf("  start→factor-loop-end %.1f  end %.1f us\n", f(tl[17][1]), f(tl[17][2]));
-      printf("   j:  fac0  facdone  W_j  q1start q1strip q1push L(j+1,j)  v_j\n");
-      for (int j = 0; j < (N + 31) / 32; ++j)
+      printf("   j:  fac0  facdone  W_j  q1start q1strip q1push L(j+1,j)  v_j | h(j+2,j): Astart Adone Wgot publish\n");
+      for (int j = 0; j < (N + 31) / 32; ++j) {
         printf("  %2d: %6.1f %6.1f %6.1f %6.1f %6.1f %6.1f %6.1f %6.1f\n", j, f(tl[j][0]), f(tl[j][3]), f(tl[j][1]), f(tl[j][4]), f(tl[j][6]), f(tl[j][7]), f(tl[j][2]), f(tl[j][5]));
+        printf("      %6.1f %6.1f %6.1f %6.1f\n", f(tl[j][10]), f(tl[j][11]), f(tl[j][9]), f(tl[j][8]));
+      }
     }
     cudaFree(dM); cudaFree(dout); cudaFree(dout2); cudaFree(info); cudaFree(dot);
   }

@@ -1,0 +1,193 @@
+// Probe: variants of the 32 x 32 diagonal factor (W on/off, Newton steps of the reciprocal sqrt).
+#include <cstdio>
+#include <cmath>
+#include "../../paper_2006_03970_b200/csrc/k_newton.cuh"
+using namespace ssn;
+template <int NEWTON> __device__ __forceinline__ double rsq_n(double d) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+#pragma unroll
+  for (int it = 0; it < NEWTON; ++it) { const double r = fma(-d * y, y, 1.0); y = fma(0.5 * y, r, y); }
+  return y;
+}
+template <bool WANTW, int NEWTON>
+__device__ __forceinline__ void df_var(const double* S, double* M, int ld, int n0, int kn, int nrow, double* Wout, double* Wsm,
+                          int* info, double* cb, int t128) {
+  const int w = t128 >> 5, lane = t128 & 31;
+  double a[8], dgw[8], wr[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int c = 8 * w + q;
+    a[q] = (lane < nrow && c < kn) ? S[lane * TLD + c] : (lane == c ? 1.0 : 0.0);
+    dgw[q] = (c < kn) ? S[c * TLD + c] : 1.0;
+    wr[q] = (lane == c) ? 1.0 : 0.0;
+  }
+  bool bad = false;
+#pragma unroll 1
+  for (int blk = 0; blk < 4; ++blk) {
+    double* Lb = cb + (blk & 1) * (CHT * 9 + 8 * 33);  // Lb[r * 9 + p] = L[r][8blk + p]
+    double* Wb = Lb + CHT * 9;                          // Wb[p * 33 + c] = W[8blk + p][c]
+    if (w == blk) {
+      const double* Lp = cb + ((blk + 1) & 1) * (CHT * 9 + 8 * 33);  // block blk − 1
+      const double* Wp = Lp + CHT * 9;
+      double lrp[8], wbp[8];
+      if (blk > 0) {
+#pragma unroll
+        for (int pp = 0; pp < 8; ++pp) {
+          lrp[pp] = Lp[lane * 9 + pp];
+          wbp[pp] = Wp[pp * 33 + lane];
+        }
+      }
+      if (blk > 0) {  // rank-8 update of this block's columns from block blk − 1, before any pivot:
+                      // eight independent chains, so only pivot 0 waits for one of them
+#pragma unroll
+        for (int p = 0; p < 8; ++p)
+#pragma unroll
+          for (int pp = 0; pp < 8; ++pp) {
+            const double l = Lp[(8 * w + p) * 9 + pp];
+            dgw[p] = fma(-l, l, dgw[p]);
+            a[p] = fma(-lrp[pp], l, a[p]);
+            if (WANTW) wr[p] = fma(-l, wbp[pp], wr[p]);
+          }
+      }
+#pragma unroll
+      for (int p = 0; p < 8; ++p) {
+        const int j = 8 * blk + p;
+        double d = dgw[p];
+        bad |= (j < kn) && !(d > 0.0);
+        d = (j < kn && d > 0.0) ? d : 1.0;
+        const double inv = rsq_n<NEWTON>(d);
+        const double lij = (lane > j) ? a[p] * inv : (lane == j ? d * inv : 0.0);
+        const double wj = wr[p] * inv;  // W row j scaled (final)
+#pragma unroll
+        for (int q = p + 1; q < 8; ++q) {
+          const double lq = __shfl_sync(0xffffffffu, lij, 8 * blk + q);  // L[8blk+q][j]
+          dgw[q] = fma(-lq, lq, dgw[q]);
+          a[q] = fma(-lij, lq, a[q]);
+          if (WANTW) wr[q] = fma(-lq, wj, wr[q]);
+        }
+        a[p] = lij;
+        wr[p] = wj;
+      }
+#pragma unroll
+      for (int p = 0; p < 8; ++p) {
+        Lb[lane * 9 + p] = a[p];
+        Wb[p * 33 + lane] = wr[p];
+      }
+    }
+    asm volatile("bar.sync 2, 128;" ::: "memory");
+    if (w > blk + 1) {  // eager rank-8 update from block blk
+      double lr[8], wb[8];
+#pragma unroll
+      for (int p = 0; p < 8; ++p) {
+        lr[p] = Lb[lane * 9 + p];
+        wb[p] = Wb[p * 33 + lane];
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const double* lc = Lb + (8 * w + q) * 9;
+#pragma unroll
+        for (int p = 0; p < 8; ++p) {
+          const double l = lc[p];  // L[8w+q][8blk+p]
+          dgw[q] = fma(-l, l, dgw[q]);
+          a[q] = fma(-lr[p], l, a[q]);
+          if (WANTW) wr[q] = fma(-l, wb[p], wr[q]);
+        }
+      }
+    }
+  }
+  if (bad && lane == 0) atomicExch(info, 1);
+  if (!M) asm volatile("bar.sync 2, 128;" ::: "memory");  // every warp has read S before L overwrites it
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int c = 8 * w + q;
+    if (M) {
+      if (lane < nrow && c < kn && c <= lane) M[(int64_t)(n0 + lane) + (int64_t)(n0 + c) * ld] = a[q];
+    } else {  // L into the smem tile itself (DSMEM-resident factor): rows < nrow, cols < kn, else 0
+      const_cast<double*>(S)[lane * TLD + c] = (lane < nrow && c < kn && c <= lane) ? a[q] : 0.0;
+    }
+    const double wv = (c < kn && lane < kn) ? wr[q] : (lane == c ? 1.0 : 0.0);  // pad: identity
+    if (Wout) Wout[c * CHT + lane] = wv;
+    if (Wsm) Wsm[c * TLD + lane] = wv;
+  }
+}
+
+
+// one warp, lane = row, the row in registers, fully unrolled (L only)
+template <int NEWTON>
+__device__ __forceinline__ void df_warp(double* S, int lane) {
+  double a0[CHT];
+#pragma unroll
+  for (int c = 0; c < CHT; ++c) a0[c] = S[lane * TLD + c];
+  double d = __shfl_sync(0xffffffffu, a0[0], 0);
+#pragma unroll
+  for (int j = 0; j < CHT; ++j) {
+    const double dd = d > 0.0 ? d : 1.0;
+    const double inv = rsq_n<NEWTON>(dd);
+    const double l0 = lane > j ? a0[j] * inv : (lane == j ? dd * inv : 0.0);
+    a0[j] = l0;
+    if (j + 1 < CHT) {
+      const double lq = __shfl_sync(0xffffffffu, l0, j + 1);
+      a0[j + 1] = fma(-l0, lq, a0[j + 1]);
+      d = __shfl_sync(0xffffffffu, a0[j + 1], j + 1);
+    }
+#pragma unroll
+    for (int q = j + 2; q < CHT; ++q) {
+      const double lq = __shfl_sync(0xffffffffu, l0, q);
+      a0[q] = fma(-l0, lq, a0[q]);
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < CHT; ++c) S[lane * TLD + c] = c <= lane ? a0[c] : 0.0;
+}
+template <int NEWTON>
+__global__ void k_warp(const double* Sg, double* M, unsigned long long* cyc) {
+  __shared__ double S[CHT * TLD];
+  for (int e = threadIdx.x; e < CHT * TLD; e += 32) S[e] = Sg[e];
+  __syncwarp();
+  long long c0 = clock64();
+  df_warp<NEWTON>(S, threadIdx.x);
+  long long c1 = clock64();
+  if (threadIdx.x == 0) cyc[0] = c1 - c0;
+  for (int e = threadIdx.x; e < CHT * CHT; e += 32) M[e] = S[(e % 32) * TLD + e / 32];
+}
+template <bool WANTW, int NEWTON>
+__global__ void k_var(const double* Sg, double* M, double* W, int* info, unsigned long long* cyc) {
+  __shared__ double S[CHT * TLD + kDiagScratch];
+  for (int e = threadIdx.x; e < CHT * TLD; e += 128) S[e] = Sg[e];
+  __syncthreads();
+  long long c0 = clock64();
+  df_var<WANTW, NEWTON>(S, M, 32, 0, 32, 32, W, nullptr, info, S + CHT * TLD, threadIdx.x);
+  long long c1 = clock64();
+  if (threadIdx.x == 0) cyc[0] = c1 - c0;
+}
+template <bool WANTW, int NEWTON> void run(const char* name, double* dS, double* dM, double* dW, int* info, unsigned long long* cyc) {
+  for (int rep = 0; rep < 5; ++rep) k_var<WANTW, NEWTON><<<1, 128>>>(dS, dM, dW, info, cyc);
+  cudaDeviceSynchronize();
+  unsigned long long c; cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
+  printf("%-24s %6llu cycles (%.0f per pivot) %s\n", name, c, c / 32.0, cudaGetErrorString(cudaGetLastError()));
+}
+int main() {
+  double h[CHT * TLD];
+  for (int r = 0; r < CHT; ++r)
+    for (int c = 0; c < TLD; ++c) h[r * TLD + c] = (r == c) ? 4.0 + r : ((c < CHT) ? 0.3 * sin(r * 7.0 + c * 13.0 + (r > c ? r * c : c * r)) : 0.0);
+  for (int r = 0; r < CHT; ++r) for (int c = 0; c < r; ++c) h[c * TLD + r] = h[r * TLD + c];
+  double *dS, *dM, *dW; int* info; unsigned long long* cyc;
+  cudaMalloc(&dS, sizeof(h)); cudaMalloc(&dM, 32 * 32 * 8); cudaMalloc(&dW, 32 * 32 * 8); cudaMalloc(&info, 4); cudaMalloc(&cyc, 64);
+  cudaMemcpy(dS, h, sizeof(h), cudaMemcpyHostToDevice);
+  run<true, 2>("W, 2 Newton", dS, dM, dW, info, cyc);
+  run<false, 2>("no W, 2 Newton", dS, dM, dW, info, cyc);
+  run<true, 1>("W, 1 Newton", dS, dM, dW, info, cyc);
+  run<false, 1>("no W, 1 Newton", dS, dM, dW, info, cyc);
+  for (int rep = 0; rep < 5; ++rep) k_warp<2><<<1, 32>>>(dS, dM, cyc);
+  cudaDeviceSynchronize();
+  unsigned long long c; cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
+  double L[32 * 32]; cudaMemcpy(L, dM, sizeof(L), cudaMemcpyDeviceToHost);
+  double e1 = 0;
+  for (int i = 0; i < 32; ++i) for (int j = 0; j <= i; ++j) {
+    double s2 = 0; for (int p = 0; p <= j; ++p) s2 += L[i + p * 32] * L[j + p * 32];
+    e1 = fmax(e1, fabs(s2 - h[i * TLD + j]));
+  }
+  printf("%-24s %6llu cycles (%.0f per pivot) err %.2e %s\n", "1 warp unrolled, L only", c, c / 32.0, e1, cudaGetErrorString(cudaGetLastError()));
+  return 0;
+}
