@@ -761,6 +761,11 @@ SSN_DEV bool eval_body(int64_t m, const double* __restrict__ y,
   const int cs = (int)(blockIdx.x % kEvalCS), rb = (int)(blockIdx.x / kEvalCS), nrb = (int)(gridDim.x / kEvalCS);
   const int64_t k = (int64_t)rb * 32 + lane;
   __shared__ double gsum[32];
+  double yk = 0.0, bk = 0.0;  // prefetched for the row-block sums below
+  if (cs == 0 && warp == 0 && k < m) {
+    yk = y[k];
+    bk = bvec[k];
+  }
   if (with_grad) {
     const int q0 = (int)((int64_t)nparts * cs / kEvalCS), q1 = (int)((int64_t)nparts * (cs + 1) / kEvalCS);
     const int b0 = q0 + (int)((int64_t)(q1 - q0) * warp / 8), b1 = q0 + (int)((int64_t)(q1 - q0) * (warp + 1) / 8);
@@ -800,12 +805,36 @@ SSN_DEV bool eval_body(int64_t m, const double* __restrict__ y,
     }
     cluster.sync();  // rank 0 has read every CTA's sums
   }
-  if (cs != 0) return false;
+  if (cs == 1 && rb == 0) {  // the scalar partials of K1/K1e, while the row blocks finish
+    if (warp != 0) return false;
+    double s[4] = {0, 0, 0, 0};
+    for (int q0 = lane; q0 < nscal; q0 += 32 * 8) {  // lane sums q ≡ lane (mod 32) ascending; 8 in flight
+      double v[8][4];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) v[u][j] = q0 + 32 * u < nscal ? __ldcg(part_scal + (q0 + 32 * u) * 4 + j) : 0.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) s[j] += v[u][j];
+    }
+    for (int j = 0; j < 4; ++j) s[j] = warp_allsum(s[j]);
+    if (lane == 0) {
+      for (int j = 0; j < 4; ++j) blk[nrb * 3 + j] = s[j];
+      __threadfence();
+      const unsigned t = atomicAdd(ticket, 1u);
+      last = (t == (unsigned)nrb);
+    }
+    __syncwarp();
+    if (!last) return false;
+  }
+  if (cs > 1 || (cs == 1 && rb != 0)) return false;
+  if (cs == 0) {
   __syncthreads();
   if (warp == 0) {
     double yy = 0.0, by = 0.0, gg = 0.0;
     if (k < m) {
-      const double yk = y[k], bk = bvec[k];
       yy = yk * yk;
       by = bk * yk;
       if (with_grad) {
@@ -824,11 +853,12 @@ SSN_DEV bool eval_body(int64_t m, const double* __restrict__ y,
       blk[rb * 3 + 2] = gg;
       __threadfence();
       const unsigned t = atomicAdd(ticket, 1u);
-      last = (t == (unsigned)nrb - 1);
+      last = (t == (unsigned)nrb);  // nrb row blocks + the scalar CTA
     }
   }
   __syncthreads();
   if (!last || warp != 0) return false;
+  }
   __threadfence();
   // warp 0 of the last CTA: lane ℓ sums entries q ≡ ℓ (mod 32) in order, then a fixed butterfly
   double a = 0, bb = 0, c = 0;
@@ -837,22 +867,11 @@ SSN_DEV bool eval_body(int64_t m, const double* __restrict__ y,
     bb += __ldcg(blk + q * 3 + 1);
     c += __ldcg(blk + q * 3 + 2);
   }
-  double s[4] = {0, 0, 0, 0};
-  for (int q0 = lane; q0 < nscal; q0 += 32 * 8) {  // lane sums q ≡ lane (mod 32) ascending; 8 in flight
-    double v[8][4];
-#pragma unroll
-    for (int u = 0; u < 8; ++u)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) v[u][j] = q0 + 32 * u < nscal ? __ldcg(part_scal + (q0 + 32 * u) * 4 + j) : 0.0;
-#pragma unroll
-    for (int u = 0; u < 8; ++u)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) s[j] += v[u][j];
-  }
+  double s[4];
+  for (int j = 0; j < 4; ++j) s[j] = __ldcg(blk + nrb * 3 + j);  // summed by CTA (0, 1)
   a = warp_allsum(a);
   bb = warp_allsum(bb);
   c = warp_allsum(c);
-  for (int j = 0; j < 4; ++j) s[j] = warp_allsum(s[j]);
   if (lane != 0) return false;
   EvalOut o;
   o.yy = a;
