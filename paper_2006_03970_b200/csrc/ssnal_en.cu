@@ -426,6 +426,11 @@ int configure(ssnal_en_problem* P) {
   int k = (int)(32768 / (K1_GRP * bytes_col));  // ~32 KB of A per tile
   if (k < 1) k = 1;
   if (k > 32) k = 32;  // ≤ 256 columns per tile
+  {  // small n: smaller tiles, so the pass spreads over the SMs and their consumer warps (a warp
+     // owns whole tiles; cfg1 with 32 KB tiles ran 13 tiles on 13 warps, 14.6 µs per pass)
+    const int64_t kmax = (n + (int64_t)K1_GRP * P->nsm * K1_NWC - 1) / ((int64_t)K1_GRP * P->nsm * K1_NWC);
+    if (k > kmax) k = (int)(kmax < 1 ? 1 : kmax);
+  }
   P->C = K1_GRP * k;   // multiple of 8: one mask byte per 8 columns, 16-B aligned tiles
   if (P->fmt) {
     P->TW = (int)((P->cstride / 4 + 31) / 32);
