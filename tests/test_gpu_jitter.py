@@ -26,8 +26,10 @@ def dup_problem(m, r, seed):
     return A, b, g
 
 
-@pytest.mark.parametrize("m,r,br", [(40, 64, 2), (64, 12, 1)])
+@pytest.mark.parametrize("m,r,br", [(40, 64, 2), (64, 12, 1), (300, 400, 2), (500, 200, 1), (600, 700, 2)])
 def test_hook_retry_matches_oracle_jittered(m, r, br):
+    """N = min(m, r) covers the three K4 kernels: k_chol_dsm (≤ 160), k_chol_d2 (161–512) and
+    k_chol_cluster (> 512)."""
     A, b, g = dup_problem(m, r, seed=m)
     kappa = 1e25
     J = np.arange(r, dtype=np.int32)
