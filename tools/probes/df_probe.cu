@@ -151,6 +151,93 @@ __global__ void k_warp(const double* Sg, double* M, unsigned long long* cyc) {
   if (threadIdx.x == 0) cyc[0] = c1 - c0;
   for (int e = threadIdx.x; e < CHT * CHT; e += 32) M[e] = S[(e % 32) * TLD + e / 32];
 }
+
+// L-only variant: the next owner applies the previous block's rank-8 update lazily, column by
+// column right before each pivot, with two partial sums (shorter chains); no W.
+template <int NEWTON>
+__device__ __forceinline__ void df_lazy(double* S, double* cb, int t128) {
+  const int w = t128 >> 5, lane = t128 & 31;
+  constexpr int BS = CHT * 9;
+  double a[8], dgw[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int c = 8 * w + q;
+    a[q] = S[lane * TLD + c];
+    dgw[q] = S[c * TLD + c];
+  }
+#pragma unroll 1
+  for (int blk = 0; blk < 4; ++blk) {
+    double* Lb = cb + (blk & 1) * BS;
+    if (w == blk) {
+      const double* Lp = cb + ((blk + 1) & 1) * BS;
+      double lrp[8];
+      if (blk > 0)
+#pragma unroll
+        for (int pp = 0; pp < 8; ++pp) lrp[pp] = Lp[lane * 9 + pp];
+#pragma unroll
+      for (int p = 0; p < 8; ++p) {
+        if (blk > 0) {
+          double d0 = 0, d1 = 0, a0 = 0, a1 = 0;
+#pragma unroll
+          for (int pp = 0; pp < 8; pp += 2) {
+            const double l0 = Lp[(8 * w + p) * 9 + pp], l1 = Lp[(8 * w + p) * 9 + pp + 1];
+            d0 = fma(l0, l0, d0); d1 = fma(l1, l1, d1);
+            a0 = fma(lrp[pp], l0, a0); a1 = fma(lrp[pp + 1], l1, a1);
+          }
+          dgw[p] -= d0 + d1;
+          a[p] -= a0 + a1;
+        }
+        const int j = 8 * blk + p;
+        double d = dgw[p];
+        d = d > 0.0 ? d : 1.0;
+        const double inv = rsq_n<NEWTON>(d);
+        const double lij = (lane > j) ? a[p] * inv : (lane == j ? d * inv : 0.0);
+#pragma unroll
+        for (int q = p + 1; q < 8; ++q) {
+          const double lq = __shfl_sync(0xffffffffu, lij, 8 * blk + q);
+          dgw[q] = fma(-lq, lq, dgw[q]);
+          a[q] = fma(-lij, lq, a[q]);
+        }
+        a[p] = lij;
+      }
+#pragma unroll
+      for (int p = 0; p < 8; ++p) Lb[lane * 9 + p] = a[p];
+    }
+    asm volatile("bar.sync 2, 128;" ::: "memory");
+    if (w > blk + 1) {
+      double lr[8];
+#pragma unroll
+      for (int p = 0; p < 8; ++p) lr[p] = Lb[lane * 9 + p];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const double* lc = Lb + (8 * w + q) * 9;
+#pragma unroll
+        for (int p = 0; p < 8; ++p) {
+          const double l = lc[p];
+          dgw[q] = fma(-l, l, dgw[q]);
+          a[q] = fma(-lr[p], l, a[q]);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int c = 8 * w + q;
+    S[lane * TLD + c] = c <= lane ? a[q] : 0.0;
+  }
+}
+template <int NEWTON>
+__global__ void k_lazy(const double* Sg, double* M, unsigned long long* cyc) {
+  __shared__ double S[CHT * TLD + kDiagScratch];
+  for (int e = threadIdx.x; e < CHT * TLD; e += 128) S[e] = Sg[e];
+  __syncthreads();
+  long long c0 = clock64();
+  df_lazy<NEWTON>(S, S + CHT * TLD, threadIdx.x);
+  long long c1 = clock64();
+  __syncthreads();
+  if (threadIdx.x == 0) cyc[0] = c1 - c0;
+  for (int e = threadIdx.x; e < CHT * CHT; e += 128) M[e] = S[(e % 32) * TLD + e / 32];
+}
 template <bool WANTW, int NEWTON>
 __global__ void k_var(const double* Sg, double* M, double* W, int* info, unsigned long long* cyc) {
   __shared__ double S[CHT * TLD + kDiagScratch];
@@ -179,6 +266,18 @@ int main() {
   run<false, 2>("no W, 2 Newton", dS, dM, dW, info, cyc);
   run<true, 1>("W, 1 Newton", dS, dM, dW, info, cyc);
   run<false, 1>("no W, 1 Newton", dS, dM, dW, info, cyc);
+  for (int v = 0; v < 2; ++v) {
+    for (int rep = 0; rep < 5; ++rep) { if (v == 0) k_lazy<2><<<1, 128>>>(dS, dM, cyc); else k_lazy<1><<<1, 128>>>(dS, dM, cyc); }
+    cudaDeviceSynchronize();
+    unsigned long long c2; cudaMemcpy(&c2, cyc, 8, cudaMemcpyDeviceToHost);
+    double L2[32 * 32]; cudaMemcpy(L2, dM, sizeof(L2), cudaMemcpyDeviceToHost);
+    double e2 = 0;
+    for (int i = 0; i < 32; ++i) for (int j = 0; j <= i; ++j) {
+      double s2 = 0; for (int p = 0; p <= j; ++p) s2 += L2[i + p * 32] * L2[j + p * 32];
+      e2 = fmax(e2, fabs(s2 - h[i * TLD + j]));
+    }
+    printf("%-24s %6llu cycles (%.0f per pivot) err %.2e %s\n", v == 0 ? "lazy split, no W, 2N" : "lazy split, no W, 1N", c2, c2 / 32.0, e2, cudaGetErrorString(cudaGetLastError()));
+  }
   for (int rep = 0; rep < 5; ++rep) k_warp<2><<<1, 32>>>(dS, dM, cyc);
   cudaDeviceSynchronize();
   unsigned long long c; cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
