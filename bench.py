@@ -121,6 +121,19 @@ def k1_bytes(m, n, geno=False):
     return a + 16 * n + 8 * m
 
 
+def small_roofline(m, n, sts, dev_s, peak, peak_src):
+    """One-CTA path (k_small_solve, m ≤ 64, n ≤ 1024): no K1 launches; the whole solve is one
+    latency-bound kernel with A L2-resident.  Reported: the effective A-pass bandwidth of the solve
+    (passes × 8mn bytes / device time) against the HBM peak, for context only."""
+    passes = sum(s["aty_passes"] for s in sts)
+    achieved = passes * 8.0 * m * n / max(dev_s, 1e-30) / 1e9
+    return {"bound": "latency", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": None, "peak_source": peak_src, "kernel": "k_small_solve",
+            "bytes_per_launch": passes * 8 * m * n, "launches": len(sts), "mean_launch_us": dev_s / max(len(sts), 1) * 1e6,
+            "share_of_step": 1.0,
+            "note": "m <= 64, n <= 1024: Algorithm 1 in one CTA (A streamed from L2 by TMA, 2-stage ring); latency-bound, not an HBM stream"}
+
+
 def geno_roofline(m, n, k1_avg, k1_gbs, hbm_peak, traffic):
     """K1g (packed genotype codes) moves 32x fewer bytes than K1 and is bound by the
     FP64 pipe, not HBM: per decoded element two bucket adds (DADD) — peak = 64 FP64 ops/clk/SM
@@ -311,7 +324,8 @@ def bench_ours(args, rank, world, local_rank):
                                else "fp64 column-major"),
                    "newton_strategy": ("exact (Eq. 18/19); CG when min(m, r) > 1e4 (P:379)" if args.cg_ratio == 0
                                        else f"CG (K6) when r > {args.cg_ratio:g} m, else exact (Eq. 18/19)")},
-        "roofline": {**({"bound": "hbm", "achieved": k1_gbs, "peak": peak, "unit": "GB/s",
+        "roofline": small_roofline(m, n, last_stats, dev_sum / max(args.steps, 1), peak, peak_src) if k1_launches == 0 and
+                    not args.geno else {**({"bound": "hbm", "achieved": k1_gbs, "peak": peak, "unit": "GB/s",
                          "frac": (k1_gbs / peak) if k1_gbs else None, "traffic": traffic, "peak_source": peak_src}
                         if not args.geno else geno_roofline(m, n, k1_avg, k1_gbs, peak, traffic)),
                      "kernel": "k1g_aty_fused" if args.geno else "k1_aty_fused",

@@ -107,6 +107,9 @@ double ssnal_en_lambda_max_l1(const ssnal_en_problem* p);
  *   time_k1=0 (1: time every K1 launch → stats.k1_time_s; CUDA events in host-driven mode,
  *     in-kernel %globaltimer stamps inside the graph),
  *   cluster_size=0 (auto: 16 if the device allows, else 8),
+ *   small=1 (m ≤ 64 and n ≤ 1024, fp64 storage, unsharded, no CG strategy: the whole solve runs in
+ *     one 512-thread CTA, k_small_solve — same iteration and statistics, reduction orders differ;
+ *     0: the multi-kernel graph / host paths),
  *   K4 variants (identical contract, results equal up to rounding): chol_dsm=1 (DSMEM-resident
  *     16-CTA cluster Cholesky for N ≤ 160; 0: the L2-tiled k_chol_cluster for every N), chol_d2=1
  *     (split-ownership DSMEM Cholesky k_chol_d2 for 160 < N ≤ 512; needs chol_dsm=1),

@@ -22,6 +22,7 @@
 #include "k_newton.cuh"
 #include "k_chol_dsm.cuh"
 #include "k_chol_d2.cuh"
+#include "k_small.cuh"
 #include "ssnal_en.h"
 
 using namespace ssn;
@@ -359,6 +360,7 @@ struct ssnal_en_problem {
   int k1_count = 0;
   // graph mode (device-resident control, k_ctl.cuh)
   int use_graph = 1;
+  int use_small = 1;  // option small: one-CTA solve (k_small_solve) for m ≤ 64, n ≤ 1024
   ssn::DevCtl* ctl = nullptr;       // device control block
   ssn::DevCtl* ctl_host = nullptr;  // pinned staging (inputs in, results back)
   EvalOut* ev_out_host = nullptr;   // pinned: final EvalOut of the current point
@@ -531,6 +533,8 @@ int configure(ssnal_en_problem* P) {
     if (cudaOccupancyMaxActiveClusters(&nclus, k_chol_d2, &cfg) == cudaSuccess && nclus >= 1) P->d2_ok = 1;
     cudaGetLastError();
   }
+  if (P->m <= kSmallMaxM && P->n <= kSmallMaxN)
+    CK(cudaFuncSetAttribute(k_small_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmallSmem));
   return SSNAL_OK;
 }
 
@@ -1641,6 +1645,63 @@ void drop_graph(ssnal_en_problem* P) {
 
 // Graph mode: the whole Algorithm 1 loop nest is one graph launch; stats are read back with the
 // objective after the caller's synchronisation (finish_stats).
+// Small problems (k_small.cuh): the whole loop nest in one CTA.  Same statistics path as graph mode
+// (device control block + final EvalOut, finish_stats).
+bool small_eligible(const ssnal_en_problem* P) {
+  return P->use_small && !sharded(P) && !P->fmt && P->m <= kSmallMaxM && P->n <= kSmallMaxN &&
+         !(P->cg_ratio > 0.0) && !((double)P->m > P->cg_threshold);  // time_k1: no K1 launches to time
+}
+
+int solve_small_core(ssnal_en_problem* P, double l1, double l2, double sigma0, double tol, int have_x0,
+                     ssnal_en_stats* S) {
+  memset(S, 0, sizeof(*S));
+  int rc;
+  int64_t rx = 0;
+  if ((rc = init_point(P, have_x0, S, &rx))) return rc;
+  DevCtl* h = P->ctl_host;
+  memset(h, 0, sizeof(DevCtl));
+  h->l1 = l1;
+  h->l2 = l2;
+  h->tol = tol;
+  h->sigma = sigma0;
+  h->sigma_factor = P->sigma_factor;
+  h->sigma_max = P->sigma_max;
+  h->mu = P->mu;
+  h->beta = P->beta;
+  h->max_outer = P->max_outer;
+  h->max_inner = P->max_inner;
+  h->max_bt = P->max_bt;
+  h->nb = P->nb;
+  h->jitter = P->jitter;
+  h->inject = P->inject_fail;
+  h->inner_tol_mode = P->inner_tol_mode;
+  CK(cudaMemcpyAsync(P->ctl, h, sizeof(DevCtl), cudaMemcpyHostToDevice, P->st));
+  SmallParams sp;
+  sp.A = P->A;
+  sp.b = P->b;
+  sp.m = (int)P->m;
+  sp.n = (int)P->n;
+  sp.x = P->x;
+  sp.y0 = P->y[0];
+  sp.w0 = P->w[0];
+  sp.Jx = P->Jx;
+  sp.Px = P->Px;
+  sp.rx = P->r_dev + 2;
+  sp.C = P->ctl;
+  sp.ev = P->ev_dev;
+  k_small_solve<<<1, kSmallThreads, kSmallSmem, P->st>>>(sp);
+  P->launches++;
+  CKL();
+  if ((rc = launch_objective(P))) return rc;
+  CK(cudaMemcpyAsync(h, P->ctl, sizeof(DevCtl), cudaMemcpyDeviceToHost, P->st));
+  CK(cudaMemcpyAsync(P->ev_out_host, P->ev_dev, sizeof(EvalOut), cudaMemcpyDeviceToHost, P->st));
+  P->stat_l1 = l1;
+  P->stat_l2 = l2;
+  P->stat_warm_pass = (have_x0 && P->init_mode == 1);
+  P->graph_pending = true;
+  return SSNAL_OK;
+}
+
 int solve_graph_core(ssnal_en_problem* P, double l1, double l2, double sigma0, double tol, int have_x0,
                      ssnal_en_stats* S) {
   memset(S, 0, sizeof(*S));
@@ -2008,6 +2069,8 @@ int ssnal_en_set_option(ssnal_en_problem* P, const char* key, double v) {
     P->cg_maxit = (int)v;
     drop_graph(P);
   }
+  else if (k == "small" && (v == 0 || v == 1))
+    P->use_small = (int)v;
   else if (k == "chol_d2" && (v == 0 || v == 1)) {
     P->use_d2 = (int)v;
     drop_graph(P);  // the K4 variant is baked into the graph
@@ -2037,6 +2100,7 @@ double ssnal_en_get_info(const ssnal_en_problem* P, const char* key) {
   if (k == "k1_smem") return (double)P->k1_smem;
   if (k == "cluster_size") return P->cluster;
   if (k == "chol_dsm") return P->chol_dsm;
+  if (k == "small") return small_eligible(P) ? 1 : 0;
   if (k == "chol_d2") return P->chol_dsm && P->use_d2 && P->d2_ok;
   if (k == "num_sms") return P->nsm;
   if (k == "graph") return P->use_graph;
@@ -2074,8 +2138,9 @@ static int solve_wrapped(ssnal_en_problem* P, double l1, double l2, double sigma
     have_x0 = P->comm_host[1] > 0;
   }
   ssnal_en_stats S;
-  rc = (P->use_graph && !sharded(P)) ? solve_graph_core(P, l1, l2, sigma0, tol, have_x0, &S)
-                                     : solve_core(P, l1, l2, sigma0, tol, have_x0, &S);
+  rc = small_eligible(P)                ? solve_small_core(P, l1, l2, sigma0, tol, have_x0, &S)
+       : (P->use_graph && !sharded(P)) ? solve_graph_core(P, l1, l2, sigma0, tol, have_x0, &S)
+                                       : solve_core(P, l1, l2, sigma0, tol, have_x0, &S);
   if (rc == SSNAL_ECUDA || rc == SSNAL_EINVAL) return rc;
   if (x_out) {
     CK(cudaMemcpyAsync(x_out, P->x, P->n * 8, xout_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, P->st));
@@ -2110,6 +2175,17 @@ static int solve_wrapped(ssnal_en_problem* P, double l1, double l2, double sigma
   if (stats) *stats = S;
   return S.status;
 }
+
+#ifdef SMALL_PROF
+int ssnal_en_small_prof(unsigned long long* out, int reset) {
+  cudaMemcpyFromSymbol(out, ssn::g_small_prof, 8 * sizeof(unsigned long long));
+  if (reset) {
+    unsigned long long z[8] = {0};
+    cudaMemcpyToSymbol(ssn::g_small_prof, z, sizeof(z));
+  }
+  return 0;
+}
+#endif
 
 int ssnal_en_solve(ssnal_en_problem* P, double l1, double l2, double sigma0, double tol, const double* x0,
                    double* x_out, ssnal_en_stats* stats) {

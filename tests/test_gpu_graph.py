@@ -21,6 +21,7 @@ _seen = {"backtracks": 0, "branch": [0, 0, 0], "stalled": 0, "not_converged": 0}
 
 
 def both(P, l1, l2, sigma0=5e-3, tol=1e-6, x0=None):
+    P.set_option("small", 0)  # the one-CTA path (k_small_solve) would serve both modes at cfg1 size
     P.set_option("graph", 0)
     xh, sh = P.solve(l1, l2, sigma0, tol, x0=x0)
     P.set_option("graph", 1)
@@ -113,6 +114,7 @@ def test_graph_matches_oracle_cfg1():
     b, _ = synth.response(cfg)
     lm = float(np.max(np.abs(oracle.aty(A, b))))
     with Problem(A, b) as P:
+        P.set_option("small", 0)
         for c in cfg.cs:
             l1, l2 = lambdas(cfg, lm, c)
             xc, _, stc, _ = oracle.solve(A, b, l1, l2, sigma0=5e-3, tol=1e-6)
@@ -128,6 +130,7 @@ def test_graph_rebuild_after_cluster_change():
     A = synth.design(cfg)
     b, _ = synth.response(cfg)
     with Problem(A, b) as P:
+        P.set_option("small", 0)
         lm = P.lambda_max_l1
         x1, s1 = P.solve(0.1 * lm, 0.05 * lm)
         P.set_option("cluster_size", 8)

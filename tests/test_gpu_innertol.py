@@ -26,9 +26,17 @@ def test_inner_tol_mode_matches_oracle(name, n):
             l1, l2 = c * cfg.alpha * lm, c * (1 - cfg.alpha) * lm
             xc, _, sc, _ = oracle.solve(A, b, l1, l2, sigma0=cfg.sigma0, tol=cfg.tol, inner_tol_mode=1)
             out = {}
+            P.set_option("small", 0)  # graph ≡ host on the multi-kernel paths
             for g in (0, 1):
                 P.set_option("graph", g)
                 out[g] = P.solve(l1, l2, cfg.sigma0, cfg.tol)
+            P.set_option("small", 1)
+            if P.info("small"):  # the one-CTA path (cfg1) with the same schedule
+                xs, ss = P.solve(l1, l2, cfg.sigma0, cfg.tol)
+                assert ss["status"] == 0 and ss["outer_iters"] == sc["outer_iters"]
+                assert abs(ss["newton_iters"] - sc["newton_iters"]) <= 1
+                assert solution_parity(xs, xc, oracle.primal_obj(A, b, xs, l1, l2),
+                                       oracle.primal_obj(A, b, xc, l1, l2))["ok"], (c, ss, sc)
             (xh, sh), (xg, sg) = out[0], out[1]
             assert np.array_equal(xh, xg)
             for k in ("outer_iters", "newton_iters", "backtracks", "branch_steps", "res_kkt1", "res_kkt3"):

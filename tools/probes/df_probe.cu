@@ -238,6 +238,42 @@ __global__ void k_lazy(const double* Sg, double* M, unsigned long long* cyc) {
   if (threadIdx.x == 0) cyc[0] = c1 - c0;
   for (int e = threadIdx.x; e < CHT * CHT; e += 128) M[e] = S[(e % 32) * TLD + e / 32];
 }
+
+// chain probe: one warp does 32 pivots as 4 blocks of 8 (no rank-8 updates, no barriers, no W)
+template <int MODE>
+__global__ void k_chain(const double* Sg, double* M, unsigned long long* cyc) {
+  const int lane = threadIdx.x;
+  double a[8], dgw[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) { a[q] = Sg[lane * TLD + q]; dgw[q] = Sg[q * TLD + q]; }
+  long long c0 = clock64();
+#pragma unroll 1
+  for (int blk = 0; blk < 4; ++blk) {
+#pragma unroll
+    for (int p = 0; p < 8; ++p) {
+      const int j = 8 * blk + p;
+      double d = dgw[p];
+      d = d > 0.0 ? d : 1.0;
+      double inv;
+      if (MODE == 0) inv = rsq_n<2>(d);
+      else if (MODE == 1) inv = rsq_n<0>(d);
+      else inv = 1.0 / sqrt(d);
+      const double lij = (lane > j) ? a[p] * inv : (lane == j ? d * inv : 0.0);
+#pragma unroll
+      for (int q = p + 1; q < 8; ++q) {
+        const double lq = __shfl_sync(0xffffffffu, lij, 8 * blk + q);
+        dgw[q] = fma(-lq, lq, dgw[q]);
+        a[q] = fma(-lij, lq, a[q]);
+      }
+      a[p] = lij;
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) { dgw[q] = dgw[q] * 0.5 + 4.0; }
+  }
+  long long c1 = clock64();
+  if (lane == 0) cyc[0] = c1 - c0;
+  for (int q = 0; q < 8; ++q) M[lane * 8 + q] = a[q];
+}
 template <bool WANTW, int NEWTON>
 __global__ void k_var(const double* Sg, double* M, double* W, int* info, unsigned long long* cyc) {
   __shared__ double S[CHT * TLD + kDiagScratch];
@@ -277,6 +313,12 @@ int main() {
       e2 = fmax(e2, fabs(s2 - h[i * TLD + j]));
     }
     printf("%-24s %6llu cycles (%.0f per pivot) err %.2e %s\n", v == 0 ? "lazy split, no W, 2N" : "lazy split, no W, 1N", c2, c2 / 32.0, e2, cudaGetErrorString(cudaGetLastError()));
+  }
+  for (int md = 0; md < 3; ++md) {
+    for (int rep = 0; rep < 5; ++rep) { if (md == 0) k_chain<0><<<1, 32>>>(dS, dM, cyc); else if (md == 1) k_chain<1><<<1, 32>>>(dS, dM, cyc); else k_chain<2><<<1, 32>>>(dS, dM, cyc); }
+    cudaDeviceSynchronize();
+    unsigned long long c3; cudaMemcpy(&c3, cyc, 8, cudaMemcpyDeviceToHost);
+    printf("chain only (%s): %llu cycles (%.0f per pivot)\n", md == 0 ? "rsqrt+2N" : (md == 1 ? "MUFU only" : "1/sqrt"), c3, c3 / 32.0);
   }
   for (int rep = 0; rep < 5; ++rep) k_warp<2><<<1, 32>>>(dS, dM, cyc);
   cudaDeviceSynchronize();
