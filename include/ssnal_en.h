@@ -130,7 +130,9 @@ double ssnal_en_lambda_max_l1(const ssnal_en_problem* p);
 int ssnal_en_set_option(ssnal_en_problem* p, const char* key, double value);
 
 /* Read-only introspection: "m", "n", "k1_cols", "k1_stages", "k1_grid", "k1_smem",
- * "cluster_size", "num_sms".  Returns NaN for unknown keys. */
+ * "cluster_size", "num_sms", "graph", "format", "cg_ratio", "cg_threshold", and which kernels a
+ * solve on this handle uses: "small" (1: the one-CTA path k_small_solve), "chol_dsm" (1: k_chol_dsm
+ * for N ≤ 160), "chol_d2" (1: k_chol_d2 for 160 < N ≤ 512).  Returns NaN for unknown keys. */
 double ssnal_en_get_info(const ssnal_en_problem* p, const char* key);
 
 /* Solve Algorithm 1 for (λ1, λ2) in the paper's unnormalised units.
