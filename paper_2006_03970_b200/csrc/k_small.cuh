@@ -445,60 +445,77 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_small_solve(const SmallPar
       }
       __syncthreads();
       SPROF_ADD(3);
-      // ---- Cholesky with the rhs as row N (forward substitution for free), one barrier per pivot:
-      // every thread recomputes 1/L_jj from the shared pivot; L[i][j] (i > j, incl. the rhs row N)
-      // goes to the unused upper triangle Mx[j + i·ld], the Schur complement stays in the lower one.
-      // Thread t: row i = j + 1 + (t mod 64), columns c ≡ j + 1 + t/64 (mod 8), c ≤ i.
+      // ---- Cholesky with the rhs as row N (forward substitution for free), TWO pivots per barrier:
+      // every thread recomputes the 2 × 2 diagonal block's factor (L_jj, L_{j+1,j}, L_{j+1,j+1}) from
+      // the shared values and applies the rank-2 update to its entries; L[i][j] (i > j, incl. the rhs
+      // row N) goes to the unused upper triangle Mx[j + i·ld], the Schur complement stays in the
+      // lower one.  Thread t: row i = j + 2 + (t mod 64), columns c ≡ j + 2 + t/64 (mod 8), c ≤ i.
       {
-        constexpr int kFW = kSmallThreads / 64;  // column groups: thread (row, group) updates ≤ 64/kFW entries
+        constexpr int kFW = kSmallThreads / 64;
         const int ti = tid & 63, tc = tid >> 6;
-        if (tid == 0) {  // pivot 0
-          const double d0 = Mx[0];
-          const bool ok = d0 > 0.0;
-          const double dd = ok ? d0 : 1.0;
-          const double inv = rsqrt_pos(dd);
-          Ld[0] = __dmul_rn(dd, inv);
-          Ld[kSmallMaxM] = inv;
-          if (!ok) sc_[16] = 1.0;
-        }
-        __syncthreads();
-        for (int j = 0; j < N; ++j) {
-          const double inv = Ld[kSmallMaxM + j];
-          const double inv2 = __dmul_rn(inv, inv);
-          const int i = j + 1 + ti;
-          if (i <= N && tc < kFW) {
-            const double mij = Mx[i + j * kSmallLd];
-            if (tc == 0) Mx[j + i * kSmallLd] = __dmul_rn(mij, inv);  // L[i][j]
-            const double t = __dmul_rn(mij, inv2);
-            // all loads first (the stores below would otherwise order every load after the previous store)
+        int badl = 0;
+        for (int j = 0; j < N; j += 2) {
+          const bool two = j + 1 < N;
+          const double a = Mx[j + j * kSmallLd];
+          const bool ok0 = a > 0.0;
+          const double d0 = ok0 ? a : 1.0;
+          const double inv0 = rsqrt_pos(d0);
+          double l10 = 0.0, d1 = 1.0, inv1 = 1.0;
+          bool ok1 = true;
+          if (two) {
+            l10 = __dmul_rn(Mx[j + 1 + j * kSmallLd], inv0);
+            const double c1 = __fma_rn(-l10, l10, Mx[j + 1 + (j + 1) * kSmallLd]);
+            ok1 = c1 > 0.0;
+            d1 = ok1 ? c1 : 1.0;
+            inv1 = rsqrt_pos(d1);
+          }
+          badl |= !ok0 || !ok1;
+          const int jn = two ? j + 2 : j + 1;  // first row / column after the block
+          if (!two && tid <= N - jn) {  // single last pivot: column j of the rows below (incl. rhs)
+            const int i = jn + tid;
+            Mx[j + i * kSmallLd] = __dmul_rn(Mx[i + j * kSmallLd], inv0);
+          }
+          const int i = jn + ti;
+          if (two && i <= N) {
+            const double li0 = __dmul_rn(Mx[i + j * kSmallLd], inv0);
+            const double li1 = __dmul_rn(__fma_rn(-li0, l10, Mx[i + (j + 1) * kSmallLd]), inv1);
+            if (tc == 0) {
+              Mx[j + i * kSmallLd] = li0;
+              Mx[j + 1 + i * kSmallLd] = li1;
+            }
             constexpr int kQ = 64 / kFW;
-            double lc[kQ], mc[kQ];
+            double m0[kQ], m1[kQ], mc[kQ];
 #pragma unroll
-            for (int q = 0; q < kQ; ++q) {  // columns c = j + 1 + tc + kFW·q ≤ min(i, N − 1)
-              const int c = j + 1 + tc + kFW * q;
+            for (int q = 0; q < kQ; ++q) {  // loads first, then the rank-2 updates
+              const int c = jn + tc + kFW * q;
               const bool ok = c <= i && c < N;
-              lc[q] = ok ? Mx[c + j * kSmallLd] : 0.0;
+              m0[q] = ok ? Mx[c + j * kSmallLd] : 0.0;
+              m1[q] = ok ? Mx[c + (j + 1) * kSmallLd] : 0.0;
               mc[q] = ok ? Mx[i + c * kSmallLd] : 0.0;
             }
 #pragma unroll
             for (int q = 0; q < kQ; ++q) {
-              const int c = j + 1 + tc + kFW * q;
+              const int c = jn + tc + kFW * q;
               if (c <= i && c < N) {
-                const double v = __fma_rn(-t, lc[q], mc[q]);
-                Mx[i + c * kSmallLd] = v;
-                if (c == j + 1 && i == j + 1) {  // the next pivot is final: its reciprocal square root now
-                  const bool okp = v > 0.0;
-                  const double dd = okp ? v : 1.0;
-                  const double iv = rsqrt_pos(dd);
-                  Ld[j + 1] = __dmul_rn(dd, iv);
-                  Ld[kSmallMaxM + j + 1] = iv;
-                  if (!okp) sc_[16] = 1.0;
-                }
+                const double lc0 = __dmul_rn(m0[q], inv0);
+                const double lc1 = __dmul_rn(__fma_rn(-lc0, l10, m1[q]), inv1);
+                Mx[i + c * kSmallLd] = __fma_rn(-li1, lc1, __fma_rn(-li0, lc0, mc[q]));
               }
+            }
+          }
+          if (tid == 0) {
+            Ld[j] = __dmul_rn(d0, inv0);
+            Ld[kSmallMaxM + j] = inv0;
+            if (two) {
+              Mx[j + (j + 1) * kSmallLd] = l10;
+              Ld[j + 1] = __dmul_rn(d1, inv1);
+              Ld[kSmallMaxM + j + 1] = inv1;
             }
           }
           __syncthreads();
         }
+        if (tid == 0 && badl) sc_[16] = 1.0;
+        __syncthreads();
       }
       SPROF_ADD(4);
       const int bad = sc_[16] != 0.0;
