@@ -1244,13 +1244,16 @@ int init_point(ssnal_en_problem* P, int have_x0, ssnal_en_stats* S, int64_t* rx)
   }
   // Initial y, w (P:242 silent; reading R8): y0 = A x0 − b if x0 ≠ 0, else 0 (decided on the device)
   if (have_x0 && P->init_mode == 1) {
-    if ((rc = launch_gather_dev(P, P->Jx, P->Px, P->r_dev + 2))) return rc;
+    // unsharded: the row-block cluster gather leaves the finished A_S x0_S in part_vec row 0
+    if ((rc = sharded(P) ? launch_gather_dev(P, P->Jx, P->Px, P->r_dev + 2)
+                         : launch_gather_vec(P, P->Jx, P->Px, P->r_dev + 2)))
+      return rc;
     if (sharded(P)) {  // y0 = Σ_ranks A_S x0_S − b; warm iff the global support is non-empty
       if ((rc = exchange_eval(P, P->part_vec, P->gax_valid, kGatherDevGrid, nullptr, 0, P->r_dev + 2))) return rc;
       k_init_y<<<1, 1024, 0, P->st>>>(m, P->b, P->xbuf, nullptr, 1, P->rg_dev, P->y[0]);
       CK(cudaMemcpyAsync(P->r_dev + 4, P->rg_dev, 8, cudaMemcpyDeviceToDevice, P->st));
     } else {
-      k_init_y<<<1, 1024, 0, P->st>>>(m, P->b, P->part_vec, P->gax_valid, kGatherDevGrid, P->r_dev + 2, P->y[0]);
+      k_init_y<<<1, 1024, 0, P->st>>>(m, P->b, P->part_vec, nullptr, 1, P->r_dev + 2, P->y[0]);
     }
     P->launches++;
     CKL();
@@ -1267,7 +1270,9 @@ int init_point(ssnal_en_problem* P, int have_x0, ssnal_en_stats* S, int64_t* rx)
 // → scratch_host[16..19] = [½‖resid‖², Σ|x|, Σx², nnz], scratch_host[20] = |supp x0| (after a sync).
 int launch_objective(ssnal_en_problem* P) {
   int rc;
-  if ((rc = launch_gather_dev(P, P->Jx, P->Px, P->r_dev + 2))) return rc;
+  if ((rc = sharded(P) ? launch_gather_dev(P, P->Jx, P->Px, P->r_dev + 2)
+                       : launch_gather_vec(P, P->Jx, P->Px, P->r_dev + 2)))
+    return rc;
   if (sharded(P)) {  // resid = Σ_ranks A_S x_S − b; Σ|x|, Σx², nnz summed over the ranks
     if ((rc = exchange_eval(P, P->part_vec, P->gax_valid, kGatherDevGrid, nullptr, 0, P->r_dev + 2))) return rc;
     k_combine<<<1, 1024, 0, P->st>>>(P->m, P->b, -1.0, P->xbuf, 1, P->tmpm, nullptr, nullptr, nullptr);
@@ -1278,8 +1283,7 @@ int launch_objective(ssnal_en_problem* P) {
     if ((rc = comm_allreduce(P, P->xbuf, 3, 0))) return rc;
     CK(cudaMemcpyAsync(P->scratch + 17, P->xbuf, 3 * 8, cudaMemcpyDeviceToDevice, P->st));
   } else {
-    k_combine<<<1, 1024, 0, P->st>>>(P->m, P->b, -1.0, P->part_vec, kGatherDevGrid, P->tmpm, nullptr, nullptr,
-                                     P->gax_valid);
+    k_combine<<<1, 1024, 0, P->st>>>(P->m, P->b, -1.0, P->part_vec, 1, P->tmpm, nullptr, nullptr, nullptr);
     P->launches++;
     CKL();
     k_objective<<<1, 1024, 0, P->st>>>(P->m, P->tmpm, P->Px, P->r_dev + 2, P->scratch + 16);
