@@ -415,81 +415,93 @@ SSN_DEV void tile_mma(const double* SA, const double* SB, double (&acc)[4][4][2]
 // writes its partial tile (lower part) to W[s] and k_gram_reduce sums the slices in order.
 // Graph mode: r, tiles, ns from the device geometry (predicated on the branch).
 constexpr int kGramSmem = GT * 36;  // doubles per operand buffer (≥ 32 · 68 of the m × m layout)
+// One (tile, K-slice) item: the 64 × 64 output tile (ti, tj) summed over reduction chunks
+// [c_lo, c_hi) into this thread's fragment acc (rows 16wr + 8i + g, cols 32wc + 8j + 2t + e).
+template <bool SMW, class Acc>
+SSN_DEV void gram_item(const Acc& A, int64_t m, const int32_t* __restrict__ J, int64_t r,
+                       const double* __restrict__ gext, int ti, int tj, int64_t c_lo, int64_t c_hi, double* sA,
+                       double* sB, double (&acc)[2][4][2]) {
+  constexpr int LD = SMW ? 36 : 68;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int wr = warp >> 1, wc = warp & 1;  // this warp's block: rows 16 wr …, cols 32 wc …
+  auto at = [&](int w, int k) { return SMW ? w * LD + k : k * LD + w; };
+  const bool dg = ti == tj;
+  const int64_t o0 = (int64_t)ti * GT, o1 = (int64_t)tj * GT;
+  double va[8], vb[8];
+  // SMW: value q is (ω = warp + 8q, κ = lane); m × m: (ω = lane + 32(q & 1), κ = warp + 8(q >> 1))
+  auto load = [&](int64_t ch) {
+    if (SMW) {
+      const int64_t k = ch * 32 + lane;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int64_t a = o0 + warp + 8 * q, b = o1 + warp + 8 * q;
+        va[q] = k >= m ? 0.0 : (a < r ? A.col(J[a]).ld(k) : ((a == r && gext) ? __ldg(gext + k) : 0.0));
+        vb[q] = (dg || k >= m) ? 0.0 : (b < r ? A.col(J[b]).ld(k) : ((b == r && gext) ? __ldg(gext + k) : 0.0));
+      }
+    } else {
+#pragma unroll
+      for (int q2 = 0; q2 < 4; ++q2) {
+        const int64_t a = ch * 32 + warp + 8 * q2;
+        const bool ok = a < r;
+        const auto col = A.col(ok ? (int64_t)J[a] : 0);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int64_t ra = o0 + lane + 32 * h, rb = o1 + lane + 32 * h;
+          va[2 * q2 + h] = (ok && ra < m) ? col.ld(ra) : 0.0;
+          vb[2 * q2 + h] = (ok && !dg && rb < m) ? col.ld(rb) : 0.0;
+        }
+      }
+    }
+  };
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  if (c_lo < c_hi) load(c_lo);
+  for (int64_t ch = c_lo; ch < c_hi; ++ch) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int w = SMW ? warp + 8 * q : lane + 32 * (q & 1);
+      const int k = SMW ? lane : warp + 8 * (q >> 1);
+      sA[at(w, k)] = va[q];
+      if (!dg) sB[at(w, k)] = vb[q];
+    }
+    __syncthreads();
+    if (ch + 1 < c_hi) load(ch + 1);
+    const double* SB = dg ? sA : sB;
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      double af[2], bf[4];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) af[i] = sA[at(16 * wr + 8 * i + g, 4 * kk + t)];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bf[j] = SB[at(32 * wc + 8 * j + g, 4 * kk + t)];
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma(acc[i][j], af[i], bf[j]);
+    }
+    __syncthreads();
+  }
+}
+
 template <bool SMW, class Acc>
 SSN_DEV void gram_body(const Acc& A, int64_t m, const int32_t* __restrict__ J, int64_t r, double* __restrict__ W,
                        const double* __restrict__ gext, int tiles, int ns, double* sA, double* sB) {
-  constexpr int LD = SMW ? 36 : 68;
   const int64_t K = SMW ? m : r;  // reduction length
   const int64_t nch = (K + 31) / 32;
   const int64_t nout = SMW ? r + (gext ? 1 : 0) : m;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
-  const int wr = warp >> 1, wc = warp & 1;  // this warp's block: rows 16 wr …, cols 32 wc …
-  auto at = [&](int w, int k) { return SMW ? w * LD + k : k * LD + w; };
+  const int wr = warp >> 1, wc = warp & 1;
   for (int item = blockIdx.x; item < tiles * ns; item += gridDim.x) {
     int ti, tj;
     tri_tile(item % tiles, &ti, &tj);
     const int s = item / tiles;
-    const bool dg = ti == tj;
     const int64_t o0 = (int64_t)ti * GT, o1 = (int64_t)tj * GT;
-    const int64_t c_lo = nch * s / ns, c_hi = nch * (s + 1) / ns;
-    double va[8], vb[8];
-    // SMW: value q is (ω = warp + 8q, κ = lane); m × m: (ω = lane + 32(q & 1), κ = warp + 8(q >> 1))
-    auto load = [&](int64_t ch) {
-      if (SMW) {
-        const int64_t k = ch * 32 + lane;
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const int64_t a = o0 + warp + 8 * q, b = o1 + warp + 8 * q;
-          va[q] = k >= m ? 0.0 : (a < r ? A.col(J[a]).ld(k) : ((a == r && gext) ? __ldg(gext + k) : 0.0));
-          vb[q] = (dg || k >= m) ? 0.0 : (b < r ? A.col(J[b]).ld(k) : ((b == r && gext) ? __ldg(gext + k) : 0.0));
-        }
-      } else {
-#pragma unroll
-        for (int q2 = 0; q2 < 4; ++q2) {
-          const int64_t a = ch * 32 + warp + 8 * q2;
-          const bool ok = a < r;
-          const auto col = A.col(ok ? (int64_t)J[a] : 0);
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int64_t ra = o0 + lane + 32 * h, rb = o1 + lane + 32 * h;
-            va[2 * q2 + h] = (ok && ra < m) ? col.ld(ra) : 0.0;
-            vb[2 * q2 + h] = (ok && !dg && rb < m) ? col.ld(rb) : 0.0;
-          }
-        }
-      }
-    };
     double acc[2][4][2];
-#pragma unroll
-    for (int i = 0; i < 2; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-    if (c_lo < c_hi) load(c_lo);
-    for (int64_t ch = c_lo; ch < c_hi; ++ch) {
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int w = SMW ? warp + 8 * q : lane + 32 * (q & 1);
-        const int k = SMW ? lane : warp + 8 * (q >> 1);
-        sA[at(w, k)] = va[q];
-        if (!dg) sB[at(w, k)] = vb[q];
-      }
-      __syncthreads();
-      if (ch + 1 < c_hi) load(ch + 1);
-      const double* SB = dg ? sA : sB;
-#pragma unroll
-      for (int kk = 0; kk < 8; ++kk) {
-        double af[2], bf[4];
-#pragma unroll
-        for (int i = 0; i < 2; ++i) af[i] = sA[at(16 * wr + 8 * i + g, 4 * kk + t)];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) bf[j] = SB[at(32 * wc + 8 * j + g, 4 * kk + t)];
-#pragma unroll
-        for (int i = 0; i < 2; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) dmma(acc[i][j], af[i], bf[j]);
-      }
-      __syncthreads();
-    }
+    gram_item<SMW>(A, m, J, r, gext, ti, tj, nch * s / ns, nch * (s + 1) / ns, sA, sB, acc);
     double* Ws = W + (size_t)s * nout * nout;
 #pragma unroll
     for (int i = 0; i < 2; ++i)
@@ -502,6 +514,84 @@ SSN_DEV void gram_body(const Acc& A, int64_t m, const int32_t* __restrict__ J, i
         }
   }
 }
+
+// K3 fused with its split-K reduction (the hot-path Newton systems, Eq. (18)/(19)): one 8-CTA
+// cluster per 64 × 64 output tile, CTA rank s sums K-slice s; the 8 partial tiles meet in
+// distributed shared memory and rank s reduces rows 8s … 8s + 7 in rank order (deterministic),
+// applying the k_gram_reduce epilogue (× mult, + diag, jitter, right-hand-side row) straight into
+// M.  No slice buffer in global memory and no second launch.  Clusters take tiles in a stride
+// loop; graph mode reads the branch and sizes from the device geometry.
+constexpr int kGramCS = 8;
+struct GramFusedArgs {
+  int branch;  // 1: SMW (Eq. (19), gext = g as the extra column r), 2: m × m (Eq. (18), g as rhs row)
+  int64_t r, nout, nmat;
+  int tiles, ld;
+  double diag, mult, jit;
+};
+template <class Acc>
+__global__ void __cluster_dims__(kGramCS, 1, 1) __launch_bounds__(256)
+    k_gram_fused(const Acc A, int64_t m, const int32_t* __restrict__ J, double* __restrict__ M,
+                 const double* __restrict__ g, GramFusedArgs ga, const DirGeo* geo) {
+  __shared__ __align__(16) double sm[2 * kGramSmem];  // operand buffers, then the partial tile (64 × 65)
+  if (geo) {
+    if (geo->branch != 1 && geo->branch != 2) return;
+    ga.branch = geo->branch;
+    ga.r = geo->r;
+    ga.nout = geo->nout;
+    ga.nmat = geo->nmat;
+    ga.tiles = geo->tiles;
+    ga.ld = geo->ld;
+    ga.diag = geo->diag;
+    ga.mult = geo->mult;
+    ga.jit = geo->jit;
+  }
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int s = (int)cluster.block_rank(), cl = (int)(blockIdx.x / kGramCS), ncl = (int)(gridDim.x / kGramCS);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gq = lane >> 2, t = lane & 3, wr = warp >> 1, wc = warp & 1;
+  const bool smw = ga.branch == 1;
+  const int64_t K = smw ? m : ga.r;
+  const int64_t nch = (K + 31) / 32;
+  double* sA = sm;
+  double* sB = sm + kGramSmem;
+  double* Pt = sm;  // partial tile [64][65]
+  if (!smw && g && cl == 0)  // the rhs row of Eq. (18): M[nmat + e·ld] = g[e]
+    for (int64_t e = s * 256 + tid; e < ga.nmat; e += kGramCS * 256) M[ga.nmat + e * ga.ld] = g[e];
+  for (int tq = cl; tq < ga.tiles; tq += ncl) {
+    int ti, tj;
+    tri_tile(tq, &ti, &tj);
+    double acc[2][4][2];
+    if (smw) gram_item<true>(A, m, J, ga.r, g, ti, tj, nch * s / kGramCS, nch * (s + 1) / kGramCS, sA, sB, acc);
+    else gram_item<false>(A, m, J, ga.r, nullptr, ti, tj, nch * s / kGramCS, nch * (s + 1) / kGramCS, sA, sB, acc);
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) Pt[(16 * wr + 8 * i + gq) * 65 + 32 * wc + 8 * j + 2 * t + e] = acc[i][j][e];
+    cluster.sync();
+    const int64_t o0 = (int64_t)ti * GT, o1 = (int64_t)tj * GT;
+    for (int e = tid; e < 8 * GT; e += 256) {
+      const int w = 8 * s + e / GT, k = e % GT;
+      const int64_t oi = o0 + w, oj = o1 + k;
+      if (oi < ga.nout && oj < ga.nout && oi >= oj) {
+        double v = 0.0;
+#pragma unroll
+        for (int q = 0; q < kGramCS; ++q) v += cluster.map_shared_rank(Pt, q)[w * 65 + k];
+        if (oi < ga.nmat) {
+          double x = (ga.mult == 1.0 ? v : ga.mult * v) + (oi == oj ? ga.diag : 0.0);
+          if (oi == oj && ga.jit != 0.0) x = __fma_rn(x, ga.jit, x);
+          M[oi + oj * ga.ld] = x;
+        } else {
+          M[oi + oj * ga.ld] = v;  // rhs row (SMW: u = A_Jᵀ g)
+        }
+      }
+    }
+    cluster.sync();  // remote reads done before the next tile reuses the buffers
+  }
+}
+
 template <bool SMW, class Acc>
 __global__ void __launch_bounds__(256) k_gram(const Acc A, int64_t m, const int32_t* __restrict__ J, int64_t r,
                                               double* __restrict__ W, const double* __restrict__ gext, int tiles,

@@ -1017,6 +1017,14 @@ int launch_cg(ssnal_en_problem* P, const int32_t* J, int64_t r, const double* g,
 
 // Gram / reduce grids: persistent CTAs (results do not depend on the grid; DirGeo fixes the work)
 int gram_grid(ssnal_en_problem* P, int items) { return items < 2 * P->nsm ? (items < 1 ? 1 : items) : 2 * P->nsm; }
+// k_gram_fused: one 8-CTA cluster per tile, at most ~2 CTAs per SM (clusters stride over tiles)
+unsigned gram_fused_grid(ssnal_en_problem* P, int tiles) {
+  int ncl = (2 * P->nsm) / kGramCS;
+  if (tiles < ncl) ncl = tiles;
+  if (ncl < 1) ncl = 1;
+  return (unsigned)(ncl * kGramCS);
+}
+
 unsigned reduce_grid(ssnal_en_problem* P, int64_t tot) {
   int64_t g = (tot + 255) / 256;
   if (g > 4 * P->nsm) g = 4 * P->nsm;
@@ -1131,16 +1139,12 @@ int newton_direction(ssnal_en_problem* P, const int32_t* J, int64_t r, const dou
     return SSNAL_OK;
   }
   CK(cudaMemsetAsync(P->info, 0, sizeof(int), P->st));
+  const GramFusedArgs gfa{geo.branch, r, geo.nout, geo.nmat, geo.tiles, geo.ld, geo.diag, geo.mult, geo.jit};
   if (geo.branch == 1) {  // Sherman–Morrison–Woodbury, Eq. (19): factor κ⁻¹I_r + A_JᵀA_J (R13)
     with_acc(P, [&](auto acc) {
-      k_gram<true><<<gram_grid(P, geo.tiles * geo.ns), 256, 0, P->st>>>(acc, m, J, r, P->W, g, geo.tiles, geo.ns,
-                                                                        nullptr);
+      k_gram_fused<<<gram_fused_grid(P, geo.tiles), 256, 0, P->st>>>(acc, m, J, P->Mmat, g, gfa, nullptr);
       return 0;
     });
-    P->launches++;
-    CKL();
-    k_gram_reduce<<<reduce_grid(P, geo.nout * geo.nout), 256, 0, P->st>>>(P->W, geo.ns, geo.nout, geo.nmat, geo.diag,
-                                                                          geo.mult, P->Mmat, geo.ld, nullptr, nullptr, 0, geo.jit);
     P->launches++;
     CKL();
     int rc = launch_chol(P, P->Mmat, geo.N, P->u, 1.0, nullptr, nullptr);  // v = (κ⁻¹I + G)⁻¹ u
@@ -1156,16 +1160,11 @@ int newton_direction(ssnal_en_problem* P, const int32_t* J, int64_t r, const dou
     CKL();
     return SSNAL_OK;
   }
-  // r ≥ m: Eq. (18), M = I_m + κ A_J A_Jᵀ; the reduce also writes g into the rhs row
+  // r ≥ m: Eq. (18), M = I_m + κ A_J A_Jᵀ; the fused reduce also writes g into the rhs row
   with_acc(P, [&](auto acc) {
-    k_gram<false><<<gram_grid(P, geo.tiles * geo.ns), 256, 0, P->st>>>(acc, m, J, r, P->W, nullptr, geo.tiles,
-                                                                       geo.ns, nullptr);
+    k_gram_fused<<<gram_fused_grid(P, geo.tiles), 256, 0, P->st>>>(acc, m, J, P->Mmat, g, gfa, nullptr);
     return 0;
   });
-  P->launches++;
-  CKL();
-  k_gram_reduce<<<reduce_grid(P, m * m), 256, 0, P->st>>>(P->W, geo.ns, m, m, geo.diag, geo.mult, P->Mmat, geo.ld, g,
-                                                          nullptr, 0, geo.jit);
   P->launches++;
   CKL();
   return launch_chol(P, P->Mmat, (int)m, d, -1.0, g, gd_dev, y, yt);  // d = −M⁻¹ g, gd = gᵀd
@@ -1180,12 +1179,11 @@ int newton_direction_graph(ssnal_en_problem* P) {
   const int32_t* J = P->J[0];
   const double* g = P->g[0];
   double* gd = P->scratch;
-  with_acc(P, [&](auto acc) {
-    k_gram_any<<<2 * P->nsm, 256, 0, P->st>>>(acc, m, J, P->W, g, geo);
+  with_acc(P, [&](auto acc) {  // worst-case grid: the m × m tiles (SMW tiles for r < m are fewer)
+    k_gram_fused<<<gram_fused_grid(P, gram_tiles(m)), 256, 0, P->st>>>(acc, m, J, P->Mmat, g, GramFusedArgs{}, geo);
     return 0;
   });
-  k_gram_reduce<<<reduce_grid(P, m * m), 256, 0, P->st>>>(P->W, 0, 0, 0, 0.0, 0.0, P->Mmat, 0, g, geo, -1, 0.0);
-  P->launches += 2;
+  P->launches += 1;
   CKL();
   int rc = launch_chol(P, P->Mmat, 0, nullptr, 0.0, nullptr, nullptr, nullptr, nullptr, geo, -1);
   if (rc) return rc;
