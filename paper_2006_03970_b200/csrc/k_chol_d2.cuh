@@ -115,12 +115,10 @@ SSN_DEV double d2_coldot(const double* M, const double* x, int lane) {
   return (s[0] + s[1]) + (s[2] + s[3]);
 }
 
-__global__ void __launch_bounds__(256, 1) k_chol_d2(const double* __restrict__ M, int N, int ld,
-                                                    double* __restrict__ out, double scale,
-                                                    const double* __restrict__ dotv, double* dot_out, int* info,
-                                                    const double* __restrict__ ybase, double* __restrict__ yt,
-                                                    const DirGeo* geo, int want, int nmin, int nmax,
-                                                    const CholArgs* ca) {
+SSN_DEV void chol_d2_body(const double* __restrict__ M, int N, int ld, double* __restrict__ out, double scale,
+                          const double* __restrict__ dotv, double* dot_out, int* info,
+                          const double* __restrict__ ybase, double* __restrict__ yt, const DirGeo* geo, int want,
+                          int nmin, int nmax, const CholArgs* ca) {
   namespace cg = cooperative_groups;
   if (geo) {  // graph mode: predicated on the branch and on nmin ≤ N ≤ nmax (uniform over the cluster)
     if ((want >= 0 ? geo->branch != want : (geo->branch != 1 && geo->branch != 2)) || geo->N > nmax ||
@@ -485,6 +483,28 @@ __global__ void __launch_bounds__(256, 1) k_chol_d2(const double* __restrict__ M
     *dot_out = sd;
   }
   cluster.sync();  // rank 0's reads complete before any CTA exits
+}
+
+__global__ void __launch_bounds__(256, 1) k_chol_d2(const double* __restrict__ M, int N, int ld,
+                                                    double* __restrict__ out, double scale,
+                                                    const double* __restrict__ dotv, double* dot_out, int* info,
+                                                    const double* __restrict__ ybase, double* __restrict__ yt,
+                                                    const DirGeo* geo, int want, int nmin, int nmax,
+                                                    const CholArgs* ca) {
+  chol_d2_body(M, N, ld, out, scale, dotv, dot_out, info, ybase, yt, geo, want, nmin, nmax, ca);
+}
+
+// Graph mode: one node for both DSMEM-resident kernels, dispatching on the device geometry's N
+// (k_chol_dsm for N ≤ 160, k_chol_d2 for 160 < N ≤ 512); dynamic shared memory kD2Smem.
+__global__ void __launch_bounds__(256, 1) k_chol_dsm_any(const double* __restrict__ M, double* __restrict__ out,
+                                                         double scale, const double* __restrict__ dotv,
+                                                         double* dot_out, int* info, const double* __restrict__ ybase,
+                                                         double* __restrict__ yt, const DirGeo* geo, int want,
+                                                         const CholArgs* ca) {
+  if (geo->N <= kDsmUseMax)
+    chol_dsm_body(M, 0, 0, out, scale, dotv, dot_out, info, ybase, yt, geo, want, kDsmUseMax, ca);
+  else
+    chol_d2_body(M, 0, 0, out, scale, dotv, dot_out, info, ybase, yt, geo, want, kDsmUseMax + 1, kDsmMaxN, ca);
 }
 
 }  // namespace ssn

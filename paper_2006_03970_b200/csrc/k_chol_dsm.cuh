@@ -22,7 +22,8 @@
 
 namespace ssn {
 
-constexpr int kDsmCS = 16;                 // cluster size = max block columns (N ≤ 512)
+constexpr int kDsmCS = 16;
+constexpr int kDsmUseMax = 160;  // k_chol_dsm for N ≤ 160 (faster there than k_chol_d2)                 // cluster size = max block columns (N ≤ 512)
 constexpr int kDsmMaxN = kDsmCS * CHT;     // 512
 constexpr int kDsmTiles = kDsmCS + 1;      // row tiles of column 0 at N = 512 (NR = 513)
 constexpr int kTileD = CHT * TLD;          // doubles per smem tile (32 × 33)
@@ -51,11 +52,10 @@ SSN_DEV void red_release_cluster_add(int* p, int v) {
   asm volatile("red.release.cluster.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-__global__ void __launch_bounds__(256, 1) k_chol_dsm(const double* __restrict__ M, int N, int ld,
-                                                     double* __restrict__ out, double scale,
-                                                     const double* __restrict__ dotv, double* dot_out, int* info,
-                                                     const double* __restrict__ ybase, double* __restrict__ yt,
-                                                     const DirGeo* geo, int want, int nmax, const CholArgs* ca) {
+SSN_DEV void chol_dsm_body(const double* __restrict__ M, int N, int ld, double* __restrict__ out, double scale,
+                           const double* __restrict__ dotv, double* dot_out, int* info,
+                           const double* __restrict__ ybase, double* __restrict__ yt, const DirGeo* geo, int want,
+                           int nmax, const CholArgs* ca) {
   namespace cg = cooperative_groups;
   if (geo) {  // graph mode: predicated on the branch and on N ≤ nmax ≤ 512 (uniform over the cluster)
     if ((want >= 0 ? geo->branch != want : (geo->branch != 1 && geo->branch != 2)) || geo->N > nmax) return;
@@ -304,6 +304,14 @@ __global__ void __launch_bounds__(256, 1) k_chol_dsm(const double* __restrict__ 
   }
   cluster.sync();  // rank 0's reads complete before any CTA exits
   if (tid == 0) DSTAMP(7);
+}
+
+__global__ void __launch_bounds__(256, 1) k_chol_dsm(const double* __restrict__ M, int N, int ld,
+                                                     double* __restrict__ out, double scale,
+                                                     const double* __restrict__ dotv, double* dot_out, int* info,
+                                                     const double* __restrict__ ybase, double* __restrict__ yt,
+                                                     const DirGeo* geo, int want, int nmax, const CholArgs* ca) {
+  chol_dsm_body(M, N, ld, out, scale, dotv, dot_out, info, ybase, yt, geo, want, nmax, ca);
 }
 
 }  // namespace ssn

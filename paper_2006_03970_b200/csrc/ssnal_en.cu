@@ -533,6 +533,10 @@ int configure(ssnal_en_problem* P) {
     if (cudaOccupancyMaxActiveClusters(&nclus, k_chol_d2, &cfg) == cudaSuccess && nclus >= 1) P->d2_ok = 1;
     cudaGetLastError();
   }
+  if (P->d2_ok) {
+    CK(cudaFuncSetAttribute(k_chol_dsm_any, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kD2Smem));
+    CK(cudaFuncSetAttribute(k_chol_dsm_any, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  }
   if (P->m <= kSmallMaxM && P->n <= kSmallMaxN)
     CK(cudaFuncSetAttribute(k_small_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmallSmem));
   return SSNAL_OK;
@@ -891,7 +895,6 @@ int launch_chol_ex(ssnal_en_problem* P, double* M, int N, int NR, int ld, double
 // DSMEM-resident K4 (k_chol_dsm.cuh): same contract as the k_chol_cluster launch below.  Used for
 // N ≤ kDsmUseMax, where it is faster (N = 100: 35 vs 47 µs; crossover near N = 192, and N = 500
 // takes ~300 vs ~211 µs: its per-owner update load is uneven).
-constexpr int kDsmUseMax = 160;
 int launch_chol_dsm(ssnal_en_problem* P, double* M, int N, double* out, double scale, const double* dotv,
                     double* dot_out, const double* ybase, double* yt, const DirGeo* geo, int want) {
   cudaLaunchConfig_t cfg = {};
@@ -942,7 +945,26 @@ int launch_chol(ssnal_en_problem* P, double* M, int N, double* out, double scale
                 double* dot_out, const double* ybase = nullptr, double* yt = nullptr, const DirGeo* geo = nullptr,
                 int want = 0) {
   int nmin = 0;
-  if (P->chol_dsm) {
+  if (geo && P->chol_dsm && P->use_d2 && P->d2_ok && P->m > kDsmUseMax) {  // one node for both DSMEM kernels
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(kDsmCS);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = kD2Smem;
+    cfg.stream = P->st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = kDsmCS;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    const CholArgs* ca = want < 0 ? P->chol_args : nullptr;
+    CK(cudaLaunchKernelEx(&cfg, k_chol_dsm_any, (const double*)M, out, scale, dotv, dot_out, P->info, ybase, yt, geo,
+                          want, ca));
+    P->launches++;
+    if (P->m <= kDsmMaxN) return SSNAL_OK;
+    nmin = kDsmMaxN + 1;
+  } else if (P->chol_dsm) {
     if (geo || N <= kDsmUseMax) {
       int rc = launch_chol_dsm(P, M, N, out, scale, dotv, dot_out, ybase, yt, geo, want);
       if (rc) return rc;
