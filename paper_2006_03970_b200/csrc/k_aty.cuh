@@ -900,6 +900,145 @@ SSN_DEV bool eval_body(int64_t m, const double* __restrict__ y,
   return true;  // the finishing thread (EvalOut written)
 }
 
+// m ≤ 512: ONE 16-CTA cluster, CTA q = row block q.  Its 8 warps split the partial rows (contiguous
+// eighths, ascending b, the same ballot / 8-in-flight loads), the warp sums are added in warp order,
+// the block's (yyᵀ, bᵀy, gᵀg) pieces go to rank 0's shared memory through DSMEM while rank 1 sums
+// the K1 scalar partials; after one cluster barrier rank 0 adds the blocks in order and writes
+// EvalOut.  No global ticket, no second reduction level.  True on rank 0, thread 0.
+constexpr int kEval16 = 16;
+SSN_DEV bool eval_body16(int64_t m, const double* __restrict__ y, const double* __restrict__ bvec,
+                         const double* __restrict__ part_vec, const int* __restrict__ part_valid, int nparts,
+                         const double* __restrict__ part_scal, int nscal, Scal sc, double nb, int with_grad,
+                         double* __restrict__ g_out, const int64_t* r_in, EvalOut* out, const double* gd_src,
+                         const int* info_src, EvalOut* host_out, unsigned long long seq, const Scal* scp,
+                         const int* pred, const double* nbp) {
+  __shared__ double red[8][33];
+  __shared__ double bsum[kEval16 * 3 + 4];  // rank 0: per-block (yy, by, gg), then the 4 scalar sums
+  if (pred && *pred == 0) return false;  // graph mode: predicated off (uniform over the cluster)
+  if (scp) sc = *scp;
+  if (nbp) nb = *nbp;
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int q = (int)cluster.block_rank();
+  const int64_t k = (int64_t)q * 32 + lane;
+  double yk = 0.0, bk = 0.0;
+  if (warp == 0 && k < m) {
+    yk = y[k];
+    bk = bvec[k];
+  }
+  double gp = 0.0;
+  if (with_grad) {
+    const int b0 = (int)((int64_t)nparts * warp / 8), b1 = (int)((int64_t)nparts * (warp + 1) / 8);
+    for (int c0 = b0; c0 < b1; c0 += 32) {
+      const int cn = min(32, b1 - c0);
+      unsigned mask;
+      if (part_valid) mask = __ballot_sync(0xffffffffu, lane < cn && part_valid[c0 + lane] != 0);
+      else mask = cn == 32 ? 0xffffffffu : ((1u << cn) - 1u);
+      while (mask) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int bit = mask ? __ffs(mask) - 1 : -1;
+          mask &= mask - 1u;
+          v[u] = (bit >= 0 && k < m) ? part_vec[(size_t)(c0 + bit) * m + k] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) gp += v[u];
+      }
+    }
+    red[warp][lane] = gp;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    double yy = 0.0, by = 0.0, gg = 0.0;
+    if (k < m) {
+      yy = yk * yk;
+      by = bk * yk;
+      if (with_grad) {
+        double t = red[0][lane];
+        for (int wi = 1; wi < 8; ++wi) t += red[wi][lane];
+        const double g = __dsub_rn(__dadd_rn(yk, bk), t);
+        g_out[k] = g;
+        gg = g * g;
+      }
+    }
+    yy = warp_allsum(yy);
+    by = warp_allsum(by);
+    gg = warp_allsum(gg);
+    if (lane == 0) {
+      double* dst = cluster.map_shared_rank(bsum, 0);
+      dst[q * 3 + 0] = yy;
+      dst[q * 3 + 1] = by;
+      dst[q * 3 + 2] = gg;
+    }
+  } else if (q == 1 && warp == 1) {  // the scalar partials of K1/K1e (lane sums q' ≡ lane mod 32, 8 in flight)
+    double s[4] = {0, 0, 0, 0};
+    for (int q0 = lane; q0 < nscal; q0 += 32 * 8) {
+      double v[8][4];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) v[u][j] = q0 + 32 * u < nscal ? __ldcg(part_scal + (q0 + 32 * u) * 4 + j) : 0.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) s[j] += v[u][j];
+    }
+    for (int j = 0; j < 4; ++j) s[j] = warp_allsum(s[j]);
+    if (lane == 0) {
+      double* dst = cluster.map_shared_rank(bsum, 0);
+      for (int j = 0; j < 4; ++j) dst[kEval16 * 3 + j] = s[j];
+    }
+  }
+  cluster.sync();  // every block's pieces are in rank 0's shared memory
+  if (q != 0 || tid != 0) return false;
+  const int nrb = (int)((m + 31) / 32);
+  double a = 0, bb = 0, c = 0;
+  for (int qq = 0; qq < nrb; ++qq) {
+    a += bsum[qq * 3 + 0];
+    bb += bsum[qq * 3 + 1];
+    c += bsum[qq * 3 + 2];
+  }
+  double s4[4];
+  for (int j = 0; j < 4; ++j) s4[j] = bsum[kEval16 * 3 + j];
+  EvalOut o;
+  o.yy = a;
+  o.by = bb;
+  o.gg = c;
+  for (int j = 0; j < 4; ++j) o.s[j] = s4[j];
+  const double tprox = __dmul_rn(sc.cpsi, s4[0]);
+  o.psi = __dadd_rn(__dadd_rn(__dmul_rn(0.5, a), bb), tprox);
+  o.psimag = fabs(0.5 * a) + fabs(bb) + fabs(tprox);
+  o.res1 = with_grad ? sqrt(c) / (1.0 + nb) : -1.0;
+  o.gd = gd_src ? *gd_src : 0.0;
+  o.r = r_in ? (long long)*r_in : -1;
+  o.info = info_src ? (long long)*info_src : 0;
+  o.seq = seq;
+  o.pad = 0;
+  *out = o;
+  if (host_out) {  // zero-copy to mapped pinned memory; seq last, after a system-scope fence
+    volatile EvalOut* h = host_out;
+    h->psi = o.psi; h->psimag = o.psimag; h->res1 = o.res1; h->yy = o.yy; h->by = o.by; h->gg = o.gg;
+    for (int j = 0; j < 4; ++j) h->s[j] = o.s[j];
+    h->gd = o.gd; h->r = o.r; h->info = o.info;
+    __threadfence_system();
+    h->seq = seq;
+  }
+  return true;
+}
+
+__global__ void __cluster_dims__(kEval16, 1, 1) __launch_bounds__(K5_THREADS)
+    k_eval_reduce16(int64_t m, const double* __restrict__ y, const double* __restrict__ bvec,
+                    const double* __restrict__ part_vec, const int* __restrict__ part_valid, int nparts,
+                    const double* __restrict__ part_scal, int nscal, Scal sc, double nb, int with_grad,
+                    double* __restrict__ g_out, const int64_t* r_in, EvalOut* out, double* blk, unsigned* ticket,
+                    const double* gd_src, const int* info_src, EvalOut* host_out, unsigned long long seq,
+                    const Scal* scp, const int* pred, const double* nbp) {
+  eval_body16(m, y, bvec, part_vec, part_valid, nparts, part_scal, nscal, sc, nb, with_grad, g_out, r_in, out, gd_src,
+              info_src, host_out, seq, scp, pred, nbp);
+}
+
 __global__ void __cluster_dims__(kEvalCS, 1, 1) __launch_bounds__(K5_THREADS) k_eval_reduce(int64_t m, const double* __restrict__ y,
                                                             const double* __restrict__ bvec,
                                                             const double* __restrict__ part_vec,

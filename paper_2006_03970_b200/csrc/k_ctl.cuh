@@ -286,4 +286,26 @@ __global__ void __cluster_dims__(kEvalCS, 1, 1) __launch_bounds__(K5_THREADS)
   if (KIND == kHookInnerEnd) ctl_inner_end(hk.C, hk.ev0, hk.m, hk.nsm, hk.wsplits, hk.info, hk.h);
 }
 
+// m ≤ 512: the same on one 16-CTA cluster (eval_body16)
+template <int KIND>
+__global__ void __cluster_dims__(kEval16, 1, 1) __launch_bounds__(K5_THREADS)
+    k_eval_ctl16(int64_t m, const double* __restrict__ y, const double* __restrict__ bvec,
+                 const double* __restrict__ part_vec, const int* __restrict__ part_valid, int nparts,
+                 const double* __restrict__ part_scal, int nscal, Scal sc, double nb, int with_grad,
+                 double* __restrict__ g_out, const int64_t* r_in, EvalOut* out, double* blk, unsigned* ticket,
+                 const double* gd_src, const int* info_src, EvalOut* host_out, unsigned long long seq,
+                 const Scal* scp, const int* pred, const double* nbp, CtlHook hk) {
+  if (KIND == kHookInnerEnd && pred && *pred == 0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) ctl_inner_end(hk.C, hk.ev0, hk.m, hk.nsm, hk.wsplits, hk.info, hk.h);
+    return;
+  }
+  if (!eval_body16(m, y, bvec, part_vec, part_valid, nparts, part_scal, nscal, sc, nb, with_grad, g_out, r_in, out,
+                   gd_src, info_src, host_out, seq, scp, pred, nbp))
+    return;
+  if (KIND == kHookInnerBegin) ctl_inner_begin(hk.C, hk.ev0, hk.m, hk.nsm, hk.wsplits, hk.info, hk.h);
+  if (KIND == kHookArmijo) ctl_armijo(hk.C, hk.ev0, hk.ev1, hk.h);
+  if (KIND == kHookBacktrack) ctl_bt(hk.C, hk.ev0, hk.ev1, hk.h);
+  if (KIND == kHookInnerEnd) ctl_inner_end(hk.C, hk.ev0, hk.m, hk.nsm, hk.wsplits, hk.info, hk.h);
+}
+
 }  // namespace ssn

@@ -360,7 +360,8 @@ struct ssnal_en_problem {
   int k1_count = 0;
   // graph mode (device-resident control, k_ctl.cuh)
   int use_graph = 1;
-  int use_small = 1;  // option small: one-CTA solve (k_small_solve) for m ≤ 64, n ≤ 1024
+  int use_small = 1;
+  int eval16_ok = 0;  // the 16-CTA-cluster evaluation kernels are schedulable (m ≤ 512)  // option small: one-CTA solve (k_small_solve) for m ≤ 64, n ≤ 1024
   ssn::DevCtl* ctl = nullptr;       // device control block
   ssn::DevCtl* ctl_host = nullptr;  // pinned staging (inputs in, results back)
   EvalOut* ev_out_host = nullptr;   // pinned: final EvalOut of the current point
@@ -536,6 +537,20 @@ int configure(ssnal_en_problem* P) {
   if (P->d2_ok) {
     CK(cudaFuncSetAttribute(k_chol_dsm_any, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kD2Smem));
     CK(cudaFuncSetAttribute(k_chol_dsm_any, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  }
+  P->eval16_ok = 0;
+  if (P->m <= 32 * kEval16) {
+    CK(cudaFuncSetAttribute(k_eval_reduce16, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    CK(cudaFuncSetAttribute(k_eval_ctl16<kHookInnerBegin>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    CK(cudaFuncSetAttribute(k_eval_ctl16<kHookArmijo>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    CK(cudaFuncSetAttribute(k_eval_ctl16<kHookBacktrack>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    CK(cudaFuncSetAttribute(k_eval_ctl16<kHookInnerEnd>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(kEval16);
+    cfg.blockDim = dim3(K5_THREADS);
+    int nclus = 0;
+    if (cudaOccupancyMaxActiveClusters(&nclus, k_eval_reduce16, &cfg) == cudaSuccess && nclus >= 1) P->eval16_ok = 1;
+    cudaGetLastError();
   }
   if (P->m <= kSmallMaxM && P->n <= kSmallMaxN)
     CK(cudaFuncSetAttribute(k_small_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmallSmem));
@@ -790,6 +805,19 @@ int launch_eval(ssnal_en_problem* P, const double* y, const Scal& sc, int with_g
 #define SSN_EVAL_ARGS                                                                                              \
   P->m, y, P->b, vec, valid, nparts, scal, nscal, sc, P->nb, with_grad, g_out, r_dev, P->ev_dev + slot, P->blk,   \
       P->ticket, gd_src, info_src, hout, P->ev_seq, scp, pred, nbp
+  if (nblk <= (unsigned)kEval16 && P->eval16_ok) {  // m ≤ 512: one 16-CTA cluster
+    const dim3 g16(kEval16);
+    switch (hook) {
+      case kHookInnerBegin: k_eval_ctl16<kHookInnerBegin><<<g16, K5_THREADS, 0, P->st>>>(SSN_EVAL_ARGS, *hk); break;
+      case kHookArmijo: k_eval_ctl16<kHookArmijo><<<g16, K5_THREADS, 0, P->st>>>(SSN_EVAL_ARGS, *hk); break;
+      case kHookBacktrack: k_eval_ctl16<kHookBacktrack><<<g16, K5_THREADS, 0, P->st>>>(SSN_EVAL_ARGS, *hk); break;
+      case kHookInnerEnd: k_eval_ctl16<kHookInnerEnd><<<g16, K5_THREADS, 0, P->st>>>(SSN_EVAL_ARGS, *hk); break;
+      default: k_eval_reduce16<<<g16, K5_THREADS, 0, P->st>>>(SSN_EVAL_ARGS);
+    }
+    P->launches++;
+    CKL();
+    return SSNAL_OK;
+  }
   switch (hook) {  // graph mode: the control decision that consumes this evaluation, in the same launch
     case kHookInnerBegin: k_eval_ctl<kHookInnerBegin><<<grid, K5_THREADS, 0, P->st>>>(SSN_EVAL_ARGS, *hk); break;
     case kHookArmijo: k_eval_ctl<kHookArmijo><<<grid, K5_THREADS, 0, P->st>>>(SSN_EVAL_ARGS, *hk); break;
