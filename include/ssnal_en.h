@@ -149,6 +149,17 @@ int ssnal_en_solve(ssnal_en_problem* p, double lambda1, double lambda2, double s
 int ssnal_en_solve_device(ssnal_en_problem* p, double lambda1, double lambda2, double sigma0, double tol,
                           const double* x0_dev, double* x_out_dev, ssnal_en_stats* stats);
 
+/* A warm-started λ path on DEVICE buffers (the path protocol of Table D.4 / BASELINE
+ * configs[1]): point i solves (lambda1[i], lambda2[i]) starting from point i − 1's solution (point 0
+ * from x0, nullable = cold).  x_out: device, npts × n (row i = point i's x).  stats: host, npts
+ * entries (nullable).  With device-resident control (graph mode or the one-CTA path) every point is
+ * enqueued before a single stream synchronisation; otherwise (host-driven control, sharded handles,
+ * certify) it is a loop over ssnal_en_solve_device.  Same results and statistics as that loop;
+ * time_total_s is the path's host time shared evenly.  Returns SSNAL_OK, or the first non-OK
+ * status of a point (all stats are still written); EINVAL/ECUDA abort the path. */
+int ssnal_en_solve_path_device(ssnal_en_problem* p, int64_t npts, const double* lambda1, const double* lambda2,
+                               double sigma0, double tol, const double* x0, double* x_out, ssnal_en_stats* stats);
+
 /* K1 hook (tests / bandwidth sweep).  All vector arguments are DEVICE pointers.
  * One fused pass at y (m) with multiplier x (n) and (σ, λ1, λ2):
  *   w_out (n) = Aᵀy; J_out (int32, capacity n) = {i : |x_i − σ w_i| > σλ1} ascending (Eq. (17));

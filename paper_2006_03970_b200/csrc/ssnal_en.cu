@@ -372,6 +372,10 @@ struct ssnal_en_problem {
   cudaGraphExec_t gexec = nullptr;
   int seg_kernels[5] = {0, 0, 0, 0, 0};
   bool graph_pending = false;
+  // λ-path call (ssnal_en_solve_path_device): per-point pinned result slots and timing events
+  void* path_slots = nullptr;
+  int64_t path_cap = 0;
+  std::vector<cudaEvent_t> path_ev;
 };
 
 namespace {
@@ -1896,6 +1900,8 @@ static int create_common(ssnal_en_problem* P) {
 
 static void destroy_bufs(ssnal_en_problem* P) {
   if (!P) return;
+  if (P->path_slots) cudaFreeHost(P->path_slots);
+  for (auto e : P->path_ev) cudaEventDestroy(e);
   pool_free(P->arena);
   cudaFree(P->Msel);
   if (P->arena_h) cudaFreeHost(P->arena_h);
@@ -2242,6 +2248,119 @@ int ssnal_en_small_prof(unsigned long long* out, int reset) {
 int ssnal_en_solve(ssnal_en_problem* P, double l1, double l2, double sigma0, double tol, const double* x0,
                    double* x_out, ssnal_en_stats* stats) {
   return solve_wrapped(P, l1, l2, sigma0, tol, x0, 0, x_out, 0, stats);
+}
+
+// A warm-started λ path on device buffers: point i starts from point i − 1's solution.
+// Device-resident control (graph or one-CTA path): every point is enqueued before ONE stream
+// synchronisation — per-point results land in pinned slots and are completed afterwards.  Other
+// modes (host-driven control, sharded handles, certify) loop over ssnal_en_solve_device.
+namespace {
+struct PathSlot {
+  DevCtl ctl;
+  EvalOut ev;
+  double scratch[64];
+  double l1, l2;
+  int warm_pass, pad;
+  int64_t launches;
+};
+}  // namespace
+
+int ssnal_en_solve_path_device(ssnal_en_problem* P, int64_t npts, const double* lambda1, const double* lambda2,
+                               double sigma0, double tol, const double* x0, double* x_out, ssnal_en_stats* stats) {
+  if (!P || npts < 1 || !lambda1 || !lambda2 || !x_out) {
+    set_err("solve_path: bad arguments");
+    return SSNAL_EINVAL;
+  }
+  const int64_t n = P->n;
+  int worst = SSNAL_OK;
+  auto fold = [&](int rc) {
+    if (rc != SSNAL_OK && worst == SSNAL_OK) worst = rc;
+  };
+  const bool deferred = !sharded(P) && !P->certify && (small_eligible(P) || P->use_graph);
+  if (!deferred) {
+    for (int64_t i = 0; i < npts; ++i) {
+      const double* xi = i == 0 ? x0 : x_out + (i - 1) * n;
+      ssnal_en_stats st;
+      const int rc = solve_wrapped(P, lambda1[i], lambda2[i], sigma0, tol, xi, 1, x_out + i * n, 1, &st);
+      if (rc == SSNAL_EINVAL || rc == SSNAL_ECUDA) return rc;
+      if (stats) stats[i] = st;
+      fold(rc);
+    }
+    return worst;
+  }
+  for (int64_t i = 0; i < npts; ++i) {
+    int rc = check_args(P, lambda1[i], lambda2[i], sigma0, tol);
+    if (rc) return rc;
+  }
+  if (P->path_cap < npts) {
+    if (P->path_slots) cudaFreeHost(P->path_slots);
+    P->path_slots = nullptr;
+    P->path_cap = 0;
+    CK(cudaHostAlloc(&P->path_slots, sizeof(PathSlot) * npts, cudaHostAllocDefault));
+    P->path_cap = npts;
+  }
+  while ((int64_t)P->path_ev.size() < 2 * npts) {
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    P->path_ev.push_back(e);
+  }
+  PathSlot* slot = (PathSlot*)P->path_slots;
+  DevCtl* ctl0 = P->ctl_host;
+  EvalOut* ev0 = P->ev_out_host;
+  double* sh0 = P->scratch_host;
+  auto t0 = std::chrono::steady_clock::now();
+  std::vector<ssnal_en_stats> S(npts);
+  int rc = SSNAL_OK;
+  for (int64_t i = 0; i < npts && rc == SSNAL_OK; ++i) {  // enqueue every point
+    P->ctl_host = &slot[i].ctl;
+    P->ev_out_host = &slot[i].ev;
+    P->scratch_host = slot[i].scratch;
+    P->launches = 0;
+    CK(cudaEventRecord(P->path_ev[2 * i], P->st));
+    const double* xi = i == 0 ? x0 : x_out + (i - 1) * n;
+    if (xi) CK(cudaMemcpyAsync(P->x, xi, n * 8, cudaMemcpyDeviceToDevice, P->st));
+    rc = small_eligible(P) ? solve_small_core(P, lambda1[i], lambda2[i], sigma0, tol, xi != nullptr, &S[i])
+                           : solve_graph_core(P, lambda1[i], lambda2[i], sigma0, tol, xi != nullptr, &S[i]);
+    if (rc == SSNAL_OK) CK(cudaMemcpyAsync(x_out + i * n, P->x, n * 8, cudaMemcpyDeviceToDevice, P->st));
+    CK(cudaEventRecord(P->path_ev[2 * i + 1], P->st));
+    slot[i].l1 = P->stat_l1;
+    slot[i].l2 = P->stat_l2;
+    slot[i].warm_pass = P->stat_warm_pass;
+    slot[i].launches = P->launches;
+  }
+  P->ctl_host = ctl0;
+  P->ev_out_host = ev0;
+  P->scratch_host = sh0;
+  CK(cudaStreamSynchronize(P->st));
+  if (rc != SSNAL_OK) return rc;
+  const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  for (int64_t i = 0; i < npts; ++i) {  // complete the statistics point by point
+    P->ctl_host = &slot[i].ctl;
+    P->ev_out_host = &slot[i].ev;
+    P->scratch_host = slot[i].scratch;
+    P->stat_l1 = slot[i].l1;
+    P->stat_l2 = slot[i].l2;
+    P->stat_warm_pass = slot[i].warm_pass;
+    P->launches = slot[i].launches;
+    P->k1_time = 0;
+    P->k1_count = 0;
+    P->graph_pending = true;
+    finish_stats(P, &S[i]);
+    S[i].primal_viol = NAN;
+    float ms = 0;
+    cudaEventElapsedTime(&ms, P->path_ev[2 * i], P->path_ev[2 * i + 1]);
+    S[i].time_device_s = ms * 1e-3;
+    S[i].time_total_s = wall / npts;  // the host time of the whole path, shared evenly
+    S[i].kernel_launches = P->launches;
+    S[i].k1_time_s = P->k1_time;
+    S[i].k1_launches = P->k1_count;
+    if (stats) stats[i] = S[i];
+    fold(S[i].status);
+  }
+  P->ctl_host = ctl0;
+  P->ev_out_host = ev0;
+  P->scratch_host = sh0;
+  return worst;
 }
 
 int ssnal_en_solve_device(ssnal_en_problem* P, double l1, double l2, double sigma0, double tol, const double* x0,

@@ -82,6 +82,7 @@ def load_library():
         L.ssnal_en_get_info.restype = _d
         L.ssnal_en_solve.argtypes = [_vp, _d, _d, _d, _d, _dp, _dp, P(Stats)]
         L.ssnal_en_solve_device.argtypes = [_vp, _d, _d, _d, _d, _vp, _vp, P(Stats)]
+        L.ssnal_en_solve_path_device.argtypes = [_vp, ctypes.c_int64, _dp, _dp, _d, _d, _vp, _vp, P(Stats)]
         L.ssnal_en_aty_fused.argtypes = [_vp, _vp, _vp, _d, _d, _d, _vp, _vp, _vp, P(_i64), _dp, _vp]
         L.ssnal_en_epilogue.argtypes = [_vp, _vp, _vp, _d, _vp, _d, _d, _d, _vp, _vp, _vp, P(_i64), _dp]
         L.ssnal_en_newton_direction.argtypes = [_vp, _vp, _i64, _vp, _d, _vp, _dp, P(_i32)]
@@ -207,6 +208,17 @@ class Problem:
                                              _vp(x0_ptr) if x0_ptr else None, _vp(x_out_ptr), ctypes.byref(st))
         _check(rc, (SSNAL_OK, SSNAL_NOT_CONVERGED, SSNAL_ENUMERIC))
         return st.as_dict()
+
+    def solve_path_device(self, lambda1s, lambda2s, sigma0, tol, x0_ptr, x_out_ptr):
+        """Warm-started λ path on device buffers (x_out: npts × n); returns the per-point stats dicts."""
+        k = len(lambda1s)
+        l1 = np.ascontiguousarray(lambda1s, dtype=np.float64)
+        l2 = np.ascontiguousarray(lambda2s, dtype=np.float64)
+        st = (Stats * k)()
+        rc = self._lib.ssnal_en_solve_path_device(self._h, k, l1.ctypes.data_as(_dp), l2.ctypes.data_as(_dp),
+                                                  sigma0, tol, _vp(x0_ptr) if x0_ptr else None, _vp(x_out_ptr), st)
+        _check(rc, (SSNAL_OK, SSNAL_NOT_CONVERGED, SSNAL_ENUMERIC))
+        return [s.as_dict() for s in st]
 
     def model_select(self, lambda2, debias=False):
         """ν, rss (after OLS de-biasing), GCV, e-BIC of the latest solution.
