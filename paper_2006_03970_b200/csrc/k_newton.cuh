@@ -605,16 +605,6 @@ __global__ void __launch_bounds__(256) k_gram(const Acc A, int64_t m, const int3
   }
   gram_body<SMW>(A, m, J, r, W, gext, tiles, ns, sA, sB);
 }
-// graph mode: one launch for both exact branches (SMW with the extra column g, or m × m)
-template <class Acc>
-__global__ void __launch_bounds__(256) k_gram_any(const Acc A, int64_t m, const int32_t* __restrict__ J,
-                                                  double* __restrict__ W, const double* __restrict__ g,
-                                                  const DirGeo* geo) {
-  __shared__ double sA[kGramSmem], sB[kGramSmem];
-  const int br = geo->branch;
-  if (br == 1) gram_body<true>(A, m, J, geo->r, W, g, geo->tiles, geo->ns, sA, sB);
-  else if (br == 2) gram_body<false>(A, m, J, geo->r, W, nullptr, geo->tiles, geo->ns, sA, sB);
-}
 
 // Warp loads rows [r0, r0+32) × cols [c0, c0+32) of M into S (row-major, TLD), zero outside
 // rows < nr and cols < nc.  One 256-B coalesced load per column (lane = row).
