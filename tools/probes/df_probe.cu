@@ -274,6 +274,120 @@ __global__ void k_chain(const double* Sg, double* M, unsigned long long* cyc) {
   if (lane == 0) cyc[0] = c1 - c0;
   for (int q = 0; q < 8; ++q) M[lane * 8 + q] = a[q];
 }
+template <int NW>
+__device__ __forceinline__ void df_nw(const double* S, double* M, int ld, int n0, int kn, int nrow, double* Wout, double* Wsm,
+                          int* info, double* cb, int t128) {
+  constexpr int BC = 32 / NW;
+  const int w = t128 >> 5, lane = t128 & 31;
+  double a[BC], dgw[BC], wr[BC];
+#pragma unroll
+  for (int q = 0; q < BC; ++q) {
+    const int c = BC * w + q;
+    a[q] = (lane < nrow && c < kn) ? S[lane * TLD + c] : (lane == c ? 1.0 : 0.0);
+    dgw[q] = (c < kn) ? S[c * TLD + c] : 1.0;
+    wr[q] = (lane == c) ? 1.0 : 0.0;
+  }
+  bool bad = false;
+#pragma unroll 1
+  for (int blk = 0; blk < NW; ++blk) {
+    double* Lb = cb + (blk & 1) * (CHT * 9 + 8 * 33);  // Lb[r * 9 + p] = L[r][BC blk + p]
+    double* Wb = Lb + CHT * 9;                          // Wb[p * 33 + c] = W[8blk + p][c]
+    if (w == blk) {
+      const double* Lp = cb + ((blk + 1) & 1) * (CHT * 9 + 8 * 33);  // block blk − 1
+      const double* Wp = Lp + CHT * 9;
+      double lrp[BC], wbp[BC];
+      if (blk > 0) {
+#pragma unroll
+        for (int pp = 0; pp < BC; ++pp) {
+          lrp[pp] = Lp[lane * 9 + pp];
+          wbp[pp] = Wp[pp * 33 + lane];
+        }
+      }
+      if (blk > 0) {  // rank-8 update of this block's columns from block blk − 1, before any pivot:
+                      // eight independent chains, so only pivot 0 waits for one of them
+#pragma unroll
+        for (int p = 0; p < BC; ++p)
+#pragma unroll
+          for (int pp = 0; pp < BC; ++pp) {
+            const double l = Lp[(BC * w + p) * 9 + pp];
+            dgw[p] = fma(-l, l, dgw[p]);
+            a[p] = fma(-lrp[pp], l, a[p]);
+            wr[p] = fma(-l, wbp[pp], wr[p]);
+          }
+      }
+#pragma unroll
+      for (int p = 0; p < BC; ++p) {
+        const int j = BC * blk + p;
+        double d = dgw[p];
+        bad |= (j < kn) && !(d > 0.0);
+        d = (j < kn && d > 0.0) ? d : 1.0;
+        const double inv = rsq_n<2>(d);
+        const double lij = (lane > j) ? a[p] * inv : (lane == j ? d * inv : 0.0);
+        const double wj = wr[p] * inv;  // W row j scaled (final)
+#pragma unroll
+        for (int q = p + 1; q < BC; ++q) {
+          const double lq = __shfl_sync(0xffffffffu, lij, BC * blk + q);  // L[8blk+q][j]
+          dgw[q] = fma(-lq, lq, dgw[q]);
+          a[q] = fma(-lij, lq, a[q]);
+          wr[q] = fma(-lq, wj, wr[q]);
+        }
+        a[p] = lij;
+        wr[p] = wj;
+      }
+#pragma unroll
+      for (int p = 0; p < BC; ++p) {
+        Lb[lane * 9 + p] = a[p];
+        Wb[p * 33 + lane] = wr[p];
+      }
+    }
+    asm volatile("bar.sync 2, %0;" :: "r"(NW * 32) : "memory");
+    if (w > blk + 1) {  // eager rank-8 update from block blk
+      double lr[BC], wb[BC];
+#pragma unroll
+      for (int p = 0; p < BC; ++p) {
+        lr[p] = Lb[lane * 9 + p];
+        wb[p] = Wb[p * 33 + lane];
+      }
+#pragma unroll
+      for (int q = 0; q < BC; ++q) {
+        const double* lc = Lb + (BC * w + q) * 9;
+#pragma unroll
+        for (int p = 0; p < BC; ++p) {
+          const double l = lc[p];  // L[8w+q][8blk+p]
+          dgw[q] = fma(-l, l, dgw[q]);
+          a[q] = fma(-lr[p], l, a[q]);
+          wr[q] = fma(-l, wb[p], wr[q]);
+        }
+      }
+    }
+  }
+  if (bad && lane == 0) atomicExch(info, 1);
+  if (!M) asm volatile("bar.sync 2, %0;" :: "r"(NW * 32) : "memory");  // every warp has read S before L overwrites it
+#pragma unroll
+  for (int q = 0; q < BC; ++q) {
+    const int c = BC * w + q;
+    if (M) {
+      if (lane < nrow && c < kn && c <= lane) M[(int64_t)(n0 + lane) + (int64_t)(n0 + c) * ld] = a[q];
+    } else {  // L into the smem tile itself (DSMEM-resident factor): rows < nrow, cols < kn, else 0
+      const_cast<double*>(S)[lane * TLD + c] = (lane < nrow && c < kn && c <= lane) ? a[q] : 0.0;
+    }
+    const double wv = (c < kn && lane < kn) ? wr[q] : (lane == c ? 1.0 : 0.0);  // pad: identity
+    if (Wout) Wout[c * CHT + lane] = wv;
+    if (Wsm) Wsm[c * TLD + lane] = wv;
+  }
+}
+
+
+template <int NW>
+__global__ void k_nw(const double* Sg, double* M, double* W, int* info, unsigned long long* cyc) {
+  __shared__ double S[CHT * TLD + kDiagScratch];
+  for (int e = threadIdx.x; e < CHT * TLD; e += NW * 32) S[e] = Sg[e];
+  __syncthreads();
+  long long c0 = clock64();
+  df_nw<NW>(S, M, 32, 0, 32, 32, W, nullptr, info, S + CHT * TLD, threadIdx.x);
+  long long c1 = clock64();
+  if (threadIdx.x == 0) cyc[0] = c1 - c0;
+}
 template <bool WANTW, int NEWTON>
 __global__ void k_var(const double* Sg, double* M, double* W, int* info, unsigned long long* cyc) {
   __shared__ double S[CHT * TLD + kDiagScratch];
@@ -320,6 +434,21 @@ int main() {
     unsigned long long c3; cudaMemcpy(&c3, cyc, 8, cudaMemcpyDeviceToHost);
     printf("chain only (%s): %llu cycles (%.0f per pivot)\n", md == 0 ? "rsqrt+2N" : (md == 1 ? "MUFU only" : "1/sqrt"), c3, c3 / 32.0);
   }
+  for (int rep = 0; rep < 5; ++rep) k_nw<8><<<1, 256>>>(dS, dM, dW, info, cyc);
+  { cudaDeviceSynchronize(); unsigned long long c8; cudaMemcpy(&c8, cyc, 8, cudaMemcpyDeviceToHost);
+    double L[32 * 32], W[32 * 32];
+    cudaMemcpy(L, dM, sizeof(L), cudaMemcpyDeviceToHost); cudaMemcpy(W, dW, sizeof(W), cudaMemcpyDeviceToHost);
+    double e1 = 0, e2 = 0;
+    for (int i = 0; i < 32; ++i) for (int j = 0; j <= i; ++j) {
+      double s2 = 0; for (int p = 0; p <= j; ++p) s2 += L[i + p * 32] * L[j + p * 32];
+      e1 = fmax(e1, fabs(s2 - h[i * TLD + j]));
+      double t = 0; for (int p = j; p <= i; ++p) t += W[i * 32 + p] * L[p + j * 32];
+      e2 = fmax(e2, fabs(t - (i == j)));
+    }
+    printf("%-24s %6llu cycles (%.0f per pivot) |LL'-A| %.2e |WL-I| %.2e %s\n", "8 warps x 4 columns", c8, c8 / 32.0, e1, e2, cudaGetErrorString(cudaGetLastError())); }
+  for (int rep = 0; rep < 5; ++rep) k_nw<4><<<1, 128>>>(dS, dM, dW, info, cyc);
+  { cudaDeviceSynchronize(); unsigned long long c4; cudaMemcpy(&c4, cyc, 8, cudaMemcpyDeviceToHost);
+    printf("%-24s %6llu cycles (%.0f per pivot)\n", "4 warps x 8 (generic)", c4, c4 / 32.0); }
   for (int rep = 0; rep < 5; ++rep) k_warp<2><<<1, 32>>>(dS, dM, cyc);
   cudaDeviceSynchronize();
   unsigned long long c; cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
