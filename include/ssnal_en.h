@@ -111,8 +111,8 @@ double ssnal_en_lambda_max_l1(const ssnal_en_problem* p);
  *     one 512-thread CTA, k_small_solve — same iteration and statistics, reduction orders differ;
  *     0: the multi-kernel graph / host paths),
  *   K4 variants (identical contract, results equal up to rounding): chol_dsm=1 (DSMEM-resident
- *     16-CTA cluster Cholesky for N ≤ 160; 0: the L2-tiled k_chol_cluster for every N), chol_d2=1
- *     (split-ownership DSMEM Cholesky k_chol_d2 for 160 < N ≤ 512; needs chol_dsm=1),
+ *     16-CTA cluster Cholesky for N ≤ 96; 0: the L2-tiled k_chol_cluster for every N), chol_d2=1
+ *     (split-ownership DSMEM Cholesky k_chol_d2 for 96 < N ≤ 512; needs chol_dsm=1),
  *   certify=0 (1: after each solve compute stats.primal_viol with one extra Aᵀ pass),
  *   graph=1 (Algorithm 1 control on the device, the whole solve one CUDA graph; 0: host-driven
  *     control with one evaluation record read per ψ evaluation — identical results),
@@ -132,7 +132,7 @@ int ssnal_en_set_option(ssnal_en_problem* p, const char* key, double value);
 /* Read-only introspection: "m", "n", "k1_cols", "k1_stages", "k1_grid", "k1_smem",
  * "cluster_size", "num_sms", "graph", "format", "cg_ratio", "cg_threshold", and which kernels a
  * solve on this handle uses: "small" (1: the one-CTA path k_small_solve), "chol_dsm" (1: k_chol_dsm
- * for N ≤ 160), "chol_d2" (1: k_chol_d2 for 160 < N ≤ 512).  Returns NaN for unknown keys. */
+ * for N ≤ 96), "chol_d2" (1: k_chol_d2 for 96 < N ≤ 512).  Returns NaN for unknown keys. */
 double ssnal_en_get_info(const ssnal_en_problem* p, const char* key);
 
 /* Solve Algorithm 1 for (λ1, λ2) in the paper's unnormalised units.

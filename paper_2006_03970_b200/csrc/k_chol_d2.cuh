@@ -1,4 +1,4 @@
-// K4, DSMEM-resident with split ownership (160 < N ≤ 512): the Cholesky factor of the N × N SPD
+// K4, DSMEM-resident with split ownership (96 < N ≤ 512): the Cholesky factor of the N × N SPD
 // matrix of Eq. (18) / (19), the forward substitution (right-hand side carried as row N) and the
 // backward substitution, by one 16-CTA cluster whose shared memory holds the whole lower triangle.
 //
@@ -38,7 +38,7 @@
 
 namespace ssn {
 
-constexpr int kD2Slots = 12;  // max tiles per CTA over 160 < N ≤ 512 (checked by tools/probes/d2_probe)
+constexpr int kD2Slots = 12;  // max tiles per CTA over N ≤ 512 (checked by tools/probes/d2_probe)
 constexpr int kD2Bytes = kTileD * 8;  // one tile (8448 B, a multiple of 16)
 constexpr size_t kD2SmemDoubles = (size_t)kD2Slots * kTileD  // owned tiles
                                   + 4 * kTileD                 // W_j of my diagonal tiles (j ≡ CTA mod 4)
@@ -495,7 +495,7 @@ __global__ void __launch_bounds__(256, 1) k_chol_d2(const double* __restrict__ M
 }
 
 // Graph mode: one node for both DSMEM-resident kernels, dispatching on the device geometry's N
-// (k_chol_dsm for N ≤ 160, k_chol_d2 for 160 < N ≤ 512); dynamic shared memory kD2Smem.
+// (k_chol_dsm for N ≤ 96, k_chol_d2 for 96 < N ≤ 512); dynamic shared memory kD2Smem.
 __global__ void __launch_bounds__(256, 1) k_chol_dsm_any(const double* __restrict__ M, double* __restrict__ out,
                                                          double scale, const double* __restrict__ dotv,
                                                          double* dot_out, int* info, const double* __restrict__ ybase,

@@ -22,8 +22,8 @@
 
 namespace ssn {
 
-constexpr int kDsmCS = 16;
-constexpr int kDsmUseMax = 160;  // k_chol_dsm for N ≤ 160 (faster there than k_chol_d2)                 // cluster size = max block columns (N ≤ 512)
+constexpr int kDsmCS = 16;  // cluster size = max block columns (N ≤ 512)
+constexpr int kDsmUseMax = 96;  // k_chol_dsm for N ≤ 96 (faster there than k_chol_d2: N = 64 20.7 vs 22.7 µs)
 constexpr int kDsmMaxN = kDsmCS * CHT;     // 512
 constexpr int kDsmTiles = kDsmCS + 1;      // row tiles of column 0 at N = 512 (NR = 513)
 constexpr int kTileD = CHT * TLD;          // doubles per smem tile (32 × 33)

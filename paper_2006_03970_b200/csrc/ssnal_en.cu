@@ -284,7 +284,7 @@ struct ssnal_en_problem {
   int use_dsm = 1;   // option chol_dsm: DSMEM-resident K4 for N ≤ 512 when schedulable
   int dsm_ok = 0;    // … schedulable on this device
   int chol_dsm = 0;  // use_dsm && dsm_ok
-  int use_d2 = 1;    // option chol_d2: split-ownership DSMEM K4 (k_chol_d2) for 160 < N ≤ 512
+  int use_d2 = 1;    // option chol_d2: split-ownership DSMEM K4 (k_chol_d2) for 96 < N ≤ 512
   int d2_ok = 0;     // … schedulable on this device
   int gax_grid = 0;
   // device buffers
@@ -925,7 +925,7 @@ int launch_chol_ex(ssnal_en_problem* P, double* M, int N, int NR, int ld, double
 }
 
 // DSMEM-resident K4 (k_chol_dsm.cuh): same contract as the k_chol_cluster launch below.  Used for
-// N ≤ kDsmUseMax, where it is faster (N = 100: 35 vs 47 µs; crossover near N = 192, and N = 500
+// N ≤ kDsmUseMax, where it is faster than k_chol_d2 (and than k_chol_cluster: N = 100 35 vs 47 µs; N = 500
 // takes ~300 vs ~211 µs: its per-owner update load is uneven).
 int launch_chol_dsm(ssnal_en_problem* P, double* M, int N, double* out, double scale, const double* dotv,
                     double* dot_out, const double* ybase, double* yt, const DirGeo* geo, int want) {
@@ -971,7 +971,7 @@ int launch_chol_d2(ssnal_en_problem* P, double* M, int N, double* out, double sc
 }
 
 // Cluster Cholesky + both triangular solves: M holds the matrix (ld = N+1) and the rhs in row N.
-// Host mode: k_chol_dsm for N ≤ 160, k_chol_d2 for 160 < N ≤ 512, else k_chol_cluster.  Graph
+// Host mode: k_chol_dsm for N ≤ 96, k_chol_d2 for 96 < N ≤ 512, else k_chol_cluster.  Graph
 // mode (geo): each kernel that can occur for this m, predicated on its N range.
 int launch_chol(ssnal_en_problem* P, double* M, int N, double* out, double scale, const double* dotv,
                 double* dot_out, const double* ybase = nullptr, double* yt = nullptr, const DirGeo* geo = nullptr,

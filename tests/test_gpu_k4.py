@@ -1,5 +1,5 @@
 """K4 variants (Eq. (18)/(19) factor and solves): the DSMEM-resident cluster
-Cholesky (k_chol_dsm, N ≤ 160) and the split-ownership DSMEM Cholesky (k_chol_d2, 160 < N ≤ 512)
+Cholesky (k_chol_dsm, N ≤ 96) and the split-ownership DSMEM Cholesky (k_chol_d2, 96 < N ≤ 512)
 against the L2-tiled cluster Cholesky (k_chol_cluster) and the oracle, through the
 Newton-direction hook, across tile edges and the switch points; and whole solves with each
 variant, graph-mode control ≡ host-mode control."""
@@ -25,7 +25,7 @@ def direction(P, J, g, kappa):
     return host(dd, m), gd, br
 
 
-@pytest.mark.parametrize("m,r", [(500, 1), (500, 31), (500, 32), (500, 33), (500, 100), (500, 160), (500, 161),
+@pytest.mark.parametrize("m,r", [(500, 1), (500, 31), (500, 32), (500, 33), (500, 96), (500, 97), (500, 100), (500, 160), (500, 161),
                                  (500, 300), (160, 159), (160, 400), (161, 400), (40, 7), (64, 1000),
                                  (500, 192), (500, 255), (500, 256), (500, 257), (500, 435), (500, 499),
                                  (500, 500), (500, 700), (511, 900), (512, 1000), (513, 1000), (400, 2000)])
