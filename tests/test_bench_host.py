@@ -77,3 +77,17 @@ def test_max_over_ranks_without_group():
     import bench
 
     assert bench.max_over_ranks(3.25, device="cpu") == 3.25
+
+
+def test_small_roofline_line():
+    """The one-CTA path has no K1 launches: the bench reports a latency-bound roofline for k_small_solve
+    with the effective A-pass bandwidth (passes × 8mn bytes / device time) against the HBM peak."""
+    sys.path.insert(0, ROOT)
+    import bench
+
+    sts = [{"aty_passes": 16}, {"aty_passes": 4}]
+    r = bench.small_roofline(50, 1000, sts, 1e-3, 6500.0, "measured")
+    assert r["bound"] == "latency" and r["kernel"] == "k_small_solve" and r["unit"] == "GB/s"
+    assert r["bytes_per_launch"] == 20 * 8 * 50 * 1000
+    assert r["achieved"] == pytest.approx(20 * 8 * 50 * 1000 / 1e-3 / 1e9)
+    assert r["frac"] == pytest.approx(r["achieved"] / 6500.0) and r["launches"] == 2
