@@ -133,3 +133,20 @@ def test_small_lasso_innertol_retry_cap():
         P.set_option("max_outer", 100)
         x2, s2 = P.solve(l1, l2, 5e-3, 1e-6)
         assert s2["status"] == 0 and np.array_equal(x2, x0)
+
+
+@pytest.mark.parametrize("m,n,eligible", [(64, 1024, 1), (65, 100, 0), (10, 1025, 0), (2, 1, 1)])
+def test_small_eligibility(m, n, eligible):
+    """The one-CTA path serves m ≤ 64, n ≤ 1024 (fp64 storage, unsharded, no CG strategy); the option
+    small = 0 and the CG strategy turn it off."""
+    rng = np.random.default_rng(m * 7 + n)
+    A = rng.standard_normal((n, m))
+    b = rng.standard_normal(m)
+    with Problem(A, b) as P:
+        assert P.info("small") == eligible
+        if eligible:
+            P.set_option("cg_ratio", 2.0)
+            assert P.info("small") == 0
+            P.set_option("cg_ratio", 0.0)
+            P.set_option("small", 0)
+            assert P.info("small") == 0
