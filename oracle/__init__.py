@@ -269,6 +269,36 @@ def solve(A, b, l1, l2, sigma0=5e-3, tol=1e-6, x0=None, trace_cap=0, **opts):
     return x, y, stats, trace
 
 
+def solve_path_lambdas(A, b, ls, sigma0=5e-3, tol=1e-6, x0=None, carry_sigma=True, max_active=None, **opts):
+    """Warm-started λ path over explicit (λ1, λ2) pairs: point i starts from point i−1's x
+    (the warm start of P:411; y0 = A x0 − b by reading R8) and, with carry_sigma, from point i−1's
+    final σ — the σ of its last inner solve (reading R38: the paper's "usually SsNAL-EN converges in
+    just one iteration", needs the σ the previous point ended with; SPEC's open question S:336
+    records the same choice).  Point 0 starts at sigma0 from x0 (None = cold).  The path stops after
+    the first point with at least max_active nonzeros.  Returns a list of (x, y, stats)."""
+    out = []
+    x = x0
+    sig = sigma0
+    for i, (l1, l2) in enumerate(ls):
+        x, y, st, _ = solve(A, b, l1, l2, sigma0=sig, tol=tol, x0=x, **opts)
+        out.append((x, y, st))
+        if carry_sigma:
+            sig = st["sigma_final"]
+        if max_active is not None and st["active"] >= max_active:
+            break
+    return out
+
+
+def solve_path(A, b, alpha, cs, sigma0=5e-3, tol=1e-6, carry_sigma=True, max_active=None, **opts):
+    """The λ path of Section 3.3 on the c grid: λmax = ‖Aᵀb‖∞/α, λ1 = cαλmax, λ2 = c(1−α)λmax
+    (P:506), warm-started as in solve_path_lambdas.  Returns (lambdas, [(x, y, stats)])."""
+    lm = lambda_max_l1(A, b) / alpha
+    ls = [(c * alpha * lm, c * (1 - alpha) * lm) for c in cs]
+    res = solve_path_lambdas(A, b, ls, sigma0=sigma0, tol=tol, carry_sigma=carry_sigma, max_active=max_active,
+                             **opts)
+    return ls[:len(res)], res
+
+
 def aty_fused(A, b, y, x, sigma, l1, l2, with_grad=True):
     """K1-equivalent: (w, J, P_J, partials[4], g)."""
     A, m, n, Ap = _A(A)
@@ -350,10 +380,10 @@ def oracle_ax(A, x):
     return out
 
 
-def cv_path(A, b, alpha, cs, k=5, sigma0=5e-3, tol=1e-6):
+def cv_path(A, b, alpha, cs, k=5, sigma0=5e-3, tol=1e-6, carry_sigma=True):
     """k-fold CV error along c ∈ cs ("cross-validation ... along the path"): λ from the FULL
     data (λmax = ‖Aᵀb‖∞/α) so every fold uses the same grid; for each fold the
-    warm-started path on the training rows, and the held-out squared error.
+    warm-started path on the training rows (σ carried, R38), and the held-out squared error.
     Returns cv[c] = Σ_folds ‖b_test − A_test x_fold(c)‖² / m (reading R35) and the minimising index."""
     A = np.ascontiguousarray(A, dtype=np.float64)
     b = np.asarray(b, dtype=np.float64)
@@ -364,10 +394,9 @@ def cv_path(A, b, alpha, cs, k=5, sigma0=5e-3, tol=1e-6):
         train = np.setdiff1d(np.arange(m), test)
         Atr, btr = np.ascontiguousarray(A[:, train]), b[train]
         Ate, bte = np.ascontiguousarray(A[:, test]), b[test]
-        x = None
-        for i, c in enumerate(cs):
-            l1, l2 = c * alpha * lm, c * (1 - alpha) * lm
-            x, _, st, _ = solve(Atr, btr, l1, l2, sigma0=sigma0, tol=tol, x0=x)
+        ls = [(c * alpha * lm, c * (1 - alpha) * lm) for c in cs]
+        for i, (x, _, _) in enumerate(solve_path_lambdas(Atr, btr, ls, sigma0=sigma0, tol=tol,
+                                                          carry_sigma=carry_sigma)):
             err[i] += residual_ss(Ate, bte, x)
     err /= m
     return err, int(np.argmin(err))

@@ -1,0 +1,73 @@
+"""Reading R38: along a warm-started λ path each point starts from the previous point's x AND its
+final σ (oracle.solve_path).  Pinned against what the paper says a warm start does: "the new solution
+is very close to the previous one and can be computed very quickly -- usually SsNAL-EN converges in
+just one iteration", on the Table D.4 protocol (100 log-spaced c from 1 to
+0.1, stopping at 100 active features), plus SPEC's soft bound of ≤ 2 outer iterations per
+warm-started step on fine grids.  Restarting σ at σ0 (carry_sigma=False, the round-1
+reading) fails the pin: it takes ≥ 3 outer iterations at every warm point.  Both readings reach the
+same minimiser (strong convexity, λ2 > 0), checked at the BASELINE tolerances."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+
+@pytest.fixture(scope="module")
+def d4_paths():
+    cfg = synth.scaled(synth.CONFIGS["cfg2"], n=20_000)  # the cfg2 (AR(1)) recipe at CPU size
+    A = synth.design(cfg)
+    b, _ = synth.response(cfg)
+    cs = np.logspace(0, -1, 100)  # Table D.4 grid
+    carry = oracle.solve_path(A, b, cfg.alpha, cs, max_active=100)
+    return cfg, A, b, cs, carry
+
+
+def warm_points(res):
+    """(stats of) the points whose start x0 was non-zero (x0 = 0 is a cold start under R8)."""
+    return [st for (_, _, st), (xp, _, _) in zip(res[1:], res[:-1]) if np.any(xp != 0)]
+
+
+def test_warm_path_converges_in_one_outer_iteration(d4_paths):
+    cfg, A, b, cs, (ls, res) = d4_paths
+    assert all(st["status"] == 0 for _, _, st in res)
+    assert res[-1][2]["active"] >= 100 and len(res) < len(cs)  # the P:412 cap ended the path
+    warm = warm_points(res)
+    assert len(warm) >= 40
+    one = sum(st["outer_iters"] == 1 for st in warm)
+    assert one >= 0.9 * len(warm), [st["outer_iters"] for st in warm]  # P:411 "usually ... one iteration"
+    assert max(st["outer_iters"] for st in warm) <= 2
+    # σ is carried: every point starts where the previous one ended, so σ never decreases
+    sig = [st["sigma_final"] for _, _, st in res]
+    assert all(b_ >= a_ for a_, b_ in zip(sig, sig[1:]))
+
+
+def test_reset_sigma_reading_fails_the_pin(d4_paths):
+    cfg, A, b, cs, (ls, res) = d4_paths
+    k = 12  # the first points suffice to show it
+    reset = oracle.solve_path_lambdas(A, b, ls[:k], carry_sigma=False)
+    warm = warm_points(reset)
+    assert min(st["outer_iters"] for st in warm) >= 3
+    # same minimiser: at tol 1e-10 both readings agree at the BASELINE tolerances (objective 1e-9
+    # relative, x∞ 1e-6, sign pattern R22); at tol 1e-6 they stop at different iterates, both within
+    # the Eq. (20) tolerance
+    tight_c = oracle.solve_path_lambdas(A, b, ls[:k], tol=1e-10)
+    tight_r = oracle.solve_path_lambdas(A, b, ls[:k], tol=1e-10, carry_sigma=False)
+    for (xc, _, _), (xr, _, _), (l1, l2) in zip(tight_c, tight_r, ls[:k]):
+        Fc, Fr = oracle.primal_obj(A, b, xc, l1, l2), oracle.primal_obj(A, b, xr, l1, l2)
+        assert abs(Fc - Fr) <= 1e-9 * abs(Fr)
+        assert np.max(np.abs(xc - xr)) <= 1e-6 * max(np.max(np.abs(xr)), 1e-300)
+        mask = np.maximum(np.abs(xc), np.abs(xr)) > 1e-8
+        assert np.array_equal(np.sign(xc[mask]), np.sign(xr[mask]))
+
+
+def test_path_points_satisfy_kkt_at_tight_tolerance():
+    """With σ carried to a large value, the solution is still the Elastic Net minimiser: at tol 1e-10
+    the KKT inclusion Aᵀ(b − Ax) − λ2x ∈ λ1∂‖x‖₁ holds to 1e-8 λ1 at every point."""
+    cfg = synth.scaled(synth.CONFIGS["cfg2"], n=5_000)
+    A = synth.design(cfg)
+    b, _ = synth.response(cfg)
+    ls, res = oracle.solve_path(A, b, cfg.alpha, np.linspace(0.9, 0.1, 10), tol=1e-10)
+    for (l1, l2), (x, _, st) in zip(ls, res):
+        assert st["status"] == 0
+        assert oracle.kkt_violation(A, b, x, l1, l2) <= 1e-8 * l1
