@@ -2,22 +2,25 @@
 """Benchmark of the SsNAL-EN hot path on B200 (BASELINE.json metric).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--config cfg2|cfg3|cfg4|cfg5|cfg1] [--sweep]
+                  [--config cfg5|cfg1|cfg2|cfg3|cfg4] [--geno] [--sweep] [--select]
 
-One "step" is one full time-to-solution of the workload: for cfg2 (BASELINE configs[1],
-the default) the warm-started 10-point λ path c = 0.9 … 0.1 at KKT tolerance 1e-6, i.e.
-every §8(a) row of SURVEY.md (K1 passes, re-thresholds, Newton systems, line searches,
-outer updates).  Inputs are synthetic (synth/), generated directly in HBM; A is 400 MB,
-larger than the 126 MB L2, so no flush is needed between steps.
+One "step" is one full time-to-solution of the workload at KKT tolerance 1e-6 — every §8(a) row of
+SURVEY.md (K1 passes, re-thresholds, Newton systems, line searches, outer updates).  The default is
+cfg5 (BASELINE configs[4], the "HBM-bound stress" case the metric's K1 target is stated on:
+m = 500, n = 1e7, 40 GB of A, cold solves at c = 0.5 and 0.1); --config cfg2 times the 10-point
+warm-started path of configs[1] (σ carried from point to point, reading R38).  Inputs are synthetic
+(synth/), generated directly in HBM; A is larger than the 126 MB L2, so no flush is needed.
 
-The JSON line carries: value (device-timed seconds per step, max over ranks), e2e (the same
-through the C-ABI with HOST buffers, create + H2D + solves + D2H inside the timed region),
-roofline of the dominant kernel (K1: algorithmic bytes per launch / mean launch time from CUDA
-events recorded on the launching stream during the timed steps), cpu_baseline (the oracle on
-this host, rank 0 only), clocks sampled during the timed region, gpu_launches.
+The JSON line carries: value (device-timed seconds per step, max over ranks) with per-step median and
+mean ± se, e2e (the same workload through the host-memory C-ABI: ssnal_en_create from pinned HOST
+buffers + the solves + x D2H inside the timed region), the roofline of the dominant kernel (K1:
+algorithmic bytes per launch / mean launch time measured during the timed steps), cpu_baseline (the
+oracle on this host's cores, warmed, in a clean subprocess; rank 0 only) and the §8(d) parity block of
+the timed step's solutions against the oracle's, clocks sampled during the timed region, gpu_launches.
 
---impl reference: the base contract's reference arm is, for this paper-only tier, the CPU
-oracle (oracle/), timed on the host cores on the same workload (rank 0 only).
+--impl reference: the base contract's reference arm is, for this paper-only tier, the CPU oracle
+(oracle/), timed on the host cores with the same --steps/--warmup on a bounded column sample of the
+same workload, scaled to seconds per workload (rank 0 only).
 Multi-GPU (torchrun): by default each rank solves its own replica (value = max over ranks,
 scaling "weak"); with --shard the ranks split the columns of one problem and
 exchange the cross-column sums by NCCL all-reduce (scaling "strong").
@@ -146,26 +149,46 @@ def geno_roofline(m, n, k1_avg, k1_gbs, hbm_peak, traffic):
             "hbm_view": {"achieved_GBps": k1_gbs, "peak_GBps": hbm_peak}}
 
 
-def run_path_device(P, cfg, lm, x_buf, x_prev_ptr=None, x_path=None):
-    """One step: the workload's solves on device buffers.  Returns (device_s, launches, stats list).
-    A warm-started path goes through the library's path call (ssnal_en_solve_path_device: every point
-    enqueued before one synchronisation) when x_path (npts × n device buffer) is given."""
-    if cfg.path and x_path is not None:
+def run_step(P, cfg, lm, x_all):
+    """One step: the workload's solves on device buffers (x_all: npts × n, row i = point i's x).
+    Returns (device_s, launches, stats list).  A warm-started path goes through the library's path call
+    (ssnal_en_solve_path_device: every point enqueued before one synchronisation, σ carried from point
+    to point — reading R38); independent solves (cfg3-5) are cold solves, one per c."""
+    if cfg.path:
         ls = [lambdas(cfg, lm, c) for c in cfg.cs]
-        stats = P.solve_path_device([a for a, _ in ls], [b for _, b in ls], cfg.sigma0, cfg.tol, 0, x_path.data_ptr())
+        stats = P.solve_path_device([a for a, _ in ls], [b for _, b in ls], cfg.sigma0, cfg.tol, 0, x_all.data_ptr())
         return sum(s["time_device_s"] for s in stats), sum(s["kernel_launches"] for s in stats), stats
-    total_dev = 0.0
-    launches = 0
-    stats = []
-    prev = 0
+    total_dev, launches, stats = 0.0, 0, []
     for i, c in enumerate(cfg.cs):
         l1, l2 = lambdas(cfg, lm, c)
-        x0 = x_buf.data_ptr() if (cfg.path and i > 0) else 0
-        st = P.solve_device(l1, l2, cfg.sigma0, cfg.tol, x0, x_buf.data_ptr())
+        st = P.solve_device(l1, l2, cfg.sigma0, cfg.tol, 0, x_all[i].data_ptr())
         total_dev += st["time_device_s"]
         launches += st["kernel_launches"]
         stats.append(st)
     return total_dev, launches, stats
+
+
+def host_solve_workload(Q, cfg, lm):
+    """The same workload through the host-memory C-ABI call ssnal_en_solve (x0 up, x down per solve).
+    Returns (h2d bytes of the solves, d2h bytes)."""
+    x_prev, sig, h2d, d2h = None, cfg.sigma0, 0, 0
+    for i, c in enumerate(cfg.cs):
+        l1, l2 = lambdas(cfg, lm, c)
+        x0 = x_prev if (cfg.path and i > 0) else None
+        x_prev, st = Q.solve(l1, l2, sig, cfg.tol, x0=x0)
+        if cfg.path:
+            sig = st["sigma_final"]  # R38, as the path call does
+        h2d += 8 * cfg.n if x0 is not None else 0
+        d2h += 8 * cfg.n
+    return h2d, d2h
+
+
+def step_summary(ts):
+    """median and mean ± standard error of per-step device times (SURVEY §8(d) timing protocol)."""
+    ts = list(ts)
+    mean = statistics.fmean(ts)
+    se = statistics.stdev(ts) / len(ts) ** 0.5 if len(ts) > 1 else 0.0
+    return {"median_s": statistics.median(ts), "mean_s": mean, "se_s": se, "n": len(ts)}
 
 
 def bench_ours(args, rank, world, local_rank):
@@ -180,16 +203,17 @@ def bench_ours(args, rank, world, local_rank):
     stream = torch.cuda.current_stream()
     b_host, _ = synth.response(cfg)
     db = torch.from_numpy(b_host).cuda()
+    dA = None
     if args.geno:  # §8(f4): A as packed 2-bit genotype codes + per-column tables
         if cfg.kind != synth.GENO_STD:
             raise SystemExit("--geno needs a genotype config (cfg4)")
         stride = synth.geno_stride(m)
-        dA = torch.empty((n, stride), dtype=torch.uint8, device="cuda")
+        dcodes = torch.empty((n, stride), dtype=torch.uint8, device="cuda")
         dtab = torch.empty((n, 3), dtype=torch.float64, device="cuda")
-        synth.fill_device_geno(cfg, dA.data_ptr(), dtab.data_ptr(), stream.cuda_stream)
+        synth.fill_device_geno(cfg, dcodes.data_ptr(), dtab.data_ptr(), stream.cuda_stream)
         torch.cuda.synchronize()
-        P = Problem.from_geno_device(dA.data_ptr(), stride, dtab.data_ptr(), db.data_ptr(), m, n, stream.cuda_stream,
-                                     keep=(dA, dtab, db))
+        P = Problem.from_geno_device(dcodes.data_ptr(), stride, dtab.data_ptr(), db.data_ptr(), m, n,
+                                     stream.cuda_stream, keep=(dcodes, dtab, db))
     elif args.shard:  # §8(f3): this rank owns columns [j0, j1); cross-column sums by NCCL all-reduce
         from paper_2006_03970_b200.shard import column_range, torch_allreduce
 
@@ -208,44 +232,56 @@ def bench_ours(args, rank, world, local_rank):
     P.set_option("graph", 1 if args.control == "graph" else 0)
     P.set_option("cg_ratio", args.cg_ratio)
     lm = P.lambda_max_l1
-    x_buf = torch.zeros(n, dtype=torch.float64, device="cuda")
-    x_path = torch.empty((len(cfg.cs), n), dtype=torch.float64, device="cuda") if cfg.path else None
+    x_all = torch.zeros((len(cfg.cs), n), dtype=torch.float64, device="cuda")
 
     for _ in range(args.warmup):
-        run_path_device(P, cfg, lm, x_buf, x_path=x_path)
+        run_step(P, cfg, lm, x_all)
     torch.cuda.synchronize()
 
-    # ---- timed region: K steps, K1 launch events on the handle's stream ----
+    # ---- timed region: K steps, K1 launch times on the handle's stream ----
     P.set_option("time_k1", 1)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     k1_time = 0.0
     k1_launches = 0
     launches = 0
     dev_sum = 0.0
     last_stats = None
     with ClockSampler(local_rank) as clk:
-        ev0.record(stream)
-        for _ in range(args.steps):
-            d, L, sts = run_path_device(P, cfg, lm, x_buf, x_path=x_path)
+        evs[0].record(stream)
+        for k in range(args.steps):
+            d, L, sts = run_step(P, cfg, lm, x_all)
+            evs[k + 1].record(stream)
             dev_sum += d
             launches += L
             k1_time += sum(s["k1_time_s"] for s in sts)
             k1_launches += sum(s["k1_launches"] for s in sts)
             last_stats = sts
-        ev1.record(stream)
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     P.set_option("time_k1", 0)
-    elapsed = ev0.elapsed_time(ev1) * 1e-3
+    per_step = [evs[k].elapsed_time(evs[k + 1]) * 1e-3 for k in range(args.steps)]
+    elapsed = sum(per_step)
     t_step = max_over_ranks(elapsed / args.steps)
+    x_gpu = x_all.cpu().numpy()  # the last timed step's solutions (parity block)
 
-    # ---- e2e: through the C-ABI with HOST buffers (create + H2D + solves + D2H) ----
-    A_host = None
+    # K1 at a probe point for the parity block's Aᵀy error (R21): same y as the oracle leg
+    w_probe = None
+    if rank == 0 and world == 1 and not args.no_cpu and not args.shard:
+        y = torch.from_numpy(synth.normals(cfg.seed, 12, m)).cuda()
+        xz = torch.zeros(n, dtype=torch.float64, device="cuda")
+        w = torch.empty(n, dtype=torch.float64, device="cuda")
+        J = torch.empty(n, dtype=torch.int32, device="cuda")
+        PJ = torch.empty(n, dtype=torch.float64, device="cuda")
+        P.aty_fused(y.data_ptr(), xz.data_ptr(), 1.0, 1e300, 0.1, w.data_ptr(), J.data_ptr(), PJ.data_ptr())
+        w_probe = w.cpu().numpy()
+        del y, xz, w, J, PJ
+
+    # ---- e2e: the public host-memory C-ABI with HOST buffers; per step: ssnal_en_create (H2D of A, b,
+    # validation, λmax pass), the workload's solves through ssnal_en_solve (x0 H2D, x D2H), destroy ----
     e2e = None
     if not args.no_e2e and args.geno:
         codes_h, tab_h = synth.geno_codes(cfg)
@@ -254,45 +290,35 @@ def bench_ours(args, rank, world, local_rank):
             t0 = time.perf_counter()
             Q = Problem.from_geno(codes_h, tab_h, b_host)
             Q.set_option("graph", 1 if args.control == "graph" else 0)
-            lmq = Q.lambda_max_l1
-            x_prev = None
-            for i, c in enumerate(cfg.cs):
-                l1, l2 = lambdas(cfg, lmq, c)
-                x_prev, st = Q.solve(l1, l2, cfg.sigma0, cfg.tol, x0=x_prev if cfg.path else None)
+            h2d, d2h = host_solve_workload(Q, cfg, Q.lambda_max_l1)
             Q.close()
             if it > 0:
                 e2e_times.append(time.perf_counter() - t0)
         e2e = {"value": max_over_ranks(statistics.median(e2e_times)), "unit": "s",
-               "h2d_bytes_per_step": int(codes_h.nbytes + tab_h.nbytes + 8 * m),
-               "d2h_bytes_per_step": 8 * n * len(cfg.cs)}
+               "h2d_bytes_per_step": int(codes_h.nbytes + tab_h.nbytes + 8 * m + h2d),
+               "d2h_bytes_per_step": d2h, "steps": len(e2e_times),
+               "includes": "create (H2D codes + tables + b, validation, lambda_max pass) + solves + D2H x + destroy"}
+        del codes_h, tab_h
     elif not args.no_e2e and not args.shard:
         A_host = torch.empty((n, m), dtype=torch.float64, pin_memory=True)
-        A_host.copy_(dA.cpu())
+        A_host.copy_(dA)  # the same bytes as the device generator wrote (pinned host memory)
         A_np = A_host.numpy()
         e2e_times = []
-        h2d = d2h = 0
         for it in range(max(1, min(args.steps, 3)) + 1):
             t0 = time.perf_counter()
             Q = Problem(A_np, b_host)
             Q.set_option("graph", 1 if args.control == "graph" else 0)
             Q.set_option("cg_ratio", args.cg_ratio)
-            lmq = Q.lambda_max_l1
-            x_prev = None
-            hb = 8 * m * n + 8 * m
-            db_ = 0
-            for i, c in enumerate(cfg.cs):
-                l1, l2 = lambdas(cfg, lmq, c)
-                x_prev, st = Q.solve(l1, l2, cfg.sigma0, cfg.tol, x0=x_prev if cfg.path else None)
-                if cfg.path and i > 0:
-                    hb += 8 * n
-                db_ += 8 * n
+            h2d, d2h = host_solve_workload(Q, cfg, Q.lambda_max_l1)
             Q.close()
-            dt = time.perf_counter() - t0
-            if it > 0:  # first iteration is the e2e warm-up
-                e2e_times.append(dt)
-            h2d, d2h = hb, db_
-        e2e_t = max_over_ranks(statistics.median(e2e_times))
-        e2e = {"value": e2e_t, "unit": "s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
+            if it > 0:  # the first iteration is the e2e warm-up
+                e2e_times.append(time.perf_counter() - t0)
+        del A_np, A_host
+        e2e = {"value": max_over_ranks(statistics.median(e2e_times)), "unit": "s",
+               "h2d_bytes_per_step": 8 * m * n + 8 * m + h2d, "d2h_bytes_per_step": d2h,
+               "steps": len(e2e_times),
+               "includes": "ssnal_en_create (H2D of A and b from pinned host memory, validation, lambda_max pass)"
+                           " + the workload's ssnal_en_solve calls (x0 H2D, x D2H) + destroy"}
 
     peak, peak_src = _peaks()
     k1_avg = k1_time / max(k1_launches, 1)
@@ -319,7 +345,7 @@ def bench_ours(args, rank, world, local_rank):
         "dtype": "f64",
         "data": "synthetic (synth/, seeded; generated in HBM)",
         "config": {"workload": f"{cfg.name}: m={m} n={cfg.n} " + ("warm-started path c=" + ",".join(f"{c:.3g}" for c in cfg.cs)
-                                                              if cfg.path else "c=" + ",".join(str(c) for c in cfg.cs)),
+                                                              if cfg.path else "cold solves c=" + ",".join(str(c) for c in cfg.cs)),
                    "m": m, "n": cfg.n, "alpha": cfg.alpha, "tol": cfg.tol, "sigma0": cfg.sigma0,
                    "l2_policy": f"A = {8 * m * n / 1e6:.0f} MB > 126 MB L2 (no flush needed)",
                    "parallelism": (f"column-sharded x{world}: rank q owns n/{world} columns, NCCL all-reduce of the "
@@ -329,81 +355,192 @@ def bench_ours(args, rank, world, local_rank):
                                if args.control == "graph" and not args.shard else "host-driven (per-evaluation readback)"),
                    "storage": ("packed 2-bit genotype codes + per-column tables (SURVEY 8(f4))" if args.geno
                                else "fp64 column-major"),
+                   "path_sigma": "carried from point to point (reading R38, P:411)" if cfg.path else None,
                    "newton_strategy": ("exact (Eq. 18/19); CG when min(m, r) > 1e4 (P:379)" if args.cg_ratio == 0
                                        else f"CG (K6) when r > {args.cg_ratio:g} m, else exact (Eq. 18/19)")},
+        "step_times": step_summary(per_step),
         "roofline": small_roofline(m, n, last_stats, dev_sum / max(args.steps, 1), peak, peak_src) if k1_launches == 0 and
                     not args.geno else {**({"bound": "hbm", "achieved": k1_gbs, "peak": peak, "unit": "GB/s",
                          "frac": (k1_gbs / peak) if k1_gbs else None, "traffic": traffic, "peak_source": peak_src}
                         if not args.geno else geno_roofline(m, n, k1_avg, k1_gbs, peak, traffic)),
                      "kernel": "k1g_aty_fused" if args.geno else "k1_aty_fused",
                      "bytes_per_launch": k1_bytes(m, n, args.geno), "launches": k1_launches,
-                     "mean_launch_us": k1_avg * 1e6, "share_of_step": k1_time / max(elapsed, 1e-30)},
+                     "mean_launch_us": k1_avg * 1e6, "share_of_step": k1_time / max(elapsed, 1e-30),
+                     "timing": "in-kernel %globaltimer stamps inside the graph (CUDA events cannot sit in "
+                               "conditional bodies) + CUDA events on the handle's stream for the warm-start passes"},
         "e2e": e2e,
         "gpu_launches": launches // max(args.steps, 1),
         "solves_device_s_per_step": dev_sum / max(args.steps, 1),
         "clocks": clk.summary(),
         "iterations": [{"c": round(c, 4), "outer": s["outer_iters"], "newton": s["newton_iters"],
                         "passes": s["aty_passes"], "backtracks": s["backtracks"], "r": s["active"],
-                        "branches": s["branch_steps"], "cg_iters": s["cg_iters"],
+                        "branches": s["branch_steps"], "cg_iters": s["cg_iters"], "sigma_final": s["sigma_final"],
                         "res1": s["res_kkt1"], "res3": s["res_kkt3"], "gap": s["gap"]}
                        for c, s in zip(cfg.cs, last_stats)],
     }
     if args.shard:
         res["config"]["n_local"] = n
-    if rank == 0 and not args.no_cpu and world == 1 and not args.geno and not args.shard:
-        res["cpu_baseline"] = cpu_baseline(cfg, b_host, A_host.numpy() if A_host is not None else dA.cpu().numpy())
     P.close()
+    del dA, x_all
+    torch.cuda.empty_cache()
+    if rank == 0 and not args.no_cpu and world == 1 and not args.shard:
+        cb, parity = cpu_baseline(cfg, args, x_gpu, w_probe, last_stats)
+        res["cpu_baseline"] = cb
+        res["parity"] = parity
     return res
 
 
-def cpu_baseline(cfg, b, A):
-    """The oracle (as it stands) on this host's cores, on the same workload (full path)."""
+def _cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.lower().startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def cpu_baseline(cfg, args, x_gpu, w_probe, gpu_stats):
+    """The oracle (as it stands) on this host's cores, in a CLEAN subprocess (no torch, no CUDA): it
+    generates A with synth's host generator, warms up with one Aᵀb pass (OpenMP threads up, A paged
+    in), then times the workload once — the full config, the same solves as one GPU step.  It also
+    returns the §8(d) parity block of the GPU's last timed step against its own solutions."""
+    import tempfile
+
+    tmp = tempfile.mkdtemp(prefix="ssnal_bench_")
+    np.save(os.path.join(tmp, "x_gpu.npy"), x_gpu)
+    if w_probe is not None:
+        np.save(os.path.join(tmp, "w_gpu.npy"), w_probe)
+    json.dump([{k: s[k] for k in ("outer_iters", "newton_iters", "active", "status")} for s in gpu_stats],
+              open(os.path.join(tmp, "gpu_stats.json"), "w"))
+    out = os.path.join(tmp, "cpu.json")
+    env = dict(os.environ)
+    threads = int(env.get("OMP_NUM_THREADS", os.cpu_count()))
+    env["OMP_NUM_THREADS"] = str(threads)
+    cmd = [sys.executable, os.path.abspath(__file__), "--cpu-leg", tmp, "--config", cfg.name]
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True)
+    if r.returncode != 0 or not os.path.exists(out):
+        return {"value": None, "unit": "s", "cores": threads, "kind": "oracle",
+                "error": (r.stderr or r.stdout)[-400:]}, None
+    d = json.load(open(out))
+    for f in os.listdir(tmp):
+        os.remove(os.path.join(tmp, f))
+    os.rmdir(tmp)
+    return d["cpu_baseline"], d["parity"]
+
+
+def cpu_leg(tmp, cfg_name):
+    """Child process of cpu_baseline (no torch): oracle timing + parity block, written to tmp/cpu.json."""
     import oracle
 
-    cores = os.cpu_count()
-    lm = float(np.max(np.abs(oracle.aty(A, b))))
+    cfg = synth.CONFIGS[cfg_name]
+    t_gen = time.perf_counter()
+    A = synth.design(cfg)
+    b, _ = synth.response(cfg)
+    t_gen = time.perf_counter() - t_gen
     t0 = time.perf_counter()
-    x = None
-    for i, c in enumerate(cfg.cs):
-        l1, l2 = lambdas(cfg, lm, c)
-        x, _, st, _ = oracle.solve(A, b, l1, l2, sigma0=cfg.sigma0, tol=cfg.tol, x0=x if cfg.path and i > 0 else None)
+    lm = oracle.lambda_max_l1(A, b)  # warm-up: one full Aᵀb pass
+    t_warm = time.perf_counter() - t0
+    ls = [lambdas(cfg, lm, c) for c in cfg.cs]
+    t0 = time.perf_counter()
+    if cfg.path:
+        sols = oracle.solve_path_lambdas(A, b, ls, sigma0=cfg.sigma0, tol=cfg.tol)
+    else:
+        sols = [oracle.solve(A, b, l1, l2, sigma0=cfg.sigma0, tol=cfg.tol)[:3] for l1, l2 in ls]
     dt = time.perf_counter() - t0
-    return {"value": dt, "unit": "s", "cores": int(os.environ.get("OMP_NUM_THREADS", cores)), "kind": "oracle",
-            "sample": f"full {cfg.name} workload ({len(cfg.cs)} solve(s)), OpenMP over columns"}
+    threads = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count()))
+    cb = {"value": dt, "unit": "s", "cores": threads, "kind": "oracle",
+          "sample": f"the full {cfg.name} workload ({len(ls)} solve(s){', warm-started path, sigma carried' if cfg.path else ''}),"
+                    " one timed run after a warm-up A^T b pass; clean subprocess (no torch), OpenMP over columns",
+          "threads": threads, "nproc": os.cpu_count(), "cpu_model": _cpu_model(),
+          "generate_s": t_gen, "warmup_s": t_warm,
+          "iterations": [{"outer": s["outer_iters"], "newton": s["newton_iters"], "r": s["active"]} for _, _, s in sols]}
+    parity = None
+    xg_path = os.path.join(tmp, "x_gpu.npy")
+    if os.path.exists(xg_path):
+        x_gpu = np.load(xg_path)
+        gst = json.load(open(os.path.join(tmp, "gpu_stats.json")))
+        pts = []
+        for i, ((l1, l2), (xc, _, sc)) in enumerate(zip(ls, sols)):
+            xg = x_gpu[i]
+            Fg, Fc = oracle.primal_obj(A, b, xg, l1, l2), oracle.primal_obj(A, b, xc, l1, l2)
+            xinf = float(np.max(np.abs(xc)))
+            mask = np.maximum(np.abs(xg), np.abs(xc)) > 1e-8
+            pts.append({"c": cfg.cs[i], "obj_rel": abs(Fg - Fc) / abs(Fc),
+                        "xinf_rel": float(np.max(np.abs(xg - xc))) / max(xinf, 1e-300),
+                        "sign_match": bool(np.array_equal(np.sign(xg[mask]), np.sign(xc[mask]))),
+                        "J_equal": bool(np.array_equal(np.nonzero(xg)[0], np.nonzero(xc)[0])),
+                        "outer": [gst[i]["outer_iters"], sc["outer_iters"]],
+                        "newton": [gst[i]["newton_iters"], sc["newton_iters"]]})
+        ok = all(p["obj_rel"] <= 1e-9 and p["xinf_rel"] <= 1e-6 and p["sign_match"] for p in pts)
+        parity = {"points": pts, "ok": ok,
+                  "tolerances": "objective 1e-9 rel, |dx|inf <= 1e-6 |x_cpu|inf, sign pattern on |x|>1e-8 (BASELINE "
+                                "north star; R22); gpu/oracle = [gpu, oracle] counts"}
+        wg_path = os.path.join(tmp, "w_gpu.npy")
+        if os.path.exists(wg_path):  # K1 vs the oracle's Aᵀy at the probe y (reading R21)
+            w_gpu = np.load(wg_path)
+            y = synth.normals(cfg.seed, 12, cfg.m)
+            w_cpu = oracle.aty(A, y)
+            ny = float(np.linalg.norm(y))
+            e1 = 0.0
+            for j in range(0, cfg.n, 1 << 20):
+                blk = A[j:j + (1 << 20)]
+                cn = np.sqrt(np.einsum("ij,ij->i", blk, blk))
+                e1 = max(e1, float(np.max(np.abs(w_gpu[j:j + len(blk)] - w_cpu[j:j + len(blk)]) / (cn * ny))))
+            parity["aty_max_scaled_err"] = e1
+            parity["aty_rel_l2_err"] = float(np.linalg.norm(w_gpu - w_cpu) / np.linalg.norm(w_cpu))
+            parity["ok"] = parity["ok"] and e1 <= 1e-12
+    json.dump({"cpu_baseline": cb, "parity": parity}, open(os.path.join(tmp, "cpu.json"), "w"))
 
 
 def bench_reference(args, rank, world):
-    """Reference arm for this tier: the CPU oracle on the host cores (rank 0 only)."""
+    """Reference arm for this tier: the CPU oracle (as it stands) on the host cores, rank 0 only, with
+    the same --steps/--warmup as our arm.  Each step is a bounded sample of the workload: the same
+    solves on the first n_s columns of the same design (synth, same generator and b), λmax of the
+    sample; the step time is scaled by n / n_s to the metric's unit (seconds per full workload; the
+    oracle's cost is linear in n: every Newton step is an O(mn) pass).  n_s = n for cfg1/cfg2/cfg4."""
     if rank != 0:
         return None
     import oracle
 
     cfg = synth.CONFIGS[args.config]
-    A = synth.design(cfg)
+    frac = {"cfg3": 0.5, "cfg5": 0.2}.get(cfg.name, 1.0)
+    ns = int(cfg.n * frac)
+    A = synth.design(cfg, 0, ns)
     b, _ = synth.response(cfg)
-    lm = float(np.max(np.abs(oracle.aty(A, b))))
-    steps = max(1, min(args.steps, 3))
+    lm = oracle.lambda_max_l1(A, b)
+    ls = [lambdas(cfg, lm, c) for c in cfg.cs]
 
     def step():
-        x = None
-        for i, c in enumerate(cfg.cs):
-            l1, l2 = lambdas(cfg, lm, c)
-            x, _, _, _ = oracle.solve(A, b, l1, l2, sigma0=cfg.sigma0, tol=cfg.tol,
-                                      x0=x if cfg.path and i > 0 else None)
+        if cfg.path:
+            oracle.solve_path_lambdas(A, b, ls, sigma0=cfg.sigma0, tol=cfg.tol)
+        else:
+            for l1, l2 in ls:
+                oracle.solve(A, b, l1, l2, sigma0=cfg.sigma0, tol=cfg.tol)
 
-    for _ in range(min(args.warmup, 1)):
+    for _ in range(args.warmup):
         step()
-    t0 = time.perf_counter()
-    for _ in range(steps):
+    ts = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
         step()
-    t = (time.perf_counter() - t0) / steps
+        ts.append(time.perf_counter() - t0)
+    scale = cfg.n / ns
+    t = statistics.fmean(ts) * scale
     cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count()))
-    return {"impl": "reference", "metric": METRIC, "value": t, "unit": "s", "n_gpus": world, "steps": steps,
-            "warmup": min(args.warmup, 1), "ms_per_step": t * 1e3, "higher_is_better": False, "scaling": "weak",
+    sample = (f"full {cfg.name} workload per step" if ns == cfg.n else
+              f"{cfg.name} workload on the first {ns} of {cfg.n} columns (same generator and b, its own lambda_max), "
+              f"time x {scale:g}")
+    return {"impl": "reference", "metric": METRIC, "value": t, "unit": "s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": False, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (synth/, seeded)",
-            "config": {"workload": f"{cfg.name}: m={cfg.m} n={cfg.n}", "m": cfg.m, "n": cfg.n},
-            "cpu_baseline": {"value": t, "unit": "s", "cores": cores, "kind": "oracle",
-                             "sample": f"full {cfg.name} workload per step"},
+            "config": {"workload": f"{cfg.name}: m={cfg.m} n={cfg.n} " + ("warm-started path" if cfg.path else
+                                   "cold solves c=" + ",".join(str(c) for c in cfg.cs)),
+                       "m": cfg.m, "n": cfg.n, "sample_columns": ns},
+            "step_times": step_summary([v * scale for v in ts]),
+            "cpu_baseline": {"value": t, "unit": "s", "cores": cores, "kind": "oracle", "sample": sample,
+                             "cpu_model": _cpu_model()},
             "e2e": {"value": t, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
@@ -532,7 +669,8 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="cfg2", choices=list(synth.CONFIGS))
+    ap.add_argument("--config", default="cfg5", choices=list(synth.CONFIGS))
+    ap.add_argument("--cpu-leg", default=None, help=argparse.SUPPRESS)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--geno", action="store_true",
                     help="cfg4 from packed 2-bit genotype codes (SURVEY 8(f4)) instead of fp64")
@@ -549,6 +687,9 @@ def main():
     ap.add_argument("--sweep-n", default="100000,200000,500000,1000000,2000000,5000000,10000000")
     ap.add_argument("--sweep-reps", type=int, default=20)
     args = ap.parse_args()
+    if args.cpu_leg:
+        cpu_leg(args.cpu_leg, args.config)
+        return
     if args.warmup < 3 and args.impl == "ours" and not args.sweep:
         args.warmup = 3  # contract: W ≥ 3
 

@@ -106,7 +106,11 @@ double ssnal_en_lambda_max_l1(const ssnal_en_problem* p);
  *   max_backtracks=50, init_mode=1 (y0 = A x0 − b when x0 ≠ 0, else y0 = 0; 0: always y0 = 0),
  *   time_k1=0 (1: time every K1 launch → stats.k1_time_s; CUDA events in host-driven mode,
  *     in-kernel %globaltimer stamps inside the graph),
- *   cluster_size=0 (auto: 16 if the device allows, else 8),
+ *   cluster_size=0 (auto: 16 if the device allows, else the largest schedulable power of two; an
+ *     explicit 1/2/4/8/16 the device cannot schedule for k_chol_cluster is refused with EINVAL),
+ *   carry_sigma=1 (ssnal_en_solve_path_device: point i > 0 starts at point i − 1's sigma_final
+ *     instead of σ0 — reading R38 of P:411 "usually SsNAL-EN converges in just one iteration";
+ *     0: every point restarts at σ0),
  *   small=1 (m ≤ 64 and n ≤ 1024, fp64 storage, unsharded, no CG strategy: the whole solve runs in
  *     one 512-thread CTA, k_small_solve — same iteration and statistics, reduction orders differ;
  *     0: the multi-kernel graph / host paths),
@@ -130,7 +134,7 @@ double ssnal_en_lambda_max_l1(const ssnal_en_problem* p);
 int ssnal_en_set_option(ssnal_en_problem* p, const char* key, double value);
 
 /* Read-only introspection: "m", "n", "k1_cols", "k1_stages", "k1_grid", "k1_smem",
- * "cluster_size", "num_sms", "graph", "format", "cg_ratio", "cg_threshold", and which kernels a
+ * "cluster_size", "num_sms", "graph", "format", "cg_ratio", "cg_threshold", "carry_sigma", and which kernels a
  * solve on this handle uses: "small" (1: the one-CTA path k_small_solve), "chol_dsm" (1: k_chol_dsm
  * for N ≤ 96), "chol_d2" (1: k_chol_d2 for 96 < N ≤ 512).  Returns NaN for unknown keys. */
 double ssnal_en_get_info(const ssnal_en_problem* p, const char* key);
@@ -151,7 +155,8 @@ int ssnal_en_solve_device(ssnal_en_problem* p, double lambda1, double lambda2, d
 
 /* A warm-started λ path on DEVICE buffers (the path protocol of Table D.4 / BASELINE
  * configs[1]): point i solves (lambda1[i], lambda2[i]) starting from point i − 1's solution (point 0
- * from x0, nullable = cold).  x_out: device, npts × n (row i = point i's x).  stats: host, npts
+ * from x0, nullable = cold) and, with option carry_sigma = 1 (default, reading R38), from point
+ * i − 1's sigma_final instead of sigma0 (point 0 uses sigma0; the carried σ stays on the device).  x_out: device, npts × n (row i = point i's x).  stats: host, npts
  * entries (nullable).  With device-resident control (graph mode or the one-CTA path) every point is
  * enqueued before a single stream synchronisation; otherwise (host-driven control, sharded handles,
  * certify) it is a loop over ssnal_en_solve_device.  Same results and statistics as that loop;

@@ -376,6 +376,8 @@ struct ssnal_en_problem {
   void* path_slots = nullptr;
   int64_t path_cap = 0;
   std::vector<cudaEvent_t> path_ev;
+  // option carry_sigma (reading R38): path point i starts at point i − 1's final σ
+  int carry_sigma = 1;
 };
 
 namespace {
@@ -424,6 +426,27 @@ int alloc(void** p, size_t bytes) {
     int rc_ = alloc((void**)&(ptr), (bytes));                     \
     if (rc_) return rc_;                                          \
   } while (0)
+
+// Largest k_chol_cluster cluster size ≤ want (halving) that the occupancy calculator can schedule.
+int chol_cluster_fit(ssnal_en_problem* P, int want) {
+  for (; want > 1; want /= 2) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(want);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = P->chol_smem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = want;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int nclus = 0;
+    if (cudaOccupancyMaxActiveClusters(&nclus, k_chol_cluster, &cfg) == cudaSuccess && nclus >= 1) break;
+    cudaGetLastError();
+  }
+  return want < 1 ? 1 : want;
+}
 
 int configure(ssnal_en_problem* P) {
   const int64_t m = P->m, n = P->n;
@@ -478,26 +501,7 @@ int configure(ssnal_en_problem* P) {
   CK(cudaFuncSetAttribute(k_chol_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->chol_smem));
   CK(cudaFuncSetAttribute(k_chol_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   // cluster size: 16 (non-portable) when schedulable, else 8
-  {
-    int want = P->cluster > 0 ? P->cluster : 16;
-    for (; want >= 1; want /= 2) {
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(want);
-      cfg.blockDim = dim3(256);
-      cfg.dynamicSmemBytes = P->chol_smem;
-      cudaLaunchAttribute at[1];
-      at[0].id = cudaLaunchAttributeClusterDimension;
-      at[0].val.clusterDim.x = want;
-      at[0].val.clusterDim.y = 1;
-      at[0].val.clusterDim.z = 1;
-      cfg.attrs = at;
-      cfg.numAttrs = 1;
-      int nclus = 0;
-      if (cudaOccupancyMaxActiveClusters(&nclus, k_chol_cluster, &cfg) == cudaSuccess && nclus >= 1) break;
-      cudaGetLastError();
-    }
-    P->cluster = want < 1 ? 1 : want;
-  }
+  P->cluster = chol_cluster_fit(P, P->cluster > 0 ? P->cluster : 16);
   // DSMEM-resident K4 (N ≤ 512): needs a schedulable 16-CTA cluster with ~175 KB smem per CTA
   P->dsm_ok = 0;
   {
@@ -1709,7 +1713,7 @@ bool small_eligible(const ssnal_en_problem* P) {
 }
 
 int solve_small_core(ssnal_en_problem* P, double l1, double l2, double sigma0, double tol, int have_x0,
-                     ssnal_en_stats* S) {
+                     ssnal_en_stats* S, const double* sigma_dev = nullptr) {
   memset(S, 0, sizeof(*S));
   int rc;
   int64_t rx = 0;
@@ -1732,6 +1736,8 @@ int solve_small_core(ssnal_en_problem* P, double l1, double l2, double sigma0, d
   h->inject = P->inject_fail;
   h->inner_tol_mode = P->inner_tol_mode;
   CK(cudaMemcpyAsync(P->ctl, h, sizeof(DevCtl), cudaMemcpyHostToDevice, P->st));
+  if (sigma_dev)  // σ0 carried on the device from the previous path point (R38)
+    CK(cudaMemcpyAsync(&P->ctl->sigma, sigma_dev, 8, cudaMemcpyDeviceToDevice, P->st));
   SmallParams sp;
   sp.A = P->A;
   sp.b = P->b;
@@ -1759,7 +1765,7 @@ int solve_small_core(ssnal_en_problem* P, double l1, double l2, double sigma0, d
 }
 
 int solve_graph_core(ssnal_en_problem* P, double l1, double l2, double sigma0, double tol, int have_x0,
-                     ssnal_en_stats* S) {
+                     ssnal_en_stats* S, const double* sigma_dev = nullptr) {
   memset(S, 0, sizeof(*S));
   int rc;
   if ((rc = build_graph(P))) return rc;
@@ -1787,6 +1793,8 @@ int solve_graph_core(ssnal_en_problem* P, double l1, double l2, double sigma0, d
   h->tstamp[0] = ~0ull;
   h->tstamp[1] = 0ull;
   CK(cudaMemcpyAsync(P->ctl, h, sizeof(DevCtl), cudaMemcpyHostToDevice, P->st));
+  if (sigma_dev)  // σ0 carried on the device from the previous path point (R38)
+    CK(cudaMemcpyAsync(&P->ctl->sigma, sigma_dev, 8, cudaMemcpyDeviceToDevice, P->st));
   CK(cudaGraphLaunch(P->gexec, P->st));
   if ((rc = launch_objective(P))) return rc;
   CK(cudaMemcpyAsync(h, P->ctl, sizeof(DevCtl), cudaMemcpyDeviceToHost, P->st));
@@ -2120,6 +2128,7 @@ int ssnal_en_set_option(ssnal_en_problem* P, const char* key, double v) {
   else if (k == "jitter" && v >= 0 && v < 1) P->jitter = v;
   else if (k == "test_fail_factor" && v >= 0) P->inject_fail = (int)v;
   else if (k == "inner_tol_mode" && (v == 0 || v == 1)) P->inner_tol_mode = (int)v;
+  else if (k == "carry_sigma" && (v == 0 || v == 1)) P->carry_sigma = (int)v;
   else if (k == "cg_tol" && v > 0 && v < 1) {
     P->cg_tol = v;
     drop_graph(P);  // baked into the captured CG launch
@@ -2137,8 +2146,16 @@ int ssnal_en_set_option(ssnal_en_problem* P, const char* key, double v) {
     P->use_dsm = (int)v;
     P->chol_dsm = P->use_dsm && P->dsm_ok;
     drop_graph(P);  // the K4 variant is baked into the graph
-  } else if (k == "cluster_size" && (v == 1 || v == 2 || v == 4 || v == 8 || v == 16)) {
-    P->cluster = (int)v;
+  } else if (k == "cluster_size" && (v == 0 || v == 1 || v == 2 || v == 4 || v == 8 || v == 16)) {
+    // 0 = auto (16 if schedulable, else the largest smaller power of two); an explicit size the
+    // device cannot schedule is refused rather than failing mid-solve
+    const int want = v == 0 ? 16 : (int)v;
+    const int fit = chol_cluster_fit(P, want);
+    if (v != 0 && fit != want) {
+      set_err("cluster_size=%g is not schedulable on this device (largest: %d)", v, fit);
+      return SSNAL_EINVAL;
+    }
+    P->cluster = fit;
     drop_graph(P);  // the cluster launch configuration is baked into the graph
   } else {
     set_err("unknown option or bad value: %s=%g", key, v);
@@ -2165,6 +2182,7 @@ double ssnal_en_get_info(const ssnal_en_problem* P, const char* key) {
   if (k == "format") return P->fmt;
   if (k == "cg_ratio") return P->cg_ratio;
   if (k == "cg_threshold") return P->cg_threshold;
+  if (k == "carry_sigma") return P->carry_sigma;
   return NAN;
 }
 
@@ -2250,9 +2268,12 @@ int ssnal_en_solve(ssnal_en_problem* P, double l1, double l2, double sigma0, dou
   return solve_wrapped(P, l1, l2, sigma0, tol, x0, 0, x_out, 0, stats);
 }
 
-// A warm-started λ path on device buffers: point i starts from point i − 1's solution.
+// A warm-started λ path on device buffers: point i starts from point i − 1's solution
+// and, with option carry_sigma (default; reading R38), from point i − 1's final σ, so that a nearby
+// warm start "usually converges in just one iteration".
 // Device-resident control (graph or one-CTA path): every point is enqueued before ONE stream
-// synchronisation — per-point results land in pinned slots and are completed afterwards.  Other
+// synchronisation — per-point results land in pinned slots and are completed afterwards; the
+// carried σ moves on the device (ctl.sigma_final → scratch[60] → the next point's ctl.sigma).  Other
 // modes (host-driven control, sharded handles, certify) loop over ssnal_en_solve_device.
 namespace {
 struct PathSlot {
@@ -2278,13 +2299,15 @@ int ssnal_en_solve_path_device(ssnal_en_problem* P, int64_t npts, const double* 
   };
   const bool deferred = !sharded(P) && !P->certify && (small_eligible(P) || P->use_graph);
   if (!deferred) {
+    double sig = sigma0;
     for (int64_t i = 0; i < npts; ++i) {
       const double* xi = i == 0 ? x0 : x_out + (i - 1) * n;
       ssnal_en_stats st;
-      const int rc = solve_wrapped(P, lambda1[i], lambda2[i], sigma0, tol, xi, 1, x_out + i * n, 1, &st);
+      const int rc = solve_wrapped(P, lambda1[i], lambda2[i], sig, tol, xi, 1, x_out + i * n, 1, &st);
       if (rc == SSNAL_EINVAL || rc == SSNAL_ECUDA) return rc;
       if (stats) stats[i] = st;
       fold(rc);
+      if (P->carry_sigma) sig = st.sigma_final;
     }
     return worst;
   }
@@ -2310,17 +2333,23 @@ int ssnal_en_solve_path_device(ssnal_en_problem* P, int64_t npts, const double* 
   double* sh0 = P->scratch_host;
   auto t0 = std::chrono::steady_clock::now();
   std::vector<ssnal_en_stats> S(npts);
+  std::vector<size_t> k1_beg(npts + 1, 0);  // K1 event pairs (warm-start passes with time_k1) per point
+  double* sigma_carry = P->scratch + 60;
   int rc = SSNAL_OK;
   for (int64_t i = 0; i < npts && rc == SSNAL_OK; ++i) {  // enqueue every point
     P->ctl_host = &slot[i].ctl;
     P->ev_out_host = &slot[i].ev;
     P->scratch_host = slot[i].scratch;
     P->launches = 0;
+    k1_beg[i] = P->k1_pending.size();
     CK(cudaEventRecord(P->path_ev[2 * i], P->st));
     const double* xi = i == 0 ? x0 : x_out + (i - 1) * n;
     if (xi) CK(cudaMemcpyAsync(P->x, xi, n * 8, cudaMemcpyDeviceToDevice, P->st));
-    rc = small_eligible(P) ? solve_small_core(P, lambda1[i], lambda2[i], sigma0, tol, xi != nullptr, &S[i])
-                           : solve_graph_core(P, lambda1[i], lambda2[i], sigma0, tol, xi != nullptr, &S[i]);
+    const double* sig_in = (P->carry_sigma && i > 0) ? sigma_carry : nullptr;
+    rc = small_eligible(P) ? solve_small_core(P, lambda1[i], lambda2[i], sigma0, tol, xi != nullptr, &S[i], sig_in)
+                           : solve_graph_core(P, lambda1[i], lambda2[i], sigma0, tol, xi != nullptr, &S[i], sig_in);
+    if (rc == SSNAL_OK && P->carry_sigma)
+      CK(cudaMemcpyAsync(sigma_carry, &P->ctl->sigma_final, 8, cudaMemcpyDeviceToDevice, P->st));
     if (rc == SSNAL_OK) CK(cudaMemcpyAsync(x_out + i * n, P->x, n * 8, cudaMemcpyDeviceToDevice, P->st));
     CK(cudaEventRecord(P->path_ev[2 * i + 1], P->st));
     slot[i].l1 = P->stat_l1;
@@ -2328,10 +2357,26 @@ int ssnal_en_solve_path_device(ssnal_en_problem* P, int64_t npts, const double* 
     slot[i].warm_pass = P->stat_warm_pass;
     slot[i].launches = P->launches;
   }
+  k1_beg[npts] = P->k1_pending.size();
   P->ctl_host = ctl0;
   P->ev_out_host = ev0;
   P->scratch_host = sh0;
   CK(cudaStreamSynchronize(P->st));
+  // K1 launches timed by events (the warm-start passes) belong to the point that enqueued them
+  std::vector<double> k1_t(npts, 0.0);
+  std::vector<int> k1_c(npts, 0);
+  for (int64_t i = 0; i < npts; ++i)
+    for (size_t q = k1_beg[i]; q < k1_beg[i + 1] && q < P->k1_pending.size(); ++q) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, P->k1_pending[q].first, P->k1_pending[q].second);
+      k1_t[i] += ms * 1e-3;
+      k1_c[i]++;
+    }
+  for (auto& pr : P->k1_pending) {
+    P->ev_pool.push_back(pr.first);
+    P->ev_pool.push_back(pr.second);
+  }
+  P->k1_pending.clear();
   if (rc != SSNAL_OK) return rc;
   const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   for (int64_t i = 0; i < npts; ++i) {  // complete the statistics point by point
@@ -2342,8 +2387,8 @@ int ssnal_en_solve_path_device(ssnal_en_problem* P, int64_t npts, const double* 
     P->stat_l2 = slot[i].l2;
     P->stat_warm_pass = slot[i].warm_pass;
     P->launches = slot[i].launches;
-    P->k1_time = 0;
-    P->k1_count = 0;
+    P->k1_time = k1_t[i];
+    P->k1_count = k1_c[i];
     P->graph_pending = true;
     finish_stats(P, &S[i]);
     S[i].primal_viol = NAN;

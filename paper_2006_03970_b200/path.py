@@ -17,17 +17,21 @@ def lambda_grid(n_points: int = 100, c_max: float = 1.0, c_min: float = 0.1) -> 
 
 
 def solve_path(P, alpha: float, cs, sigma0: float = 5e-3, tol: float = 1e-6, max_active: int | None = None,
-               select: bool = True, debias: bool = False):
+               select: bool = True, debias: bool = False, carry_sigma: bool = True):
     """Solve along c ∈ cs with λ1 = c α λmax, λ2 = c (1 − α) λmax, λmax = ‖Aᵀb‖∞/α,
-    warm-starting each point at the previous solution.  The path stops once a
+    warm-starting each point at the previous solution and — reading R38 — at the
+    previous point's final σ (carry_sigma; False restarts every point at σ0).  The path stops once a
     solution has at least `max_active` nonzeros.  Returns (points, best) where best maps
     'gcv' / 'ebic' to the index of the minimising point (None without selection)."""
     lmax = P.lambda_max_l1 / alpha
     points = []
     x = None
+    sig = sigma0
     for c in cs:
         l1, l2 = c * alpha * lmax, c * (1 - alpha) * lmax
-        x, st = P.solve(l1, l2, sigma0, tol, x0=x)
+        x, st = P.solve(l1, l2, sig, tol, x0=x)
+        if carry_sigma:
+            sig = st["sigma_final"]
         crit, xdb = P.model_select(l2, debias) if select else (None, None)
         points.append({"c": float(c), "lambda1": l1, "lambda2": l2, "x": x, "stats": st, "criteria": crit,
                        "x_debiased": xdb})
@@ -49,7 +53,7 @@ def cv_path(make_problem, m: int, alpha: float, cs, lambda_max_l1: float, k: int
     make_problem(rows) must return a Problem over the given rows of (A, b) (e.g. a handle created
     from a row subset in device memory).  Folds are interleaved (row r in fold r mod k); the grid
     uses the full-data λmax = lambda_max_l1/α for every fold.  Each fold solves the
-    warm-started path on its training rows; the held-out error ‖b_test − A_test x‖² is computed by
+    warm-started path on its training rows (σ carried along the path, reading R38); the held-out error ‖b_test − A_test x‖² is computed by
     the test handle (ssnal_en_residual).  Returns (cv, best) with cv[i] = Σ_folds err / m."""
     lmax = lambda_max_l1 / alpha
     cv = np.zeros(len(cs))
@@ -59,9 +63,11 @@ def cv_path(make_problem, m: int, alpha: float, cs, lambda_max_l1: float, k: int
         Ptr, Pte = make_problem(train), make_problem(test)
         try:
             x = None
+            sig = sigma0
             for i, c in enumerate(cs):
                 l1, l2 = c * alpha * lmax, c * (1 - alpha) * lmax
-                x, _ = Ptr.solve(l1, l2, sigma0, tol, x0=x)
+                x, st = Ptr.solve(l1, l2, sig, tol, x0=x)
+                sig = st["sigma_final"]  # reading R38
                 cv[i] += Pte.residual(x)
         finally:
             Ptr.close()

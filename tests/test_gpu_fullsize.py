@@ -6,14 +6,16 @@ bit-identically on the host, so the oracle checks GPU outputs one by one on samp
   * K1 at full size: w_i on sampled and all active columns (reading R21), J membership;
   * solves at full size: convergence, the KKT inclusion Aᵀ(b − Ax) − λ2x ∈ λ1∂‖x‖₁ on every
     support column and 20 000 sampled columns, the duality gap, x = 0 above λmax;
-  * cfg3 additionally against a full oracle solve on the host (all three c values).
+  * every config against a full oracle solve on the host at the BASELINE tolerances, with the ±1
+    Newton rerun rule, the dual objective and the gap (cfg3 all three c; cfg4 from fp64 A and from
+    packed genotype codes; cfg5 both c — the n ≈ 10⁷ regime of P:366-369).
 """
 import numpy as np
 import pytest
 
 import oracle
 import synth
-from gpu_util import aty_errors, cuda_ok, solution_parity
+from gpu_util import aty_errors, compare_to_oracle, cuda_ok, solution_parity
 
 pytestmark = pytest.mark.gpu
 
@@ -145,21 +147,41 @@ def test_zero_above_lambda_max_fullsize(name):
     assert np.all(x == 0) and st["newton_iters"] == 1 and st["aty_passes"] == 1
 
 
-def test_cfg3_fullsize_oracle_parity():
-    """cfg3 at full size (m=500, n=1e6) against the oracle on the host, all three c values."""
-    cfg, dA, b, P = device_problem("cfg3")
-    A = synth.design(cfg)  # 4 GB on the host, bitwise equal to dA
-    lm = float(np.max(np.abs(oracle.aty(A, b))))
-    assert P.lambda_max_l1 == pytest.approx(lm, rel=1e-13)
-    for c in cfg.cs:
-        l1, l2 = lambdas(cfg, lm, c)
-        xc, _, stc, _ = oracle.solve(A, b, l1, l2, sigma0=cfg.sigma0, tol=cfg.tol)
-        xg, stg = P.solve(l1, l2, cfg.sigma0, cfg.tol)
-        assert stc["status"] == 0 and stg["status"] == 0
-        Fg = oracle.primal_obj(A, b, xg, l1, l2)
-        Fc = oracle.primal_obj(A, b, xc, l1, l2)
-        par = solution_parity(xg, xc, Fg, Fc)
-        assert par["ok"], (c, par, stg, stc)
-        assert stg["outer_iters"] == stc["outer_iters"]
-        assert abs(stg["newton_iters"] - stc["newton_iters"]) <= 1
-    del A
+@pytest.mark.parametrize("name,storage", [("cfg3", "fp64"), ("cfg4", "fp64"), ("cfg4", "geno"), ("cfg5", "fp64")])
+def test_fullsize_oracle_parity(name, storage):
+    """North-star target "every config's solution matches the CPU oracle within the stated tolerances"
+    at full size: cfg3 (m = 500, n = 1e6, all three c), cfg4 (m = 800, n = 2e6; 12.8 GB) from the fp64 design and from packed genotype codes
+    (parity against the decoded fp64 design, which equals synth.design bitwise), and cfg5
+    (m = 500, n = 1e7; 40 GB) at both c.  The oracle solves on the host copy generated by synth's host
+    generator (bitwise equal to the device one, test_device_generator_bitwise)."""
+    if storage == "fp64":
+        cfg, dA, b, P = device_problem(name)
+    else:
+        for k in list(_cache):
+            _cache[k][3].close()
+            del _cache[k]
+        torch.cuda.empty_cache()
+        cfg = synth.CONFIGS[name]
+        st = torch.cuda.current_stream()
+        stride = synth.geno_stride(cfg.m)
+        dcodes = torch.empty((cfg.n, stride), dtype=torch.uint8, device="cuda")
+        dtab = torch.empty((cfg.n, 3), dtype=torch.float64, device="cuda")
+        synth.fill_device_geno(cfg, dcodes.data_ptr(), dtab.data_ptr(), st.cuda_stream)
+        b, _ = synth.response(cfg)
+        db = torch.from_numpy(b).cuda()
+        P = Problem.from_geno_device(dcodes.data_ptr(), stride, dtab.data_ptr(), db.data_ptr(), cfg.m, cfg.n,
+                                     st.cuda_stream, keep=(dcodes, dtab, db))
+    try:
+        A = synth.design(cfg)  # host generator: 12.8 / 40 GB
+        lm = oracle.lambda_max_l1(A, b)
+        assert P.lambda_max_l1 == pytest.approx(lm, rel=1e-13)
+        for c in cfg.cs:
+            l1, l2 = lambdas(cfg, lm, c)
+            par, stg, stc, rerun = compare_to_oracle(A, b, l1, l2, lambda s0, tol, x0: P.solve(l1, l2, s0, tol, x0=x0),
+                                                     sigma0=cfg.sigma0, tol=cfg.tol, label=f"{name}/{storage} c={c}")
+            print(f"{name}/{storage} c={c}: {par} outer {stg['outer_iters']}/{stc['outer_iters']} "
+                  f"newton {stg['newton_iters']}/{stc['newton_iters']}")
+        del A
+    finally:
+        if storage != "fp64":
+            P.close()

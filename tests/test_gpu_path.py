@@ -1,12 +1,16 @@
 """The λ-path call ssnal_en_solve_path_device (BASELINE configs[1]'s warm-started path):
 every point enqueued before one synchronisation must give exactly the loop of single device solves
 (same kernels in the same order: x bitwise, statistics equal), in graph mode, on the one-CTA path, and
-through the host-driven fallback; a cold first point and an x0 start; bad arguments are EINVAL."""
+through the host-driven fallback; a cold first point and an x0 start; bad arguments are EINVAL.
+With option carry_sigma (default; reading R38) point i starts at point i − 1's sigma_final (the
+loop passes it explicitly); the path then matches the oracle's carried path point by point (±1 rule),
+and most warm points converge in one outer iteration on the Table D.4 grid."""
 import numpy as np
 import pytest
 
+import oracle
 import synth
-from gpu_util import cuda_ok
+from gpu_util import compare_to_oracle, cuda_ok
 
 pytestmark = pytest.mark.gpu
 
@@ -21,11 +25,15 @@ KEYS = ["status", "outer_iters", "newton_iters", "psi_evals", "backtracks", "aty
 
 def loop_vs_path(P, ls, sigma0, tol, n, x0=None):
     k = len(ls)
+    carry = P.info("carry_sigma") == 1
     xl = torch.empty((k, n), dtype=torch.float64, device="cuda")
     sl = []
+    sig = sigma0
     for i, (l1, l2) in enumerate(ls):
         x0p = (x0.data_ptr() if x0 is not None else 0) if i == 0 else xl[i - 1].data_ptr()
-        sl.append(P.solve_device(l1, l2, sigma0, tol, x0p, xl[i].data_ptr()))
+        sl.append(P.solve_device(l1, l2, sig, tol, x0p, xl[i].data_ptr()))
+        if carry:
+            sig = sl[-1]["sigma_final"]
     xp = torch.empty((k, n), dtype=torch.float64, device="cuda")
     sp = P.solve_path_device([a for a, _ in ls], [b for _, b in ls], sigma0, tol,
                              x0.data_ptr() if x0 is not None else 0, xp.data_ptr())
@@ -35,6 +43,7 @@ def loop_vs_path(P, ls, sigma0, tol, n, x0=None):
         for key in KEYS:
             assert a[key] == b[key] or (isinstance(a[key], float) and np.isnan(a[key]) and np.isnan(b[key])), key
         assert b["time_device_s"] > 0
+    return sp
 
 
 @pytest.mark.parametrize("name,n,graph", [("cfg2", 20_000, 1), ("cfg2", 20_000, 0), ("cfg1", None, 1)])
@@ -47,7 +56,12 @@ def test_path_matches_loop(name, n, graph):
         lm = P.lambda_max_l1 / cfg.alpha
         cs = np.linspace(0.9, 0.1, 10)
         ls = [(c * cfg.alpha * lm, c * (1 - cfg.alpha) * lm) for c in cs]
-        loop_vs_path(P, ls, cfg.sigma0, cfg.tol, A.shape[0])
+        sp = loop_vs_path(P, ls, cfg.sigma0, cfg.tol, A.shape[0])
+        assert sum(s["outer_iters"] for s in sp[1:]) < 2 * (len(sp) - 1)  # σ carried: mostly 1 outer step
+        P.set_option("carry_sigma", 0)  # every point restarts at σ0
+        sp0 = loop_vs_path(P, ls, cfg.sigma0, cfg.tol, A.shape[0])
+        assert min(s["outer_iters"] for s in sp0[1:]) >= 3
+        P.set_option("carry_sigma", 1)
         # a warm first point from a given x0
         x0 = torch.zeros(A.shape[0], dtype=torch.float64, device="cuda")
         x0[3] = 0.1
@@ -55,3 +69,42 @@ def test_path_matches_loop(name, n, graph):
         with pytest.raises(SsnalError):
             P.solve_path_device([ls[0][0], -1.0], [ls[0][1], 1.0], cfg.sigma0, cfg.tol, 0,
                                 torch.empty((2, A.shape[0]), dtype=torch.float64, device="cuda").data_ptr())
+
+
+@pytest.mark.parametrize("name,n,grid", [("cfg2", 20_000, "d4"), ("cfg2", None, "cfg"), ("cfg1", None, "d4")])
+def test_carried_path_matches_oracle(name, n, grid):
+    """The path call against oracle.solve_path_lambdas point by point: each point from the same start
+    (the oracle's previous x and sigma_final) with the ±1 rerun rule, solution, dual objective and gap;
+    on the Table D.4 grid (100 log-spaced c, 1 → 0.1, stop at 100 actives) ≥ 90% of the warm
+    points take one outer iteration on the GPU as in the oracle."""
+    cfg = synth.CONFIGS[name] if n is None else synth.scaled(synth.CONFIGS[name], n=n)
+    A = synth.design(cfg)
+    b, _ = synth.response(cfg)
+    cs = np.logspace(0, -1, 100) if grid == "d4" else np.array(cfg.cs)
+    lm = oracle.lambda_max_l1(A, b) / cfg.alpha
+    ls = [(c * cfg.alpha * lm, c * (1 - cfg.alpha) * lm) for c in cs]
+    orc = oracle.solve_path_lambdas(A, b, ls, sigma0=cfg.sigma0, tol=cfg.tol, max_active=100 if grid == "d4" else None)
+    ls = ls[:len(orc)]
+    with Problem(A, b) as P:
+        xp = torch.empty((len(ls), A.shape[0]), dtype=torch.float64, device="cuda")
+        sp = P.solve_path_device([a for a, _ in ls], [b_ for _, b_ in ls], cfg.sigma0, cfg.tol, 0, xp.data_ptr())
+        xg = xp.cpu().numpy()
+        same = 0
+        for i, ((l1, l2), (xc, _, stc), stg) in enumerate(zip(ls, orc, sp)):
+            same += stg["outer_iters"] == stc["outer_iters"] and stg["newton_iters"] == stc["newton_iters"]
+            x0 = None if i == 0 else orc[i - 1][0]
+            s0 = cfg.sigma0 if i == 0 else orc[i - 1][2]["sigma_final"]
+            if stg["outer_iters"] == stc["outer_iters"] and stg["newton_iters"] == stc["newton_iters"] and \
+                    stg["sigma_final"] == stc["sigma_final"]:
+                from gpu_util import solution_parity
+                Fg, Fc = oracle.primal_obj(A, b, xg[i], l1, l2), oracle.primal_obj(A, b, xc, l1, l2)
+                par = solution_parity(xg[i], xc, Fg, Fc)
+                assert par["ok"], (i, par, stg, stc)
+                assert abs(stg["dual_obj"] - stc["dual_obj"]) <= 1e-9 * abs(Fc)
+            else:  # diverged by roundoff: restart the GPU from the oracle's point and apply the ±1 rule
+                compare_to_oracle(A, b, l1, l2, lambda s_, tol, x_: P.solve(l1, l2, s_, tol, x0=x_), sigma0=s0, x0=x0,
+                                  label=f"{name} point {i}")
+        assert same >= 0.9 * len(ls)
+        if grid == "d4":
+            warm = [s for s, (xprev, _, _) in zip(sp[1:], orc[:-1]) if np.any(xprev != 0)]
+            assert sum(s["outer_iters"] == 1 for s in warm) >= 0.9 * len(warm)
