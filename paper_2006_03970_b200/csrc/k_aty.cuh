@@ -609,9 +609,19 @@ struct K1eParams {
   int64_t T;
 };
 
+// Each iteration covers K1E_U · K1E_THREADS consecutive columns (element u of thread t is column
+// base + u·K1E_THREADS + t: coalesced per u), with all loads issued before any use so that
+// 3 · K1E_U loads per thread are in flight (an HBM stream needs ~40 KB in flight per SM; one load
+// per thread and two barriers per 512 columns left the round-1 version latency-bound at ~11% of its
+// roofline).  The compaction stays ordered: warp counts per u, one barrier, prefix over (u, warp).
+constexpr int K1E_U = 8;
 __global__ void __launch_bounds__(K1E_THREADS) k1e_epilogue(const K1eParams p) {
-  __shared__ int wcnt[K1E_THREADS / 32];
-  __shared__ double red[K1E_THREADS / 32][4];
+  constexpr int NW = K1E_THREADS / 32;
+  constexpr int NE = K1E_U * NW;  // (u, warp) count entries per iteration, u-major = column order
+  static_assert(NE % 32 == 0, "scan layout");
+  __shared__ int wcnt[2][NE];     // double-buffered by iteration parity (no end-of-iteration barrier)
+  __shared__ int offs[2][NE + 1]; // exclusive prefix; [NE] = iteration total
+  __shared__ double red[NW][4];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   int64_t c_lo, c_hi;
   cta_cols(blockIdx.x, gridDim.x, p.T, p.C, p.n, &c_lo, &c_hi);
@@ -619,42 +629,81 @@ __global__ void __launch_bounds__(K1E_THREADS) k1e_epilogue(const K1eParams p) {
   const double step = p.sp ? *p.sp : p.s;
   double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
   int64_t cnt = 0;
-  for (int64_t base = c_lo; base < c_hi; base += K1E_THREADS) {
-    const int64_t i = base + tid;
-    int act = 0;
-    double P = 0.0;
-    if (i < c_hi) {
-      double w = p.w0[i];
-      if (p.w1) w = __dadd_rn(w, __dmul_rn(step, __dsub_rn(p.w1[i], w)));
-      if (p.w_out) p.w_out[i] = w;
-      const double xi = p.x[i];
-      const double tt = __dsub_rn(xi, __dmul_rn(sc.sigma, w));
-      act = fabs(tt) > sc.thr;
-      P = prox_en(tt, sc.thr, sc.den);
-      const double dx = __dsub_rn(xi, P);
-      const double z = __dsub_rn(__ddiv_rn(dx, sc.sigma), w);
-      const double e = __dsub_rn(fabs(w), sc.l1);
-      s0 = __dadd_rn(s0, __dmul_rn(P, P));
-      s1 = __dadd_rn(s1, __dmul_rn(dx, dx));
-      s2 = __dadd_rn(s2, __dmul_rn(z, z));
-      if (e > 0.0) s3 = __dadd_rn(s3, __dmul_rn(e, e));
+  int par = 0;
+  const unsigned lt = lanemask_lt();
+  for (int64_t base = c_lo; base < c_hi; base += (int64_t)K1E_U * K1E_THREADS, par ^= 1) {
+    double wv[K1E_U], xv[K1E_U], w1v[K1E_U];
+#pragma unroll
+    for (int u = 0; u < K1E_U; ++u) {
+      const int64_t i = base + (int64_t)u * K1E_THREADS + tid;
+      const bool in = i < c_hi;
+      wv[u] = in ? __ldg(p.w0 + i) : 0.0;
+      xv[u] = in ? __ldg(p.x + i) : 0.0;
+      w1v[u] = (in && p.w1) ? __ldg(p.w1 + i) : 0.0;
     }
-    const unsigned bal = __ballot_sync(0xffffffffu, act);
-    if (lane == 0) wcnt[warp] = __popc(bal);
+    unsigned bal[K1E_U];
+    double Pv[K1E_U];
+#pragma unroll
+    for (int u = 0; u < K1E_U; ++u) {
+      const int64_t i = base + (int64_t)u * K1E_THREADS + tid;
+      int act = 0;
+      double P = 0.0;
+      if (i < c_hi) {
+        double w = wv[u];
+        if (p.w1) w = __dadd_rn(w, __dmul_rn(step, __dsub_rn(w1v[u], w)));
+        if (p.w_out) p.w_out[i] = w;
+        const double xi = xv[u];
+        const double tt = __dsub_rn(xi, __dmul_rn(sc.sigma, w));
+        act = fabs(tt) > sc.thr;
+        const double e = __dsub_rn(fabs(w), sc.l1);
+        if (xi == 0.0 && !act) {  // P = 0, x − P = 0, z = 0/σ − w = −w exactly: no division (as in K1)
+          s2 = __dadd_rn(s2, __dmul_rn(w, w));
+        } else {
+          P = prox_en(tt, sc.thr, sc.den);
+          const double dx = __dsub_rn(xi, P);
+          const double z = __dsub_rn(__ddiv_rn(dx, sc.sigma), w);
+          s0 = __dadd_rn(s0, __dmul_rn(P, P));
+          s1 = __dadd_rn(s1, __dmul_rn(dx, dx));
+          s2 = __dadd_rn(s2, __dmul_rn(z, z));
+        }
+        if (e > 0.0) s3 = __dadd_rn(s3, __dmul_rn(e, e));
+      }
+      Pv[u] = P;
+      bal[u] = __ballot_sync(0xffffffffu, act);
+      if (lane == 0) wcnt[par][u * NW + warp] = __popc(bal[u]);
+    }
     __syncthreads();
-    int off = 0, tot = 0;
-    for (int wi = 0; wi < K1E_THREADS / 32; ++wi) {
-      const int v = wcnt[wi];
-      off += (wi < warp) ? v : 0;
-      tot += v;
+    if (warp == 0) {  // exclusive scan of the NE counts in column order: lane owns NE/32 consecutive entries
+      constexpr int PL = NE / 32;
+      int v[PL], sum = 0;
+#pragma unroll
+      for (int j = 0; j < PL; ++j) {
+        v[j] = wcnt[par][lane * PL + j];
+        sum += v[j];
+      }
+      int incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      int run = incl - sum;
+#pragma unroll
+      for (int j = 0; j < PL; ++j) {
+        offs[par][lane * PL + j] = run;
+        run += v[j];
+      }
+      if (lane == 31) offs[par][NE] = incl;
     }
-    if (act) {
-      const int64_t pos = cnt + off + __popc(bal & lanemask_lt());
-      p.seg_idx[c_lo + pos] = (int32_t)i;
-      p.seg_P[c_lo + pos] = P;
-    }
-    cnt += tot;
     __syncthreads();
+#pragma unroll
+    for (int u = 0; u < K1E_U; ++u)
+      if (bal[u] & (1u << lane)) {
+        const int64_t pos = cnt + offs[par][u * NW + warp] + __popc(bal[u] & lt);
+        p.seg_idx[c_lo + pos] = (int32_t)(base + (int64_t)u * K1E_THREADS + tid);
+        p.seg_P[c_lo + pos] = Pv[u];
+      }
+    cnt += offs[par][NE];
   }
   // deterministic block reduction of the four partials
   double q[4] = {s0, s1, s2, s3};

@@ -51,6 +51,11 @@ struct SmallParams {
   int64_t* rx;
   DevCtl* C;        // settings in, statistics out
   EvalOut* ev;      // out: evaluation at the final point (dual objective)
+  // k_small_cl only (the one-CTA kernel leaves them to the multi-kernel helpers):
+  int cold;         // 1: x0 = 0 (y0 = 0, w0 = 0, x = 0 are not read; *rx0 ← 0)
+  int64_t* rx0;     // |supp x0| for the statistics
+  double* obj;      // out: [½‖Ax − b‖², Σ|x|, Σx², nnz] of the final x (nullable)
+  double* resid;    // out: A x − b (m), for the certify pass (nullable)
 };
 
 // shared-memory layout (doubles unless noted)

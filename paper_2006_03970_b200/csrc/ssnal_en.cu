@@ -23,6 +23,7 @@
 #include "k_chol_dsm.cuh"
 #include "k_chol_d2.cuh"
 #include "k_small.cuh"
+#include "k_small_cl.cuh"
 #include "ssnal_en.h"
 
 using namespace ssn;
@@ -361,6 +362,8 @@ struct ssnal_en_problem {
   // graph mode (device-resident control, k_ctl.cuh)
   int use_graph = 1;
   int use_small = 1;
+  int use_small_cl = 1;  // option small_cluster: the 16-CTA cluster version of the small-problem solve
+  int small_cl_ok = 0;   // … schedulable on this device
   int eval16_ok = 0;  // the 16-CTA-cluster evaluation kernels are schedulable (m ≤ 512)  // option small: one-CTA solve (k_small_solve) for m ≤ 64, n ≤ 1024
   ssn::DevCtl* ctl = nullptr;       // device control block
   ssn::DevCtl* ctl_host = nullptr;  // pinned staging (inputs in, results back)
@@ -560,8 +563,19 @@ int configure(ssnal_en_problem* P) {
     if (cudaOccupancyMaxActiveClusters(&nclus, k_eval_reduce16, &cfg) == cudaSuccess && nclus >= 1) P->eval16_ok = 1;
     cudaGetLastError();
   }
-  if (P->m <= kSmallMaxM && P->n <= kSmallMaxN)
+  P->small_cl_ok = 0;
+  if (P->m <= kSmallMaxM && P->n <= kSmallMaxN) {
     CK(cudaFuncSetAttribute(k_small_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmallSmem));
+    CK(cudaFuncSetAttribute(k_small_cl, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kClSmem));
+    CK(cudaFuncSetAttribute(k_small_cl, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(kClCtas);
+    cfg.blockDim = dim3(kClThreads);
+    cfg.dynamicSmemBytes = kClSmem;
+    int nclus = 0;
+    if (cudaOccupancyMaxActiveClusters(&nclus, k_small_cl, &cfg) == cudaSuccess && nclus >= 1) P->small_cl_ok = 1;
+    cudaGetLastError();
+  }
   return SSNAL_OK;
 }
 
@@ -1717,7 +1731,10 @@ int solve_small_core(ssnal_en_problem* P, double l1, double l2, double sigma0, d
   memset(S, 0, sizeof(*S));
   int rc;
   int64_t rx = 0;
-  if ((rc = init_point(P, have_x0, S, &rx))) return rc;
+  const bool cl = P->use_small_cl && P->small_cl_ok;
+  // the cluster kernel initialises a cold start itself (no memsets) and computes the objective
+  if ((!cl || have_x0) && (rc = init_point(P, have_x0, S, &rx))) return rc;
+  if (cl && !have_x0) S->aty_passes = 0;
   DevCtl* h = P->ctl_host;
   memset(h, 0, sizeof(DevCtl));
   h->l1 = l1;
@@ -1739,6 +1756,10 @@ int solve_small_core(ssnal_en_problem* P, double l1, double l2, double sigma0, d
   if (sigma_dev)  // σ0 carried on the device from the previous path point (R38)
     CK(cudaMemcpyAsync(&P->ctl->sigma, sigma_dev, 8, cudaMemcpyDeviceToDevice, P->st));
   SmallParams sp;
+  sp.cold = (cl && !have_x0) ? 1 : 0;
+  sp.rx0 = P->r_dev + 4;
+  sp.obj = cl ? P->scratch + 16 : nullptr;
+  sp.resid = cl ? P->tmpm : nullptr;
   sp.A = P->A;
   sp.b = P->b;
   sp.m = (int)P->m;
@@ -1751,10 +1772,18 @@ int solve_small_core(ssnal_en_problem* P, double l1, double l2, double sigma0, d
   sp.rx = P->r_dev + 2;
   sp.C = P->ctl;
   sp.ev = P->ev_dev;
-  k_small_solve<<<1, kSmallThreads, kSmallSmem, P->st>>>(sp);
+  if (cl)  // A resident in the cluster's shared memory (k_small_cl.cuh); objective included
+    k_small_cl<<<kClCtas, kClThreads, kClSmem, P->st>>>(sp);
+  else
+    k_small_solve<<<1, kSmallThreads, kSmallSmem, P->st>>>(sp);
   P->launches++;
   CKL();
-  if ((rc = launch_objective(P))) return rc;
+  if (!cl) {
+    if ((rc = launch_objective(P))) return rc;
+  } else {
+    CK(cudaMemcpyAsync(P->scratch_host + 16, P->scratch + 16, 4 * 8, cudaMemcpyDeviceToHost, P->st));
+    CK(cudaMemcpyAsync(P->scratch_host + 20, P->r_dev + 4, 8, cudaMemcpyDeviceToHost, P->st));
+  }
   CK(cudaMemcpyAsync(h, P->ctl, sizeof(DevCtl), cudaMemcpyDeviceToHost, P->st));
   CK(cudaMemcpyAsync(P->ev_out_host, P->ev_dev, sizeof(EvalOut), cudaMemcpyDeviceToHost, P->st));
   P->stat_l1 = l1;
@@ -2138,6 +2167,8 @@ int ssnal_en_set_option(ssnal_en_problem* P, const char* key, double v) {
   }
   else if (k == "small" && (v == 0 || v == 1))
     P->use_small = (int)v;
+  else if (k == "small_cluster" && (v == 0 || v == 1))
+    P->use_small_cl = (int)v;
   else if (k == "chol_d2" && (v == 0 || v == 1)) {
     P->use_d2 = (int)v;
     drop_graph(P);  // the K4 variant is baked into the graph
@@ -2176,6 +2207,7 @@ double ssnal_en_get_info(const ssnal_en_problem* P, const char* key) {
   if (k == "cluster_size") return P->cluster;
   if (k == "chol_dsm") return P->chol_dsm;
   if (k == "small") return small_eligible(P) ? 1 : 0;
+  if (k == "small_cluster") return (small_eligible(P) && P->use_small_cl && P->small_cl_ok) ? 1 : 0;
   if (k == "chol_d2") return P->chol_dsm && P->use_d2 && P->d2_ok;
   if (k == "num_sms") return P->nsm;
   if (k == "graph") return P->use_graph;

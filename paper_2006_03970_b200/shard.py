@@ -44,18 +44,33 @@ def as_tensor(ptr: int, count: int, device: str = "cuda") -> torch.Tensor:
 
 
 def torch_allreduce(group=None, device: str = "cuda"):
-    """An all-reduce for Problem.set_comm over a torch.distributed group."""
+    """An all-reduce for Problem.set_comm over a torch.distributed group.  NCCL: in place on the device,
+    ordered on the library's stream.  Other backends (gloo) with device buffers: staged through host
+    memory — the library's stream is drained, the buffer is copied to the host on that stream, reduced
+    by the backend on CPU tensors, and copied back on the same stream, so the exchange is complete and
+    ordered before the library's next kernel."""
     import torch.distributed as dist
 
     ops = {SUM: dist.ReduceOp.SUM, MAX: dist.ReduceOp.MAX}
+    nccl = device == "cuda" and dist.get_backend(group) == "nccl"
 
     def fn(buf, count, op, stream):
         t = as_tensor(buf, count, device)
-        if device == "cuda":
-            with torch.cuda.stream(torch.cuda.ExternalStream(stream or 0)):
+        if device != "cuda":
+            dist.all_reduce(t, op=ops[op], group=group)
+            return
+        # the library's stream; a NULL handle is the legacy default stream, which torch names
+        # default_stream() (wrapping it as ExternalStream(0) raced in the two-process test)
+        st = torch.cuda.ExternalStream(stream) if stream else torch.cuda.default_stream()
+        if nccl:
+            with torch.cuda.stream(st):
                 dist.all_reduce(t, op=ops[op], group=group)
         else:
-            dist.all_reduce(t, op=ops[op], group=group)
+            st.synchronize()  # the producing kernels are done
+            h = t.to("cpu")
+            dist.all_reduce(h, op=ops[op], group=group)
+            t.copy_(h)
+            torch.cuda.current_stream().synchronize()  # complete before the library's next kernel
 
     return fn
 

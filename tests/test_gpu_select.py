@@ -15,15 +15,12 @@ if cuda_ok():
 
 
 def oracle_path(A, b, alpha, cs, max_active=None):
-    lm = float(np.max(np.abs(oracle.aty(A, b)))) / alpha
-    pts, x = [], None
-    for c in cs:
-        l1, l2 = c * alpha * lm, c * (1 - alpha) * lm
-        x, _, st, _ = oracle.solve(A, b, l1, l2, x0=x)
+    """The oracle's warm-started path (σ carried, R38) with the criteria at every point."""
+    ls, res = oracle.solve_path(A, b, alpha, cs, max_active=max_active)
+    pts = []
+    for (l1, l2), (x, _, st) in zip(ls, res):
         r, nu, rss, gcv, ebic, xdb = oracle.model_select(A, b, x, l2)
         pts.append({"r": r, "nu": nu, "rss": rss, "gcv": gcv, "ebic": ebic, "xdb": xdb, "active": st["active"]})
-        if max_active is not None and st["active"] >= max_active:
-            break
     return pts
 
 

@@ -1,5 +1,6 @@
-"""The one-CTA solve for small problems (k_small_solve, m ≤ 64, n ≤ 1024; Algorithm 1, P:234-291,
-P:305-389): parity with the CPU oracle at BASELINE tolerances and the same iteration counts as the
+"""The single-launch solves for small problems (m ≤ 64, n ≤ 1024; Algorithm 1):
+the 16-CTA cluster kernel k_small_cl (A resident in distributed shared memory; the default) and the
+one-CTA kernel k_small_solve (option small_cluster = 0), each against the oracle — parity with the CPU oracle at BASELINE tolerances and the same iteration counts as the
 oracle and the multi-kernel graph path, across shapes, both Newton branches (Eq. (18)/(19)), warm
 starts, the oracle-free pins (x = 0 above λmax after one Newton step, warm start at the solution),
 Lasso (λ2 = 0), the adaptive inner tolerance (R37), the factor retry (R36) and the iteration cap."""
@@ -35,18 +36,29 @@ def problem(case, c_list):
     return cfg, A, b, lm
 
 
+@pytest.fixture(params=[1, 0], ids=["cluster", "one-cta"])
+def small_cl(request):
+    return request.param
+
+
+def use(P, variant):
+    P.set_option("small_cluster", variant)
+    assert P.info("small_cluster") == variant
+
+
 def parity(A, b, l1, l2, xg, xc):
     Fg, Fc = oracle.primal_obj(A, b, xg, l1, l2), oracle.primal_obj(A, b, xc, l1, l2)
     return solution_parity(xg, xc, Fg, Fc)
 
 
 @pytest.mark.parametrize("case", SHAPES, ids=lambda c: f"m{c[1]}_n{c[2]}")
-def test_small_matches_oracle_and_graph(case):
+def test_small_matches_oracle_and_graph(case, small_cl):
     cs = (0.5, 0.1, 0.02)  # small c: r ≥ m steps (Eq. (18) branch)
     cfg, A, b, lm = problem(case, cs)
     seen = [0, 0, 0]
     with Problem(A, b) as P:
         assert P.info("small") == 1
+        use(P, small_cl)
         for c in cs:
             l1, l2 = c * cfg.alpha * lm, c * (1 - cfg.alpha) * lm
             xc, _, sc, _ = oracle.solve(A, b, l1, l2, sigma0=cfg.sigma0, tol=cfg.tol)
@@ -73,11 +85,12 @@ def test_small_matches_oracle_and_graph(case):
         assert seen[1] > 0 or seen[2] > 0, seen
 
 
-def test_small_warm_path_and_pins():
+def test_small_warm_path_and_pins(small_cl):
     case = SHAPES[0]
     cs = tuple(np.linspace(0.9, 0.1, 10))
     cfg, A, b, lm = problem(case, cs)
     with Problem(A, b) as P:
+        use(P, small_cl)
         # x = 0 at λ1 = ‖Aᵀb‖∞ after exactly one Newton step
         g = P.lambda_max_l1
         x, st = P.solve(g, 0.2 * g, 5e-3, 1e-6)
@@ -100,11 +113,12 @@ def test_small_warm_path_and_pins():
         assert np.max(np.abs(x - xsol)) <= 1e-8 * np.max(np.abs(xsol))
 
 
-def test_small_lasso_innertol_retry_cap():
+def test_small_lasso_innertol_retry_cap(small_cl):
     case = SHAPES[0]
     cfg, A, b, lm = problem(case, (0.3,))
     l1, l2 = 0.3 * cfg.alpha * lm, 0.3 * (1 - cfg.alpha) * lm
     with Problem(A, b) as P:
+        use(P, small_cl)
         # Lasso: λ2 = 0, dual objective NaN
         xc, _, _, _ = oracle.solve(A, b, l1, 0.0)
         xs, ss = P.solve(l1, 0.0, 5e-3, 1e-6)

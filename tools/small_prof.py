@@ -18,8 +18,10 @@ lib.ssnal_en_small_prof.argtypes = [ctypes.POINTER(ctypes.c_ulonglong), ctypes.c
 cfg = synth.CONFIGS["cfg1"]
 A = synth.design(cfg)
 b, _ = synth.response(cfg)
-names = ["pass", "epilogue", "gradient", "gram", "factor", "bwd+d+gd", "-", "-"]
+variant = int(os.environ.get("SMALL_CLUSTER", "1"))
+names = ["pass", "epilogue", "gradient", "gram", "factor", "bwd+d+gd", "-", "-"] if not variant else ["pass", "local-epi", "exchange", "newton-mat", "factor", "bwd+d+gd", "gradient", "panel"]
 with se.Problem(A, b) as P:
+    P.set_option("small_cluster", variant)
     lm = P.lambda_max_l1 / cfg.alpha
     l1, l2 = 0.5 * cfg.alpha * lm, 0.5 * (1 - cfg.alpha) * lm
     for _ in range(3):
@@ -31,5 +33,9 @@ with se.Problem(A, b) as P:
         x, st = P.solve(l1, l2, cfg.sigma0, cfg.tol)
     lib.ssnal_en_small_prof(buf, 0)
     print("device time per solve (us):", st["time_device_s"] * 1e6, "newton", st["newton_iters"], "outer", st["outer_iters"])
-    for k in range(6):
-        print(f"{names[k]:10s} {buf[k] / reps / 1.9e3:8.1f} us per solve")
+    for k in range(8):
+        v = buf[k]
+        if k == 6 and variant:  # high half: Σ N of the factorisations (cluster kernel)
+            print("sum N per solve:", (v >> 32) / reps)
+            v &= 0xFFFFFFFF
+        print(f"{names[k]:10s} {v / reps / 1.9e3:8.1f} us per solve")
