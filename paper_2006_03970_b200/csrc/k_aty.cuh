@@ -55,6 +55,7 @@ struct K1Params {
   const uint8_t* codes; // n × cstride bytes: 2-bit codes, row k in bits 2(k%4) of byte k/4
   const double* tab;    // n × 3: decoded value of codes 0, 1, 2 for each column
   int64_t cstride;      // bytes per column (multiple of 16)
+  uint32_t bfr_off;     // K1g: byte offset of the shared B-fragment table (32 k-blocks × 32 lanes × 8 B)
 };
 
 // Reduce-scatter of 8 per-lane partial sums a[0..7] across the warp: afterwards every
@@ -439,25 +440,81 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1g_aty_fused(const K1Params p)
   }
 
   // ---------------- consumer warps ----------------
-  double yr[TW][16], gacc[TW][16];
+  // a_jᵀy = v0 ΣY + (v1 − v0) S1 + (v2 − v0) S2 with the bucket sums S_g = Σ_{k: g_kj = g} y_k.  The
+  // bucket sums are exact integer dot products on the INT8 tensor cores (mma.sync m16n8k32 u8,
+  // SASS IMMA): y is rounded once to 64-bit fixed point Y = rint(y·2^e) (2^e the largest power of two
+  // with m·max|y|·2^e < 2^62, so every partial sum fits), split into 8 byte limbs (the B operand:
+  // 32 rows × 8 limbs, kept in registers for the whole launch), and each column's code bytes expand
+  // to the 0/1 bit planes [g = 1], [g = 2] (the A operand: 16 columns × 32 rows; code 3 is rejected
+  // at create, so g = 1 ⇔ bit 0, g = 2 ⇔ bit 1).  The int32 accumulators per limb are exact
+  // (≤ 1024 · 255); Σ_l C_l 2^{8l} mod 2^64 is the exact two's-complement S·2^e, converted to fp64
+  // once.  Rounding y costs ≤ m·2^{-e-1} ≈ m²·max|y|·2^{-63} per bucket sum, ~1e-13 of the R21 bound
+  // (DESIGN.md §5).  Thread (g = lane/4, t = lane%4) of the warp's 16-column group: A rows (columns)
+  // g and g + 8, k = 4t … 4t + 3 and 16 + 4t …; B limb g of the same k; C columns (limbs) 2t, 2t + 1.
+  const int gq = lane >> 2, tq = lane & 3;
+  const int nkb = (int)((m + 31) / 32);
+  double ysum = 0.0, ymax = 0.0;  // Σ y (fixed lane then butterfly order), max |y|
+  for (int64_t row = lane; row < m; row += 32) {
+    const double yv = p.y[row];
+    ysum += yv;
+    ymax = fmax(ymax, fabs(yv));
+  }
+  ysum = warp_allsum(ysum);
+  ymax = warp_allmax(ymax);
+  int ex = 0;
+  if (ymax > 0.0) {
+    int e2;
+    frexp(ymax * (double)m, &e2);  // m·max|y| < 2^e2
+    ex = 62 - e2;
+  }
+  const double unscale = ldexp(1.0, -ex);
+  // B fragments (limb gq of Y at rows 32kb + 4tq + i and 32kb + 16 + 4tq + i), identical for every
+  // warp: built once per CTA into shared memory, read per k-block (conflict-free: entry kb·32 + lane)
+  uint2* bsm = reinterpret_cast<uint2*>(smem + p.bfr_off);
+  for (int kb = warp; kb < 32; kb += K1_NWC) {
+    uint32_t v[2] = {0u, 0u};
+    if (kb < nkb) {
 #pragma unroll
-  for (int t = 0; t < TW; ++t)
+      for (int h = 0; h < 2; ++h)
 #pragma unroll
-    for (int q = 0; q < 16; ++q) {
-      const int64_t row = 16 * (lane + 32 * t) + q;
-      yr[t][q] = row < m ? p.y[row] : 0.0;
-      gacc[t][q] = 0.0;
+        for (int i = 0; i < 4; ++i) {
+          const int64_t row = 32 * kb + 16 * h + 4 * tq + i;
+          const long long Y = row < m ? __double2ll_rn(ldexp(p.y[row], ex)) : 0ll;
+          v[h] |= (uint32_t)(((unsigned long long)Y >> (8 * gq)) & 0xFFull) << (8 * i);
+        }
     }
-  double ysum = 0.0;  // Σ y over this lane's rows (the g = 0 bucket is ΣY − S1 − S2)
+    bsm[kb * 32 + lane] = make_uint2(v[0], v[1]);
+  }
+  named_bar_sync(1, K1_NWC * 32);
+  double gacc[TW][16];
 #pragma unroll
   for (int t = 0; t < TW; ++t)
 #pragma unroll
-    for (int q = 0; q < 16; ++q) ysum += yr[t][q];
+    for (int q = 0; q < 16; ++q) gacc[t][q] = 0.0;
   const Scal sc = p.scp ? *p.scp : p.sc;
   const bool leader = (lane & 3) == 0;
   const int gcol = lane >> 2;
   double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
   bool any_active = false;
+
+  // code byte → 4 bytes of the bit plane (bit `sh` of each 2-bit code): the set bits 0, 2, 4, 6 of
+  // (x >> sh) & 0x55 move to bits 0, 8, 16, 24 by one multiply (carries land on odd bit positions)
+  auto plane = [](uint32_t x, int sh) { return (((x >> sh) & 0x55u) * 0x41041u) & 0x01010101u; };
+  auto imma = [](int (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0, uint32_t b1) {
+    asm volatile("mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+                 : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+                 : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+  };
+  // Σ_l C_l 2^{8l} over the quad's limbs (mod 2^64), for this thread's two C rows
+  auto limbs = [&](const int (&c)[4], unsigned long long& ra, unsigned long long& rb) {
+    ra = ((unsigned long long)(long long)c[0] << (16 * tq)) + ((unsigned long long)(long long)c[1] << (16 * tq + 8));
+    rb = ((unsigned long long)(long long)c[2] << (16 * tq)) + ((unsigned long long)(long long)c[3] << (16 * tq + 8));
+#pragma unroll
+    for (int o = 1; o < 4; o <<= 1) {
+      ra += __shfl_xor_sync(0xffffffffu, ra, o);
+      rb += __shfl_xor_sync(0xffffffffu, rb, o);
+    }
+  };
 
   for (int64_t it = warp; it < ntiles; it += K1_NWC) {
     const int s = (int)(it % S);
@@ -470,41 +527,9 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1g_aty_fused(const K1Params p)
     const unsigned char* Cs = reinterpret_cast<const unsigned char*>(ring + (size_t)s * p.stage_elems);
     const double* Ts = ring + (size_t)s * p.stage_elems + code_elems;
     const double* Xs = xring + (size_t)s * p.xstage_elems;
-    for (int g = 0; g * K1_GRP < nc; ++g) {
-      // bucket sums S1 = Σ y [g = 1], S2 = Σ y [g = 2] over this lane's rows (code 3 is rejected at
-      // create, so g = 1 ⇔ bit 0 and g = 2 ⇔ bit 1): two bit-tested predicated adds per element
-      double b1[K1_GRP], b2[K1_GRP];
-#pragma unroll
-      for (int c = 0; c < K1_GRP; ++c) b1[c] = b2[c] = 0.0;
-#pragma unroll
-      for (int t = 0; t < TW; ++t) {
-        const int wi = lane + 32 * t;
-        uint32_t wd[K1_GRP];
-#pragma unroll
-        for (int c = 0; c < K1_GRP; ++c) {
-          const int cc = g * K1_GRP + c;
-          wd[c] = (cc < nc && wi < nwords) ? reinterpret_cast<const uint32_t*>(Cs + (size_t)cc * cs)[wi] : 0u;
-        }
-#pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          const double yv = yr[t][q];
-#pragma unroll
-          for (int c = 0; c < K1_GRP; ++c) {
-            add_if_bit(b1[c], yv, wd[c], 1u << (2 * q));
-            add_if_bit(b2[c], yv, wd[c], 2u << (2 * q));
-          }
-        }
-      }
-      // lane partial of column c: v0 ΣY + (v1 − v0) S1 + (v2 − v0) S2
-      double a[K1_GRP];
-#pragma unroll
-      for (int c = 0; c < K1_GRP; ++c) {
-        const int cc = g * K1_GRP + c;
-        const bool cv = cc < nc;
-        const double v0 = cv ? Ts[3 * cc] : 0.0, v1 = cv ? Ts[3 * cc + 1] : 0.0, v2 = cv ? Ts[3 * cc + 2] : 0.0;
-        a[c] = fma(v2 - v0, b2[c], fma(v1 - v0, b1[c], v0 * ysum));
-      }
-      const double w = reduce8(a, lane);
+
+    // epilogue of the 8-column group g (lanes 4c … 4c + 3 hold column g·8 + c's value w)
+    auto epi8 = [&](int g, double w) {
       const int c = g * K1_GRP + gcol;
       const bool valid = c < nc;
       if (p.fused) {
@@ -566,6 +591,61 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1g_aty_fused(const K1Params p)
         if (valid) {
           s0 = fmax(s0, fabs(w));
           if (leader) p.w_out[c0 + c] = w;
+        }
+      }
+    };
+
+    // two 16-column groups per iteration (independent chains: the loop is latency-, not pipe-bound)
+    for (int g32 = 0; g32 * 32 < nc; ++g32) {
+      int cA[2], cB[2];
+      bool vA[2], vB[2];
+      const unsigned char* pA[2];
+      const unsigned char* pB[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        cA[u] = g32 * 32 + 16 * u + gq;  // this thread's A rows (columns) of group u
+        cB[u] = cA[u] + 8;
+        vA[u] = cA[u] < nc;
+        vB[u] = cB[u] < nc;
+        pA[u] = Cs + (size_t)(vA[u] ? cA[u] : 0) * cs;
+        pB[u] = Cs + (size_t)(vB[u] ? cB[u] : 0) * cs;
+      }
+      int acc1[2][4], acc2[2][4];  // [group][C fragment], planes [g = 1], [g = 2]
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc1[u][e] = acc2[u][e] = 0;
+#pragma unroll
+      for (int kb = 0; kb < 32; ++kb) {
+        if (kb < nkb) {
+          const uint2 bb = bsm[kb * 32 + lane];
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const uint2 wa = vA[u] ? *reinterpret_cast<const uint2*>(pA[u] + 8 * kb) : make_uint2(0u, 0u);
+            const uint2 wb = vB[u] ? *reinterpret_cast<const uint2*>(pB[u] + 8 * kb) : make_uint2(0u, 0u);
+            const uint32_t xa0 = (wa.x >> (8 * tq)) & 0xFFu, xa1 = (wa.y >> (8 * tq)) & 0xFFu;
+            const uint32_t xb0 = (wb.x >> (8 * tq)) & 0xFFu, xb1 = (wb.y >> (8 * tq)) & 0xFFu;
+            imma(acc1[u], plane(xa0, 0), plane(xb0, 0), plane(xa1, 0), plane(xb1, 0), bb.x, bb.y);
+            imma(acc2[u], plane(xa0, 1), plane(xb0, 1), plane(xa1, 1), plane(xb1, 1), bb.x, bb.y);
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        if (g32 * 32 + 16 * u >= nc) break;
+        unsigned long long s1a, s1b, s2a, s2b;
+        limbs(acc1[u], s1a, s1b);
+        limbs(acc2[u], s2a, s2b);
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+          const int cc = half ? cB[u] : cA[u];
+          const bool cv = cc < nc;
+          const double S1 = (double)(long long)(half ? s1b : s1a) * unscale;
+          const double S2 = (double)(long long)(half ? s2b : s2a) * unscale;
+          const double v0 = cv ? Ts[3 * cc] : 0.0, v1 = cv ? Ts[3 * cc + 1] : 0.0, v2 = cv ? Ts[3 * cc + 2] : 0.0;
+          const double w = fma(v2 - v0, S2, fma(v1 - v0, S1, v0 * ysum));
+          const int g8 = g32 * 4 + 2 * u + half;
+          if (g8 < (nc + K1_GRP - 1) / K1_GRP) epi8(g8, w);
         }
       }
     }

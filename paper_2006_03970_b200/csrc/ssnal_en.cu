@@ -279,6 +279,7 @@ struct ssnal_en_problem {
   int MR = 0, C = 0, S = 0, G = 0;
   int64_t T = 0;
   size_t k1_smem = 0;
+  uint32_t k1_bfr_off = 0;  // K1g: offset of the shared B-fragment table
   uint32_t stage_elems = 0, xstage_elems = 0;
   int cluster = 16;
   size_t chol_smem = 0;
@@ -456,7 +457,9 @@ int configure(ssnal_en_problem* P) {
   P->MR = mr_bucket(m);
   // bytes of A per column in a K1 stage: fp64 (8m) or packed codes + table (cstride + 24)
   const int64_t bytes_col = P->fmt ? P->cstride + 24 : 8 * m;
-  int k = (int)(32768 / (K1_GRP * bytes_col));  // ~32 KB of A per tile
+  // ~32 KB of A per tile (fp64); packed codes: ~16 KB, so ≥ 2 tiles per consumer warp fit the ring
+  // (K1g is issue-bound, so a consumer must find its next tile loaded when it finishes one)
+  int k = (int)((P->fmt ? 16384 : 32768) / (K1_GRP * bytes_col));
   if (k < 1) k = 1;
   if (k > 32) k = 32;  // ≤ 256 columns per tile
   {  // small n: smaller tiles, so the pass spreads over the SMs and their consumer warps (a warp
@@ -475,11 +478,15 @@ int configure(ssnal_en_problem* P) {
   P->xstage_elems = (uint32_t)((P->C + 15) / 16 * 16);
   const size_t per_stage = (size_t)(P->stage_elems + P->xstage_elems) * 8;
   int S = (int)((200 * 1024) / per_stage);
-  if (S > 8) S = 8;
+  if (S > (P->fmt ? 2 * K1_NWC : 8)) S = P->fmt ? 2 * K1_NWC : 8;
   if (S < 2) S = 2;
   while ((size_t)S * P->stage_elems < (size_t)K1_NWC * m + K1_NWC * 4 + K1_NWC) ++S;
   P->S = S;
   P->k1_smem = (size_t)S * per_stage + 2 * S * 8 + 64 + 4 * S + 16;
+  if (P->fmt) {  // K1g: shared B-fragment table after the ring and barriers (32 × 32 × 8 B)
+    P->k1_bfr_off = (uint32_t)((P->k1_smem + 15) / 16 * 16);
+    P->k1_smem = P->k1_bfr_off + 32 * 32 * 8;
+  }
   P->T = (n + P->C - 1) / P->C;
   P->G = (int)(P->T < P->nsm ? P->T : P->nsm);
   P->gax_grid = P->nsm;
@@ -713,6 +720,7 @@ int launch_k1(ssnal_en_problem* P, const double* y, const double* x, const Scal&
   k.codes = P->codes;
   k.tab = P->tab;
   k.cstride = P->cstride;
+  k.bfr_off = P->k1_bfr_off;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   const bool ev_time = P->time_k1 && !P->capturing;
   if (ev_time) {
