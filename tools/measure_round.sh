@@ -1,17 +1,33 @@
 #!/bin/bash
-# Round measurement pass on one B200 (run under gpurun): every bench config, the reference arm,
-# the ncu launch list of the cfg2 path (host-driven mode) and --set full captures of K4 (k_chol_d2) and K1.
+# Round measurement pass on one B200 (run under gpurun): the GPU test suite, every bench config, the
+# reference arm, the ncu launch lists (cfg2 path and cfg5, host-driven mode: ncu cannot profile the
+# kernel nodes of graphs with conditional nodes) and `--set full` captures of the main kernels.
+# Everything lands in gpurun_out/r2/; the summaries are copied to profiles/ afterwards.
 set -x
 cd $GRAFT_REPO_ROOT
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > gpurun_out/m_smi.txt
-python bench.py > gpurun_out/m_cfg2.json 2> gpurun_out/m_cfg2.err
-python bench.py --config cfg1 > gpurun_out/m_cfg1.json 2> gpurun_out/m_cfg1.err
-python bench.py --config cfg3 > gpurun_out/m_cfg3.json 2> gpurun_out/m_cfg3.err
-python bench.py --config cfg4 > gpurun_out/m_cfg4.json 2> gpurun_out/m_cfg4.err
-python bench.py --config cfg4 --geno > gpurun_out/m_cfg4g.json 2> gpurun_out/m_cfg4g.err
-python bench.py --config cfg5 --no-e2e > gpurun_out/m_cfg5.json 2> gpurun_out/m_cfg5.err
-python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/m_ref.json 2> gpurun_out/m_ref.err
-ncu --metrics gpu__time_duration.sum --clock-control none -c 5000 --csv --log-file gpurun_out/m_launches_cfg2.csv python bench.py --steps 1 --warmup 3 --no-cpu --no-e2e --control host > gpurun_out/m_ncu_list.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:k_chol_d2 -s 40 -c 1 -o gpurun_out/m_d2 python bench.py --steps 1 --warmup 3 --no-cpu --no-e2e --control host > gpurun_out/m_ncu_d2.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:k1_aty_fused -s 30 -c 1 -o gpurun_out/m_k1 python bench.py --steps 1 --warmup 3 --no-cpu --no-e2e --control host > gpurun_out/m_ncu_k1.log 2>&1
-echo done
+O=gpurun_out/r2; mkdir -p $O
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $O/smi.txt
+lscpu > $O/lscpu.txt; nproc >> $O/lscpu.txt; free -g >> $O/lscpu.txt
+timeout 2400 python -m pytest tests -m gpu -q > $O/gputests.log 2>&1; echo "gpu tests rc=$?" >> $O/status.txt
+timeout 900 python bench.py --steps 20 --warmup 5 > $O/bench_cfg5.json 2> $O/bench_cfg5.err; echo "cfg5 rc=$?" >> $O/status.txt
+timeout 900 python bench.py --impl reference --steps 20 --warmup 5 > $O/bench_ref_cfg5.json 2> $O/bench_ref.err; echo "ref rc=$?" >> $O/status.txt
+for c in cfg1 cfg2 cfg3 cfg4; do
+  timeout 900 python bench.py --config $c --steps 20 --warmup 5 > $O/bench_$c.json 2> $O/bench_$c.err; echo "$c rc=$?" >> $O/status.txt
+done
+timeout 900 python bench.py --config cfg4 --geno --steps 20 --warmup 5 > $O/bench_cfg4_geno.json 2> $O/bench_cfg4g.err; echo "cfg4g rc=$?" >> $O/status.txt
+timeout 900 python bench.py --sweep > $O/bench_sweep.jsonl 2> $O/sweep.err; echo "sweep rc=$?" >> $O/status.txt
+timeout 900 python bench.py --select --cv 5 --steps 5 --warmup 3 > $O/bench_select.json 2> $O/select.err; echo "select rc=$?" >> $O/status.txt
+timeout 900 python bench.py --config cfg2 --shard --steps 10 --warmup 3 --no-cpu --no-e2e > $O/bench_cfg2_shard.json 2> $O/shard.err; echo "shard rc=$?" >> $O/status.txt
+# launch lists (cold-cache, serialised: compare shares, not absolutes)
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 20000 --csv --log-file $O/launches_cfg2.csv python bench.py --config cfg2 --steps 1 --warmup 3 --no-cpu --no-e2e --control host > $O/ncu_list2.log 2>&1
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 20000 --csv --log-file $O/launches_cfg5.csv python bench.py --config cfg5 --steps 1 --warmup 3 --no-cpu --no-e2e --control host > $O/ncu_list5.log 2>&1
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 20000 --csv --log-file $O/launches_cfg1.csv python bench.py --config cfg1 --steps 2 --warmup 3 --no-cpu --no-e2e > $O/ncu_list1.log 2>&1
+# --set full captures
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k1_aty_fused -s 10 -c 1 -o $O/k1_n1e7 python bench.py --config cfg5 --steps 1 --warmup 3 --no-cpu --no-e2e --control host > $O/ncu_k1.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k1e_epilogue -s 10 -c 1 -o $O/k1e_n1e7 python bench.py --config cfg5 --steps 1 --warmup 3 --no-cpu --no-e2e --control host > $O/ncu_k1e.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k1g_aty_fused -s 10 -c 1 -o $O/k1g_cfg4 python bench.py --config cfg4 --geno --steps 1 --warmup 3 --no-cpu --no-e2e --control host > $O/ncu_k1g.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_chol_d2 -s 40 -c 1 -o $O/k4_d2_cfg2 python bench.py --config cfg2 --steps 1 --warmup 3 --no-cpu --no-e2e --control host > $O/ncu_d2.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_gram_fused -c 1 -o $O/k3_mxm_r10193 python tools/ncu_newton.py --r 10193 --n 20000 > $O/ncu_k3a.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_gram_fused -c 1 -o $O/k3_smw_r435 python tools/ncu_newton.py --r 435 > $O/ncu_k3b.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_small_cl -s 3 -c 1 -o $O/k7_cfg1 python bench.py --config cfg1 --steps 1 --warmup 3 --no-cpu --no-e2e > $O/ncu_k7.log 2>&1
+echo done >> $O/status.txt
