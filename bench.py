@@ -125,16 +125,18 @@ def k1_bytes(m, n, geno=False):
 
 
 def small_roofline(m, n, sts, dev_s, peak, peak_src):
-    """One-CTA path (k_small_solve, m ≤ 64, n ≤ 1024): no K1 launches; the whole solve is one
-    latency-bound kernel with A L2-resident.  Reported: the effective A-pass bandwidth of the solve
-    (passes × 8mn bytes / device time) against the HBM peak, for context only."""
+    """Single-launch small-problem path (k_small_cl: one 16-CTA cluster, A resident in distributed
+    shared memory; m ≤ 64, n ≤ 1024): no K1 launches; the whole solve is one latency-bound kernel.
+    Reported: the effective A-pass bandwidth of the solve (passes × 8mn bytes / device time) against
+    the HBM peak, for context only."""
     passes = sum(s["aty_passes"] for s in sts)
     achieved = passes * 8.0 * m * n / max(dev_s, 1e-30) / 1e9
     return {"bound": "latency", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": None, "peak_source": peak_src, "kernel": "k_small_solve",
+            "traffic": None, "peak_source": peak_src, "kernel": "k_small_cl",
             "bytes_per_launch": passes * 8 * m * n, "launches": len(sts), "mean_launch_us": dev_s / max(len(sts), 1) * 1e6,
             "share_of_step": 1.0,
-            "note": "m <= 64, n <= 1024: Algorithm 1 in one CTA (A streamed from L2 by TMA, 2-stage ring); latency-bound, not an HBM stream"}
+            "note": "m <= 64, n <= 1024: Algorithm 1 in one launch of one 16-CTA cluster (A resident in distributed "
+                    "shared memory); latency-bound (pivot chains, cluster barriers), not an HBM stream"}
 
 
 def geno_roofline(m, n, k1_avg, k1_gbs, hbm_peak, traffic):

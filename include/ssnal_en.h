@@ -111,9 +111,11 @@ double ssnal_en_lambda_max_l1(const ssnal_en_problem* p);
  *   carry_sigma=1 (ssnal_en_solve_path_device: point i > 0 starts at point i − 1's sigma_final
  *     instead of σ0 — reading R38 of P:411 "usually SsNAL-EN converges in just one iteration";
  *     0: every point restarts at σ0),
- *   small=1 (m ≤ 64 and n ≤ 1024, fp64 storage, unsharded, no CG strategy: the whole solve runs in
- *     one 512-thread CTA, k_small_solve — same iteration and statistics, reduction orders differ;
- *     0: the multi-kernel graph / host paths),
+ *   small=1 (m ≤ 64 and n ≤ 1024, fp64 storage, unsharded, no CG strategy: the whole solve is ONE
+ *     kernel launch — same iteration and statistics, reduction orders differ; 0: the multi-kernel
+ *     graph / host paths), small_cluster=1 (that launch is k_small_cl, one 16-CTA cluster with A
+ *     resident in distributed shared memory, when such a cluster is schedulable; 0: k_small_solve,
+ *     one 512-thread CTA streaming A from L2),
  *   K4 variants (identical contract, results equal up to rounding): chol_dsm=1 (DSMEM-resident
  *     16-CTA cluster Cholesky for N ≤ 96; 0: the L2-tiled k_chol_cluster for every N), chol_d2=1
  *     (split-ownership DSMEM Cholesky k_chol_d2 for 96 < N ≤ 512; needs chol_dsm=1),
@@ -135,7 +137,8 @@ int ssnal_en_set_option(ssnal_en_problem* p, const char* key, double value);
 
 /* Read-only introspection: "m", "n", "k1_cols", "k1_stages", "k1_grid", "k1_smem",
  * "cluster_size", "num_sms", "graph", "format", "cg_ratio", "cg_threshold", "carry_sigma", and which kernels a
- * solve on this handle uses: "small" (1: the one-CTA path k_small_solve), "chol_dsm" (1: k_chol_dsm
+ * solve on this handle uses: "small" (1: the single-launch small-problem path), "small_cluster" (1: that
+ * path runs k_small_cl, 0: k_small_solve), "chol_dsm" (1: k_chol_dsm
  * for N ≤ 96), "chol_d2" (1: k_chol_d2 for 96 < N ≤ 512).  Returns NaN for unknown keys. */
 double ssnal_en_get_info(const ssnal_en_problem* p, const char* key);
 

@@ -80,14 +80,57 @@ def test_max_over_ranks_without_group():
 
 
 def test_small_roofline_line():
-    """The one-CTA path has no K1 launches: the bench reports a latency-bound roofline for k_small_solve
-    with the effective A-pass bandwidth (passes × 8mn bytes / device time) against the HBM peak."""
+    """The single-launch small-problem path has no K1 launches: the bench reports a latency-bound roofline
+    for k_small_cl with the effective A-pass bandwidth (passes × 8mn bytes / device time) against the HBM peak."""
     sys.path.insert(0, ROOT)
     import bench
 
     sts = [{"aty_passes": 16}, {"aty_passes": 4}]
     r = bench.small_roofline(50, 1000, sts, 1e-3, 6500.0, "measured")
-    assert r["bound"] == "latency" and r["kernel"] == "k_small_solve" and r["unit"] == "GB/s"
+    assert r["bound"] == "latency" and r["kernel"] == "k_small_cl" and r["unit"] == "GB/s"
     assert r["bytes_per_launch"] == 20 * 8 * 50 * 1000
     assert r["achieved"] == pytest.approx(20 * 8 * 50 * 1000 / 1e-3 / 1e9)
     assert r["frac"] == pytest.approx(r["achieved"] / 6500.0) and r["launches"] == 2
+
+
+def test_cpu_leg_parity_block(tmp_path):
+    """The clean-process oracle leg of bench.py (cpu_baseline + the §8(d) parity block): fed the oracle's
+    own solutions as the 'GPU' solutions, every parity metric is exact; fed a perturbed x, it flags it."""
+    sys.path.insert(0, ROOT)
+    import numpy as np
+
+    import bench
+    import oracle
+    import synth
+
+    cfg = synth.CONFIGS["cfg1"]
+    A = synth.design(cfg)
+    b, _ = synth.response(cfg)
+    lm = oracle.lambda_max_l1(A, b)
+    xs, sts = [], []
+    for c in cfg.cs:
+        l1, l2 = bench.lambdas(cfg, lm, c)
+        x, _, st, _ = oracle.solve(A, b, l1, l2, sigma0=cfg.sigma0, tol=cfg.tol)
+        xs.append(x)
+        sts.append(st)
+    for bad in (False, True):
+        d = tmp_path / ("bad" if bad else "ok")
+        d.mkdir()
+        xg = np.array(xs)
+        if bad:
+            xg[0, np.argmax(np.abs(xg[0]))] *= 1.01
+        np.save(d / "x_gpu.npy", xg)
+        np.save(d / "w_gpu.npy", oracle.aty(A, synth.normals(cfg.seed, 12, cfg.m)))
+        json.dump([{k: s[k] for k in ("outer_iters", "newton_iters", "active", "status")} for s in sts],
+                  open(d / "gpu_stats.json", "w"))
+        bench.cpu_leg(str(d), "cfg1")
+        out = json.load(open(d / "cpu.json"))
+        cb, par = out["cpu_baseline"], out["parity"]
+        assert cb["kind"] == "oracle" and cb["value"] > 0 and cb["threads"] >= 1
+        assert par["aty_max_scaled_err"] == 0.0
+        p0 = par["points"][0]
+        assert p0["outer"][0] == p0["outer"][1] and p0["newton"][0] == p0["newton"][1]
+        if bad:
+            assert not par["ok"] and p0["xinf_rel"] > 1e-3
+        else:
+            assert par["ok"] and p0["obj_rel"] == 0.0 and p0["xinf_rel"] == 0.0 and p0["J_equal"]
