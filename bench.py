@@ -189,6 +189,22 @@ def host_solve_workload(Q, cfg, lm):
     return h2d, d2h
 
 
+def _host_room(bytes_per_rank, world):
+    """Whether every local rank can pin its own host copy of A for the e2e leg (25% headroom)."""
+    try:
+        import psutil
+
+        return psutil.virtual_memory().available > 1.25 * bytes_per_rank * world
+    except Exception:
+        return world == 1
+
+
+def _host_room_all(bytes_per_rank, world):
+    """_host_room decided jointly (every rank skips or runs the e2e leg: it contains collectives)."""
+    ok = _host_room(bytes_per_rank, world)
+    return ok if world == 1 else max_over_ranks(0.0 if ok else 1.0) == 0.0
+
+
 def step_summary(ts):
     """median and mean ± standard error of per-step device times (SURVEY §8(d) timing protocol)."""
     ts = list(ts)
@@ -305,6 +321,9 @@ def bench_ours(args, rank, world, local_rank):
                "d2h_bytes_per_step": d2h, "steps": len(e2e_times),
                "includes": "create (H2D codes + tables + b, validation, lambda_max pass) + solves + D2H x + destroy"}
         del codes_h, tab_h
+    elif not args.no_e2e and not args.shard and not _host_room_all(8 * m * n, world):
+        e2e = {"value": None, "unit": "s", "skipped": f"host RAM: {world} rank(s) x {8 * m * n / 1e9:.0f} GB of pinned A "
+                                                     "would not fit (psutil available memory)"}
     elif not args.no_e2e and not args.shard:
         A_host = torch.empty((n, m), dtype=torch.float64, pin_memory=True)
         A_host.copy_(dA)  # the same bytes as the device generator wrote (pinned host memory)

@@ -22,12 +22,22 @@ timeout 900 python bench.py --config cfg2 --shard --steps 10 --warmup 3 --no-cpu
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 20000 --csv --log-file $O/launches_cfg2.csv python bench.py --config cfg2 --steps 1 --warmup 3 --no-cpu --no-e2e --control host > $O/ncu_list2.log 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 20000 --csv --log-file $O/launches_cfg5.csv python bench.py --config cfg5 --steps 1 --warmup 3 --no-cpu --no-e2e --control host > $O/ncu_list5.log 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 20000 --csv --log-file $O/launches_cfg1.csv python bench.py --config cfg1 --steps 2 --warmup 3 --no-cpu --no-e2e > $O/ncu_list1.log 2>&1
-# --set full captures
+# --set full captures, summarised on the box (details + raw pages as CSV); the reports themselves are
+# deleted (gpurun copies back at most 64 MiB)
+summ() { ncu -i $O/$1.ncu-rep --page details --csv > $O/$1_details.csv 2>/dev/null; ncu -i $O/$1.ncu-rep --page raw --csv > $O/$1_raw.csv 2>/dev/null; ncu -i $O/$1.ncu-rep --page source --csv --print-source sass > $O/$1_sass.csv 2>/dev/null; gzip -f $O/$1_sass.csv; rm -f $O/$1.ncu-rep; }
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k1_aty_fused -s 10 -c 1 -o $O/k1_n1e7 python bench.py --config cfg5 --steps 1 --warmup 3 --no-cpu --no-e2e --control host > $O/ncu_k1.log 2>&1
+summ k1_n1e7
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k1e_epilogue -s 10 -c 1 -o $O/k1e_n1e7 python bench.py --config cfg5 --steps 1 --warmup 3 --no-cpu --no-e2e --control host > $O/ncu_k1e.log 2>&1
+summ k1e_n1e7
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k1g_aty_fused -s 10 -c 1 -o $O/k1g_cfg4 python bench.py --config cfg4 --geno --steps 1 --warmup 3 --no-cpu --no-e2e --control host > $O/ncu_k1g.log 2>&1
+summ k1g_cfg4
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_chol_d2 -s 40 -c 1 -o $O/k4_d2_cfg2 python bench.py --config cfg2 --steps 1 --warmup 3 --no-cpu --no-e2e --control host > $O/ncu_d2.log 2>&1
+summ k4_d2_cfg2
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_gram_fused -c 1 -o $O/k3_mxm_r10193 python tools/ncu_newton.py --r 10193 --n 20000 > $O/ncu_k3a.log 2>&1
+summ k3_mxm_r10193
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_gram_fused -c 1 -o $O/k3_smw_r435 python tools/ncu_newton.py --r 435 > $O/ncu_k3b.log 2>&1
+summ k3_smw_r435
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_small_cl -s 3 -c 1 -o $O/k7_cfg1 python bench.py --config cfg1 --steps 1 --warmup 3 --no-cpu --no-e2e > $O/ncu_k7.log 2>&1
+summ k7_cfg1
+du -sh $O >> $O/status.txt
 echo done >> $O/status.txt
