@@ -285,9 +285,8 @@ __global__ void __cluster_dims__(kClCtas, 1, 1) __launch_bounds__(kClThreads, 1)
       const bool smw = r < m;
       br = smw ? 1 : 2;
       const int N = smw ? r : m;
-      // Matrix entries (i, c), i ≥ c (rows i ≤ N: row N is the right-hand side).  SMW: every CTA forms
-      // the whole matrix from the gathered columns.  m × m: rank q computes the columns c ≡ q (mod 16),
-      // warp per column, lanes over rows, and stores them into every rank's copy.
+      // Matrix entries (i, c), i ≥ c (rows i ≤ N: row N is the right-hand side): rank q computes the
+      // columns c ≡ q (mod 16), warp per column, lanes over rows, and stores them into every rank's copy.
       if (smw) {
         // gather the r active columns (position j = offs[rank] + local index): warp w takes positions
         // j ≡ w (mod 8); the owner's local index and the column rows arrive in two DSMEM round trips
@@ -318,9 +317,8 @@ __global__ void __cluster_dims__(kClCtas, 1, 1) __launch_bounds__(kClThreads, 1)
           }
         }
         __syncthreads();
-        // κ⁻¹I_r + A_JᵀA_J (lower) and u = A_Jᵀg (row N): r < m ≤ 64 columns are already in every
-        // CTA, so each CTA forms the whole (small) matrix itself — no DSMEM stores, no cluster barrier
-        for (int c = warp; c < N; c += kClNW) {
+        // κ⁻¹I_r + A_JᵀA_J (lower) and u = A_Jᵀg (row N)
+        for (int c = q + kClCtas * warp; c < N; c += kClCtas * kClNW) {
           const double* bc = AJ + c * m;
           for (int i = c + lane; i <= N; i += 32) {
             const double* ai = i < N ? AJ + i * m : g;
@@ -336,10 +334,9 @@ __global__ void __cluster_dims__(kClCtas, 1, 1) __launch_bounds__(kClThreads, 1)
               v = __dadd_rn(v, 1.0 / kappa);
               if (jit != 0.0) v = __fma_rn(v, jit, v);
             }
-            Mx[i + c * kClLd] = v;
+            for (int rq = 0; rq < kClCtas; ++rq) cluster.map_shared_rank(Mx, rq)[i + c * kClLd] = v;
           }
         }
-        __syncthreads();
       } else {
         // local partial Gram Σ_{a ∈ J_q} a_a a_aᵀ (lower m × m, AJ[i + 64 c]), then this rank's columns of
         // I_m + κ Σ_ranks (partials), the partials summed in rank order, into every rank's copy
@@ -372,8 +369,8 @@ __global__ void __cluster_dims__(kClCtas, 1, 1) __launch_bounds__(kClThreads, 1)
             for (int rq = 0; rq < kClCtas; ++rq) cluster.map_shared_rank(Mx, rq)[i + c * kClLd] = v;
           }
         if (tid < m) Mx[m + tid * kClLd] = g[tid];
-        cluster.sync();  // every copy of the Newton matrix complete (and the partial Grams read)
       }
+      cluster.sync();  // every copy of the Newton matrix complete (and the partial Grams read)
       CPROF_ADD(3);
 #ifdef SMALL_PROF
       if (q == 0 && tid == 0) g_small_prof[6] += (unsigned long long)N << 32;  // Σ N in the high half
