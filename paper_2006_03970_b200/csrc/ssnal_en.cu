@@ -1894,7 +1894,7 @@ extern "C" {
 
 const char* ssnal_en_last_error(void) { return g_err.c_str(); }
 
-const char* ssnal_en_version(void) { return "ssnal_en_b200 0.1 (sm_100a, fp64)"; }
+const char* ssnal_en_version(void) { return "ssnal_en_b200 0.2 (sm_100a, fp64)"; }
 
 static int create_common(ssnal_en_problem* P) {
   CK(cudaGetDevice(&P->dev));

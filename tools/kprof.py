@@ -19,6 +19,10 @@ import torch  # noqa: E402
 from torch.profiler import ProfilerActivity, profile  # noqa: E402
 
 import synth  # noqa: E402
+import paper_2006_03970_b200.ssnal_en as _se  # noqa: E402
+
+if os.environ.get("SSNAL_EN_LIB"):  # A/B a variant build of the library (probe use only)
+    _se.LIB_PATH = os.environ["SSNAL_EN_LIB"]
 from paper_2006_03970_b200 import Problem  # noqa: E402
 
 
@@ -75,7 +79,8 @@ def main():
 def newton(args):
     import numpy as np
 
-    m, n = 500, 4000
+    m = 500
+    n = max(4000, 2 * max(int(v) for v in args.newton.split(",")))
     cfg = synth.Config("t", m, n, synth.IID_STD, 5, 1.0, 2.0, 5.0, 0.7, (0.5,), 3)
     A = synth.design(cfg)
     b, _ = synth.response(cfg)
