@@ -449,10 +449,19 @@ def cpu_baseline(cfg, args, x_gpu, w_probe, gpu_stats):
         return {"value": None, "unit": "s", "cores": threads, "kind": "oracle",
                 "error": (r.stderr or r.stdout)[-400:]}, None
     d = json.load(open(out))
+    cb = d["cpu_baseline"]
+    if cfg.name in ("cfg1", "cfg2", "cfg3") and threads > 1:
+        # the oracle also at one thread for the configs where that stays bounded
+        os.remove(os.path.join(tmp, "x_gpu.npy"))  # timing only, no second parity block
+        env["OMP_NUM_THREADS"] = "1"
+        r1 = subprocess.run(cmd, env=env, capture_output=True, text=True)
+        if r1.returncode == 0 and os.path.exists(out):
+            d1 = json.load(open(out))["cpu_baseline"]
+            cb["one_thread"] = {"value": d1["value"], "threads": 1, "speedup_nproc": d1["value"] / cb["value"]}
     for f in os.listdir(tmp):
         os.remove(os.path.join(tmp, f))
     os.rmdir(tmp)
-    return d["cpu_baseline"], d["parity"]
+    return cb, d["parity"]
 
 
 def cpu_leg(tmp, cfg_name):

@@ -56,6 +56,16 @@ struct SmallParams {
   int64_t* rx0;     // |supp x0| for the statistics
   double* obj;      // out: [½‖Ax − b‖², Σ|x|, Σx², nnz] of the final x (nullable)
   double* resid;    // out: A x − b (m), for the certify pass (nullable)
+  // k_small_cl launch-overhead trims (nullable / 0 = off): settings by value instead of an H2D copy of
+  // the control block, the carried σ0 read from the device, results written straight into the
+  // caller's mapped pinned host mirrors and the caller's device x buffer (no copies after the launch)
+  int use_cin;
+  DevCtl cin;
+  const double* sigma_in;
+  DevCtl* cout_host;
+  EvalOut* ev_host;
+  double* rx0_host;  // |supp x0| as int64 bits (scratch slot 20)
+  double* xout;
 };
 
 // shared-memory layout (doubles unless noted)

@@ -95,7 +95,10 @@ __global__ void __cluster_dims__(kClCtas, 1, 1) __launch_bounds__(kClThreads, 1)
   constexpr unsigned FULL = 0xffffffffu;
 
   __shared__ DevCtl C;
-  if (tid == 0) C = *p.C;
+  if (tid == 0) {
+    C = p.use_cin ? p.cin : *p.C;
+    if (p.sigma_in) C.sigma = *p.sigma_in;  // σ0 carried from the previous path point (R38)
+  }
   for (int e = tid; e < nl * m; e += kClThreads) As[e] = __ldg(p.A + (int64_t)c0 * m + e);
   for (int i = tid; i < nl; i += kClThreads) {  // cold start (R8): x = 0, y0 = 0, w0 = Aᵀ0 = 0
     xs[i] = p.cold ? 0.0 : p.x[c0 + i];
@@ -105,7 +108,10 @@ __global__ void __cluster_dims__(kClCtas, 1, 1) __launch_bounds__(kClThreads, 1)
     ys[tid] = p.cold ? 0.0 : p.y0[tid];
     bs[tid] = p.b[tid];
   }
-  if (p.cold && q == 0 && tid == 0) *p.rx0 = 0;
+  if (p.cold && q == 0 && tid == 0) {
+    *p.rx0 = 0;
+    if (p.rx0_host) *reinterpret_cast<int64_t*>(p.rx0_host) = 0;
+  }
   __syncthreads();
   const double l1 = C.l1, l2 = C.l2, tol = C.tol, nb = C.nb;
   int rbuf = 0;  // record buffer parity (see exchange)
@@ -694,29 +700,35 @@ __global__ void __cluster_dims__(kClCtas, 1, 1) __launch_bounds__(kClThreads, 1)
     }
   }
   // ---- outputs ----
-  for (int i = tid; i < nl; i += kClThreads) p.x[c0 + i] = xs[i];
+  for (int i = tid; i < nl; i += kClThreads) {
+    p.x[c0 + i] = xs[i];
+    if (p.xout) p.xout[c0 + i] = xs[i];
+  }
   if (q == 0 && tid == 0) {
-    DevCtl* o = p.C;
-    o->outer_iters = k;
-    o->newton_iters = newton;
-    o->psi_evals = psi_evals;
-    o->backtracks = backtracks;
-    o->aty_passes = aty;
-    for (int b = 0; b < 4; ++b) o->branch_steps[b] = brs[b];
-    o->cg_iters = 0;
-    o->jitter_retries = jretries;
-    o->stalled = stalled;
-    o->res1 = res1;
-    o->res3 = res3;
-    o->sigma_final = sigma;
-    o->converged = converged;
-    o->numeric = numeric;
-    o->numeric_kind = numeric_kind;
-    o->numeric_r = numeric_r;
-    o->seg_outer = o->seg_inner = o->seg_bt = o->seg_grad = 0;
-    o->k1_ns = 0;
-    o->k1_cnt = 0;
+    DevCtl o = C;  // settings as used, then the statistics
+    o.outer_iters = k;
+    o.newton_iters = newton;
+    o.psi_evals = psi_evals;
+    o.backtracks = backtracks;
+    o.aty_passes = aty;
+    for (int b = 0; b < 4; ++b) o.branch_steps[b] = brs[b];
+    o.cg_iters = 0;
+    o.jitter_retries = jretries;
+    o.stalled = stalled;
+    o.res1 = res1;
+    o.res3 = res3;
+    o.sigma_final = sigma;
+    o.converged = converged;
+    o.numeric = numeric;
+    o.numeric_kind = numeric_kind;
+    o.numeric_r = numeric_r;
+    o.seg_outer = o.seg_inner = o.seg_bt = o.seg_grad = 0;
+    o.k1_ns = 0;
+    o.k1_cnt = 0;
+    *p.C = o;  // device control block (the carried σ of a path is read from it)
     *p.ev = ev;
+    if (p.cout_host) *p.cout_host = o;  // the mapped host mirrors: no copies after the launch
+    if (p.ev_host) *p.ev_host = ev;
   }
   cluster.sync();  // no rank exits while another may still read its shared memory
 }

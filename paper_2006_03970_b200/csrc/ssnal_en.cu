@@ -382,6 +382,9 @@ struct ssnal_en_problem {
   std::vector<cudaEvent_t> path_ev;
   // option carry_sigma (reading R38): path point i starts at point i − 1's final σ
   int carry_sigma = 1;
+  // small-problem cluster path: the caller's device x buffer the kernel writes directly (no copy)
+  double* direct_xout = nullptr;
+  bool xout_done = false;
 };
 
 namespace {
@@ -1760,13 +1763,27 @@ int solve_small_core(ssnal_en_problem* P, double l1, double l2, double sigma0, d
   h->jitter = P->jitter;
   h->inject = P->inject_fail;
   h->inner_tol_mode = P->inner_tol_mode;
-  CK(cudaMemcpyAsync(P->ctl, h, sizeof(DevCtl), cudaMemcpyHostToDevice, P->st));
-  if (sigma_dev)  // σ0 carried on the device from the previous path point (R38)
-    CK(cudaMemcpyAsync(&P->ctl->sigma, sigma_dev, 8, cudaMemcpyDeviceToDevice, P->st));
   SmallParams sp;
+  memset(&sp, 0, sizeof(sp));
+  if (cl) {  // settings by value, results straight into the mapped host mirrors (no copies)
+    sp.use_cin = 1;
+    sp.cin = *h;
+    sp.sigma_in = sigma_dev;
+    CK(cudaHostGetDevicePointer((void**)&sp.cout_host, h, 0));
+    CK(cudaHostGetDevicePointer((void**)&sp.ev_host, P->ev_out_host, 0));
+    double* sh_dev = nullptr;
+    CK(cudaHostGetDevicePointer((void**)&sh_dev, P->scratch_host, 0));
+    sp.obj = sh_dev + 16;
+    sp.rx0_host = sh_dev + 20;
+    sp.xout = P->direct_xout;
+    P->xout_done = P->direct_xout != nullptr;
+  } else {
+    CK(cudaMemcpyAsync(P->ctl, h, sizeof(DevCtl), cudaMemcpyHostToDevice, P->st));
+    if (sigma_dev)  // σ0 carried on the device from the previous path point (R38)
+      CK(cudaMemcpyAsync(&P->ctl->sigma, sigma_dev, 8, cudaMemcpyDeviceToDevice, P->st));
+  }
   sp.cold = (cl && !have_x0) ? 1 : 0;
   sp.rx0 = P->r_dev + 4;
-  sp.obj = cl ? P->scratch + 16 : nullptr;
   sp.resid = cl ? P->tmpm : nullptr;
   sp.A = P->A;
   sp.b = P->b;
@@ -1788,12 +1805,11 @@ int solve_small_core(ssnal_en_problem* P, double l1, double l2, double sigma0, d
   CKL();
   if (!cl) {
     if ((rc = launch_objective(P))) return rc;
-  } else {
-    CK(cudaMemcpyAsync(P->scratch_host + 16, P->scratch + 16, 4 * 8, cudaMemcpyDeviceToHost, P->st));
+    CK(cudaMemcpyAsync(h, P->ctl, sizeof(DevCtl), cudaMemcpyDeviceToHost, P->st));
+    CK(cudaMemcpyAsync(P->ev_out_host, P->ev_dev, sizeof(EvalOut), cudaMemcpyDeviceToHost, P->st));
+  } else if (have_x0) {  // warm start: |supp x0| was counted by init_point on the device
     CK(cudaMemcpyAsync(P->scratch_host + 20, P->r_dev + 4, 8, cudaMemcpyDeviceToHost, P->st));
   }
-  CK(cudaMemcpyAsync(h, P->ctl, sizeof(DevCtl), cudaMemcpyDeviceToHost, P->st));
-  CK(cudaMemcpyAsync(P->ev_out_host, P->ev_dev, sizeof(EvalOut), cudaMemcpyDeviceToHost, P->st));
   P->stat_l1 = l1;
   P->stat_l2 = l2;
   P->stat_warm_pass = (have_x0 && P->init_mode == 1);
@@ -2254,13 +2270,17 @@ static int solve_wrapped(ssnal_en_problem* P, double l1, double l2, double sigma
     have_x0 = P->comm_host[1] > 0;
   }
   ssnal_en_stats S;
+  P->direct_xout = (x_out && xout_dev && x_out != x0) ? x_out : nullptr;
+  P->xout_done = false;
   rc = small_eligible(P)                ? solve_small_core(P, l1, l2, sigma0, tol, have_x0, &S)
        : (P->use_graph && !sharded(P)) ? solve_graph_core(P, l1, l2, sigma0, tol, have_x0, &S)
                                        : solve_core(P, l1, l2, sigma0, tol, have_x0, &S);
   if (rc == SSNAL_ECUDA || rc == SSNAL_EINVAL) return rc;
-  if (x_out) {
+  if (x_out && !P->xout_done) {
     CK(cudaMemcpyAsync(x_out, P->x, P->n * 8, xout_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, P->st));
   }
+  P->direct_xout = nullptr;
+  P->xout_done = false;
   CK(cudaEventRecord(e1, P->st));
   CK(cudaStreamSynchronize(P->st));
   harvest_k1(P);
@@ -2359,7 +2379,7 @@ int ssnal_en_solve_path_device(ssnal_en_problem* P, int64_t npts, const double* 
     if (P->path_slots) cudaFreeHost(P->path_slots);
     P->path_slots = nullptr;
     P->path_cap = 0;
-    CK(cudaHostAlloc(&P->path_slots, sizeof(PathSlot) * npts, cudaHostAllocDefault));
+    CK(cudaHostAlloc(&P->path_slots, sizeof(PathSlot) * npts, cudaHostAllocMapped));  // kernels write results here
     P->path_cap = npts;
   }
   while ((int64_t)P->path_ev.size() < 2 * npts) {
@@ -2386,11 +2406,15 @@ int ssnal_en_solve_path_device(ssnal_en_problem* P, int64_t npts, const double* 
     const double* xi = i == 0 ? x0 : x_out + (i - 1) * n;
     if (xi) CK(cudaMemcpyAsync(P->x, xi, n * 8, cudaMemcpyDeviceToDevice, P->st));
     const double* sig_in = (P->carry_sigma && i > 0) ? sigma_carry : nullptr;
+    P->direct_xout = x_out + i * n;
+    P->xout_done = false;
     rc = small_eligible(P) ? solve_small_core(P, lambda1[i], lambda2[i], sigma0, tol, xi != nullptr, &S[i], sig_in)
                            : solve_graph_core(P, lambda1[i], lambda2[i], sigma0, tol, xi != nullptr, &S[i], sig_in);
     if (rc == SSNAL_OK && P->carry_sigma)
       CK(cudaMemcpyAsync(sigma_carry, &P->ctl->sigma_final, 8, cudaMemcpyDeviceToDevice, P->st));
-    if (rc == SSNAL_OK) CK(cudaMemcpyAsync(x_out + i * n, P->x, n * 8, cudaMemcpyDeviceToDevice, P->st));
+    if (rc == SSNAL_OK && !P->xout_done) CK(cudaMemcpyAsync(x_out + i * n, P->x, n * 8, cudaMemcpyDeviceToDevice, P->st));
+    P->direct_xout = nullptr;
+    P->xout_done = false;
     CK(cudaEventRecord(P->path_ev[2 * i + 1], P->st));
     slot[i].l1 = P->stat_l1;
     slot[i].l2 = P->stat_l2;
