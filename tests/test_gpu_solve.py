@@ -147,6 +147,17 @@ def test_invalid_arguments():
                 P.solve(*args)
         with pytest.raises(SsnalError):
             P.set_option("no_such_option", 1)
+        for key, bad in (("carry_sigma", 2), ("small_cluster", 3), ("cluster_size", 3), ("cluster_size", 32)):
+            with pytest.raises(SsnalError):
+                P.set_option(key, bad)
+        # cluster_size 0 = auto (the largest schedulable power of two); an explicit schedulable size is kept
+        P.set_option("cluster_size", 0)
+        auto = P.info("cluster_size")
+        assert auto in (1, 2, 4, 8, 16)
+        P.set_option("cluster_size", 8)
+        assert P.info("cluster_size") == 8
+        P.set_option("carry_sigma", 0)
+        assert P.info("carry_sigma") == 0
 
 
 EDGE = [  # (kind, m, n, c, alpha, seed): tiny / odd / largest-m shapes; small c pushes r ≥ m (Eq. (18) branch)
