@@ -734,6 +734,10 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hook (tools/, never used for a reported number): run the multi-rank code path with every
+    # rank on device 0 and a gloo group, on a box with one GPU
+    if os.environ.get("BENCH_TEST_ONE_DEVICE") == "1":
+        local_rank = 0
 
     if args.impl == "reference":
         res = bench_reference(args, rank, world)
@@ -755,7 +759,7 @@ def main():
 
         torch.cuda.set_device(local_rank)
         if world > 1:
-            dist.init_process_group("nccl")
+            dist.init_process_group("gloo" if os.environ.get("BENCH_TEST_ONE_DEVICE") == "1" else "nccl")
         else:  # a one-rank NCCL group, so the sharded path runs its real all-reduces
             import socket
 

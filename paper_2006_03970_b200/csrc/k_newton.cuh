@@ -572,8 +572,9 @@ __global__ void __cluster_dims__(kGramCS, 1, 1) __launch_bounds__(256)
         for (int e = 0; e < 2; ++e) Pt[(16 * wr + 8 * i + gq) * 65 + 32 * wc + 8 * j + 2 * t + e] = acc[i][j][e];
     cluster.sync();
     const int64_t o0 = (int64_t)ti * GT, o1 = (int64_t)tj * GT;
-    for (int e = tid; e < 8 * GT; e += 256) {
-      const int w = 8 * s + e / GT, k = e % GT;
+    constexpr int RPR = GT / kGramCS;  // output rows reduced by each rank
+    for (int e = tid; e < RPR * GT; e += 256) {
+      const int w = RPR * s + e / GT, k = e % GT;
       const int64_t oi = o0 + w, oj = o1 + k;
       if (oi < ga.nout && oj < ga.nout && oi >= oj) {
         double v = 0.0;
