@@ -657,48 +657,61 @@ def bench_select(args):
 
 
 def sweep(args):
-    """K1 bandwidth sweep: m = 500, n = 1e5 … 1e7, r ≈ 1e-4 n."""
+    """K1 bandwidth sweep: m = 500, n = 1e5 … 1e7, plus spot checks at m = 50 and m = 800
+    (n = 1e6); y ~ N(0, I), x with 100 nonzeros ±U[1,2], σ = 1, λ1 at the (1 − 1e-4) quantile of |x − σAᵀy|
+    (r ≈ 1e-4 n, the typical regime) and at the median (r ≈ n/2, the compaction worst case); median of
+    --sweep-reps launches.  t_k1 = CUDA events around the K1 launch alone (option time_k1, get_info
+    "k1_time_s"); t_call = the whole hook (K1 + the ordered concatenation + the ψ/∇ψ reduction + sync)."""
     import torch
 
     from paper_2006_03970_b200 import Problem
 
     peak, _ = _peaks()
-    base = synth.CONFIGS["cfg5"]
-    ns = [int(v) for v in args.sweep_n.split(",")]
     stream = torch.cuda.current_stream()
-    nmax = max(ns)
-    dA = torch.empty((nmax, base.m), dtype=torch.float64, device="cuda")
-    synth.fill_device(base, dA.data_ptr(), stream.cuda_stream)
-    torch.cuda.synchronize()
-    for n in ns:
-        m = base.m
-        b = torch.from_numpy(synth.normals(5, 11, m)).cuda()
-        P = Problem.from_device(dA.data_ptr(), b.data_ptr(), m, n, stream.cuda_stream, keep=(dA, b))
-        y = torch.from_numpy(synth.normals(5, 12, m)).cuda()
-        x = torch.zeros(n, dtype=torch.float64, device="cuda")
-        w = torch.empty(n, dtype=torch.float64, device="cuda")
-        J = torch.empty(n, dtype=torch.int32, device="cuda")
-        PJ = torch.empty(n, dtype=torch.float64, device="cuda")
-        # λ1 at the (1 − 1e-4) quantile of |Aᵀy| (σ = 1, x = 0): r ≈ 1e-4 n
-        P.aty_fused(y.data_ptr(), x.data_ptr(), 1.0, 1e30, 0.1, w.data_ptr(), J.data_ptr(), PJ.data_ptr())
-        q = float(torch.quantile(w.abs()[: min(n, 16_000_000)].float(), 1 - 1e-4).item()) if n > 1 else 0.0
-        for lab, l1 in (("r~1e-4n", q), ("r~n/2", float(w.abs().median().item()))):
-            P.set_option("time_k1", 1)
-            ts = []
-            for it in range(args.sweep_reps + 3):
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
-                r, _ = P.aty_fused(y.data_ptr(), x.data_ptr(), 1.0, l1, 0.1, w.data_ptr(), J.data_ptr(),
-                                   PJ.data_ptr())
-                e1.record(stream)
-                torch.cuda.synchronize()
-                if it >= 3:
-                    ts.append(e0.elapsed_time(e1) * 1e-3)
-            t = statistics.median(ts)
-            gbs = k1_bytes(m, n) / t / 1e9
-            print(json.dumps({"sweep": "k1", "m": m, "n": n, "case": lab, "r": r, "t_med_us": t * 1e6,
-                              "GBps": gbs, "frac_of_measured": gbs / peak, "pct_of_8TBps": gbs / 8000}), flush=True)
-        P.close()
+    cases = [(500, int(v)) for v in args.sweep_n.split(",")] + [(50, 1_000_000), (800, 1_000_000)]
+    for m in sorted({mm for mm, _ in cases}):
+        base = synth.scaled(synth.CONFIGS["cfg5"], m=m, n=max(nn for mm, nn in cases if mm == m))
+        dA = torch.empty((base.n, m), dtype=torch.float64, device="cuda")
+        synth.fill_device(base, dA.data_ptr(), stream.cuda_stream)
+        torch.cuda.synchronize()
+        for n in [nn for mm, nn in cases if mm == m]:
+            b = torch.from_numpy(synth.normals(5, 11, m)).cuda()
+            P = Problem.from_device(dA.data_ptr(), b.data_ptr(), m, n, stream.cuda_stream, keep=(dA, b))
+            y = torch.from_numpy(synth.normals(5, 12, m)).cuda()
+            xh = np.zeros(n)
+            k = min(100, n)
+            idx = np.unique((synth.uniforms(5, 13, k) * n).astype(np.int64) % n)
+            xh[idx] = np.where(synth.uniforms(5, 14, len(idx)) < 0.5, -1.0, 1.0) * (1.0 + synth.uniforms(5, 15, len(idx)))
+            x = torch.from_numpy(xh).cuda()
+            w = torch.empty(n, dtype=torch.float64, device="cuda")
+            J = torch.empty(n, dtype=torch.int32, device="cuda")
+            PJ = torch.empty(n, dtype=torch.float64, device="cuda")
+            P.aty_fused(y.data_ptr(), x.data_ptr(), 1.0, 1e30, 0.1, w.data_ptr(), J.data_ptr(), PJ.data_ptr())
+            t_abs = (x - w).abs()[: min(n, 16_000_000)].float()  # |x − σw| with σ = 1
+            q = float(torch.quantile(t_abs, 1 - 1e-4).item()) if n > 1 else 0.0
+            for lab, l1 in (("r~1e-4n", q), ("r~n/2", float(t_abs.median().item()))):
+                ts = []
+                for it in range(args.sweep_reps + 3):
+                    if it == 3:
+                        P.set_option("time_k1", 1)  # resets the K1 accumulators after the warm-ups
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                    r, _ = P.aty_fused(y.data_ptr(), x.data_ptr(), 1.0, l1, 0.1, w.data_ptr(), J.data_ptr(),
+                                       PJ.data_ptr())
+                    e1.record(stream)
+                    torch.cuda.synchronize()
+                    if it >= 3:
+                        ts.append(e0.elapsed_time(e1) * 1e-3)
+                t_call = statistics.median(ts)
+                t_k1 = P.info("k1_time_s") / max(P.info("k1_launches"), 1)
+                P.set_option("time_k1", 0)
+                gbs = k1_bytes(m, n) / t_k1 / 1e9
+                print(json.dumps({"sweep": "k1", "m": m, "n": n, "case": lab, "r": r, "t_k1_us": t_k1 * 1e6,
+                                  "t_call_us": t_call * 1e6, "GBps": gbs, "frac_of_measured": gbs / peak,
+                                  "pct_of_8TBps": gbs / 8000}), flush=True)
+            P.close()
+        del dA
+        torch.cuda.empty_cache()
 
 
 def main():
@@ -723,7 +736,7 @@ def main():
     ap.add_argument("--shard", action="store_true",
                     help="column-sharded solve across the ranks (SURVEY 8(f3)) instead of replicas")
     ap.add_argument("--sweep-n", default="100000,200000,500000,1000000,2000000,5000000,10000000")
-    ap.add_argument("--sweep-reps", type=int, default=20)
+    ap.add_argument("--sweep-reps", type=int, default=50)
     args = ap.parse_args()
     if args.cpu_leg:
         cpu_leg(args.cpu_leg, args.config)

@@ -136,7 +136,9 @@ double ssnal_en_lambda_max_l1(const ssnal_en_problem* p);
 int ssnal_en_set_option(ssnal_en_problem* p, const char* key, double value);
 
 /* Read-only introspection: "m", "n", "k1_cols", "k1_stages", "k1_grid", "k1_smem",
- * "cluster_size", "num_sms", "graph", "format", "cg_ratio", "cg_threshold", "carry_sigma", and which kernels a
+ * "cluster_size", "num_sms", "graph", "format", "cg_ratio", "cg_threshold", "carry_sigma", "k1_time_s" /
+ * "k1_launches" (Σ device time and count of the K1 launches of ssnal_en_aty_fused calls since option time_k1
+ * was last set; CUDA events around the K1 launch alone), and which kernels a
  * solve on this handle uses: "small" (1: the single-launch small-problem path), "small_cluster" (1: that
  * path runs k_small_cl, 0: k_small_solve), "chol_dsm" (1: k_chol_dsm
  * for N ≤ 96), "chol_d2" (1: k_chol_d2 for 96 < N ≤ 512).  Returns NaN for unknown keys. */

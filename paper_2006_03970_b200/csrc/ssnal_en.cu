@@ -2168,7 +2168,11 @@ int ssnal_en_set_option(ssnal_en_problem* P, const char* key, double v) {
   else if (k == "max_inner" && v >= 1) P->max_inner = (int)v;
   else if (k == "max_backtracks" && v >= 0) P->max_bt = (int)v;
   else if (k == "init_mode" && (v == 0 || v == 1)) P->init_mode = (int)v;
-  else if (k == "time_k1") P->time_k1 = v != 0;
+  else if (k == "time_k1") {  // also resets the K1 timing accumulators read by get_info("k1_time_s")
+    P->time_k1 = v != 0;
+    P->k1_time = 0;
+    P->k1_count = 0;
+  }
   else if (k == "certify" && (v == 0 || v == 1)) P->certify = (int)v;
   else if (k == "graph" && (v == 0 || v == 1)) P->use_graph = (int)v;
   else if (k == "cg_ratio" && v >= 0) {
@@ -2239,6 +2243,8 @@ double ssnal_en_get_info(const ssnal_en_problem* P, const char* key) {
   if (k == "cg_ratio") return P->cg_ratio;
   if (k == "cg_threshold") return P->cg_threshold;
   if (k == "carry_sigma") return P->carry_sigma;
+  if (k == "k1_time_s") return P->k1_time;       // Σ K1 launch times timed by the hook calls (option time_k1)
+  if (k == "k1_launches") return P->k1_count;
   return NAN;
 }
 
@@ -2495,6 +2501,7 @@ int ssnal_en_aty_fused(ssnal_en_problem* P, const double* y, const double* x, do
   EvalOut e;
   rc = fetch_eval(P, 3, &e);
   if (rc) return rc;
+  harvest_k1(P);  // option time_k1: the K1 launch's own event time (get_info "k1_time_s")
   if (r_out) *r_out = e.r;
   if (partials_out)
     for (int j = 0; j < 4; ++j) partials_out[j] = e.s[j];
