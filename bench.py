@@ -236,8 +236,8 @@ def bench_ours(args, rank, world, local_rank):
         torch.cuda.synchronize()
         P = Problem.from_geno_device(dcodes.data_ptr(), stride, dtab.data_ptr(), db.data_ptr(), m, n,
                                      stream.cuda_stream, keep=(dcodes, dtab, db))
-    elif args.shard:  # §8(f3): this rank owns columns [j0, j1); cross-column sums by NCCL all-reduce
-        from paper_2006_03970_b200.shard import column_range, torch_allreduce
+    elif args.shard:  # §8(f3): this rank owns columns [j0, j1); cross-column sums over the ranks
+        from paper_2006_03970_b200.shard import attach_peers, column_range, torch_allreduce
 
         j0, j1 = column_range(cfg.n, rank, world)
         n = j1 - j0
@@ -245,7 +245,10 @@ def bench_ours(args, rank, world, local_rank):
         synth.fill_device(cfg, dA.data_ptr(), stream.cuda_stream, j0, j1)
         torch.cuda.synchronize()
         P = Problem.from_device(dA.data_ptr(), db.data_ptr(), m, n, stream.cuda_stream, keep=(dA, db))
-        P.set_comm(torch_allreduce(), rank, world)
+        if args.shard_comm == "peer":  # device-resident exchanges over peer memory (CUDA IPC, NVLink)
+            attach_peers(P)
+        else:  # a host callback per exchange: NCCL all-reduce (host-driven control)
+            P.set_comm(torch_allreduce(), rank, world)
     else:
         dA = torch.empty((n, m), dtype=torch.float64, device="cuda")
         synth.fill_device(cfg, dA.data_ptr(), stream.cuda_stream)
@@ -373,11 +376,14 @@ def bench_ours(args, rank, world, local_rank):
                                                               if cfg.path else "cold solves c=" + ",".join(str(c) for c in cfg.cs)),
                    "m": m, "n": cfg.n, "alpha": cfg.alpha, "tol": cfg.tol, "sigma0": cfg.sigma0,
                    "l2_policy": f"A = {8 * m * n / 1e6:.0f} MB > 126 MB L2 (no flush needed)",
-                   "parallelism": (f"column-sharded x{world}: rank q owns n/{world} columns, NCCL all-reduce of the "
-                                   "per-evaluation partials and the Newton-system exchange (SURVEY 8(f3))"
+                   "parallelism": ((f"column-sharded x{world}: rank q owns n/{world} columns; per-evaluation "
+                                    "partials and the Newton-system exchange (SURVEY 8(f3)) "
+                                    + ("as device kernels over peer memory (CUDA IPC regions, rank-ordered sums)"
+                                       if args.shard_comm == "peer" else "by NCCL all-reduce host callbacks"))
                                    if args.shard else f"replicas x{world}"),
                    "control": ("device-resident, one CUDA graph per solve (nested conditional WHILE)"
-                               if args.control == "graph" and not args.shard else "host-driven (per-evaluation readback)"),
+                               if args.control == "graph" and (not args.shard or args.shard_comm == "peer")
+                               else "host-driven (per-evaluation readback)"),
                    "storage": ("packed 2-bit genotype codes + per-column tables (SURVEY 8(f4))" if args.geno
                                else "fp64 column-major"),
                    "path_sigma": "carried from point to point (reading R38, P:411)" if cfg.path else None,
@@ -735,6 +741,8 @@ def main():
     ap.add_argument("--cv", type=int, default=0, help="with --select: k-fold cross-validation over a 20-point grid")
     ap.add_argument("--shard", action="store_true",
                     help="column-sharded solve across the ranks (SURVEY 8(f3)) instead of replicas")
+    ap.add_argument("--shard-comm", default="peer", choices=["peer", "nccl"],
+                    help="with --shard: device-resident exchanges over peer memory (default) or NCCL host callbacks")
     ap.add_argument("--sweep-n", default="100000,200000,500000,1000000,2000000,5000000,10000000")
     ap.add_argument("--sweep-reps", type=int, default=50)
     args = ap.parse_args()
@@ -751,6 +759,8 @@ def main():
     # rank on device 0 and a gloo group, on a box with one GPU
     if os.environ.get("BENCH_TEST_ONE_DEVICE") == "1":
         local_rank = 0
+        if world > 1:  # ranks sharing one GPU must not spin on one another: host-callback exchanges
+            args.shard_comm = "nccl"
 
     if args.impl == "reference":
         res = bench_reference(args, rank, world)

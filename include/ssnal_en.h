@@ -39,6 +39,9 @@ enum {
 
 typedef struct ssnal_en_problem ssnal_en_problem; /* opaque handle */
 
+/* Bytes of one exported exchange-region handle (a cudaIpcMemHandle_t), ssnal_en_peer_export. */
+#define SSNAL_EN_IPC_HANDLE_BYTES 64
+
 /* Caller-supplied all-reduce for column-sharded handles (see ssnal_en_set_comm). */
 typedef int (*ssnal_en_allreduce_fn)(void* ctx, double* buf, int64_t count, int op, void* stream);
 
@@ -231,7 +234,8 @@ int ssnal_en_residual_device(ssnal_en_problem* p, const double* x_dev, double* r
  * prefix offset of an r × m buffer, so the sum is an all-gather; SMW Eq. (19) on the result) or
  * the partial m × m Gram A_J A_Jᵀ (r ≥ m, Eq. (18)); plus the warm-start A x0, the objective and
  * λmax.  All ranks therefore hold identical reduced values and take identical control decisions;
- * solves run host-driven (graph mode and the CG strategy are not used on a sharded handle).
+ * solves run host-driven (a host callback cannot sit inside the graph; see ssnal_en_peer_attach
+ * for the device-resident provider) and the CG strategy is not used on a sharded handle.
  *   fn(ctx, buf, count, op, stream): all-reduce count doubles at the DEVICE pointer buf in place,
  *     op 0 = sum, 1 = max, ordered after the work already queued on `stream` (cudaStream_t) and
  *     complete before work queued after the call; return 0 on success.  Called only from inside
@@ -241,6 +245,41 @@ int ssnal_en_residual_device(ssnal_en_problem* p, const double* x_dev, double* r
  * set_comm exchanges λmax (lambda_max_l1 becomes the global value).  rank ∈ [0, nranks).  Stats:
  * active, primal_obj, gap, res_kkt* are global.  Returns SSNAL_EINVAL for bad arguments. */
 int ssnal_en_set_comm(ssnal_en_problem* p, ssnal_en_allreduce_fn fn, void* ctx, int rank, int nranks);
+
+/* Column-sharded solves with DEVICE-RESIDENT exchanges over peer memory ("a few
+ * µs with … symmetric memory"; one process per GPU, NVLink / NVSwitch peers).  The same exchange
+ * points and the same rank-ordered sums as ssnal_en_set_comm, but every exchange is a kernel of this
+ * library — each rank writes its contribution straight into a slot of EVERY rank's exchange region
+ * (P2P stores), raises a flag per region, and sums the G slots of its own region in rank order
+ * 0 … G−1 once all flags reached the exchange's epoch — so the solve keeps its device-resident
+ * control (one CUDA graph with conditional nodes per solve; option graph = 1, the default) and no
+ * host callback runs inside a solve.  The compute and the collective are fused where one follows
+ * the other: the gather of the active columns writes them into the peers (the all-gather of the SMW
+ * branch, Eq. (19)), and the split-K reduction of the local partial Gram deposits it into the peers
+ * (Eq. (18)).  Waits give up after 20 s (the call then returns SSNAL_ECUDA).
+ *   1. ssnal_en_peer_export(p, nranks, handle_out): allocates this rank's exchange region (about
+ *      8·nranks·max(m, 8)·m bytes + 2 evaluation records per rank) and writes its CUDA IPC handle
+ *      (SSNAL_EN_IPC_HANDLE_BYTES bytes, host memory) to handle_out.  1 ≤ nranks ≤ 16.
+ *   2. The caller all-gathers the handles (any transport, e.g. torch.distributed.all_gather_object).
+ *   3. ssnal_en_peer_attach(p, rank, nranks, handles): handles = nranks × SSNAL_EN_IPC_HANDLE_BYTES
+ *      bytes in rank order (host); maps the peers' regions (cudaIpcOpenMemHandle; the own one is used
+ *      directly) and exchanges λmax (a collective call: every rank must call it).  Replaces a
+ *      set_comm provider.  SSNAL_EINVAL if export was not called with the same nranks.
+ * Solve calls follow the rules of ssnal_en_set_comm (same arguments and options on every rank,
+ * x0 / x_out are the rank's slices).  The exchange region is freed by destroy or a new export. */
+int ssnal_en_peer_export(ssnal_en_problem* p, int nranks, void* handle_out);
+int ssnal_en_peer_attach(ssnal_en_problem* p, int rank, int nranks, const void* handles);
+
+/* Test hook for the exchange protocol of ssnal_en_peer_attach on ONE device: nranks ranks are
+ * emulated by nranks CTAs of one cooperative launch (co-resident, so their waits on one another
+ * cannot deadlock), each with its own region inside one allocation, running `iters` exchanges (two
+ * small ones, then a big one, repeated) of `count` doubles through the same deposit / flag / epoch /
+ * rank-ordered-sum code as the solve's exchanges.  Every sum is checked in the kernel against its
+ * closed form; *mismatch_out = number of wrong elements over all ranks and exchanges.  small_out /
+ * big_out (host, nranks × count, nullable) receive each rank's last small / big sum.
+ * 1 ≤ nranks ≤ 16, 1 ≤ count ≤ 65536.  SSNAL_ECUDA if a wait timed out. */
+int ssnal_en_peer_selftest(int nranks, int iters, int64_t count, int64_t* mismatch_out, double* small_out,
+                           double* big_out);
 
 void ssnal_en_destroy(ssnal_en_problem* p);
 

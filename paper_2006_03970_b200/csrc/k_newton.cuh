@@ -531,10 +531,10 @@ struct GramFusedArgs {
 template <class Acc>
 __global__ void __cluster_dims__(kGramCS, 1, 1) __launch_bounds__(256)
     k_gram_fused(const Acc A, int64_t m, const int32_t* __restrict__ J, double* __restrict__ M,
-                 const double* __restrict__ g, GramFusedArgs ga, const DirGeo* geo) {
+                 const double* __restrict__ g, GramFusedArgs ga, const DirGeo* geo, int only = 0) {
   __shared__ __align__(16) double sm[2 * kGramSmem];  // operand buffers, then the partial tile (64 × 65)
-  if (geo) {
-    if (geo->branch != 1 && geo->branch != 2) return;
+  if (geo) {  // only > 0: this branch alone (the sharded SMW form on the gathered columns)
+    if ((geo->branch != 1 && geo->branch != 2) || (only && geo->branch != only)) return;
     ga.branch = geo->branch;
     ga.r = geo->r;
     ga.nout = geo->nout;
@@ -1299,25 +1299,6 @@ __global__ void k_init_y(int64_t m, const double* __restrict__ bvec, const doubl
       if (!valid || valid[b]) s += parts[(size_t)b * m + k];
     y[k] = warm ? (-1.0 * bvec[k] + s) : 0.0;
   }
-}
-// §8(f3) exchange record of one evaluation: out[0, m) = Σ_b part_vec[b] (ascending b, valid ones;
-// none if nparts = 0), out[m, m+4) = Σ_q part_scal[q][·] (ascending q), out[m+4] = r (local count).
-__global__ void __launch_bounds__(1024) k_prereduce(int64_t m, const double* __restrict__ part_vec,
-                                                    const int* __restrict__ valid, int nparts,
-                                                    const double* __restrict__ part_scal, int nscal,
-                                                    const int64_t* __restrict__ r_dev, double* __restrict__ out) {
-  for (int64_t k = threadIdx.x; k < m; k += blockDim.x) {
-    double s = 0.0;
-    for (int b = 0; b < nparts; ++b)
-      if (!valid || valid[b]) s += part_vec[(size_t)b * m + k];
-    out[k] = s;
-  }
-  if (threadIdx.x < 4) {
-    double s = 0.0;
-    for (int q = 0; q < nscal; ++q) s += part_scal[q * 4 + threadIdx.x];
-    out[m + threadIdx.x] = s;
-  }
-  if (threadIdx.x == 4) out[m + 4] = r_dev ? (double)*r_dev : 0.0;
 }
 __global__ void k_to_i64(const double* src, int64_t* dst) { *dst = (int64_t)*src; }
 // columns A[:, J[a]], a < r, densely into out (column-major, m × r) — the local share of a gather

@@ -24,6 +24,7 @@
 #include "k_chol_d2.cuh"
 #include "k_small.cuh"
 #include "k_small_cl.cuh"
+#include "k_peer.cuh"
 #include "ssnal_en.h"
 
 using namespace ssn;
@@ -345,6 +346,15 @@ struct ssnal_en_problem {
   int64_t* rg_dev = nullptr;         // global r for the eval record
   int32_t* iota = nullptr;           // 0 … m−1: indices of the gathered active columns
   double* comm_host = nullptr;       // pinned staging (nranks + 8 doubles)
+  // §8(f3) device-resident exchanges over peer memory (k_peer.cuh; ssnal_en_peer_export / _attach):
+  // the exchanges are kernels, so sharded solves keep the graph's device-resident control
+  int peer = 0;                                     // 1: attached (comm_fn unused)
+  char* peer_region = nullptr;                      // this rank's region (cudaMalloc: IPC-exportable)
+  int peer_nranks = 0;                              // ranks the region was sized for
+  char* peer_open[kPeerMaxRanks] = {};              // the peers' regions mapped by cudaIpcOpenMemHandle
+  PeerComm pc = {};
+  unsigned long long* peer_epoch = nullptr;         // [0] epoch; then ticket (unsigned), err (int)
+  int32_t* peer_idx = nullptr;                      // gathered-column index list (SMW all-gather)
   CholArgs* chol_args = nullptr;  // graph mode: K4 outputs per exact branch (device, 2 entries)
   int inner_tol_mode = 0;  // 1: tol_in = max(tol, 0.1 res3 at the outer start) (R37)
   int inject_fail = 0;    // test hook: the next N factorisations of a solve report failure
@@ -867,8 +877,47 @@ int launch_eval(ssnal_en_problem* P, const double* y, const Scal& sc, int with_g
 // ---- §8(f3) column sharding: exchanges through the caller's all-reduce ----
 bool sharded(const ssnal_en_problem* P) { return P->comm_size > 0; }
 
+unsigned reduce_grid(ssnal_en_problem* P, int64_t tot);
+// Peer-memory all-reduce (k_peer.cuh): one CTA through the double-buffered small slots, or a
+// multi-CTA deposit into the big slots followed by a waiting rank-ordered reduction.
+int peer_allreduce(ssnal_en_problem* P, double* buf, int64_t count, int op) {
+  if (count <= P->pc.ss) {
+    k_peer_allreduce<<<1, 1024, 0, P->st>>>(P->pc, buf, count, op);
+    P->launches++;
+  } else {
+    if (count > P->pc.sb) {
+      set_err("peer all-reduce of %lld doubles exceeds the exchange slot (%lld)", (long long)count,
+              (long long)P->pc.sb);
+      return SSNAL_EINVAL;
+    }
+    const unsigned grid = reduce_grid(P, count);
+    k_peer_put_big<<<grid, 256, 0, P->st>>>(P->pc, buf, count);
+    k_peer_reduce_big<<<grid, 256, 0, P->st>>>(P->pc, buf, count, op);
+    P->launches += 2;
+  }
+  CKL();
+  return SSNAL_OK;
+}
+
+// After a stream synchronisation: a peer exchange that timed out or saw inconsistent counts leaves
+// an error code in device memory (k_peer.cuh) — the call fails instead of returning bad results.
+int peer_check(ssnal_en_problem* P) {
+  int v[2] = {0, 0};  // ticket, err
+  CK(cudaMemcpy(v, P->peer_epoch + 1, 8, cudaMemcpyDeviceToHost));
+  if (v[1] == 1) {
+    set_err("peer exchange timed out (a rank stopped participating)");
+    return SSNAL_ECUDA;
+  }
+  if (v[1] != 0) {
+    set_err("peer exchange: gathered active counts disagree with the global r (code %d)", v[1]);
+    return SSNAL_ECUDA;
+  }
+  return SSNAL_OK;
+}
+
 int comm_allreduce(ssnal_en_problem* P, double* buf, int64_t count, int op) {
   CKL();
+  if (P->peer) return peer_allreduce(P, buf, count, op);
   const int rc = P->comm_fn(P->comm_ctx, buf, count, op, (void*)P->st);
   if (rc) {
     set_err("all-reduce callback failed (%d)", rc);
@@ -881,7 +930,14 @@ int comm_allreduce(ssnal_en_problem* P, double* buf, int64_t count, int op) {
 // rg_dev = the global r.  vec/nparts/valid: the partial m-vectors (nparts = 0: none).
 int exchange_eval(ssnal_en_problem* P, const double* vec, const int* valid, int nparts, const double* scal, int nscal,
                   const int64_t* r_local) {
-  k_prereduce<<<1, 1024, 0, P->st>>>(P->m, vec, valid, nparts, scal, nscal, r_local, P->xbuf);
+  if (P->peer) {  // record + deposit + wait + rank-ordered sum in one kernel
+    k_peer_eval<<<kRecCS, 256, 0, P->st>>>(P->pc, P->m, vec, valid, nparts, scal, nscal, r_local, P->xbuf,
+                                           P->rg_dev, nullptr);
+    P->launches++;
+    CKL();
+    return SSNAL_OK;
+  }
+  k_prereduce16<<<kRecCS, 256, 0, P->st>>>(P->m, vec, valid, nparts, scal, nscal, r_local, P->xbuf);
   P->launches++;
   int rc = comm_allreduce(P, P->xbuf, P->m + 5, 0);
   if (rc) return rc;
@@ -1168,12 +1224,9 @@ int newton_direction_sharded(ssnal_en_problem* P, const int32_t* J, int64_t rg, 
     DirGeo geo = make_geo(rg, m, P->nsm, P->W_splits, kappa, 1.0 / kappa, 0.0, INFINITY);
     geo.jit = jit;
     const AccA ga{GA, m};
-    k_gram<true><<<gram_grid(P, geo.tiles * geo.ns), 256, 0, P->st>>>(ga, m, P->iota, rg, P->W, g, geo.tiles, geo.ns,
-                                                                      nullptr);
-    k_gram_reduce<<<reduce_grid(P, geo.nout * geo.nout), 256, 0, P->st>>>(P->W, geo.ns, geo.nout, geo.nmat, geo.diag,
-                                                                          geo.mult, P->Mmat, geo.ld, nullptr, nullptr, 0,
-                                                                          geo.jit);
-    P->launches += 2;
+    const GramFusedArgs gfa{1, rg, geo.nout, geo.nmat, geo.tiles, geo.ld, geo.diag, geo.mult, geo.jit};
+    k_gram_fused<<<gram_fused_grid(P, geo.tiles), 256, 0, P->st>>>(ga, m, P->iota, P->Mmat, g, gfa, nullptr);
+    P->launches++;
     CKL();
     if ((rc = launch_chol(P, P->Mmat, geo.N, P->u, 1.0, nullptr, nullptr))) return rc;
     k_gather_rows<<<gather_rows_grid(P), 256, 0, P->st>>>(ga, m, P->iota, P->u, rg, nullptr, nullptr, nullptr,
@@ -1256,7 +1309,43 @@ int newton_direction(ssnal_en_problem* P, const int32_t* J, int64_t r, const dou
 // Graph mode: every branch's kernels, predicated on the device geometry C->geo (computed by the
 // control kernels from r); worst-case grids, surplus CTAs exit.  Same work decomposition as
 // newton_direction for the same r.  Reads J[0], g[0], y[0]; writes d, y[1], gᵀd → scratch[0].
+// Graph mode on a peer-attached sharded handle (§8(f3)): the same branch kernels as the
+// host-driven sharded direction, with the exchanges fused into them over peer memory —
+//   0 < r < m: k_peer_put_cols writes the local A_J into every rank's big slot (the all-gather),
+//              k_peer_index orders the gathered columns by rank, SMW Eq. (19) reads them in place;
+//   r ≥ m:     the local partial Gram (k_gram_local) is deposited into every rank by k_peer_put_gram
+//              and k_peer_gram_sum forms I_m + κ Σ_q in rank order (Eq. (18)).
+// Every kernel is predicated on the global branch (geo from the global r); worst-case grids.
+int newton_direction_graph_peer(ssnal_en_problem* P) {
+  const int64_t m = P->m;
+  const DirGeo* geo = &P->ctl->geo;
+  const AccA ga{(const double*)(P->pc.base[P->pc.rank] + peer_big_off(P->pc.size, P->pc.ss)), m};
+  const unsigned gsm = 2 * P->nsm;
+  with_acc(P, [&](auto acc) {
+    k_peer_put_cols<<<gsm, 256, 0, P->st>>>(P->pc, acc, m, P->J[0], P->r_dev + 0, geo);
+    k_gram_local<<<gsm, 256, 0, P->st>>>(acc, m, P->J[0], P->r_dev + 0, P->W, geo, P->nsm, P->W_splits);
+    return 0;
+  });
+  k_peer_index<<<1, 1024, 0, P->st>>>(P->pc, geo, 0, P->peer_idx);
+  // SMW on the gathered columns: the fused split-K Gram (its grid covers the worst case r < m)
+  k_gram_fused<<<gram_fused_grid(P, gram_tiles(m)), 256, 0, P->st>>>(ga, m, P->peer_idx, P->Mmat, P->g[0],
+                                                                     GramFusedArgs{}, geo, 1);
+  k_peer_put_gram<<<reduce_grid(P, m * m), 256, 0, P->st>>>(P->pc, P->W, P->r_dev + 0, m, geo, P->nsm, P->W_splits);
+  k_peer_gram_sum<<<reduce_grid(P, m * m), 256, 0, P->st>>>(P->pc, m, P->Mmat, P->g[0], geo, 0.0, 0, 0.0);
+  P->launches += 6;
+  CKL();
+  int rc = launch_chol(P, P->Mmat, 0, nullptr, 0.0, nullptr, nullptr, nullptr, nullptr, geo, -1);
+  if (rc) return rc;
+  k_gather_rows<<<gather_rows_grid(P), 256, 0, P->st>>>(ga, m, P->peer_idx, P->u, 0, nullptr, nullptr, geo, kGatherSmw,
+                                                         P->d, P->g[0], P->y[0], P->y[1], P->scratch, P->blk,
+                                                         P->ticket);
+  P->launches++;
+  CKL();
+  return SSNAL_OK;
+}
+
 int newton_direction_graph(ssnal_en_problem* P) {
+  if (P->peer) return newton_direction_graph_peer(P);
   const int64_t m = P->m;
   const DirGeo* geo = &P->ctl->geo;
   const int32_t* J = P->J[0];
@@ -1581,6 +1670,20 @@ int capture_graph(ssnal_en_problem* P, cudaGraph_t G) {
   const Scal none = make_scal(1.0, 0.0, 0.0);  // placeholder: every kernel reads C->sc
   int rc;
   cudaGraphConditionalHandle h_outer, h_inner, h_bt;
+  // ψ evaluation + the control decision that consumes it; on a peer-attached sharded handle the
+  // evaluation record is first summed over the ranks by k_peer_eval (same predicate on every rank)
+  auto eval_at = [&](const double* y, int with_grad, const int* valid, int nparts, double* g_out, int64_t* r_loc,
+                     int slot, const double* gd_src, const int* info_src, const int* pred, int hook,
+                     const CtlHook* hk) -> int {
+    if (!P->peer)
+      return launch_eval(P, y, none, with_grad, valid, nparts, g_out, r_loc, slot, gd_src, info_src, &C->sc, pred,
+                         nullptr, nullptr, 0, hook, hk);
+    k_peer_eval<<<kRecCS, 256, 0, P->st>>>(P->pc, m, nparts ? P->part_vec : nullptr, valid, nparts, P->part_scal,
+                                           P->G, r_loc, P->xbuf, P->rg_dev, pred);
+    P->launches++;
+    return launch_eval(P, y, none, with_grad, nullptr, nparts ? 1 : 0, g_out, P->rg_dev, slot, gd_src, info_src, &C->sc,
+                       pred, P->xbuf, P->xbuf + m, 1, hook, hk);
+  };
   CK(cudaGraphConditionalHandleCreate(&h_outer, G, 1, cudaGraphCondAssignDefault));
   cudaGraph_t body_o, body_i, body_b;
   {
@@ -1605,8 +1708,7 @@ int capture_graph(ssnal_en_problem* P, cudaGraph_t G) {
   if ((rc = launch_finalize(P, P->J[0], P->PJ[0], P->r_dev + 0))) return rc;
   if ((rc = launch_gather_vec(P, P->J[0], P->PJ[0], P->r_dev + 0))) return rc;
   CtlHook hk{C, P->ev_dev + 0, nullptr, m, P->nsm, P->W_splits, P->info, h_inner};
-  if ((rc = launch_eval(P, P->y[0], none, 1, nullptr, 1, P->g[0], P->r_dev + 0, 0, nullptr, nullptr, &C->sc, nullptr,
-                        nullptr, nullptr, 0, kHookInnerBegin, &hk)))
+  if ((rc = eval_at(P->y[0], 1, nullptr, 1, P->g[0], P->r_dev + 0, 0, nullptr, nullptr, nullptr, kHookInnerBegin, &hk)))
     return rc;
   P->seg_kernels[0] = (int)(P->launches - L);
   if ((rc = add_while(P->cap[0], h_inner, &body_i))) return rc;
@@ -1621,8 +1723,8 @@ int capture_graph(ssnal_en_problem* P, cudaGraph_t G) {
     if ((rc = launch_k1(P, P->y[1], P->x, none, 1, P->w[1], &C->sc, C->tstamp))) return rc;
     if ((rc = launch_finalize(P, P->J[1], P->PJ[1], P->r_dev + 1))) return rc;
     CtlHook ha{C, P->ev_dev + 0, P->ev_dev + 1, m, P->nsm, P->W_splits, P->info, h_bt};
-    if ((rc = launch_eval(P, P->y[1], none, 1, P->cta_cnt, P->G, P->g[1], P->r_dev + 1, 1, P->scratch, P->info,
-                          &C->sc, nullptr, nullptr, nullptr, 0, kHookArmijo, &ha)))
+    if ((rc = eval_at(P->y[1], 1, P->cta_cnt, P->G, P->g[1], P->r_dev + 1, 1, P->scratch, P->info, nullptr, kHookArmijo,
+                      &ha)))
       return rc;
     P->seg_kernels[1] = (int)(P->launches - L);
     if ((rc = add_while(P->cap[1], h_bt, &body_b))) return rc;
@@ -1637,8 +1739,8 @@ int capture_graph(ssnal_en_problem* P, cudaGraph_t G) {
       if ((rc = launch_k1e(P, P->w[0], P->w[1], 0.0, P->x, none, P->w[2], &C->sc, &C->s))) return rc;
       if ((rc = launch_finalize(P, P->J[1], P->PJ[1], P->r_dev + 1))) return rc;
       CtlHook hb{C, P->ev_dev + 0, P->ev_dev + 2, m, P->nsm, P->W_splits, P->info, h_bt};
-      if ((rc = launch_eval(P, P->y[1], none, 0, nullptr, 0, nullptr, P->r_dev + 1, 2, nullptr, nullptr, &C->sc,
-                            nullptr, nullptr, nullptr, 0, kHookBacktrack, &hb)))
+      if ((rc = eval_at(P->y[1], 0, nullptr, 0, nullptr, P->r_dev + 1, 2, nullptr, nullptr, nullptr, kHookBacktrack,
+                        &hb)))
         return rc;
       P->seg_kernels[2] = (int)(P->launches - L);
       cudaGraph_t tmp;
@@ -1653,8 +1755,8 @@ int capture_graph(ssnal_en_problem* P, cudaGraph_t G) {
     P->launches++;
     if ((rc = launch_gather_vec(P, P->J[0], P->PJ[0], P->r_dev + 0, &C->need_grad))) return rc;
     CtlHook he{C, P->ev_dev + 0, nullptr, m, P->nsm, P->W_splits, P->info, h_inner};
-    if ((rc = launch_eval(P, P->y[0], none, 1, nullptr, 1, P->g[0], P->r_dev + 0, 0, nullptr, nullptr, &C->sc,
-                          &C->need_grad, nullptr, nullptr, 0, kHookInnerEnd, &he)))
+    if ((rc = eval_at(P->y[0], 1, nullptr, 1, P->g[0], P->r_dev + 0, 0, nullptr, nullptr, &C->need_grad, kHookInnerEnd,
+                      &he)))
       return rc;
     P->seg_kernels[3] = (int)(P->launches - L);
     cudaGraph_t tmp;
@@ -1837,8 +1939,8 @@ int solve_graph_core(ssnal_en_problem* P, double l1, double l2, double sigma0, d
   h->max_outer = P->max_outer;
   h->max_inner = P->max_inner;
   h->max_bt = P->max_bt;
-  h->cg_ratio = P->cg_ratio;
-  h->cg_threshold = P->cg_threshold;
+  h->cg_ratio = sharded(P) ? 0.0 : P->cg_ratio;  // sharded: exact branches only (as host-driven)
+  h->cg_threshold = sharded(P) ? INFINITY : P->cg_threshold;
   h->nb = P->nb;
   h->jitter = P->jitter;
   h->inject = P->inject_fail;
@@ -1959,6 +2061,23 @@ static int create_common(ssnal_en_problem* P) {
   return SSNAL_OK;
 }
 
+// §8(f3) peer exchange state: close the peers' IPC mappings, free this rank's region
+static void peer_release(ssnal_en_problem* P) {
+  for (int q = 0; q < kPeerMaxRanks; ++q)
+    if (P->peer_open[q]) {
+      cudaIpcCloseMemHandle(P->peer_open[q]);
+      P->peer_open[q] = nullptr;
+    }
+  cudaFree(P->peer_region);
+  cudaFree(P->peer_epoch);
+  cudaFree(P->peer_idx);
+  P->peer_region = nullptr;
+  P->peer_epoch = nullptr;
+  P->peer_idx = nullptr;
+  P->peer = 0;
+  P->peer_nranks = 0;
+}
+
 static void destroy_bufs(ssnal_en_problem* P) {
   if (!P) return;
   if (P->path_slots) cudaFreeHost(P->path_slots);
@@ -1980,6 +2099,7 @@ static void destroy_bufs(ssnal_en_problem* P) {
   cudaFree(P->rg_dev);
   cudaFree(P->iota);
   if (P->comm_host) cudaFreeHost(P->comm_host);
+  peer_release(P);
   pool_free(P->A_own);
   pool_free(P->codes_own);
   pool_free(P->tab_own);
@@ -2279,7 +2399,7 @@ static int solve_wrapped(ssnal_en_problem* P, double l1, double l2, double sigma
   P->direct_xout = (x_out && xout_dev && x_out != x0) ? x_out : nullptr;
   P->xout_done = false;
   rc = small_eligible(P)                ? solve_small_core(P, l1, l2, sigma0, tol, have_x0, &S)
-       : (P->use_graph && !sharded(P)) ? solve_graph_core(P, l1, l2, sigma0, tol, have_x0, &S)
+       : (P->use_graph && (!sharded(P) || P->peer)) ? solve_graph_core(P, l1, l2, sigma0, tol, have_x0, &S)
                                        : solve_core(P, l1, l2, sigma0, tol, have_x0, &S);
   if (rc == SSNAL_ECUDA || rc == SSNAL_EINVAL) return rc;
   if (x_out && !P->xout_done) {
@@ -2290,6 +2410,7 @@ static int solve_wrapped(ssnal_en_problem* P, double l1, double l2, double sigma
   CK(cudaEventRecord(e1, P->st));
   CK(cudaStreamSynchronize(P->st));
   harvest_k1(P);
+  if (P->peer && (rc = peer_check(P))) return rc;
   finish_stats(P, &S);
   S.primal_viol = NAN;
   if (P->certify) {  // one extra Aᵀ pass at Ax − b (tmpm holds it from the objective), outside TTS
@@ -2363,7 +2484,9 @@ int ssnal_en_solve_path_device(ssnal_en_problem* P, int64_t npts, const double* 
   auto fold = [&](int rc) {
     if (rc != SSNAL_OK && worst == SSNAL_OK) worst = rc;
   };
-  const bool deferred = !sharded(P) && !P->certify && (small_eligible(P) || P->use_graph);
+  // peer-attached sharded handles keep the deferred path (their exchanges are kernels); host-callback
+  // providers need host-driven control
+  const bool deferred = (!sharded(P) || P->peer) && !P->certify && (small_eligible(P) || P->use_graph);
   if (!deferred) {
     double sig = sigma0;
     for (int64_t i = 0; i < npts; ++i) {
@@ -2402,6 +2525,15 @@ int ssnal_en_solve_path_device(ssnal_en_problem* P, int64_t npts, const double* 
   std::vector<size_t> k1_beg(npts + 1, 0);  // K1 event pairs (warm-start passes with time_k1) per point
   double* sigma_carry = P->scratch + 60;
   int rc = SSNAL_OK;
+  int have0 = x0 != nullptr;
+  if (sharded(P)) {  // point 0: warm iff any rank has an x0 slice (the others count as zero)
+    P->comm_host[0] = have0;
+    CK(cudaMemcpyAsync(P->xbuf, P->comm_host, 8, cudaMemcpyHostToDevice, P->st));
+    if ((rc = comm_allreduce(P, P->xbuf, 1, 0))) return rc;
+    CK(cudaMemcpyAsync(P->comm_host + 1, P->xbuf, 8, cudaMemcpyDeviceToHost, P->st));
+    CK(cudaStreamSynchronize(P->st));
+    have0 = P->comm_host[1] > 0;
+  }
   for (int64_t i = 0; i < npts && rc == SSNAL_OK; ++i) {  // enqueue every point
     P->ctl_host = &slot[i].ctl;
     P->ev_out_host = &slot[i].ev;
@@ -2411,11 +2543,13 @@ int ssnal_en_solve_path_device(ssnal_en_problem* P, int64_t npts, const double* 
     CK(cudaEventRecord(P->path_ev[2 * i], P->st));
     const double* xi = i == 0 ? x0 : x_out + (i - 1) * n;
     if (xi) CK(cudaMemcpyAsync(P->x, xi, n * 8, cudaMemcpyDeviceToDevice, P->st));
+    else if (i == 0 && have0) CK(cudaMemsetAsync(P->x, 0, n * 8, P->st));  // sharded: no slice here
+    const int warm = i == 0 ? have0 : 1;
     const double* sig_in = (P->carry_sigma && i > 0) ? sigma_carry : nullptr;
     P->direct_xout = x_out + i * n;
     P->xout_done = false;
-    rc = small_eligible(P) ? solve_small_core(P, lambda1[i], lambda2[i], sigma0, tol, xi != nullptr, &S[i], sig_in)
-                           : solve_graph_core(P, lambda1[i], lambda2[i], sigma0, tol, xi != nullptr, &S[i], sig_in);
+    rc = small_eligible(P) ? solve_small_core(P, lambda1[i], lambda2[i], sigma0, tol, warm, &S[i], sig_in)
+                           : solve_graph_core(P, lambda1[i], lambda2[i], sigma0, tol, warm, &S[i], sig_in);
     if (rc == SSNAL_OK && P->carry_sigma)
       CK(cudaMemcpyAsync(sigma_carry, &P->ctl->sigma_final, 8, cudaMemcpyDeviceToDevice, P->st));
     if (rc == SSNAL_OK && !P->xout_done) CK(cudaMemcpyAsync(x_out + i * n, P->x, n * 8, cudaMemcpyDeviceToDevice, P->st));
@@ -2448,6 +2582,7 @@ int ssnal_en_solve_path_device(ssnal_en_problem* P, int64_t npts, const double* 
   }
   P->k1_pending.clear();
   if (rc != SSNAL_OK) return rc;
+  if (P->peer && (rc = peer_check(P))) return rc;
   const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   for (int64_t i = 0; i < npts; ++i) {  // complete the statistics point by point
     P->ctl_host = &slot[i].ctl;
@@ -2719,11 +2854,8 @@ int ssnal_en_residual_device(ssnal_en_problem* P, const double* x, double* rss_o
   return residual_impl(P, x, 1, rss_out);
 }
 
-int ssnal_en_set_comm(ssnal_en_problem* P, ssnal_en_allreduce_fn fn, void* ctx, int rank, int nranks) {
-  if (!P || !fn || nranks < 1 || rank < 0 || rank >= nranks) {
-    set_err("invalid argument");
-    return SSNAL_EINVAL;
-  }
+// Buffers of a sharded handle and the rank bookkeeping (both exchange providers)
+static int comm_setup(ssnal_en_problem* P, int rank, int nranks) {
   const int64_t m = P->m;
   if (!P->xbuf) {
     int rc;
@@ -2734,21 +2866,169 @@ int ssnal_en_set_comm(ssnal_en_problem* P, ssnal_en_allreduce_fn fn, void* ctx, 
   if (P->comm_host) cudaFreeHost(P->comm_host);
   P->comm_host = nullptr;
   CK(cudaHostAlloc((void**)&P->comm_host, (size_t)(nranks + 16) * 8, cudaHostAllocDefault));
-  P->comm_fn = fn;
-  P->comm_ctx = ctx;
   P->comm_rank = rank;
   P->comm_size = nranks;
+  CK(cudaFuncSetAttribute(k_prereduce16, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));  // 16-CTA clusters
+  CK(cudaFuncSetAttribute(k_peer_eval, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   k_iota<<<1, 1024, 0, P->st>>>(P->iota, m);
   CKL();
-  // λmax = max over the ranks of the local ‖A_qᵀb‖∞
+  drop_graph(P);  // the graph's evaluations and directions depend on the exchange provider
+  return SSNAL_OK;
+}
+
+// λmax = max over the ranks of the local ‖A_qᵀb‖∞ (the first exchange of a sharded handle)
+static int comm_lambda_max(ssnal_en_problem* P) {
   P->comm_host[0] = P->lambda_max;
   CK(cudaMemcpyAsync(P->xbuf, P->comm_host, 8, cudaMemcpyHostToDevice, P->st));
   int rc = comm_allreduce(P, P->xbuf, 1, 1);
   if (rc) return rc;
   CK(cudaMemcpyAsync(P->comm_host + 1, P->xbuf, 8, cudaMemcpyDeviceToHost, P->st));
   CK(cudaStreamSynchronize(P->st));
+  if (P->peer && (rc = peer_check(P))) return rc;
   P->lambda_max = P->comm_host[1];
   return SSNAL_OK;
+}
+
+int ssnal_en_peer_export(ssnal_en_problem* P, int nranks, void* handle_out) {
+  if (!P || !handle_out || nranks < 1 || nranks > kPeerMaxRanks) {
+    set_err("invalid argument (nranks must be in [1, %d])", kPeerMaxRanks);
+    return SSNAL_EINVAL;
+  }
+  peer_release(P);
+  const int64_t m = P->m;
+  const int64_t ss = (m + 16 + kPeerMaxRanks + 31) / 32 * 32;  // an evaluation record, counts, scalars
+  const int64_t ccap = m < 8 ? 8 : m;                           // gathered columns per rank (r_q < m)
+  const int64_t sb = ccap * m;                                  // ≥ m² (partial Gram)
+  const size_t bytes = (size_t)peer_region_bytes(nranks, ss, sb);
+  CK(cudaMalloc((void**)&P->peer_region, bytes));  // not the stream-ordered pool: IPC-exportable
+  CK(cudaMemset(P->peer_region, 0, bytes));        // flags = 0 before any peer can write
+  CK(cudaMalloc((void**)&P->peer_epoch, 64));
+  CK(cudaMemset(P->peer_epoch, 0, 64));
+  CK(cudaMalloc((void**)&P->peer_idx, (size_t)(m + 1) * 4));
+  CK(cudaDeviceSynchronize());
+  cudaIpcMemHandle_t h;
+  CK(cudaIpcGetMemHandle(&h, P->peer_region));
+  static_assert(sizeof(cudaIpcMemHandle_t) == SSNAL_EN_IPC_HANDLE_BYTES, "IPC handle size");
+  memcpy(handle_out, &h, sizeof(h));
+  P->peer_nranks = nranks;
+  P->pc = PeerComm{};
+  P->pc.size = nranks;
+  P->pc.ss = ss;
+  P->pc.sb = sb;
+  P->pc.ccap = ccap;
+  return SSNAL_OK;
+}
+
+int ssnal_en_peer_attach(ssnal_en_problem* P, int rank, int nranks, const void* handles) {
+  if (!P || !handles || !P->peer_region || nranks != P->peer_nranks || rank < 0 || rank >= nranks) {
+    set_err("invalid argument (call ssnal_en_peer_export with the same nranks first)");
+    return SSNAL_EINVAL;
+  }
+  const char* hb = (const char*)handles;
+  for (int q = 0; q < nranks; ++q) {
+    if (q == rank) {
+      P->pc.base[q] = P->peer_region;
+      continue;
+    }
+    if (P->peer_open[q]) {
+      cudaIpcCloseMemHandle(P->peer_open[q]);
+      P->peer_open[q] = nullptr;
+    }
+    cudaIpcMemHandle_t h;
+    memcpy(&h, hb + (size_t)q * SSNAL_EN_IPC_HANDLE_BYTES, sizeof(h));
+    void* ptr = nullptr;
+    CK(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    P->peer_open[q] = (char*)ptr;
+    P->pc.base[q] = (char*)ptr;
+  }
+  P->pc.rank = rank;
+  P->pc.epoch = P->peer_epoch;
+  P->pc.ticket = (unsigned*)(P->peer_epoch + 1);
+  P->pc.err = (int*)(P->peer_epoch + 1) + 1;
+  int rc = comm_setup(P, rank, nranks);
+  if (rc) return rc;
+  P->comm_fn = nullptr;
+  P->comm_ctx = nullptr;
+  P->peer = 1;
+  return comm_lambda_max(P);
+}
+
+int ssnal_en_peer_selftest(int nranks, int iters, int64_t count, int64_t* mismatch_out, double* small_out,
+                           double* big_out) {
+  if (nranks < 1 || nranks > kPeerMaxRanks || iters < 1 || count < 1 || count > 65536 || !mismatch_out) {
+    set_err("invalid argument");
+    return SSNAL_EINVAL;
+  }
+  const int64_t ss = (count + 31) / 32 * 32;
+  const size_t rb = ((size_t)peer_region_bytes(nranks, ss, ss) + 255) / 256 * 256;
+  char* all = nullptr;
+  char** bases = nullptr;
+  unsigned long long* ep = nullptr;
+  int *errs = nullptr, *mis = nullptr;
+  double *ls = nullptr, *lb = nullptr;
+  int rc = SSNAL_OK;
+  auto fail = [&](const char* what, cudaError_t e) {
+    set_err("peer selftest: %s: %s", what, cudaGetErrorString(e));
+    rc = SSNAL_ECUDA;
+  };
+  cudaError_t e;
+  if ((e = cudaMalloc((void**)&all, rb * nranks)) != cudaSuccess) fail("alloc", e);
+  if (!rc && (e = cudaMalloc((void**)&bases, kPeerMaxRanks * sizeof(char*))) != cudaSuccess) fail("alloc", e);
+  if (!rc && (e = cudaMalloc((void**)&ep, kPeerMaxRanks * 8 + 2 * kPeerMaxRanks * 4 + 64)) != cudaSuccess)
+    fail("alloc", e);
+  if (!rc && (e = cudaMalloc((void**)&ls, (size_t)2 * nranks * count * 8)) != cudaSuccess) fail("alloc", e);
+  if (!rc) {
+    errs = (int*)(ep + kPeerMaxRanks);
+    mis = errs + kPeerMaxRanks;
+    lb = ls + (size_t)nranks * count;
+    std::vector<char*> hb(kPeerMaxRanks, nullptr);
+    for (int q = 0; q < nranks; ++q) hb[q] = all + (size_t)q * rb;
+    cudaMemset(all, 0, rb * nranks);
+    cudaMemset(ep, 0, kPeerMaxRanks * 8 + 2 * kPeerMaxRanks * 4 + 64);
+    cudaMemcpy(bases, hb.data(), kPeerMaxRanks * sizeof(char*), cudaMemcpyHostToDevice);
+    PeerComm proto{};
+    proto.size = nranks;
+    proto.ss = ss;
+    proto.sb = ss;
+    proto.ccap = 1;
+    char* const* cb = bases;
+    void* args[] = {&proto, (void*)&cb, &iters, &count, &ep, &errs, &mis, &ls, &lb};
+    if ((e = cudaLaunchCooperativeKernel((const void*)k_peer_emulate, dim3(nranks), dim3(256), args, 0, 0)) !=
+        cudaSuccess)
+      fail("launch", e);
+    else if ((e = cudaDeviceSynchronize()) != cudaSuccess)
+      fail("run", e);
+  }
+  if (!rc) {
+    int herr[kPeerMaxRanks + 1];
+    cudaMemcpy(herr, errs, (kPeerMaxRanks + 1) * 4, cudaMemcpyDeviceToHost);
+    *mismatch_out = herr[kPeerMaxRanks];
+    for (int q = 0; q < nranks; ++q)
+      if (herr[q]) {
+        set_err("peer selftest: rank %d timed out", q);
+        rc = SSNAL_ECUDA;
+      }
+    if (small_out) cudaMemcpy(small_out, ls, (size_t)nranks * count * 8, cudaMemcpyDeviceToHost);
+    if (big_out) cudaMemcpy(big_out, lb, (size_t)nranks * count * 8, cudaMemcpyDeviceToHost);
+  }
+  cudaFree(all);
+  cudaFree(bases);
+  cudaFree(ep);
+  cudaFree(ls);
+  return rc;
+}
+
+int ssnal_en_set_comm(ssnal_en_problem* P, ssnal_en_allreduce_fn fn, void* ctx, int rank, int nranks) {
+  if (!P || !fn || nranks < 1 || rank < 0 || rank >= nranks) {
+    set_err("invalid argument");
+    return SSNAL_EINVAL;
+  }
+  peer_release(P);
+  int rc = comm_setup(P, rank, nranks);
+  if (rc) return rc;
+  P->comm_fn = fn;
+  P->comm_ctx = ctx;
+  return comm_lambda_max(P);
 }
 
 void ssnal_en_destroy(ssnal_en_problem* P) {

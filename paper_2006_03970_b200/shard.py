@@ -1,10 +1,15 @@
 """Column-sharded solves: rank q of G owns a contiguous block of columns of A,
-and the library sums every cross-column quantity through an all-reduce the caller supplies
-(`Problem.set_comm`; the exchange points are listed at ssnal_en_set_comm in include/ssnal_en.h).
+and the library sums every cross-column quantity over the ranks (the exchange points are listed at
+ssnal_en_set_comm in include/ssnal_en.h).
 
-Two all-reduce providers:
-  * `torch_allreduce(group)` — torch.distributed (NCCL on GPUs, one process per GPU; gloo on CPU
-    for the host-side tests), stream-ordered with the library's stream;
+Exchange providers:
+  * `attach_peers(problem, group)` — the default for one process per GPU: device-resident exchanges
+    over peer memory inside the library (ssnal_en_peer_export / _attach: CUDA IPC regions, P2P
+    stores over NVLink, rank-ordered sums), so sharded solves keep the graph's device-resident
+    control; torch.distributed only carries the 64-byte IPC handles once;
+  * `torch_allreduce(group)` — a host callback per exchange over torch.distributed (NCCL on GPUs;
+    gloo on CPU for the host-side tests), stream-ordered with the library's stream (host-driven
+    control);
   * `ThreadGroup(G)` — G shards of one problem on one device in one process, one thread each,
     summing through host barriers (a test harness: the kernels of different shards never wait on
     one another; the threads synchronise on the host).
@@ -41,6 +46,30 @@ def as_tensor(ptr: int, count: int, device: str = "cuda") -> torch.Tensor:
     import numpy as np
 
     return torch.from_numpy(np.asarray(_Cai(ptr, count, device)))
+
+
+def exchange_handles(handle: bytes, group=None):
+    """All-gather every rank's exchange-region handle in rank order (torch.distributed when it is
+    initialised, else a single rank)."""
+    import torch.distributed as dist
+
+    if not (dist.is_available() and dist.is_initialized()):
+        return 0, 1, [handle]
+    rank, size = dist.get_rank(group), dist.get_world_size(group)
+    out = [None] * size
+    dist.all_gather_object(out, handle, group=group)
+    return rank, size, out
+
+
+def attach_peers(problem, group=None):
+    """Make `problem` (this rank's column block) a rank of a sharded solve with device-resident
+    exchanges over peer memory: export its exchange region, all-gather the IPC handles, attach."""
+    import torch.distributed as dist
+
+    size = dist.get_world_size(group) if (dist.is_available() and dist.is_initialized()) else 1
+    rank, size, handles = exchange_handles(problem.peer_export(size), group)
+    problem.peer_attach(rank, size, handles)
+    return rank, size
 
 
 def torch_allreduce(group=None, device: str = "cuda"):

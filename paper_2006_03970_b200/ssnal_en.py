@@ -91,16 +91,35 @@ def load_library():
         L.ssnal_en_residual.argtypes = [_vp, _dp, _dp]
         L.ssnal_en_residual_device.argtypes = [_vp, _vp, _dp]
         L.ssnal_en_set_comm.argtypes = [_vp, ALLREDUCE_FN, _vp, ctypes.c_int, ctypes.c_int]
+        L.ssnal_en_peer_export.argtypes = [_vp, ctypes.c_int, _vp]
+        L.ssnal_en_peer_attach.argtypes = [_vp, ctypes.c_int, ctypes.c_int, _vp]
+        L.ssnal_en_peer_selftest.argtypes = [ctypes.c_int, ctypes.c_int, _i64, P(_i64), _dp, _dp]
         L.ssnal_en_destroy.argtypes = [_vp]
         L.ssnal_en_destroy.restype = None
         L.ssnal_en_last_error.restype = ctypes.c_char_p
         L.ssnal_en_version.restype = ctypes.c_char_p
         for f in ("create", "create_device", "create_geno", "create_geno_device", "residual", "residual_device",
                   "set_option", "solve", "solve_device", "aty_fused", "epilogue",
-                  "newton_direction", "set_comm"):
+                  "newton_direction", "set_comm", "peer_export", "peer_attach", "peer_selftest"):
             getattr(L, "ssnal_en_" + f).restype = ctypes.c_int
         _lib = L
     return _lib
+
+
+IPC_HANDLE_BYTES = 64  # SSNAL_EN_IPC_HANDLE_BYTES
+
+
+def peer_selftest(nranks: int, iters: int, count: int):
+    """The exchange protocol of peer-attached sharded solves with nranks ranks emulated as the CTAs of
+    one cooperative launch on the current device (ssnal_en_peer_selftest): returns (mismatches,
+    last small sums, last big sums) with the sums as (nranks, count) arrays."""
+    L = load_library()
+    mis = _i64(0)
+    small = np.zeros((nranks, count))
+    big = np.zeros((nranks, count))
+    _check(L.ssnal_en_peer_selftest(nranks, iters, count, ctypes.byref(mis),
+                                    small.ctypes.data_as(_dp), big.ctypes.data_as(_dp)))
+    return mis.value, small, big
 
 
 def _check(rc, allow=(SSNAL_OK,)):
@@ -269,6 +288,23 @@ class Problem:
 
         self._comm_cb = ALLREDUCE_FN(cb)  # kept alive with the handle
         _check(self._lib.ssnal_en_set_comm(self._h, self._comm_cb, None, rank, nranks))
+
+    def peer_export(self, nranks: int) -> bytes:
+        """Allocate this rank's exchange region for a peer-memory sharded solve (§8(f3)) and return its
+        IPC handle (IPC_HANDLE_BYTES bytes).  See ssnal_en_peer_export in include/ssnal_en.h."""
+        buf = ctypes.create_string_buffer(IPC_HANDLE_BYTES)
+        _check(self._lib.ssnal_en_peer_export(self._h, nranks, buf))
+        return buf.raw
+
+    def peer_attach(self, rank: int, nranks: int, handles):
+        """Map the peers' exchange regions (handles: every rank's peer_export bytes, rank order) and
+        make this handle rank `rank` of a sharded solve with device-resident exchanges (a collective
+        call).  See ssnal_en_peer_attach in include/ssnal_en.h."""
+        blob = b"".join(bytes(h) for h in handles)
+        if len(handles) != nranks or len(blob) != nranks * IPC_HANDLE_BYTES:
+            raise ValueError("need one IPC handle per rank")
+        buf = ctypes.create_string_buffer(blob, len(blob))
+        _check(self._lib.ssnal_en_peer_attach(self._h, rank, nranks, buf))
 
     def close(self):
         if getattr(self, "_h", None):

@@ -68,3 +68,68 @@ def test_torch_allreduce_gloo_world2():
     for r in (0, 1):
         assert np.array_equal(np.array(res[r][0]), want)  # sums, identical on both ranks
         assert res[r][1] == 8.0  # max
+
+
+class _FakeProblem:
+    """Stands in for a Problem in the handle exchange of shard.attach_peers (no GPU): records the
+    export size and the handles it is attached with."""
+
+    def __init__(self, rank):
+        self.rank = rank
+        self.exported = None
+        self.attached = None
+
+    def peer_export(self, nranks):
+        self.exported = nranks
+        return bytes([self.rank + 1]) * 64  # a distinct 64-byte "IPC handle" per rank
+
+    def peer_attach(self, rank, nranks, handles):
+        self.attached = (rank, nranks, [bytes(h) for h in handles])
+
+
+def _attach_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    sys.path.insert(0, ROOT)
+    from paper_2006_03970_b200.shard import attach_peers
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    P = _FakeProblem(rank)
+    ret = attach_peers(P)
+    q.put((rank, ret, P.exported, P.attached))
+    dist.destroy_process_group()
+
+
+def test_attach_peers_exchanges_handles_gloo_world2():
+    """shard.attach_peers (the device-resident exchange provider, ssnal_en_peer_export / _attach):
+    every rank exports a region sized for the world, receives every rank's IPC handle in rank order
+    and attaches as its own rank."""
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_attach_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in procs:
+        r, ret, exported, attached = q.get(timeout=120)
+        res[r] = (ret, exported, attached)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in (0, 1):
+        ret, exported, attached = res[r]
+        assert ret == (r, 2) and exported == 2
+        assert attached == (r, 2, [bytes([1]) * 64, bytes([2]) * 64])
+
+
+def test_attach_peers_single_process():
+    """Without torch.distributed the handle is a one-rank group."""
+    sys.path.insert(0, ROOT)
+    from paper_2006_03970_b200.shard import attach_peers
+
+    P = _FakeProblem(0)
+    assert attach_peers(P) == (0, 1)
+    assert P.exported == 1 and P.attached == (0, 1, [bytes([1]) * 64])
