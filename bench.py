@@ -683,6 +683,8 @@ def sweep(args):
         for n in [nn for mm, nn in cases if mm == m]:
             b = torch.from_numpy(synth.normals(5, 11, m)).cuda()
             P = Problem.from_device(dA.data_ptr(), b.data_ptr(), m, n, stream.cuda_stream, keep=(dA, b))
+            if args.k1_stages:
+                P.set_option("k1_stages", args.k1_stages)
             y = torch.from_numpy(synth.normals(5, 12, m)).cuda()
             xh = np.zeros(n)
             k = min(100, n)
@@ -712,7 +714,8 @@ def sweep(args):
                 t_k1 = P.info("k1_time_s") / max(P.info("k1_launches"), 1)
                 P.set_option("time_k1", 0)
                 gbs = k1_bytes(m, n) / t_k1 / 1e9
-                print(json.dumps({"sweep": "k1", "m": m, "n": n, "case": lab, "r": r, "t_k1_us": t_k1 * 1e6,
+                print(json.dumps({"sweep": "k1", "m": m, "n": n, "case": lab, "r": r, "k1_stages": P.info("k1_stages"),
+                                  "t_k1_us": t_k1 * 1e6,
                                   "t_call_us": t_call * 1e6, "GBps": gbs, "frac_of_measured": gbs / peak,
                                   "pct_of_8TBps": gbs / 8000}), flush=True)
             P.close()
@@ -745,6 +748,7 @@ def main():
                     help="with --shard: device-resident exchanges over peer memory (default) or NCCL host callbacks")
     ap.add_argument("--sweep-n", default="100000,200000,500000,1000000,2000000,5000000,10000000")
     ap.add_argument("--sweep-reps", type=int, default=50)
+    ap.add_argument("--k1-stages", type=int, default=0, help="with --sweep: K1 ring depth (0 = the library default)")
     args = ap.parse_args()
     if args.cpu_leg:
         cpu_leg(args.cpu_leg, args.config)

@@ -2313,6 +2313,20 @@ int ssnal_en_set_option(ssnal_en_problem* P, const char* key, double v) {
     P->cg_maxit = (int)v;
     drop_graph(P);
   }
+  else if (k == "k1_stages" && v >= 2 && v <= 16 && !P->fmt) {
+    // depth of K1's bulk-copy ring (default: as many ~32 KB stages as fit 200 KB, ≤ 8)
+    const int S = (int)v;
+    const size_t per_stage = (size_t)(P->stage_elems + P->xstage_elems) * 8;
+    const size_t smem = (size_t)S * per_stage + 2 * S * 8 + 64 + 4 * S + 16;
+    if ((size_t)S * P->stage_elems < (size_t)K1_NWC * P->m + K1_NWC * 4 + K1_NWC || smem > 227 * 1024) {
+      set_err("k1_stages=%d does not fit (m=%lld)", S, (long long)P->m);
+      return SSNAL_EINVAL;
+    }
+    CK(cudaFuncSetAttribute(k1_for(P->MR), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    P->S = S;
+    P->k1_smem = smem;
+    drop_graph(P);  // the K1 launch configuration is baked into the graph
+  }
   else if (k == "small" && (v == 0 || v == 1))
     P->use_small = (int)v;
   else if (k == "small_cluster" && (v == 0 || v == 1))
