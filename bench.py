@@ -256,6 +256,9 @@ def bench_ours(args, rank, world, local_rank):
         P = Problem.from_device(dA.data_ptr(), db.data_ptr(), m, n, stream.cuda_stream, keep=(dA, db))
     P.set_option("graph", 1 if args.control == "graph" else 0)
     P.set_option("cg_ratio", args.cg_ratio)
+    for kv in args.opt:  # library options for A/B runs (recorded in config)
+        k, v = kv.split("=")
+        P.set_option(k, float(v))
     lm = P.lambda_max_l1
     x_all = torch.zeros((len(cfg.cs), n), dtype=torch.float64, device="cuda")
 
@@ -415,6 +418,8 @@ def bench_ours(args, rank, world, local_rank):
     }
     if args.shard:
         res["config"]["n_local"] = n
+    if args.opt:
+        res["config"]["options"] = dict(kv.split("=") for kv in args.opt)
     P.close()
     del dA, x_all
     torch.cuda.empty_cache()
@@ -749,6 +754,7 @@ def main():
     ap.add_argument("--sweep-n", default="100000,200000,500000,1000000,2000000,5000000,10000000")
     ap.add_argument("--sweep-reps", type=int, default=50)
     ap.add_argument("--k1-stages", type=int, default=0, help="with --sweep: K1 ring depth (0 = the library default)")
+    ap.add_argument("--opt", action="append", default=[], help="library option key=value for the run (repeatable)")
     args = ap.parse_args()
     if args.cpu_leg:
         cpu_leg(args.cpu_leg, args.config)

@@ -593,6 +593,100 @@ __global__ void __cluster_dims__(kGramCS, 1, 1) __launch_bounds__(256)
   }
 }
 
+// K3 split over the whole GPU (the hot-path Newton systems): k_gram_fused gives each 64 × 64 tile an
+// 8-CTA cluster, and at m = 500 only 33 of the 36 m × m clusters fit at once (GPC packing), so a
+// second round of 3 clusters doubled the time at large r.  Here the work items are (tile, K-slice)
+// pairs with ns = min(grid / tiles, chunks / minch) slices per tile, so every item runs in ONE round of a
+// cooperative launch (all CTAs co-resident): CTA b takes item b, sums its K-slice of the tile on
+// the FP64 tensor cores (gram_item), stores the partial tile to P (L2), and arrives on the tile's
+// counter; the ns CTAs of a tile wait for all ns partials, then slice s reduces rows
+// [64s/ns, 64(s+1)/ns) of the tile over the slices in slice order (deterministic) with the
+// k_gram_reduce epilogue (× mult, + diag, jitter, rhs row) straight into M.  The last CTA of a tile
+// to finish resets its counters for the next launch.  Graph mode: branch and sizes from geo;
+// only > 0 restricts to one branch (sharded SMW on gathered columns).
+template <class Acc>
+__global__ void __launch_bounds__(256, 2)
+    k_gram_sk(const Acc A, int64_t m, const int32_t* __restrict__ J, double* __restrict__ M,
+              const double* __restrict__ g, GramFusedArgs ga, const DirGeo* geo, int only, double* __restrict__ Pt,
+              unsigned* __restrict__ cnt, int minch) {
+  __shared__ __align__(16) double sm[2 * kGramSmem];
+  __shared__ bool last;
+  if (geo) {
+    if ((geo->branch != 1 && geo->branch != 2) || (only && geo->branch != only)) return;
+    ga.branch = geo->branch;
+    ga.r = geo->r;
+    ga.nout = geo->nout;
+    ga.nmat = geo->nmat;
+    ga.tiles = geo->tiles;
+    ga.ld = geo->ld;
+    ga.diag = geo->diag;
+    ga.mult = geo->mult;
+    ga.jit = geo->jit;
+  }
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gq = lane >> 2, t = lane & 3, wr = warp >> 1, wc = warp & 1;
+  const bool smw = ga.branch == 1;
+  const int64_t K = smw ? m : ga.r;
+  const int64_t nch = (K + 31) / 32;
+  int ns = (int)gridDim.x / ga.tiles;  // slices per tile: one round, ≥ minch reduction chunks each (the
+  if (ns > nch / minch) ns = (int)(nch / minch);  // partial tiles cost L2 traffic ∝ tiles · ns)
+  if (ns < 1) ns = 1;
+  if (!smw && g)  // the rhs row of Eq. (18): M[nmat + e·ld] = g[e]
+    for (int64_t e = (int64_t)blockIdx.x * 256 + tid; e < ga.nmat; e += (int64_t)gridDim.x * 256)
+      M[ga.nmat + e * ga.ld] = g[e];
+  for (int item = blockIdx.x; item < ga.tiles * ns; item += gridDim.x) {  // one round when tiles ≤ grid
+    const int tq = item / ns, s = item % ns;
+    int ti, tj;
+    tri_tile(tq, &ti, &tj);
+    double acc[2][4][2];
+    if (smw) gram_item<true>(A, m, J, ga.r, g, ti, tj, nch * s / ns, nch * (s + 1) / ns, sm, sm + kGramSmem, acc);
+    else gram_item<false>(A, m, J, ga.r, nullptr, ti, tj, nch * s / ns, nch * (s + 1) / ns, sm, sm + kGramSmem, acc);
+    double* Pi = Pt + (size_t)item * GT * GT;
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) __stcg(Pi + (16 * wr + 8 * i + gq) * GT + 32 * wc + 8 * j + 2 * t + e, acc[i][j][e]);
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) {
+      atomicAdd(cnt + 2 * tq, 1u);
+      while (atomicAdd(cnt + 2 * tq, 0u) < (unsigned)ns) {
+      }
+      __threadfence();
+    }
+    __syncthreads();
+    const int64_t o0 = (int64_t)ti * GT, o1 = (int64_t)tj * GT;
+    const int w0 = GT * s / ns, w1 = GT * (s + 1) / ns;
+    const double* Pb = Pt + (size_t)tq * ns * GT * GT;
+    for (int e = tid; e < (w1 - w0) * GT; e += 256) {
+      const int w = w0 + e / GT, k = e % GT;
+      const int64_t oi = o0 + w, oj = o1 + k;
+      if (oi < ga.nout && oj < ga.nout && oi >= oj) {
+        double v = 0.0;
+        for (int q = 0; q < ns; ++q) v += __ldcg(Pb + (size_t)q * GT * GT + w * GT + k);
+        if (oi < ga.nmat) {
+          double x = (ga.mult == 1.0 ? v : ga.mult * v) + (oi == oj ? ga.diag : 0.0);
+          if (oi == oj && ga.jit != 0.0) x = __fma_rn(x, ga.jit, x);
+          M[oi + oj * ga.ld] = x;
+        } else {
+          M[oi + oj * ga.ld] = v;  // rhs row (SMW: u = A_Jᵀ g)
+        }
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {  // the tile's last finisher resets both counters (every waiter is past its wait)
+      last = atomicAdd(cnt + 2 * tq + 1, 1u) == (unsigned)ns - 1;
+      if (last) {
+        cnt[2 * tq] = 0u;
+        cnt[2 * tq + 1] = 0u;
+      }
+    }
+    __syncthreads();
+  }
+}
+
 template <bool SMW, class Acc>
 __global__ void __launch_bounds__(256) k_gram(const Acc A, int64_t m, const int32_t* __restrict__ J, int64_t r,
                                               double* __restrict__ W, const double* __restrict__ gext, int tiles,

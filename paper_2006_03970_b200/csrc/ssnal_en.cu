@@ -290,6 +290,11 @@ struct ssnal_en_problem {
   int use_d2 = 1;    // option chol_d2: split-ownership DSMEM K4 (k_chol_d2) for 96 < N ≤ 512
   int d2_ok = 0;     // … schedulable on this device
   int gax_grid = 0;
+  int use_gram_sk = 1;  // option gram_sk: K3 as one cooperative round of (tile, K-slice) items (k_gram_sk)
+  int gsk_grid = 0;     // its grid: SMs × co-resident CTAs per SM (≤ 2)
+  int gsk_minch = 1;    // option gram_sk_minch: ≥ this many 32-wide reduction chunks per (tile, slice) item
+  double* gsk_part = nullptr;  // its partial tiles (max(grid, tiles) × 64 × 64)
+  unsigned* gsk_cnt = nullptr;  // its per-tile arrival / finish counters
   // device buffers
   double* w[3] = {nullptr, nullptr, nullptr};  // current / trial / backtrack
   double* x = nullptr;
@@ -569,6 +574,15 @@ int configure(ssnal_en_problem* P) {
     CK(cudaFuncSetAttribute(k_chol_dsm_any, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kD2Smem));
     CK(cudaFuncSetAttribute(k_chol_dsm_any, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   }
+  {  // k_gram_sk: co-resident CTAs per SM for its cooperative launch (both accessors: the sharded SMW
+     // form reads gathered fp64 columns even on a genotype handle)
+    int oa = 0, og = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oa, k_gram_sk<AccA>, 256, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&og, k_gram_sk<AccG>, 256, 0));
+    int occ = std::min(std::min(oa, og), 2);
+    P->gsk_grid = P->nsm * std::max(occ, 1);
+    if (occ < 1) P->use_gram_sk = 0;
+  }
   P->eval16_ok = 0;
   if (P->m <= 32 * kEval16) {
     CK(cudaFuncSetAttribute(k_eval_reduce16, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -653,6 +667,9 @@ int allocate(ssnal_en_problem* P) {
   d.add((void**)&P->cg_scal, (size_t)P->nsm * 2 * 8 + 64);
   d.add((void**)&P->ctl, sizeof(DevCtl));
   d.add((void**)&P->kflag, 256 * sizeof(int));
+  const int gsk_tiles = gram_tiles(m + 1);
+  d.add((void**)&P->gsk_part, (size_t)std::max(P->gsk_grid, gsk_tiles) * GT * GT * 8);
+  d.add((void**)&P->gsk_cnt, (size_t)(2 * gsk_tiles + 64) * 4);
   P->arena = pool_alloc(d.total);
   if (!P->arena) {
     set_err("device allocation of %zu bytes failed", d.total);
@@ -660,6 +677,7 @@ int allocate(ssnal_en_problem* P) {
   }
   d.assign((char*)P->arena);
   CK(cudaMemset(P->ticket, 0, 64));
+  CK(cudaMemset(P->gsk_cnt, 0, (size_t)(2 * gsk_tiles + 64) * 4));
   Arena h;
   h.add((void**)&P->ev_host, sizeof(EvalOut) * 4);
   h.add((void**)&P->scratch_host, 64 * 8);
@@ -1164,6 +1182,51 @@ unsigned gram_fused_grid(ssnal_en_problem* P, int tiles) {
   return (unsigned)(ncl * kGramCS);
 }
 
+// K3 of the Newton systems (Eq. (18)/(19)): k_gram_sk (one cooperative round over the whole GPU) or,
+// with option gram_sk = 0, k_gram_fused (8-CTA clusters per tile).  geo: graph mode (worst-case
+// grid); only > 0: one branch alone.
+template <class Acc>
+int launch_gram_one(ssnal_en_problem* P, const Acc& acc, const int32_t* J, const double* g, const GramFusedArgs& gfa,
+                    const DirGeo* geo, int only, bool sk) {
+  if (only < 0) return SSNAL_OK;
+  if (!sk) {
+    k_gram_fused<<<gram_fused_grid(P, geo ? gram_tiles(P->m) : gfa.tiles), 256, 0, P->st>>>(acc, P->m, J, P->Mmat, g,
+                                                                                           gfa, geo, only);
+  } else {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(P->gsk_grid);
+    cfg.blockDim = dim3(256);
+    cfg.stream = P->st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, k_gram_sk<Acc>, acc, P->m, J, P->Mmat, g, gfa, geo, only, P->gsk_part, P->gsk_cnt,
+                          P->gsk_minch));
+  }
+  P->launches++;
+  CKL();
+  return SSNAL_OK;
+}
+
+template <class Acc>
+int launch_gram(ssnal_en_problem* P, const Acc& acc, const int32_t* J, const double* g, const GramFusedArgs& gfa,
+                const DirGeo* geo, int only = 0) {
+  // option gram_sk: 0 = k_gram_fused for both branches; 1 (default) = k_gram_fused for the SMW branch
+  // (few tiles, K = m: its DSMEM reduction beats the L2 round trip of the partials and the launch of a
+  // full-GPU grid) and k_gram_sk for m × m (36 tiles at m = 500, K = r large); 2 = k_gram_sk for both.
+  // Graph mode with option 1: one node of each, predicated on its branch.
+  if (P->use_gram_sk == 1) {
+    if (geo) {
+      int rc = launch_gram_one(P, acc, J, g, gfa, geo, only == 2 ? -1 : 1, 0);
+      if (rc) return rc;
+      return only == 1 ? SSNAL_OK : launch_gram_one(P, acc, J, g, gfa, geo, 2, 1);
+    }
+    return launch_gram_one(P, acc, J, g, gfa, nullptr, only, gfa.branch == 2);
+  }
+  return launch_gram_one(P, acc, J, g, gfa, geo, only, P->use_gram_sk == 2);
+}
 unsigned reduce_grid(ssnal_en_problem* P, int64_t tot) {
   int64_t g = (tot + 255) / 256;
   if (g > 4 * P->nsm) g = 4 * P->nsm;
@@ -1225,8 +1288,7 @@ int newton_direction_sharded(ssnal_en_problem* P, const int32_t* J, int64_t rg, 
     geo.jit = jit;
     const AccA ga{GA, m};
     const GramFusedArgs gfa{1, rg, geo.nout, geo.nmat, geo.tiles, geo.ld, geo.diag, geo.mult, geo.jit};
-    k_gram_fused<<<gram_fused_grid(P, geo.tiles), 256, 0, P->st>>>(ga, m, P->iota, P->Mmat, g, gfa, nullptr);
-    P->launches++;
+    if ((rc = launch_gram(P, ga, P->iota, g, gfa, nullptr))) return rc;
     CKL();
     if ((rc = launch_chol(P, P->Mmat, geo.N, P->u, 1.0, nullptr, nullptr))) return rc;
     k_gather_rows<<<gather_rows_grid(P), 256, 0, P->st>>>(ga, m, P->iota, P->u, rg, nullptr, nullptr, nullptr,
@@ -1277,13 +1339,9 @@ int newton_direction(ssnal_en_problem* P, const int32_t* J, int64_t r, const dou
   CK(cudaMemsetAsync(P->info, 0, sizeof(int), P->st));
   const GramFusedArgs gfa{geo.branch, r, geo.nout, geo.nmat, geo.tiles, geo.ld, geo.diag, geo.mult, geo.jit};
   if (geo.branch == 1) {  // Sherman–Morrison–Woodbury, Eq. (19): factor κ⁻¹I_r + A_JᵀA_J (R13)
-    with_acc(P, [&](auto acc) {
-      k_gram_fused<<<gram_fused_grid(P, geo.tiles), 256, 0, P->st>>>(acc, m, J, P->Mmat, g, gfa, nullptr);
-      return 0;
-    });
-    P->launches++;
-    CKL();
-    int rc = launch_chol(P, P->Mmat, geo.N, P->u, 1.0, nullptr, nullptr);  // v = (κ⁻¹I + G)⁻¹ u
+    int rc = with_acc(P, [&](auto acc) { return launch_gram(P, acc, J, g, gfa, nullptr); });
+    if (rc) return rc;
+    rc = launch_chol(P, P->Mmat, geo.N, P->u, 1.0, nullptr, nullptr);  // v = (κ⁻¹I + G)⁻¹ u
     if (rc) return rc;
     // d = −g + A_J v, gᵀd, y_t = y + d (last-CTA finalisation)
     with_acc(P, [&](auto acc) {
@@ -1297,12 +1355,7 @@ int newton_direction(ssnal_en_problem* P, const int32_t* J, int64_t r, const dou
     return SSNAL_OK;
   }
   // r ≥ m: Eq. (18), M = I_m + κ A_J A_Jᵀ; the fused reduce also writes g into the rhs row
-  with_acc(P, [&](auto acc) {
-    k_gram_fused<<<gram_fused_grid(P, geo.tiles), 256, 0, P->st>>>(acc, m, J, P->Mmat, g, gfa, nullptr);
-    return 0;
-  });
-  P->launches++;
-  CKL();
+  if (int rc = with_acc(P, [&](auto acc) { return launch_gram(P, acc, J, g, gfa, nullptr); })) return rc;
   return launch_chol(P, P->Mmat, (int)m, d, -1.0, g, gd_dev, y, yt);  // d = −M⁻¹ g, gd = gᵀd
 }
 
@@ -1327,14 +1380,15 @@ int newton_direction_graph_peer(ssnal_en_problem* P) {
     return 0;
   });
   k_peer_index<<<1, 1024, 0, P->st>>>(P->pc, geo, 0, P->peer_idx);
-  // SMW on the gathered columns: the fused split-K Gram (its grid covers the worst case r < m)
-  k_gram_fused<<<gram_fused_grid(P, gram_tiles(m)), 256, 0, P->st>>>(ga, m, P->peer_idx, P->Mmat, P->g[0],
-                                                                     GramFusedArgs{}, geo, 1);
+  P->launches += 3;
+  // SMW on the gathered columns (the K3 launch of the unsharded graph, restricted to branch 1)
+  int rc = launch_gram(P, ga, P->peer_idx, P->g[0], GramFusedArgs{}, geo, 1);
+  if (rc) return rc;
   k_peer_put_gram<<<reduce_grid(P, m * m), 256, 0, P->st>>>(P->pc, P->W, P->r_dev + 0, m, geo, P->nsm, P->W_splits);
   k_peer_gram_sum<<<reduce_grid(P, m * m), 256, 0, P->st>>>(P->pc, m, P->Mmat, P->g[0], geo, 0.0, 0, 0.0);
-  P->launches += 6;
+  P->launches += 2;
   CKL();
-  int rc = launch_chol(P, P->Mmat, 0, nullptr, 0.0, nullptr, nullptr, nullptr, nullptr, geo, -1);
+  rc = launch_chol(P, P->Mmat, 0, nullptr, 0.0, nullptr, nullptr, nullptr, nullptr, geo, -1);
   if (rc) return rc;
   k_gather_rows<<<gather_rows_grid(P), 256, 0, P->st>>>(ga, m, P->peer_idx, P->u, 0, nullptr, nullptr, geo, kGatherSmw,
                                                          P->d, P->g[0], P->y[0], P->y[1], P->scratch, P->blk,
@@ -1351,13 +1405,10 @@ int newton_direction_graph(ssnal_en_problem* P) {
   const int32_t* J = P->J[0];
   const double* g = P->g[0];
   double* gd = P->scratch;
-  with_acc(P, [&](auto acc) {  // worst-case grid: the m × m tiles (SMW tiles for r < m are fewer)
-    k_gram_fused<<<gram_fused_grid(P, gram_tiles(m)), 256, 0, P->st>>>(acc, m, J, P->Mmat, g, GramFusedArgs{}, geo);
-    return 0;
-  });
-  P->launches += 1;
-  CKL();
-  int rc = launch_chol(P, P->Mmat, 0, nullptr, 0.0, nullptr, nullptr, nullptr, nullptr, geo, -1);
+  // K3 (worst-case grid: the m × m tiles; the SMW tiles for r < m are fewer)
+  int rc = with_acc(P, [&](auto acc) { return launch_gram(P, acc, J, g, GramFusedArgs{}, geo); });
+  if (rc) return rc;
+  rc = launch_chol(P, P->Mmat, 0, nullptr, 0.0, nullptr, nullptr, nullptr, nullptr, geo, -1);
   if (rc) return rc;
   with_acc(P, [&](auto acc) {  // SMW back-substitution, or d = −g when r = 0
     k_gather_rows<<<gather_rows_grid(P), 256, 0, P->st>>>(acc, m, J, P->u, 0, nullptr, nullptr, geo, kGatherSmw, P->d,
@@ -2327,6 +2378,14 @@ int ssnal_en_set_option(ssnal_en_problem* P, const char* key, double v) {
     P->k1_smem = smem;
     drop_graph(P);  // the K1 launch configuration is baked into the graph
   }
+  else if (k == "gram_sk_minch" && v >= 1 && v <= 64) {
+    P->gsk_minch = (int)v;
+    drop_graph(P);
+  }
+  else if (k == "gram_sk" && (v == 0 || v == 1 || v == 2)) {
+    P->use_gram_sk = (int)v;
+    drop_graph(P);  // the K3 launch is baked into the graph
+  }
   else if (k == "small" && (v == 0 || v == 1))
     P->use_small = (int)v;
   else if (k == "small_cluster" && (v == 0 || v == 1))
@@ -2364,6 +2423,8 @@ double ssnal_en_get_info(const ssnal_en_problem* P, const char* key) {
   if (k == "n") return (double)P->n;
   if (k == "k1_cols") return P->C;
   if (k == "k1_stages") return P->S;
+  if (k == "gram_sk") return P->use_gram_sk;
+  if (k == "gram_sk_grid") return P->gsk_grid;
   if (k == "k1_grid") return P->G;
   if (k == "k1_smem") return (double)P->k1_smem;
   if (k == "cluster_size") return P->cluster;

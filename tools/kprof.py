@@ -33,6 +33,7 @@ def main():
     ap.add_argument("--n", type=int, default=0)
     ap.add_argument("--control", default="graph", choices=["graph", "host"])
     ap.add_argument("--newton", default="", help="comma list of r: time the Newton direction hook (m=500)")
+    ap.add_argument("--set", action="append", default=[], help="library option key=value (repeatable)")
     args = ap.parse_args()
     if args.newton:
         return newton(args)
@@ -47,6 +48,9 @@ def main():
     db = torch.from_numpy(b).cuda()
     P = Problem.from_device(dA.data_ptr(), db.data_ptr(), m, n, st.cuda_stream, keep=(dA, db))
     P.set_option("graph", 1 if args.control == "graph" else 0)
+    for kv in args.set:
+        k, v = kv.split("=")
+        P.set_option(k, float(v))
     lm = P.lambda_max_l1 / cfg.alpha
     x = torch.zeros(n, dtype=torch.float64, device="cuda")
 
@@ -85,6 +89,9 @@ def newton(args):
     A = synth.design(cfg)
     b, _ = synth.response(cfg)
     P = Problem(A, b)
+    for kv in args.set:
+        k, v = kv.split("=")
+        P.set_option(k, float(v))
     g = torch.from_numpy(synth.normals(3, 8, m)).cuda()
     d = torch.empty(m, dtype=torch.float64, device="cuda")
     for r in [int(v) for v in args.newton.split(",")]:
