@@ -54,10 +54,15 @@ def main():
     lm = P.lambda_max_l1 / cfg.alpha
     x = torch.zeros(n, dtype=torch.float64, device="cuda")
 
+    X = torch.zeros((len(cfg.cs), n), dtype=torch.float64, device="cuda")
+
     def step():
+        if cfg.path:  # the bench's warm-started path (σ carried, one synchronisation per path)
+            P.solve_path_device([c * cfg.alpha * lm for c in cfg.cs], [c * (1 - cfg.alpha) * lm for c in cfg.cs],
+                                cfg.sigma0, cfg.tol, 0, X.data_ptr())
+            return
         for i, c in enumerate(cfg.cs):
-            P.solve_device(c * cfg.alpha * lm, c * (1 - cfg.alpha) * lm, cfg.sigma0, cfg.tol,
-                           x.data_ptr() if (cfg.path and i > 0) else 0, x.data_ptr())
+            P.solve_device(c * cfg.alpha * lm, c * (1 - cfg.alpha) * lm, cfg.sigma0, cfg.tol, 0, x.data_ptr())
 
     for _ in range(3):
         step()

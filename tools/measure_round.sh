@@ -5,7 +5,7 @@
 # Everything lands in gpurun_out/r2/; the summaries are copied to profiles/ afterwards.
 set -x
 cd $GRAFT_REPO_ROOT
-O=gpurun_out/r2; mkdir -p $O
+O=${MEASURE_OUT:-gpurun_out/r2}; mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $O/smi.txt
 lscpu > $O/lscpu.txt; nproc >> $O/lscpu.txt; free -g >> $O/lscpu.txt
 timeout 2400 python -m pytest tests -m gpu -q > $O/gputests.log 2>&1; echo "gpu tests rc=$?" >> $O/status.txt
@@ -18,6 +18,9 @@ timeout 900 python bench.py --config cfg4 --geno --steps 20 --warmup 5 > $O/benc
 timeout 900 python bench.py --sweep > $O/bench_sweep.jsonl 2> $O/sweep.err; echo "sweep rc=$?" >> $O/status.txt
 timeout 900 python bench.py --select --cv 5 --steps 5 --warmup 3 > $O/bench_select.json 2> $O/select.err; echo "select rc=$?" >> $O/status.txt
 timeout 900 python bench.py --config cfg2 --shard --steps 10 --warmup 3 --no-cpu --no-e2e > $O/bench_cfg2_shard.json 2> $O/shard.err; echo "shard rc=$?" >> $O/status.txt
+timeout 900 python bench.py --config cfg2 --shard --shard-comm nccl --steps 10 --warmup 3 --no-cpu --no-e2e > $O/bench_cfg2_shard_nccl.json 2> $O/shard_nccl.err; echo "shard nccl rc=$?" >> $O/status.txt
+timeout 300 tools/probes/read_probe > $O/read_probe.jsonl 2>&1; echo "read probe rc=$?" >> $O/status.txt
+timeout 600 python tools/kprof.py --newton 20,100,250,435,700,1165,2000,5000,10193 > $O/kprof_newton.txt 2>&1
 # launch lists (cold-cache, serialised: compare shares, not absolutes)
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 20000 --csv --log-file $O/launches_cfg2.csv python bench.py --config cfg2 --steps 1 --warmup 3 --no-cpu --no-e2e --control host > $O/ncu_list2.log 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 20000 --csv --log-file $O/launches_cfg5.csv python bench.py --config cfg5 --steps 1 --warmup 3 --no-cpu --no-e2e --control host > $O/ncu_list5.log 2>&1
@@ -33,11 +36,13 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:k1g_
 summ k1g_cfg4
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_chol_d2 -s 40 -c 1 -o $O/k4_d2_cfg2 python bench.py --config cfg2 --steps 1 --warmup 3 --no-cpu --no-e2e --control host > $O/ncu_d2.log 2>&1
 summ k4_d2_cfg2
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_gram_fused -c 1 -o $O/k3_mxm_r10193 python tools/ncu_newton.py --r 10193 --n 20000 > $O/ncu_k3a.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_gram_sk -c 1 -o $O/k3_mxm_r10193 python tools/ncu_newton.py --r 10193 --n 20000 > $O/ncu_k3a.log 2>&1
 summ k3_mxm_r10193
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_gram_fused -c 1 -o $O/k3_smw_r435 python tools/ncu_newton.py --r 435 > $O/ncu_k3b.log 2>&1
 summ k3_smw_r435
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_small_cl -s 3 -c 1 -o $O/k7_cfg1 python bench.py --config cfg1 --steps 1 --warmup 3 --no-cpu --no-e2e > $O/ncu_k7.log 2>&1
 summ k7_cfg1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_peer_eval -s 20 -c 1 -o $O/peer_eval_cfg2 python bench.py --config cfg2 --shard --steps 1 --warmup 3 --no-cpu --no-e2e --control host > $O/ncu_peer.log 2>&1
+summ peer_eval_cfg2
 du -sh $O >> $O/status.txt
 echo done >> $O/status.txt
