@@ -46,6 +46,22 @@ import synth  # noqa: E402
 METRIC = "time-to-solution (s) at KKT 1e-6; fused A^T·y kernel GB/s vs B200 HBM peak"
 
 
+def _read_ceiling():
+    """The best plain READ stream measured on this pool's B200s by tools/probes/read_probe (committed
+    under profiles/): context for K1, which reads 8mn bytes and writes 8n; the roofline denominator stays
+    the driver's copy rate."""
+    p = os.path.join(ROOT, "profiles", "r2_read_ceiling_probe.jsonl")
+    if not os.path.exists(p):
+        return None
+    best = 0.0
+    for line in open(p):
+        try:
+            best = max(best, float(json.loads(line).get("GBps", 0.0)))
+        except (ValueError, AttributeError):
+            pass
+    return best or None
+
+
 def _peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -397,9 +413,12 @@ def bench_ours(args, rank, world, local_rank):
                     not args.geno else {**({"bound": "hbm", "achieved": k1_gbs, "peak": peak, "unit": "GB/s",
                          "frac": (k1_gbs / peak) if k1_gbs else None, "traffic": traffic, "peak_source": peak_src,
                          "frac_of_nominal_8TBps": (k1_gbs / 8000.0) if k1_gbs else None,
+                         "read_ceiling_GBps": _read_ceiling(),
+                         "frac_of_read_ceiling": (k1_gbs / _read_ceiling()) if (k1_gbs and _read_ceiling()) else None,
                          "note": "peak = the driver's measured copy rate (read+write bytes of a bf16 copy); a "
                                  "read-dominated stream can exceed it, so frac > 1 is possible; the nominal "
-                                 "8 TB/s view is frac_of_nominal_8TBps (north-star target >= 0.70)"}
+                                 "8 TB/s view is frac_of_nominal_8TBps (north-star target >= 0.70); read_ceiling_GBps "
+                                 "is the best plain read stream of tools/probes/read_probe on this pool"}
                         if not args.geno else geno_roofline(m, n, k1_avg, k1_gbs, peak, traffic)),
                      "kernel": "k1g_aty_fused" if args.geno else "k1_aty_fused",
                      "bytes_per_launch": k1_bytes(m, n, args.geno), "launches": k1_launches,

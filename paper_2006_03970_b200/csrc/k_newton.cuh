@@ -573,8 +573,8 @@ __global__ void __cluster_dims__(kGramCS, 1, 1) __launch_bounds__(256)
     cluster.sync();
     const int64_t o0 = (int64_t)ti * GT, o1 = (int64_t)tj * GT;
     constexpr int RPR = GT / kGramCS;  // output rows reduced by each rank
-    for (int e = tid; e < RPR * GT; e += 256) {
-      const int w = RPR * s + e / GT, k = e % GT;
+    for (int e = tid; e < RPR * GT; e += 256) {  // rows fastest: 64-byte column segments of M
+      const int w = RPR * s + e % RPR, k = e / RPR;
       const int64_t oi = o0 + w, oj = o1 + k;
       if (oi < ga.nout && oj < ga.nout && oi >= oj) {
         double v = 0.0;
@@ -598,7 +598,7 @@ __global__ void __cluster_dims__(kGramCS, 1, 1) __launch_bounds__(256)
 // second round of 3 clusters doubled the time at large r.  Here the work items are (tile, K-slice)
 // pairs with ns = min(grid / tiles, chunks / minch) slices per tile, so every item runs in ONE round of a
 // cooperative launch (all CTAs co-resident): CTA b takes item b, sums its K-slice of the tile on
-// the FP64 tensor cores (gram_item), stores the partial tile to P (L2), and arrives on the tile's
+// the FP64 tensor cores (gram_item), stores the partial tile to P (L2, column-major), and arrives on the tile's
 // counter; the ns CTAs of a tile wait for all ns partials, then slice s reduces rows
 // [64s/ns, 64(s+1)/ns) of the tile over the slices in slice order (deterministic) with the
 // k_gram_reduce epilogue (× mult, + diag, jitter, rhs row) straight into M.  The last CTA of a tile
@@ -647,7 +647,7 @@ __global__ void __launch_bounds__(256, 2)
 #pragma unroll
       for (int j = 0; j < 4; ++j)
 #pragma unroll
-        for (int e = 0; e < 2; ++e) __stcg(Pi + (16 * wr + 8 * i + gq) * GT + 32 * wc + 8 * j + 2 * t + e, acc[i][j][e]);
+        for (int e = 0; e < 2; ++e) __stcg(Pi + (32 * wc + 8 * j + 2 * t + e) * GT + 16 * wr + 8 * i + gq, acc[i][j][e]);
     __threadfence();
     __syncthreads();
     if (tid == 0) {
@@ -660,12 +660,13 @@ __global__ void __launch_bounds__(256, 2)
     const int64_t o0 = (int64_t)ti * GT, o1 = (int64_t)tj * GT;
     const int w0 = GT * s / ns, w1 = GT * (s + 1) / ns;
     const double* Pb = Pt + (size_t)tq * ns * GT * GT;
-    for (int e = tid; e < (w1 - w0) * GT; e += 256) {
-      const int w = w0 + e / GT, k = e % GT;
+    const int nr = w1 - w0;
+    for (int e = tid; e < nr * GT; e += 256) {  // rows fastest: contiguous partial-tile columns and M segments
+      const int w = w0 + e % nr, k = e / nr;
       const int64_t oi = o0 + w, oj = o1 + k;
       if (oi < ga.nout && oj < ga.nout && oi >= oj) {
         double v = 0.0;
-        for (int q = 0; q < ns; ++q) v += __ldcg(Pb + (size_t)q * GT * GT + w * GT + k);
+        for (int q = 0; q < ns; ++q) v += __ldcg(Pb + (size_t)q * GT * GT + k * GT + w);
         if (oi < ga.nmat) {
           double x = (ga.mult == 1.0 ? v : ga.mult * v) + (oi == oj ? ga.diag : 0.0);
           if (oi == oj && ga.jit != 0.0) x = __fma_rn(x, ga.jit, x);

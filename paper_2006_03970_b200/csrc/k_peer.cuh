@@ -90,7 +90,7 @@ SSN_DEV bool peer_wait(const PeerComm& pc, unsigned long long e) {
 // ---- the evaluation record of a sharded ψ evaluation ----
 // rec[k], k < m: Σ_b part_vec[b][k] over the valid rows; m ≤ k < m + 4: Σ_q part_scal[q][k − m];
 // k = m + 4: the local r.  One 16-CTA cluster: CTA c takes the 32-element blocks kb ≡ c (mod 16);
-// lane = element, warp w sums rows b ≡ w (mod 8) ascending (4 loads in flight), the 8 warp sums are
+// lane = element, warp w sums rows b ≡ w (mod 8) ascending (8 loads in flight), the 8 warp sums are
 // added in warp order — a fixed order, so every caller that uses rec_block gets identical bits.
 constexpr int kRecCS = 16;
 SSN_DEV void rec_block(int kb, int64_t m, const double* __restrict__ part_vec, const int* __restrict__ valid,
@@ -100,17 +100,17 @@ SSN_DEV void rec_block(int kb, int64_t m, const double* __restrict__ part_vec, c
   const int64_t k = (int64_t)kb * 32 + lane;
   double s = 0.0;
   if (k < m) {
-    for (int b0 = warp; b0 < nparts; b0 += 32) {
-      double v[4];
-      bool ok[4];
+    for (int b0 = warp; b0 < nparts; b0 += 64) {
+      double v[8];
+      bool ok[8];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < 8; ++u) {
         const int b = b0 + 8 * u;
         ok[u] = b < nparts && (!valid || valid[b]);
-        v[u] = ok[u] ? part_vec[(size_t)b * m + k] : 0.0;
+        v[u] = ok[u] ? __ldcg(part_vec + (size_t)b * m + k) : 0.0;
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int u = 0; u < 8; ++u)
         if (ok[u]) s += v[u];
     }
   } else if (k < m + 4) {
