@@ -573,8 +573,9 @@ __global__ void __cluster_dims__(kGramCS, 1, 1) __launch_bounds__(256)
     cluster.sync();
     const int64_t o0 = (int64_t)ti * GT, o1 = (int64_t)tj * GT;
     constexpr int RPR = GT / kGramCS;  // output rows reduced by each rank
-    for (int e = tid; e < RPR * GT; e += 256) {  // rows fastest: 64-byte column segments of M
-      const int w = RPR * s + e % RPR, k = e / RPR;
+    for (int e = tid; e < RPR * GT; e += 256) {  // columns fastest: contiguous DSMEM reads of the partial
+      const int w = RPR * s + e / GT, k = e % GT;  // tiles (rows fastest coalesces the M stores but scatters
+                                                   // the remote reads: r = 435 15.3 → 24.1 µs, measured)
       const int64_t oi = o0 + w, oj = o1 + k;
       if (oi < ga.nout && oj < ga.nout && oi >= oj) {
         double v = 0.0;
