@@ -257,76 +257,76 @@ __global__ void k_peer_reduce_big(PeerComm pc, double* __restrict__ buf, int64_t
   }
 }
 
-// SMW branch (0 < r < m, Eq. (19)): the all-gather of the active columns fused into the gather.
-// Column a of this rank's local A_J goes straight to column a of big slot [rank] in EVERY rank's
-// region (capacity ccap ≥ m columns of m doubles), its count to cnt[rank]; the last CTA signals.
-// graph mode: predicated on the global branch (geo).
+// A sharded Newton direction in graph mode (§8(f3)), predicated on the GLOBAL branch (geo), in two
+// merged nodes (each serves both branches, so a step pays no predicated-off node for them):
+//
+// SMW branch (0 < r < m, Eq. (19)) — the all-gather of the active columns fused into the gather:
+//   dir1: column a of this rank's local A_J goes straight to column a of big slot [rank] in EVERY
+//         rank's region (capacity ccap ≥ m columns of m doubles), its count to cnt[rank]; the last
+//         CTA signals;
+//   dir2: one CTA waits for the gathered columns, then idx[0, rg) = the big-region column of each
+//         gathered column in rank order (rank q's column i → q·ccap + i), so the SMW kernels read A_J
+//         through AccA{big, m} and idx exactly as from a packed r × m buffer (counts that do not add
+//         up to the global r set err = 2).
+// m × m branch (r ≥ m, Eq. (18)) — the GEMM → all-gather fusion of the partial Grams:
+//   dir1: the local partial Gram A_J A_Jᵀ of this rank's active columns (split-K slices into W; ns
+//         from the LOCAL r, as the host-driven sharded path);
+//   dir2: its slices summed (k_gram_reduce's order and epilogue with diag 0, mult 1) and deposited
+//         into big slot [rank] of every rank; the last CTA signals;
+//   k_peer_gram_sum (below) then forms the Newton matrix on every rank.
 template <class Acc>
-__global__ void __launch_bounds__(256) k_peer_put_cols(PeerComm pc, const Acc A, int64_t m,
-                                                       const int32_t* __restrict__ J,
-                                                       const int64_t* __restrict__ r_dev, const DirGeo* geo) {
-  if (geo && geo->branch != 1) return;
-  const int64_t r = *r_dev;
-  for (int64_t a = blockIdx.x; a < r; a += gridDim.x) {
-    const auto col = A.col(J[a]);
-    for (int64_t k = threadIdx.x; k < m; k += blockDim.x) {
-      const double v = col.ld(k);
-      for (int q = 0; q < pc.size; ++q) peer_big(pc, q, pc.rank)[a * m + k] = v;
-    }
-  }
-  if (blockIdx.x == 0 && threadIdx.x == 0)
-    for (int q = 0; q < pc.size; ++q) peer_cnt(pc, q)[pc.rank] = r;
-  peer_last_cta_signal(pc);
-}
-// One CTA: wait for the gathered columns, then idx[0, rg) = the big-region column of each gathered
-// column in rank order (rank q's column i → q·ccap + i), so the SMW kernels read A_J through
-// AccA{big, m} and idx exactly as from a packed r × m buffer.  Counts that do not add up to the
-// global r set err = 2.
-__global__ void k_peer_index(PeerComm pc, const DirGeo* geo, int64_t rg, int32_t* __restrict__ idx) {
-  __shared__ int64_t off[kPeerMaxRanks + 1];
-  if (geo) {
-    if (geo->branch != 1) return;
-    rg = geo->r;
-  }
-  peer_cta_wait(pc);
-  if (threadIdx.x == 0) {
-    off[0] = 0;
-    for (int q = 0; q < pc.size; ++q) off[q + 1] = off[q] + *(volatile int64_t*)(peer_cnt(pc, pc.rank) + q);
-    if (off[pc.size] != rg) atomicExch(pc.err, 2);
-  }
-  __syncthreads();
-  for (int q = 0; q < pc.size; ++q)
-    for (int64_t i = threadIdx.x; i < off[q + 1] - off[q] && off[q] + i < rg; i += blockDim.x)
-      idx[off[q] + i] = (int32_t)(q * pc.ccap + i);
-}
-
-// m × m branch (r ≥ m, Eq. (18)): the local partial Gram A_J A_Jᵀ of this rank's active columns
-// (split-K slices into W; ns from the LOCAL r, as the host-driven sharded path) …
-template <class Acc>
-__global__ void __launch_bounds__(256) k_gram_local(const Acc A, int64_t m, const int32_t* __restrict__ J,
-                                                    const int64_t* __restrict__ r_dev, double* __restrict__ W,
-                                                    const DirGeo* geo, int nsm, int wsplits) {
+__global__ void __launch_bounds__(256) k_peer_dir1(PeerComm pc, const Acc A, int64_t m, const int32_t* __restrict__ J,
+                                                   const int64_t* __restrict__ r_dev, double* __restrict__ W,
+                                                   const DirGeo* geo, int nsm, int wsplits) {
   __shared__ double sA[kGramSmem], sB[kGramSmem];
-  if (geo && geo->branch != 2) return;
+  const int br = geo->branch;
   const int64_t r = *r_dev;
-  const int tiles = gram_tiles(m), ns = gram_splits(nsm, tiles, r, wsplits);
-  gram_body<false>(A, m, J, r, W, nullptr, tiles, ns, sA, sB);
-}
-// … its slices summed (k_gram_reduce's order and epilogue with diag 0, mult 1) and deposited into
-// big slot [rank] of every rank (the GEMM → all-gather fusion of the partial Grams) …
-__global__ void k_peer_put_gram(PeerComm pc, const double* __restrict__ W, const int64_t* __restrict__ r_dev,
-                                int64_t m, const DirGeo* geo, int nsm, int wsplits) {
-  if (geo && geo->branch != 2) return;
-  const int ns = gram_splits(nsm, gram_tiles(m), *r_dev, wsplits);
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m * m; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = e % m, j = e / m;
-    if (i < j) continue;
-    double s = 0.0;
-    for (int q = 0; q < ns; ++q) s += W[(size_t)q * m * m + e];
-    const double v = s + 0.0;  // k_gram_reduce with diag = 0: + 0.0 on every stored entry
-    for (int q = 0; q < pc.size; ++q) peer_big(pc, q, pc.rank)[e] = v;
+  if (br == 1) {
+    for (int64_t a = blockIdx.x; a < r; a += gridDim.x) {
+      const auto col = A.col(J[a]);
+      for (int64_t k = threadIdx.x; k < m; k += blockDim.x) {
+        const double v = col.ld(k);
+        for (int q = 0; q < pc.size; ++q) peer_big(pc, q, pc.rank)[a * m + k] = v;
+      }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+      for (int q = 0; q < pc.size; ++q) peer_cnt(pc, q)[pc.rank] = r;
+    peer_last_cta_signal(pc);
+  } else if (br == 2) {
+    const int tiles = gram_tiles(m), ns = gram_splits(nsm, tiles, r, wsplits);
+    gram_body<false>(A, m, J, r, W, nullptr, tiles, ns, sA, sB);
   }
-  peer_last_cta_signal(pc);
+}
+__global__ void k_peer_dir2(PeerComm pc, const double* __restrict__ W, const int64_t* __restrict__ r_dev, int64_t m,
+                            const DirGeo* geo, int nsm, int wsplits, int32_t* __restrict__ idx) {
+  __shared__ int64_t off[kPeerMaxRanks + 1];
+  const int br = geo->branch;
+  if (br == 1) {
+    if (blockIdx.x != 0) return;
+    const int64_t rg = geo->r;
+    peer_cta_wait(pc);
+    if (threadIdx.x == 0) {
+      off[0] = 0;
+      for (int q = 0; q < pc.size; ++q) off[q + 1] = off[q] + *(volatile int64_t*)(peer_cnt(pc, pc.rank) + q);
+      if (off[pc.size] != rg) atomicExch(pc.err, 2);
+    }
+    __syncthreads();
+    for (int q = 0; q < pc.size; ++q)
+      for (int64_t i = threadIdx.x; i < off[q + 1] - off[q] && off[q] + i < rg; i += blockDim.x)
+        idx[off[q] + i] = (int32_t)(q * pc.ccap + i);
+  } else if (br == 2) {
+    const int ns = gram_splits(nsm, gram_tiles(m), *r_dev, wsplits);
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m * m;
+         e += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t i = e % m, j = e / m;
+      if (i < j) continue;
+      double s = 0.0;
+      for (int q = 0; q < ns; ++q) s += W[(size_t)q * m * m + e];
+      const double v = s + 0.0;  // k_gram_reduce with diag = 0: + 0.0 on every stored entry
+      for (int q = 0; q < pc.size; ++q) peer_big(pc, q, pc.rank)[e] = v;
+    }
+    peer_last_cta_signal(pc);
+  }
 }
 // … and every rank forms M = I_m + κ Σ_q (rank order) with the jitter and the rhs row g, as
 // k_gram_reduce(Σ, ns = 1, diag = 1, mult = κ) does on the summed buffer of the host-driven path.

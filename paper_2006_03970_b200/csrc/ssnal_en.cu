@@ -1363,11 +1363,11 @@ int newton_direction(ssnal_en_problem* P, const int32_t* J, int64_t r, const dou
 // control kernels from r); worst-case grids, surplus CTAs exit.  Same work decomposition as
 // newton_direction for the same r.  Reads J[0], g[0], y[0]; writes d, y[1], gᵀd → scratch[0].
 // Graph mode on a peer-attached sharded handle (§8(f3)): the same branch kernels as the
-// host-driven sharded direction, with the exchanges fused into them over peer memory —
-//   0 < r < m: k_peer_put_cols writes the local A_J into every rank's big slot (the all-gather),
-//              k_peer_index orders the gathered columns by rank, SMW Eq. (19) reads them in place;
-//   r ≥ m:     the local partial Gram (k_gram_local) is deposited into every rank by k_peer_put_gram
-//              and k_peer_gram_sum forms I_m + κ Σ_q in rank order (Eq. (18)).
+// host-driven sharded direction, with the exchanges fused into them over peer memory (k_peer.cuh) —
+//   0 < r < m: k_peer_dir1 writes the local A_J into every rank's big slot (the all-gather),
+//              k_peer_dir2 orders the gathered columns by rank, SMW Eq. (19) reads them in place;
+//   r ≥ m:     k_peer_dir1 forms the local partial Gram, k_peer_dir2 deposits it into every rank and
+//              k_peer_gram_sum forms I_m + κ Σ_q in rank order (Eq. (18)).
 // Every kernel is predicated on the global branch (geo from the global r); worst-case grids.
 int newton_direction_graph_peer(ssnal_en_problem* P) {
   const int64_t m = P->m;
@@ -1375,18 +1375,17 @@ int newton_direction_graph_peer(ssnal_en_problem* P) {
   const AccA ga{(const double*)(P->pc.base[P->pc.rank] + peer_big_off(P->pc.size, P->pc.ss)), m};
   const unsigned gsm = 2 * P->nsm;
   with_acc(P, [&](auto acc) {
-    k_peer_put_cols<<<gsm, 256, 0, P->st>>>(P->pc, acc, m, P->J[0], P->r_dev + 0, geo);
-    k_gram_local<<<gsm, 256, 0, P->st>>>(acc, m, P->J[0], P->r_dev + 0, P->W, geo, P->nsm, P->W_splits);
+    k_peer_dir1<<<gsm, 256, 0, P->st>>>(P->pc, acc, m, P->J[0], P->r_dev + 0, P->W, geo, P->nsm, P->W_splits);
     return 0;
   });
-  k_peer_index<<<1, 1024, 0, P->st>>>(P->pc, geo, 0, P->peer_idx);
-  P->launches += 3;
+  k_peer_dir2<<<reduce_grid(P, m * m), 256, 0, P->st>>>(P->pc, P->W, P->r_dev + 0, m, geo, P->nsm, P->W_splits,
+                                                        P->peer_idx);
+  P->launches += 2;
   // SMW on the gathered columns (the K3 launch of the unsharded graph, restricted to branch 1)
   int rc = launch_gram(P, ga, P->peer_idx, P->g[0], GramFusedArgs{}, geo, 1);
   if (rc) return rc;
-  k_peer_put_gram<<<reduce_grid(P, m * m), 256, 0, P->st>>>(P->pc, P->W, P->r_dev + 0, m, geo, P->nsm, P->W_splits);
   k_peer_gram_sum<<<reduce_grid(P, m * m), 256, 0, P->st>>>(P->pc, m, P->Mmat, P->g[0], geo, 0.0, 0, 0.0);
-  P->launches += 2;
+  P->launches++;
   CKL();
   rc = launch_chol(P, P->Mmat, 0, nullptr, 0.0, nullptr, nullptr, nullptr, nullptr, geo, -1);
   if (rc) return rc;
