@@ -398,6 +398,145 @@ __global__ void k_var(const double* Sg, double* M, double* W, int* info, unsigne
   long long c1 = clock64();
   if (threadIdx.x == 0) cyc[0] = c1 - c0;
 }
+// Reciprocal-pivot chain (LDL^T-style): the Schur complement is kept UNNORMALISED inside a block, so
+// the dependent chain per pivot is rcp(d) -> c*inv -> fma into the next diagonal replica (the column
+// values c are shuffled before inv is known); L = a * rsqrt(d) and W = D^-1/2 U^-1 off the chain.
+__device__ __forceinline__ double rcp_pos(double d) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+#pragma unroll
+  for (int it = 0; it < 2; ++it) { const double e = fma(-d, y, 1.0); y = fma(y, e, y); }
+  return y;
+}
+__device__ __forceinline__ void df_rcp(const double* S, double* M, int ld, int n0, int kn, int nrow, double* Wout,
+                                       double* Wsm, int* info, double* cb, int t128) {
+  const int w = t128 >> 5, lane = t128 & 31;
+  double a[8], dgw[8], wr[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int c = 8 * w + q;
+    a[q] = (lane < nrow && c < kn) ? S[lane * TLD + c] : (lane == c ? 1.0 : 0.0);
+    dgw[q] = (c < kn) ? S[c * TLD + c] : 1.0;
+    wr[q] = (lane == c) ? 1.0 : 0.0;
+  }
+  bool bad = false;
+#pragma unroll 1
+  for (int blk = 0; blk < 4; ++blk) {
+    double* Lb = cb + (blk & 1) * (CHT * 9 + 8 * 33);
+    double* Wb = Lb + CHT * 9;
+    if (w == blk) {
+      const double* Lp = cb + ((blk + 1) & 1) * (CHT * 9 + 8 * 33);
+      const double* Wp = Lp + CHT * 9;
+      double lrp[8], wbp[8];
+      if (blk > 0) {
+#pragma unroll
+        for (int pp = 0; pp < 8; ++pp) {
+          lrp[pp] = Lp[lane * 9 + pp];
+          wbp[pp] = Wp[pp * 33 + lane];
+        }
+#pragma unroll
+        for (int p = 0; p < 8; ++p)
+#pragma unroll
+          for (int pp = 0; pp < 8; ++pp) {
+            const double l = Lp[(8 * w + p) * 9 + pp];
+            dgw[p] = fma(-l, l, dgw[p]);
+            a[p] = fma(-lrp[pp], l, a[p]);
+            wr[p] = fma(-l, wbp[pp], wr[p]);
+          }
+      }
+#pragma unroll
+      for (int p = 0; p < 8; ++p) {
+        const int j = 8 * blk + p;
+        double cq[8];  // unnormalised column j at rows 8blk+q (final after pivot j-1): off the chain
+#pragma unroll
+        for (int q = p + 1; q < 8; ++q) cq[q] = __shfl_sync(0xffffffffu, a[p], 8 * blk + q);
+        double d = dgw[p];
+        bad |= (j < kn) && !(d > 0.0);
+        d = (j < kn && d > 0.0) ? d : 1.0;
+        const double inv = rcp_pos(d);   // the chain
+        const double rs = rsqrt_pos(d);  // off the chain (L and W scaling)
+        const double t = a[p] * inv;     // a_ij / d_j
+#pragma unroll
+        for (int q = p + 1; q < 8; ++q) {
+          const double u = cq[q] * inv;  // u_qj = a_qj / d_j
+          dgw[q] = fma(-cq[q], u, dgw[q]);
+          a[q] = fma(-t, cq[q], a[q]);
+          wr[q] = fma(-u, wr[p], wr[q]);  // rows of U^-1
+        }
+        a[p] = (lane > j) ? a[p] * rs : (lane == j ? d * rs : 0.0);
+        wr[p] = wr[p] * rs;  // W row j = rsqrt(d_j) * (U^-1 row j)
+      }
+#pragma unroll
+      for (int p = 0; p < 8; ++p) {
+        Lb[lane * 9 + p] = a[p];
+        Wb[p * 33 + lane] = wr[p];
+      }
+    }
+    asm volatile("bar.sync 2, 128;" ::: "memory");
+    if (w > blk + 1) {
+      double lr[8], wb[8];
+#pragma unroll
+      for (int p = 0; p < 8; ++p) {
+        lr[p] = Lb[lane * 9 + p];
+        wb[p] = Wb[p * 33 + lane];
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const double* lc = Lb + (8 * w + q) * 9;
+#pragma unroll
+        for (int p = 0; p < 8; ++p) {
+          const double l = lc[p];
+          dgw[q] = fma(-l, l, dgw[q]);
+          a[q] = fma(-lr[p], l, a[q]);
+          wr[q] = fma(-l, wb[p], wr[q]);
+        }
+      }
+    }
+  }
+  if (bad && lane == 0) atomicExch(info, 1);
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int c = 8 * w + q;
+    if (lane < nrow && c < kn && c <= lane) M[(int64_t)(n0 + lane) + (int64_t)(n0 + c) * ld] = a[q];
+    const double wv = (c < kn && lane < kn) ? wr[q] : (lane == c ? 1.0 : 0.0);
+    if (Wout) Wout[c * CHT + lane] = wv;
+  }
+}
+__global__ void k_rcp(const double* Sg, double* M, double* W, int* info, unsigned long long* cyc) {
+  __shared__ double S[CHT * TLD + kDiagScratch];
+  for (int e = threadIdx.x; e < CHT * TLD; e += 128) S[e] = Sg[e];
+  __syncthreads();
+  long long c0 = clock64();
+  df_rcp(S, M, 32, 0, 32, 32, W, nullptr, info, S + CHT * TLD, threadIdx.x);
+  long long c1 = clock64();
+  if (threadIdx.x == 0) cyc[0] = c1 - c0;
+}
+__global__ void k_cur(const double* Sg, double* M, double* W, int* info, unsigned long long* cyc) {
+  __shared__ double S[CHT * TLD + kDiagScratch];
+  for (int e = threadIdx.x; e < CHT * TLD; e += 128) S[e] = Sg[e];
+  __syncthreads();
+  long long c0 = clock64();
+  diag_factor4(S, M, 32, 0, 32, 32, W, nullptr, info, S + CHT * TLD, threadIdx.x);
+  long long c1 = clock64();
+  if (threadIdx.x == 0) cyc[0] = c1 - c0;
+}
+template <class K> void run_lw(const char* name, K kern, const double* h, double* dS, double* dM, double* dW, int* info,
+                               unsigned long long* cyc) {
+  for (int rep = 0; rep < 5; ++rep) kern<<<1, 128>>>(dS, dM, dW, info, cyc);
+  cudaDeviceSynchronize();
+  unsigned long long c; cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
+  double L[32 * 32], W[32 * 32];
+  cudaMemcpy(L, dM, sizeof(L), cudaMemcpyDeviceToHost); cudaMemcpy(W, dW, sizeof(W), cudaMemcpyDeviceToHost);
+  double e1 = 0, e2 = 0;
+  for (int i = 0; i < 32; ++i) for (int j = 0; j <= i; ++j) {
+    double s2 = 0; for (int p = 0; p <= j; ++p) s2 += L[i + p * 32] * L[j + p * 32];
+    e1 = fmax(e1, fabs(s2 - h[i * TLD + j]));
+    double t = 0; for (int p = j; p <= i; ++p) t += W[i * 32 + p] * L[p + j * 32];
+    e2 = fmax(e2, fabs(t - (i == j)));
+  }
+  printf("%-24s %6llu cycles (%.0f per pivot) |LL'-A| %.2e |WL-I| %.2e %s\n", name, c, c / 32.0, e1, e2,
+         cudaGetErrorString(cudaGetLastError()));
+}
 template <bool WANTW, int NEWTON> void run(const char* name, double* dS, double* dM, double* dW, int* info, unsigned long long* cyc) {
   for (int rep = 0; rep < 5; ++rep) k_var<WANTW, NEWTON><<<1, 128>>>(dS, dM, dW, info, cyc);
   cudaDeviceSynchronize();
@@ -412,6 +551,11 @@ int main() {
   double *dS, *dM, *dW; int* info; unsigned long long* cyc;
   cudaMalloc(&dS, sizeof(h)); cudaMalloc(&dM, 32 * 32 * 8); cudaMalloc(&dW, 32 * 32 * 8); cudaMalloc(&info, 4); cudaMalloc(&cyc, 64);
   cudaMemcpy(dS, h, sizeof(h), cudaMemcpyHostToDevice);
+  cudaMemset(dM, 0, 32 * 32 * 8);
+  for (int k = 0; k < 3; ++k) {
+    run_lw("diag_factor4 (current)", k_cur, h, dS, dM, dW, info, cyc);
+    run_lw("reciprocal chain", k_rcp, h, dS, dM, dW, info, cyc);
+  }
   run<true, 2>("W, 2 Newton", dS, dM, dW, info, cyc);
   run<false, 2>("no W, 2 Newton", dS, dM, dW, info, cyc);
   run<true, 1>("W, 1 Newton", dS, dM, dW, info, cyc);
