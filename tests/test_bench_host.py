@@ -134,3 +134,21 @@ def test_cpu_leg_parity_block(tmp_path):
             assert not par["ok"] and p0["xinf_rel"] > 1e-3
         else:
             assert par["ok"] and p0["obj_rel"] == 0.0 and p0["xinf_rel"] == 0.0 and p0["J_equal"]
+
+
+def test_read_ceiling_context():
+    """The roofline line's read-ceiling context is the best GB/s of the committed read probe."""
+    import json
+    import sys
+
+    sys.path.insert(0, ROOT)
+    import bench
+
+    p = os.path.join(ROOT, "profiles", "r2_read_ceiling_probe.jsonl")
+    best = 0.0
+    for line in open(p):
+        try:
+            best = max(best, float(json.loads(line).get("GBps", 0.0)))
+        except ValueError:
+            pass
+    assert bench._read_ceiling() == best and best > 7000.0
