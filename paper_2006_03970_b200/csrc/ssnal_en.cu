@@ -495,8 +495,12 @@ int configure(ssnal_en_problem* P) {
   }
   P->xstage_elems = (uint32_t)((P->C + 15) / 16 * 16);
   const size_t per_stage = (size_t)(P->stage_elems + P->xstage_elems) * 8;
-  int S = (int)((200 * 1024) / per_stage);
-  if (S > (P->fmt ? 2 * K1_NWC : 8)) S = P->fmt ? 2 * K1_NWC : 8;
+  // ring depth: as many stages as fit ~224 KB, at most 6 (measured at n = 1e7 / 1e6, r ≈ 1e-4 n:
+  // m = 500 (32 KB stages) 5 / 6 / 7 stages 7.15 / 7.13 / 6.74 TB/s; m = 800 (51 KB stages) 3 / 4
+  // stages 6.78 / 7.12 TB/s — profiles/r2_k1_stages_sweep.jsonl, r2_k1_stages_m800.jsonl)
+  // (packed genotypes keep a 200 KB ring of ≤ 14 stages: 13 → 14 stages was 1% slower at cfg4)
+  int S = (int)(((P->fmt ? 200 : 224) * 1024) / per_stage);
+  if (S > (P->fmt ? 2 * K1_NWC : 6)) S = P->fmt ? 2 * K1_NWC : 6;
   if (S < 2) S = 2;
   while ((size_t)S * P->stage_elems < (size_t)K1_NWC * m + K1_NWC * 4 + K1_NWC) ++S;
   P->S = S;

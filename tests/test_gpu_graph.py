@@ -143,28 +143,29 @@ def test_graph_rebuild_after_cluster_change():
 def test_gram_kernel_options_agree(mode):
     """Option gram_sk selects the K3 kernel (0: k_gram_fused for both branches, 1: fused for SMW and
     k_gram_sk for m × m — the default —, 2: k_gram_sk for both); graph ≡ host bitwise in every mode and
-    every mode meets the oracle (cfg3 recipe at n = 2e4: SMW and m × m steps)."""
+    every mode meets the oracle (cfg3 recipe at n = 2e4: SMW steps at c = 0.3, m × m at c = 0.05)."""
     cfg = synth.scaled(synth.CONFIGS["cfg3"], n=20_000)
     A = synth.design(cfg)
     b, _ = synth.response(cfg)
     lm = float(np.max(np.abs(oracle.aty(A, b)))) / cfg.alpha
-    l1, l2 = 0.05 * cfg.alpha * lm, 0.05 * (1 - cfg.alpha) * lm
-    out = {}
-    for graph in (1, 0):
-        with Problem(A, b) as P:
-            P.set_option("gram_sk", mode)
-            P.set_option("graph", graph)
-            out[graph] = P.solve(l1, l2, cfg.sigma0, cfg.tol)
-    assert np.array_equal(out[0][0], out[1][0])
-    for k in ("outer_iters", "newton_iters", "branch_steps", "res_kkt1", "res_kkt3", "primal_obj", "dual_obj"):
-        assert out[0][1][k] == out[1][1][k], k
-    assert out[1][1]["branch_steps"][1] > 0 and out[1][1]["branch_steps"][2] > 0
-    compare_to_oracle(A, b, l1, l2, lambda s0, tol, x0: out[1] if (s0, tol, x0) == (cfg.sigma0, cfg.tol, None)
-                      else _solve_mode(A, b, l1, l2, s0, tol, x0, mode), sigma0=cfg.sigma0, tol=cfg.tol,
-                      label=("gram_sk", mode))
+    seen = np.zeros(4, dtype=int)
+    for c in (0.3, 0.05):
+        l1, l2 = c * cfg.alpha * lm, c * (1 - cfg.alpha) * lm
+        out = {}
+        for graph in (1, 0):
+            with Problem(A, b) as P:
+                P.set_option("gram_sk", mode)
+                P.set_option("graph", graph)
+                out[graph] = P.solve(l1, l2, cfg.sigma0, cfg.tol)
+        assert np.array_equal(out[0][0], out[1][0])
+        for k in ("outer_iters", "newton_iters", "branch_steps", "res_kkt1", "res_kkt3", "primal_obj", "dual_obj"):
+            assert out[0][1][k] == out[1][1][k], k
+        seen += np.array(out[1][1]["branch_steps"])
 
+        def gpu(s0, tol, x0, mode=mode, l1=l1, l2=l2):
+            with Problem(A, b) as P:
+                P.set_option("gram_sk", mode)
+                return P.solve(l1, l2, s0, tol, x0=x0)
 
-def _solve_mode(A, b, l1, l2, s0, tol, x0, mode):
-    with Problem(A, b) as P:
-        P.set_option("gram_sk", mode)
-        return P.solve(l1, l2, s0, tol, x0=x0)
+        compare_to_oracle(A, b, l1, l2, gpu, sigma0=cfg.sigma0, tol=cfg.tol, label=("gram_sk", mode, c))
+    assert seen[1] > 0 and seen[2] > 0
