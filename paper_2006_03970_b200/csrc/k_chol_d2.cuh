@@ -5,10 +5,13 @@
 // Ownership.  k_chol_dsm gives CTA j all of block column j, so owner j absorbs j·(T − j) tile
 // updates on one SM and the middle owners fall behind the panel chain.  Here the tiles are split
 // by role:
-//   chain tiles (j, j) and (j + 1, j)  → CTA j mod 4  (the critical path: factor, W_j = L_jj⁻¹,
+//   chain tiles (j, j) and (j + 1, j)  → CTA j mod NC  (the critical path: factor, W_j = L_jj⁻¹,
 //                                         L_{j+1,j}; W_j never leaves the CTA for that TRSM);
-//   trailing tiles (i, j), i ≥ j + 2   → CTA 4 + ((i − j − 2) + 3j) mod 12, so the trailing tiles
-//                                         of one column land on distinct CTAs.
+//   trailing tiles (i, j), i ≥ j + 2   → CTA NC + ((i − j − 2) + 3j) mod (16 − NC), so the
+//                                         trailing tiles of one column land on distinct CTAs.
+// NC = kD2Chain = 5 chain CTAs: each chain CTA absorbs every earlier panel into its chain tiles
+// between its own columns, so more chain CTAs give each more time for that look-ahead (4 → 5:
+// 5% faster at N = 435–512; 6 leaves too few trailing CTAs at large N and needs 13 tile slots).
 // Every CTA keeps its tiles in shared memory for the whole launch (≤ 12 × 8.4 KB).
 //
 // Schedule (per 128-thread quad; the tiles of a CTA alternate between its two quads, so a chain
@@ -38,10 +41,12 @@
 
 namespace ssn {
 
-constexpr int kD2Slots = 12;  // max tiles per CTA over N ≤ 512 (checked by tools/probes/d2_probe)
+constexpr int kD2Slots = 12;  // max tiles per CTA over N ≤ 512 for 4 or 5 chain CTAs (13 for 6; tools/probes/d2_probe)
+constexpr int kD2Chain = 5;   // chain CTAs (tools/probes/d2_probe: 4 / 5 / 6 chain CTAs, N = 435: 148.7 / 140.6 /
+                              // 142.7 µs, N = 500: 182.7 / 173.6 / 178.1 µs)
 constexpr int kD2Bytes = kTileD * 8;  // one tile (8448 B, a multiple of 16)
 constexpr size_t kD2SmemDoubles = (size_t)kD2Slots * kTileD  // owned tiles
-                                  + 4 * kTileD                 // W_j of my diagonal tiles (j ≡ CTA mod 4)
+                                  + 4 * kTileD                 // W_j of my diagonal tiles (j ≡ CTA mod NC, ≤ 4)
                                   + 4 * kTileD                 // B operands (2 per quad); P_j in the backward
                                   + kTileD                     // inbox: L_{j,j−1} pushed by the previous chain CTA
                                   + kDiagScratch               // diag_factor4 scratch; partial staging later
@@ -59,15 +64,22 @@ __device__ unsigned long long g_d2[18][8];
 #define D2STAMP(k, e) do {} while (0)
 #endif
 
-SSN_DEV int d2_owner(int i, int j) { return i - j <= 1 ? (j & 3) : 4 + (i - j - 2 + 3 * j) % 12; }
-SSN_DEV int d2_cnt12(int len, int res) { return len > res ? (len - res + 11) / 12 : 0; }  // #{x < len : x ≡ res (12)}
+// NC chain CTAs (the chain tiles of column j on CTA j mod NC; lc = the column's index on its chain
+// CTA) and NT = 16 − NC trailing CTAs (tile (i, j), i ≥ j + 2, on NC + ((i − j − 2) + 3j) mod NT).
+template <int NC> SSN_DEV int d2_owner(int i, int j) {
+  return i - j <= 1 ? j % NC : NC + (i - j - 2 + 3 * j) % (kDsmCS - NC);
+}
+template <int NC> SSN_DEV int d2_lc(int j) { return j / NC; }
+template <int NC> SSN_DEV int d2_col(int c, int q) { return c + NC * q; }
+SSN_DEV int d2_cntm(int len, int res, int mod) { return len > res ? (len - res + mod - 1) / mod : 0; }  // #{x < len : x ≡ res (mod)}
 // position of tile (i, j) in its owner's list (column-major order of the owner's tiles)
-SSN_DEV int d2_slot(int i, int j, int ntr) {
-  if (i - j <= 1) return 2 * (j >> 2) + (i - j);
-  const int h = (i - j - 2 + 3 * j) % 12;
+template <int NC> SSN_DEV int d2_slot(int i, int j, int ntr) {
+  constexpr int NT = kDsmCS - NC;
+  if (i - j <= 1) return 2 * d2_lc<NC>(j) + (i - j);
+  const int h = (i - j - 2 + 3 * j) % NT;
   int s = 0;
-  for (int jj = 0; jj < j; ++jj) s += d2_cnt12(ntr - jj - 2, ((h - 3 * jj) % 12 + 12) % 12);
-  return s + (i - j - 2) / 12;
+  for (int jj = 0; jj < j; ++jj) s += d2_cntm(ntr - jj - 2, ((h - 3 * jj) % NT + NT) % NT, NT);
+  return s + (i - j - 2) / NT;
 }
 
 SSN_DEV uint32_t d2_mapa(const void* p, int rank) {
@@ -115,6 +127,7 @@ SSN_DEV double d2_coldot(const double* M, const double* x, int lane) {
   return (s[0] + s[1]) + (s[2] + s[3]);
 }
 
+template <int NC>
 SSN_DEV void chol_d2_body(const double* __restrict__ M, int N, int ld, double* __restrict__ out, double scale,
                           const double* __restrict__ dotv, double* dot_out, int* info,
                           const double* __restrict__ ybase, double* __restrict__ yt, const DirGeo* geo, int want,
@@ -160,29 +173,33 @@ SSN_DEV void chol_d2_body(const double* __restrict__ M, int N, int ld, double* _
   const int t128 = tid & 127;
   const int NR = N + 1;
   const int ntc = (N + CHT - 1) / CHT, ntr = (NR + CHT - 1) / CHT;
-  const bool chain = me < 4;
-  const int jtop = chain && me < ntc ? me + 4 * ((ntc - 1 - me) >> 2) : -1;  // my highest chain column
+  constexpr int NT = kDsmCS - NC;
+  const bool chain = me < NC;
+  int nchain = 0;  // my chain columns d2_col<NC>(me, 0 … nchain − 1), ascending (≤ 4 for NC ≥ 4)
+  if (chain)
+    while (nchain < 4 && d2_col<NC>(me, nchain) < ntc) ++nchain;
+  const int jtop = nchain ? d2_col<NC>(me, nchain - 1) : -1;  // my highest chain column
   if (tid < 3 * kD2Slots + 8) rdy[tid] = 0;  // rdy, done, list, pready, bcast
   if (tid == 0) {
     dred[0] = 0.0;
     mbar_init(ibar, 1);
     for (int i = 0; i < kDsmCS; ++i) mbar_init(vbar + i, 1);
-    for (int q = 0; q < 4; ++q) mbar_init(pbar + q, max(1, chain ? ntc - (me + 4 * q) - 3 : 1));
+    for (int q = 0; q < 4; ++q) mbar_init(pbar + q, max(1, chain ? ntc - d2_col<NC>(me, q) - 3 : 1));
     fence_mbar_init();
   }
   for (int t = tid; t < 17 * 16; t += blockDim.x) {
     const int i = t >> 4, j = t & 15;
     if (j < ntc && i >= j && i < ntr) {
-      const int s = d2_slot(i, j, ntr);
+      const int s = d2_slot<NC>(i, j, ntr);
       tslot[t] = (unsigned char)s;
-      if (d2_owner(i, j) == me) list[s] = (i << 8) | j;
+      if (d2_owner<NC>(i, j) == me) list[s] = (i << 8) | j;
     }
   }
   int nmine = 0;
   if (chain) {
-    for (int j = me; j < ntc; j += 4) nmine += (j + 1 < ntr) ? 2 : 1;
+    for (int q = 0; q < nchain; ++q) nmine += (d2_col<NC>(me, q) + 1 < ntr) ? 2 : 1;
   } else {
-    for (int j = 0; j < ntc; ++j) nmine += d2_cnt12(ntr - j - 2, ((me - 4 - 3 * j) % 12 + 12) % 12);
+    for (int j = 0; j < ntc; ++j) nmine += d2_cntm(ntr - j - 2, ((me - NC - 3 * j) % NT + NT) % NT, NT);
   }
   __syncthreads();
   for (int s = warp; s < nmine; s += 8) {
@@ -201,9 +218,9 @@ SSN_DEV void chol_d2_body(const double* __restrict__ M, int N, int ld, double* _
 
   auto qbar = [&]() { asm volatile("bar.sync %0, 128;" ::"r"(2 + quad) : "memory"); };
   auto rtile = [&](int i, int j) {
-    return cluster.map_shared_rank(T, d2_owner(i, j)) + tslot[i * 16 + j] * kTileD;
+    return cluster.map_shared_rank(T, d2_owner<NC>(i, j)) + tslot[i * 16 + j] * kTileD;
   };
-  auto rflag = [&](int i, int j) { return cluster.map_shared_rank(rdy, d2_owner(i, j)) + tslot[i * 16 + j]; };
+  auto rflag = [&](int i, int j) { return cluster.map_shared_rank(rdy, d2_owner<NC>(i, j)) + tslot[i * 16 + j]; };
   const int g = lane >> 2, t = lane & 3, qw = warp & 3;
   auto strip_af = [&](double* S, const double (&af)[8], const double* SB, double sgn, bool acc0) {
     double part[4][4][2];
@@ -249,7 +266,7 @@ SSN_DEV void chol_d2_body(const double* __restrict__ M, int N, int ld, double* _
       const bool inb = chain && k == j - 1;          // B (and A when i == j) from the inbox
       const int* fa = i == j ? nullptr : rflag(i, k);  // A = L_{i,k} (i > j: never the inbox)
       const int* fb = inb ? nullptr : rflag(j, k);
-      const uint32_t ipar = (uint32_t)((j >> 2) - (me == 0)) & 1u;  // receptions before this one (CTA 0: none for column 0)
+      const uint32_t ipar = (uint32_t)(d2_lc<NC>(j) - (me == 0)) & 1u;  // receptions before this one (CTA 0: none for column 0)
       if (blocking) {
         if (t128 == 0) {
           if (inb) d2_mbar_wait(ibar, ipar);
@@ -294,7 +311,7 @@ SSN_DEV void chol_d2_body(const double* __restrict__ M, int N, int ld, double* _
     if (i == j) {
       qbar();  // every warp's rows of S are final
       const int c0 = CHT * j;
-      diag_factor4(S, nullptr, 0, c0, min(CHT, N - c0), min(CHT, NR - c0), nullptr, Wb + (j >> 2) * kTileD, info,
+      diag_factor4(S, nullptr, 0, c0, min(CHT, N - c0), min(CHT, NR - c0), nullptr, Wb + d2_lc<NC>(j) * kTileD, info,
                    dscr, t128);
       if (t128 == 0) D2STAMP(j, 3);
       qbar();
@@ -302,19 +319,19 @@ SSN_DEV void chol_d2_body(const double* __restrict__ M, int N, int ld, double* _
       if (t128 == 0) D2STAMP(j, 1);
     } else if (chain) {  // (j + 1, j): W_j is local; push the result to the next chain CTA first
       if (t128 == 0)
-        while (ld_acquire_cluster(rdy + 2 * (j >> 2)) == 0) {
+        while (ld_acquire_cluster(rdy + 2 * d2_lc<NC>(j)) == 0) {
         }
       qbar();
       if (t128 == 0) D2STAMP(j, 4);
       double af[8];
       load_af(S, af);  // this warp's own rows
-      strip_af(S, af, Wb + (j >> 2) * kTileD, 1.0, false);
+      strip_af(S, af, Wb + d2_lc<NC>(j) * kTileD, 1.0, false);
       fence_proxy_async();
       qbar();
       if (t128 == 0) D2STAMP(j, 6);
       if (t128 == 0) {
         if (i < ntc) {  // column i exists: its chain CTA absorbs L_{i,j} from its inbox
-          const int c = i & 3;
+          const int c = i % NC;
           const uint32_t rb = d2_mapa(ibar, c);
           d2_remote_expect(rb, kD2Bytes);
           d2_push(d2_mapa(inbox, c), S, kD2Bytes, rb);
@@ -325,13 +342,13 @@ SSN_DEV void chol_d2_body(const double* __restrict__ M, int N, int ld, double* _
         D2STAMP(j, 2);
       }
     } else {
-      const int od = j & 3;
+      const int od = j % NC;
       if (t128 == 0)
-        while (ld_acquire_cluster(cluster.map_shared_rank(rdy, od) + 2 * (j >> 2)) == 0) {
+        while (ld_acquire_cluster(cluster.map_shared_rank(rdy, od) + 2 * d2_lc<NC>(j)) == 0) {
         }
       qbar();
       double* B = Bq + (2 * quad + (nab++ & 1)) * kTileD;
-      copy_tile(cluster.map_shared_rank(Wb, od) + (j >> 2) * kTileD, B);
+      copy_tile(cluster.map_shared_rank(Wb, od) + d2_lc<NC>(j) * kTileD, B);
       qbar();
       double af[8];
       load_af(S, af);
@@ -366,10 +383,10 @@ SSN_DEV void chol_d2_body(const double* __restrict__ M, int N, int ld, double* _
   // ---- backward substitution v = L⁻ᵀ z ----
   const int rt = N / CHT, rrow = N % CHT;
   if (chain && warp >= 2 && warp < 6) {  // P_j = L_{j+1,j} W_j for my q-th column (q = warp − 2)
-    const int q = warp - 2, j = jtop - 4 * q;
+    const int q = warp - 2, j = q < nchain ? d2_col<NC>(me, nchain - 1 - q) : -1;
     if (jtop >= 0 && j >= 0 && j + 1 < ntc) {
-      const double* L1 = T + (2 * (j >> 2) + 1) * kTileD;
-      const double* W = Wb + (j >> 2) * kTileD;
+      const double* L1 = T + (2 * d2_lc<NC>(j) + 1) * kTileD;
+      const double* W = Wb + d2_lc<NC>(j) * kTileD;
       double* P = Bq + q * kTileD;
 #pragma unroll 1
       for (int r = 0; r < CHT; ++r) P[r * TLD + lane] = d2_coldot(W, L1 + r * TLD, lane);  // Σ_s L1[r][s] W[s][c]
@@ -382,15 +399,16 @@ SSN_DEV void chol_d2_body(const double* __restrict__ M, int N, int ld, double* _
     double dp = 0.0;
     double* xb = dred + 32;
 #pragma unroll 1
-    for (int q = 0, j = jtop; j >= 0; ++q, j -= 4) {
+    for (int q = 0; q < nchain; ++q) {  // my columns, descending
+      const int j = d2_col<NC>(me, nchain - 1 - q);
       const int* fz = rflag(rt, j);
       while (ld_acquire_cluster(fz) == 0) {
       }
       double acc = rtile(rt, j)[rrow * TLD + lane];  // z_j[c], c = lane
       const int np = ntc - j - 3;
       if (np > 0) {
-        d2_mbar_wait(pbar + (j >> 2), 0);
-        for (int i = ntc - 1; i >= j + 3; --i) acc -= pacc[((j >> 2) * kDsmCS + i) * 32 + lane];
+        d2_mbar_wait(pbar + d2_lc<NC>(j), 0);
+        for (int i = ntc - 1; i >= j + 3; --i) acc -= pacc[(d2_lc<NC>(j) * kDsmCS + i) * 32 + lane];
       }
       if (j + 2 < ntc) {
         const int* f2 = rflag(j + 2, j);
@@ -409,7 +427,7 @@ SSN_DEV void chol_d2_body(const double* __restrict__ M, int N, int ld, double* _
       }
       xb[lane] = acc;
       __syncwarp();
-      double v = d2_coldot(Wb + (j >> 2) * kTileD, xb, lane);  // u_j = W_jᵀ acc
+      double v = d2_coldot(Wb + d2_lc<NC>(j) * kTileD, xb, lane);  // u_j = W_jᵀ acc
       if (j + 1 < ntc) {
         while (*(volatile int*)(pready + q) == 0) {
         }
@@ -425,7 +443,7 @@ SSN_DEV void chol_d2_body(const double* __restrict__ M, int N, int ld, double* _
       if (lane == 0) {
         D2STAMP(j, 5);
         for (int p = 1; p < kDsmCS; ++p) {  // the chain CTAs of j − 1, j − 2, j − 3 first, then the rest
-          const int c = p < 4 ? (me + 4 - p) & 3 : p;
+          const int c = p < NC ? (me + NC - p) % NC : p;
           const uint32_t rb = d2_mapa(vbar + j, c);
           d2_remote_expect(rb, 256);
           d2_push(d2_mapa(vin + j * 32, c), vin + j * 32, 256, rb);
@@ -462,7 +480,7 @@ SSN_DEV void chol_d2_body(const double* __restrict__ M, int N, int ld, double* _
         fence_proxy_async();
         __syncwarp();
         if (lane == 0) {
-          const int c = j & 3, q = j >> 2;
+          const int c = j % NC, q = d2_lc<NC>(j);
           const uint32_t rb = d2_mapa(pbar + q, c);
           d2_remote_expect(rb, 256);
           d2_push(d2_mapa(pacc + (q * kDsmCS + i) * 32, c), stage + s * 32, 256, rb);
@@ -479,24 +497,27 @@ SSN_DEV void chol_d2_body(const double* __restrict__ M, int N, int ld, double* _
   if (me == 0 && tid == 0) D2STAMP(17, 2);
   if (me == 0 && tid == 0 && dot_out) {
     double sd = 0.0;
-    for (int q = 0; q < 4; ++q) sd += cluster.map_shared_rank(dred, q)[0];
+    for (int q = 0; q < NC; ++q) sd += cluster.map_shared_rank(dred, q)[0];
     *dot_out = sd;
   }
   cluster.sync();  // rank 0's reads complete before any CTA exits
 }
 
-__global__ void __launch_bounds__(256, 1) k_chol_d2(const double* __restrict__ M, int N, int ld,
-                                                    double* __restrict__ out, double scale,
-                                                    const double* __restrict__ dotv, double* dot_out, int* info,
-                                                    const double* __restrict__ ybase, double* __restrict__ yt,
-                                                    const DirGeo* geo, int want, int nmin, int nmax,
-                                                    const CholArgs* ca) {
-  chol_d2_body(M, N, ld, out, scale, dotv, dot_out, info, ybase, yt, geo, want, nmin, nmax, ca);
+template <int NC>
+__global__ void __launch_bounds__(256, 1) k_chol_d2t(const double* __restrict__ M, int N, int ld,
+                                                     double* __restrict__ out, double scale,
+                                                     const double* __restrict__ dotv, double* dot_out, int* info,
+                                                     const double* __restrict__ ybase, double* __restrict__ yt,
+                                                     const DirGeo* geo, int want, int nmin, int nmax,
+                                                     const CholArgs* ca) {
+  chol_d2_body<NC>(M, N, ld, out, scale, dotv, dot_out, info, ybase, yt, geo, want, nmin, nmax, ca);
 }
+constexpr auto k_chol_d2 = k_chol_d2t<kD2Chain>;
 
 // Graph mode: one node for both DSMEM-resident kernels, dispatching on the device geometry's N
 // (k_chol_dsm for N ≤ 96, k_chol_d2 for 96 < N ≤ 512); dynamic shared memory kD2Smem.
-__global__ void __launch_bounds__(256, 1) k_chol_dsm_any(const double* __restrict__ M, double* __restrict__ out,
+template <int NC>
+__global__ void __launch_bounds__(256, 1) k_chol_dsm_anyt(const double* __restrict__ M, double* __restrict__ out,
                                                          double scale, const double* __restrict__ dotv,
                                                          double* dot_out, int* info, const double* __restrict__ ybase,
                                                          double* __restrict__ yt, const DirGeo* geo, int want,
@@ -504,7 +525,8 @@ __global__ void __launch_bounds__(256, 1) k_chol_dsm_any(const double* __restric
   if (geo->N <= kDsmUseMax)
     chol_dsm_body(M, 0, 0, out, scale, dotv, dot_out, info, ybase, yt, geo, want, kDsmUseMax, ca);
   else
-    chol_d2_body(M, 0, 0, out, scale, dotv, dot_out, info, ybase, yt, geo, want, kDsmUseMax + 1, kDsmMaxN, ca);
+    chol_d2_body<NC>(M, 0, 0, out, scale, dotv, dot_out, info, ybase, yt, geo, want, kDsmUseMax + 1, kDsmMaxN, ca);
 }
+constexpr auto k_chol_dsm_any = k_chol_dsm_anyt<kD2Chain>;
 
 }  // namespace ssn

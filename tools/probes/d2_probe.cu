@@ -38,8 +38,10 @@ static void host_solve(const std::vector<double>& Mh, int N, int ld, std::vector
 }
 
 int main(int argc, char** argv) {
-  cudaFuncSetAttribute(k_chol_d2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kD2Smem);
-  cudaFuncSetAttribute(k_chol_d2, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  for (auto kf : {k_chol_d2t<4>, k_chol_d2t<5>}) {  // (6 chain CTAs needs kD2Slots = 13)  // kD2Slots must cover 6 (13 slots) for this probe
+    cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kD2Smem);
+    cudaFuncSetAttribute(kf, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  }
   cudaFuncSetAttribute(k_chol_dsm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDsmSmem);
   cudaFuncSetAttribute(k_chol_dsm, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   std::vector<int> Ns = {161, 192, 200, 255, 256, 257, 300, 391, 435, 480, 500, 511, 512};
@@ -77,45 +79,45 @@ int main(int argc, char** argv) {
     cfg.attrs = at; cfg.numAttrs = 1;
     const DirGeo* nog = nullptr;
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-    float ms2 = 0, ms1 = 0;
-    for (int pass = 0; pass < 2; ++pass) {
-      cfg.dynamicSmemBytes = kD2Smem;
-      for (int it = 0; it < 3; ++it)
-        cudaLaunchKernelEx(&cfg, k_chol_d2, (const double*)dM, N, ld, dout, 1.0, (const double*)dout2, dot, info,
-                           (const double*)nullptr, (double*)nullptr, nog, 0, 0, kDsmMaxN, (const CholArgs*)nullptr);
-      cudaEventRecord(e0);
-      for (int it = 0; it < 20; ++it)
-        cudaLaunchKernelEx(&cfg, k_chol_d2, (const double*)dM, N, ld, dout, 1.0, (const double*)dout2, dot, info,
-                           (const double*)nullptr, (double*)nullptr, nog, 0, 0, kDsmMaxN, (const CholArgs*)nullptr);
-      cudaEventRecord(e1); cudaEventSynchronize(e1);
-      cudaEventElapsedTime(&ms2, e0, e1);
-      cfg.dynamicSmemBytes = kDsmSmem;
-      cudaEventRecord(e0);
-      for (int it = 0; it < 20; ++it)
-        cudaLaunchKernelEx(&cfg, k_chol_dsm, (const double*)dM, N, ld, dout2, 1.0, (const double*)nullptr,
-                           (double*)nullptr, info, (const double*)nullptr, (double*)nullptr, nog, 0, kDsmMaxN,
-                           (const CholArgs*)nullptr);
-      cudaEventRecord(e1); cudaEventSynchronize(e1);
-      cudaEventElapsedTime(&ms1, e0, e1);
-    }
-    cudaError_t err = cudaDeviceSynchronize();
-    std::vector<double> x2(N), x1(N);
-    cudaMemcpy(x2.data(), dout, N * 8, cudaMemcpyDeviceToHost);
-    cudaMemcpy(x1.data(), dout2, N * 8, cudaMemcpyDeviceToHost);
-    double dotv = 0; cudaMemcpy(&dotv, dot, 8, cudaMemcpyDeviceToHost);
-    int hinfo = 0; cudaMemcpy(&hinfo, info, 4, cudaMemcpyDeviceToHost);
-    double e2 = 0, e1r = 0, xm = 0, dref = 0;
-    for (int i = 0; i < N; ++i) {
-      xm = fmax(xm, fabs(xr[i]));
-      e2 = fmax(e2, fabs(x2[i] - xr[i]));
-      e1r = fmax(e1r, fabs(x1[i] - xr[i]));
-      dref += x1[i] * x2[i];  // dotv = out of the dsm run (same as d2's out up to rounding)
-    }
-    const bool ok = err == cudaSuccess && hinfo == 0 && e2 <= 1e-11 * xm && fabs(dotv - dref) <= 1e-9 * fabs(dref);
+    float msv[2] = {0, 0};
+    double ev[2] = {0, 0};
+    int iv[2] = {0, 0};
+    cudaError_t err = cudaSuccess;
+    double xm = 0;
+    for (int pass = 0; pass < 2; ++pass)
+      for (int v = 0; v < 2; ++v) {  // chain CTAs: 4 (round-2 design), 5 (the library's kD2Chain)
+        auto kf = v == 0 ? k_chol_d2t<4> : k_chol_d2t<5>;
+        cfg.dynamicSmemBytes = kD2Smem;
+        cudaMemset(info, 0, 4);
+        for (int it = 0; it < 3; ++it)
+          cudaLaunchKernelEx(&cfg, kf, (const double*)dM, N, ld, dout, 1.0, (const double*)nullptr, (double*)nullptr,
+                             info, (const double*)nullptr, (double*)nullptr, nog, 0, 0, kDsmMaxN,
+                             (const CholArgs*)nullptr);
+        cudaEventRecord(e0);
+        for (int it = 0; it < 20; ++it)
+          cudaLaunchKernelEx(&cfg, kf, (const double*)dM, N, ld, dout, 1.0, (const double*)nullptr, (double*)nullptr,
+                             info, (const double*)nullptr, (double*)nullptr, nog, 0, 0, kDsmMaxN,
+                             (const CholArgs*)nullptr);
+        cudaEventRecord(e1); cudaEventSynchronize(e1);
+        cudaEventElapsedTime(&msv[v], e0, e1);
+        err = cudaDeviceSynchronize();
+        if (err != cudaSuccess) break;
+        std::vector<double> x2(N);
+        cudaMemcpy(x2.data(), dout, N * 8, cudaMemcpyDeviceToHost);
+        cudaMemcpy(&iv[v], info, 4, cudaMemcpyDeviceToHost);
+        double e2 = 0;
+        xm = 0;
+        for (int i = 0; i < N; ++i) {
+          xm = fmax(xm, fabs(xr[i]));
+          e2 = fmax(e2, fabs(x2[i] - xr[i]));
+        }
+        ev[v] = e2;
+      }
+    bool ok = err == cudaSuccess;
+    for (int v = 0; v < 2; ++v) ok = ok && iv[v] == 0 && ev[v] <= 1e-11 * xm;
     fails += !ok;
-    printf("N=%3d d2 %6.1f us  dsm %6.1f us  err d2 %.2e dsm %.2e (rel to %.2e) dot %.3e/%.3e info %d %s %s\n", N,
-           ms2 * 1e3 / 20, ms1 * 1e3 / 20, e2 / xm, e1r / xm, xm, dotv, dref, hinfo, cudaGetErrorString(err),
-           ok ? "OK" : "FAIL");
+    printf("N=%3d chain4 %6.1f us  chain5 %6.1f us  err %.2e %.2e %s %s\n", N, msv[0] * 1e3 / 20, msv[1] * 1e3 / 20,
+           ev[0] / xm, ev[1] / xm, cudaGetErrorString(err), ok ? "OK" : "FAIL");
     if (getenv("D2_TIMELINE")) {
       unsigned long long tl[18][12];
       cudaMemcpyFromSymbol(tl, g_d2, sizeof(tl));
