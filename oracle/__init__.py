@@ -73,8 +73,8 @@ def lib():
             "orc_dual_obj": (_d, [_dp, _i64, _dp, _dp, _i64, _d, _d]),
             "orc_kkt_violation": (_d, [_dp, _dp, _i64, _i64, _dp, _d, _d]),
             "orc_default_opts": (None, [ctypes.POINTER(Opts)]),
-            "orc_solve": (ctypes.c_int, [_dp, _dp, _i64, _i64, _d, _d, _d, _d, _dp, ctypes.POINTER(Opts), _dp, _dp,
-                                         ctypes.POINTER(Stats), ctypes.POINTER(Trace), _i64, _lp]),
+            "orc_solve": (ctypes.c_int, [_dp, _dp, _i64, _i64, _d, _d, _d, _d, _dp, _dp, ctypes.POINTER(Opts), _dp,
+                                         _dp, ctypes.POINTER(Stats), ctypes.POINTER(Trace), _i64, _lp]),
             "orc_aty_fused": (_i64, [_dp, _dp, _i64, _i64, _dp, _dp, _d, _d, _d, _dp, _lp, _dp, _dp, _dp]),
             "orc_dof": (_d, [_dp, _i64, _lp, _i64, _d]),
             "orc_ols": (ctypes.c_int, [_dp, _dp, _i64, _lp, _i64, _dp, _dp]),
@@ -248,8 +248,9 @@ def default_opts(**kw) -> Opts:
     return o
 
 
-def solve(A, b, l1, l2, sigma0=5e-3, tol=1e-6, x0=None, trace_cap=0, **opts):
-    """Algorithm 1 (SsNAL-EN).  Returns (x, y, stats dict, trace list)."""
+def solve(A, b, l1, l2, sigma0=5e-3, tol=1e-6, x0=None, trace_cap=0, y0=None, **opts):
+    """Algorithm 1 (SsNAL-EN).  y0: the dual start of a warm-started path point (reading R39; None:
+    y0 = A x0 − b for a warm start, R8).  Returns (x, y, stats dict, trace list)."""
     A, m, n, Ap = _A(A)
     b, bp = _f64(b)
     o = default_opts(**opts)
@@ -259,9 +260,12 @@ def solve(A, b, l1, l2, sigma0=5e-3, tol=1e-6, x0=None, trace_cap=0, **opts):
     x0p = None
     if x0 is not None:
         x0, x0p = _f64(x0)
+    y0p = None
+    if y0 is not None:
+        y0, y0p = _f64(y0)
     tr = (Trace * max(trace_cap, 1))()
     tl = ctypes.c_int64(0)
-    lib().orc_solve(Ap, bp, m, n, l1, l2, sigma0, tol, x0p, ctypes.byref(o), x.ctypes.data_as(_dp),
+    lib().orc_solve(Ap, bp, m, n, l1, l2, sigma0, tol, x0p, y0p, ctypes.byref(o), x.ctypes.data_as(_dp),
                     y.ctypes.data_as(_dp), ctypes.byref(st), tr if trace_cap else None, trace_cap, ctypes.byref(tl))
     stats = {f: getattr(st, f) for f, _ in Stats._fields_}
     stats["branch_steps"] = list(st.branch_steps)
@@ -269,18 +273,24 @@ def solve(A, b, l1, l2, sigma0=5e-3, tol=1e-6, x0=None, trace_cap=0, **opts):
     return x, y, stats, trace
 
 
-def solve_path_lambdas(A, b, ls, sigma0=5e-3, tol=1e-6, x0=None, carry_sigma=True, max_active=None, **opts):
+def solve_path_lambdas(A, b, ls, sigma0=5e-3, tol=1e-6, x0=None, carry_sigma=True, max_active=None,
+                       carry_dual=True, **opts):
     """Warm-started λ path over explicit (λ1, λ2) pairs: point i starts from point i−1's x
     (the warm start of P:411; y0 = A x0 − b by reading R8) and, with carry_sigma, from point i−1's
     final σ — the σ of its last inner solve (reading R38: the paper's "usually SsNAL-EN converges in
     just one iteration", needs the σ the previous point ended with; SPEC's open question S:336
-    records the same choice).  Point 0 starts at sigma0 from x0 (None = cold).  The path stops after
-    the first point with at least max_active nonzeros.  Returns a list of (x, y, stats)."""
+    records the same choice).  With carry_dual (reading R39, P:236-246 + P:409-411: "the solution at the
+    previous value" is Algorithm 1's whole starting point) point i > 0 also starts at point i − 1's
+    final y instead of y0 = A x0 − b, so no Aᵀ pass is spent on the warm start.  Point 0 starts at
+    sigma0 from x0 (None = cold).  The path stops after the first point with at least max_active
+    nonzeros.  Returns a list of (x, y, stats)."""
     out = []
     x = x0
+    y = None
     sig = sigma0
     for i, (l1, l2) in enumerate(ls):
-        x, y, st, _ = solve(A, b, l1, l2, sigma0=sig, tol=tol, x0=x, **opts)
+        x, y, st, _ = solve(A, b, l1, l2, sigma0=sig, tol=tol, x0=x, y0=y if (carry_dual and i > 0) else None,
+                            **opts)
         out.append((x, y, st))
         if carry_sigma:
             sig = st["sigma_final"]
@@ -289,13 +299,13 @@ def solve_path_lambdas(A, b, ls, sigma0=5e-3, tol=1e-6, x0=None, carry_sigma=Tru
     return out
 
 
-def solve_path(A, b, alpha, cs, sigma0=5e-3, tol=1e-6, carry_sigma=True, max_active=None, **opts):
+def solve_path(A, b, alpha, cs, sigma0=5e-3, tol=1e-6, carry_sigma=True, max_active=None, carry_dual=True, **opts):
     """The λ path of Section 3.3 on the c grid: λmax = ‖Aᵀb‖∞/α, λ1 = cαλmax, λ2 = c(1−α)λmax
     (P:506), warm-started as in solve_path_lambdas.  Returns (lambdas, [(x, y, stats)])."""
     lm = lambda_max_l1(A, b) / alpha
     ls = [(c * alpha * lm, c * (1 - alpha) * lm) for c in cs]
     res = solve_path_lambdas(A, b, ls, sigma0=sigma0, tol=tol, carry_sigma=carry_sigma, max_active=max_active,
-                             **opts)
+                             carry_dual=carry_dual, **opts)
     return ls[:len(res)], res
 
 
@@ -380,7 +390,7 @@ def oracle_ax(A, x):
     return out
 
 
-def cv_path(A, b, alpha, cs, k=5, sigma0=5e-3, tol=1e-6, carry_sigma=True):
+def cv_path(A, b, alpha, cs, k=5, sigma0=5e-3, tol=1e-6, carry_sigma=True, carry_dual=True):
     """k-fold CV error along c ∈ cs ("cross-validation ... along the path"): λ from the FULL
     data (λmax = ‖Aᵀb‖∞/α) so every fold uses the same grid; for each fold the
     warm-started path on the training rows (σ carried, R38), and the held-out squared error.
@@ -396,7 +406,7 @@ def cv_path(A, b, alpha, cs, k=5, sigma0=5e-3, tol=1e-6, carry_sigma=True):
         Ate, bte = np.ascontiguousarray(A[:, test]), b[test]
         ls = [(c * alpha * lm, c * (1 - alpha) * lm) for c in cs]
         for i, (x, _, _) in enumerate(solve_path_lambdas(Atr, btr, ls, sigma0=sigma0, tol=tol,
-                                                          carry_sigma=carry_sigma)):
+                                                          carry_sigma=carry_sigma, carry_dual=carry_dual)):
             err[i] += residual_ss(Ate, bte, x)
     err /= m
     return err, int(np.argmin(err))

@@ -481,12 +481,16 @@ void orc_default_opts(orc_opts* o) {
   o->jitter = 1e-10;
 }
 
-/* SsNAL-EN (Algorithm 1).  x0 may be NULL (cold start).  x_out (n) and y_out (m,
- * nullable) receive the final iterates.  trace (nullable) receives up to
- * trace_cap Newton-step records; *trace_len their count.  Returns stats.status. */
+/* SsNAL-EN (Algorithm 1).  x0 may be NULL (cold start).  y0 (nullable): the dual starting point of
+ * a warm-started path point — the previous point's final y (reading R39: Algorithm 1 starts "from the
+ * initial values y0, z0, x0, σ0", and a path point uses "the solution at the previous
+ * value for initialization"); with y0 the start is (x0, y0) and w0 = Aᵀy0 is the previous
+ * point's w (recomputed here, but not counted as an aty pass: the method has it already).  x_out (n)
+ * and y_out (m, nullable) receive the final iterates.  trace (nullable) receives up to trace_cap
+ * Newton-step records; *trace_len their count.  Returns stats.status. */
 int orc_solve(const double* A, const double* b, i64 m, i64 n, double l1, double l2, double sigma0, double tol,
-              const double* x0, const orc_opts* opts_in, double* x_out, double* y_out, orc_stats* st,
-              orc_trace* trace, i64 trace_cap, i64* trace_len) {
+              const double* x0, const double* y0, const orc_opts* opts_in, double* x_out, double* y_out,
+              orc_stats* st, orc_trace* trace, i64 trace_cap, i64* trace_len) {
   orc_opts o;
   if (opts_in) o = *opts_in; else orc_default_opts(&o);
   orc_stats S;
@@ -515,7 +519,10 @@ int orc_solve(const double* A, const double* b, i64 m, i64 n, double l1, double 
       if (x0[i] != 0.0) warm = 1;
     }
   }
-  if (warm && o.init_mode == 1) {
+  if (y0) {  /* R39: the previous path point's final dual iterate (and its w = Aᵀy) */
+    for (i64 k = 0; k < m; ++k) y[k] = y0[k];
+    orc_aty(A, m, n, y, w);
+  } else if (warm && o.init_mode == 1) {
     orc_ax(A, m, n, x, y);
     for (i64 k = 0; k < m; ++k) y[k] -= b[k];
     orc_aty(A, m, n, y, w);

@@ -44,8 +44,8 @@ struct SmallParams {
   const double* b;
   int m, n;
   double* x;        // in: x after init_point (dense); out: final x
-  const double* y0; // initial y (init_point)
-  const double* w0; // initial w = Aᵀy0 (0 when cold)
+  double* y0;       // initial y (init_point); on exit the final y (the next path point starts there, R39)
+  double* w0;       // initial w = Aᵀy0 (0 when cold); on exit the final w
   int32_t* Jx;      // out: support of x (ascending) and its values, count
   double* Px;
   int64_t* rx;
@@ -714,8 +714,13 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_small_solve(const SmallPar
     }
     sigma = fmin(C.sigma_factor * sigma, C.sigma_max);
   }
-  // ---- outputs ----
-  for (int i = tid; i < n; i += kSmallThreads) p.x[i] = xs[i];
+  // ---- outputs ----  (x; and the final dual iterate y, w = Aᵀy, which the next point of a path starts
+  // from under reading R39 — y0 / w0 were read at the start, so overwriting them is safe)
+  for (int i = tid; i < n; i += kSmallThreads) {
+    p.x[i] = xs[i];
+    p.w0[i] = w[wcur * kSmallMaxN + i];
+  }
+  if (tid < m) p.y0[tid] = ys[cur * kSmallMaxM + tid];
   if (tid == 0) {
     DevCtl* o = p.C;
     o->outer_iters = k;

@@ -699,11 +699,14 @@ __global__ void __cluster_dims__(kClCtas, 1, 1) __launch_bounds__(kClThreads, 1)
       }
     }
   }
-  // ---- outputs ----
+  // ---- outputs ----  (x; and the final dual iterate y, w = Aᵀy for the next point of a path,
+  // reading R39 — every CTA read y0 / w0 at the start, before the first cluster barrier)
   for (int i = tid; i < nl; i += kClThreads) {
     p.x[c0 + i] = xs[i];
     if (p.xout) p.xout[c0 + i] = xs[i];
+    p.w0[c0 + i] = w[wcur * kClCols + i];
   }
+  if (q == 0 && tid < m) p.y0[tid] = ys[cur * kSmallMaxM + tid];
   if (q == 0 && tid == 0) {
     DevCtl o = C;  // settings as used, then the statistics
     o.outer_iters = k;

@@ -397,6 +397,11 @@ struct ssnal_en_problem {
   std::vector<cudaEvent_t> path_ev;
   // option carry_sigma (reading R38): path point i starts at point i − 1's final σ
   int carry_sigma = 1;
+  // option carry_dual (reading R39): path point i > 0 also starts at point i − 1's final dual
+  // iterate y (and its w = Aᵀy), so the warm start costs no Aᵀ pass; option warm_dual: the same for
+  // a single warm-started solve (the handle's y, w from its previous solve instead of y0 = A x0 − b)
+  int carry_dual = 1;
+  int warm_dual = 0;
   // small-problem cluster path: the caller's device x buffer the kernel writes directly (no copy)
   double* direct_xout = nullptr;
   bool xout_done = false;
@@ -1449,7 +1454,7 @@ int check_args(ssnal_en_problem* P, double l1, double l2, double sigma0, double 
 // Start point (both modes).  x (P->x) holds x0 on entry (device).  Writes the support of x
 // (Jx, Px, r_dev[2]), y0 into y[0] and w0 = Aᵀy0 into w[0].  *rx = host-known |supp x| (0 cold,
 // −1 = on the device only).
-int init_point(ssnal_en_problem* P, int have_x0, ssnal_en_stats* S, int64_t* rx) {
+int init_point(ssnal_en_problem* P, int have_x0, ssnal_en_stats* S, int64_t* rx, bool keep_dual = false) {
   const int64_t m = P->m, n = P->n;
   int rc;
   // Support of x (Jx, Px, rx): K1e with w = 0, σ = 1, λ = 0 selects x ≠ 0 and P = x.
@@ -1466,6 +1471,9 @@ int init_point(ssnal_en_problem* P, int have_x0, ssnal_en_stats* S, int64_t* rx)
     CK(cudaMemsetAsync(P->r_dev + 2, 0, 8, P->st));
     CK(cudaMemsetAsync(P->r_dev + 4, 0, 8, P->st));
   }
+  // keep_dual (reading R39, a warm-started path point): y[0] and w[0] = Aᵀy[0] still hold the
+  // previous solve's final dual iterate — the start of this one, no Aᵀ pass
+  if (keep_dual) return SSNAL_OK;
   // Initial y, w (P:242 silent; reading R8): y0 = A x0 − b if x0 ≠ 0, else 0 (decided on the device)
   if (have_x0 && P->init_mode == 1) {
     // unsharded: the row-block cluster gather leaves the finished A_S x0_S in part_vec row 0
@@ -1521,7 +1529,7 @@ int launch_objective(ssnal_en_problem* P) {
 
 // Host-driven mode: control decisions on the CPU from the EvalOut records (mapped memory).
 int solve_core(ssnal_en_problem* P, double l1, double l2, double sigma0, double tol, int have_x0,
-               ssnal_en_stats* S) {
+               ssnal_en_stats* S, bool keep_dual = false) {
   const int64_t m = P->m;
   memset(S, 0, sizeof(*S));
   int rc;
@@ -1530,7 +1538,7 @@ int solve_core(ssnal_en_problem* P, double l1, double l2, double sigma0, double 
   EvalOut ev, evt;
   int64_t rx = 0;
   CK(cudaMemsetAsync(&P->ctl->cg_iters, 0, sizeof(int), P->st));
-  if ((rc = init_point(P, have_x0, S, &rx))) return rc;
+  if ((rc = init_point(P, have_x0, S, &rx, keep_dual))) return rc;
 
   double sigma = sigma0;
   int converged = 0, numeric = 0, k;
@@ -1686,13 +1694,17 @@ int solve_core(ssnal_en_problem* P, double l1, double l2, double sigma0, double 
   S->outer_iters = k;
   S->sigma_final = sigma;
   S->status = numeric ? SSNAL_ENUMERIC : (converged ? SSNAL_OK : SSNAL_NOT_CONVERGED);
+  // the final dual iterate into the fixed slots y[0], w[0], as graph mode leaves it, so that the next
+  // solve of a path can start there (reading R39, option warm_dual / carry_dual)
+  if (cur != 0) CK(cudaMemcpyAsync(P->y[0], P->y[cur], P->m * 8, cudaMemcpyDeviceToDevice, P->st));
+  if (wcur != 0) CK(cudaMemcpyAsync(P->w[0], P->w[wcur], P->n * 8, cudaMemcpyDeviceToDevice, P->st));
   // Stats: F(x) (Eq. (1)) via resid = A x − b; D(y) = −½yᵀy − bᵀy − Σ(|w|−λ1)²₊/(2λ2)
   if ((rc = launch_objective(P))) return rc;
   S->dual_obj = (l2 > 0) ? (-(0.5 * ev.yy + ev.by) - ev.s[3] / (2.0 * l2)) : NAN;
   CK(cudaMemcpyAsync(P->scratch_host + 40, &P->ctl->cg_iters, sizeof(int), cudaMemcpyDeviceToHost, P->st));
   P->stat_l1 = l1;
   P->stat_l2 = l2;
-  P->stat_warm_pass = (have_x0 && P->init_mode == 1);
+  P->stat_warm_pass = (have_x0 && P->init_mode == 1 && !keep_dual);
   P->graph_pending = false;
   return S->status;
 }
@@ -1894,13 +1906,13 @@ bool small_eligible(const ssnal_en_problem* P) {
 }
 
 int solve_small_core(ssnal_en_problem* P, double l1, double l2, double sigma0, double tol, int have_x0,
-                     ssnal_en_stats* S, const double* sigma_dev = nullptr) {
+                     ssnal_en_stats* S, const double* sigma_dev = nullptr, bool keep_dual = false) {
   memset(S, 0, sizeof(*S));
   int rc;
   int64_t rx = 0;
   const bool cl = P->use_small_cl && P->small_cl_ok;
   // the cluster kernel initialises a cold start itself (no memsets) and computes the objective
-  if ((!cl || have_x0) && (rc = init_point(P, have_x0, S, &rx))) return rc;
+  if ((!cl || have_x0) && (rc = init_point(P, have_x0, S, &rx, keep_dual))) return rc;
   if (cl && !have_x0) S->aty_passes = 0;
   DevCtl* h = P->ctl_host;
   memset(h, 0, sizeof(DevCtl));
@@ -1968,18 +1980,18 @@ int solve_small_core(ssnal_en_problem* P, double l1, double l2, double sigma0, d
   }
   P->stat_l1 = l1;
   P->stat_l2 = l2;
-  P->stat_warm_pass = (have_x0 && P->init_mode == 1);
+  P->stat_warm_pass = (have_x0 && P->init_mode == 1 && !keep_dual);
   P->graph_pending = true;
   return SSNAL_OK;
 }
 
 int solve_graph_core(ssnal_en_problem* P, double l1, double l2, double sigma0, double tol, int have_x0,
-                     ssnal_en_stats* S, const double* sigma_dev = nullptr) {
+                     ssnal_en_stats* S, const double* sigma_dev = nullptr, bool keep_dual = false) {
   memset(S, 0, sizeof(*S));
   int rc;
   if ((rc = build_graph(P))) return rc;
   int64_t rx = 0;
-  if ((rc = init_point(P, have_x0, S, &rx))) return rc;
+  if ((rc = init_point(P, have_x0, S, &rx, keep_dual))) return rc;
   DevCtl* h = P->ctl_host;
   memset(h, 0, sizeof(DevCtl));
   h->l1 = l1;
@@ -2010,7 +2022,7 @@ int solve_graph_core(ssnal_en_problem* P, double l1, double l2, double sigma0, d
   CK(cudaMemcpyAsync(P->ev_out_host, P->ev_dev, sizeof(EvalOut), cudaMemcpyDeviceToHost, P->st));
   P->stat_l1 = l1;
   P->stat_l2 = l2;
-  P->stat_warm_pass = (have_x0 && P->init_mode == 1);
+  P->stat_warm_pass = (have_x0 && P->init_mode == 1 && !keep_dual);
   P->graph_pending = true;
   return SSNAL_OK;
 }
@@ -2360,6 +2372,8 @@ int ssnal_en_set_option(ssnal_en_problem* P, const char* key, double v) {
   else if (k == "test_fail_factor" && v >= 0) P->inject_fail = (int)v;
   else if (k == "inner_tol_mode" && (v == 0 || v == 1)) P->inner_tol_mode = (int)v;
   else if (k == "carry_sigma" && (v == 0 || v == 1)) P->carry_sigma = (int)v;
+  else if (k == "carry_dual" && (v == 0 || v == 1)) P->carry_dual = (int)v;
+  else if (k == "warm_dual" && (v == 0 || v == 1)) P->warm_dual = (int)v;
   else if (k == "cg_tol" && v > 0 && v < 1) {
     P->cg_tol = v;
     drop_graph(P);  // baked into the captured CG launch
@@ -2441,6 +2455,8 @@ double ssnal_en_get_info(const ssnal_en_problem* P, const char* key) {
   if (k == "cg_ratio") return P->cg_ratio;
   if (k == "cg_threshold") return P->cg_threshold;
   if (k == "carry_sigma") return P->carry_sigma;
+  if (k == "carry_dual") return P->carry_dual;
+  if (k == "warm_dual") return P->warm_dual;
   if (k == "k1_time_s") return P->k1_time;       // Σ K1 launch times timed by the hook calls (option time_k1)
   if (k == "k1_launches") return P->k1_count;
   return NAN;
@@ -2476,9 +2492,10 @@ static int solve_wrapped(ssnal_en_problem* P, double l1, double l2, double sigma
   ssnal_en_stats S;
   P->direct_xout = (x_out && xout_dev && x_out != x0) ? x_out : nullptr;
   P->xout_done = false;
-  rc = small_eligible(P)                ? solve_small_core(P, l1, l2, sigma0, tol, have_x0, &S)
-       : (P->use_graph && (!sharded(P) || P->peer)) ? solve_graph_core(P, l1, l2, sigma0, tol, have_x0, &S)
-                                       : solve_core(P, l1, l2, sigma0, tol, have_x0, &S);
+  const bool keep = P->warm_dual && have_x0;  // R39: start from the handle's previous (y, w)
+  rc = small_eligible(P)                ? solve_small_core(P, l1, l2, sigma0, tol, have_x0, &S, nullptr, keep)
+       : (P->use_graph && (!sharded(P) || P->peer)) ? solve_graph_core(P, l1, l2, sigma0, tol, have_x0, &S, nullptr, keep)
+                                       : solve_core(P, l1, l2, sigma0, tol, have_x0, &S, keep);
   if (rc == SSNAL_ECUDA || rc == SSNAL_EINVAL) return rc;
   if (x_out && !P->xout_done) {
     CK(cudaMemcpyAsync(x_out, P->x, P->n * 8, xout_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, P->st));
@@ -2570,7 +2587,10 @@ int ssnal_en_solve_path_device(ssnal_en_problem* P, int64_t npts, const double* 
     for (int64_t i = 0; i < npts; ++i) {
       const double* xi = i == 0 ? x0 : x_out + (i - 1) * n;
       ssnal_en_stats st;
+      const int keep_wd = P->warm_dual;
+      P->warm_dual = (P->carry_dual && i > 0) ? 1 : keep_wd;  // R39 along the path
       const int rc = solve_wrapped(P, lambda1[i], lambda2[i], sig, tol, xi, 1, x_out + i * n, 1, &st);
+      P->warm_dual = keep_wd;
       if (rc == SSNAL_EINVAL || rc == SSNAL_ECUDA) return rc;
       if (stats) stats[i] = st;
       fold(rc);
@@ -2626,8 +2646,9 @@ int ssnal_en_solve_path_device(ssnal_en_problem* P, int64_t npts, const double* 
     const double* sig_in = (P->carry_sigma && i > 0) ? sigma_carry : nullptr;
     P->direct_xout = x_out + i * n;
     P->xout_done = false;
-    rc = small_eligible(P) ? solve_small_core(P, lambda1[i], lambda2[i], sigma0, tol, warm, &S[i], sig_in)
-                           : solve_graph_core(P, lambda1[i], lambda2[i], sigma0, tol, warm, &S[i], sig_in);
+    const bool keep = P->carry_dual && i > 0;  // R39: the previous point's final (y, w)
+    rc = small_eligible(P) ? solve_small_core(P, lambda1[i], lambda2[i], sigma0, tol, warm, &S[i], sig_in, keep)
+                           : solve_graph_core(P, lambda1[i], lambda2[i], sigma0, tol, warm, &S[i], sig_in, keep);
     if (rc == SSNAL_OK && P->carry_sigma)
       CK(cudaMemcpyAsync(sigma_carry, &P->ctl->sigma_final, 8, cudaMemcpyDeviceToDevice, P->st));
     if (rc == SSNAL_OK && !P->xout_done) CK(cudaMemcpyAsync(x_out + i * n, P->x, n * 8, cudaMemcpyDeviceToDevice, P->st));

@@ -17,18 +17,21 @@ def lambda_grid(n_points: int = 100, c_max: float = 1.0, c_min: float = 0.1) -> 
 
 
 def solve_path(P, alpha: float, cs, sigma0: float = 5e-3, tol: float = 1e-6, max_active: int | None = None,
-               select: bool = True, debias: bool = False, carry_sigma: bool = True):
+               select: bool = True, debias: bool = False, carry_sigma: bool = True, carry_dual: bool = True):
     """Solve along c ∈ cs with λ1 = c α λmax, λ2 = c (1 − α) λmax, λmax = ‖Aᵀb‖∞/α,
     warm-starting each point at the previous solution and — reading R38 — at the
-    previous point's final σ (carry_sigma; False restarts every point at σ0).  The path stops once a
+    previous point's final σ (carry_sigma; False restarts every point at σ0) and — reading R39 — at its
+    final dual iterate (carry_dual: option warm_dual for every point after the first, so the warm start
+    costs no Aᵀ pass; the handle keeps y and w between the calls).  The path stops once a
     solution has at least `max_active` nonzeros.  Returns (points, best) where best maps
     'gcv' / 'ebic' to the index of the minimising point (None without selection)."""
     lmax = P.lambda_max_l1 / alpha
     points = []
     x = None
     sig = sigma0
-    for c in cs:
+    for i, c in enumerate(cs):
         l1, l2 = c * alpha * lmax, c * (1 - alpha) * lmax
+        P.set_option("warm_dual", 1 if (carry_dual and i > 0) else 0)
         x, st = P.solve(l1, l2, sig, tol, x0=x)
         if carry_sigma:
             sig = st["sigma_final"]
@@ -37,6 +40,7 @@ def solve_path(P, alpha: float, cs, sigma0: float = 5e-3, tol: float = 1e-6, max
                        "x_debiased": xdb})
         if max_active is not None and st["active"] >= max_active:
             break
+    P.set_option("warm_dual", 0)
     best = {}
     if select:
         for key in ("gcv", "ebic"):
@@ -47,7 +51,7 @@ def solve_path(P, alpha: float, cs, sigma0: float = 5e-3, tol: float = 1e-6, max
 
 
 def cv_path(make_problem, m: int, alpha: float, cs, lambda_max_l1: float, k: int = 5, sigma0: float = 5e-3,
-            tol: float = 1e-6):
+            tol: float = 1e-6, carry_dual: bool = True):
     """k-fold cross-validation along the path (Section 3.3; reading R35).
 
     make_problem(rows) must return a Problem over the given rows of (A, b) (e.g. a handle created
@@ -66,6 +70,7 @@ def cv_path(make_problem, m: int, alpha: float, cs, lambda_max_l1: float, k: int
             sig = sigma0
             for i, c in enumerate(cs):
                 l1, l2 = c * alpha * lmax, c * (1 - alpha) * lmax
+                Ptr.set_option("warm_dual", 1 if (carry_dual and i > 0) else 0)  # reading R39
                 x, st = Ptr.solve(l1, l2, sig, tol, x0=x)
                 sig = st["sigma_final"]  # reading R38
                 cv[i] += Pte.residual(x)

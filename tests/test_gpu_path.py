@@ -3,7 +3,8 @@ every point enqueued before one synchronisation must give exactly the loop of si
 (same kernels in the same order: x bitwise, statistics equal), in graph mode, on the one-CTA path, and
 through the host-driven fallback; a cold first point and an x0 start; bad arguments are EINVAL.
 With option carry_sigma (default; reading R38) point i starts at point i − 1's sigma_final (the
-loop passes it explicitly); the path then matches the oracle's carried path point by point (±1 rule),
+loop passes it explicitly) and, with carry_dual (default; reading R39), at its final dual iterate (the
+loop sets warm_dual); the path then matches the oracle's carried path point by point (±1 rule),
 and most warm points converge in one outer iteration on the Table D.4 grid."""
 import numpy as np
 import pytest
@@ -26,14 +27,17 @@ KEYS = ["status", "outer_iters", "newton_iters", "psi_evals", "backtracks", "aty
 def loop_vs_path(P, ls, sigma0, tol, n, x0=None):
     k = len(ls)
     carry = P.info("carry_sigma") == 1
+    dual = P.info("carry_dual") == 1  # R39: the loop starts point i > 0 from the handle's (y, w)
     xl = torch.empty((k, n), dtype=torch.float64, device="cuda")
     sl = []
     sig = sigma0
     for i, (l1, l2) in enumerate(ls):
         x0p = (x0.data_ptr() if x0 is not None else 0) if i == 0 else xl[i - 1].data_ptr()
+        P.set_option("warm_dual", 1 if (dual and i > 0) else 0)
         sl.append(P.solve_device(l1, l2, sig, tol, x0p, xl[i].data_ptr()))
         if carry:
             sig = sl[-1]["sigma_final"]
+    P.set_option("warm_dual", 0)
     xp = torch.empty((k, n), dtype=torch.float64, device="cuda")
     sp = P.solve_path_device([a for a, _ in ls], [b for _, b in ls], sigma0, tol,
                              x0.data_ptr() if x0 is not None else 0, xp.data_ptr())
@@ -62,6 +66,12 @@ def test_path_matches_loop(name, n, graph):
         sp0 = loop_vs_path(P, ls, cfg.sigma0, cfg.tol, A.shape[0])
         assert min(s["outer_iters"] for s in sp0[1:]) >= 3
         P.set_option("carry_sigma", 1)
+        # R39: with the dual carried the warm start costs no Aᵀ pass; carry_dual = 0 restores y0 = A x0 − b
+        assert all(s["aty_passes"] == s["newton_iters"] for s in sp[1:])
+        P.set_option("carry_dual", 0)
+        sp8 = loop_vs_path(P, ls, cfg.sigma0, cfg.tol, A.shape[0])
+        assert sum(s["aty_passes"] for s in sp8) > sum(s["aty_passes"] for s in sp)
+        P.set_option("carry_dual", 1)
         # a warm first point from a given x0
         x0 = torch.zeros(A.shape[0], dtype=torch.float64, device="cuda")
         x0[3] = 0.1

@@ -1,5 +1,5 @@
-"""Reading R38: along a warm-started λ path each point starts from the previous point's x AND its
-final σ (oracle.solve_path).  Pinned against what the paper says a warm start does: "the new solution
+"""Readings R38 / R39: along a warm-started λ path each point starts from the previous point's x, its
+final σ and (R39) its final dual iterate y (oracle.solve_path).  Pinned against what the paper says a warm start does: "the new solution
 is very close to the previous one and can be computed very quickly -- usually SsNAL-EN converges in
 just one iteration", on the Table D.4 protocol (100 log-spaced c from 1 to
 0.1, stopping at 100 active features), plus SPEC's soft bound of ≤ 2 outer iterations per
@@ -71,3 +71,25 @@ def test_path_points_satisfy_kkt_at_tight_tolerance():
     for (l1, l2), (x, _, st) in zip(ls, res):
         assert st["status"] == 0
         assert oracle.kkt_violation(A, b, x, l1, l2) <= 1e-8 * l1
+
+
+def test_carried_dual_saves_the_warm_start_pass(d4_paths):
+    """Reading R39 (Algorithm 1 starts "from the initial values y0, z0, x0, σ0"; a path
+    point uses "the solution at the previous value for initialization"): each point i > 0
+    starts from point i − 1's final (x, y, σ).  Against the R8 restart y0 = A x0 − b (carry_dual=False)
+    on the Table D.4 protocol: the warm start costs no Aᵀ pass (aty_passes = Newton steps at every
+    point after the first), the pin of P:411 still holds, and both readings reach the same minimiser
+    at tol 1e-10 (BASELINE tolerances)."""
+    cfg, A, b, cs, (ls, res) = d4_paths
+    r8 = oracle.solve_path_lambdas(A, b, ls[:len(res)], carry_dual=False)
+    for (_, _, st), (_, _, s8), (xp, _, _) in zip(res[1:], r8[1:], r8[:-1]):
+        assert st["aty_passes"] == st["newton_iters"]
+        assert s8["aty_passes"] == s8["newton_iters"] + (1 if np.any(xp != 0) else 0)  # R8: y0 = A x0 − b
+    assert sum(st["aty_passes"] for _, _, st in res) < sum(st["aty_passes"] for _, _, st in r8)
+    k = 12
+    tight_d = oracle.solve_path_lambdas(A, b, ls[:k], tol=1e-10)
+    tight_8 = oracle.solve_path_lambdas(A, b, ls[:k], tol=1e-10, carry_dual=False)
+    for (xd, _, _), (x8, _, _), (l1, l2) in zip(tight_d, tight_8, ls[:k]):
+        Fd, F8 = oracle.primal_obj(A, b, xd, l1, l2), oracle.primal_obj(A, b, x8, l1, l2)
+        assert abs(Fd - F8) <= 1e-9 * abs(F8)
+        assert np.max(np.abs(xd - x8)) <= 1e-6 * max(np.max(np.abs(x8)), 1e-300)
