@@ -620,10 +620,17 @@ __global__ void __cluster_dims__(kClCtas, 1, 1) __launch_bounds__(kClThreads, 1)
     if (numeric) break;
     res3 = (sqrt(ev.s[1]) / sigma) / (1.0 + sqrt(ev.yy) + sqrt(ev.s[2]));
     res1 = ev.res1;
-    // multiplier update Eq. (10): x ← P, local columns; support list at the rank's offset
+    // multiplier update Eq. (10): x ← P, local columns; support list at the rank's offset.
+    // The current dual iterate (y, w = Aᵀy) goes to y0 / w0 at every outer step: the last one is the
+    // final iterate the next point of a path starts from (reading R39; every CTA read y0 / w0 at the
+    // start, before the first cluster barrier)
     const int* offs = offsb + cur * (kClCtas + 1);
     const int cntq = offs[q + 1] - offs[q];
-    for (int i = tid; i < nl; i += kClThreads) xs[i] = 0.0;
+    for (int i = tid; i < nl; i += kClThreads) {
+      xs[i] = 0.0;
+      p.w0[c0 + i] = w[wcur * kClCols + i];
+    }
+    if (q == 0 && tid < m) p.y0[tid] = ys[cur * kSmallMaxM + tid];
     __syncthreads();
     for (int a = tid; a < cntq; a += kClThreads) {
       const int la = Jl[cur * kClCols + a];
@@ -699,14 +706,11 @@ __global__ void __cluster_dims__(kClCtas, 1, 1) __launch_bounds__(kClThreads, 1)
       }
     }
   }
-  // ---- outputs ----  (x; and the final dual iterate y, w = Aᵀy for the next point of a path,
-  // reading R39 — every CTA read y0 / w0 at the start, before the first cluster barrier)
+  // ---- outputs ----
   for (int i = tid; i < nl; i += kClThreads) {
     p.x[c0 + i] = xs[i];
     if (p.xout) p.xout[c0 + i] = xs[i];
-    p.w0[c0 + i] = w[wcur * kClCols + i];
   }
-  if (q == 0 && tid < m) p.y0[tid] = ys[cur * kSmallMaxM + tid];
   if (q == 0 && tid == 0) {
     DevCtl o = C;  // settings as used, then the statistics
     o.outer_iters = k;
