@@ -197,6 +197,7 @@ def host_solve_workload(Q, cfg, lm):
     for i, c in enumerate(cfg.cs):
         l1, l2 = lambdas(cfg, lm, c)
         x0 = x_prev if (cfg.path and i > 0) else None
+        Q.set_option("warm_dual", 1 if (cfg.path and i > 0) else 0)  # R39, as the path call does
         x_prev, st = Q.solve(l1, l2, sig, cfg.tol, x0=x0)
         if cfg.path:
             sig = st["sigma_final"]  # R38, as the path call does
@@ -406,6 +407,9 @@ def bench_ours(args, rank, world, local_rank):
                    "storage": ("packed 2-bit genotype codes + per-column tables (SURVEY 8(f4))" if args.geno
                                else "fp64 column-major"),
                    "path_sigma": "carried from point to point (reading R38, P:411)" if cfg.path else None,
+                   "path_dual": ("each point after the first starts from the previous point's final y, w = A^T y "
+                                 "(reading R39, P:236-246 + P:409-411): no A^T pass for the warm start")
+                                if cfg.path else None,
                    "newton_strategy": ("exact (Eq. 18/19); CG when min(m, r) > 1e4 (P:379)" if args.cg_ratio == 0
                                        else f"CG (K6) when r > {args.cg_ratio:g} m, else exact (Eq. 18/19)")},
         "step_times": step_summary(per_step),
