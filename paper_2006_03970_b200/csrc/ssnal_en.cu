@@ -1454,9 +1454,17 @@ int check_args(ssnal_en_problem* P, double l1, double l2, double sigma0, double 
 // Start point (both modes).  x (P->x) holds x0 on entry (device).  Writes the support of x
 // (Jx, Px, r_dev[2]), y0 into y[0] and w0 = Aᵀy0 into w[0].  *rx = host-known |supp x| (0 cold,
 // −1 = on the device only).
-int init_point(ssnal_en_problem* P, int have_x0, ssnal_en_stats* S, int64_t* rx, bool keep_dual = false) {
+int init_point(ssnal_en_problem* P, int have_x0, ssnal_en_stats* S, int64_t* rx, bool keep_dual = false,
+               bool support_current = false) {
   const int64_t m = P->m, n = P->n;
   int rc;
+  if (keep_dual && support_current && have_x0) {
+    // a path point continuing from the previous solve on this handle: x, its support (Jx, Px, r_dev[2])
+    // and the dual iterate (y[0], w[0]) are all that solve's final state — nothing to recompute
+    CK(cudaMemcpyAsync(P->r_dev + 4, P->r_dev + 2, 8, cudaMemcpyDeviceToDevice, P->st));  // |supp x0| for stats
+    *rx = -1;
+    return SSNAL_OK;
+  }
   // Support of x (Jx, Px, rx): K1e with w = 0, σ = 1, λ = 0 selects x ≠ 0 and P = x.
   *rx = 0;
   if (have_x0) {
@@ -1906,13 +1914,14 @@ bool small_eligible(const ssnal_en_problem* P) {
 }
 
 int solve_small_core(ssnal_en_problem* P, double l1, double l2, double sigma0, double tol, int have_x0,
-                     ssnal_en_stats* S, const double* sigma_dev = nullptr, bool keep_dual = false) {
+                     ssnal_en_stats* S, const double* sigma_dev = nullptr, bool keep_dual = false,
+                     bool support_current = false) {
   memset(S, 0, sizeof(*S));
   int rc;
   int64_t rx = 0;
   const bool cl = P->use_small_cl && P->small_cl_ok;
   // the cluster kernel initialises a cold start itself (no memsets) and computes the objective
-  if ((!cl || have_x0) && (rc = init_point(P, have_x0, S, &rx, keep_dual))) return rc;
+  if ((!cl || have_x0) && (rc = init_point(P, have_x0, S, &rx, keep_dual, support_current))) return rc;
   if (cl && !have_x0) S->aty_passes = 0;
   DevCtl* h = P->ctl_host;
   memset(h, 0, sizeof(DevCtl));
@@ -1986,12 +1995,13 @@ int solve_small_core(ssnal_en_problem* P, double l1, double l2, double sigma0, d
 }
 
 int solve_graph_core(ssnal_en_problem* P, double l1, double l2, double sigma0, double tol, int have_x0,
-                     ssnal_en_stats* S, const double* sigma_dev = nullptr, bool keep_dual = false) {
+                     ssnal_en_stats* S, const double* sigma_dev = nullptr, bool keep_dual = false,
+                     bool support_current = false) {
   memset(S, 0, sizeof(*S));
   int rc;
   if ((rc = build_graph(P))) return rc;
   int64_t rx = 0;
-  if ((rc = init_point(P, have_x0, S, &rx, keep_dual))) return rc;
+  if ((rc = init_point(P, have_x0, S, &rx, keep_dual, support_current))) return rc;
   DevCtl* h = P->ctl_host;
   memset(h, 0, sizeof(DevCtl));
   h->l1 = l1;
@@ -2640,15 +2650,15 @@ int ssnal_en_solve_path_device(ssnal_en_problem* P, int64_t npts, const double* 
     k1_beg[i] = P->k1_pending.size();
     CK(cudaEventRecord(P->path_ev[2 * i], P->st));
     const double* xi = i == 0 ? x0 : x_out + (i - 1) * n;
-    if (xi) CK(cudaMemcpyAsync(P->x, xi, n * 8, cudaMemcpyDeviceToDevice, P->st));
-    else if (i == 0 && have0) CK(cudaMemsetAsync(P->x, 0, n * 8, P->st));  // sharded: no slice here
+    const bool keep = P->carry_dual && i > 0;  // R39: the previous point's final (x, y, w) and support
+    if (xi && !keep) CK(cudaMemcpyAsync(P->x, xi, n * 8, cudaMemcpyDeviceToDevice, P->st));
+    else if (i == 0 && have0 && !xi) CK(cudaMemsetAsync(P->x, 0, n * 8, P->st));  // sharded: no slice here
     const int warm = i == 0 ? have0 : 1;
     const double* sig_in = (P->carry_sigma && i > 0) ? sigma_carry : nullptr;
     P->direct_xout = x_out + i * n;
     P->xout_done = false;
-    const bool keep = P->carry_dual && i > 0;  // R39: the previous point's final (y, w)
-    rc = small_eligible(P) ? solve_small_core(P, lambda1[i], lambda2[i], sigma0, tol, warm, &S[i], sig_in, keep)
-                           : solve_graph_core(P, lambda1[i], lambda2[i], sigma0, tol, warm, &S[i], sig_in, keep);
+    rc = small_eligible(P) ? solve_small_core(P, lambda1[i], lambda2[i], sigma0, tol, warm, &S[i], sig_in, keep, keep)
+                           : solve_graph_core(P, lambda1[i], lambda2[i], sigma0, tol, warm, &S[i], sig_in, keep, keep);
     if (rc == SSNAL_OK && P->carry_sigma)
       CK(cudaMemcpyAsync(sigma_carry, &P->ctl->sigma_final, 8, cudaMemcpyDeviceToDevice, P->st));
     if (rc == SSNAL_OK && !P->xout_done) CK(cudaMemcpyAsync(x_out + i * n, P->x, n * 8, cudaMemcpyDeviceToDevice, P->st));
