@@ -259,6 +259,67 @@ __global__ void k_max_reduce(const double* in, int cnt, double* out) {
 
 }  // namespace
 
+// λ path results, one pinned (mapped) slot per point: written by the host-side copies of a point solved
+// by its own graph launch, or directly by k_path_end in the device-resident path graph.
+struct PathSlot {
+  DevCtl ctl;
+  EvalOut ev;
+  double scratch[64];
+  double l1, l2;
+  int warm_pass, pad;
+  int64_t launches;
+  unsigned long long t0, t1;  // path graph: %globaltimer at the point's begin / end
+};
+// device state of the path graph (ssnal_en_solve_path_device, points 1 … npts − 1 in one launch)
+struct PathDev {
+  const double* l1s;
+  const double* l2s;
+  double* xout;          // the caller's x_out (npts × n)
+  long long i, npts;     // current point, point count
+  int carry_sigma, pad;
+  unsigned long long t0;
+  DevCtl tmpl;           // the solve settings (σ0 in tmpl.sigma), copied into the control block per point
+};
+
+namespace {
+// point i > 0 begins (reading R38/R39: from the previous point's final x, y, w and — with
+// carry_sigma — σ, all still in the handle): its settings and λ into the control block, |supp x0|
+// for the stats, and the outer loop armed
+__global__ void k_path_begin(DevCtl* C, PathDev* pd, int64_t* r_dev, cudaGraphConditionalHandle h_outer) {
+  const long long i = pd->i;
+  const double sig = pd->carry_sigma ? C->sigma_final : pd->tmpl.sigma;
+  DevCtl c = pd->tmpl;
+  c.l1 = pd->l1s[i];
+  c.l2 = pd->l2s[i];
+  c.sigma = sig;
+  *C = c;
+  r_dev[4] = r_dev[2];
+  pd->t0 = global_ns();
+  cudaGraphSetConditional(h_outer, 1);
+}
+__global__ void k_path_copy_x(const double* __restrict__ x, const PathDev* pd, int64_t n) {
+  double* dst = pd->xout + pd->i * n;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+    dst[k] = x[k];
+}
+// point i ends: its control block, final evaluation record and objective pieces into its (mapped
+// pinned) slot, the next point or the end of the path
+__global__ void k_path_end(const DevCtl* C, const EvalOut* ev, const double* scratch, const int64_t* r_dev,
+                           PathSlot* slots, PathDev* pd, cudaGraphConditionalHandle h_path) {
+  const long long i = pd->i;
+  PathSlot* sl = slots + i;
+  sl->ctl = *C;
+  sl->ev = ev[0];
+  for (int j = 16; j < 20; ++j) sl->scratch[j] = scratch[j];
+  *reinterpret_cast<long long*>(sl->scratch + 20) = r_dev[4];
+  sl->t0 = pd->t0;
+  sl->t1 = global_ns();
+  __threadfence_system();
+  pd->i = i + 1;
+  cudaGraphSetConditional(h_path, i + 1 < pd->npts);
+}
+}  // namespace
+
 // ===========================================================================
 struct ssnal_en_problem {
   int64_t m = 0, n = 0;
@@ -402,6 +463,17 @@ struct ssnal_en_problem {
   // a single warm-started solve (the handle's y, w from its previous solve instead of y0 = A x0 − b)
   int carry_dual = 1;
   int warm_dual = 0;
+  // device-resident λ path (option path_graph): points 1 … npts − 1 of ssnal_en_solve_path_device
+  // in ONE launch of a graph whose WHILE loop runs the solve graph's body once per point
+  int use_path_graph = 1;
+  cudaStream_t cap_path = nullptr;
+  cudaGraph_t pgraph = nullptr;
+  cudaGraphExec_t pgexec = nullptr;
+  PathDev* pdev = nullptr;       // device
+  PathDev* pdev_host = nullptr;  // pinned staging
+  double* path_l = nullptr;      // device λ1[path_lcap], λ2[path_lcap]
+  int64_t path_lcap = 0;
+  int pgraph_fixed = 0;          // kernel nodes per point outside the solve's segments
   // small-problem cluster path: the caller's device x buffer the kernel writes directly (no copy)
   double* direct_xout = nullptr;
   bool xout_done = false;
@@ -1738,7 +1810,10 @@ int add_while(cudaStream_t st, cudaGraphConditionalHandle h, cudaGraph_t* body) 
 }
 
 // Captures the three loop levels into the bodies of nested WHILE nodes (see k_ctl.cuh).
-int capture_graph(ssnal_en_problem* P, cudaGraph_t G) {
+// body_pre / h_pre (path graph): capture the solve into an existing outer-loop body whose WHILE node
+// (handle h_pre) the caller has added; otherwise the outer WHILE node is added at the root of G.
+int capture_graph(ssnal_en_problem* P, cudaGraph_t G, cudaGraph_t body_pre = nullptr,
+                  cudaGraphConditionalHandle h_pre = 0) {
   const int64_t m = P->m, n = P->n;
   DevCtl* C = P->ctl;
   const Scal none = make_scal(1.0, 0.0, 0.0);  // placeholder: every kernel reads C->sc
@@ -1758,9 +1833,12 @@ int capture_graph(ssnal_en_problem* P, cudaGraph_t G) {
     return launch_eval(P, y, none, with_grad, nullptr, nparts ? 1 : 0, g_out, P->rg_dev, slot, gd_src, info_src, &C->sc,
                        pred, P->xbuf, P->xbuf + m, 1, hook, hk);
   };
-  CK(cudaGraphConditionalHandleCreate(&h_outer, G, 1, cudaGraphCondAssignDefault));
   cudaGraph_t body_o, body_i, body_b;
-  {
+  if (body_pre) {
+    h_outer = h_pre;
+    body_o = body_pre;
+  } else {
+    CK(cudaGraphConditionalHandleCreate(&h_outer, G, 1, cudaGraphCondAssignDefault));
     cudaGraphNodeParams cp = {};
     cp.type = cudaGraphNodeTypeConditional;
     cp.conditional.handle = h_outer;
@@ -1897,11 +1975,125 @@ int build_graph(ssnal_en_problem* P) {
   return SSNAL_OK;
 }
 
+void drop_path_graph(ssnal_en_problem* P) {
+  if (P->pgexec) cudaGraphExecDestroy(P->pgexec);
+  if (P->pgraph) cudaGraphDestroy(P->pgraph);
+  P->pgexec = nullptr;
+  P->pgraph = nullptr;
+}
+
 void drop_graph(ssnal_en_problem* P) {
   if (P->gexec) cudaGraphExecDestroy(P->gexec);
   if (P->graph) cudaGraphDestroy(P->graph);
   P->gexec = nullptr;
   P->graph = nullptr;
+  drop_path_graph(P);  // it embeds the same solve body
+}
+
+// The device-resident λ path: WHILE (point < npts) { k_path_begin; the solve (the solve graph's
+// nested WHILE loops, captured again into this body); the objective pieces; x → x_out[point];
+// k_path_end } — points 1 … npts − 1 of a warm-started path in one launch, no host round trip
+// between points (the host only reads the per-point slots after the path).  Unsharded, multi-kernel
+// graph mode, the dual and x carried (reading R39).
+int build_path_graph(ssnal_en_problem* P, PathSlot* slots_dev) {
+  if (P->pgexec) return SSNAL_OK;
+  int rc;
+  if (!P->pdev) {
+    if ((rc = alloc((void**)&P->pdev, sizeof(PathDev)))) return rc;
+    CK(cudaHostAlloc((void**)&P->pdev_host, sizeof(PathDev), cudaHostAllocDefault));
+  }
+  for (int i = 0; i < 3; ++i)
+    if (!P->cap[i]) CK(cudaStreamCreateWithFlags(&P->cap[i], cudaStreamNonBlocking));
+  if (!P->cap_path) CK(cudaStreamCreateWithFlags(&P->cap_path, cudaStreamNonBlocking));
+  cudaGraph_t G;
+  CK(cudaGraphCreate(&G, 0));
+  cudaGraphConditionalHandle h_path;
+  CK(cudaGraphConditionalHandleCreate(&h_path, G, 1, cudaGraphCondAssignDefault));
+  cudaGraph_t body_p;
+  {
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h_path;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t node;
+    CK(cudaGraphAddNode(&node, G, nullptr, 0, &cp));
+    body_p = cp.conditional.phGraph_out[0];
+  }
+  cudaStream_t saved = P->st;
+  const int64_t L0 = P->launches;
+  P->capturing = true;
+  bool cap_open = false;
+  rc = SSNAL_OK;
+  do {
+    cudaError_t e = cudaStreamBeginCaptureToGraph(P->cap_path, body_p, nullptr, nullptr, 0,
+                                                  cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) {
+      set_err("path graph capture: %s", cudaGetErrorString(e));
+      rc = SSNAL_ECUDA;
+      break;
+    }
+    cap_open = true;
+    P->st = P->cap_path;
+    cudaGraphConditionalHandle h_outer;
+    if ((e = cudaGraphConditionalHandleCreate(&h_outer, body_p, 0, 0)) != cudaSuccess) {
+      set_err("path graph handle: %s", cudaGetErrorString(e));
+      rc = SSNAL_ECUDA;
+      break;
+    }
+    k_path_begin<<<1, 1, 0, P->st>>>(P->ctl, P->pdev, P->r_dev, h_outer);
+    cudaGraph_t body_o;
+    if ((rc = add_while(P->cap_path, h_outer, &body_o))) break;
+    if ((rc = capture_graph(P, G, body_o, h_outer))) break;  // the solve, on cap[0..2]
+    P->st = P->cap_path;
+    // the objective pieces of the final x (launch_objective without its host copies)
+    if ((rc = launch_gather_vec(P, P->Jx, P->Px, P->r_dev + 2))) break;
+    k_combine<<<1, 1024, 0, P->st>>>(P->m, P->b, -1.0, P->part_vec, 1, P->tmpm, nullptr, nullptr, nullptr);
+    k_objective<<<1, 1024, 0, P->st>>>(P->m, P->tmpm, P->Px, P->r_dev + 2, P->scratch + 16);
+    k_path_copy_x<<<2 * P->nsm, 256, 0, P->st>>>(P->x, P->pdev, P->n);
+    k_path_end<<<1, 1, 0, P->st>>>(P->ctl, P->ev_dev, P->scratch, P->r_dev, slots_dev, P->pdev, h_path);
+    if ((e = cudaGetLastError()) != cudaSuccess) {
+      set_err("path graph capture launch: %s", cudaGetErrorString(e));
+      rc = SSNAL_ECUDA;
+      break;
+    }
+    P->pgraph_fixed = 6;  // begin, gather, combine, objective, copy, end
+  } while (false);
+  for (int d = P->cap_depth; d > 0; --d) {  // a capture left open inside capture_graph by a failure
+    cudaGraph_t tmp;
+    cudaStreamEndCapture(P->cap[d - 1], &tmp);
+  }
+  P->cap_depth = 0;
+  if (cap_open) {
+    cudaGraph_t tmp;
+    cudaError_t e = cudaStreamEndCapture(P->cap_path, &tmp);
+    if (e != cudaSuccess && rc == SSNAL_OK) {
+      set_err("path graph end capture: %s", cudaGetErrorString(e));
+      rc = SSNAL_ECUDA;
+    }
+  }
+  P->capturing = false;
+  P->st = saved;
+  P->launches = L0;
+  if (rc == SSNAL_OK) {
+    cudaError_t e = cudaGraphInstantiate(&P->pgexec, G, 0);
+    if (e != cudaSuccess) {
+      set_err("path graph instantiate: %s", cudaGetErrorString(e));
+      P->pgexec = nullptr;
+      rc = SSNAL_ECUDA;
+    } else if ((e = cudaGraphUpload(P->pgexec, P->st)) != cudaSuccess) {
+      set_err("path graph upload: %s", cudaGetErrorString(e));
+      rc = SSNAL_ECUDA;
+    }
+  }
+  if (rc) {
+    cudaGetLastError();
+    cudaGraphDestroy(G);
+    drop_path_graph(P);
+    return rc;
+  }
+  P->pgraph = G;
+  return SSNAL_OK;
 }
 
 // Graph mode: the whole Algorithm 1 loop nest is one graph launch; stats are read back with the
@@ -2176,6 +2368,11 @@ static void destroy_bufs(ssnal_en_problem* P) {
   cudaFree(P->iota);
   if (P->comm_host) cudaFreeHost(P->comm_host);
   peer_release(P);
+  drop_path_graph(P);
+  if (P->cap_path) cudaStreamDestroy(P->cap_path);
+  cudaFree(P->pdev);
+  cudaFree(P->path_l);
+  if (P->pdev_host) cudaFreeHost(P->pdev_host);
   pool_free(P->A_own);
   pool_free(P->codes_own);
   pool_free(P->tab_own);
@@ -2383,6 +2580,7 @@ int ssnal_en_set_option(ssnal_en_problem* P, const char* key, double v) {
   else if (k == "inner_tol_mode" && (v == 0 || v == 1)) P->inner_tol_mode = (int)v;
   else if (k == "carry_sigma" && (v == 0 || v == 1)) P->carry_sigma = (int)v;
   else if (k == "carry_dual" && (v == 0 || v == 1)) P->carry_dual = (int)v;
+  else if (k == "path_graph" && (v == 0 || v == 1)) P->use_path_graph = (int)v;
   else if (k == "warm_dual" && (v == 0 || v == 1)) P->warm_dual = (int)v;
   else if (k == "cg_tol" && v > 0 && v < 1) {
     P->cg_tol = v;
@@ -2466,6 +2664,7 @@ double ssnal_en_get_info(const ssnal_en_problem* P, const char* key) {
   if (k == "cg_threshold") return P->cg_threshold;
   if (k == "carry_sigma") return P->carry_sigma;
   if (k == "carry_dual") return P->carry_dual;
+  if (k == "path_graph") return P->use_path_graph;
   if (k == "warm_dual") return P->warm_dual;
   if (k == "k1_time_s") return P->k1_time;       // Σ K1 launch times timed by the hook calls (option time_k1)
   if (k == "k1_launches") return P->k1_count;
@@ -2567,16 +2766,6 @@ int ssnal_en_solve(ssnal_en_problem* P, double l1, double l2, double sigma0, dou
 // synchronisation — per-point results land in pinned slots and are completed afterwards; the
 // carried σ moves on the device (ctl.sigma_final → scratch[60] → the next point's ctl.sigma).  Other
 // modes (host-driven control, sharded handles, certify) loop over ssnal_en_solve_device.
-namespace {
-struct PathSlot {
-  DevCtl ctl;
-  EvalOut ev;
-  double scratch[64];
-  double l1, l2;
-  int warm_pass, pad;
-  int64_t launches;
-};
-}  // namespace
 
 int ssnal_en_solve_path_device(ssnal_en_problem* P, int64_t npts, const double* lambda1, const double* lambda2,
                                double sigma0, double tol, const double* x0, double* x_out, ssnal_en_stats* stats) {
@@ -2613,11 +2802,30 @@ int ssnal_en_solve_path_device(ssnal_en_problem* P, int64_t npts, const double* 
     if (rc) return rc;
   }
   if (P->path_cap < npts) {
+    drop_path_graph(P);  // it writes into the slots
     if (P->path_slots) cudaFreeHost(P->path_slots);
     P->path_slots = nullptr;
     P->path_cap = 0;
     CK(cudaHostAlloc(&P->path_slots, sizeof(PathSlot) * npts, cudaHostAllocMapped));  // kernels write results here
     P->path_cap = npts;
+  }
+  // points 1 … npts − 1 in one launch of the device-resident path graph (unsharded graph mode, the
+  // dual carried — reading R39); point 0 runs as a single solve first
+  const bool pg = P->use_path_graph && npts > 1 && P->carry_dual && !small_eligible(P) && P->use_graph &&
+                  !sharded(P);
+  if (pg) {
+    int rc0;
+    if ((rc0 = build_graph(P))) return rc0;  // also uploads the K4 output table both graphs read
+    PathSlot* slots_dev = nullptr;
+    CK(cudaHostGetDevicePointer((void**)&slots_dev, P->path_slots, 0));
+    if ((rc0 = build_path_graph(P, slots_dev))) return rc0;
+    if (P->path_lcap < npts) {
+      cudaFree(P->path_l);
+      P->path_l = nullptr;
+      P->path_lcap = 0;
+      if ((rc0 = alloc((void**)&P->path_l, (size_t)2 * npts * 8))) return rc0;
+      P->path_lcap = npts;
+    }
   }
   while ((int64_t)P->path_ev.size() < 2 * npts) {
     cudaEvent_t e;
@@ -2643,6 +2851,47 @@ int ssnal_en_solve_path_device(ssnal_en_problem* P, int64_t npts, const double* 
     have0 = P->comm_host[1] > 0;
   }
   for (int64_t i = 0; i < npts && rc == SSNAL_OK; ++i) {  // enqueue every point
+    if (pg && i == 1) {  // the rest of the path: one graph launch
+      CK(cudaMemcpyAsync(P->path_l, lambda1, npts * 8, cudaMemcpyHostToDevice, P->st));
+      CK(cudaMemcpyAsync(P->path_l + P->path_lcap, lambda2, npts * 8, cudaMemcpyHostToDevice, P->st));
+      PathDev* pd = P->pdev_host;
+      pd->l1s = P->path_l;
+      pd->l2s = P->path_l + P->path_lcap;
+      pd->xout = x_out;
+      pd->i = 1;
+      pd->npts = npts;
+      pd->carry_sigma = P->carry_sigma;
+      pd->t0 = 0;
+      DevCtl* h = &pd->tmpl;  // the settings, as solve_graph_core fills them
+      memset(h, 0, sizeof(DevCtl));
+      h->tol = tol;
+      h->sigma = sigma0;
+      h->sigma_factor = P->sigma_factor;
+      h->sigma_max = P->sigma_max;
+      h->mu = P->mu;
+      h->beta = P->beta;
+      h->max_outer = P->max_outer;
+      h->max_inner = P->max_inner;
+      h->max_bt = P->max_bt;
+      h->cg_ratio = P->cg_ratio;
+      h->cg_threshold = P->cg_threshold;
+      h->nb = P->nb;
+      h->jitter = P->jitter;
+      h->inject = P->inject_fail;
+      h->inner_tol_mode = P->inner_tol_mode;
+      h->tstamp[0] = ~0ull;
+      h->tstamp[1] = 0ull;
+      CK(cudaMemcpyAsync(P->pdev, pd, sizeof(PathDev), cudaMemcpyHostToDevice, P->st));
+      CK(cudaGraphLaunch(P->pgexec, P->st));
+      for (int64_t q = 1; q < npts; ++q) {
+        slot[q].l1 = lambda1[q];
+        slot[q].l2 = lambda2[q];
+        slot[q].warm_pass = 0;  // R39: no warm-start pass
+        slot[q].launches = P->pgraph_fixed;
+        k1_beg[q] = P->k1_pending.size();
+      }
+      break;
+    }
     P->ctl_host = &slot[i].ctl;
     P->ev_out_host = &slot[i].ev;
     P->scratch_host = slot[i].scratch;
@@ -2707,7 +2956,11 @@ int ssnal_en_solve_path_device(ssnal_en_problem* P, int64_t npts, const double* 
     finish_stats(P, &S[i]);
     S[i].primal_viol = NAN;
     float ms = 0;
-    cudaEventElapsedTime(&ms, P->path_ev[2 * i], P->path_ev[2 * i + 1]);
+    if (pg && i > 0) {  // in-kernel stamps of the path graph (events cannot sit inside its loop)
+      ms = (float)((double)(slot[i].t1 - slot[i].t0) * 1e-6);
+    } else {
+      cudaEventElapsedTime(&ms, P->path_ev[2 * i], P->path_ev[2 * i + 1]);
+    }
     S[i].time_device_s = ms * 1e-3;
     S[i].time_total_s = wall / npts;  // the host time of the whole path, shared evenly
     S[i].kernel_launches = P->launches;
