@@ -609,7 +609,7 @@ template <class Acc>
 __global__ void __launch_bounds__(256, 2)
     k_gram_sk(const Acc A, int64_t m, const int32_t* __restrict__ J, double* __restrict__ M,
               const double* __restrict__ g, GramFusedArgs ga, const DirGeo* geo, int only, double* __restrict__ Pt,
-              unsigned* __restrict__ cnt, int minch) {
+              unsigned* __restrict__ cnt, int minch, const int64_t* __restrict__ r_loc = nullptr, int raw = 0) {
   __shared__ __align__(16) double sm[2 * kGramSmem];
   __shared__ bool last;
   if (geo) {
@@ -623,6 +623,14 @@ __global__ void __launch_bounds__(256, 2)
     ga.diag = geo->diag;
     ga.mult = geo->mult;
     ga.jit = geo->jit;
+  }
+  if (raw) {  // §8(f3): the raw local partial Gram (m × m, ld = m) of a sharded rank's own columns
+    if (r_loc) ga.r = *r_loc;
+    ga.mult = 1.0;
+    ga.diag = 0.0;
+    ga.jit = 0.0;
+    ga.ld = ga.nout;
+    g = nullptr;
   }
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gq = lane >> 2, t = lane & 3, wr = warp >> 1, wc = warp & 1;

@@ -269,16 +269,13 @@ __global__ void k_peer_reduce_big(PeerComm pc, double* __restrict__ buf, int64_t
 //         through AccA{big, m} and idx exactly as from a packed r × m buffer (counts that do not add
 //         up to the global r set err = 2).
 // m × m branch (r ≥ m, Eq. (18)) — the GEMM → all-gather fusion of the partial Grams:
-//   dir1: the local partial Gram A_J A_Jᵀ of this rank's active columns (split-K slices into W; ns
-//         from the LOCAL r, as the host-driven sharded path);
-//   dir2: its slices summed (k_gram_reduce's order and epilogue with diag 0, mult 1) and deposited
-//         into big slot [rank] of every rank; the last CTA signals;
+//   k_gram_sk (raw mode, a node of its own): the local partial Gram A_J A_Jᵀ of this rank's active
+//         columns into W (m × m, ld = m), as the host-driven sharded path forms it;
+//   dir2: the partial deposited into big slot [rank] of every rank; the last CTA signals;
 //   k_peer_gram_sum (below) then forms the Newton matrix on every rank.
 template <class Acc>
 __global__ void __launch_bounds__(256) k_peer_dir1(PeerComm pc, const Acc A, int64_t m, const int32_t* __restrict__ J,
-                                                   const int64_t* __restrict__ r_dev, double* __restrict__ W,
-                                                   const DirGeo* geo, int nsm, int wsplits) {
-  __shared__ double sA[kGramSmem], sB[kGramSmem];
+                                                   const int64_t* __restrict__ r_dev, const DirGeo* geo) {
   const int br = geo->branch;
   const int64_t r = *r_dev;
   if (br == 1) {
@@ -292,13 +289,10 @@ __global__ void __launch_bounds__(256) k_peer_dir1(PeerComm pc, const Acc A, int
     if (blockIdx.x == 0 && threadIdx.x == 0)
       for (int q = 0; q < pc.size; ++q) peer_cnt(pc, q)[pc.rank] = r;
     peer_last_cta_signal(pc);
-  } else if (br == 2) {
-    const int tiles = gram_tiles(m), ns = gram_splits(nsm, tiles, r, wsplits);
-    gram_body<false>(A, m, J, r, W, nullptr, tiles, ns, sA, sB);
   }
 }
-__global__ void k_peer_dir2(PeerComm pc, const double* __restrict__ W, const int64_t* __restrict__ r_dev, int64_t m,
-                            const DirGeo* geo, int nsm, int wsplits, int32_t* __restrict__ idx) {
+__global__ void k_peer_dir2(PeerComm pc, const double* __restrict__ W, int64_t m, const DirGeo* geo,
+                            int32_t* __restrict__ idx) {
   __shared__ int64_t off[kPeerMaxRanks + 1];
   const int br = geo->branch;
   if (br == 1) {
@@ -315,14 +309,11 @@ __global__ void k_peer_dir2(PeerComm pc, const double* __restrict__ W, const int
       for (int64_t i = threadIdx.x; i < off[q + 1] - off[q] && off[q] + i < rg; i += blockDim.x)
         idx[off[q] + i] = (int32_t)(q * pc.ccap + i);
   } else if (br == 2) {
-    const int ns = gram_splits(nsm, gram_tiles(m), *r_dev, wsplits);
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m * m;
          e += (int64_t)gridDim.x * blockDim.x) {
       const int64_t i = e % m, j = e / m;
       if (i < j) continue;
-      double s = 0.0;
-      for (int q = 0; q < ns; ++q) s += W[(size_t)q * m * m + e];
-      const double v = s + 0.0;  // k_gram_reduce with diag = 0: + 0.0 on every stored entry
+      const double v = W[e];  // the raw partial (lower part) of k_gram_sk
       for (int q = 0; q < pc.size; ++q) peer_big(pc, q, pc.rank)[e] = v;
     }
     peer_last_cta_signal(pc);

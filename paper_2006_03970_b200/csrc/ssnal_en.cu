@@ -1263,6 +1263,29 @@ unsigned gram_fused_grid(ssnal_en_problem* P, int tiles) {
   return (unsigned)(ncl * kGramCS);
 }
 
+// §8(f3): a sharded rank's raw local partial Gram A_J A_Jᵀ (m × m, ld = m, lower) into out by k_gram_sk;
+// graph mode: predicated on the global branch 2, the local r from r_loc.
+template <class Acc>
+int launch_gram_raw(ssnal_en_problem* P, const Acc& acc, const int32_t* J, int64_t r_host, const int64_t* r_loc,
+                    double* out, const DirGeo* geo) {
+  const int64_t m = P->m;
+  const GramFusedArgs gfa{2, r_host, m, m, gram_tiles(m), (int)m, 0.0, 1.0, 0.0};
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(P->gsk_grid);
+  cfg.blockDim = dim3(256);
+  cfg.stream = P->st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, k_gram_sk<Acc>, acc, m, J, out, (const double*)nullptr, gfa, geo, 2, P->gsk_part,
+                        P->gsk_cnt, P->gsk_minch, r_loc, 1));
+  P->launches++;
+  CKL();
+  return SSNAL_OK;
+}
+
 // K3 of the Newton systems (Eq. (18)/(19)): k_gram_sk (one cooperative round over the whole GPU) or,
 // with option gram_sk = 0, k_gram_fused (8-CTA clusters per tile).  geo: graph mode (worst-case
 // grid); only > 0: one branch alone.
@@ -1284,7 +1307,7 @@ int launch_gram_one(ssnal_en_problem* P, const Acc& acc, const int32_t* J, const
     cfg.attrs = at;
     cfg.numAttrs = 1;
     CK(cudaLaunchKernelEx(&cfg, k_gram_sk<Acc>, acc, P->m, J, P->Mmat, g, gfa, geo, only, P->gsk_part, P->gsk_cnt,
-                          P->gsk_minch));
+                          P->gsk_minch, (const int64_t*)nullptr, 0));
   }
   P->launches++;
   CKL();
@@ -1380,14 +1403,10 @@ int newton_direction_sharded(ssnal_en_problem* P, const int32_t* J, int64_t rg, 
     return SSNAL_OK;
   }
   *branch = 2;
-  const int tiles = gram_tiles(m), ns = gram_splits(P->nsm, tiles, rl, P->W_splits);
-  with_acc(P, [&](auto acc) {
-    k_gram<false><<<gram_grid(P, tiles * ns), 256, 0, P->st>>>(acc, m, J, rl, P->W, nullptr, tiles, ns, nullptr);
-    return 0;
-  });
   CK(cudaMemsetAsync(P->xbuf, 0, (size_t)m * m * 8, P->st));
-  k_gram_reduce<<<reduce_grid(P, m * m), 256, 0, P->st>>>(P->W, ns, m, m, 0.0, 1.0, P->xbuf, m, nullptr, nullptr, 0, 0.0);
-  P->launches += 2;
+  // the raw local partial Gram (k_gram_sk: one cooperative round) straight into the exchange buffer
+  if ((rc = with_acc(P, [&](auto acc) { return launch_gram_raw(P, acc, J, rl, nullptr, P->xbuf, nullptr); })))
+    return rc;
   if ((rc = comm_allreduce(P, P->xbuf, m * m, 0))) return rc;
   k_gram_reduce<<<reduce_grid(P, m * m), 256, 0, P->st>>>(P->xbuf, 1, m, m, 1.0, kappa, P->Mmat, m + 1, g, nullptr, 0,
                                                           jit);
@@ -1455,15 +1474,16 @@ int newton_direction_graph_peer(ssnal_en_problem* P) {
   const DirGeo* geo = &P->ctl->geo;
   const AccA ga{(const double*)(P->pc.base[P->pc.rank] + peer_big_off(P->pc.size, P->pc.ss)), m};
   const unsigned gsm = 2 * P->nsm;
-  with_acc(P, [&](auto acc) {
-    k_peer_dir1<<<gsm, 256, 0, P->st>>>(P->pc, acc, m, P->J[0], P->r_dev + 0, P->W, geo, P->nsm, P->W_splits);
-    return 0;
+  int rc = with_acc(P, [&](auto acc) {
+    k_peer_dir1<<<gsm, 256, 0, P->st>>>(P->pc, acc, m, P->J[0], P->r_dev + 0, geo);  // SMW: the all-gather
+    P->launches++;
+    return launch_gram_raw(P, acc, P->J[0], 0, P->r_dev + 0, P->W, geo);  // m × m: the local partial Gram
   });
-  k_peer_dir2<<<reduce_grid(P, m * m), 256, 0, P->st>>>(P->pc, P->W, P->r_dev + 0, m, geo, P->nsm, P->W_splits,
-                                                        P->peer_idx);
-  P->launches += 2;
+  if (rc) return rc;
+  k_peer_dir2<<<reduce_grid(P, m * m), 256, 0, P->st>>>(P->pc, P->W, m, geo, P->peer_idx);
+  P->launches++;
   // SMW on the gathered columns (the K3 launch of the unsharded graph, restricted to branch 1)
-  int rc = launch_gram(P, ga, P->peer_idx, P->g[0], GramFusedArgs{}, geo, 1);
+  rc = launch_gram(P, ga, P->peer_idx, P->g[0], GramFusedArgs{}, geo, 1);
   if (rc) return rc;
   k_peer_gram_sum<<<reduce_grid(P, m * m), 256, 0, P->st>>>(P->pc, m, P->Mmat, P->g[0], geo, 0.0, 0, 0.0);
   P->launches++;
@@ -1580,7 +1600,9 @@ int init_point(ssnal_en_problem* P, int have_x0, ssnal_en_stats* S, int64_t* rx,
 
 // Objective pieces at the final x (both modes): resid = A x − b from the support (Jx, Px, r_dev[2])
 // → scratch_host[16..19] = [½‖resid‖², Σ|x|, Σx², nnz], scratch_host[20] = |supp x0| (after a sync).
-int launch_objective(ssnal_en_problem* P) {
+// The objective pieces' kernels (and, sharded, their exchanges) without the host copies: also
+// captured into the path graph.
+int objective_kernels(ssnal_en_problem* P) {
   int rc;
   if ((rc = sharded(P) ? launch_gather_dev(P, P->Jx, P->Px, P->r_dev + 2)
                        : launch_gather_vec(P, P->Jx, P->Px, P->r_dev + 2)))
@@ -1602,6 +1624,12 @@ int launch_objective(ssnal_en_problem* P) {
     P->launches++;
     CKL();
   }
+  return SSNAL_OK;
+}
+
+int launch_objective(ssnal_en_problem* P) {
+  int rc = objective_kernels(P);
+  if (rc) return rc;
   CK(cudaMemcpyAsync(P->scratch_host + 16, P->scratch + 16, 4 * 8, cudaMemcpyDeviceToHost, P->st));
   CK(cudaMemcpyAsync(P->scratch_host + 20, P->r_dev + 4, 8, cudaMemcpyDeviceToHost, P->st));
   return SSNAL_OK;
@@ -1993,8 +2021,8 @@ void drop_graph(ssnal_en_problem* P) {
 // The device-resident λ path: WHILE (point < npts) { k_path_begin; the solve (the solve graph's
 // nested WHILE loops, captured again into this body); the objective pieces; x → x_out[point];
 // k_path_end } — points 1 … npts − 1 of a warm-started path in one launch, no host round trip
-// between points (the host only reads the per-point slots after the path).  Unsharded, multi-kernel
-// graph mode, the dual and x carried (reading R39).
+// between points (the host only reads the per-point slots after the path).  Multi-kernel graph mode
+// (unsharded or peer-sharded), the dual and x carried (reading R39).
 int build_path_graph(ssnal_en_problem* P, PathSlot* slots_dev) {
   if (P->pgexec) return SSNAL_OK;
   int rc;
@@ -2046,10 +2074,11 @@ int build_path_graph(ssnal_en_problem* P, PathSlot* slots_dev) {
     if ((rc = add_while(P->cap_path, h_outer, &body_o))) break;
     if ((rc = capture_graph(P, G, body_o, h_outer))) break;  // the solve, on cap[0..2]
     P->st = P->cap_path;
-    // the objective pieces of the final x (launch_objective without its host copies)
-    if ((rc = launch_gather_vec(P, P->Jx, P->Px, P->r_dev + 2))) break;
-    k_combine<<<1, 1024, 0, P->st>>>(P->m, P->b, -1.0, P->part_vec, 1, P->tmpm, nullptr, nullptr, nullptr);
-    k_objective<<<1, 1024, 0, P->st>>>(P->m, P->tmpm, P->Px, P->r_dev + 2, P->scratch + 16);
+    // the objective pieces of the final x (launch_objective without its host copies; peer-sharded:
+    // with its exchanges, all kernels)
+    const int64_t L1 = P->launches;
+    if ((rc = objective_kernels(P))) break;
+    const int nobj = (int)(P->launches - L1);
     k_path_copy_x<<<2 * P->nsm, 256, 0, P->st>>>(P->x, P->pdev, P->n);
     k_path_end<<<1, 1, 0, P->st>>>(P->ctl, P->ev_dev, P->scratch, P->r_dev, slots_dev, P->pdev, h_path);
     if ((e = cudaGetLastError()) != cudaSuccess) {
@@ -2057,7 +2086,7 @@ int build_path_graph(ssnal_en_problem* P, PathSlot* slots_dev) {
       rc = SSNAL_ECUDA;
       break;
     }
-    P->pgraph_fixed = 6;  // begin, gather, combine, objective, copy, end
+    P->pgraph_fixed = 3 + nobj;  // begin, the objective's kernels, copy, end
   } while (false);
   for (int d = P->cap_depth; d > 0; --d) {  // a capture left open inside capture_graph by a failure
     cudaGraph_t tmp;
@@ -2812,7 +2841,7 @@ int ssnal_en_solve_path_device(ssnal_en_problem* P, int64_t npts, const double* 
   // points 1 … npts − 1 in one launch of the device-resident path graph (unsharded graph mode, the
   // dual carried — reading R39); point 0 runs as a single solve first
   const bool pg = P->use_path_graph && npts > 1 && P->carry_dual && !small_eligible(P) && P->use_graph &&
-                  !sharded(P);
+                  (!sharded(P) || P->peer);
   if (pg) {
     int rc0;
     if ((rc0 = build_graph(P))) return rc0;  // also uploads the K4 output table both graphs read
