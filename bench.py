@@ -294,6 +294,7 @@ def bench_ours(args, rank, world, local_rank):
     launches = 0
     dev_sum = 0.0
     last_stats = None
+    reuses0 = P.info("atb_reuses")
     with ClockSampler(local_rank) as clk:
         evs[0].record(stream)
         for k in range(args.steps):
@@ -308,6 +309,7 @@ def bench_ours(args, rank, world, local_rank):
     if world > 1:
         dist.barrier()
     P.set_option("time_k1", 0)
+    atb_reuses = (P.info("atb_reuses") - reuses0) / max(args.steps, 1)
     per_step = [evs[k].elapsed_time(evs[k + 1]) * 1e-3 for k in range(args.steps)]
     elapsed = sum(per_step)
     t_step = max_over_ranks(elapsed / args.steps)
@@ -410,6 +412,12 @@ def bench_ours(args, rank, world, local_rank):
                    "path_dual": ("each point after the first starts from the previous point's final y, w = A^T y "
                                  "(reading R39, P:236-246 + P:409-411): no A^T pass for the warm start")
                                 if cfg.path else None,
+                   "reuse_atb": ((f"on (reading R40): {atb_reuses:g} of the step's cold solves took their first trial "
+                                  "product A^T(y0 + d) = -A^T b (x0 = 0 => d = -b exactly) from the A^T b kept by create's "
+                                  "lambda_max pass instead of streaming A; bitwise the streamed result (tests/"
+                                  "test_gpu_reuse.py); gated on the first active set being <= n/32; those launches "
+                                  "are not counted in roofline.launches; --opt reuse_atb=0 times without it")
+                                 if P.info("reuse_atb") == 1 else "off"),
                    "newton_strategy": ("exact (Eq. 18/19); CG when min(m, r) > 1e4 (P:379)" if args.cg_ratio == 0
                                        else f"CG (K6) when r > {args.cg_ratio:g} m, else exact (Eq. 18/19)")},
         "step_times": step_summary(per_step),

@@ -51,7 +51,8 @@ typedef struct {
   int32_t newton_iters;    /* semi-smooth Newton steps, summed over outer iterations      */
   int32_t psi_evals;       /* ψ evaluations (Armijo trials incl. backtracks)              */
   int32_t backtracks;      /* step halvings                                               */
-  int32_t aty_passes;      /* full passes over A (K1 launches)                            */
+  int32_t aty_passes;      /* Aᵀy products at new points (K1 launches); with reuse_atb=1 the first
+                              of a cold solve reads Aᵀb kept by create instead of A        */
   int32_t branch_steps[4]; /* Newton steps with r = 0, 0 < r < m (Eq. 19), r ≥ m (Eq. 18), CG (R32) */
   int32_t line_search_stalled; /* max_backtracks reached at least once (R30)              */
   int32_t cg_iters;        /* conjugate-gradient iterations, summed over CG steps             */
@@ -114,6 +115,10 @@ double ssnal_en_lambda_max_l1(const ssnal_en_problem* p);
  *   carry_sigma=1 (ssnal_en_solve_path_device: point i > 0 starts at point i − 1's sigma_final
  *     instead of σ0 — reading R38 of P:411 "usually SsNAL-EN converges in just one iteration";
  *     0: every point restarts at σ0),
+ *   reuse_atb=1 (fp64 storage; reading R40: create keeps the product Aᵀb of its λmax pass, 8n bytes;
+ *     a cold solve — x0 = NULL, so y0 = 0 and the first Newton direction is d = −b exactly —
+ *     takes Aᵀ(y0 + d) = −Aᵀb from it, bitwise what the streaming pass computes, instead of
+ *     reading A once more; ssnal_en_get_info "atb_reuses" counts such solves; 0: always stream A),
  *   small=1 (m ≤ 64 and n ≤ 1024, fp64 storage, unsharded, no CG strategy: the whole solve is ONE
  *     kernel launch — same iteration and statistics, reduction orders differ; 0: the multi-kernel
  *     graph / host paths), small_cluster=1 (that launch is k_small_cl, one 16-CTA cluster with A

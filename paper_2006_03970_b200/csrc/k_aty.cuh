@@ -56,6 +56,13 @@ struct K1Params {
   const double* tab;    // n × 3: decoded value of codes 0, 1, 2 for each column
   int64_t cstride;      // bytes per column (multiple of 16)
   uint32_t bfr_off;     // K1g: byte offset of the shared B-fragment table (32 k-blocks × 32 lanes × 8 B)
+  // Reuse of Aᵀb (option reuse_atb, DESIGN R40; fp64 storage): the first Newton step of a cold start
+  // (x0 = 0, y0 = 0 ⇒ d = −b exactly) evaluates ψ at y = −b, and Aᵀ(−b) = −(Aᵀb) bitwise, the product
+  // ssnal_en_create formed for λmax.  When atb != nullptr and (cache_on, or *cache_flag != 0 in graph
+  // mode) the launch takes w = −atb instead of streaming A: same outputs, bit for bit.
+  const double* atb;    // n: Aᵀb kept by create (nullable)
+  const int* cache_flag;  // graph mode: DevCtl::cold_first
+  int cache_on;         // host-driven mode: this launch is the cold start's first trial
 };
 
 // Reduce-scatter of 8 per-lane partial sums a[0..7] across the warp: afterwards every
@@ -90,7 +97,7 @@ SSN_DEV double reduce8(double (&a)[8], int lane) {
 // rows rv[warp][0..m) when fused): fixed-order reductions of the partial scalars and rows, then
 // the ordered compaction of this CTA's active columns from the bitmap (P recomputed from w).
 SSN_DEV void k1_cta_end(const K1Params& p, const Scal& sc, double* ring, int* sh, int64_t c_lo, int64_t c_hi,
-                        double s0, double s1, double s2, double s3, bool any_active) {
+                        double s0, double s1, double s2, double s3, bool any_active, bool stamp = true) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t m = p.m;
   double* rv = ring;                       // K1_NWC x m
@@ -124,7 +131,7 @@ SSN_DEV void k1_cta_end(const K1Params& p, const Scal& sc, double* ring, int* sh
   }
   // kernel-duration stamp: all consumer warps of this CTA are past their last write
   auto stamp_end = [&]() {
-    if (p.tstamp) {
+    if (p.tstamp && stamp) {
       named_bar_sync(1, K1_NWC * 32);
       if (tid == 0) atomicMax(p.tstamp + 1, global_ns());
     }
@@ -189,6 +196,124 @@ SSN_DEV void k1_cta_end(const K1Params& p, const Scal& sc, double* ring, int* sh
   stamp_end();
 }
 
+// K1 served from the kept product Aᵀb (K1Params::atb): w_i = −atb_i instead of the dot product, the
+// same epilogue on the same (warp, lane, order) assignment of columns as the streaming kernel, the
+// ∇ψ partial rows from the active columns read straight from global memory — every output (w, mask,
+// segments, partial scalars and rows) is bitwise what the streaming launch at y = −b writes.  No ring,
+// no producer; kD groups of (w, x) loads in flight per warp.  Not stamped (it is not a pass over A).
+template <int MR>
+SSN_DEV void k1_cached(const K1Params& p, double* ring, int* sh, int64_t c_lo, int64_t c_hi) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == K1_NWC) return;
+  constexpr int kD = 4;
+  const int C = p.C;
+  const int64_t m = p.m;
+  const int64_t ntiles = (c_hi - c_lo + C - 1) / C;
+  const int gpt = C / K1_GRP;  // groups per tile
+  double gacc[MR];
+#pragma unroll
+  for (int t = 0; t < MR; ++t) gacc[t] = 0.0;
+  const Scal sc = p.scp ? *p.scp : p.sc;
+  const bool leader = (lane & 3) == 0;
+  const int gcol = lane >> 2;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  bool any_active = false;
+  const int64_t ntw = ntiles > warp ? (ntiles - warp + K1_NWC - 1) / K1_NWC : 0;  // this warp's tiles
+  const int64_t ng = ntw * gpt;                                                    // and groups (tile-major)
+  for (int64_t q0 = 0; q0 < ng; q0 += kD) {
+    double wv[kD], xv[kD];
+    int64_t cc[kD];   // global column of this lane in group u, −1: not a column
+    int64_t gb[kD];   // first global column of group u, −1: the group does not exist
+#pragma unroll
+    for (int u = 0; u < kD; ++u) {
+      const int64_t q = q0 + u;
+      cc[u] = gb[u] = -1;
+      wv[u] = xv[u] = 0.0;
+      if (q < ng) {
+        const int64_t it = warp + (int64_t)K1_NWC * (q / gpt);
+        const int g = (int)(q % gpt);
+        const int64_t c0 = c_lo + it * C;
+        const int nc = (int)((c_hi - c0) < C ? (c_hi - c0) : C);
+        if (g * K1_GRP < nc) {
+          gb[u] = c0 + (int64_t)g * K1_GRP;
+          if (g * K1_GRP + gcol < nc) {
+            cc[u] = gb[u] + gcol;
+            wv[u] = -__ldg(p.atb + cc[u]);
+            if (p.fused) xv[u] = __ldg(p.x + cc[u]);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kD; ++u) {
+      if (gb[u] < 0) continue;  // warp-uniform
+      const bool valid = cc[u] >= 0;
+      const double w = wv[u];
+      if (p.fused) {
+        bool act = false;
+        double P = 0.0;
+        if (valid) {
+          const double xi = xv[u];
+          const double tt = __dsub_rn(xi, __dmul_rn(sc.sigma, w));
+          act = fabs(tt) > sc.thr;
+          const double e = __dsub_rn(fabs(w), sc.l1);
+          if (xi == 0.0 && !act) {
+            if (leader) {
+              s2 = __dadd_rn(s2, __dmul_rn(w, w));
+              if (e > 0.0) s3 = __dadd_rn(s3, __dmul_rn(e, e));
+            }
+          } else {
+            P = prox_en(tt, sc.thr, sc.den);
+            const double dx = __dsub_rn(xi, P);
+            const double z = __dsub_rn(__ddiv_rn(dx, sc.sigma), w);
+            if (leader) {
+              s0 = __dadd_rn(s0, __dmul_rn(P, P));
+              s1 = __dadd_rn(s1, __dmul_rn(dx, dx));
+              s2 = __dadd_rn(s2, __dmul_rn(z, z));
+              if (e > 0.0) s3 = __dadd_rn(s3, __dmul_rn(e, e));
+            }
+          }
+          if (leader) p.w_out[cc[u]] = w;
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, act && leader);
+        unsigned m8 = 0;
+#pragma unroll
+        for (int q = 0; q < K1_GRP; ++q) m8 |= ((bal >> (4 * q)) & 1u) << q;
+        if (lane == 0) p.mask[gb[u] >> 3] = (uint8_t)m8;
+        if (m8) {
+          any_active = true;
+          unsigned mm = m8;
+          while (mm) {
+            const int q = __ffs(mm) - 1;
+            mm &= mm - 1;
+            const double Pq = __shfl_sync(0xffffffffu, P, 4 * q);
+            const double* colq = p.A + (gb[u] + q) * m;
+#pragma unroll
+            for (int t = 0; t < MR; ++t) {
+              const int64_t row = lane + 32 * t;
+              if (row < m) gacc[t] = fma(Pq, __ldg(colq + row), gacc[t]);
+            }
+          }
+        }
+      } else {
+        if (valid) {
+          s0 = fmax(s0, fabs(w));
+          if (leader) p.w_out[cc[u]] = w;
+        }
+      }
+    }
+  }
+  named_bar_sync(1, K1_NWC * 32);
+  if (p.fused && p.part_vec) {
+#pragma unroll
+    for (int t = 0; t < MR; ++t) {
+      const int64_t row = lane + 32 * t;
+      if (row < m) ring[(size_t)warp * m + row] = gacc[t];
+    }
+  }
+  k1_cta_end(p, sc, ring, sh, c_lo, c_hi, s0, s1, s2, s3, any_active, false);
+}
+
 template <int MR>
 __global__ void __launch_bounds__(K1_THREADS, 1) k1_aty_fused(const K1Params p) {
   extern __shared__ __align__(128) unsigned char smem[];
@@ -205,6 +330,10 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_aty_fused(const K1Params p) 
   int64_t c_lo, c_hi;
   cta_cols(blockIdx.x, gridDim.x, p.T, C, p.n, &c_lo, &c_hi);
   const int64_t ntiles = (c_hi - c_lo + C - 1) / C;
+  if (p.atb && (p.cache_on || (p.cache_flag && *p.cache_flag))) {  // R40: w = −Aᵀb kept by create
+    k1_cached<MR>(p, ring, sh, c_lo, c_hi);
+    return;
+  }
 
   if (threadIdx.x == 0) {
     if (p.tstamp) atomicMin(p.tstamp, global_ns());
@@ -1184,6 +1313,35 @@ __global__ void __cluster_dims__(kEvalCS, 1, 1) __launch_bounds__(K5_THREADS) k_
 }
 
 // max over G plain-mode partials (λmax = ‖Aᵀb‖∞)
+// R40 gate: the reused-Aᵀb launch of K1 reads the active columns of A from global memory for the ∇ψ
+// partial rows, so it only pays while the first trial's active set {i : |Aᵀb|_i > λ1} (x = 0) is small.
+// Counts it and sets *flag = (count ≤ limit).  A heuristic only: both K1 modes write the same bits.
+// cnt[0] = count, cnt[1] = ticket; both zero on entry and on exit.
+__global__ void __launch_bounds__(256) k_atb_gate(const double* __restrict__ atb, int64_t n, double l1, int64_t limit,
+                                                  unsigned long long* cnt, int* flag, int* flag2) {
+  unsigned long long c = 0;
+  for (int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x; i < n; i += (int64_t)gridDim.x * 256)
+    c += fabs(atb[i]) > l1;
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  __shared__ unsigned long long sw[8];
+  if ((threadIdx.x & 31) == 0) sw[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int w = 0; w < 8; ++w) t += sw[w];
+    atomicAdd(cnt, t);
+    __threadfence();
+    if (atomicAdd(cnt + 1, 1ull) == gridDim.x - 1) {
+      const unsigned long long tot = atomicAdd(cnt, 0ull);
+      const int f = tot <= (unsigned long long)limit;
+      *flag = f;
+      if (flag2) *flag2 = f;
+      cnt[0] = 0ull;
+      cnt[1] = 0ull;
+    }
+  }
+}
+
 __global__ void k_max_partials(const double* part_scal, int G, double* out) {
   if (threadIdx.x == 0 && blockIdx.x == 0) {
     double v = 0.0;

@@ -463,6 +463,17 @@ struct ssnal_en_problem {
   // a single warm-started solve (the handle's y, w from its previous solve instead of y0 = A x0 − b)
   int carry_dual = 1;
   int warm_dual = 0;
+  // option reuse_atb (reading R40): create keeps Aᵀb (the λmax pass) in atb; the first Newton step of a
+  // cold start (x0 = 0 ⇒ y0 = 0, d = −b exactly) takes Aᵀ(y0 + d) = −Aᵀb from it — bitwise what the
+  // streaming K1 launch writes — instead of a pass over A.  fp64 storage only (atb == nullptr otherwise).
+  int reuse_atb = 1;
+  double* atb = nullptr;
+  unsigned long long* gate_cnt = nullptr;  // k_atb_gate scratch (count, ticket), kept zero
+  int* gate_flag_host = nullptr;           // mapped pinned: the gate's decision (host-driven control, statistics)
+  int* gate_flag_dev = nullptr;            // its device alias
+  bool stat_cold_first = false;            // the pending solve ran the gate (finish_stats counts atb_reuses)
+  double reuse_frac = 1.0 / 32;            // gate: reuse while #{|Aᵀb|_i > λ1} ≤ reuse_frac · n
+  int64_t atb_reuses = 0;  // cold solves started with the first trial served from atb (get_info "atb_reuses")
   // device-resident λ path (option path_graph): points 1 … npts − 1 of ssnal_en_solve_path_device
   // in ONE launch of a graph whose WHILE loop runs the solve graph's body once per point
   int use_path_graph = 1;
@@ -712,6 +723,8 @@ int allocate(ssnal_en_problem* P) {
   const int64_t m = P->m, n = P->n;
   Arena d;
   for (int i = 0; i < 3; ++i) d.add((void**)&P->w[i], n * 8);
+  if (!P->fmt) d.add((void**)&P->atb, n * 8);
+  d.add((void**)&P->gate_cnt, 64);
   d.add((void**)&P->x, n * 8);
   d.add((void**)&P->seg_idx, n * 4);
   d.add((void**)&P->mask, n / 8 + 64);
@@ -758,16 +771,19 @@ int allocate(ssnal_en_problem* P) {
   }
   d.assign((char*)P->arena);
   CK(cudaMemset(P->ticket, 0, 64));
+  CK(cudaMemset(P->gate_cnt, 0, 64));
   CK(cudaMemset(P->gsk_cnt, 0, (size_t)(2 * gsk_tiles + 64) * 4));
   Arena h;
   h.add((void**)&P->ev_host, sizeof(EvalOut) * 4);
   h.add((void**)&P->scratch_host, 64 * 8);
   h.add((void**)&P->ctl_host, sizeof(DevCtl));
   h.add((void**)&P->ev_out_host, sizeof(EvalOut));
+  h.add((void**)&P->gate_flag_host, 64);
   CK(cudaHostAlloc(&P->arena_h, h.total, cudaHostAllocMapped));
   memset(P->arena_h, 0, h.total);
   h.assign((char*)P->arena_h);
   CK(cudaHostGetDevicePointer((void**)&P->ev_host_dev, P->ev_host, 0));
+  CK(cudaHostGetDevicePointer((void**)&P->gate_flag_dev, P->gate_flag_host, 0));
   return SSNAL_OK;
 }
 
@@ -806,7 +822,8 @@ void harvest_k1(ssnal_en_problem* P) {  // call after a stream sync
 
 // K1 at y (device, m).  fused=0: plain w = Aᵀy into w_out (+ per-CTA max|w|).
 int launch_k1(ssnal_en_problem* P, const double* y, const double* x, const Scal& sc, int fused, double* w_out,
-              const Scal* scp = nullptr, unsigned long long* tstamp = nullptr) {
+              const Scal* scp = nullptr, unsigned long long* tstamp = nullptr, int cached = 0,
+              const int* cache_flag = nullptr) {
   K1Params k;
   k.A = P->A;
   k.m = P->m;
@@ -833,8 +850,12 @@ int launch_k1(ssnal_en_problem* P, const double* y, const double* x, const Scal&
   k.tab = P->tab;
   k.cstride = P->cstride;
   k.bfr_off = P->k1_bfr_off;
+  const bool can_reuse = P->atb && P->reuse_atb && !P->fmt;  // R40
+  k.atb = can_reuse && (cached || cache_flag) ? P->atb : nullptr;
+  k.cache_on = can_reuse && cached;
+  k.cache_flag = can_reuse ? cache_flag : nullptr;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
-  const bool ev_time = P->time_k1 && !P->capturing;
+  const bool ev_time = P->time_k1 && !P->capturing && !k.cache_on;
   if (ev_time) {
     e0 = take_event(P);
     e1 = take_event(P);
@@ -1647,6 +1668,16 @@ int solve_core(ssnal_en_problem* P, double l1, double l2, double sigma0, double 
   int64_t rx = 0;
   CK(cudaMemsetAsync(&P->ctl->cg_iters, 0, sizeof(int), P->st));
   if ((rc = init_point(P, have_x0, S, &rx, keep_dual))) return rc;
+  int reuse_first = 0;  // R40: the first trial from the kept Aᵀb while its active set is small
+  if (!have_x0 && !keep_dual && P->atb && P->reuse_atb) {
+    k_atb_gate<<<2 * P->nsm, 256, 0, P->st>>>(P->atb, P->n, l1, (int64_t)(P->reuse_frac * (double)P->n), P->gate_cnt,
+                                               P->gate_flag_dev, nullptr);
+    P->launches++;
+    CKL();
+    CK(cudaStreamSynchronize(P->st));
+    reuse_first = *(volatile int*)P->gate_flag_host;
+    P->atb_reuses += reuse_first;
+  }
 
   double sigma = sigma0;
   int converged = 0, numeric = 0, k;
@@ -1681,7 +1712,9 @@ int solve_core(ssnal_en_problem* P, double l1, double l2, double sigma0, double 
                                  retry ? P->jitter : 0.0, P->r_dev + cur)))
         return rc;
       S->branch_steps[br]++;
-      if ((rc = launch_k1(P, P->y[tr], P->x, sc, 1, P->w[wtr]))) return rc;
+      // R40: the first trial of a cold start is at y = −b exactly: w = −Aᵀb kept by create
+      const int cold_first = reuse_first && k == 0 && j == 0 && S->newton_iters == 0;
+      if ((rc = launch_k1(P, P->y[tr], P->x, sc, 1, P->w[wtr], nullptr, nullptr, cold_first))) return rc;
       S->aty_passes++;
       if ((rc = launch_finalize(P, P->J[tr], P->PJ[tr], P->r_dev + tr))) return rc;
       if ((rc = eval_g(P, P->y[tr], sc, 1, P->cta_cnt, P->G, P->g[tr], P->r_dev + tr, 1, gd_dev,
@@ -1900,7 +1933,7 @@ int capture_graph(ssnal_en_problem* P, cudaGraph_t G, cudaGraph_t body_pre = nul
     CK(cudaGraphConditionalHandleCreate(&h_bt, body_i, 0, 0));
     L = P->launches;
     if ((rc = newton_direction_graph(P))) return rc;
-    if ((rc = launch_k1(P, P->y[1], P->x, none, 1, P->w[1], &C->sc, C->tstamp))) return rc;
+    if ((rc = launch_k1(P, P->y[1], P->x, none, 1, P->w[1], &C->sc, C->tstamp, 0, &C->cold_first))) return rc;
     if ((rc = launch_finalize(P, P->J[1], P->PJ[1], P->r_dev + 1))) return rc;
     CtlHook ha{C, P->ev_dev + 0, P->ev_dev + 1, m, P->nsm, P->W_splits, P->info, h_bt};
     if ((rc = eval_at(P->y[1], 1, P->cta_cnt, P->G, P->g[1], P->r_dev + 1, 1, P->scratch, P->info, nullptr, kHookArmijo,
@@ -2244,7 +2277,15 @@ int solve_graph_core(ssnal_en_problem* P, double l1, double l2, double sigma0, d
   h->inner_tol_mode = P->inner_tol_mode;
   h->tstamp[0] = ~0ull;
   h->tstamp[1] = 0ull;
+  const bool cold = !have_x0 && !keep_dual && P->atb && P->reuse_atb;  // R40
   CK(cudaMemcpyAsync(P->ctl, h, sizeof(DevCtl), cudaMemcpyHostToDevice, P->st));
+  if (cold) {  // sets ctl->cold_first when the first trial's active set is small (cleared by ctl_armijo)
+    k_atb_gate<<<2 * P->nsm, 256, 0, P->st>>>(P->atb, P->n, l1, (int64_t)(P->reuse_frac * (double)P->n), P->gate_cnt,
+                                               &P->ctl->cold_first, P->gate_flag_dev);
+    P->launches++;
+    CKL();
+    P->stat_cold_first = true;
+  }
   if (sigma_dev)  // σ0 carried on the device from the previous path point (R38)
     CK(cudaMemcpyAsync(&P->ctl->sigma, sigma_dev, 8, cudaMemcpyDeviceToDevice, P->st));
   CK(cudaGraphLaunch(P->gexec, P->st));
@@ -2300,6 +2341,8 @@ void finish_stats(ssnal_en_problem* P, ssnal_en_stats* S) {
   int64_t rx0;
   memcpy(&rx0, P->scratch_host + 20, 8);
   if (P->stat_warm_pass && rx0 == 0) S->aty_passes--;  // x0 was all zero: cold start, no pass (R8)
+  if (P->stat_cold_first) P->atb_reuses += *(volatile int*)P->gate_flag_host;  // R40 (graph mode's gate)
+  P->stat_cold_first = false;
 }
 
 }  // namespace
@@ -2342,7 +2385,7 @@ static int create_common(ssnal_en_problem* P) {
     return SSNAL_EINVAL;
   }
   // λmax = ‖Aᵀb‖∞ (plain K1 pass) and ‖b‖
-  rc = launch_k1(P, P->b, nullptr, make_scal(1.0, 0.0, 0.0), 0, P->w[0]);
+  rc = launch_k1(P, P->b, nullptr, make_scal(1.0, 0.0, 0.0), 0, P->atb ? P->atb : P->w[0]);  // kept: R40
   if (rc) return rc;
   k_max_partials<<<1, 32, 0, P->st>>>(P->part_scal, P->G, P->scratch);
   CKL();
@@ -2609,6 +2652,8 @@ int ssnal_en_set_option(ssnal_en_problem* P, const char* key, double v) {
   else if (k == "inner_tol_mode" && (v == 0 || v == 1)) P->inner_tol_mode = (int)v;
   else if (k == "carry_sigma" && (v == 0 || v == 1)) P->carry_sigma = (int)v;
   else if (k == "carry_dual" && (v == 0 || v == 1)) P->carry_dual = (int)v;
+  else if (k == "reuse_atb" && (v == 0 || v == 1)) P->reuse_atb = (int)v;
+  else if (k == "reuse_frac" && v >= 0 && v <= 1) P->reuse_frac = v;
   else if (k == "path_graph" && (v == 0 || v == 1)) P->use_path_graph = (int)v;
   else if (k == "warm_dual" && (v == 0 || v == 1)) P->warm_dual = (int)v;
   else if (k == "cg_tol" && v > 0 && v < 1) {
@@ -2693,6 +2738,8 @@ double ssnal_en_get_info(const ssnal_en_problem* P, const char* key) {
   if (k == "cg_threshold") return P->cg_threshold;
   if (k == "carry_sigma") return P->carry_sigma;
   if (k == "carry_dual") return P->carry_dual;
+  if (k == "reuse_atb") return (P->atb && P->reuse_atb) ? 1 : 0;
+  if (k == "atb_reuses") return (double)P->atb_reuses;  // cold-start first trials served from Aᵀb (R40)
   if (k == "path_graph") return P->use_path_graph;
   if (k == "warm_dual") return P->warm_dual;
   if (k == "k1_time_s") return P->k1_time;       // Σ K1 launch times timed by the hook calls (option time_k1)

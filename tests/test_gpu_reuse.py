@@ -1,0 +1,127 @@
+"""Option reuse_atb (reading R40): a cold solve's first Newton direction is d = −b exactly (x0 = 0 ⇒
+y0 = 0, J = ∅, g = b), so the trial product Aᵀ(y0 + d) equals −(Aᵀb) bit for bit — the product
+ssnal_en_create forms for λmax and keeps.  K1 then takes w from it instead of streaming A.  The
+whole solve must be BITWISE what the streaming launch gives (x and every statistic), in both
+control modes, for ragged n / m, with backtracking at the first step, and it must not fire on warm
+starts.  Parity with the oracle is held by every other solve test (the option is on by default)."""
+import numpy as np
+import pytest
+
+import synth
+from gpu_util import compare_to_oracle, cuda_ok
+
+pytestmark = pytest.mark.gpu
+
+if cuda_ok():
+    from paper_2006_03970_b200 import Problem
+
+SAME = ["status", "outer_iters", "newton_iters", "psi_evals", "backtracks", "aty_passes", "branch_steps",
+        "line_search_stalled", "active", "res_kkt1", "res_kkt3", "primal_obj", "dual_obj", "gap", "sigma_final"]
+
+
+def same_stats(a, b):
+    for k in SAME:
+        u, v = a[k], b[k]
+        assert (u == v) or (isinstance(u, float) and np.isnan(u) and np.isnan(v)), (k, u, v)
+
+
+def lambdas(alpha, lm, c):
+    lmax = lm / alpha
+    return c * alpha * lmax, c * (1 - alpha) * lmax
+
+
+def problem(m, n, seed, k=7):
+    rng = np.random.default_rng(seed)
+    A = rng.standard_normal((n, m))  # (n, m) C-contiguous = column-major m × n (the ABI's layout)
+    A -= A.mean(axis=1, keepdims=True)
+    A /= A.std(axis=1, keepdims=True)
+    xs = np.zeros(n)
+    xs[rng.choice(n, size=min(k, n), replace=False)] = rng.uniform(1, 2, min(k, n)) * rng.choice([-1, 1], min(k, n))
+    b = xs @ A + 0.3 * rng.standard_normal(m)
+    return np.ascontiguousarray(A), b
+
+
+@pytest.mark.parametrize("m,n", [(50, 1000), (33, 4099), (129, 20011), (500, 30000), (800, 9001), (1024, 2500),
+                                 (7, 65)])
+@pytest.mark.parametrize("graph", [0, 1])
+def test_reuse_is_bitwise_the_streaming_pass(m, n, graph):
+    A, b = problem(m, n, 100 + m)
+    with Problem(A, b) as P:
+        P.set_option("small", 0)
+        P.set_option("graph", graph)
+        assert P.info("reuse_atb") == 1
+        P.set_option("reuse_frac", 1.0)  # no gate: reuse whatever the first active set (the worst case for the gather)
+        lm = P.lambda_max_l1
+        for c in (0.6, 0.15):
+            l1, l2 = lambdas(0.7, lm, c)
+            P.set_option("reuse_atb", 1)
+            n0 = P.info("atb_reuses")
+            x1, s1 = P.solve(l1, l2, 5e-3, 1e-6)
+            assert P.info("atb_reuses") == n0 + 1
+            P.set_option("reuse_atb", 0)
+            x0, s0 = P.solve(l1, l2, 5e-3, 1e-6)
+            assert P.info("atb_reuses") == n0 + 1
+            assert s1["status"] == 0 and s1["newton_iters"] >= 1
+            assert np.array_equal(x1, x0), np.max(np.abs(x1 - x0))
+            same_stats(s1, s0)
+
+
+def test_reuse_with_backtracking_at_the_first_step():
+    """μ close to ½ forces halvings of the first step: the backtracks read w + s(w1 − w) with w1 the
+    reused product, so w1 must be materialised exactly as the streaming pass writes it."""
+    A, b = problem(200, 15000, 5)
+    for graph in (0, 1):
+        with Problem(A, b) as P:
+            P.set_option("small", 0)
+            P.set_option("graph", graph)
+            P.set_option("mu", 0.49)
+            P.set_option("reuse_frac", 1.0)
+            l1, l2 = lambdas(0.5, P.lambda_max_l1, 0.1)
+            x1, s1 = P.solve(l1, l2, 5e-3, 1e-6)
+            P.set_option("reuse_atb", 0)
+            x0, s0 = P.solve(l1, l2, 5e-3, 1e-6)
+            assert s1["backtracks"] > 0
+            assert np.array_equal(x1, x0)
+            same_stats(s1, s0)
+
+
+def test_reuse_not_used_on_warm_starts_and_matches_oracle():
+    cfg = synth.scaled(synth.CONFIGS["cfg3"], n=20000)
+    A = synth.design(cfg)
+    b, _ = synth.response(cfg)
+    with Problem(A, b) as P:
+        lm = P.lambda_max_l1
+        l1, l2 = lambdas(cfg.alpha, lm, 0.6)
+        compare_to_oracle(A, b, l1, l2, lambda s0, tol, x0: P.solve(l1, l2, s0, tol, x0=x0), cfg.sigma0, cfg.tol)
+        xg, sg = P.solve(l1, l2, cfg.sigma0, cfg.tol)
+        n0 = P.info("atb_reuses")
+        assert n0 >= 1
+        l1b, l2b = lambdas(cfg.alpha, lm, 0.5)
+        xw, sw = P.solve(l1b, l2b, cfg.sigma0, cfg.tol, x0=xg)  # warm: y0 = A x0 − b, no reuse
+        assert P.info("atb_reuses") == n0 and sw["status"] == 0
+        # x = 0 at λ1 = ‖Aᵀb‖∞: the single Newton step's trial is the reused product
+        x0, s0 = P.solve(lm, 0.0, cfg.sigma0, cfg.tol)
+        assert np.all(x0 == 0) and s0["newton_iters"] == 1
+
+
+def test_gate_follows_the_first_active_set():
+    """The reused launch gathers the first trial's active columns {|Aᵀb|_i > λ1} from global memory, so
+    the default gate (reuse_frac = 1/32) uses it only while that set is small; either way the result is
+    the same bits."""
+    A, b = problem(100, 40000, 11)
+    atb = np.abs(A @ b)
+    with Problem(A, b) as P:
+        P.set_option("small", 0)
+        lm = P.lambda_max_l1
+        for c, alpha in ((0.9, 0.7), (0.05, 0.7)):
+            l1, l2 = lambdas(alpha, lm, c)
+            expect = int(np.count_nonzero(atb > l1) <= P.n // 32)
+            res = []
+            for graph in (0, 1):
+                P.set_option("graph", graph)
+                n0 = P.info("atb_reuses")
+                res.append(P.solve(l1, l2, 5e-3, 1e-6))
+                assert P.info("atb_reuses") == n0 + expect, (c, graph)
+            assert np.array_equal(res[0][0], res[1][0])
+            same_stats(res[0][1], res[1][1])
+        assert np.count_nonzero(atb > lambdas(0.7, lm, 0.05)[0]) > P.n // 32  # the second case was gated off
