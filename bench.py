@@ -412,11 +412,12 @@ def bench_ours(args, rank, world, local_rank):
                    "path_dual": ("each point after the first starts from the previous point's final y, w = A^T y "
                                  "(reading R39, P:236-246 + P:409-411): no A^T pass for the warm start")
                                 if cfg.path else None,
-                   "reuse_atb": ((f"on (reading R40): {atb_reuses:g} of the step's cold solves took their first trial "
-                                  "product A^T(y0 + d) = -A^T b (x0 = 0 => d = -b exactly) from the A^T b kept by create's "
-                                  "lambda_max pass instead of streaming A; bitwise the streamed result (tests/"
-                                  "test_gpu_reuse.py); gated on the first active set being <= n/32; those launches "
-                                  "are not counted in roofline.launches; --opt reuse_atb=0 times without it")
+                   "reuse_atb": ((f"on (reading R40): in {atb_reuses:g} of the step's cold solves K1 was allowed to serve a "
+                                  "trial at y == -b (bitwise; the first Newton steps after x0 = 0, while J is empty: "
+                                  "d = -(y + b)) from the A^T b kept by create's lambda_max pass instead of streaming A; "
+                                  "bitwise the streamed result (tests/test_gpu_reuse.py); allowed while "
+                                  "#{|A^T b|_i > lambda1} <= n/32 and 8mn >= 2 GB; such launches are not counted in roofline.launches; "
+                                  "--opt reuse_atb=0 times without it")
                                  if P.info("reuse_atb") == 1 else "off"),
                    "newton_strategy": ("exact (Eq. 18/19); CG when min(m, r) > 1e4 (P:379)" if args.cg_ratio == 0
                                        else f"CG (K6) when r > {args.cg_ratio:g} m, else exact (Eq. 18/19)")},

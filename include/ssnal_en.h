@@ -115,10 +115,15 @@ double ssnal_en_lambda_max_l1(const ssnal_en_problem* p);
  *   carry_sigma=1 (ssnal_en_solve_path_device: point i > 0 starts at point i − 1's sigma_final
  *     instead of σ0 — reading R38 of P:411 "usually SsNAL-EN converges in just one iteration";
  *     0: every point restarts at σ0),
- *   reuse_atb=1 (fp64 storage; reading R40: create keeps the product Aᵀb of its λmax pass, 8n bytes;
- *     a cold solve — x0 = NULL, so y0 = 0 and the first Newton direction is d = −b exactly —
- *     takes Aᵀ(y0 + d) = −Aᵀb from it, bitwise what the streaming pass computes, instead of
- *     reading A once more; ssnal_en_get_info "atb_reuses" counts such solves; 0: always stream A),
+ *   reuse_atb=1 (fp64 storage; reading R40: create keeps the product Aᵀb of its λmax pass, 8n bytes.
+ *     After a cold start (x0 = NULL ⇒ x = 0, y0 = 0) the active set is empty for the first Newton
+ *     step(s), so g = y + b, d = −g and the trial point y + d is −b: K1 compares its y with −b bit
+ *     for bit and, if equal, takes Aᵀy = −Aᵀb from the kept product — bitwise what the streaming pass
+ *     computes — instead of reading A once more.  Allowed per solve only while the active set at
+ *     y = −b, #{i : |Aᵀb|_i > λ1}, is at most reuse_frac·n (=1/32: those columns are then gathered for
+ *     ∇ψ) and only for designs of at least reuse_min_bytes (=2 GB: the gate costs one small kernel
+ *     and a stream synchronisation per cold solve); ssnal_en_get_info "atb_reuses" counts the solves
+ *     that were allowed; 0: always stream A),
  *   small=1 (m ≤ 64 and n ≤ 1024, fp64 storage, unsharded, no CG strategy: the whole solve is ONE
  *     kernel launch — same iteration and statistics, reduction orders differ; 0: the multi-kernel
  *     graph / host paths), small_cluster=1 (that launch is k_small_cl, one 16-CTA cluster with A

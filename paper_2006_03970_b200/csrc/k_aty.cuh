@@ -56,13 +56,15 @@ struct K1Params {
   const double* tab;    // n × 3: decoded value of codes 0, 1, 2 for each column
   int64_t cstride;      // bytes per column (multiple of 16)
   uint32_t bfr_off;     // K1g: byte offset of the shared B-fragment table (32 k-blocks × 32 lanes × 8 B)
-  // Reuse of Aᵀb (option reuse_atb, DESIGN R40; fp64 storage): the first Newton step of a cold start
-  // (x0 = 0, y0 = 0 ⇒ d = −b exactly) evaluates ψ at y = −b, and Aᵀ(−b) = −(Aᵀb) bitwise, the product
-  // ssnal_en_create formed for λmax.  When atb != nullptr and (cache_on, or *cache_flag != 0 in graph
-  // mode) the launch takes w = −atb instead of streaming A: same outputs, bit for bit.
-  const double* atb;    // n: Aᵀb kept by create (nullable)
-  const int* cache_flag;  // graph mode: DevCtl::cold_first
-  int cache_on;         // host-driven mode: this launch is the cold start's first trial
+  // Reuse of Aᵀb (option reuse_atb, DESIGN R40; fp64 storage): while the active set is empty (a cold
+  // start's first Newton steps: x = 0, J = ∅ ⇒ g = y + b, d = −g) the trial point y + d is −b, and
+  // Aᵀ(−b) = −(Aᵀb) bitwise, the product ssnal_en_create formed for λmax.  When atb != nullptr and the
+  // solve's gate allowed it (the REUSE instantiation of the kernel is launched: host-driven mode, or
+  // the handle's second solve graph) the launch compares y with −b bit for bit and, if equal, takes
+  // w = −atb instead of streaming A: same outputs, bit for bit.  The plain instantiation carries no
+  // such branch (it cost the n = 1e5 launch 5 µs of code generation: 62.9 → 68.0 µs, same-box A/B).
+  const double* atb;    // n: Aᵀb kept by create (REUSE instantiation only)
+  const double* bvec;   // m: b
 };
 
 // Reduce-scatter of 8 per-lane partial sums a[0..7] across the warp: afterwards every
@@ -205,7 +207,7 @@ template <int MR>
 SSN_DEV void k1_cached(const K1Params& p, double* ring, int* sh, int64_t c_lo, int64_t c_hi) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == K1_NWC) return;
-  constexpr int kD = 4;
+  constexpr int kD = 8;
   const int C = p.C;
   const int64_t m = p.m;
   const int64_t ntiles = (c_hi - c_lo + C - 1) / C;
@@ -218,37 +220,35 @@ SSN_DEV void k1_cached(const K1Params& p, double* ring, int* sh, int64_t c_lo, i
   const int gcol = lane >> 2;
   double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
   bool any_active = false;
-  const int64_t ntw = ntiles > warp ? (ntiles - warp + K1_NWC - 1) / K1_NWC : 0;  // this warp's tiles
-  const int64_t ng = ntw * gpt;                                                    // and groups (tile-major)
-  for (int64_t q0 = 0; q0 < ng; q0 += kD) {
+  const int ntw = ntiles > warp ? (int)((ntiles - warp + K1_NWC - 1) / K1_NWC) : 0;  // this warp's tiles
+  int tk = 0, tg = 0;  // next group: tile warp + K1_NWC·tk of this CTA, group tg of it
+  while (tk < ntw) {
     double wv[kD], xv[kD];
     int64_t cc[kD];   // global column of this lane in group u, −1: not a column
     int64_t gb[kD];   // first global column of group u, −1: the group does not exist
+    // all loads of the batch issue back to back (clamped addresses, no branch, no use before the batch is out)
 #pragma unroll
     for (int u = 0; u < kD; ++u) {
-      const int64_t q = q0 + u;
-      cc[u] = gb[u] = -1;
-      wv[u] = xv[u] = 0.0;
-      if (q < ng) {
-        const int64_t it = warp + (int64_t)K1_NWC * (q / gpt);
-        const int g = (int)(q % gpt);
-        const int64_t c0 = c_lo + it * C;
-        const int nc = (int)((c_hi - c0) < C ? (c_hi - c0) : C);
-        if (g * K1_GRP < nc) {
-          gb[u] = c0 + (int64_t)g * K1_GRP;
-          if (g * K1_GRP + gcol < nc) {
-            cc[u] = gb[u] + gcol;
-            wv[u] = -__ldg(p.atb + cc[u]);
-            if (p.fused) xv[u] = __ldg(p.x + cc[u]);
-          }
-        }
+      const bool tile_ok = tk < ntw;
+      const int64_t c0 = c_lo + (int64_t)(warp + K1_NWC * (tile_ok ? tk : 0)) * C;
+      const int nc = (int)((c_hi - c0) < C ? (c_hi - c0) : C);
+      const bool grp = tile_ok && tg * K1_GRP < nc;
+      const bool col = grp && tg * K1_GRP + gcol < nc;
+      gb[u] = grp ? c0 + (int64_t)tg * K1_GRP : -1;
+      cc[u] = col ? gb[u] + gcol : -1;
+      const int64_t ca = col ? cc[u] : c_lo;
+      wv[u] = __ldg(p.atb + ca);
+      xv[u] = p.fused ? __ldg(p.x + ca) : 0.0;
+      if (++tg == gpt) {
+        tg = 0;
+        ++tk;
       }
     }
 #pragma unroll
     for (int u = 0; u < kD; ++u) {
       if (gb[u] < 0) continue;  // warp-uniform
       const bool valid = cc[u] >= 0;
-      const double w = wv[u];
+      const double w = -wv[u];  // Aᵀ(−b) = −(Aᵀb) bitwise
       if (p.fused) {
         bool act = false;
         double P = 0.0;
@@ -314,7 +314,7 @@ SSN_DEV void k1_cached(const K1Params& p, double* ring, int* sh, int64_t c_lo, i
   k1_cta_end(p, sc, ring, sh, c_lo, c_hi, s0, s1, s2, s3, any_active, false);
 }
 
-template <int MR>
+template <int MR, bool REUSE = false>
 __global__ void __launch_bounds__(K1_THREADS, 1) k1_aty_fused(const K1Params p) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -330,9 +330,14 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_aty_fused(const K1Params p) 
   int64_t c_lo, c_hi;
   cta_cols(blockIdx.x, gridDim.x, p.T, C, p.n, &c_lo, &c_hi);
   const int64_t ntiles = (c_hi - c_lo + C - 1) / C;
-  if (p.atb && (p.cache_on || (p.cache_flag && *p.cache_flag))) {  // R40: w = −Aᵀb kept by create
-    k1_cached<MR>(p, ring, sh, c_lo, c_hi);
-    return;
+  if constexpr (REUSE) {  // R40: y == −b ⇒ w = −Aᵀb kept by create
+    bool eq = true;
+    for (int64_t row = threadIdx.x; row < m; row += K1_THREADS)
+      eq = eq && (__double_as_longlong(p.y[row]) == __double_as_longlong(-p.bvec[row]));
+    if (__syncthreads_and(eq)) {
+      k1_cached<MR>(p, ring, sh, c_lo, c_hi);
+      return;
+    }
   }
 
   if (threadIdx.x == 0) {

@@ -24,8 +24,7 @@ struct DevCtl {
   double cg_ratio, cg_threshold;  // Newton strategy (R32)
   double nb;                      // ‖b‖ (res1 denominator, Eq. (15))
   double jitter;                  // factor retry scale (R36); 0 = no retry
-  int max_outer, max_inner, max_bt;
-  int cold_first;  // R40: the next trial K1 is the cold start's first (y = −b): served from Aᵀb; cleared after it
+  int max_outer, max_inner, max_bt, pad0;
   // state
   Scal sc;           // σ-dependent scalars of the current outer iteration
   double kinv;       // 1/κ
@@ -118,7 +117,6 @@ SSN_DEV void ctl_armijo(DevCtl* C, const EvalOut* ev0, const EvalOut* ev1, cudaG
   C->seg_inner++;
   C->psi_evals++;
   C->aty_passes++;
-  C->cold_first = 0;
   C->branch_steps[C->geo.branch]++;
   if (C->tstamp[1] > C->tstamp[0]) {
     C->k1_ns += C->tstamp[1] - C->tstamp[0];

@@ -88,17 +88,20 @@ int mr_bucket(int64_t m) {
 
 typedef void (*k1_fn)(const K1Params);
 
-k1_fn k1_for(int mr) {
+template <bool R>
+k1_fn k1_for_r(int mr) {
   switch (mr) {
-    case 1: return k1_aty_fused<1>;
-    case 2: return k1_aty_fused<2>;
-    case 4: return k1_aty_fused<4>;
-    case 8: return k1_aty_fused<8>;
-    case 16: return k1_aty_fused<16>;
-    case 25: return k1_aty_fused<25>;
-    default: return k1_aty_fused<32>;
+    case 1: return k1_aty_fused<1, R>;
+    case 2: return k1_aty_fused<2, R>;
+    case 4: return k1_aty_fused<4, R>;
+    case 8: return k1_aty_fused<8, R>;
+    case 16: return k1_aty_fused<16, R>;
+    case 25: return k1_aty_fused<25, R>;
+    default: return k1_aty_fused<32, R>;
   }
 }
+// reuse: the instantiation that checks y == −b and serves Aᵀy from the kept Aᵀb (R40)
+k1_fn k1_for(int mr, bool reuse = false) { return reuse ? k1_for_r<true>(mr) : k1_for_r<false>(mr); }
 k1_fn k1g_for(int tw) { return tw <= 1 ? k1g_aty_fused<1> : k1g_aty_fused<2>; }
 
 // Kernels that read individual columns are templated on the column accessor (AccA: fp64 design,
@@ -471,7 +474,11 @@ struct ssnal_en_problem {
   unsigned long long* gate_cnt = nullptr;  // k_atb_gate scratch (count, ticket), kept zero
   int* gate_flag_host = nullptr;           // mapped pinned: the gate's decision (host-driven control, statistics)
   int* gate_flag_dev = nullptr;            // its device alias
-  bool stat_cold_first = false;            // the pending solve ran the gate (finish_stats counts atb_reuses)
+  int64_t reuse_min_bytes = 2ll << 30;     // no gate for designs below 2 GB: its synchronisation (and the REUSE
+                                           // instantiation's slower small-n launch) cost cfg2 (0.4 GB) +0.25 ms per path
+  bool capture_reuse = false;              // capture_graph: the trial K1 node is the REUSE instantiation
+  cudaGraph_t graph_r = nullptr;           // second solve graph (REUSE trial K1), built on first use
+  cudaGraphExec_t gexec_r = nullptr;
   double reuse_frac = 1.0 / 32;            // gate: reuse while #{|Aᵀb|_i > λ1} ≤ reuse_frac · n
   int64_t atb_reuses = 0;  // cold solves started with the first trial served from atb (get_info "atb_reuses")
   // device-resident λ path (option path_graph): points 1 … npts − 1 of ssnal_en_solve_path_device
@@ -606,6 +613,8 @@ int configure(ssnal_en_problem* P) {
   }
   CK(cudaFuncSetAttribute(P->fmt ? k1g_for(P->TW) : k1_for(P->MR), cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)P->k1_smem));
+  if (!P->fmt)
+    CK(cudaFuncSetAttribute(k1_for(P->MR, true), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->k1_smem));
   const size_t gsm = (size_t)8 * m * 8;
   P->cg_smem_bytes = cg_smem(m);
   if (P->fmt) {
@@ -822,8 +831,7 @@ void harvest_k1(ssnal_en_problem* P) {  // call after a stream sync
 
 // K1 at y (device, m).  fused=0: plain w = Aᵀy into w_out (+ per-CTA max|w|).
 int launch_k1(ssnal_en_problem* P, const double* y, const double* x, const Scal& sc, int fused, double* w_out,
-              const Scal* scp = nullptr, unsigned long long* tstamp = nullptr, int cached = 0,
-              const int* cache_flag = nullptr) {
+              const Scal* scp = nullptr, unsigned long long* tstamp = nullptr, int reuse = 0, int notime = 0) {
   K1Params k;
   k.A = P->A;
   k.m = P->m;
@@ -850,18 +858,17 @@ int launch_k1(ssnal_en_problem* P, const double* y, const double* x, const Scal&
   k.tab = P->tab;
   k.cstride = P->cstride;
   k.bfr_off = P->k1_bfr_off;
-  const bool can_reuse = P->atb && P->reuse_atb && !P->fmt;  // R40
-  k.atb = can_reuse && (cached || cache_flag) ? P->atb : nullptr;
-  k.cache_on = can_reuse && cached;
-  k.cache_flag = can_reuse ? cache_flag : nullptr;
+  const bool use_r = reuse && fused && P->atb && !P->fmt;  // R40: the launch may be served from the kept Aᵀb
+  k.atb = use_r ? P->atb : nullptr;
+  k.bvec = P->b;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
-  const bool ev_time = P->time_k1 && !P->capturing && !k.cache_on;
+  const bool ev_time = P->time_k1 && !P->capturing && !notime;  // notime: may be served from Aᵀb (not a pass over A)
   if (ev_time) {
     e0 = take_event(P);
     e1 = take_event(P);
     cudaEventRecord(e0, P->st);
   }
-  (P->fmt ? k1g_for(P->TW) : k1_for(P->MR))<<<P->G, K1_THREADS, P->k1_smem, P->st>>>(k);
+  (P->fmt ? k1g_for(P->TW) : k1_for(P->MR, use_r))<<<P->G, K1_THREADS, P->k1_smem, P->st>>>(k);
   P->launches++;
   if (ev_time) {
     cudaEventRecord(e1, P->st);
@@ -1657,6 +1664,24 @@ int launch_objective(ssnal_en_problem* P) {
 }
 
 // Host-driven mode: control decisions on the CPU from the EvalOut records (mapped memory).
+// R40 gate for a cold solve (x0 = 0, y0 = 0): may this solve's trial K1 launches serve y == −b from the
+// Aᵀb kept by create?  Yes while the active set at y = −b, #{|Aᵀb|_i > λ1}, is at most reuse_frac·n
+// (those columns are gathered from global memory for the ∇ψ rows).  One small kernel and one stream
+// synchronisation, only for cold solves on designs of at least reuse_min_bytes (2 GB).
+int reuse_gate(ssnal_en_problem* P, double l1, int have_x0, bool keep_dual, int* allow) {
+  *allow = 0;
+  if (have_x0 || keep_dual || !P->atb || !P->reuse_atb || P->fmt) return SSNAL_OK;
+  if ((int64_t)8 * P->m * P->n < P->reuse_min_bytes) return SSNAL_OK;
+  k_atb_gate<<<2 * P->nsm, 256, 0, P->st>>>(P->atb, P->n, l1, (int64_t)(P->reuse_frac * (double)P->n), P->gate_cnt,
+                                             P->gate_flag_dev, nullptr);
+  P->launches++;
+  CKL();
+  CK(cudaStreamSynchronize(P->st));
+  *allow = *(volatile int*)P->gate_flag_host;
+  P->atb_reuses += *allow;
+  return SSNAL_OK;
+}
+
 int solve_core(ssnal_en_problem* P, double l1, double l2, double sigma0, double tol, int have_x0,
                ssnal_en_stats* S, bool keep_dual = false) {
   const int64_t m = P->m;
@@ -1668,16 +1693,8 @@ int solve_core(ssnal_en_problem* P, double l1, double l2, double sigma0, double 
   int64_t rx = 0;
   CK(cudaMemsetAsync(&P->ctl->cg_iters, 0, sizeof(int), P->st));
   if ((rc = init_point(P, have_x0, S, &rx, keep_dual))) return rc;
-  int reuse_first = 0;  // R40: the first trial from the kept Aᵀb while its active set is small
-  if (!have_x0 && !keep_dual && P->atb && P->reuse_atb) {
-    k_atb_gate<<<2 * P->nsm, 256, 0, P->st>>>(P->atb, P->n, l1, (int64_t)(P->reuse_frac * (double)P->n), P->gate_cnt,
-                                               P->gate_flag_dev, nullptr);
-    P->launches++;
-    CKL();
-    CK(cudaStreamSynchronize(P->st));
-    reuse_first = *(volatile int*)P->gate_flag_host;
-    P->atb_reuses += reuse_first;
-  }
+  int reuse_first = 0;  // R40: trials at y == −b from the kept Aᵀb while its active set is small
+  if ((rc = reuse_gate(P, l1, have_x0, keep_dual, &reuse_first))) return rc;
 
   double sigma = sigma0;
   int converged = 0, numeric = 0, k;
@@ -1712,9 +1729,10 @@ int solve_core(ssnal_en_problem* P, double l1, double l2, double sigma0, double 
                                  retry ? P->jitter : 0.0, P->r_dev + cur)))
         return rc;
       S->branch_steps[br]++;
-      // R40: the first trial of a cold start is at y = −b exactly: w = −Aᵀb kept by create
-      const int cold_first = reuse_first && k == 0 && j == 0 && S->newton_iters == 0;
-      if ((rc = launch_k1(P, P->y[tr], P->x, sc, 1, P->w[wtr], nullptr, nullptr, cold_first))) return rc;
+      // R40: while J = ∅ after a cold start the trial is at y = −b: K1 checks and takes w = −Aᵀb kept by create
+      if ((rc = launch_k1(P, P->y[tr], P->x, sc, 1, P->w[wtr], nullptr, nullptr, reuse_first,
+                          reuse_first && ev.r == 0)))
+        return rc;
       S->aty_passes++;
       if ((rc = launch_finalize(P, P->J[tr], P->PJ[tr], P->r_dev + tr))) return rc;
       if ((rc = eval_g(P, P->y[tr], sc, 1, P->cta_cnt, P->G, P->g[tr], P->r_dev + tr, 1, gd_dev,
@@ -1933,7 +1951,7 @@ int capture_graph(ssnal_en_problem* P, cudaGraph_t G, cudaGraph_t body_pre = nul
     CK(cudaGraphConditionalHandleCreate(&h_bt, body_i, 0, 0));
     L = P->launches;
     if ((rc = newton_direction_graph(P))) return rc;
-    if ((rc = launch_k1(P, P->y[1], P->x, none, 1, P->w[1], &C->sc, C->tstamp, 0, &C->cold_first))) return rc;
+    if ((rc = launch_k1(P, P->y[1], P->x, none, 1, P->w[1], &C->sc, C->tstamp, P->capture_reuse))) return rc;
     if ((rc = launch_finalize(P, P->J[1], P->PJ[1], P->r_dev + 1))) return rc;
     CtlHook ha{C, P->ev_dev + 0, P->ev_dev + 1, m, P->nsm, P->W_splits, P->info, h_bt};
     if ((rc = eval_at(P->y[1], 1, P->cta_cnt, P->G, P->g[1], P->r_dev + 1, 1, P->scratch, P->info, nullptr, kHookArmijo,
@@ -1991,8 +2009,10 @@ int capture_graph(ssnal_en_problem* P, cudaGraph_t G, cudaGraph_t body_pre = nul
   return SSNAL_OK;
 }
 
-int build_graph(ssnal_en_problem* P) {
-  if (P->gexec) return SSNAL_OK;
+int build_graph(ssnal_en_problem* P, bool reuse = false) {
+  cudaGraphExec_t& gexec = reuse ? P->gexec_r : P->gexec;
+  cudaGraph_t& graph = reuse ? P->graph_r : P->graph;
+  if (gexec) return SSNAL_OK;
   {  // K4 outputs per exact branch for the graph's branch-agnostic launch (k_chol_* with want < 0):
      // [0] SMW v → u; [1] m × m d = −M⁻¹g, gᵀd = scratch[0], y[1] = y[0] + d
     const CholArgs ca[2] = {{P->u, 1.0, nullptr, nullptr, nullptr, nullptr},
@@ -2006,7 +2026,9 @@ int build_graph(ssnal_en_problem* P) {
   cudaStream_t saved = P->st;
   const int64_t L0 = P->launches;
   P->capturing = true;
+  P->capture_reuse = reuse;
   int rc = capture_graph(P, G);
+  P->capture_reuse = false;
   // unwind any capture left open by a failure
   for (int d = P->cap_depth; d > 0; --d) {
     cudaGraph_t tmp;
@@ -2017,12 +2039,12 @@ int build_graph(ssnal_en_problem* P) {
   P->st = saved;
   P->launches = L0;
   if (rc == SSNAL_OK) {
-    cudaError_t e = cudaGraphInstantiate(&P->gexec, G, 0);
+    cudaError_t e = cudaGraphInstantiate(&gexec, G, 0);
     if (e != cudaSuccess) {
       set_err("cudaGraphInstantiate: %s", cudaGetErrorString(e));
       rc = SSNAL_ECUDA;
-      P->gexec = nullptr;
-    } else if ((e = cudaGraphUpload(P->gexec, P->st)) != cudaSuccess) {  // device-side setup off the first solve
+      gexec = nullptr;
+    } else if ((e = cudaGraphUpload(gexec, P->st)) != cudaSuccess) {  // device-side setup off the first solve
       set_err("cudaGraphUpload: %s", cudaGetErrorString(e));
       rc = SSNAL_ECUDA;
     }
@@ -2032,7 +2054,7 @@ int build_graph(ssnal_en_problem* P) {
     cudaGraphDestroy(G);
     return rc;
   }
-  P->graph = G;
+  graph = G;
   return SSNAL_OK;
 }
 
@@ -2046,8 +2068,10 @@ void drop_path_graph(ssnal_en_problem* P) {
 void drop_graph(ssnal_en_problem* P) {
   if (P->gexec) cudaGraphExecDestroy(P->gexec);
   if (P->graph) cudaGraphDestroy(P->graph);
-  P->gexec = nullptr;
-  P->graph = nullptr;
+  if (P->gexec_r) cudaGraphExecDestroy(P->gexec_r);
+  if (P->graph_r) cudaGraphDestroy(P->graph_r);
+  P->gexec = P->gexec_r = nullptr;
+  P->graph = P->graph_r = nullptr;
   drop_path_graph(P);  // it embeds the same solve body
 }
 
@@ -2277,18 +2301,13 @@ int solve_graph_core(ssnal_en_problem* P, double l1, double l2, double sigma0, d
   h->inner_tol_mode = P->inner_tol_mode;
   h->tstamp[0] = ~0ull;
   h->tstamp[1] = 0ull;
-  const bool cold = !have_x0 && !keep_dual && P->atb && P->reuse_atb;  // R40
+  int reuse = 0;  // R40: the solve graph whose trial K1 may serve y == −b from the kept Aᵀb
+  if ((rc = reuse_gate(P, l1, have_x0, keep_dual, &reuse))) return rc;
+  if (reuse && (rc = build_graph(P, true))) return rc;
   CK(cudaMemcpyAsync(P->ctl, h, sizeof(DevCtl), cudaMemcpyHostToDevice, P->st));
-  if (cold) {  // sets ctl->cold_first when the first trial's active set is small (cleared by ctl_armijo)
-    k_atb_gate<<<2 * P->nsm, 256, 0, P->st>>>(P->atb, P->n, l1, (int64_t)(P->reuse_frac * (double)P->n), P->gate_cnt,
-                                               &P->ctl->cold_first, P->gate_flag_dev);
-    P->launches++;
-    CKL();
-    P->stat_cold_first = true;
-  }
   if (sigma_dev)  // σ0 carried on the device from the previous path point (R38)
     CK(cudaMemcpyAsync(&P->ctl->sigma, sigma_dev, 8, cudaMemcpyDeviceToDevice, P->st));
-  CK(cudaGraphLaunch(P->gexec, P->st));
+  CK(cudaGraphLaunch(reuse ? P->gexec_r : P->gexec, P->st));
   if ((rc = launch_objective(P))) return rc;
   CK(cudaMemcpyAsync(h, P->ctl, sizeof(DevCtl), cudaMemcpyDeviceToHost, P->st));
   CK(cudaMemcpyAsync(P->ev_out_host, P->ev_dev, sizeof(EvalOut), cudaMemcpyDeviceToHost, P->st));
@@ -2341,8 +2360,6 @@ void finish_stats(ssnal_en_problem* P, ssnal_en_stats* S) {
   int64_t rx0;
   memcpy(&rx0, P->scratch_host + 20, 8);
   if (P->stat_warm_pass && rx0 == 0) S->aty_passes--;  // x0 was all zero: cold start, no pass (R8)
-  if (P->stat_cold_first) P->atb_reuses += *(volatile int*)P->gate_flag_host;  // R40 (graph mode's gate)
-  P->stat_cold_first = false;
 }
 
 }  // namespace
@@ -2364,6 +2381,9 @@ static int create_common(ssnal_en_problem* P) {
   // Capture + instantiate the solve graph now: host work that overlaps the asynchronous upload of A
   // (ssnal_en_create with pinned input) instead of delaying the first solve.
   if (P->use_graph && (rc = build_graph(P))) return rc;
+  if (P->use_graph && P->atb && P->reuse_atb && (int64_t)8 * P->m * P->n >= P->reuse_min_bytes &&
+      (rc = build_graph(P, true)))  // R40: the cold-solve graph with the REUSE trial K1
+    return rc;
   // validate inputs on the device
   CK(cudaMemsetAsync(P->flags, 0, 8, P->st));
   if (P->fmt)
@@ -2654,6 +2674,7 @@ int ssnal_en_set_option(ssnal_en_problem* P, const char* key, double v) {
   else if (k == "carry_dual" && (v == 0 || v == 1)) P->carry_dual = (int)v;
   else if (k == "reuse_atb" && (v == 0 || v == 1)) P->reuse_atb = (int)v;
   else if (k == "reuse_frac" && v >= 0 && v <= 1) P->reuse_frac = v;
+  else if (k == "reuse_min_bytes" && v >= 0) P->reuse_min_bytes = (int64_t)v;
   else if (k == "path_graph" && (v == 0 || v == 1)) P->use_path_graph = (int)v;
   else if (k == "warm_dual" && (v == 0 || v == 1)) P->warm_dual = (int)v;
   else if (k == "cg_tol" && v > 0 && v < 1) {

@@ -51,6 +51,7 @@ def test_reuse_is_bitwise_the_streaming_pass(m, n, graph):
         P.set_option("graph", graph)
         assert P.info("reuse_atb") == 1
         P.set_option("reuse_frac", 1.0)  # no gate: reuse whatever the first active set (the worst case for the gather)
+        P.set_option("reuse_min_bytes", 0)  # the default skips the gate (and its sync) for designs below 2 GB
         lm = P.lambda_max_l1
         for c in (0.6, 0.15):
             l1, l2 = lambdas(0.7, lm, c)
@@ -76,6 +77,7 @@ def test_reuse_with_backtracking_at_the_first_step():
             P.set_option("graph", graph)
             P.set_option("mu", 0.49)
             P.set_option("reuse_frac", 1.0)
+            P.set_option("reuse_min_bytes", 0)
             l1, l2 = lambdas(0.5, P.lambda_max_l1, 0.1)
             x1, s1 = P.solve(l1, l2, 5e-3, 1e-6)
             P.set_option("reuse_atb", 0)
@@ -90,6 +92,7 @@ def test_reuse_not_used_on_warm_starts_and_matches_oracle():
     A = synth.design(cfg)
     b, _ = synth.response(cfg)
     with Problem(A, b) as P:
+        P.set_option("reuse_min_bytes", 0)
         lm = P.lambda_max_l1
         l1, l2 = lambdas(cfg.alpha, lm, 0.6)
         compare_to_oracle(A, b, l1, l2, lambda s0, tol, x0: P.solve(l1, l2, s0, tol, x0=x0), cfg.sigma0, cfg.tol)
@@ -112,6 +115,7 @@ def test_gate_follows_the_first_active_set():
     atb = np.abs(A @ b)
     with Problem(A, b) as P:
         P.set_option("small", 0)
+        P.set_option("reuse_min_bytes", 0)
         lm = P.lambda_max_l1
         for c, alpha in ((0.9, 0.7), (0.05, 0.7)):
             l1, l2 = lambdas(alpha, lm, c)
@@ -125,3 +129,13 @@ def test_gate_follows_the_first_active_set():
             assert np.array_equal(res[0][0], res[1][0])
             same_stats(res[0][1], res[1][1])
         assert np.count_nonzero(atb > lambdas(0.7, lm, 0.05)[0]) > P.n // 32  # the second case was gated off
+
+
+def test_small_designs_skip_the_gate():
+    """Below reuse_min_bytes (2 GB of A) a pass costs less than the gate's synchronisation: no gate."""
+    A, b = problem(100, 5000, 3)
+    with Problem(A, b) as P:
+        P.set_option("small", 0)
+        l1, l2 = lambdas(0.7, P.lambda_max_l1, 0.9)
+        x, st = P.solve(l1, l2, 5e-3, 1e-6)
+        assert st["status"] == 0 and P.info("atb_reuses") == 0
