@@ -139,3 +139,53 @@ def test_small_designs_skip_the_gate():
         l1, l2 = lambdas(0.7, P.lambda_max_l1, 0.9)
         x, st = P.solve(l1, l2, 5e-3, 1e-6)
         assert st["status"] == 0 and P.info("atb_reuses") == 0
+
+
+def test_reuse_on_sharded_handles():
+    """Column-sharded handles (§8(f3)): every rank gates on its own block (the decision only changes
+    which K1 instantiation runs, never a bit of the result), through the host-callback provider with
+    2 shards, and through the peer-kernel provider in both control modes."""
+    from paper_2006_03970_b200.shard import ThreadGroup, attach_peers, column_range, run_threads
+
+    cfg = synth.scaled(synth.CONFIGS["cfg3"], n=12000)
+    A = synth.design(cfg)
+    b, _ = synth.response(cfg)
+    with Problem(A, b) as P:
+        P.set_option("small", 0)
+        lm = P.lambda_max_l1
+        l1, l2 = lambdas(cfg.alpha, lm, 0.6)
+        P.set_option("reuse_atb", 0)
+        xref, sref = P.solve(l1, l2, cfg.sigma0, cfg.tol)
+    # peer provider (G = 1, real exchange kernels), host-driven and graph control
+    for graph in (0, 1):
+        with Problem(A, b) as P:
+            assert attach_peers(P) == (0, 1)
+            P.set_option("graph", graph)
+            P.set_option("reuse_min_bytes", 0)
+            x1, s1 = P.solve(l1, l2, cfg.sigma0, cfg.tol)
+            assert P.info("atb_reuses") == 1
+            P.set_option("reuse_atb", 0)
+            x0, s0 = P.solve(l1, l2, cfg.sigma0, cfg.tol)
+            assert np.array_equal(x1, x0)
+            same_stats(s1, s0)
+            assert np.max(np.abs(x1 - xref)) <= 1e-9 * np.max(np.abs(xref))
+    # two shards, one thread each, host callbacks
+    G = 2
+    grp = ThreadGroup(G)
+    shards = []
+    for q in range(G):
+        j0, j1 = column_range(A.shape[0], q, G)
+        shards.append(Problem(np.ascontiguousarray(A[j0:j1]), b))
+    run_threads([(lambda q=q: shards[q].set_comm(grp.member(q), q, G)) for q in range(G)], grp)
+    outs = {}
+    for on in (1, 0):
+        for S in shards:
+            S.set_option("reuse_atb", on)
+            S.set_option("reuse_min_bytes", 0)
+        res = run_threads([(lambda q=q: shards[q].solve(l1, l2, cfg.sigma0, cfg.tol)) for q in range(G)], grp)
+        outs[on] = (np.concatenate([r[0] for r in res]), res[0][1])
+    assert sum(S.info("atb_reuses") for S in shards) >= 1
+    assert np.array_equal(outs[1][0], outs[0][0])
+    same_stats(outs[1][1], outs[0][1])
+    for S in shards:
+        S.close()
