@@ -30,6 +30,11 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 20000 -
 summ() { ncu -i $O/$1.ncu-rep --page details --csv > $O/$1_details.csv 2>/dev/null; ncu -i $O/$1.ncu-rep --page raw --csv > $O/$1_raw.csv 2>/dev/null; ncu -i $O/$1.ncu-rep --page source --csv --print-source sass > $O/$1_sass.csv 2>/dev/null; gzip -f $O/$1_sass.csv; rm -f $O/$1.ncu-rep; }
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k1_aty_fused -s 10 -c 1 -o $O/k1_n1e7 python bench.py --config cfg5 --steps 1 --warmup 3 --no-cpu --no-e2e --control host > $O/ncu_k1.log 2>&1
 summ k1_n1e7
+# the REUSE instantiation's launch served from the kept A^T b (R40): launch 0 is create's lambda_max pass, launch 1 the cold solve's first trial
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k1_aty_fused -s 1 -c 1 -o $O/k1c_n1e7 python bench.py --config cfg5 --steps 1 --warmup 0 --no-cpu --no-e2e --control host > $O/ncu_k1c.log 2>&1
+summ k1c_n1e7
+timeout 900 python bench.py --steps 10 --warmup 3 --no-cpu --no-e2e --opt reuse_atb=0 > $O/bench_cfg5_noreuse.json 2> $O/bench_cfg5_noreuse.err; echo "cfg5 noreuse rc=$?" >> $O/status.txt
+timeout 900 python bench.py --config cfg3 --steps 10 --warmup 3 --no-cpu --no-e2e --opt reuse_atb=0 > $O/bench_cfg3_noreuse.json 2> $O/bench_cfg3_noreuse.err; echo "cfg3 noreuse rc=$?" >> $O/status.txt
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k1e_epilogue -s 10 -c 1 -o $O/k1e_n1e7 python bench.py --config cfg5 --steps 1 --warmup 3 --no-cpu --no-e2e --control host > $O/ncu_k1e.log 2>&1
 summ k1e_n1e7
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k1g_aty_fused -s 10 -c 1 -o $O/k1g_cfg4 python bench.py --config cfg4 --geno --steps 1 --warmup 3 --no-cpu --no-e2e --control host > $O/ncu_k1g.log 2>&1
