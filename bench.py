@@ -416,7 +416,7 @@ def bench_ours(args, rank, world, local_rank):
                                   "trial at y == -b (bitwise; the first Newton steps after x0 = 0, while J is empty: "
                                   "d = -(y + b)) from the A^T b kept by create's lambda_max pass instead of streaming A; "
                                   "bitwise the streamed result (tests/test_gpu_reuse.py); allowed while "
-                                  "#{|A^T b|_i > lambda1} <= n/4 and 8mn >= 2 GB; such launches are not counted in roofline.launches; "
+                                  "#{|A^T b|_i > lambda1} <= 0.3 n and 8mn >= 2 GB; such launches are not counted in roofline.launches; "
                                   "--opt reuse_atb=0 times without it")
                                  if P.info("reuse_atb") == 1 else "off"),
                    "newton_strategy": ("exact (Eq. 18/19); CG when min(m, r) > 1e4 (P:379)" if args.cg_ratio == 0

@@ -120,7 +120,7 @@ double ssnal_en_lambda_max_l1(const ssnal_en_problem* p);
  *     step(s), so g = y + b, d = −g and the trial point y + d is −b: K1 compares its y with −b bit
  *     for bit and, if equal, takes Aᵀy = −Aᵀb from the kept product — bitwise what the streaming pass
  *     computes — instead of reading A once more.  Allowed per solve only while the active set at
- *     y = −b, #{i : |Aᵀb|_i > λ1}, is at most reuse_frac·n (=1/4: those columns are then gathered for
+ *     y = −b, #{i : |Aᵀb|_i > λ1}, is at most reuse_frac·n (=0.3: those columns are then gathered for
  *     ∇ψ) and only for designs of at least reuse_min_bytes (=2 GB: the gate costs one small kernel
  *     and a stream synchronisation per cold solve); ssnal_en_get_info "atb_reuses" counts the solves
  *     that were allowed; 0: always stream A),

@@ -479,7 +479,7 @@ struct ssnal_en_problem {
   bool capture_reuse = false;              // capture_graph: the trial K1 node is the REUSE instantiation
   cudaGraph_t graph_r = nullptr;           // second solve graph (REUSE trial K1), built on first use
   cudaGraphExec_t gexec_r = nullptr;
-  double reuse_frac = 0.25;                // gate: reuse while #{|Aᵀb|_i > λ1} ≤ reuse_frac · n (the gather of those
+  double reuse_frac = 0.3;                 // gate: reuse while #{|Aᵀb|_i > λ1} ≤ reuse_frac · n (the gather of those
                                            // columns runs at ~4 TB/s against 7.1 for the stream: break-even near n/2)
   int64_t atb_reuses = 0;  // cold solves started with the first trial served from atb (get_info "atb_reuses")
   // device-resident λ path (option path_graph): points 1 … npts − 1 of ssnal_en_solve_path_device

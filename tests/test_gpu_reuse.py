@@ -109,7 +109,7 @@ def test_reuse_not_used_on_warm_starts_and_matches_oracle():
 
 def test_gate_follows_the_first_active_set():
     """The reused launch gathers the first trial's active columns {|Aᵀb|_i > λ1} from global memory, so
-    the default gate (reuse_frac = 1/4) uses it only while that set is small; either way the result is
+    the default gate (reuse_frac = 0.3) uses it only while that set is small; either way the result is
     the same bits."""
     A, b = problem(100, 40000, 11)
     atb = np.abs(A @ b)
@@ -119,7 +119,7 @@ def test_gate_follows_the_first_active_set():
         lm = P.lambda_max_l1
         for c, alpha in ((0.9, 0.7), (0.05, 0.7)):
             l1, l2 = lambdas(alpha, lm, c)
-            expect = int(np.count_nonzero(atb > l1) <= P.n // 4)
+            expect = int(np.count_nonzero(atb > l1) <= int(0.3 * P.n))
             res = []
             for graph in (0, 1):
                 P.set_option("graph", graph)
@@ -128,7 +128,7 @@ def test_gate_follows_the_first_active_set():
                 assert P.info("atb_reuses") == n0 + expect, (c, graph)
             assert np.array_equal(res[0][0], res[1][0])
             same_stats(res[0][1], res[1][1])
-        assert np.count_nonzero(atb > lambdas(0.7, lm, 0.05)[0]) > P.n // 4  # the second case was gated off
+        assert np.count_nonzero(atb > lambdas(0.7, lm, 0.05)[0]) > int(0.3 * P.n)  # the second case was gated off
 
 
 def test_small_designs_skip_the_gate():
