@@ -115,7 +115,7 @@ double ssnal_en_lambda_max_l1(const ssnal_en_problem* p);
  *   carry_sigma=1 (ssnal_en_solve_path_device: point i > 0 starts at point i − 1's sigma_final
  *     instead of σ0 — reading R38 of P:411 "usually SsNAL-EN converges in just one iteration";
  *     0: every point restarts at σ0),
- *   reuse_atb=1 (fp64 storage; reading R40: create keeps the product Aᵀb of its λmax pass, 8n bytes.
+ *   reuse_atb=1 (both storage formats; reading R40: create keeps the product Aᵀb of its λmax pass, 8n bytes.
  *     After a cold start (x0 = NULL ⇒ x = 0, y0 = 0) the active set is empty for the first Newton
  *     step(s), so g = y + b, d = −g and the trial point y + d is −b: K1 compares its y with −b bit
  *     for bit and, if equal, takes Aᵀy = −Aᵀb from the kept product — bitwise what the streaming pass

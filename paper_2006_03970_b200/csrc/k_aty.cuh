@@ -56,7 +56,7 @@ struct K1Params {
   const double* tab;    // n × 3: decoded value of codes 0, 1, 2 for each column
   int64_t cstride;      // bytes per column (multiple of 16)
   uint32_t bfr_off;     // K1g: byte offset of the shared B-fragment table (32 k-blocks × 32 lanes × 8 B)
-  // Reuse of Aᵀb (option reuse_atb, DESIGN R40; fp64 storage): while the active set is empty (a cold
+  // Reuse of Aᵀb (option reuse_atb, DESIGN R40; K1 and K1g): while the active set is empty (a cold
   // start's first Newton steps: x = 0, J = ∅ ⇒ g = y + b, d = −g) the trial point y + d is −b, and
   // Aᵀ(−b) = −(Aᵀb) bitwise, the product ssnal_en_create formed for λmax.  When atb != nullptr and the
   // solve's gate allowed it (the REUSE instantiation of the kernel is launched: host-driven mode, or
@@ -198,12 +198,27 @@ SSN_DEV void k1_cta_end(const K1Params& p, const Scal& sc, double* ring, int* sh
   stamp_end();
 }
 
+// acc += v when (word & bit) != 0 — a predicated add, no branch (K1g's inner loop)
+SSN_DEV void add_if_bit(double& acc, double v, uint32_t word, uint32_t bit) {
+  asm("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\tand.b32 t, %2, %3;\n\tsetp.ne.u32 p, t, 0;\n\t@p add.f64 %0, %0, %1;\n\t}"
+      : "+d"(acc)
+      : "d"(v), "r"(word), "r"(bit));
+}
+// x = v when (word & bit) != 0 — a predicated move
+SSN_DEV void sel_if_bit(double& x, double v, uint32_t word, uint32_t bit) {
+  asm("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\tand.b32 t, %2, %3;\n\tsetp.ne.u32 p, t, 0;\n\t@p mov.f64 %0, %1;\n\t}"
+      : "+d"(x)
+      : "d"(v), "r"(word), "r"(bit));
+}
+
 // K1 served from the kept product Aᵀb (K1Params::atb): w_i = −atb_i instead of the dot product, the
 // same epilogue on the same (warp, lane, order) assignment of columns as the streaming kernel, the
 // ∇ψ partial rows from the active columns read straight from global memory — every output (w, mask,
 // segments, partial scalars and rows) is bitwise what the streaming launch at y = −b writes.  No ring,
 // no producer; kD groups of (w, x) loads in flight per warp.  Not stamped (it is not a pass over A).
-template <int MR>
+// GENO: packed genotype storage (K1g's layout of the ∇ψ partial rows: lane ℓ owns code words ℓ + 32t,
+// 16 rows each; MR = TW words per lane).
+template <int MR, bool GENO = false>
 SSN_DEV void k1_cached(const K1Params& p, double* ring, int* sh, int64_t c_lo, int64_t c_hi) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == K1_NWC) return;
@@ -212,9 +227,11 @@ SSN_DEV void k1_cached(const K1Params& p, double* ring, int* sh, int64_t c_lo, i
   const int64_t m = p.m;
   const int64_t ntiles = (c_hi - c_lo + C - 1) / C;
   const int gpt = C / K1_GRP;  // groups per tile
-  double gacc[MR];
+  constexpr int NG = GENO ? 16 * MR : MR;
+  double gacc[NG];
 #pragma unroll
-  for (int t = 0; t < MR; ++t) gacc[t] = 0.0;
+  for (int t = 0; t < NG; ++t) gacc[t] = 0.0;
+  const int nwords = (int)(p.cstride >> 2);
   const Scal sc = p.scp ? *p.scp : p.sc;
   const bool leader = (lane & 3) == 0;
   const int gcol = lane >> 2;
@@ -287,11 +304,29 @@ SSN_DEV void k1_cached(const K1Params& p, double* ring, int* sh, int64_t c_lo, i
             const int q = __ffs(mm) - 1;
             mm &= mm - 1;
             const double Pq = __shfl_sync(0xffffffffu, P, 4 * q);
-            const double* colq = p.A + (gb[u] + q) * m;
+            if constexpr (GENO) {
+              const int64_t cq = gb[u] + q;
+              const double v0 = __ldg(p.tab + 3 * cq), v1 = __ldg(p.tab + 3 * cq + 1), v2 = __ldg(p.tab + 3 * cq + 2);
+              const uint32_t* wcol = reinterpret_cast<const uint32_t*>(p.codes + cq * p.cstride);
 #pragma unroll
-            for (int t = 0; t < MR; ++t) {
-              const int64_t row = lane + 32 * t;
-              if (row < m) gacc[t] = fma(Pq, __ldg(colq + row), gacc[t]);
+              for (int t = 0; t < MR; ++t) {
+                const int wi = lane + 32 * t;
+                const uint32_t word = (wi < nwords) ? __ldg(wcol + wi) : 0u;
+#pragma unroll
+                for (int e = 0; e < 16; ++e) {
+                  double v = v0;
+                  sel_if_bit(v, v1, word, 1u << (2 * e));
+                  sel_if_bit(v, v2, word, 2u << (2 * e));
+                  gacc[16 * t + e] = fma(Pq, v, gacc[16 * t + e]);
+                }
+              }
+            } else {
+              const double* colq = p.A + (gb[u] + q) * m;
+#pragma unroll
+              for (int t = 0; t < MR; ++t) {
+                const int64_t row = lane + 32 * t;
+                if (row < m) gacc[t] = fma(Pq, __ldg(colq + row), gacc[t]);
+              }
             }
           }
         }
@@ -305,10 +340,20 @@ SSN_DEV void k1_cached(const K1Params& p, double* ring, int* sh, int64_t c_lo, i
   }
   named_bar_sync(1, K1_NWC * 32);
   if (p.fused && p.part_vec) {
+    if constexpr (GENO) {
 #pragma unroll
-    for (int t = 0; t < MR; ++t) {
-      const int64_t row = lane + 32 * t;
-      if (row < m) ring[(size_t)warp * m + row] = gacc[t];
+      for (int t = 0; t < MR; ++t)
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const int64_t row = 16 * (lane + 32 * t) + e;
+          if (row < m) ring[(size_t)warp * m + row] = gacc[16 * t + e];
+        }
+    } else {
+#pragma unroll
+      for (int t = 0; t < MR; ++t) {
+        const int64_t row = lane + 32 * t;
+        if (row < m) ring[(size_t)warp * m + row] = gacc[t];
+      }
     }
   }
   k1_cta_end(p, sc, ring, sh, c_lo, c_hi, s0, s1, s2, s3, any_active, false);
@@ -491,19 +536,6 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_aty_fused(const K1Params p) 
   k1_cta_end(p, sc, ring, sh, c_lo, c_hi, s0, s1, s2, s3, any_active);
 }
 
-// acc += v when (word & bit) != 0 — a predicated add, no branch (K1g's inner loop)
-SSN_DEV void add_if_bit(double& acc, double v, uint32_t word, uint32_t bit) {
-  asm("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\tand.b32 t, %2, %3;\n\tsetp.ne.u32 p, t, 0;\n\t@p add.f64 %0, %0, %1;\n\t}"
-      : "+d"(acc)
-      : "d"(v), "r"(word), "r"(bit));
-}
-// x = v when (word & bit) != 0 — a predicated move
-SSN_DEV void sel_if_bit(double& x, double v, uint32_t word, uint32_t bit) {
-  asm("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\tand.b32 t, %2, %3;\n\tsetp.ne.u32 p, t, 0;\n\t@p mov.f64 %0, %1;\n\t}"
-      : "+d"(x)
-      : "d"(v), "r"(word), "r"(bit));
-}
-
 // ---------------------------------------------------------------------------
 // K1g: K1 over packed 2-bit genotype codes.  Column j is cstride bytes of
 // codes g ∈ {0,1,2} and a 3-entry table v_j[g] (the standardised value, bit-exact with the
@@ -514,7 +546,7 @@ SSN_DEV void sel_if_bit(double& x, double v, uint32_t word, uint32_t bit) {
 // with the bucket sums S_g = Σ_{k: g_kj = g} y_k: per element two bit-tested predicated adds.
 // The 8-column transpose-reduce, the epilogue and the CTA end are K1's.
 // ---------------------------------------------------------------------------
-template <int TW>
+template <int TW, bool REUSE = false>
 __global__ void __launch_bounds__(K1_THREADS, 1) k1g_aty_fused(const K1Params p) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -532,6 +564,15 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1g_aty_fused(const K1Params p)
   int64_t c_lo, c_hi;
   cta_cols(blockIdx.x, gridDim.x, p.T, C, p.n, &c_lo, &c_hi);
   const int64_t ntiles = (c_hi - c_lo + C - 1) / C;
+  if constexpr (REUSE) {  // R40: y == −b ⇒ w = −Aᵀb kept by create (Aᵀ(−y) = −Aᵀy bitwise here too: rint is odd)
+    bool eq = true;
+    for (int64_t row = threadIdx.x; row < m; row += K1_THREADS)
+      eq = eq && (__double_as_longlong(p.y[row]) == __double_as_longlong(-p.bvec[row]));
+    if (__syncthreads_and(eq)) {
+      k1_cached<TW, true>(p, ring, sh, c_lo, c_hi);
+      return;
+    }
+  }
   if (threadIdx.x == 0) {
     if (p.tstamp) atomicMin(p.tstamp, global_ns());
     for (int s = 0; s < S; ++s) {

@@ -102,7 +102,10 @@ k1_fn k1_for_r(int mr) {
 }
 // reuse: the instantiation that checks y == −b and serves Aᵀy from the kept Aᵀb (R40)
 k1_fn k1_for(int mr, bool reuse = false) { return reuse ? k1_for_r<true>(mr) : k1_for_r<false>(mr); }
-k1_fn k1g_for(int tw) { return tw <= 1 ? k1g_aty_fused<1> : k1g_aty_fused<2>; }
+k1_fn k1g_for(int tw, bool reuse = false) {
+  if (reuse) return tw <= 1 ? k1g_aty_fused<1, true> : k1g_aty_fused<2, true>;
+  return tw <= 1 ? k1g_aty_fused<1> : k1g_aty_fused<2>;
+}
 
 // Kernels that read individual columns are templated on the column accessor (AccA: fp64 design,
 // AccG: packed genotype codes, §8(f4)); these tables pick the register-tile variant.
@@ -468,7 +471,7 @@ struct ssnal_en_problem {
   int warm_dual = 0;
   // option reuse_atb (reading R40): create keeps Aᵀb (the λmax pass) in atb; the first Newton step of a
   // cold start (x0 = 0 ⇒ y0 = 0, d = −b exactly) takes Aᵀ(y0 + d) = −Aᵀb from it — bitwise what the
-  // streaming K1 launch writes — instead of a pass over A.  fp64 storage only (atb == nullptr otherwise).
+  // streaming K1 / K1g launch writes — instead of a pass over A.
   int reuse_atb = 1;
   double* atb = nullptr;
   unsigned long long* gate_cnt = nullptr;  // k_atb_gate scratch (count, ticket), kept zero
@@ -614,8 +617,8 @@ int configure(ssnal_en_problem* P) {
   }
   CK(cudaFuncSetAttribute(P->fmt ? k1g_for(P->TW) : k1_for(P->MR), cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)P->k1_smem));
-  if (!P->fmt)
-    CK(cudaFuncSetAttribute(k1_for(P->MR, true), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->k1_smem));
+  CK(cudaFuncSetAttribute(P->fmt ? k1g_for(P->TW, true) : k1_for(P->MR, true),
+                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->k1_smem));
   const size_t gsm = (size_t)8 * m * 8;
   P->cg_smem_bytes = cg_smem(m);
   if (P->fmt) {
@@ -733,7 +736,7 @@ int allocate(ssnal_en_problem* P) {
   const int64_t m = P->m, n = P->n;
   Arena d;
   for (int i = 0; i < 3; ++i) d.add((void**)&P->w[i], n * 8);
-  if (!P->fmt) d.add((void**)&P->atb, n * 8);
+  d.add((void**)&P->atb, n * 8);
   d.add((void**)&P->gate_cnt, 64);
   d.add((void**)&P->x, n * 8);
   d.add((void**)&P->seg_idx, n * 4);
@@ -859,7 +862,7 @@ int launch_k1(ssnal_en_problem* P, const double* y, const double* x, const Scal&
   k.tab = P->tab;
   k.cstride = P->cstride;
   k.bfr_off = P->k1_bfr_off;
-  const bool use_r = reuse && fused && P->atb && !P->fmt;  // R40: the launch may be served from the kept Aᵀb
+  const bool use_r = reuse && fused && P->atb;  // R40: the launch may be served from the kept Aᵀb
   k.atb = use_r ? P->atb : nullptr;
   k.bvec = P->b;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -869,7 +872,7 @@ int launch_k1(ssnal_en_problem* P, const double* y, const double* x, const Scal&
     e1 = take_event(P);
     cudaEventRecord(e0, P->st);
   }
-  (P->fmt ? k1g_for(P->TW) : k1_for(P->MR, use_r))<<<P->G, K1_THREADS, P->k1_smem, P->st>>>(k);
+  (P->fmt ? k1g_for(P->TW, use_r) : k1_for(P->MR, use_r))<<<P->G, K1_THREADS, P->k1_smem, P->st>>>(k);
   P->launches++;
   if (ev_time) {
     cudaEventRecord(e1, P->st);
@@ -1671,7 +1674,7 @@ int launch_objective(ssnal_en_problem* P) {
 // synchronisation, only for cold solves on designs of at least reuse_min_bytes (2 GB).
 int reuse_gate(ssnal_en_problem* P, double l1, int have_x0, bool keep_dual, int* allow) {
   *allow = 0;
-  if (have_x0 || keep_dual || !P->atb || !P->reuse_atb || P->fmt) return SSNAL_OK;
+  if (have_x0 || keep_dual || !P->atb || !P->reuse_atb) return SSNAL_OK;
   if ((int64_t)8 * P->m * P->n < P->reuse_min_bytes) return SSNAL_OK;
   k_atb_gate<<<2 * P->nsm, 256, 0, P->st>>>(P->atb, P->n, l1, (int64_t)(P->reuse_frac * (double)P->n), P->gate_cnt,
                                              P->gate_flag_dev, nullptr);

@@ -189,3 +189,31 @@ def test_reuse_on_sharded_handles():
     same_stats(outs[1][1], outs[0][1])
     for S in shards:
         S.close()
+
+
+@pytest.mark.parametrize("m,n", [(800, 6000), (203, 9001), (64, 2048)])
+@pytest.mark.parametrize("graph", [0, 1])
+def test_reuse_on_packed_genotypes(m, n, graph):
+    """K1g's REUSE instantiation (packed 2-bit codes, §8(f4)): Aᵀ(−b) = −(Aᵀb) bitwise there too (the
+    fixed-point rounding of y is odd), the ∇ψ rows decoded from the active columns' codes."""
+    cfg = synth.scaled(synth.CONFIGS["cfg4"], n=n, m=m)
+    codes, tab = synth.geno_codes(cfg)
+    b, _ = synth.response(cfg)
+    with Problem.from_geno(codes, tab, b) as P:
+        P.set_option("small", 0)
+        P.set_option("graph", graph)
+        P.set_option("reuse_frac", 1.0)
+        P.set_option("reuse_min_bytes", 0)
+        assert P.info("reuse_atb") == 1
+        lm = P.lambda_max_l1
+        for c in (0.6, 0.2):
+            l1, l2 = lambdas(cfg.alpha, lm, c)
+            P.set_option("reuse_atb", 1)
+            n0 = P.info("atb_reuses")
+            x1, s1 = P.solve(l1, l2, cfg.sigma0, cfg.tol)
+            assert P.info("atb_reuses") == n0 + 1
+            P.set_option("reuse_atb", 0)
+            x0, s0 = P.solve(l1, l2, cfg.sigma0, cfg.tol)
+            assert s1["status"] == 0 and s1["newton_iters"] >= 1
+            assert np.array_equal(x1, x0), np.max(np.abs(x1 - x0))
+            same_stats(s1, s0)
