@@ -19,7 +19,7 @@ timeout 900 python bench.py --sweep > $O/bench_sweep.jsonl 2> $O/sweep.err; echo
 timeout 900 python bench.py --select --cv 5 --steps 5 --warmup 3 > $O/bench_select.json 2> $O/select.err; echo "select rc=$?" >> $O/status.txt
 timeout 900 python bench.py --config cfg2 --shard --steps 10 --warmup 3 --no-cpu --no-e2e > $O/bench_cfg2_shard.json 2> $O/shard.err; echo "shard rc=$?" >> $O/status.txt
 timeout 900 python bench.py --config cfg2 --shard --shard-comm nccl --steps 10 --warmup 3 --no-cpu --no-e2e > $O/bench_cfg2_shard_nccl.json 2> $O/shard_nccl.err; echo "shard nccl rc=$?" >> $O/status.txt
-timeout 300 tools/probes/read_probe > $O/read_probe.jsonl 2>&1; echo "read probe rc=$?" >> $O/status.txt
+(cd tools/probes && bash build.sh > /dev/null 2>&1); timeout 300 tools/probes/read_probe > $O/read_probe.jsonl 2>&1; echo "read probe rc=$?" >> $O/status.txt
 timeout 600 python tools/kprof.py --newton 20,100,250,435,700,1165,2000,5000,10193 > $O/kprof_newton.txt 2>&1
 # launch lists (cold-cache, serialised: compare shares, not absolutes)
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 20000 --csv --log-file $O/launches_cfg2.csv python bench.py --config cfg2 --steps 1 --warmup 3 --no-cpu --no-e2e --control host > $O/ncu_list2.log 2>&1
@@ -35,6 +35,8 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:k1_a
 summ k1c_n1e7
 timeout 900 python bench.py --steps 10 --warmup 3 --no-cpu --no-e2e --opt reuse_atb=0 > $O/bench_cfg5_noreuse.json 2> $O/bench_cfg5_noreuse.err; echo "cfg5 noreuse rc=$?" >> $O/status.txt
 timeout 900 python bench.py --config cfg3 --steps 10 --warmup 3 --no-cpu --no-e2e --opt reuse_atb=0 > $O/bench_cfg3_noreuse.json 2> $O/bench_cfg3_noreuse.err; echo "cfg3 noreuse rc=$?" >> $O/status.txt
+timeout 900 python bench.py --config cfg4 --steps 10 --warmup 3 --no-cpu --no-e2e --opt reuse_atb=0 > $O/bench_cfg4_noreuse.json 2> $O/bench_cfg4_noreuse.err; echo "cfg4 noreuse rc=$?" >> $O/status.txt
+timeout 900 python bench.py --config cfg4 --geno --steps 10 --warmup 3 --no-cpu --no-e2e --opt reuse_atb=0 > $O/bench_cfg4_geno_noreuse.json 2> $O/bench_cfg4_geno_noreuse.err; echo "cfg4g noreuse rc=$?" >> $O/status.txt
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k1e_epilogue -s 10 -c 1 -o $O/k1e_n1e7 python bench.py --config cfg5 --steps 1 --warmup 3 --no-cpu --no-e2e --control host > $O/ncu_k1e.log 2>&1
 summ k1e_n1e7
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k1g_aty_fused -s 10 -c 1 -o $O/k1g_cfg4 python bench.py --config cfg4 --geno --steps 1 --warmup 3 --no-cpu --no-e2e --control host > $O/ncu_k1g.log 2>&1
