@@ -415,8 +415,9 @@ def bench_ours(args, rank, world, local_rank):
                    "reuse_atb": ((f"on (reading R40): in {atb_reuses:g} of the step's cold solves K1 was allowed to serve a "
                                   "trial at y == -b (bitwise; the first Newton steps after x0 = 0, while J is empty: "
                                   "d = -(y + b)) from the A^T b kept by create's lambda_max pass instead of streaming A; "
-                                  "bitwise the streamed result (tests/test_gpu_reuse.py); allowed while "
-                                  "#{|A^T b|_i > lambda1} <= 0.3 n and 8mn >= 2 GB; such launches are not counted in roofline.launches; "
+                                  "bitwise the streamed result (tests/test_gpu_reuse.py); with the grad-psi rows gathered while "
+                                  "#{|A^T b|_i > lambda1} <= 0.3 n, psi-only above (Armijo rejects s = 1 there; if it accepts, the "
+                                  "trial is redone streamed); designs >= 2 GB; such launches are not counted in roofline.launches; "
                                   "--opt reuse_atb=0 times without it")
                                  if P.info("reuse_atb") == 1 else "off"),
                    "newton_strategy": ("exact (Eq. 18/19); CG when min(m, r) > 1e4 (P:379)" if args.cg_ratio == 0

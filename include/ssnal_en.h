@@ -119,11 +119,14 @@ double ssnal_en_lambda_max_l1(const ssnal_en_problem* p);
  *     After a cold start (x0 = NULL ⇒ x = 0, y0 = 0) the active set is empty for the first Newton
  *     step(s), so g = y + b, d = −g and the trial point y + d is −b: K1 compares its y with −b bit
  *     for bit and, if equal, takes Aᵀy = −Aᵀb from the kept product — bitwise what the streaming pass
- *     computes — instead of reading A once more.  Allowed per solve only while the active set at
- *     y = −b, #{i : |Aᵀb|_i > λ1}, is at most reuse_frac·n (=0.3: those columns are then gathered for
- *     ∇ψ) and only for designs of at least reuse_min_bytes (=2 GB: the gate costs one small kernel
- *     and a stream synchronisation per cold solve); ssnal_en_get_info "atb_reuses" counts the solves
- *     that were allowed; 0: always stream A),
+ *     computes — instead of reading A once more.  While the active set at y = −b,
+ *     #{i : |Aᵀb|_i > λ1}, is at most reuse_frac·n (=0.3) its columns are gathered for ∇ψ; above
+ *     (reuse_psi_only=1, unsharded handles) the trial is served ψ-only — Armijo usually rejects
+ *     s = 1 there and the gradient is rebuilt at the accepted step; if it accepts, the same trial is
+ *     redone streamed — so the iterates stay bitwise those of the streamed solve either way.  Only
+ *     for designs of at least reuse_min_bytes (=2 GB: the gate costs one small kernel and a stream
+ *     synchronisation per cold solve); ssnal_en_get_info "atb_reuses" counts the solves that
+ *     were allowed; 0: always stream A),
  *   small=1 (m ≤ 64 and n ≤ 1024, fp64 storage, unsharded, no CG strategy: the whole solve is ONE
  *     kernel launch — same iteration and statistics, reduction orders differ; 0: the multi-kernel
  *     graph / host paths), small_cluster=1 (that launch is k_small_cl, one 16-CTA cluster with A

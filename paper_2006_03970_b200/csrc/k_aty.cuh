@@ -65,6 +65,19 @@ struct K1Params {
   // such branch (it cost the n = 1e5 launch 5 µs of code generation: 62.9 → 68.0 µs, same-box A/B).
   const double* atb;    // n: Aᵀb kept by create (REUSE instantiation only)
   const double* bvec;   // m: b
+  // REUSE instantiation: how a launch at y == −b is served.  rmode (host value, or *rmodep in graph mode):
+  //   1: from atb, with the ∇ψ rows gathered from the active columns (every output of the stream);
+  //   2: from atb, ψ only — no ∇ψ rows (they are worth a large part of a pass when most columns are
+  //      active at −b, and Armijo usually rejects s = 1 there, after which the gradient is recomputed at
+  //      the accepted step anyway); *gmiss ← 1 tells the control to redo the launch streamed if it accepts
+  //      s = 1 after all;  0: stream.
+  // pred (nullable): the launch runs only if *pred != 0 (the redo node of the graph); force_stream: never
+  // serve from atb (the redo).  gmiss (nullable): ← 0 by a streamed launch, ← 1 by a ψ-only one.
+  int rmode;
+  const int* rmodep;
+  const int* pred;
+  int force_stream;
+  int* gmiss;
 };
 
 // Reduce-scatter of 8 per-lane partial sums a[0..7] across the warp: afterwards every
@@ -219,7 +232,7 @@ SSN_DEV void sel_if_bit(double& x, double v, uint32_t word, uint32_t bit) {
 // GENO: packed genotype storage (K1g's layout of the ∇ψ partial rows: lane ℓ owns code words ℓ + 32t,
 // 16 rows each; MR = TW words per lane).
 template <int MR, bool GENO = false>
-SSN_DEV void k1_cached(const K1Params& p, double* ring, int* sh, int64_t c_lo, int64_t c_hi) {
+SSN_DEV void k1_cached(const K1Params& p, double* ring, int* sh, int64_t c_lo, int64_t c_hi, bool psi_only) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == K1_NWC) return;
   constexpr int kD = 8;
@@ -297,8 +310,8 @@ SSN_DEV void k1_cached(const K1Params& p, double* ring, int* sh, int64_t c_lo, i
 #pragma unroll
         for (int q = 0; q < K1_GRP; ++q) m8 |= ((bal >> (4 * q)) & 1u) << q;
         if (lane == 0) p.mask[gb[u] >> 3] = (uint8_t)m8;
-        if (m8) {
-          any_active = true;
+        if (m8) any_active = true;
+        if (m8 && !psi_only) {
           unsigned mm = m8;
           while (mm) {
             const int q = __ffs(mm) - 1;
@@ -376,11 +389,16 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_aty_fused(const K1Params p) 
   cta_cols(blockIdx.x, gridDim.x, p.T, C, p.n, &c_lo, &c_hi);
   const int64_t ntiles = (c_hi - c_lo + C - 1) / C;
   if constexpr (REUSE) {  // R40: y == −b ⇒ w = −Aᵀb kept by create
-    bool eq = true;
-    for (int64_t row = threadIdx.x; row < m; row += K1_THREADS)
-      eq = eq && (__double_as_longlong(p.y[row]) == __double_as_longlong(-p.bvec[row]));
-    if (__syncthreads_and(eq)) {
-      k1_cached<MR>(p, ring, sh, c_lo, c_hi);
+    if (p.pred && *p.pred == 0) return;
+    const int mode = p.force_stream ? 0 : (p.rmodep ? *p.rmodep : p.rmode);
+    bool eq = mode != 0;
+    if (eq)
+      for (int64_t row = threadIdx.x; row < m; row += K1_THREADS)
+        eq = eq && (__double_as_longlong(p.y[row]) == __double_as_longlong(-p.bvec[row]));
+    const bool cached = __syncthreads_and(eq);
+    if (p.gmiss && blockIdx.x == 0 && threadIdx.x == 0) *p.gmiss = (cached && mode == 2) ? 1 : 0;
+    if (cached) {
+      k1_cached<MR>(p, ring, sh, c_lo, c_hi, mode == 2);
       return;
     }
   }
@@ -565,11 +583,16 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1g_aty_fused(const K1Params p)
   cta_cols(blockIdx.x, gridDim.x, p.T, C, p.n, &c_lo, &c_hi);
   const int64_t ntiles = (c_hi - c_lo + C - 1) / C;
   if constexpr (REUSE) {  // R40: y == −b ⇒ w = −Aᵀb kept by create (Aᵀ(−y) = −Aᵀy bitwise here too: rint is odd)
-    bool eq = true;
-    for (int64_t row = threadIdx.x; row < m; row += K1_THREADS)
-      eq = eq && (__double_as_longlong(p.y[row]) == __double_as_longlong(-p.bvec[row]));
-    if (__syncthreads_and(eq)) {
-      k1_cached<TW, true>(p, ring, sh, c_lo, c_hi);
+    if (p.pred && *p.pred == 0) return;
+    const int mode = p.force_stream ? 0 : (p.rmodep ? *p.rmodep : p.rmode);
+    bool eq = mode != 0;
+    if (eq)
+      for (int64_t row = threadIdx.x; row < m; row += K1_THREADS)
+        eq = eq && (__double_as_longlong(p.y[row]) == __double_as_longlong(-p.bvec[row]));
+    const bool cached = __syncthreads_and(eq);
+    if (p.gmiss && blockIdx.x == 0 && threadIdx.x == 0) *p.gmiss = (cached && mode == 2) ? 1 : 0;
+    if (cached) {
+      k1_cached<TW, true>(p, ring, sh, c_lo, c_hi, mode == 2);
       return;
     }
   }
@@ -982,7 +1005,8 @@ __global__ void __launch_bounds__(K1E_THREADS) k1e_epilogue(const K1eParams p) {
 __global__ void __launch_bounds__(256) k1_finalize(const int32_t* __restrict__ seg_idx,
                                                    const double* __restrict__ seg_P, const int* __restrict__ cta_cnt,
                                                    int G, int64_t T, int C, int64_t n, int32_t* __restrict__ J,
-                                                   double* __restrict__ PJ, int64_t* r_out) {
+                                                   double* __restrict__ PJ, int64_t* r_out, const int* pred = nullptr) {
+  if (pred && *pred == 0) return;
   __shared__ long long sh[2][8];
   const int b = blockIdx.x, tid = threadIdx.x;
   long long off = 0, tot = 0;

@@ -24,7 +24,8 @@ struct DevCtl {
   double cg_ratio, cg_threshold;  // Newton strategy (R32)
   double nb;                      // ‖b‖ (res1 denominator, Eq. (15))
   double jitter;                  // factor retry scale (R36); 0 = no retry
-  int max_outer, max_inner, max_bt, pad0;
+  int max_outer, max_inner, max_bt;
+  int reuse_mode;  // R40 (the reuse graph): how its trial K1 serves y == −b — 1 with the ∇ψ rows, 2 ψ only (K1Params::rmode)
   // state
   Scal sc;           // σ-dependent scalars of the current outer iteration
   double kinv;       // 1/κ
@@ -44,6 +45,8 @@ struct DevCtl {
   unsigned long long k1_ns;  // Σ K1 durations from the in-kernel globaltimer stamps
   int k1_cnt, jitter_retries;
   unsigned long long tstamp[2];
+  int gmiss;  // R40: the last trial K1 was served ψ-only — its ∇ψ rows are missing
+  int redo;   // R40: Armijo accepted s = 1 on such a trial: the redo nodes stream the pass and decide again
 };
 
 constexpr double kEpsDev = 2.220446049250313e-16;
@@ -113,17 +116,23 @@ SSN_DEV void ctl_inner_begin(DevCtl* C, const EvalOut* ev0, int64_t m, int nsm, 
 }
 
 // after the trial evaluation at s = 1: numeric checks, first Armijo test, K1 timing
-SSN_DEV void ctl_armijo(DevCtl* C, const EvalOut* ev0, const EvalOut* ev1, cudaGraphConditionalHandle h_bt) {
-  C->seg_inner++;
-  C->psi_evals++;
-  C->aty_passes++;
-  C->branch_steps[C->geo.branch]++;
+SSN_DEV void ctl_armijo(DevCtl* C, const EvalOut* ev0, const EvalOut* ev1, cudaGraphConditionalHandle h_bt,
+                        bool redo_pass = false) {
   if (C->tstamp[1] > C->tstamp[0]) {
     C->k1_ns += C->tstamp[1] - C->tstamp[0];
     C->k1_cnt++;
   }
   C->tstamp[0] = ~0ull;
   C->tstamp[1] = 0ull;
+  if (redo_pass) {  // R40: the same trial, now streamed (bitwise the same ψ, with its ∇ψ): decide again
+    C->redo = 0;
+    cudaGraphSetConditional(h_bt, bt_next(C, armijo_ok(C, ev1->psi, ev0->psi, ev0->psimag)));
+    return;
+  }
+  C->seg_inner++;
+  C->psi_evals++;
+  C->aty_passes++;
+  C->branch_steps[C->geo.branch]++;
   C->nbt = 0;
   C->s = 1.0;
   const bool fac = C->geo.branch == 1 || C->geo.branch == 2;
@@ -150,7 +159,13 @@ SSN_DEV void ctl_armijo(DevCtl* C, const EvalOut* ev0, const EvalOut* ev1, cudaG
     return;
   }
   C->gd = ev1->gd;
-  cudaGraphSetConditional(h_bt, bt_next(C, armijo_ok(C, ev1->psi, ev0->psi, ev0->psimag)));
+  const bool ok = armijo_ok(C, ev1->psi, ev0->psi, ev0->psimag);
+  if (ok && C->gmiss) {  // R40: s = 1 accepted on a ψ-only trial: the redo nodes stream it (no decision yet)
+    C->redo = 1;
+    cudaGraphSetConditional(h_bt, 0);
+    return;
+  }
+  cudaGraphSetConditional(h_bt, bt_next(C, ok));
 }
 
 // after a backtrack evaluation (no gradient) at the current s
@@ -263,7 +278,7 @@ struct CtlHook {
   int* info;
   cudaGraphConditionalHandle h;
 };
-enum { kHookInnerBegin = 1, kHookArmijo = 2, kHookBacktrack = 3, kHookInnerEnd = 4 };
+enum { kHookInnerBegin = 1, kHookArmijo = 2, kHookBacktrack = 3, kHookInnerEnd = 4, kHookArmijoRedo = 5 };
 
 template <int KIND>
 __global__ void __cluster_dims__(kEvalCS, 1, 1) __launch_bounds__(K5_THREADS)
@@ -282,6 +297,7 @@ __global__ void __cluster_dims__(kEvalCS, 1, 1) __launch_bounds__(K5_THREADS)
     return;
   if (KIND == kHookInnerBegin) ctl_inner_begin(hk.C, hk.ev0, hk.m, hk.nsm, hk.wsplits, hk.info, hk.h);
   if (KIND == kHookArmijo) ctl_armijo(hk.C, hk.ev0, hk.ev1, hk.h);
+  if (KIND == kHookArmijoRedo) ctl_armijo(hk.C, hk.ev0, hk.ev1, hk.h, true);
   if (KIND == kHookBacktrack) ctl_bt(hk.C, hk.ev0, hk.ev1, hk.h);
   if (KIND == kHookInnerEnd) ctl_inner_end(hk.C, hk.ev0, hk.m, hk.nsm, hk.wsplits, hk.info, hk.h);
 }
@@ -304,6 +320,7 @@ __global__ void __cluster_dims__(kEval16, 1, 1) __launch_bounds__(K5_THREADS)
     return;
   if (KIND == kHookInnerBegin) ctl_inner_begin(hk.C, hk.ev0, hk.m, hk.nsm, hk.wsplits, hk.info, hk.h);
   if (KIND == kHookArmijo) ctl_armijo(hk.C, hk.ev0, hk.ev1, hk.h);
+  if (KIND == kHookArmijoRedo) ctl_armijo(hk.C, hk.ev0, hk.ev1, hk.h, true);
   if (KIND == kHookBacktrack) ctl_bt(hk.C, hk.ev0, hk.ev1, hk.h);
   if (KIND == kHookInnerEnd) ctl_inner_end(hk.C, hk.ev0, hk.m, hk.nsm, hk.wsplits, hk.info, hk.h);
 }

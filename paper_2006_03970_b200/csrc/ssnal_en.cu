@@ -457,6 +457,8 @@ struct ssnal_en_problem {
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t gexec = nullptr;
   int seg_kernels[5] = {0, 0, 0, 0, 0};
+  int seg_kernels_r[5] = {0, 0, 0, 0, 0};  // the reuse graph's (its inner body carries the redo nodes)
+  bool stat_graph_r = false;               // the pending solve ran the reuse graph
   bool graph_pending = false;
   // λ-path call (ssnal_en_solve_path_device): per-point pinned result slots and timing events
   void* path_slots = nullptr;
@@ -477,6 +479,7 @@ struct ssnal_en_problem {
   unsigned long long* gate_cnt = nullptr;  // k_atb_gate scratch (count, ticket), kept zero
   int* gate_flag_host = nullptr;           // mapped pinned: the gate's decision (host-driven control, statistics)
   int* gate_flag_dev = nullptr;            // its device alias
+  int reuse_psi_only = 1;                  // above reuse_frac: serve ψ only, redo streamed if s = 1 is accepted
   int64_t reuse_min_bytes = 2ll << 30;     // no gate for designs below 2 GB: its synchronisation (and the REUSE
                                            // instantiation's slower small-n launch) cost cfg2 (0.4 GB) +0.25 ms per path
   bool capture_reuse = false;              // capture_graph: the trial K1 node is the REUSE instantiation
@@ -693,6 +696,7 @@ int configure(ssnal_en_problem* P) {
     CK(cudaFuncSetAttribute(k_eval_reduce16, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     CK(cudaFuncSetAttribute(k_eval_ctl16<kHookInnerBegin>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     CK(cudaFuncSetAttribute(k_eval_ctl16<kHookArmijo>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    CK(cudaFuncSetAttribute(k_eval_ctl16<kHookArmijoRedo>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     CK(cudaFuncSetAttribute(k_eval_ctl16<kHookBacktrack>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     CK(cudaFuncSetAttribute(k_eval_ctl16<kHookInnerEnd>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     cudaLaunchConfig_t cfg = {};
@@ -835,7 +839,10 @@ void harvest_k1(ssnal_en_problem* P) {  // call after a stream sync
 
 // K1 at y (device, m).  fused=0: plain w = Aᵀy into w_out (+ per-CTA max|w|).
 int launch_k1(ssnal_en_problem* P, const double* y, const double* x, const Scal& sc, int fused, double* w_out,
-              const Scal* scp = nullptr, unsigned long long* tstamp = nullptr, int reuse = 0, int notime = 0) {
+              const Scal* scp = nullptr, unsigned long long* tstamp = nullptr, int reuse = 0, int notime = 0,
+              const int* pred = nullptr, int force_stream = 0) {
+  // reuse: 0 plain instantiation; 1 / 2 the REUSE instantiation with that K1Params::rmode; −1 the REUSE
+  // instantiation with the mode, the ψ-only flag and (pred) the redo predicate in the control block (graph)
   K1Params k;
   k.A = P->A;
   k.m = P->m;
@@ -865,6 +872,11 @@ int launch_k1(ssnal_en_problem* P, const double* y, const double* x, const Scal&
   const bool use_r = reuse && fused && P->atb;  // R40: the launch may be served from the kept Aᵀb
   k.atb = use_r ? P->atb : nullptr;
   k.bvec = P->b;
+  k.rmode = reuse > 0 ? reuse : 0;
+  k.rmodep = (use_r && reuse < 0) ? &P->ctl->reuse_mode : nullptr;
+  k.pred = use_r ? pred : nullptr;
+  k.force_stream = force_stream;
+  k.gmiss = !use_r ? nullptr : (reuse < 0 ? &P->ctl->gmiss : P->gate_flag_dev + 1);
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   const bool ev_time = P->time_k1 && !P->capturing && !notime;  // notime: may be served from Aᵀb (not a pass over A)
   if (ev_time) {
@@ -906,8 +918,8 @@ int launch_k1e(ssnal_en_problem* P, const double* w0, const double* w1, double s
   return SSNAL_OK;
 }
 
-int launch_finalize(ssnal_en_problem* P, int32_t* J, double* PJ, int64_t* r_dev) {
-  k1_finalize<<<P->G, 256, 0, P->st>>>(P->seg_idx, P->seg_P, P->cta_cnt, P->G, P->T, P->C, P->n, J, PJ, r_dev);
+int launch_finalize(ssnal_en_problem* P, int32_t* J, double* PJ, int64_t* r_dev, const int* pred = nullptr) {
+  k1_finalize<<<P->G, 256, 0, P->st>>>(P->seg_idx, P->seg_P, P->cta_cnt, P->G, P->T, P->C, P->n, J, PJ, r_dev, pred);
   P->launches++;
   CKL();
   return SSNAL_OK;
@@ -984,6 +996,7 @@ int launch_eval(ssnal_en_problem* P, const double* y, const Scal& sc, int with_g
     switch (hook) {
       case kHookInnerBegin: k_eval_ctl16<kHookInnerBegin><<<g16, K5_THREADS, 0, P->st>>>(SSN_EVAL_ARGS, *hk); break;
       case kHookArmijo: k_eval_ctl16<kHookArmijo><<<g16, K5_THREADS, 0, P->st>>>(SSN_EVAL_ARGS, *hk); break;
+      case kHookArmijoRedo: k_eval_ctl16<kHookArmijoRedo><<<g16, K5_THREADS, 0, P->st>>>(SSN_EVAL_ARGS, *hk); break;
       case kHookBacktrack: k_eval_ctl16<kHookBacktrack><<<g16, K5_THREADS, 0, P->st>>>(SSN_EVAL_ARGS, *hk); break;
       case kHookInnerEnd: k_eval_ctl16<kHookInnerEnd><<<g16, K5_THREADS, 0, P->st>>>(SSN_EVAL_ARGS, *hk); break;
       default: k_eval_reduce16<<<g16, K5_THREADS, 0, P->st>>>(SSN_EVAL_ARGS);
@@ -995,6 +1008,7 @@ int launch_eval(ssnal_en_problem* P, const double* y, const Scal& sc, int with_g
   switch (hook) {  // graph mode: the control decision that consumes this evaluation, in the same launch
     case kHookInnerBegin: k_eval_ctl<kHookInnerBegin><<<grid, K5_THREADS, 0, P->st>>>(SSN_EVAL_ARGS, *hk); break;
     case kHookArmijo: k_eval_ctl<kHookArmijo><<<grid, K5_THREADS, 0, P->st>>>(SSN_EVAL_ARGS, *hk); break;
+    case kHookArmijoRedo: k_eval_ctl<kHookArmijoRedo><<<grid, K5_THREADS, 0, P->st>>>(SSN_EVAL_ARGS, *hk); break;
     case kHookBacktrack: k_eval_ctl<kHookBacktrack><<<grid, K5_THREADS, 0, P->st>>>(SSN_EVAL_ARGS, *hk); break;
     case kHookInnerEnd: k_eval_ctl<kHookInnerEnd><<<grid, K5_THREADS, 0, P->st>>>(SSN_EVAL_ARGS, *hk); break;
     default: k_eval_reduce<<<grid, K5_THREADS, 0, P->st>>>(SSN_EVAL_ARGS);
@@ -1673,7 +1687,7 @@ int launch_objective(ssnal_en_problem* P) {
 // (those columns are gathered from global memory for the ∇ψ rows).  One small kernel and one stream
 // synchronisation, only for cold solves on designs of at least reuse_min_bytes (2 GB).
 int reuse_gate(ssnal_en_problem* P, double l1, int have_x0, bool keep_dual, int* allow) {
-  *allow = 0;
+  *allow = 0;  // → K1Params::rmode: 1 with the ∇ψ rows (small active set at −b), 2 ψ only (large; unsharded handles)
   if (have_x0 || keep_dual || !P->atb || !P->reuse_atb) return SSNAL_OK;
   if ((int64_t)8 * P->m * P->n < P->reuse_min_bytes) return SSNAL_OK;
   k_atb_gate<<<2 * P->nsm, 256, 0, P->st>>>(P->atb, P->n, l1, (int64_t)(P->reuse_frac * (double)P->n), P->gate_cnt,
@@ -1681,8 +1695,8 @@ int reuse_gate(ssnal_en_problem* P, double l1, int have_x0, bool keep_dual, int*
   P->launches++;
   CKL();
   CK(cudaStreamSynchronize(P->st));
-  *allow = *(volatile int*)P->gate_flag_host;
-  P->atb_reuses += *allow;
+  *allow = *(volatile int*)P->gate_flag_host ? 1 : ((P->reuse_psi_only && !sharded(P)) ? 2 : 0);
+  P->atb_reuses += *allow != 0;
   return SSNAL_OK;
 }
 
@@ -1744,6 +1758,14 @@ int solve_core(ssnal_en_problem* P, double l1, double l2, double sigma0, double 
         return rc;
       if ((rc = fetch_eval(P, 1, &evt))) return rc;
       S->psi_evals++;
+      if (reuse_first == 2 && ((volatile int*)P->gate_flag_host)[1] && isfinite(evt.psi) && isfinite(evt.gd) &&
+          evt.psi - ev.psi <= P->mu * evt.gd + 10.0 * kEps * ev.psimag) {
+        // R40: s = 1 accepted on a ψ-only trial — the same trial streamed (bitwise the same ψ, with its ∇ψ)
+        if ((rc = launch_k1(P, P->y[tr], P->x, sc, 1, P->w[wtr]))) return rc;
+        if ((rc = launch_finalize(P, P->J[tr], P->PJ[tr], P->r_dev + tr))) return rc;
+        if ((rc = eval_g(P, P->y[tr], sc, 1, P->cta_cnt, P->G, P->g[tr], P->r_dev + tr, 1, gd_dev, nullptr))) return rc;
+        if ((rc = fetch_eval(P, 1, &evt))) return rc;
+      }
       if ((br == 1 || br == 2) && inject > 0) {
         inject--;
         evt.info = 1;
@@ -1945,7 +1967,7 @@ int capture_graph(ssnal_en_problem* P, cudaGraph_t G, cudaGraph_t body_pre = nul
   CtlHook hk{C, P->ev_dev + 0, nullptr, m, P->nsm, P->W_splits, P->info, h_inner};
   if ((rc = eval_at(P->y[0], 1, nullptr, 1, P->g[0], P->r_dev + 0, 0, nullptr, nullptr, nullptr, kHookInnerBegin, &hk)))
     return rc;
-  P->seg_kernels[0] = (int)(P->launches - L);
+  (P->capture_reuse ? P->seg_kernels_r : P->seg_kernels)[0] = (int)(P->launches - L);
   if ((rc = add_while(P->cap[0], h_inner, &body_i))) return rc;
   {
     // ---- inner body: direction, trial K1 at y + d, Armijo ----
@@ -1955,13 +1977,20 @@ int capture_graph(ssnal_en_problem* P, cudaGraph_t G, cudaGraph_t body_pre = nul
     CK(cudaGraphConditionalHandleCreate(&h_bt, body_i, 0, 0));
     L = P->launches;
     if ((rc = newton_direction_graph(P))) return rc;
-    if ((rc = launch_k1(P, P->y[1], P->x, none, 1, P->w[1], &C->sc, C->tstamp, P->capture_reuse))) return rc;
+    if ((rc = launch_k1(P, P->y[1], P->x, none, 1, P->w[1], &C->sc, C->tstamp, P->capture_reuse ? -1 : 0))) return rc;
     if ((rc = launch_finalize(P, P->J[1], P->PJ[1], P->r_dev + 1))) return rc;
     CtlHook ha{C, P->ev_dev + 0, P->ev_dev + 1, m, P->nsm, P->W_splits, P->info, h_bt};
     if ((rc = eval_at(P->y[1], 1, P->cta_cnt, P->G, P->g[1], P->r_dev + 1, 1, P->scratch, P->info, nullptr, kHookArmijo,
                       &ha)))
       return rc;
-    P->seg_kernels[1] = (int)(P->launches - L);
+    if (P->capture_reuse) {  // R40 redo (predicated on C->redo): a ψ-only trial whose s = 1 Armijo accepted, streamed
+      if ((rc = launch_k1(P, P->y[1], P->x, none, 1, P->w[1], &C->sc, C->tstamp, -1, 0, &C->redo, 1))) return rc;
+      if ((rc = launch_finalize(P, P->J[1], P->PJ[1], P->r_dev + 1, &C->redo))) return rc;
+      if ((rc = eval_at(P->y[1], 1, P->cta_cnt, P->G, P->g[1], P->r_dev + 1, 1, P->scratch, nullptr, &C->redo,
+                        kHookArmijoRedo, &ha)))
+        return rc;
+    }
+    (P->capture_reuse ? P->seg_kernels_r : P->seg_kernels)[1] = (int)(P->launches - L);
     if ((rc = add_while(P->cap[1], h_bt, &body_b))) return rc;
     {
       // ---- backtrack body: y + s d, K1e from w + s (w1 − w), Armijo ----
@@ -1977,7 +2006,7 @@ int capture_graph(ssnal_en_problem* P, cudaGraph_t G, cudaGraph_t body_pre = nul
       if ((rc = eval_at(P->y[1], 0, nullptr, 0, nullptr, P->r_dev + 1, 2, nullptr, nullptr, nullptr, kHookBacktrack,
                         &hb)))
         return rc;
-      P->seg_kernels[2] = (int)(P->launches - L);
+      (P->capture_reuse ? P->seg_kernels_r : P->seg_kernels)[2] = (int)(P->launches - L);
       cudaGraph_t tmp;
       CK(cudaStreamEndCapture(P->cap[2], &tmp));
       P->cap_depth = 2;
@@ -1993,7 +2022,7 @@ int capture_graph(ssnal_en_problem* P, cudaGraph_t G, cudaGraph_t body_pre = nul
     if ((rc = eval_at(P->y[0], 1, nullptr, 1, P->g[0], P->r_dev + 0, 0, nullptr, nullptr, &C->need_grad, kHookInnerEnd,
                       &he)))
       return rc;
-    P->seg_kernels[3] = (int)(P->launches - L);
+    (P->capture_reuse ? P->seg_kernels_r : P->seg_kernels)[3] = (int)(P->launches - L);
     cudaGraph_t tmp;
     CK(cudaStreamEndCapture(P->cap[1], &tmp));
     P->cap_depth = 1;
@@ -2006,7 +2035,7 @@ int capture_graph(ssnal_en_problem* P, cudaGraph_t G, cudaGraph_t body_pre = nul
   k_ctl_outer_end<<<1, 1, 0, P->st>>>(C, P->ev_dev + 0, h_outer);
   P->launches += 3;
   CKL();
-  P->seg_kernels[4] = (int)(P->launches - L);
+  (P->capture_reuse ? P->seg_kernels_r : P->seg_kernels)[4] = (int)(P->launches - L);
   cudaGraph_t tmp;
   CK(cudaStreamEndCapture(P->cap[0], &tmp));
   P->cap_depth = 0;
@@ -2305,13 +2334,15 @@ int solve_graph_core(ssnal_en_problem* P, double l1, double l2, double sigma0, d
   h->inner_tol_mode = P->inner_tol_mode;
   h->tstamp[0] = ~0ull;
   h->tstamp[1] = 0ull;
-  int reuse = 0;  // R40: the solve graph whose trial K1 may serve y == −b from the kept Aᵀb
+  int reuse = 0;  // R40: the solve graph whose trial K1 may serve y == −b from the kept Aᵀb (mode 1 / 2)
   if ((rc = reuse_gate(P, l1, have_x0, keep_dual, &reuse))) return rc;
   if (reuse && (rc = build_graph(P, true))) return rc;
+  h->reuse_mode = reuse;
   CK(cudaMemcpyAsync(P->ctl, h, sizeof(DevCtl), cudaMemcpyHostToDevice, P->st));
   if (sigma_dev)  // σ0 carried on the device from the previous path point (R38)
     CK(cudaMemcpyAsync(&P->ctl->sigma, sigma_dev, 8, cudaMemcpyDeviceToDevice, P->st));
   CK(cudaGraphLaunch(reuse ? P->gexec_r : P->gexec, P->st));
+  P->stat_graph_r = reuse != 0;
   if ((rc = launch_objective(P))) return rc;
   CK(cudaMemcpyAsync(h, P->ctl, sizeof(DevCtl), cudaMemcpyDeviceToHost, P->st));
   CK(cudaMemcpyAsync(P->ev_out_host, P->ev_dev, sizeof(EvalOut), cudaMemcpyDeviceToHost, P->st));
@@ -2344,9 +2375,10 @@ void finish_stats(ssnal_en_problem* P, ssnal_en_stats* S) {
     else if (C->numeric) set_err("non-finite psi/gd");
     const double l2 = P->stat_l2;
     S->dual_obj = (l2 > 0) ? (-(0.5 * ev->yy + ev->by) - ev->s[3] / (2.0 * l2)) : NAN;
-    P->launches += (int64_t)C->seg_outer * (P->seg_kernels[0] + P->seg_kernels[4]) +
-                   (int64_t)C->seg_inner * (P->seg_kernels[1] + P->seg_kernels[3]) +
-                   (int64_t)C->seg_bt * P->seg_kernels[2];
+    const int* sk = P->stat_graph_r ? P->seg_kernels_r : P->seg_kernels;
+    P->launches += (int64_t)C->seg_outer * (sk[0] + sk[4]) + (int64_t)C->seg_inner * (sk[1] + sk[3]) +
+                   (int64_t)C->seg_bt * sk[2];
+    P->stat_graph_r = false;
     if (P->time_k1) {  // in-kernel globaltimer stamps (events cannot sit inside conditional bodies)
       P->k1_time += C->k1_ns * 1e-9;
       P->k1_count += C->k1_cnt;
@@ -2678,6 +2710,7 @@ int ssnal_en_set_option(ssnal_en_problem* P, const char* key, double v) {
   else if (k == "carry_dual" && (v == 0 || v == 1)) P->carry_dual = (int)v;
   else if (k == "reuse_atb" && (v == 0 || v == 1)) P->reuse_atb = (int)v;
   else if (k == "reuse_frac" && v >= 0 && v <= 1) P->reuse_frac = v;
+  else if (k == "reuse_psi_only" && (v == 0 || v == 1)) P->reuse_psi_only = (int)v;
   else if (k == "reuse_min_bytes" && v >= 0) P->reuse_min_bytes = (int64_t)v;
   else if (k == "path_graph" && (v == 0 || v == 1)) P->use_path_graph = (int)v;
   else if (k == "warm_dual" && (v == 0 || v == 1)) P->warm_dual = (int)v;
@@ -2988,6 +3021,7 @@ int ssnal_en_solve_path_device(ssnal_en_problem* P, int64_t npts, const double* 
         slot[q].l1 = lambda1[q];
         slot[q].l2 = lambda2[q];
         slot[q].warm_pass = 0;  // R39: no warm-start pass
+        slot[q].pad = 0;        // the path graph embeds the plain solve body
         slot[q].launches = P->pgraph_fixed;
         k1_beg[q] = P->k1_pending.size();
       }
@@ -3018,6 +3052,7 @@ int ssnal_en_solve_path_device(ssnal_en_problem* P, int64_t npts, const double* 
     slot[i].l1 = P->stat_l1;
     slot[i].l2 = P->stat_l2;
     slot[i].warm_pass = P->stat_warm_pass;
+    slot[i].pad = P->stat_graph_r ? 1 : 0;
     slot[i].launches = P->launches;
   }
   k1_beg[npts] = P->k1_pending.size();
@@ -3050,6 +3085,7 @@ int ssnal_en_solve_path_device(ssnal_en_problem* P, int64_t npts, const double* 
     P->stat_l1 = slot[i].l1;
     P->stat_l2 = slot[i].l2;
     P->stat_warm_pass = slot[i].warm_pass;
+    P->stat_graph_r = slot[i].pad != 0;
     P->launches = slot[i].launches;
     P->k1_time = k1_t[i];
     P->k1_count = k1_c[i];

@@ -116,6 +116,7 @@ def test_gate_follows_the_first_active_set():
     with Problem(A, b) as P:
         P.set_option("small", 0)
         P.set_option("reuse_min_bytes", 0)
+        P.set_option("reuse_psi_only", 0)  # above the gate: stream (the ψ-only mode has its own test below)
         lm = P.lambda_max_l1
         for c, alpha in ((0.9, 0.7), (0.05, 0.7)):
             l1, l2 = lambdas(alpha, lm, c)
@@ -217,3 +218,38 @@ def test_reuse_on_packed_genotypes(m, n, graph):
             assert s1["status"] == 0 and s1["newton_iters"] >= 1
             assert np.array_equal(x1, x0), np.max(np.abs(x1 - x0))
             same_stats(s1, s0)
+
+
+def test_psi_only_trials_and_the_streamed_redo():
+    """Above reuse_frac the trial at y = −b is served ψ-only (no ∇ψ rows: most columns are active there);
+    Armijo usually rejects s = 1 and the gradient is rebuilt at the accepted step, else the trial is redone
+    streamed.  Both outcomes must give the bits of the plain solve, in both control modes: small λ (large
+    active set, s = 1 rejected) and λ near λmax with reuse_frac = 0 (ψ-only although J is tiny: s = 1 is
+    accepted, the redo runs)."""
+    A, b = problem(120, 30000, 21)
+    for graph in (0, 1):
+        with Problem(A, b) as P:
+            P.set_option("small", 0)
+            P.set_option("graph", graph)
+            P.set_option("reuse_min_bytes", 0)
+            lm = P.lambda_max_l1
+            seen = {"rejected": 0, "accepted": 0}
+            for c, frac in ((0.05, 0.3), (0.02, 0.3), (0.9, 0.0), (0.6, 0.0), (0.3, 0.0)):
+                l1, l2 = lambdas(0.7, lm, c)
+                P.set_option("reuse_frac", frac)
+                P.set_option("reuse_atb", 1)
+                n0 = P.info("atb_reuses")
+                x1, s1 = P.solve(l1, l2, 5e-3, 1e-6)
+                assert P.info("atb_reuses") == n0 + 1
+                P.set_option("reuse_atb", 0)
+                x0, s0 = P.solve(l1, l2, 5e-3, 1e-6)
+                assert np.array_equal(x1, x0), (c, graph, np.max(np.abs(x1 - x0)))
+                same_stats(s1, s0)
+                seen["rejected" if s1["backtracks"] > 0 else "accepted"] += 1
+            assert seen["rejected"] > 0 and seen["accepted"] > 0, seen
+            # reuse_psi_only = 0: above the gate the solve streams
+            P.set_option("reuse_atb", 1)
+            P.set_option("reuse_psi_only", 0)
+            n0 = P.info("atb_reuses")
+            P.solve(l1, l2, 5e-3, 1e-6)
+            assert P.info("atb_reuses") == n0
