@@ -369,7 +369,9 @@ SSN_DEV void k1_cached(const K1Params& p, double* ring, int* sh, int64_t c_lo, i
       }
     }
   }
-  k1_cta_end(p, sc, ring, sh, c_lo, c_hi, s0, s1, s2, s3, any_active, false);
+  // ψ-only: nothing reads this trial's active set (a rejected trial is re-thresholded by the backtrack, an
+  // accepted one is redone streamed): no compaction, no ∇ψ rows — the CTA reports an empty segment
+  k1_cta_end(p, sc, ring, sh, c_lo, c_hi, s0, s1, s2, s3, any_active && !psi_only, false);
 }
 
 template <int MR, bool REUSE = false>
