@@ -3,7 +3,7 @@ every execution path of the library — the one-cluster launch (when eligible), 
 host-driven control, and the graph with the Aᵀb reuse of reading R40 forced on (no size gate, both of
 its modes) — and each compared with the oracle by the SURVEY §8(c) rule (equal counts or the ±1 rerun
 of both at tol 1e-10; objective 1e-9, ‖Δx‖∞ ≤ 1e-6‖x‖∞, sign pattern; dual objective and gap).  The
-fixed-shape tests pin the tile edges; this one looks for anything the hand-picked shapes miss."""
+warm-started solve from the cold solution follows on both control modes.  The fixed-shape tests pin the tile edges; this one looks for anything the hand-picked shapes miss."""
 import numpy as np
 import pytest
 
@@ -54,3 +54,10 @@ def test_random_problem_all_paths(case):
                 P.set_option(k, v)
             compare_to_oracle(A, b, l1, l2, lambda s0, tol, x0: P.solve(l1, l2, s0, tol, x0=x0), sigma0=sigma0,
                               label=f"{label} {case}")
+        # a warm-started solve at a smaller λ from that solution (R8: y0 = A x0 − b), graph and host control
+        xc, _, _, _ = oracle.solve(A, b, l1, l2, sigma0=sigma0, tol=1e-6)
+        w1, w2 = 0.7 * l1, 0.7 * l2
+        for graph in (1, 0):
+            P.set_option("graph", graph)
+            compare_to_oracle(A, b, w1, w2, lambda s0, tol, x0: P.solve(w1, w2, s0, tol, x0=x0), sigma0=sigma0, x0=xc,
+                              label=f"warm graph={graph} {case}")
