@@ -2416,7 +2416,9 @@ static int create_common(ssnal_en_problem* P) {
   if (rc) return rc;
   // Capture + instantiate the solve graph now: host work that overlaps the asynchronous upload of A
   // (ssnal_en_create with pinned input) instead of delaying the first solve.
-  if (P->use_graph && (rc = build_graph(P))) return rc;
+  // (not for handles the one-launch small path serves: their solves never launch it; a later set_option
+  // that makes the handle ineligible builds it on the first solve)
+  if (P->use_graph && !small_eligible(P) && (rc = build_graph(P))) return rc;
   if (P->use_graph && P->atb && P->reuse_atb && (int64_t)8 * P->m * P->n >= P->reuse_min_bytes &&
       (rc = build_graph(P, true)))  // R40: the cold-solve graph with the REUSE trial K1
     return rc;
