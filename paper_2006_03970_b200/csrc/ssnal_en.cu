@@ -482,6 +482,7 @@ struct ssnal_en_problem {
   int reuse_psi_only = 1;                  // above reuse_frac: serve ψ only, redo streamed if s = 1 is accepted
   int64_t reuse_min_bytes = 2ll << 30;     // no gate for designs below 2 GB: its synchronisation (and the REUSE
                                            // instantiation's slower small-n launch) cost cfg2 (0.4 GB) +0.25 ms per path
+  bool prepared = false;                   // create_prepare ran (configure + allocate)
   bool capture_reuse = false;              // capture_graph: the trial K1 node is the REUSE instantiation
   cudaGraph_t graph_r = nullptr;           // second solve graph (REUSE trial K1), built on first use
   cudaGraphExec_t gexec_r = nullptr;
@@ -789,6 +790,14 @@ int allocate(ssnal_en_problem* P) {
   d.assign((char*)P->arena);
   CK(cudaMemset(P->ticket, 0, 64));
   CK(cudaMemset(P->gate_cnt, 0, 64));
+  {  // K4 outputs per exact branch for the graph's branch-agnostic launch (k_chol_* with want < 0):
+     // [0] SMW v → u; [1] m × m d = −M⁻¹g, gᵀd = scratch[0], y[1] = y[0] + d.  Uploaded here, before the
+     // caller's A is enqueued: a synchronous copy in build_graph would wait for that upload and serialise
+     // the graph capture behind it.
+    const CholArgs ca[2] = {{P->u, 1.0, nullptr, nullptr, nullptr, nullptr},
+                            {P->d, -1.0, P->g[0], P->scratch, P->y[0], P->y[1]}};
+    CK(cudaMemcpy(P->chol_args, ca, sizeof(ca), cudaMemcpyHostToDevice));
+  }
   CK(cudaMemset(P->gsk_cnt, 0, (size_t)(2 * gsk_tiles + 64) * 4));
   Arena h;
   h.add((void**)&P->ev_host, sizeof(EvalOut) * 4);
@@ -2046,12 +2055,6 @@ int build_graph(ssnal_en_problem* P, bool reuse = false) {
   cudaGraphExec_t& gexec = reuse ? P->gexec_r : P->gexec;
   cudaGraph_t& graph = reuse ? P->graph_r : P->graph;
   if (gexec) return SSNAL_OK;
-  {  // K4 outputs per exact branch for the graph's branch-agnostic launch (k_chol_* with want < 0):
-     // [0] SMW v → u; [1] m × m d = −M⁻¹g, gᵀd = scratch[0], y[1] = y[0] + d
-    const CholArgs ca[2] = {{P->u, 1.0, nullptr, nullptr, nullptr, nullptr},
-                            {P->d, -1.0, P->g[0], P->scratch, P->y[0], P->y[1]}};
-    CK(cudaMemcpy(P->chol_args, ca, sizeof(ca), cudaMemcpyHostToDevice));
-  }
   for (int i = 0; i < 3; ++i)
     if (!P->cap[i]) CK(cudaStreamCreateWithFlags(&P->cap[i], cudaStreamNonBlocking));
   cudaGraph_t G;
@@ -2407,12 +2410,23 @@ const char* ssnal_en_last_error(void) { return g_err.c_str(); }
 
 const char* ssnal_en_version(void) { return "ssnal_en_b200 0.2 (sm_100a, fp64)"; }
 
-static int create_common(ssnal_en_problem* P) {
+// Device query, launch configuration and every allocation of the handle.  The host-memory creates call it
+// BEFORE they enqueue the upload of A: the pool allocations synchronise the default stream, and behind
+// the upload they would wait for it (cfg2: 7.3 ms) and push the graph capture after it instead of under it.
+static int create_prepare(ssnal_en_problem* P) {
+  if (P->prepared) return SSNAL_OK;
   CK(cudaGetDevice(&P->dev));
   CK(cudaDeviceGetAttribute(&P->nsm, cudaDevAttrMultiProcessorCount, P->dev));
   int rc = configure(P);
   if (rc) return rc;
   rc = allocate(P);
+  if (rc) return rc;
+  P->prepared = true;
+  return SSNAL_OK;
+}
+
+static int create_common(ssnal_en_problem* P) {
+  int rc = create_prepare(P);
   if (rc) return rc;
   // Capture + instantiate the solve graph now: host work that overlaps the asynchronous upload of A
   // (ssnal_en_create with pinned input) instead of delaying the first solve.
@@ -2536,6 +2550,12 @@ int ssnal_en_create(const double* A_colmajor, const double* b, int64_t m, int64_
     delete P;
     return SSNAL_ECUDA;
   }
+  P->st = nullptr;
+  if ((rc = create_prepare(P))) {
+    destroy_bufs(P);
+    delete P;
+    return rc;
+  }
   // asynchronous for pinned input (overlaps the graph build in create_common); staged otherwise
   if (cudaMemcpyAsync(P->A_own, A_colmajor, (size_t)m * n * 8, cudaMemcpyHostToDevice, 0) != cudaSuccess ||
       cudaMemcpyAsync(P->b_own, b, (size_t)m * 8, cudaMemcpyHostToDevice, 0) != cudaSuccess) {
@@ -2652,6 +2672,12 @@ int ssnal_en_create_geno(const uint8_t* codes, int64_t stride, const double* tab
     destroy_bufs(P);
     delete P;
     return SSNAL_ECUDA;
+  }
+  P->st = nullptr;
+  if ((rc = create_prepare(P))) {  // before the upload is enqueued (see create_prepare)
+    destroy_bufs(P);
+    delete P;
+    return rc;
   }
   if (cudaMemcpyAsync(P->codes_own, codes, (size_t)n * stride, cudaMemcpyHostToDevice, 0) != cudaSuccess ||
       cudaMemcpyAsync(P->tab_own, tab, (size_t)n * 3 * 8, cudaMemcpyHostToDevice, 0) != cudaSuccess ||
