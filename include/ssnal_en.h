@@ -51,8 +51,8 @@ typedef struct {
   int32_t newton_iters;    /* semi-smooth Newton steps, summed over outer iterations      */
   int32_t psi_evals;       /* ψ evaluations (Armijo trials incl. backtracks)              */
   int32_t backtracks;      /* step halvings                                               */
-  int32_t aty_passes;      /* Aᵀy products at new points (K1 launches); with reuse_atb=1 the first
-                              of a cold solve reads Aᵀb kept by create instead of A        */
+  int32_t aty_passes;      /* Aᵀy products at new points (K1 launches); with reuse_atb=1 a cold
+                              solve's trials at y = −b read Aᵀb kept by create instead of A */
   int32_t branch_steps[4]; /* Newton steps with r = 0, 0 < r < m (Eq. 19), r ≥ m (Eq. 18), CG (R32) */
   int32_t line_search_stalled; /* max_backtracks reached at least once (R30)              */
   int32_t cg_iters;        /* conjugate-gradient iterations, summed over CG steps             */
