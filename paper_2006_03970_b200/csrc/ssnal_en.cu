@@ -2759,6 +2759,7 @@ int ssnal_en_set_option(ssnal_en_problem* P, const char* key, double v) {
       return SSNAL_EINVAL;
     }
     CK(cudaFuncSetAttribute(k1_for(P->MR), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CK(cudaFuncSetAttribute(k1_for(P->MR, true), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     P->S = S;
     P->k1_smem = smem;
     drop_graph(P);  // the K1 launch configuration is baked into the graph

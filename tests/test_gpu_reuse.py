@@ -253,3 +253,20 @@ def test_psi_only_trials_and_the_streamed_redo():
             n0 = P.info("atb_reuses")
             P.solve(l1, l2, 5e-3, 1e-6)
             assert P.info("atb_reuses") == n0
+
+
+def test_reuse_with_a_deeper_k1_ring():
+    """Option k1_stages changes the dynamic shared memory of both K1 instantiations (a larger ring than
+    the one configured at create must not make the REUSE launch fail)."""
+    A, b = problem(64, 9000, 31)  # small stages: the default ring is far below 224 KB, 16 stages still fit
+    with Problem(A, b) as P:
+        P.set_option("small", 0)
+        P.set_option("reuse_min_bytes", 0)
+        l1, l2 = lambdas(0.7, P.lambda_max_l1, 0.5)
+        x0, s0 = P.solve(l1, l2, 5e-3, 1e-6)
+        P.set_option("k1_stages", 16)
+        for graph in (1, 0):
+            P.set_option("graph", graph)
+            x1, s1 = P.solve(l1, l2, 5e-3, 1e-6)
+            assert np.array_equal(x1, x0)
+            same_stats(s1, s0)
