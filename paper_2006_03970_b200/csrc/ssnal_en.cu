@@ -619,20 +619,21 @@ int configure(ssnal_en_problem* P) {
     set_err("K1 shared memory %zu exceeds 227 KB (m=%lld)", P->k1_smem, (long long)m);
     return SSNAL_EINVAL;
   }
+  // the attribute is per function and process-wide: always the device maximum, so that a later handle with a
+  // smaller ring (same MR bucket) cannot lower the cap under a live handle with a larger one
   CK(cudaFuncSetAttribute(P->fmt ? k1g_for(P->TW) : k1_for(P->MR), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (int)P->k1_smem));
+                          227 * 1024));
   CK(cudaFuncSetAttribute(P->fmt ? k1g_for(P->TW, true) : k1_for(P->MR, true),
-                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->k1_smem));
-  const size_t gsm = (size_t)8 * m * 8;
+                          cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
   P->cg_smem_bytes = cg_smem(m);
+  // per-function caps at the size of the largest supported m (1024), not this handle's (see above)
+  const int gsm_cap = 8 * 1024 * 8, cg_cap = (int)cg_smem(1024);
   if (P->fmt) {
-    CK(cudaFuncSetAttribute(gax_for<AccG>(P->MR), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsm));
-    CK(cudaFuncSetAttribute(cg_for<AccG>(P->MR), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)P->cg_smem_bytes));
+    CK(cudaFuncSetAttribute(gax_for<AccG>(P->MR), cudaFuncAttributeMaxDynamicSharedMemorySize, gsm_cap));
+    CK(cudaFuncSetAttribute(cg_for<AccG>(P->MR), cudaFuncAttributeMaxDynamicSharedMemorySize, cg_cap));
   } else {
-    CK(cudaFuncSetAttribute(gax_for<AccA>(P->MR), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsm));
-    CK(cudaFuncSetAttribute(cg_for<AccA>(P->MR), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)P->cg_smem_bytes));
+    CK(cudaFuncSetAttribute(gax_for<AccA>(P->MR), cudaFuncAttributeMaxDynamicSharedMemorySize, gsm_cap));
+    CK(cudaFuncSetAttribute(cg_for<AccA>(P->MR), cudaFuncAttributeMaxDynamicSharedMemorySize, cg_cap));
   }
   P->chol_smem = kCholSmem;
   CK(cudaFuncSetAttribute(k_chol_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->chol_smem));
@@ -2758,8 +2759,6 @@ int ssnal_en_set_option(ssnal_en_problem* P, const char* key, double v) {
       set_err("k1_stages=%d does not fit (m=%lld)", S, (long long)P->m);
       return SSNAL_EINVAL;
     }
-    CK(cudaFuncSetAttribute(k1_for(P->MR), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    CK(cudaFuncSetAttribute(k1_for(P->MR, true), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     P->S = S;
     P->k1_smem = smem;
     drop_graph(P);  // the K1 launch configuration is baked into the graph

@@ -200,3 +200,14 @@ def test_certify_primal_violation(name, n):
             ref = oracle.kkt_violation(A, b, x, l1, l2)
             assert st["primal_viol"] == pytest.approx(ref, rel=1e-6, abs=1e-12 * l1)
         assert st["primal_viol"] <= 1e-7 * l1
+
+
+def test_two_live_handles_with_different_k1_rings():
+    """Two handles in the same K1 register bucket (m = 300 and m = 500 → MR = 16) but with different ring
+    sizes, alive at once: the second create must not lower the first one's dynamic shared-memory cap."""
+    cfgs = [synth.scaled(synth.CONFIGS["cfg3"], n=4000, m=500), synth.scaled(synth.CONFIGS["cfg3"], n=4000, m=300)]
+    data = [(synth.design(c), synth.response(c)[0]) for c in cfgs]
+    with Problem(*data[0]) as P0, Problem(*data[1]) as P1:
+        for P, (A, b), cfg in ((P0, data[0], cfgs[0]), (P1, data[1], cfgs[1]), (P0, data[0], cfgs[0])):
+            l1, l2 = lambdas(cfg, P.lambda_max_l1, 0.3)
+            compare_to_oracle(A, b, l1, l2, lambda s0, tol, x0: P.solve(l1, l2, s0, tol, x0=x0), label="two handles")
